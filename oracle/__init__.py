@@ -1,0 +1,218 @@
+"""CPU oracle for the restricted-PCG energy minimisation (arXiv 2208.02995).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_2208_02995_b200``) never imports it, and
+this package never imports the product path: the two share no code.
+
+The arithmetic lives in ``emin_oracle.c`` (plain C, fp64, single thread);
+this file is ctypes marshalling only.  See the C file's header for the
+paper passages each step follows and DESIGN.md §3 for the readings of the
+garbled passages.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "emin_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+STOP_REASONS = {0: "running", 1: "gamma<=0", 2: "y'Ky==0", 3: "tau", 4: "stagnation"}
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no -ffast-math, IEEE fp64)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC",
+                               "-ffp-contract=off", "-o", _LIB_PATH, _SRC, "-lm"])
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = C.CDLL(_LIB_PATH)
+        P = C.c_void_p
+        i64, i32, dbl = C.c_int64, C.c_int, C.c_double
+        lib.oracle_create.argtypes = [C.POINTER(P), i64, i64, P, P, P, P, P, P, P, i32, P, P,
+                                      dbl, dbl, dbl, i32]
+        lib.oracle_create.restype = i32
+        lib.oracle_iterate.argtypes = [P, i32, C.POINTER(i32), P]
+        lib.oracle_iterate.restype = i32
+        for name, rt in [("oracle_nF", i64), ("oracle_nnzW", i64), ("oracle_E0", dbl),
+                         ("oracle_dE1", dbl), ("oracle_k_total", i64), ("oracle_stopped", i32),
+                         ("oracle_n_svd", i64), ("oracle_n_frozen", i64),
+                         ("oracle_sum_diag_cc", dbl), ("oracle_energy", dbl)]:
+            getattr(lib, name).argtypes = [P]
+            getattr(lib, name).restype = rt
+        lib.oracle_energy_of.argtypes = [P, P]
+        lib.oracle_energy_of.restype = dbl
+        lib.oracle_destroy.argtypes = [P]
+        lib.oracle_reset.argtypes = [P]
+        lib.oracle_get_W.argtypes = [P, P]
+        lib.oracle_get_P.argtypes = [P, P]
+        lib.oracle_copy_layout.argtypes = [P, P, P, P]
+        lib.oracle_copy_vec.argtypes = [P, i32, P]
+        lib.oracle_copy_Q.argtypes = [P, P, P]
+        lib.oracle_project.argtypes = [P, P, P]
+        lib.oracle_masked_AX.argtypes = [P, P, i32, P]
+        lib.oracle_setup_row.argtypes = [i32, i32, P, P, dbl, P, P, C.POINTER(i32)]
+        lib.oracle_setup_row.restype = i32
+        _lib = lib
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, where):
+        super().__init__(f"oracle {where} failed with status {code}")
+        self.code = code
+
+
+class Oracle:
+    """Oracle state for one problem (see workloads.problems.Problem)."""
+
+    def __init__(self, prob, rank_tol=1e-10, tau=0.0, stagnation_rel=1e-30, project_z=True,
+                 P_val="from_problem"):
+        lib = _load()
+        self._keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return a
+        Pv = prob.P_val if isinstance(P_val, str) else P_val
+        h = C.c_void_p()
+        st = lib.oracle_create(C.byref(h), prob.n, prob.nc,
+                               _p(arr(prob.A_rowptr, np.int64)), _p(arr(prob.A_col, np.int32)),
+                               _p(arr(prob.A_val, np.float64)), _p(arr(prob.is_coarse, np.uint8)),
+                               _p(arr(prob.P_rowptr, np.int64)), _p(arr(prob.P_col, np.int32)),
+                               _p(None if Pv is None else arr(Pv, np.float64)),
+                               prob.nv, _p(arr(prob.B, np.float64)), _p(arr(prob.Bc, np.float64)),
+                               rank_tol, tau, stagnation_rel, 1 if project_z else 0)
+        self._keep = []
+        if st != 0:
+            raise OracleError(st, "create")
+        self._h = h
+        self._lib = lib
+        self.nv = prob.nv
+        self.nF = lib.oracle_nF(h)
+        self.nnzW = lib.oracle_nnzW(h)
+        self.nnzP = int(prob.P_rowptr[-1])
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.oracle_destroy(h)
+            self._h = None
+
+    # -- Alg. 3 -----------------------------------------------------------
+    def iterate(self, k):
+        dE = np.zeros(max(k, 1))
+        kd = C.c_int(0)
+        st = self._lib.oracle_iterate(self._h, k, C.byref(kd), _p(dE))
+        if st != 0:
+            raise OracleError(st, "iterate")
+        return kd.value, dE[:kd.value].copy()
+
+    def reset(self):
+        self._lib.oracle_reset(self._h)
+
+    # -- results -----------------------------------------------------------
+    @property
+    def E0(self):
+        return self._lib.oracle_E0(self._h)
+
+    @property
+    def dE1(self):
+        return self._lib.oracle_dE1(self._h)
+
+    @property
+    def k_total(self):
+        return self._lib.oracle_k_total(self._h)
+
+    @property
+    def stop_reason(self):
+        return STOP_REASONS[self._lib.oracle_stopped(self._h)]
+
+    @property
+    def n_svd(self):
+        return self._lib.oracle_n_svd(self._h)
+
+    @property
+    def n_frozen(self):
+        return self._lib.oracle_n_frozen(self._h)
+
+    def energy(self):
+        return self._lib.oracle_energy(self._h)
+
+    def energy_of(self, W):
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        return self._lib.oracle_energy_of(self._h, _p(W))
+
+    def get_W(self):
+        out = np.empty(self.nnzW)
+        self._lib.oracle_get_W(self._h, _p(out))
+        return out
+
+    def get_P(self):
+        out = np.empty(self.nnzP)
+        self._lib.oracle_get_P(self._h, _p(out))
+        return out
+
+    def layout(self):
+        wptr = np.empty(self.nF + 1, np.int64)
+        wcol = np.empty(self.nnzW, np.int32)
+        frow = np.empty(self.nF, np.int64)
+        self._lib.oracle_copy_layout(self._h, _p(wptr), _p(wcol), _p(frow))
+        return wptr, wcol, frow
+
+    def vec(self, name):
+        which = {"w0": 0, "dw": 1, "r": 2, "y": 3, "yb": 4, "d": 5}[name]
+        out = np.empty(self.nF if which == 5 else self.nnzW)
+        self._lib.oracle_copy_vec(self._h, which, _p(out))
+        return out
+
+    def Q(self):
+        Q = np.empty((self.nnzW, self.nv))
+        k = np.empty(self.nF, np.int32)
+        self._lib.oracle_copy_Q(self._h, _p(Q), _p(k))
+        return Q, k
+
+    # -- the pieces --------------------------------------------------------
+    def project(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        self._lib.oracle_project(self._h, _p(x), _p(out))
+        return out
+
+    def masked_AX(self, X, with_fc=False):
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        out = np.empty_like(X)
+        self._lib.oracle_masked_AX(self._h, _p(X), 1 if with_fc else 0, _p(out))
+        return out
+
+
+def setup_row(M, r, tol=1e-10):
+    """Alg. 2 on one row: M = B_c(J,:) (nj x nv), r = v - M^T w^.
+    Returns (Q [nj, nv] zero-padded, delta [nj], k, used_svd)."""
+    lib = _load()
+    M = np.asarray(M, dtype=np.float64)
+    nj, nv = M.shape
+    Mc = np.ascontiguousarray(M.T)            # column-major nj x nv
+    rv = np.ascontiguousarray(r, dtype=np.float64)
+    Q = np.zeros((nj, nv))
+    delta = np.zeros(nj)
+    used = C.c_int(0)
+    k = lib.oracle_setup_row(nj, nv, _p(Mc), _p(rv), tol, _p(Q), _p(delta), C.byref(used))
+    return Q, delta, k, bool(used.value)

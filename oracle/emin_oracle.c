@@ -1,0 +1,602 @@
+/*
+ * emin_oracle.c -- plain, slow, obviously-correct fp64 CPU oracle for the
+ * restricted PCG energy minimisation of an AMG prolongation
+ * (arXiv 2208.02995, PAPER.md = /root/reference/PAPER.md).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_2208_02995_b200/csrc); neither includes or links the other.
+ *
+ * What it computes, step by step in the paper's order and notation, with the
+ * readings of SURVEY.md §8c / DESIGN.md §3 where the paper is garbled:
+ *
+ *   setup   Alg. 2 EMIN_SetUp per F row i, rows ascending:
+ *           M_i = B_c(J_i,:) (|J_i| x nv, reading A5), r_i = b_i - M_i^T w^_i,
+ *           economy Householder QR if |J_i| >= nv and rank(R) = nv
+ *           (rank_tol relative, A6): delta_i = Q_i R_i^{-T} r_i ; otherwise
+ *           one-sided Jacobi SVD, k_i = #{sigma > rank_tol sigma_max},
+ *           Q_i = U(:,1:k_i), delta_i = U_k Sigma_k^{-1} V_k^T r_i.
+ *           w0_i = w^_i + delta_i.
+ *   r0      r = Pi_B (f - K w0) = -Pi_B (A P0)|_F-pattern  (Alg. 3 line 3,
+ *           P:838, sign reading A1, projection reading A2).
+ *   iterate Alg. 3 with readings A3 (k = 1), A4 (stop exits the
+ *           loop without the update, P is still formed), A18 (guards):
+ *             z = Pi_B M^{-1} r  (Jacobi, M = diag(K) = A(i,i) per row,
+ *                                 Theorem 1; projected)
+ *             gamma = r^T z ; gamma <= 0 -> converged stop
+ *             y = z (k = 1) else y = z + (gamma/gamma_old) y
+ *             gamma_old = gamma
+ *             yb = Pi_B K y          (K y = A Y on the fixed pattern)
+ *             den = y^T yb ; den < 0 -> breakdown ; den == 0 -> stop
+ *             alpha = gamma/den ; dE_k = gamma alpha       (Eq. CG_dEa)
+ *             tau > 0, k > 1, dE_k < tau dE_1 -> stop      (Eq. relRed)
+ *             dE_k <= stag E0 -> stop                       (A18)
+ *             dw += alpha y ; r -= alpha yb
+ *   energy  tr(P^T A P) by its definition (Eq. trace), P = [W; I].
+ *
+ * Summation order: per-row sums ascending in A's column order; global sums
+ * row-ascending with Neumaier compensation.
+ *
+ * Parity pins (tests/test_oracle_*.py): dense KKT solve, null-space solve,
+ * 1D closed form, config 1b/2b converge to the symmetric equal-weight P,
+ * constraint at every iterate, monotone + telescoping energy, Theorem 1,
+ * S:288 least-norm example, masked product == gather(dense A P),
+ * energy == dense tr(P^T A P), QR/SVD vs numpy.linalg.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_ERR_ARG 1
+#define OR_ERR_CSR 2
+#define OR_ERR_PATTERN 3
+#define OR_ERR_BC 4
+#define OR_ERR_DIAG 5
+#define OR_ERR_NONFINITE 6
+#define OR_ERR_BREAKDOWN 7
+
+/* stop reasons */
+#define OR_RUN 0
+#define OR_STOP_GAMMA 1
+#define OR_STOP_DEN 2
+#define OR_STOP_TAU 3
+#define OR_STOP_STAG 4
+
+typedef struct {
+    int64_t n, nc, nF, nnzW;
+    int nv;
+    double rank_tol, tau, stag;
+    int project_z;                 /* 1: z = Pi M^-1 r (literal P:840) */
+    /* full operator, copied */
+    int64_t *Arp; int32_t *Acol; double *Aval;
+    uint8_t *isc;
+    int64_t *coarse_of;            /* global -> coarse id or -1 */
+    int64_t *fid;                  /* global -> F index or -1 */
+    int64_t *frow;                 /* F index -> global row */
+    /* full P pattern (all rows), copied */
+    int64_t *Prp; int32_t *Pcol;
+    /* W layout over F rows */
+    int64_t *wptr; int32_t *wcol;
+    double *Q;                     /* nnzW * nv, row-major per entry, zero-padded */
+    int *krank;                    /* numerical rank k_i per F row */
+    double *d;                     /* A(i,i) per F row */
+    double *w0, *dw, *r, *y, *yb, *z;
+    double sum_diag_cc;
+    /* CG state */
+    double gamma_old, dE1, E0;
+    int64_t k_total;
+    int stopped;
+    /* report */
+    int64_t n_svd, n_frozen;
+} oracle_t;
+
+/* ---------------- Neumaier-compensated accumulation -------------------- */
+typedef struct { double s, c; } nsum_t;
+static void nsum_add(nsum_t *a, double x) {
+    double t = a->s + x;
+    if (fabs(a->s) >= fabs(x)) a->c += (a->s - t) + x;
+    else a->c += (x - t) + a->s;
+    a->s = t;
+}
+static double nsum_val(const nsum_t *a) { return a->s + a->c; }
+
+/* ---------------- small dense helpers (column-major, local) ------------ */
+
+/* Householder economy QR of M (n x m, n >= m, column-major, ld = n).
+ * On return Q (n x m, column-major) and R (m x m, column-major, upper). */
+static void householder_qr(int n, int m, const double *M, double *Q, double *R) {
+    double *Wk = (double *)malloc(sizeof(double) * n * m);
+    double *V = (double *)calloc((size_t)n * m, sizeof(double));  /* reflectors */
+    double *vn = (double *)calloc(m, sizeof(double));              /* v^T v */
+    memcpy(Wk, M, sizeof(double) * n * m);
+    for (int j = 0; j < m; ++j) {
+        double nrm2 = 0.0;
+        for (int t = j; t < n; ++t) nrm2 += Wk[t + j * n] * Wk[t + j * n];
+        double nrm = sqrt(nrm2);
+        double x0 = Wk[j + j * n];
+        double alpha = (x0 >= 0.0) ? -nrm : nrm;
+        for (int t = j; t < n; ++t) V[t + j * n] = Wk[t + j * n];
+        V[j + j * n] -= alpha;
+        double vv = 0.0;
+        for (int t = j; t < n; ++t) vv += V[t + j * n] * V[t + j * n];
+        vn[j] = vv;
+        if (vv > 0.0) {
+            for (int c = j; c < m; ++c) {
+                double s = 0.0;
+                for (int t = j; t < n; ++t) s += V[t + j * n] * Wk[t + c * n];
+                s = 2.0 * s / vv;
+                for (int t = j; t < n; ++t) Wk[t + c * n] -= s * V[t + j * n];
+            }
+        }
+    }
+    for (int c = 0; c < m; ++c)
+        for (int rr = 0; rr < m; ++rr) R[rr + c * m] = (rr <= c) ? Wk[rr + c * n] : 0.0;
+    /* Q = H_0 ... H_{m-1} [I; 0] */
+    for (int c = 0; c < m; ++c)
+        for (int t = 0; t < n; ++t) Q[t + c * n] = (t == c) ? 1.0 : 0.0;
+    for (int j = m - 1; j >= 0; --j) {
+        if (vn[j] <= 0.0) continue;
+        for (int c = 0; c < m; ++c) {
+            double s = 0.0;
+            for (int t = j; t < n; ++t) s += V[t + j * n] * Q[t + c * n];
+            s = 2.0 * s / vn[j];
+            for (int t = j; t < n; ++t) Q[t + c * n] -= s * V[t + j * n];
+        }
+    }
+    free(Wk); free(V); free(vn);
+}
+
+/* One-sided (Hestenes) Jacobi SVD of M (n x m, column-major): on return
+ * U holds the rotated columns (= U Sigma), V (m x m) the right vectors. */
+static void jacobi_svd(int n, int m, const double *M, double *US, double *V) {
+    memcpy(US, M, sizeof(double) * n * m);
+    for (int c = 0; c < m; ++c)
+        for (int rr = 0; rr < m; ++rr) V[rr + c * m] = (rr == c) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        int rotated = 0;
+        for (int p = 0; p < m - 1; ++p) {
+            for (int q = p + 1; q < m; ++q) {
+                double a = 0.0, b = 0.0, c = 0.0;
+                for (int t = 0; t < n; ++t) {
+                    a += US[t + p * n] * US[t + p * n];
+                    b += US[t + q * n] * US[t + q * n];
+                    c += US[t + p * n] * US[t + q * n];
+                }
+                if (c == 0.0 || fabs(c) <= 1e-15 * sqrt(a * b)) continue;
+                rotated = 1;
+                double zeta = (b - a) / (2.0 * c);
+                double tt = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+                for (int t = 0; t < n; ++t) {
+                    double up = US[t + p * n], uq = US[t + q * n];
+                    US[t + p * n] = cs * up - sn * uq;
+                    US[t + q * n] = sn * up + cs * uq;
+                }
+                for (int t = 0; t < m; ++t) {
+                    double vp = V[t + p * m], vq = V[t + q * m];
+                    V[t + p * m] = cs * vp - sn * vq;
+                    V[t + q * m] = sn * vp + cs * vq;
+                }
+            }
+        }
+        if (!rotated) break;
+    }
+}
+
+/* Alg. 2 for one row.  M = B_c(J_i,:) (nj x nv, col-major), rvec = r_i (nv).
+ * Writes Qrow (nj x nv, ROW-major per entry, zero-padded beyond k), delta (nj).
+ * Returns k (numerical rank); *used_svd set if the SVD branch ran. */
+static int emin_setup_row(int nj, int nv, const double *M, const double *rvec, double tol,
+                          double *Qrow, double *delta, int *used_svd) {
+    *used_svd = 0;
+    for (int t = 0; t < nj * nv; ++t) Qrow[t] = 0.0;
+    for (int t = 0; t < nj; ++t) delta[t] = 0.0;
+    if (nj >= nv) {
+        double *Q = (double *)malloc(sizeof(double) * nj * nv);
+        double *R = (double *)malloc(sizeof(double) * nv * nv);
+        householder_qr(nj, nv, M, Q, R);
+        double rmax = 0.0, rmin = INFINITY;
+        for (int j = 0; j < nv; ++j) {
+            double a = fabs(R[j + j * nv]);
+            if (a > rmax) rmax = a;
+            if (a < rmin) rmin = a;
+        }
+        if (rmax > 0.0 && rmin > tol * rmax) {
+            /* delta = Q R^{-T} r : solve R^T u = r (forward), delta = Q u */
+            double *u = (double *)malloc(sizeof(double) * nv);
+            for (int j = 0; j < nv; ++j) {
+                double s = rvec[j];
+                for (int l = 0; l < j; ++l) s -= R[l + j * nv] * u[l];
+                u[j] = s / R[j + j * nv];
+            }
+            for (int t = 0; t < nj; ++t) {
+                double s = 0.0;
+                for (int j = 0; j < nv; ++j) s += Q[t + j * nj] * u[j];
+                delta[t] = s;
+                for (int j = 0; j < nv; ++j) Qrow[t * nv + j] = Q[t + j * nj];
+            }
+            free(u); free(Q); free(R);
+            return nv;
+        }
+        free(Q); free(R);
+    }
+    /* SVD branch, P:648-653 (reading A5: delta = U_k Sigma_k^-1 V_k^T r) */
+    *used_svd = 1;
+    double *US = (double *)malloc(sizeof(double) * nj * nv);
+    double *V = (double *)malloc(sizeof(double) * nv * nv);
+    jacobi_svd(nj, nv, M, US, V);
+    double smax = 0.0;
+    double *sig = (double *)malloc(sizeof(double) * nv);
+    for (int j = 0; j < nv; ++j) {
+        double s = 0.0;
+        for (int t = 0; t < nj; ++t) s += US[t + j * nj] * US[t + j * nj];
+        sig[j] = sqrt(s);
+        if (sig[j] > smax) smax = sig[j];
+    }
+    /* keep columns in descending sigma order (stable by index) */
+    int k = 0;
+    int *order = (int *)malloc(sizeof(int) * nv);
+    for (int j = 0; j < nv; ++j) order[j] = j;
+    for (int a = 1; a < nv; ++a)
+        for (int b = a; b > 0 && sig[order[b]] > sig[order[b - 1]]; --b) {
+            int tmp = order[b]; order[b] = order[b - 1]; order[b - 1] = tmp;
+        }
+    for (int a = 0; a < nv; ++a) {
+        int j = order[a];
+        if (!(smax > 0.0 && sig[j] > tol * smax)) continue;
+        double vr = 0.0;
+        for (int l = 0; l < nv; ++l) vr += V[l + j * nv] * rvec[l];
+        for (int t = 0; t < nj; ++t) {
+            double u = US[t + j * nj] / sig[j];
+            Qrow[t * nv + k] = u;
+            delta[t] += u * (vr / sig[j]);
+        }
+        ++k;
+    }
+    free(order); free(sig); free(US); free(V);
+    return k;
+}
+
+/* ---------------- the pieces of the path -------------------------------- */
+
+/* (Pi x)_i = x_i - Q_i (Q_i^T x_i)   (Pi_B = I - Q Q^T) */
+void oracle_project(const oracle_t *o, const double *x, double *out) {
+    int nv = o->nv;
+    for (int64_t i = 0; i < o->nF; ++i) {
+        int64_t b = o->wptr[i], e = o->wptr[i + 1];
+        double c[16];
+        for (int m = 0; m < nv; ++m) {
+            double s = 0.0;
+            for (int64_t p = b; p < e; ++p) s += o->Q[p * nv + m] * x[p];
+            c[m] = s;
+        }
+        for (int64_t p = b; p < e; ++p) {
+            double s = 0.0;
+            for (int m = 0; m < nv; ++m) s += o->Q[p * nv + m] * c[m];
+            out[p] = x[p] - s;
+        }
+    }
+}
+
+/* Masked product on the F pattern:
+ *   out(i,j) = sum_{k in F} A(i,k) X(k,j)  [+ A(i,c_j) if with_fc]
+ * for j in J_i, where X(k,j) = 0 if j not in J_k.  Summed in the order of
+ * row i of A; J_i and J_k are merged as sorted lists. */
+void oracle_masked_AX(const oracle_t *o, const double *X, int with_fc, double *out) {
+    for (int64_t i = 0; i < o->nF; ++i) {
+        int64_t g = o->frow[i];
+        int64_t b = o->wptr[i], e = o->wptr[i + 1];
+        for (int64_t p = b; p < e; ++p) out[p] = 0.0;
+        for (int64_t q = o->Arp[g]; q < o->Arp[g + 1]; ++q) {
+            int64_t c = o->Acol[q];
+            double a = o->Aval[q];
+            if (!o->isc[c]) {
+                int64_t k = o->fid[c];
+                int64_t pi = b, pk = o->wptr[k], ek = o->wptr[k + 1];
+                while (pi < e && pk < ek) {
+                    if (o->wcol[pi] == o->wcol[pk]) { out[pi] += a * X[pk]; ++pi; ++pk; }
+                    else if (o->wcol[pi] < o->wcol[pk]) ++pi;
+                    else ++pk;
+                }
+            } else if (with_fc) {
+                int64_t j = o->coarse_of[c];
+                for (int64_t p = b; p < e; ++p)
+                    if (o->wcol[p] == j) out[p] += a;
+            }
+        }
+    }
+}
+
+static double dot_w(const oracle_t *o, const double *a, const double *b) {
+    nsum_t s = {0.0, 0.0};
+    for (int64_t p = 0; p < o->nnzW; ++p) nsum_add(&s, a[p] * b[p]);
+    return nsum_val(&s);
+}
+
+/* tr(P^T A P) by definition, P = [W; I] on the full row set (Eq. trace). */
+double oracle_energy_of(const oracle_t *o, const double *W) {
+    nsum_t tot = {0.0, 0.0};
+    for (int64_t r = 0; r < o->n; ++r) {
+        /* P row r: pattern and values */
+        int64_t rb, re;
+        const int32_t *rc;
+        const double *rv;
+        double one = 1.0;
+        int32_t cself;
+        if (o->isc[r]) { cself = (int32_t)o->coarse_of[r]; rc = &cself; rv = &one; rb = 0; re = 1; }
+        else { int64_t i = o->fid[r]; rb = o->wptr[i]; re = o->wptr[i + 1]; rc = o->wcol; rv = W; }
+        for (int64_t p = rb; p < re; ++p) {
+            int32_t j = rc[p];
+            double prj = rv[p];
+            /* (A P)(r, j) */
+            double apj = 0.0;
+            for (int64_t q = o->Arp[r]; q < o->Arp[r + 1]; ++q) {
+                int64_t k = o->Acol[q];
+                double pkj = 0.0;
+                if (o->isc[k]) pkj = (o->coarse_of[k] == j) ? 1.0 : 0.0;
+                else {
+                    int64_t kk = o->fid[k];
+                    for (int64_t s = o->wptr[kk]; s < o->wptr[kk + 1]; ++s)
+                        if (o->wcol[s] == j) { pkj = W[s]; break; }
+                }
+                apj += o->Aval[q] * pkj;
+            }
+            nsum_add(&tot, prj * apj);
+        }
+    }
+    return nsum_val(&tot);
+}
+
+/* ---------------- lifecycle --------------------------------------------- */
+
+void oracle_destroy(oracle_t *o) {
+    if (!o) return;
+    free(o->Arp); free(o->Acol); free(o->Aval); free(o->isc); free(o->coarse_of);
+    free(o->fid); free(o->frow); free(o->Prp); free(o->Pcol); free(o->wptr);
+    free(o->wcol); free(o->Q); free(o->krank); free(o->d); free(o->w0); free(o->dw);
+    free(o->r); free(o->y); free(o->yb); free(o->z);
+    free(o);
+}
+
+/* Build the oracle state; returns status, *out = NULL on failure. */
+int oracle_create(oracle_t **out, int64_t n, int64_t nc,
+                  const int64_t *A_rowptr, const int32_t *A_col, const double *A_val,
+                  const uint8_t *is_coarse,
+                  const int64_t *P_rowptr, const int32_t *P_col, const double *P_val,
+                  int nv, const double *B, const double *Bc,
+                  double rank_tol, double tau, double stag, int project_z) {
+    *out = NULL;
+    if (n <= 0 || nc < 0 || nv <= 0 || nv > 16) return OR_ERR_ARG;
+    oracle_t *o = (oracle_t *)calloc(1, sizeof(oracle_t));
+    o->n = n; o->nc = nc; o->nv = nv;
+    o->rank_tol = rank_tol; o->tau = tau; o->stag = stag; o->project_z = project_z;
+    int64_t nnzA = A_rowptr[n];
+    o->Arp = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+    o->Acol = (int32_t *)malloc(sizeof(int32_t) * (nnzA ? nnzA : 1));
+    o->Aval = (double *)malloc(sizeof(double) * (nnzA ? nnzA : 1));
+    memcpy(o->Arp, A_rowptr, sizeof(int64_t) * (n + 1));
+    memcpy(o->Acol, A_col, sizeof(int32_t) * nnzA);
+    memcpy(o->Aval, A_val, sizeof(double) * nnzA);
+    o->isc = (uint8_t *)malloc(n);
+    memcpy(o->isc, is_coarse, n);
+    /* CSR validity: rowptr monotone, columns in range and strictly increasing */
+    if (A_rowptr[0] != 0) { oracle_destroy(o); return OR_ERR_CSR; }
+    for (int64_t r = 0; r < n; ++r) {
+        if (A_rowptr[r + 1] < A_rowptr[r]) { oracle_destroy(o); return OR_ERR_CSR; }
+        for (int64_t q = A_rowptr[r]; q < A_rowptr[r + 1]; ++q) {
+            if (A_col[q] < 0 || A_col[q] >= n) { oracle_destroy(o); return OR_ERR_CSR; }
+            if (q > A_rowptr[r] && A_col[q] <= A_col[q - 1]) { oracle_destroy(o); return OR_ERR_CSR; }
+            if (!isfinite(A_val[q])) { oracle_destroy(o); return OR_ERR_NONFINITE; }
+        }
+    }
+    /* C/F numbering: coarse ids and F ids ascending with the global index */
+    o->coarse_of = (int64_t *)malloc(sizeof(int64_t) * n);
+    o->fid = (int64_t *)malloc(sizeof(int64_t) * n);
+    int64_t cc = 0, ff = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        if (is_coarse[r]) { o->coarse_of[r] = cc++; o->fid[r] = -1; }
+        else { o->coarse_of[r] = -1; o->fid[r] = ff++; }
+    }
+    if (cc != nc) { oracle_destroy(o); return OR_ERR_ARG; }
+    o->nF = ff;
+    o->frow = (int64_t *)malloc(sizeof(int64_t) * (ff ? ff : 1));
+    for (int64_t r = 0; r < n; ++r) if (!is_coarse[r]) o->frow[o->fid[r]] = r;
+    /* pattern: C row c must be exactly {coarse(c)}; F rows non-empty, sorted */
+    int64_t nnzP = P_rowptr[n];
+    o->Prp = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+    o->Pcol = (int32_t *)malloc(sizeof(int32_t) * (nnzP ? nnzP : 1));
+    memcpy(o->Prp, P_rowptr, sizeof(int64_t) * (n + 1));
+    memcpy(o->Pcol, P_col, sizeof(int32_t) * nnzP);
+    o->wptr = (int64_t *)malloc(sizeof(int64_t) * (ff + 1));
+    o->wptr[0] = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        int64_t len = P_rowptr[r + 1] - P_rowptr[r];
+        if (len < 0) { oracle_destroy(o); return OR_ERR_PATTERN; }
+        for (int64_t q = P_rowptr[r]; q < P_rowptr[r + 1]; ++q) {
+            if (P_col[q] < 0 || P_col[q] >= nc) { oracle_destroy(o); return OR_ERR_PATTERN; }
+            if (q > P_rowptr[r] && P_col[q] <= P_col[q - 1]) { oracle_destroy(o); return OR_ERR_PATTERN; }
+        }
+        if (is_coarse[r]) {
+            if (len != 1 || P_col[P_rowptr[r]] != o->coarse_of[r]) { oracle_destroy(o); return OR_ERR_PATTERN; }
+            if (P_val && P_val[P_rowptr[r]] != 1.0) { oracle_destroy(o); return OR_ERR_PATTERN; }
+        } else {
+            if (len == 0) { oracle_destroy(o); return OR_ERR_PATTERN; }
+            int64_t i = o->fid[r];
+            o->wptr[i + 1] = o->wptr[i] + len;
+        }
+    }
+    o->nnzW = o->wptr[ff];
+    int64_t W = o->nnzW ? o->nnzW : 1;
+    o->wcol = (int32_t *)malloc(sizeof(int32_t) * W);
+    for (int64_t i = 0; i < ff; ++i) {
+        int64_t r = o->frow[i];
+        memcpy(o->wcol + o->wptr[i], P_col + P_rowptr[r], sizeof(int32_t) * (o->wptr[i + 1] - o->wptr[i]));
+    }
+    /* B_c(coarse(c),:) must equal B(c,:) exactly (reading A21) */
+    for (int64_t r = 0; r < n; ++r)
+        if (is_coarse[r])
+            for (int m = 0; m < nv; ++m)
+                if (Bc[o->coarse_of[r] * nv + m] != B[r * nv + m]) { oracle_destroy(o); return OR_ERR_BC; }
+    /* diagonal of the F rows and sum of the C diagonal */
+    o->d = (double *)malloc(sizeof(double) * (ff ? ff : 1));
+    nsum_t dcc = {0.0, 0.0};
+    for (int64_t r = 0; r < n; ++r) {
+        double dv = 0.0;
+        for (int64_t q = A_rowptr[r]; q < A_rowptr[r + 1]; ++q) if (A_col[q] == r) dv = A_val[q];
+        if (is_coarse[r]) nsum_add(&dcc, dv);
+        else {
+            if (!(dv > 0.0)) { oracle_destroy(o); return OR_ERR_DIAG; }
+            o->d[o->fid[r]] = dv;
+        }
+    }
+    o->sum_diag_cc = nsum_val(&dcc);
+    /* Alg. 2 per F row */
+    o->Q = (double *)calloc((size_t)W * nv, sizeof(double));
+    o->krank = (int *)calloc(ff ? ff : 1, sizeof(int));
+    o->w0 = (double *)calloc(W, sizeof(double));
+    o->dw = (double *)calloc(W, sizeof(double));
+    o->r = (double *)calloc(W, sizeof(double));
+    o->y = (double *)calloc(W, sizeof(double));
+    o->yb = (double *)calloc(W, sizeof(double));
+    o->z = (double *)calloc(W, sizeof(double));
+    for (int64_t i = 0; i < ff; ++i) {
+        int64_t r = o->frow[i], b = o->wptr[i];
+        int nj = (int)(o->wptr[i + 1] - b);
+        double *M = (double *)malloc(sizeof(double) * nj * nv);
+        double *wh = (double *)malloc(sizeof(double) * nj);
+        double *delta = (double *)malloc(sizeof(double) * nj);
+        double rv[16];
+        for (int t = 0; t < nj; ++t) {
+            int32_t j = o->wcol[b + t];
+            for (int m = 0; m < nv; ++m) M[t + m * nj] = Bc[(int64_t)j * nv + m];
+            wh[t] = P_val ? P_val[P_rowptr[r] + t] : 0.0;
+        }
+        for (int m = 0; m < nv; ++m) {              /* r_i = v_i - M^T w^ */
+            double s = B[r * nv + m];
+            for (int t = 0; t < nj; ++t) s -= M[t + m * nj] * wh[t];
+            rv[m] = s;
+        }
+        int used_svd = 0;
+        int k = emin_setup_row(nj, nv, M, rv, rank_tol, o->Q + b * nv, delta, &used_svd);
+        o->krank[i] = k;
+        if (used_svd) o->n_svd++;
+        if (nj == k) o->n_frozen++;
+        for (int t = 0; t < nj; ++t) o->w0[b + t] = wh[t] + delta[t];
+        free(M); free(wh); free(delta);
+    }
+    /* r0 = -Pi (A P0)|F   (readings A1, A2) */
+    double *G = (double *)malloc(sizeof(double) * W);
+    oracle_masked_AX(o, o->w0, 1, G);
+    oracle_project(o, G, o->r);
+    for (int64_t p = 0; p < o->nnzW; ++p) o->r[p] = -o->r[p];
+    free(G);
+    o->E0 = oracle_energy_of(o, o->w0);
+    o->k_total = 0; o->stopped = OR_RUN; o->gamma_old = 0.0; o->dE1 = 0.0;
+    *out = o;
+    return OR_OK;
+}
+
+/* Alg. 3 main loop, continuing from the current state for up to kmax
+ * iterations.  dE (nullable, length kmax) receives dE of applied steps.
+ * Returns status; *k_done = number of applied updates in this call. */
+int oracle_iterate(oracle_t *o, int kmax, int *k_done, double *dE) {
+    *k_done = 0;
+    int64_t W = o->nnzW;
+    for (int it = 0; it < kmax; ++it) {
+        if (o->stopped) break;
+        int64_t k = o->k_total + 1;
+        /* z = Pi M^-1 r, Jacobi M = A(i,i) per row block */
+        for (int64_t i = 0; i < o->nF; ++i)
+            for (int64_t p = o->wptr[i]; p < o->wptr[i + 1]; ++p) o->z[p] = o->r[p] / o->d[i];
+        if (o->project_z) oracle_project(o, o->z, o->z);
+        double gamma = dot_w(o, o->r, o->z);
+        if (!(gamma > 0.0)) { o->stopped = OR_STOP_GAMMA; break; }
+        if (k == 1) { for (int64_t p = 0; p < W; ++p) o->y[p] = o->z[p]; }
+        else {
+            double beta = gamma / o->gamma_old;
+            for (int64_t p = 0; p < W; ++p) o->y[p] = o->z[p] + beta * o->y[p];
+        }
+        o->gamma_old = gamma;
+        oracle_masked_AX(o, o->y, 0, o->yb);
+        oracle_project(o, o->yb, o->yb);
+        double den = dot_w(o, o->y, o->yb);
+        if (den < 0.0) { o->stopped = OR_STOP_DEN; return OR_ERR_BREAKDOWN; }
+        if (den == 0.0) { o->stopped = OR_STOP_DEN; break; }
+        double alpha = gamma / den;
+        double dEk = gamma * alpha;
+        if (k == 1) o->dE1 = dEk;
+        if (o->tau > 0.0 && k > 1 && dEk < o->tau * o->dE1) { o->stopped = OR_STOP_TAU; break; }
+        if (dEk <= o->stag * o->E0) { o->stopped = OR_STOP_STAG; break; }
+        for (int64_t p = 0; p < W; ++p) o->dw[p] += alpha * o->y[p];
+        for (int64_t p = 0; p < W; ++p) o->r[p] -= alpha * o->yb[p];
+        if (dE) dE[*k_done] = dEk;
+        o->k_total = k;
+        (*k_done)++;
+    }
+    return OR_OK;
+}
+
+/* w = w0 + dw */
+void oracle_get_W(const oracle_t *o, double *W) {
+    for (int64_t p = 0; p < o->nnzW; ++p) W[p] = o->w0[p] + o->dw[p];
+}
+/* full P values in the input CSR order, C rows = 1 */
+void oracle_get_P(const oracle_t *o, double *Pval) {
+    for (int64_t r = 0; r < o->n; ++r) {
+        if (o->isc[r]) { Pval[o->Prp[r]] = 1.0; continue; }
+        int64_t i = o->fid[r];
+        for (int64_t t = 0; t < o->wptr[i + 1] - o->wptr[i]; ++t)
+            Pval[o->Prp[r] + t] = o->w0[o->wptr[i] + t] + o->dw[o->wptr[i] + t];
+    }
+}
+double oracle_energy(const oracle_t *o) {
+    double *W = (double *)malloc(sizeof(double) * (o->nnzW ? o->nnzW : 1));
+    oracle_get_W(o, W);
+    double e = oracle_energy_of(o, W);
+    free(W);
+    return e;
+}
+void oracle_reset(oracle_t *o) {
+    memset(o->dw, 0, sizeof(double) * o->nnzW);
+    double *G = (double *)malloc(sizeof(double) * (o->nnzW ? o->nnzW : 1));
+    oracle_masked_AX(o, o->w0, 1, G);
+    oracle_project(o, G, o->r);
+    for (int64_t p = 0; p < o->nnzW; ++p) o->r[p] = -o->r[p];
+    free(G);
+    o->k_total = 0; o->stopped = OR_RUN; o->gamma_old = 0.0; o->dE1 = 0.0;
+}
+
+/* ---------------- accessors for the Python wrapper ----------------------- */
+int64_t oracle_nF(const oracle_t *o) { return o->nF; }
+int64_t oracle_nnzW(const oracle_t *o) { return o->nnzW; }
+double oracle_E0(const oracle_t *o) { return o->E0; }
+double oracle_dE1(const oracle_t *o) { return o->dE1; }
+int64_t oracle_k_total(const oracle_t *o) { return o->k_total; }
+int oracle_stopped(const oracle_t *o) { return o->stopped; }
+int64_t oracle_n_svd(const oracle_t *o) { return o->n_svd; }
+int64_t oracle_n_frozen(const oracle_t *o) { return o->n_frozen; }
+double oracle_sum_diag_cc(const oracle_t *o) { return o->sum_diag_cc; }
+void oracle_copy_layout(const oracle_t *o, int64_t *wptr, int32_t *wcol, int64_t *frow) {
+    memcpy(wptr, o->wptr, sizeof(int64_t) * (o->nF + 1));
+    memcpy(wcol, o->wcol, sizeof(int32_t) * o->nnzW);
+    memcpy(frow, o->frow, sizeof(int64_t) * o->nF);
+}
+void oracle_copy_vec(const oracle_t *o, int which, double *out) {
+    const double *src = which == 0 ? o->w0 : which == 1 ? o->dw : which == 2 ? o->r
+                      : which == 3 ? o->y : which == 4 ? o->yb : o->d;
+    int64_t len = which == 5 ? o->nF : o->nnzW;
+    memcpy(out, src, sizeof(double) * len);
+}
+void oracle_copy_Q(const oracle_t *o, double *Q, int *krank) {
+    memcpy(Q, o->Q, sizeof(double) * o->nnzW * o->nv);
+    memcpy(krank, o->krank, sizeof(int) * o->nF);
+}
+/* Setup-row entry point for the QR/SVD pins: M col-major nj x nv. */
+int oracle_setup_row(int nj, int nv, const double *M, const double *rvec, double tol,
+                     double *Qrow, double *delta, int *used_svd) {
+    return emin_setup_row(nj, nv, M, rvec, tol, Qrow, delta, used_svd);
+}

@@ -1,0 +1,387 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(not against itself).  CPU only (-m "not gpu").
+
+Each test names the passage it pins (P:n = PAPER.md, S:n = SPEC.md lines).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import dense_ref as D
+from oracle import Oracle, OracleError, setup_row
+from workloads.problems import make_config
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# --------------------------------------------------------------------------
+# Alg. 2 per row: QR branch, SVD branch, least-norm delta
+# --------------------------------------------------------------------------
+
+def test_setup_row_least_norm_S288():
+    g = GOLD["least_norm_S288"]
+    Q, delta, k, svd = setup_row(np.array(g["M"]), np.array(g["r"]))
+    assert k == g["k"] and not svd
+    assert np.allclose(delta, g["delta"], atol=1e-15, rtol=0)
+    assert np.allclose(np.abs(Q[:, 0]), [2 ** -0.5] * 2, atol=1e-15)
+
+
+def test_setup_row_qr_S80():
+    g = GOLD["qr_S80"]
+    Q, delta, k, svd = setup_row(np.array(g["M"]), np.array(g["r"]))
+    assert k == 1 and not svd
+    assert np.allclose(np.abs(Q[:, 0]), g["Q_abs"], atol=1e-15)
+    assert np.allclose(delta, g["delta"], atol=1e-15)
+
+
+def test_setup_row_rank_deficient_routes_to_svd():
+    g = GOLD["rank_deficient_S289"]
+    M = np.array(g["M"])
+    r = np.array(g["r"])
+    Q, delta, k, svd = setup_row(M, r)
+    assert svd and k == g["k"]
+    # least-squares / least-norm solution of M^T delta = r (library pinv)
+    assert np.allclose(delta, np.linalg.pinv(M.T, rcond=1e-10) @ r, atol=1e-13)
+    # Q spans range(M)
+    U = np.linalg.svd(M, full_matrices=False)[0][:, :1]
+    assert np.allclose(Q[:, :1] @ Q[:, :1].T, U @ U.T, atol=1e-13)
+    assert np.all(Q[:, 1:] == 0.0)
+
+
+@pytest.mark.parametrize("nj,nv,seed", [(5, 1, 0), (12, 6, 1), (41, 6, 2), (54, 6, 3), (6, 6, 4)])
+def test_setup_row_matches_lstsq_and_projector(nj, nv, seed):
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((nj, nv))
+    r = rng.standard_normal(nv)
+    Q, delta, k, svd = setup_row(M, r)
+    assert k == nv and not svd
+    # least-norm solution of M^T delta = r
+    ref = np.linalg.lstsq(M.T, r, rcond=None)[0]
+    assert np.allclose(delta, ref, atol=1e-12 * max(1, np.abs(ref).max()))
+    assert np.allclose(M.T @ delta, r, atol=1e-12)
+    # Q orthonormal basis of range(M): Q Q^T equals the SVD projector
+    assert np.allclose(Q.T @ Q, np.eye(nv), atol=1e-13)
+    U = np.linalg.svd(M, full_matrices=False)[0]
+    assert np.allclose(Q @ Q.T, U @ U.T, atol=1e-13)
+
+
+def test_setup_row_skinny_uses_svd():
+    # |J| < nv: SVD branch, k = |J|, delta = least-squares solution
+    rng = np.random.default_rng(7)
+    M = rng.standard_normal((3, 6))
+    r = rng.standard_normal(6)
+    Q, delta, k, svd = setup_row(M, r)
+    assert svd and k == 3
+    assert np.allclose(delta, np.linalg.pinv(M.T) @ r, atol=1e-12)
+
+
+# --------------------------------------------------------------------------
+# masked product, projection, energy vs dense definitions
+# --------------------------------------------------------------------------
+
+def _integer_problem(seed=0):
+    """Tiny SPD-agnostic problem with integer values so that dense and
+    sparse sums are exact in fp64 regardless of order."""
+    p = make_config("1b", size=8)
+    rng = np.random.default_rng(seed)
+    p.A_val = rng.integers(-4, 5, p.A_val.size).astype(np.float64)
+    rows = np.repeat(np.arange(p.n), np.diff(p.A_rowptr))
+    p.A_val[rows == p.A_col] = rng.integers(1, 9, p.n)   # positive diagonal
+    return p
+
+
+def test_masked_product_equals_gather_of_dense_product():
+    p = _integer_problem()
+    o = Oracle(p)
+    A = D.dense_A(p)
+    rng = np.random.default_rng(1)
+    X = rng.integers(-3, 4, o.nnzW).astype(np.float64)
+    r, j = D.w_entries(p)
+    PX = D.P_of(p, X)
+    # without the C-identity term: A_FF-part only
+    PF = PX.copy()
+    PF[p.is_coarse == 1] = 0.0
+    full = A @ PF
+    assert np.array_equal(o.masked_AX(X, with_fc=False), full[r, j])
+    # with the C-identity term: (A P)|F-pattern
+    assert np.array_equal(o.masked_AX(X, with_fc=True), (A @ PX)[r, j])
+
+
+def test_masked_product_identity_S71():
+    p = make_config("1b", size=8)
+    rows = np.repeat(np.arange(p.n), np.diff(p.A_rowptr))
+    keep = rows == p.A_col
+    p.A_rowptr = np.r_[0, np.cumsum(np.bincount(rows[keep], minlength=p.n))].astype(np.int64)
+    p.A_col = p.A_col[keep]
+    p.A_val = np.ones(keep.sum())
+    o = Oracle(p)
+    X = np.random.default_rng(0).standard_normal(o.nnzW)
+    assert np.array_equal(o.masked_AX(X), X)
+
+
+def test_energy_equals_dense_trace():
+    p = _integer_problem(3)
+    o = Oracle(p)
+    W = np.random.default_rng(5).integers(-3, 4, o.nnzW).astype(np.float64)
+    assert o.energy_of(W) == D.energy(p, W)
+
+
+def test_projection_nv1_closed_form_and_idempotent():
+    p = make_config("2b", size=6)
+    o = Oracle(p)
+    wptr, _, _ = o.layout()
+    x = np.random.default_rng(2).standard_normal(o.nnzW)
+    px = o.project(x)
+    # nv = 1, B = 1: Q_i = 1/sqrt|J_i| -> Pi subtracts the row mean
+    ref = x.copy()
+    for i in range(o.nF):
+        s, e = wptr[i], wptr[i + 1]
+        ref[s:e] -= x[s:e].mean()
+    assert np.allclose(px, ref, atol=1e-15)
+    assert np.allclose(o.project(px), px, atol=1e-15)
+
+
+def test_projection_annihilates_range_and_is_idempotent_elasticity():
+    p = make_config("4", size=3)
+    o = Oracle(p)
+    wptr, wcol, frow = o.layout()
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(o.nnzW)
+    px = o.project(x)
+    assert np.allclose(o.project(px), px, atol=1e-13)
+    # B~^T (Pi x) = 0 row by row and Pi(M_i c) = 0
+    for i in range(o.nF):
+        s, e = wptr[i], wptr[i + 1]
+        M = p.Bc[wcol[s:e]]
+        assert np.abs(M.T @ px[s:e]).max() <= 1e-12 * np.linalg.norm(x[s:e])
+        y = np.zeros(o.nnzW)
+        y[s:e] = M @ rng.standard_normal(p.nv)
+        assert np.abs(o.project(y)[s:e]).max() <= 1e-12 * np.abs(y).max()
+
+
+# --------------------------------------------------------------------------
+# the whole path against the dense problem statement
+# --------------------------------------------------------------------------
+
+SMALL = [("1b", 8), ("2b", 6), ("3", 6), ("4", 2), ("4", 3)]
+
+
+@pytest.mark.parametrize("name,size", SMALL)
+def test_setup_satisfies_constraint_and_r0_is_projected_negative_gradient(name, size):
+    p = make_config(name, size=size)
+    o = Oracle(p)
+    w0 = o.vec("w0")
+    Cm, b = D.constraint_matrix(p)
+    assert np.abs(Cm @ w0 - b).max() <= 1e-12 * max(1.0, np.abs(b).max())
+    # r0 = Pi(f - K w0) = -Pi grad E(w0)/2 with grad from the dense trace (A1, A2)
+    H, g, _ = D.quadratic_form(p)
+    grad = H @ w0 + g
+    r0 = o.vec("r")
+    ref = -o.project(grad / 2.0)
+    assert np.allclose(r0, ref, atol=1e-12 * np.abs(ref).max())
+    # and E0 is the dense trace
+    assert abs(o.E0 - D.energy(p, w0)) <= 1e-12 * abs(o.E0)
+
+
+@pytest.mark.parametrize("name,size", SMALL)
+def test_converged_pcg_matches_dense_kkt(name, size):
+    p = make_config(name, size=size)
+    o = Oracle(p)
+    o.iterate(400)
+    W = o.get_W()
+    w_kkt = D.kkt_solution(p)
+    w_ns = D.nullspace_solution(p, o.vec("w0"))
+    scale = np.abs(w_kkt).max()
+    assert np.abs(W - w_kkt).max() <= 1e-9 * scale
+    assert np.abs(W - w_ns).max() <= 1e-9 * scale
+    Eref = D.energy(p, w_kkt)
+    assert abs(o.energy() - Eref) <= 1e-11 * abs(Eref)
+
+
+@pytest.mark.parametrize("name,size,k", [("1b", 8, 12), ("3", 6, 20), ("4", 3, 15), ("2b", 6, 15)])
+def test_every_iterate_constraint_monotone_telescoping(name, size, k):
+    p = make_config(name, size=size)
+    o = Oracle(p)
+    A = D.dense_A(p)
+    Cm, b = D.constraint_matrix(p)
+    E_prev = o.E0
+    tele = o.E0
+    for it in range(k):
+        kd, dE = o.iterate(1)
+        if kd == 0:
+            break
+        W = o.get_W()
+        E = D.energy(p, W, A)
+        assert np.abs(Cm @ W - b).max() <= 1e-12 * max(1.0, np.abs(b).max())
+        assert E <= E_prev + 1e-12 * abs(E_prev)            # monotone (Eq. CG_dE)
+        tele -= dE[0]
+        assert abs(E - tele) <= 1e-10 * abs(o.E0)           # E_k = E_0 - sum dE_j
+        assert abs((E_prev - E) - dE[0]) <= 1e-9 * abs(o.E0)
+        E_prev = E
+
+
+def test_1d_closed_form():
+    g = GOLD["closed_form_1d"]
+    p = make_config("1d", size=g["n"])
+    assert p.nc == g["n_C"]
+    o = Oracle(p)
+    assert o.E0 > g["E_star"] + 1e-3          # least-norm start is not optimal
+    o.iterate(200)
+    W = o.get_W()
+    wptr, wcol, frow = o.layout()
+    cid_glob = np.flatnonzero(p.is_coarse)
+    for i in range(o.nF):
+        for t in range(wptr[i], wptr[i + 1]):
+            adjacent = abs(int(cid_glob[wcol[t]]) - int(frow[i])) == 1
+            assert abs(W[t] - (0.5 if adjacent else 0.0)) <= 1e-13
+    assert abs(o.energy() - g["E_star"]) <= 1e-12 * g["E_star"]
+
+
+def test_config1_degenerate_and_1b_converges_to_symmetric_P():
+    g = GOLD["config1_symmetric_limit"]
+    p1 = make_config("1")
+    o1 = Oracle(p1)
+    W1 = o1.vec("w0")
+    assert D.energy(p1, W1) == g["E_star"]
+    # degenerate start: first energy decrease is round-off (finding 4)
+    o1n = Oracle(p1, stagnation_rel=0.0)
+    kd, dE = o1n.iterate(1)
+    assert kd == 1 and dE[0] <= 1e-20 * o1n.E0
+    # the guard (A18) stops it without any update
+    kd, _ = o1.iterate(20)
+    assert kd == 0 and o1.stop_reason in ("stagnation", "gamma<=0")
+    p1b = make_config("1b")
+    o = Oracle(p1b)
+    kd, dE = o.iterate(60)
+    assert np.abs(o.get_W() - W1).max() <= 1e-10
+    assert abs(o.energy() - g["E_star"]) <= 1e-10 * g["E_star"]
+
+
+def test_theorem1_and_corollary():
+    """diag(Z^T K Z) = A(i,i) per row block, Z^T D_K Z diagonal, Z^T D_K Q = 0
+    (Theorem 1 / Corollary) on K = H/2 from the dense trace."""
+    p = make_config("4", size=2)
+    o = Oracle(p)
+    H, _, _ = D.quadratic_form(p)
+    K = H / 2.0
+    Q, krank = o.Q()
+    wptr, wcol, frow = o.layout()
+    m = o.nnzW
+    Zb, Qb = [], []
+    for i in range(o.nF):
+        s, e = wptr[i], wptr[i + 1]
+        Qi = Q[s:e, :krank[i]]
+        Zi = sla.null_space(Qi.T)
+        Zfull = np.zeros((m, Zi.shape[1]))
+        Zfull[s:e] = Zi
+        Qfull = np.zeros((m, Qi.shape[1]))
+        Qfull[s:e] = Qi
+        Zb.append((i, Zfull))
+        Qb.append(Qfull)
+    Z = np.hstack([z for _, z in Zb])
+    Qm = np.hstack(Qb)
+    DK = np.diag(np.diag(K))
+    dz = np.diag(Z.T @ K @ Z)
+    expect = np.concatenate([[p.A_val[p.A_rowptr[frow[i]]:p.A_rowptr[frow[i] + 1]]
+                              [p.A_col[p.A_rowptr[frow[i]]:p.A_rowptr[frow[i] + 1]] == frow[i]][0]]
+                             * z.shape[1] for i, z in Zb])
+    assert np.allclose(dz, expect, rtol=1e-12, atol=0)
+    ZDZ = Z.T @ DK @ Z
+    assert np.abs(ZDZ - np.diag(np.diag(ZDZ))).max() <= 1e-12 * np.abs(DK).max()
+    assert np.abs(Z.T @ DK @ Qm).max() <= 1e-12 * np.abs(DK).max()
+    # the oracle's Jacobi diagonal is diag(K) row by row
+    d = o.vec("d")
+    assert np.allclose(np.repeat(d, np.diff(wptr)), np.diag(K), rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("name,size", [("4", 3), ("3", 6)])
+def test_jacobi_needs_no_post_projection(name, size):
+    """P:911-914 / reading A7: with M_J the post-projection changes nothing
+    beyond round-off."""
+    p = make_config(name, size=size)
+    a = Oracle(p, project_z=True)
+    b = Oracle(p, project_z=False)
+    a.iterate(15)
+    b.iterate(15)
+    Wa, Wb = a.get_W(), b.get_W()
+    assert np.abs(Wa - Wb).max() <= 1e-12 * np.abs(Wa).max()
+
+
+def test_basis_invariance():
+    """P is invariant under B -> B M (A17): same constraint set."""
+    p = make_config("4", size=3)
+    a = Oracle(p)
+    a.iterate(10)
+    rng = np.random.default_rng(11)
+    Mx = rng.standard_normal((6, 6)) + 3 * np.eye(6)
+    p.B = p.B @ Mx
+    p.Bc = p.Bc @ Mx
+    b = Oracle(p)
+    b.iterate(10)
+    assert np.abs(a.get_W() - b.get_W()).max() <= 1e-10 * np.abs(a.get_W()).max()
+
+
+def test_tau_one_runs_exactly_one_update():
+    """tau = 1: dE_2 < dE_1 stops at k = 2 without its update (S:334, P:852 + A4)."""
+    p = make_config("1b", size=8)
+    o = Oracle(p, tau=1.0)
+    kd, dE = o.iterate(20)
+    assert kd == 1 and o.stop_reason == "tau"
+
+
+def test_iterate_composes():
+    p = make_config("3", size=6)
+    a = Oracle(p)
+    b = Oracle(p)
+    a.iterate(7)
+    a.iterate(5)
+    b.iterate(12)
+    assert np.array_equal(a.get_W(), b.get_W())
+
+
+def test_reset_restores_start():
+    p = make_config("1b", size=8)
+    o = Oracle(p)
+    _, dE1 = o.iterate(5)
+    o.reset()
+    _, dE2 = o.iterate(5)
+    assert np.array_equal(dE1, dE2)
+
+
+# --------------------------------------------------------------------------
+# input validation (error contract of the ABI)
+# --------------------------------------------------------------------------
+
+def test_validation_errors():
+    p = make_config("1b", size=8)
+    bad = make_config("1b", size=8)
+    bad.Bc = bad.Bc.copy()
+    bad.Bc[0, 0] = 2.0
+    with pytest.raises(OracleError) as e:
+        Oracle(bad)
+    assert e.value.code == 4
+    bad = make_config("1b", size=8)
+    c = int(np.flatnonzero(bad.is_coarse)[0])
+    bad.P_col = bad.P_col.copy()
+    bad.P_col[bad.P_rowptr[c]] = 1
+    with pytest.raises(OracleError) as e:
+        Oracle(bad)
+    assert e.value.code == 3
+    bad = make_config("1b", size=8)
+    bad.A_val = bad.A_val.copy()
+    rows = np.repeat(np.arange(bad.n), np.diff(bad.A_rowptr))
+    f = int(np.flatnonzero(bad.is_coarse == 0)[0])
+    bad.A_val[(rows == f) & (bad.A_col == f)] = -1.0
+    with pytest.raises(OracleError) as e:
+        Oracle(bad)
+    assert e.value.code == 5
+    bad = make_config("1b", size=8)
+    bad.A_col = bad.A_col.copy()
+    bad.A_col[[0, 1]] = bad.A_col[[1, 0]]
+    with pytest.raises(OracleError) as e:
+        Oracle(bad)
+    assert e.value.code == 2
+    Oracle(p)
