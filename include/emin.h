@@ -1,0 +1,169 @@
+/*
+ * emin.h -- C ABI of the B200-native restricted-PCG energy minimisation of an
+ * AMG prolongation (arXiv 2208.02995).  PAPER.md = /root/reference/PAPER.md,
+ * cited as P:<line> [section / equation / algorithm].
+ *
+ * Problem (Eq. inKern + trace, Eq. TSP/Constr):
+ *     minimise tr(P^T A P)  over P = [W; I] (Eq. prol)
+ *     subject to  W on a fixed sparsity pattern and P B_c = B.
+ * Method: Alg. 2 EMIN_SetUp once, then Alg. 3 EMIN_PCG
+ * with the Jacobi preconditioner M_1, K applied
+ * matrix-free as the masked product A.P on the pattern, Pi_B
+ * applied row by row from small orthonormal Q_i.  Readings of the
+ * garbled passages are listed in DESIGN.md §3.
+ *
+ * Conventions for every call
+ *  - All functions return emin_status; EMIN_OK (= 0) on success.
+ *  - Layouts: CSR with int64 row pointers and int32 column indices, values
+ *    fp64; dense blocks row-major.  Rows of A, P and B are the rows this
+ *    process OWNS, [row_begin, row_end) of the global numbering (the whole
+ *    matrix on one GPU); column indices are GLOBAL.
+ *  - Pointers are host pointers unless opts->inputs_on_device = 1, in which
+ *    case they are device pointers on the current CUDA device.  Inputs are
+ *    read only during emin_setup (copied); the caller keeps ownership.
+ *  - The context owns all device memory it allocates and releases it in
+ *    emin_destroy.  Outputs go to caller-allocated buffers.
+ *  - Work is enqueued on opts->stream (cudaStream_t, NULL = legacy default).
+ *    emin_iterate is asynchronous unless k_done or dE is non-NULL.
+ *  - Multi-GPU: emin_setup, emin_iterate, emin_energy and emin_reset are
+ *    collective over opts->nccl_comm (every rank calls them in the same
+ *    order); nccl_comm = NULL means one GPU owning all rows.
+ *  - After a failing call other than emin_setup the context stays valid;
+ *    emin_destroy is always safe (also on NULL).
+ */
+#ifndef EMIN_H_
+#define EMIN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct emin_ctx_s* emin_ctx;
+
+typedef enum {
+  EMIN_OK = 0,
+  EMIN_ERR_ARG = 1,        /* bad scalar argument, NULL pointer, nv out of [1,8] */
+  EMIN_ERR_CSR = 2,        /* A rowptr not monotone, column out of range, unsorted or duplicate */
+  EMIN_ERR_PATTERN = 3,    /* C row != {coarse(c)} (value 1 if P_val given), F row empty,
+                              unsorted or out of [0, nc), or an F row longer than EMIN_MAX_ROW */
+  EMIN_ERR_BC = 4,         /* B_c(coarse(c),:) != B(c,:) bitwise (reading A21) */
+  EMIN_ERR_DIAG = 5,       /* A(i,i) missing or <= 0 on an F row (Jacobi) */
+  EMIN_ERR_NONFINITE = 6,  /* NaN/Inf in A, B, B_c or P_val */
+  EMIN_ERR_BREAKDOWN = 7,  /* y^T Pi K y < 0 (SPD A makes it >= 0) */
+  EMIN_ERR_CUDA = 8,
+  EMIN_ERR_NCCL = 9,
+  EMIN_ERR_OOM = 10,
+  EMIN_ERR_STATE = 11      /* call on a context in the wrong state */
+} emin_status;
+
+/* Longest F-row pattern the kernels accept (|J_i|). */
+#define EMIN_MAX_ROW 128
+
+typedef struct {
+  int32_t block_size;           /* 1 = point rows; 3 = nodal hint: rows 3m..3m+2 share J
+                                   (elasticity), enables the 3x3 block kernels when valid */
+  double  rank_tol;             /* relative rank tolerance of Alg. 2's QR/SVD tests, 1e-10
+                                   (reading A6) */
+  double  tau;                  /* stop when dE_k < tau dE_1, k > 1 (Eq. relRed);
+                                   0 = run exactly k steps.  Paper default 0.1 */
+  int32_t project_after_jacobi; /* 1 = literal Alg. 3 line P:840 (z = Pi M^-1 r); 0 = skip the
+                                   post-projection, exact for Jacobi (reading A7) */
+  double  stagnation_rel;       /* stop (no update) when dE_k <= stagnation_rel * E_0
+                                   (reading A18; 1e-30 default, 0 disables) */
+  void*   stream;               /* cudaStream_t */
+  void*   nccl_comm;            /* ncclComm_t or NULL (one GPU) */
+  int64_t row_begin, row_end;   /* owned global rows; [0, n_global) on one GPU */
+  int32_t inputs_on_device;     /* 1: the array arguments of emin_setup are device pointers */
+} emin_opts;
+
+typedef struct {
+  double  E0;          /* tr(P0^T A P0) after Alg. 2 */
+  double  dE1;         /* first energy decrease (0 before the first step) */
+  int64_t k_total;     /* accepted PCG steps since setup/reset */
+  int32_t stop_reason; /* 0 running, 1 gamma <= 0, 2 y'Ky == 0, 3 tau, 4 stagnation,
+                          5 breakdown */
+  int64_t n_svd_rows;  /* F rows that took Alg. 2's SVD branch */
+  int64_t n_frozen_rows;  /* F rows with |J_i| == rank (no free dof) */
+  int64_t n_fine, nnz_W, nnz_AFF;  /* owned F rows, W entries, A_FF entries */
+  int32_t kernel_path; /* 0 generic warp-per-row, 1 scalar lane-per-entry, 2 nodal 3x3 */
+  int32_t nranks;
+} emin_report_t;
+
+/* Fill opts with defaults (rank_tol 1e-10, tau 0, project_after_jacobi 0,
+ * stagnation_rel 1e-30, block_size 1, one GPU over [0, n_global)). */
+void emin_default_opts(emin_opts* opts, int64_t n_global);
+
+/* Alg. 2 + the start of Alg. 3:
+ *   validates the inputs, builds the F-row structures, per F row i the
+ *   orthonormal Q_i of M_i = B_c(J_i,:) and the correction delta_i, the
+ *   start W0 = W^ + delta, r0 = Pi_B(f - K w0) = -Pi_B (A P0)|_F (reading A1)
+ *   and E0.
+ * n_global, nc_global : global row count and coarse count.
+ * A_rowptr [m+1], A_col, A_val : owned rows of A (m = row_end - row_begin),
+ *   global column ids, strictly increasing per row; A must be SPD.
+ * is_coarse [n_global] : 1 for C points, 0 for F points (global).  Coarse
+ *   id of a C point = its rank among C points in ascending global order.
+ * P_rowptr [m+1], P_col : pattern of the owned rows of P, coarse ids,
+ *   strictly increasing; C rows must be exactly {coarse(c)}.
+ * P_val (nullable, same layout) : starting W^ (NULL: W^ = 0, least-norm
+ *   start, reading A9); its C-row values must be 1.
+ * nv in [1, 8]; B [m x nv] owned rows of the near kernel; Bc [nc_global x nv].
+ * On failure *out = NULL and the status says why. */
+emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_global,
+                       const int64_t* A_rowptr, const int32_t* A_col, const double* A_val,
+                       const uint8_t* is_coarse,
+                       const int64_t* P_rowptr, const int32_t* P_col, const double* P_val,
+                       int32_t nv, const double* B, const double* Bc,
+                       const emin_opts* opts);
+
+/* Run up to k steps of Alg. 3 from the current state.
+ * k_done (nullable): accepted steps in this call; dE (nullable, length k):
+ * their energy decreases dE_j = gamma alpha (Eq. CG_dEa).  Passing
+ * either forces a stream synchronisation.  emin_iterate(k1); emin_iterate(k2)
+ * is bitwise equal to emin_iterate(k1 + k2).  EMIN_ERR_BREAKDOWN is reported
+ * by the first call that observes it (synchronously only if k_done/dE given,
+ * else by the next emin_report/emin_energy/emin_get_P). */
+emin_status emin_iterate(emin_ctx ctx, int32_t k, int32_t* k_done, double* dE);
+
+/* E = tr(P^T A P) of the current iterate (Eq. trace; by
+ * Eq. trInc P:417-426 = sum_F W.(A_FF W + 2 A_FC) + tr(A_CC)).  Synchronous.
+ * Collective. */
+emin_status emin_energy(emin_ctx ctx, double* E);
+
+/* Current P values of the owned rows in the input CSR order (C rows = 1),
+ * W = W0 + dW.  P_val is a host pointer unless
+ * opts.inputs_on_device, then a device pointer.  Synchronous. */
+emin_status emin_get_P(emin_ctx ctx, double* P_val);
+
+/* Back to W0, r0 (for benchmark repeats).  Collective. */
+emin_status emin_reset(emin_ctx ctx);
+
+/* Counters and scalars (synchronous). */
+emin_status emin_report(emin_ctx ctx, emin_report_t* rep);
+
+void emin_destroy(emin_ctx ctx);
+
+const char* emin_status_str(emin_status s);
+/* Last error message recorded on ctx (or of the last failed emin_setup when
+ * ctx == NULL).  Never NULL. */
+const char* emin_last_error(emin_ctx ctx);
+
+/* Index structure the context built (for parity tests), host outputs:
+ * wptr [n_fine+1] W-layout row pointers of the owned F rows (ascending
+ * global order), wcol [nnz_W] coarse ids, pofs [n_fine] offset of each F
+ * row in the caller's P CSR (relative to P_rowptr[0]).  Synchronous. */
+emin_status emin_get_layout(emin_ctx ctx, int64_t* wptr, int32_t* wcol, int64_t* pofs);
+
+/* Device time of the most recent emin_iterate's kernels, per kernel class,
+ * accumulated with CUDA events on the launching stream when profiling is
+ * enabled (emin_set_profiling(ctx, 1)); ms[0] stage I, ms[1] stage II,
+ * ms[2] masked SpGEMM, ms[3] scalar/reduction kernels; launches[4] counts. */
+emin_status emin_set_profiling(emin_ctx ctx, int32_t on);
+emin_status emin_kernel_times(emin_ctx ctx, double* ms, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMIN_H_ */

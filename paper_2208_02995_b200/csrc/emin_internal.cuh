@@ -1,0 +1,163 @@
+// emin_internal.cuh -- internal types and device helpers of libemin (sm_100a).
+// Not part of the ABI; see include/emin.h.  Shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/emin.h"
+
+#define EMIN_NV_MAX 8
+#define EMIN_WARP 32
+
+// Device-resident CG scalars (Alg. 3 state).  One instance per
+// context; updated only by the single-block scalar kernels, read by all.
+struct DevState {
+  double gamma;       // r^T z of the current step
+  double gamma_old;
+  double beta;        // gamma / gamma_old
+  double alpha_pend;  // alpha of the accepted step whose updates are pending
+  double den;         // y^T Pi K y
+  double dE1;         // dE of the first step (Eq. relRed)
+  double E0;          // tr(P0^T A P0)
+  double tau, stag;
+  int64_t k_total;    // accepted steps since setup / reset
+  int32_t stopped;    // 0 running, 1 gamma<=0, 2 den==0, 3 tau, 4 stagnation, 5 breakdown
+  int32_t pend;       // r -= alpha_pend yb pending (applied by stage I)
+  int32_t pendw;      // dw += alpha_pend y pending (applied by stage II)
+  int32_t k_call;     // accepted steps in the current emin_iterate call
+};
+
+// Error flag bits raised by the validation kernels.
+enum : int32_t {
+  EF_CSR = 1, EF_PATTERN = 2, EF_BC = 4, EF_DIAG = 8, EF_NONFINITE = 16, EF_ROWLEN = 32
+};
+
+// Plain-pointer view of the device data used by the kernels.
+struct DevView {
+  int64_t nF;       // owned F rows
+  int64_t nFh;      // owned + halo F rows (halo rows are appended)
+  int64_t nnzW;     // owned W entries
+  int32_t nv;
+  const int64_t* wptr;   // [nFh+1]
+  const int32_t* wcol;   // [wptr[nFh]]
+  const int64_t* affptr; // [nF+1] A_FF in local F ids
+  const int32_t* affcol;
+  const double* affval;
+  const int64_t* afcptr; // [nF+1] A_FC with coarse ids (setup / energy only)
+  const int32_t* afccol;
+  const double* afcval;
+  const double* d;       // A(i,i) per owned F row
+  const double* Q;       // [nnzW * nv] row-major per entry, zero padded
+  DevState* st;
+};
+
+struct emin_ctx_s {
+  emin_opts opts;
+  cudaStream_t stream = nullptr;
+  void* comm = nullptr;
+  int rank = 0, nranks = 1;
+  int64_t n_global = 0, nc_global = 0, m_owned = 0;
+  int64_t nF = 0, nFh = 0, nnzW = 0, nnzWh = 0, nnzAFF = 0, nnzAFC = 0, nnzP = 0;
+  int32_t nv = 1;
+  int32_t max_row = 0;
+  int32_t group = 1;           // lanes per row in the streaming stages
+  int32_t kernel_path = 0;
+  // device arrays (owned by ctx)
+  int64_t *wptr = nullptr, *affptr = nullptr, *afcptr = nullptr, *pofs = nullptr, *cofs = nullptr;
+  uint8_t* isc_own = nullptr;  // is_coarse of the owned rows
+  cudaStream_t cap_stream = nullptr;  // capture stream for the CUDA graphs
+  int64_t k_launched = 0;      // upper bound of k_total (host side)
+  int breakdown_reported = 0;
+  int32_t *wcol = nullptr, *affcol = nullptr, *afccol = nullptr;
+  double *affval = nullptr, *afcval = nullptr, *d = nullptr, *Q = nullptr;
+  double *w0 = nullptr, *dw = nullptr, *r = nullptr, *r0 = nullptr, *y = nullptr, *yb = nullptr;
+  double *partials = nullptr;  // per-block reduction partials
+  int32_t n_partials = 0;
+  double *dE_hist = nullptr;
+  int64_t dE_cap = 0;
+  DevState* st = nullptr;
+  double sum_diag_cc = 0.0;
+  int64_t n_svd = 0, n_frozen = 0, n_crows = 0;
+  // launch geometry
+  int grid_rows = 0, grid_spgemm = 0, grid_red = 0;
+  // graphs: one per k (cached)
+  cudaGraphExec_t graph = nullptr;
+  int graph_k = -1;
+  int graph_prof = 0;
+  // profiling
+  int profiling = 0;
+  std::vector<cudaEvent_t> ev;
+  double prof_ms[4] = {0, 0, 0, 0};
+  int64_t prof_launches[4] = {0, 0, 0, 0};
+  std::string last_error;
+  DevView view() const {
+    DevView v;
+    v.nF = nF; v.nFh = nFh; v.nnzW = nnzW; v.nv = nv;
+    v.wptr = wptr; v.wcol = wcol; v.affptr = affptr; v.affcol = affcol; v.affval = affval;
+    v.afcptr = afcptr; v.afccol = afccol; v.afcval = afcval; v.d = d; v.Q = Q; v.st = st;
+    return v;
+  }
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over aligned groups of G lanes (butterfly; identical result in every
+// lane of the group; fixed order => deterministic).
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of one double (fixed tree); result valid in
+// thread 0.  blockDim.x must be a multiple of 32 and <= 1024.
+__device__ __forceinline__ double block_sum(double v, double* sh /* >= 32 */) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  double t = 0.0;
+  if (w == 0) {
+    t = (l < nw) ? sh[l] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;
+}
+
+// lower_bound of key in sorted a[0..n)
+__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int32_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// -------------------------------------------------------------- host side
+#define EMIN_CUDA_TRY(ctx, call)                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      if (ctx) (ctx)->last_error = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      return (e_ == cudaErrorMemoryAllocation) ? EMIN_ERR_OOM : EMIN_ERR_CUDA;     \
+    }                                                                              \
+  } while (0)
+
+// exclusive scan of int64 counts (in may alias out); returns total via *total_dev
+// (device pointer, may be null).  Implemented in util.cu.
+cudaError_t emin_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* total_dev,
+                          int64_t* scratch, cudaStream_t s);
+int64_t emin_scan_scratch_elems(int64_t n);
+
+int emin_num_sms();

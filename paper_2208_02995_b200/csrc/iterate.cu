@@ -1,0 +1,529 @@
+// iterate.cu -- Alg. 3 EMIN_PCG on the device: the two streaming
+// stages, the masked SpGEMM step, the single-block scalar kernels, CUDA-graph
+// capture of k iterations, and the remaining ABI calls.
+//
+// Per iteration (all scalars stay in device memory, no host sync):
+//   stage I   r -= alpha_{k-1} yb (deferred update of step k-1);
+//             z = D^-1 r [Pi]; partial gamma = r.z
+//   scalar    gamma; stop if gamma <= 0; beta = gamma/gamma_old
+//   stage II  dw += alpha_{k-1} y_{k-1} (deferred);
+//             y = z + beta y (y = z at k = 1)
+//   SpGEMM    yb = Pi K y = Pi (A Y)|pattern; partial y.yb
+//   scalar    alpha = gamma / y.yb ; dE = gamma alpha ; stop tests   (A4, A18)
+// The deferral moves no arithmetic: each element sees exactly the update
+// Alg. 3 applies, one kernel later; a stopped step leaves nothing pending.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "emin_internal.cuh"
+#include "masked.cuh"
+#include "kernels_fast.cuh"
+
+namespace {
+
+// ------------------------------------------------------------ stage I
+template <int G, bool PROJ>
+__global__ void __launch_bounds__(256)
+k_stage1(DevView v, double* __restrict__ r, const double* __restrict__ yb, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = st->pend;
+  const double ap = st->alpha_pend;
+  const int lg = threadIdx.x & (G - 1);
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int nv = v.nv;
+  double part = 0.0;
+  // warp-uniform trip count: the PROJ path shuffles inside the loop
+  for (int64_t i = gid; __any_sync(0xffffffffu, i < v.nF); i += ng) {
+    const bool act = i < v.nF;
+    const int64_t b = act ? v.wptr[i] : 0, e = act ? v.wptr[i + 1] : 0;
+    const double di = act ? v.d[i] : 1.0;
+    if (!PROJ) {
+      for (int64_t p = b + lg; p < e; p += G) {
+        double rv = r[p];
+        if (pend) { rv = rv - ap * yb[p]; r[p] = rv; }
+        const double z = rv / di;
+        part = fma(rv, z, part);
+      }
+    } else {
+      double dots[EMIN_NV_MAX];
+#pragma unroll
+      for (int m = 0; m < EMIN_NV_MAX; ++m) dots[m] = 0.0;
+      for (int64_t p = b + lg; p < e; p += G) {
+        double rv = r[p];
+        if (pend) { rv = rv - ap * yb[p]; r[p] = rv; }
+        const double z = rv / di;
+#pragma unroll
+        for (int m = 0; m < EMIN_NV_MAX; ++m) if (m < nv) dots[m] = fma(v.Q[p * nv + m], z, dots[m]);
+      }
+#pragma unroll
+      for (int m = 0; m < EMIN_NV_MAX; ++m) if (m < nv) dots[m] = group_sum<G>(dots[m]);
+      for (int64_t p = b + lg; p < e; p += G) {
+        const double rv = r[p];
+        double z = rv / di, s = 0.0;
+#pragma unroll
+        for (int m = 0; m < EMIN_NV_MAX; ++m) if (m < nv) s = fma(v.Q[p * nv + m], dots[m], s);
+        z -= s;
+        part = fma(rv, z, part);
+      }
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// ------------------------------------------------------------ stage II
+template <int G, bool PROJ>
+__global__ void __launch_bounds__(256)
+k_stage2(DevView v, const double* __restrict__ r, double* __restrict__ y, double* __restrict__ dw) {
+  const DevState* st = v.st;
+  const int stopped = st->stopped;
+  const int pendw = st->pendw;
+  if (stopped && !pendw) return;
+  const double ap = st->alpha_pend;
+  const double beta = st->beta;
+  const bool first = (st->k_total == 0);
+  const int lg = threadIdx.x & (G - 1);
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int nv = v.nv;
+  // warp-uniform trip count: the PROJ path shuffles inside the loop
+  for (int64_t i = gid; __any_sync(0xffffffffu, i < v.nF); i += ng) {
+    const bool act = i < v.nF;
+    const int64_t b = act ? v.wptr[i] : 0, e = act ? v.wptr[i + 1] : 0;
+    const double di = act ? v.d[i] : 1.0;
+    double dots[EMIN_NV_MAX];
+#pragma unroll
+    for (int m = 0; m < EMIN_NV_MAX; ++m) dots[m] = 0.0;
+    if (PROJ && !stopped) {
+      for (int64_t p = b + lg; p < e; p += G) {
+        const double z = r[p] / di;
+#pragma unroll
+        for (int m = 0; m < EMIN_NV_MAX; ++m) if (m < nv) dots[m] = fma(v.Q[p * nv + m], z, dots[m]);
+      }
+#pragma unroll
+      for (int m = 0; m < EMIN_NV_MAX; ++m) if (m < nv) dots[m] = group_sum<G>(dots[m]);
+    }
+    for (int64_t p = b + lg; p < e; p += G) {
+      const double yo = y[p];
+      if (pendw) dw[p] = dw[p] + ap * yo;
+      if (!stopped) {
+        double z = r[p] / di;
+        if (PROJ) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < EMIN_NV_MAX; ++m) if (m < nv) s = fma(v.Q[p * nv + m], dots[m], s);
+          z -= s;
+        }
+        y[p] = first ? z : z + beta * yo;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ scalars
+__device__ double reduce_partials(const double* __restrict__ p, int np, double* sh) {
+  double s = 0.0;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) s += p[k];
+  return block_sum(s, sh);
+}
+
+__global__ void k_scalar_gamma(DevState* st, const double* __restrict__ partials, int np) {
+  __shared__ double sh[32];
+  if (st->stopped) return;
+  const double g = reduce_partials(partials, np, sh);
+  if (threadIdx.x == 0) {
+    st->pendw = st->pend;
+    st->pend = 0;
+    if (!(g > 0.0)) { st->stopped = 1; return; }
+    st->beta = (st->k_total == 0) ? 0.0 : g / st->gamma_old;
+    st->gamma = g;
+    st->gamma_old = g;
+  }
+}
+
+__global__ void k_scalar_alpha(DevState* st, const double* __restrict__ partials, int np,
+                               double* __restrict__ dE_hist) {
+  __shared__ double sh[32];
+  if (threadIdx.x == 0) st->pendw = 0;
+  if (st->stopped) return;
+  const double den = reduce_partials(partials, np, sh);
+  if (threadIdx.x == 0) {
+    st->den = den;
+    if (den < 0.0) { st->stopped = 5; return; }
+    if (den == 0.0) { st->stopped = 2; return; }
+    const double alpha = st->gamma / den;
+    const double dE = st->gamma * alpha;
+    const int64_t k = st->k_total + 1;
+    if (k == 1) st->dE1 = dE;
+    if (st->tau > 0.0 && k > 1 && dE < st->tau * st->dE1) { st->stopped = 3; return; }
+    if (dE <= st->stag * st->E0) { st->stopped = 4; return; }
+    st->alpha_pend = alpha;
+    st->pend = 1;
+    dE_hist[st->k_total] = dE;
+    st->k_total = k;
+    st->k_call += 1;
+  }
+}
+
+// apply a pending update (before reading W or r from outside the loop)
+__global__ void k_flush(DevView v, double* __restrict__ r, const double* __restrict__ yb,
+                        double* __restrict__ dw, const double* __restrict__ y) {
+  const DevState* st = v.st;
+  if (!st->pend) return;
+  const double ap = st->alpha_pend;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.nnzW;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    r[p] = r[p] - ap * yb[p];
+    dw[p] = dw[p] + ap * y[p];
+  }
+}
+__global__ void k_flush_done(DevState* st) { st->pend = 0; }
+
+__global__ void k_reset_state(DevState* st, const double* __restrict__ Epart, int np, double add,
+                              double tau, double stag) {
+  __shared__ double sh[32];
+  const double e = reduce_partials(Epart, np, sh);
+  if (threadIdx.x == 0) {
+    st->gamma = st->gamma_old = st->beta = st->alpha_pend = st->den = st->dE1 = 0.0;
+    st->E0 = e + add;
+    st->tau = tau;
+    st->stag = stag;
+    st->k_total = 0;
+    st->stopped = 0;
+    st->pend = st->pendw = 0;
+    st->k_call = 0;
+  }
+}
+
+__global__ void k_energy_out(const double* __restrict__ partials, int np, double add, double* out) {
+  __shared__ double sh[32];
+  const double e = reduce_partials(partials, np, sh);
+  if (threadIdx.x == 0) *out = e + add;
+}
+
+__global__ void k_get_P(DevView v, const double* __restrict__ w0, const double* __restrict__ dw,
+                        const int64_t* __restrict__ pofs, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < v.nF; i += nw) {
+    const int64_t b = v.wptr[i];
+    const int nj = (int)(v.wptr[i + 1] - b);
+    const int64_t o = pofs[i];
+    for (int t = lane; t < nj; t += 32) out[o + t] = w0[b + t] + dw[b + t];
+  }
+}
+__global__ void k_get_P_crows(int64_t m, const uint8_t* __restrict__ isc, const int64_t* __restrict__ prp,
+                              double* __restrict__ out) {
+  for (int64_t rl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rl < m; rl += (int64_t)gridDim.x * blockDim.x)
+    if (isc[rl]) out[prp[rl] - prp[0]] = 1.0;
+}
+
+int pick_group(double avg) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int G = 1; G <= 32; G <<= 1) {
+    const double eff = avg / (std::ceil(avg / G) * G);
+    if (eff >= best_eff - 1e-12) { best = G; best_eff = eff; }
+  }
+  return best;
+}
+
+template <int G>
+void launch_stage1_g(emin_ctx c, cudaStream_t s) {
+  const DevView v = c->view();
+  if (c->opts.project_after_jacobi)
+    k_stage1<G, true><<<c->grid_rows, 256, 0, s>>>(v, c->r, c->yb, c->partials);
+  else
+    k_stage1<G, false><<<c->grid_rows, 256, 0, s>>>(v, c->r, c->yb, c->partials);
+}
+template <int G>
+void launch_stage2_g(emin_ctx c, cudaStream_t s) {
+  const DevView v = c->view();
+  if (c->opts.project_after_jacobi)
+    k_stage2<G, true><<<c->grid_rows, 256, 0, s>>>(v, c->r, c->y, c->dw);
+  else
+    k_stage2<G, false><<<c->grid_rows, 256, 0, s>>>(v, c->r, c->y, c->dw);
+}
+void launch_stage(emin_ctx c, int which, cudaStream_t s) {
+  switch (c->group) {
+#define CASE_G(GG) case GG: which == 1 ? launch_stage1_g<GG>(c, s) : launch_stage2_g<GG>(c, s); break;
+    CASE_G(1) CASE_G(2) CASE_G(4) CASE_G(8) CASE_G(16) CASE_G(32)
+#undef CASE_G
+  }
+}
+
+}  // namespace
+
+// ============================================================ internal API
+// mode: MM_ITER (X = y), MM_R0 (X = w0), MM_ENERGY (X = w0, X2 = dw)
+int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
+                       cudaStream_t s) {
+  const DevView v = c->view();
+  const int grid = c->grid_spgemm;
+  if (mode == MM_ITER && c->kernel_path == 1) {
+    launch_scalar_spgemm(c, s);
+    return grid;
+  }
+  const int mc = c->max_row <= 32 ? 1 : c->max_row <= 64 ? 2 : 4;
+#define LAUNCH_M(MODE, MC, SUMX) \
+  k_masked_generic<MODE, MC, SUMX><<<grid, 256, 0, s>>>(v, X, X2, out, c->partials)
+  if (mode == MM_ITER) {
+    if (mc == 1) LAUNCH_M(MM_ITER, 1, false); else if (mc == 2) LAUNCH_M(MM_ITER, 2, false); else LAUNCH_M(MM_ITER, 4, false);
+  } else if (mode == MM_R0) {
+    if (mc == 1) LAUNCH_M(MM_R0, 1, false); else if (mc == 2) LAUNCH_M(MM_R0, 2, false); else LAUNCH_M(MM_R0, 4, false);
+  } else {
+    if (mc == 1) LAUNCH_M(MM_ENERGY, 1, true); else if (mc == 2) LAUNCH_M(MM_ENERGY, 2, true); else LAUNCH_M(MM_ENERGY, 4, true);
+  }
+#undef LAUNCH_M
+  return grid;
+}
+
+// r0 = -Pi (A P0)|F, E0, fresh CG state (end of setup and emin_reset)
+emin_status emin_finish_r0(emin_ctx c) {
+  cudaStream_t s = c->stream;
+  const int SM = emin_num_sms();
+  if (!c->grid_spgemm) {
+    c->group = pick_group(c->nF ? (double)c->nnzW / (double)c->nF : 1.0);
+    c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF * c->group + 255) / 256, (int64_t)SM * 8));
+    c->grid_spgemm = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF + 7) / 8, (int64_t)SM * 8));
+    c->kernel_path = select_fast_path(c);
+    if (c->kernel_path == 1) c->grid_spgemm = scalar_spgemm_grid(c);
+    c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
+    if (c->grid_red > c->n_partials) { c->last_error = "partials buffer too small"; return EMIN_ERR_STATE; }
+  }
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(c->dw, 0, sizeof(double) * std::max<int64_t>(c->nnzW, 1), s));
+  emin_launch_masked(c, MM_R0, c->w0, nullptr, c->r, s);
+  // energy of P0 (dw = 0)
+  const int g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, s);
+  k_reset_state<<<1, 1024, 0, s>>>(c->st, c->partials, g, c->sum_diag_cc, c->opts.tau, c->opts.stagnation_rel);
+  EMIN_CUDA_TRY(c, cudaGetLastError());
+  c->k_launched = 0;
+  c->breakdown_reported = 0;
+  return EMIN_OK;
+}
+
+static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev) {
+  auto rec = [&](int t) {
+    if (ev) cudaEventRecordWithFlags(ev[t], s, cudaEventRecordExternal);
+  };
+  rec(0);
+  launch_stage(c, 1, s);
+  rec(1);
+  k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, c->partials, c->grid_rows);
+  rec(2);
+  launch_stage(c, 2, s);
+  rec(3);
+  const int g = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
+  rec(4);
+  k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, c->partials, g, c->dE_hist);
+  rec(5);
+}
+
+static emin_status build_graph(emin_ctx c, int k) {
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  if (!c->cap_stream) EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  const int prof = c->profiling;
+  if (prof) {
+    const size_t need = (size_t)6 * k;
+    while (c->ev.size() < need) {
+      cudaEvent_t e;
+      EMIN_CUDA_TRY(c, cudaEventCreate(&e));
+      c->ev.push_back(e);
+    }
+  }
+  cudaStream_t s = c->cap_stream;
+  EMIN_CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  cudaMemsetAsync(&c->st->k_call, 0, sizeof(int32_t), s);
+  for (int it = 0; it < k; ++it) enqueue_iteration(c, s, prof ? &c->ev[6 * it] : nullptr);
+  cudaGraph_t g;
+  EMIN_CUDA_TRY(c, cudaStreamEndCapture(s, &g));
+  cudaError_t e = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  EMIN_CUDA_TRY(c, e);
+  c->graph_k = k;
+  c->graph_prof = prof;
+  return EMIN_OK;
+}
+
+static emin_status ensure_hist(emin_ctx c, int64_t need) {
+  if (need <= c->dE_cap) return EMIN_OK;
+  int64_t cap = std::max<int64_t>(need, std::max<int64_t>(64, 2 * c->dE_cap));
+  double* nh;
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&nh, sizeof(double) * cap, c->stream));
+  if (c->dE_hist) {
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(nh, c->dE_hist, sizeof(double) * c->dE_cap, cudaMemcpyDeviceToDevice, c->stream));
+    cudaFreeAsync(c->dE_hist, c->stream);
+  }
+  c->dE_hist = nh;
+  c->dE_cap = cap;
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; c->graph_k = -1; }
+  return EMIN_OK;
+}
+
+extern "C" emin_status emin_iterate(emin_ctx c, int32_t k, int32_t* k_done, double* dE) {
+  if (!c) return EMIN_ERR_ARG;
+  if (k < 0) { c->last_error = "k < 0"; return EMIN_ERR_ARG; }
+  if (k_done) *k_done = 0;
+  if (k == 0) return EMIN_OK;
+  emin_status st = ensure_hist(c, c->k_launched + k);
+  if (st != EMIN_OK) return st;
+  if (!c->graph || c->graph_k != k || c->graph_prof != c->profiling) {
+    st = build_graph(c, k);
+    if (st != EMIN_OK) return st;
+  }
+  EMIN_CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
+  c->k_launched += k;
+  if (c->profiling) {
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int it = 0; it < k; ++it) {
+      cudaEvent_t* e = &c->ev[6 * it];
+      float t[5];
+      for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&t[j], e[j], e[j + 1]);
+      c->prof_ms[0] += t[0];
+      c->prof_ms[1] += t[2];
+      c->prof_ms[2] += t[3];
+      c->prof_ms[3] += t[1] + t[4];
+      c->prof_launches[0] += 1; c->prof_launches[1] += 1; c->prof_launches[2] += 1;
+      c->prof_launches[3] += 2;
+    }
+  }
+  if (k_done || dE) {
+    DevState h;
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(&h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (k_done) *k_done = h.k_call;
+    if (dE && h.k_call > 0)
+      EMIN_CUDA_TRY(c, cudaMemcpy(dE, c->dE_hist + (h.k_total - h.k_call), sizeof(double) * h.k_call,
+                                  cudaMemcpyDeviceToHost));
+    if (h.stopped == 5 && !c->breakdown_reported) {
+      c->breakdown_reported = 1;
+      c->last_error = "y^T Pi K y < 0 (breakdown)";
+      return EMIN_ERR_BREAKDOWN;
+    }
+  }
+  EMIN_CUDA_TRY(c, cudaGetLastError());
+  return EMIN_OK;
+}
+
+static void flush(emin_ctx c) {
+  const int SM = emin_num_sms();
+  k_flush<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->r, c->yb, c->dw, c->y);
+  k_flush_done<<<1, 1, 0, c->stream>>>(c->st);
+}
+
+extern "C" emin_status emin_energy(emin_ctx c, double* E) {
+  if (!c || !E) return EMIN_ERR_ARG;
+  flush(c);
+  const int g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, c->stream);
+  double* dev;
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&dev, sizeof(double), c->stream));
+  k_energy_out<<<1, 1024, 0, c->stream>>>(c->partials, g, c->sum_diag_cc, dev);
+  EMIN_CUDA_TRY(c, cudaMemcpyAsync(E, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  cudaFreeAsync(dev, c->stream);
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return EMIN_OK;
+}
+
+extern "C" emin_status emin_get_P(emin_ctx c, double* P_val) {
+  if (!c || !P_val) return EMIN_ERR_ARG;
+  flush(c);
+  const int SM = emin_num_sms();
+  double* out = P_val;
+  if (!c->opts.inputs_on_device)
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&out, sizeof(double) * std::max<int64_t>(c->nnzP, 1), c->stream));
+  k_get_P<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->w0, c->dw, c->pofs, out);
+  k_get_P_crows<<<SM * 8, 256, 0, c->stream>>>(c->m_owned, c->isc_own, c->cofs, out);
+  EMIN_CUDA_TRY(c, cudaGetLastError());
+  if (!c->opts.inputs_on_device) {
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(P_val, out, sizeof(double) * c->nnzP, cudaMemcpyDeviceToHost, c->stream));
+    cudaFreeAsync(out, c->stream);
+  }
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return EMIN_OK;
+}
+
+extern "C" emin_status emin_reset(emin_ctx c) {
+  if (!c) return EMIN_ERR_ARG;
+  return emin_finish_r0(c);
+}
+
+extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
+  if (!c || !rep) return EMIN_ERR_ARG;
+  DevState h;
+  EMIN_CUDA_TRY(c, cudaMemcpyAsync(&h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  std::memset(rep, 0, sizeof(*rep));
+  rep->E0 = h.E0;
+  rep->dE1 = h.dE1;
+  rep->k_total = h.k_total;
+  rep->stop_reason = h.stopped;
+  rep->n_svd_rows = c->n_svd;
+  rep->n_frozen_rows = c->n_frozen;
+  rep->n_fine = c->nF;
+  rep->nnz_W = c->nnzW;
+  rep->nnz_AFF = c->nnzAFF;
+  rep->kernel_path = c->kernel_path;
+  rep->nranks = c->nranks;
+  if (h.stopped == 5 && !c->breakdown_reported) {
+    c->breakdown_reported = 1;
+    return EMIN_ERR_BREAKDOWN;
+  }
+  return EMIN_OK;
+}
+
+extern "C" emin_status emin_get_layout(emin_ctx c, int64_t* wptr, int32_t* wcol, int64_t* pofs) {
+  if (!c) return EMIN_ERR_ARG;
+  if (wptr) EMIN_CUDA_TRY(c, cudaMemcpyAsync(wptr, c->wptr, sizeof(int64_t) * (c->nF + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (wcol && c->nnzW)
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(wcol, c->wcol, sizeof(int32_t) * c->nnzW, cudaMemcpyDeviceToHost, c->stream));
+  if (pofs && c->nF) EMIN_CUDA_TRY(c, cudaMemcpyAsync(pofs, c->pofs, sizeof(int64_t) * c->nF, cudaMemcpyDeviceToHost, c->stream));
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return EMIN_OK;
+}
+
+extern "C" emin_status emin_set_profiling(emin_ctx c, int32_t on) {
+  if (!c) return EMIN_ERR_ARG;
+  c->profiling = on ? 1 : 0;
+  for (int j = 0; j < 4; ++j) { c->prof_ms[j] = 0.0; c->prof_launches[j] = 0; }
+  return EMIN_OK;
+}
+
+extern "C" emin_status emin_kernel_times(emin_ctx c, double* ms, int64_t* launches) {
+  if (!c) return EMIN_ERR_ARG;
+  for (int j = 0; j < 4; ++j) {
+    if (ms) ms[j] = c->prof_ms[j];
+    if (launches) launches[j] = c->prof_launches[j];
+  }
+  return EMIN_OK;
+}
+
+void emin_free_all(emin_ctx c) {
+  cudaStream_t s = c->stream;
+  void* ptrs[] = {c->wptr, c->affptr, c->afcptr, c->pofs, c->cofs, c->isc_own, c->wcol, c->affcol,
+                  c->afccol, c->affval, c->afcval, c->d, c->Q, c->w0, c->dw, c->r, c->r0, c->y,
+                  c->yb, c->partials, c->dE_hist, c->st};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, s);
+  free_fast_path(c);
+  cudaStreamSynchronize(s);
+}
+
+extern "C" void emin_destroy(emin_ctx c) {
+  if (!c) return;
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  emin_free_all(c);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  delete c;
+}
+
+extern "C" const char* emin_setup_error_internal();
+extern "C" const char* emin_last_error(emin_ctx c) {
+  if (!c) return emin_setup_error_internal();
+  return c->last_error.c_str();
+}

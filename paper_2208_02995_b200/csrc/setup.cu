@@ -1,0 +1,697 @@
+// setup.cu -- emin_setup: validation, F-row index preparation, Alg. 2
+// (EMIN_SetUp) per F row, r0 and E0 (start of Alg. 3).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "emin_internal.cuh"
+#include "masked.cuh"
+
+namespace {
+
+thread_local std::string g_setup_error;
+
+// ------------------------------------------------------------ index prep
+__global__ void k_coarse_flags(const uint8_t* __restrict__ isc, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = isc[r] ? 1 : 0;
+}
+
+struct RowsArgs {
+  int64_t m, row_begin, row_end, n_global, nc_global;
+  int64_t fbegin;                 // global F id of the first owned F row
+  const int64_t* Arp; const int32_t* Acol; const double* Aval;
+  const uint8_t* isc; const int64_t* cidx;   // exclusive scan of is_coarse (global)
+  const int64_t* Prp; const int32_t* Pcol; const double* Pval;
+  int64_t* cnt_ff; int64_t* cnt_fc; int64_t* cnt_w;  // per owned F row
+  double* d; double* dcc;          // F-row diagonal; C-row diagonal (per owned row, 0 for F)
+  int32_t* err; int64_t* err_row; int32_t* max_row;
+};
+
+__device__ __forceinline__ void raise_err(const RowsArgs& a, int32_t bit, int64_t row) {
+  atomicOr(a.err, bit);
+  atomicMin((unsigned long long*)a.err_row, (unsigned long long)row);
+}
+
+// Validation + per-row counts (one thread per owned row; setup only).
+__global__ void k_rows(RowsArgs a) {
+  for (int64_t rl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rl < a.m;
+       rl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = a.row_begin + rl;
+    const bool coarse = a.isc[r] != 0;
+    const int64_t fl = (r - a.cidx[r]) - a.fbegin;   // local F id (valid if !coarse)
+    // ---- A row
+    const int64_t qb = a.Arp[rl] - a.Arp[0], qe = a.Arp[rl + 1] - a.Arp[0];
+    if (qe < qb) { raise_err(a, EF_CSR, r); continue; }
+    int64_t nff = 0, nfc = 0;
+    double diag = 0.0;
+    bool has_diag = false;
+    int32_t prev = -1;
+    for (int64_t q = qb; q < qe; ++q) {
+      const int32_t c = a.Acol[q];
+      const double v = a.Aval[q];
+      if (c < 0 || c >= a.n_global || c <= prev) { raise_err(a, EF_CSR, r); break; }
+      prev = c;
+      if (!isfinite(v)) raise_err(a, EF_NONFINITE, r);
+      if (c == r) { diag = v; has_diag = true; }
+      if (a.isc[c]) ++nfc; else ++nff;
+    }
+    if (coarse) {
+      a.dcc[rl] = diag;
+    } else {
+      a.dcc[rl] = 0.0;
+      if (!has_diag || !(diag > 0.0)) raise_err(a, EF_DIAG, r);
+      a.d[fl] = diag;
+      a.cnt_ff[fl] = nff;
+      a.cnt_fc[fl] = nfc;
+    }
+    // ---- P row
+    const int64_t pb = a.Prp[rl] - a.Prp[0], pe = a.Prp[rl + 1] - a.Prp[0];
+    const int64_t len = pe - pb;
+    if (len < 0) { raise_err(a, EF_PATTERN, r); continue; }
+    if (coarse) {
+      if (len != 1 || a.Pcol[pb] != (int32_t)a.cidx[r] || (a.Pval && a.Pval[pb] != 1.0))
+        raise_err(a, EF_PATTERN, r);
+    } else {
+      if (len == 0) raise_err(a, EF_PATTERN, r);
+      if (len > EMIN_MAX_ROW) raise_err(a, EF_ROWLEN, r);
+      int32_t pp = -1;
+      for (int64_t q = pb; q < pe; ++q) {
+        const int32_t c = a.Pcol[q];
+        if (c < 0 || c >= a.nc_global || c <= pp) { raise_err(a, EF_PATTERN, r); break; }
+        pp = c;
+        if (a.Pval && !isfinite(a.Pval[q])) raise_err(a, EF_NONFINITE, r);
+      }
+      a.cnt_w[fl] = len;
+      atomicMax(a.max_row, (int32_t)(len < INT_MAX ? len : INT_MAX));
+    }
+  }
+}
+
+__global__ void k_check_B(int64_t m, int64_t row_begin, int32_t nv, const uint8_t* __restrict__ isc,
+                          const int64_t* __restrict__ cidx, const double* __restrict__ B,
+                          const double* __restrict__ Bc, int64_t nc, int32_t* err, int64_t* err_row) {
+  const int64_t tot = m * nv;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rl = e / nv;
+    const int mm = (int)(e % nv);
+    const int64_t r = row_begin + rl;
+    const double b = B[e];
+    if (!isfinite(b)) { atomicOr(err, EF_NONFINITE); atomicMin((unsigned long long*)err_row, (unsigned long long)r); }
+    if (isc[r] && Bc[cidx[r] * nv + mm] != b) {
+      atomicOr(err, EF_BC);
+      atomicMin((unsigned long long*)err_row, (unsigned long long)r);
+    }
+  }
+  const int64_t tc = nc * nv;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tc; e += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(Bc[e])) atomicOr(err, EF_NONFINITE);
+}
+
+struct FillArgs {
+  int64_t m, row_begin, row_end, fbegin, nF;
+  const int64_t* Arp; const int32_t* Acol; const double* Aval;
+  const uint8_t* isc; const int64_t* cidx;
+  const int64_t* Prp; const int32_t* Pcol; const double* Pval;
+  const int64_t* wptr; const int64_t* affptr; const int64_t* afcptr;
+  int32_t* wcol; double* what; int64_t* pofs;
+  int32_t* affcol; double* affval; int32_t* afccol; double* afcval;
+  int64_t* frow;   // local F id -> local row
+};
+
+// F rows: copy the pattern into the W layout, split A into A_FF (local F
+// ids) and A_FC (coarse ids).  One warp per owned row (coalesced copies).
+__global__ void k_fill(FillArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t rl = gw; rl < a.m; rl += nw) {
+    const int64_t r = a.row_begin + rl;
+    if (a.isc[r]) continue;
+    const int64_t fl = (r - a.cidx[r]) - a.fbegin;
+    if (lane == 0) { a.frow[fl] = rl; a.pofs[fl] = a.Prp[rl] - a.Prp[0]; }
+    const int64_t pb = a.Prp[rl] - a.Prp[0];
+    const int64_t wb = a.wptr[fl];
+    const int len = (int)(a.wptr[fl + 1] - wb);
+    for (int t = lane; t < len; t += 32) {
+      a.wcol[wb + t] = a.Pcol[pb + t];
+      a.what[wb + t] = a.Pval ? a.Pval[pb + t] : 0.0;
+    }
+    const int64_t qb = a.Arp[rl] - a.Arp[0], qe = a.Arp[rl + 1] - a.Arp[0];
+    int64_t off_ff = a.affptr[fl], off_fc = a.afcptr[fl];
+    for (int64_t q0 = qb; q0 < qe; q0 += 32) {
+      const int64_t q = q0 + lane;
+      bool valid = q < qe;
+      int32_t c = valid ? a.Acol[q] : 0;
+      double v = valid ? a.Aval[q] : 0.0;
+      const bool coarse = valid && a.isc[c];
+      const bool fine = valid && !coarse;
+      const unsigned mf = __ballot_sync(0xffffffffu, fine);
+      const unsigned mc = __ballot_sync(0xffffffffu, coarse);
+      const unsigned lt = (1u << lane) - 1u;
+      if (fine) {
+        const int64_t gF = (int64_t)c - a.cidx[c];
+        const int64_t loc = gF - a.fbegin;     // owned (single GPU: always)
+        const int64_t pos = off_ff + __popc(mf & lt);
+        a.affcol[pos] = (int32_t)loc;
+        a.affval[pos] = v;
+      }
+      if (coarse) {
+        const int64_t pos = off_fc + __popc(mc & lt);
+        a.afccol[pos] = (int32_t)a.cidx[c];
+        a.afcval[pos] = v;
+      }
+      off_ff += __popc(mf);
+      off_fc += __popc(mc);
+    }
+  }
+}
+
+// ------------------------------------------------------------ Alg. 2
+// One warp per owned F row i (P:626-659 with readings A5, A6):
+//   M = B_c(J_i,:) (nj x nv), r = b_i - M^T w^_i,
+//   QR branch (nj >= nv, rank(R) = nv): M = Q R by twice-iterated
+//     classical Gram-Schmidt (an economy QR; Pi depends only on range(M)),
+//     delta = Q R^{-T} r (least-norm solution of M^T delta = r);
+//   SVD branch otherwise: one-sided Jacobi SVD of M, k = #{s > tol s_max},
+//     Q = U(:,1:k), delta = U_k S_k^{-1} V_k^T r.
+//   w0 = w^ + delta ; Q stored row-major per entry, zero padded to nv.
+template <int MAXC>
+__global__ void __launch_bounds__(128)
+k_alg2(DevView v, const double* __restrict__ Bc, const double* __restrict__ B,
+       const int64_t* __restrict__ frow, const double* __restrict__ what, double tol,
+       double* __restrict__ Qout, double* __restrict__ w0, unsigned long long* counters) {
+  __shared__ double Rs[4][EMIN_NV_MAX][EMIN_NV_MAX];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nv = v.nv;
+  double (*R)[EMIN_NV_MAX] = Rs[wib];
+  for (int64_t i = gw; i < v.nF; i += nw) {
+    const int64_t b = v.wptr[i];
+    const int nj = (int)(v.wptr[i + 1] - b);
+    const int64_t rl = frow[i];
+    int32_t jj[MAXC];
+    double wh[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int t = lane + 32 * c;
+      jj[c] = (t < nj) ? v.wcol[b + t] : 0;
+      wh[c] = (t < nj) ? what[b + t] : 0.0;
+    }
+    auto Mval = [&](int c, int m) -> double {
+      return (lane + 32 * c < nj) ? __ldg(Bc + (int64_t)jj[c] * nv + m) : 0.0;
+    };
+    double rv[EMIN_NV_MAX];
+#pragma unroll
+    for (int m = 0; m < EMIN_NV_MAX; ++m) {
+      rv[m] = 0.0;
+      if (m < nv) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) s = fma(Mval(c, m), wh[c], s);
+        rv[m] = B[rl * nv + m] - warp_sum(s);
+      }
+    }
+    double q[MAXC][EMIN_NV_MAX];
+    double delta[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) delta[c] = 0.0;
+    bool qr_ok = false;
+    int krank = 0;
+    if (nj >= nv) {
+      // ---- CGS2 QR
+#pragma unroll
+      for (int j = 0; j < EMIN_NV_MAX; ++j) {
+        if (j >= nv) break;
+        double vc[MAXC];
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) vc[c] = Mval(c, j);
+        double rcol[EMIN_NV_MAX];
+#pragma unroll
+        for (int l = 0; l < EMIN_NV_MAX; ++l) rcol[l] = 0.0;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+          for (int l = 0; l < EMIN_NV_MAX; ++l) {
+            if (l < j) {
+              double s = 0.0;
+#pragma unroll
+              for (int c = 0; c < MAXC; ++c) s = fma(q[c][l], vc[c], s);
+              const double h = warp_sum(s);
+              rcol[l] += h;
+#pragma unroll
+              for (int c = 0; c < MAXC; ++c) vc[c] = fma(-h, q[c][l], vc[c]);
+            }
+          }
+        }
+        double s2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) s2 = fma(vc[c], vc[c], s2);
+        const double nrm = sqrt(warp_sum(s2));
+        rcol[j] = nrm;
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) q[c][j] = (nrm > 0.0) ? vc[c] / nrm : 0.0;
+        if (lane == 0) {
+#pragma unroll
+          for (int l = 0; l < EMIN_NV_MAX; ++l) if (l <= j) R[l][j] = rcol[l];
+        }
+      }
+      __syncwarp();
+      double rmax = 0.0, rmin = INFINITY;
+      for (int j = 0; j < nv; ++j) {
+        const double a = fabs(R[j][j]);
+        rmax = fmax(rmax, a);
+        rmin = fmin(rmin, a);
+      }
+      qr_ok = (rmax > 0.0) && (rmin > tol * rmax);
+      if (qr_ok) {
+        // R^T u = r (forward substitution), delta = Q u
+        double u[EMIN_NV_MAX];
+#pragma unroll
+        for (int j = 0; j < EMIN_NV_MAX; ++j) {
+          u[j] = 0.0;
+          if (j < nv) {
+            double s = rv[j];
+#pragma unroll
+            for (int l = 0; l < EMIN_NV_MAX; ++l) if (l < j) s -= R[l][j] * u[l];
+            u[j] = s / R[j][j];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < EMIN_NV_MAX; ++j) if (j < nv) s = fma(q[c][j], u[j], s);
+          delta[c] = s;
+        }
+        krank = nv;
+      }
+      __syncwarp();
+    }
+    if (!qr_ok) {
+      // ---- one-sided Jacobi SVD; V lives in shared memory (R slot reused)
+      double (*V)[EMIN_NV_MAX] = R;
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+        for (int j = 0; j < EMIN_NV_MAX; ++j) q[c][j] = (j < nv) ? Mval(c, j) : 0.0;
+      if (lane < EMIN_NV_MAX)
+        for (int j = 0; j < EMIN_NV_MAX; ++j) V[lane][j] = (lane == j) ? 1.0 : 0.0;
+      __syncwarp();
+      for (int sweep = 0; sweep < 100; ++sweep) {
+        bool rotated = false;
+#pragma unroll
+        for (int p = 0; p < EMIN_NV_MAX - 1; ++p) {
+#pragma unroll
+          for (int qq = p + 1; qq < EMIN_NV_MAX; ++qq) {
+            if (qq < nv) {
+              double sa = 0.0, sb = 0.0, sc = 0.0;
+#pragma unroll
+              for (int c = 0; c < MAXC; ++c) {
+                sa = fma(q[c][p], q[c][p], sa);
+                sb = fma(q[c][qq], q[c][qq], sb);
+                sc = fma(q[c][p], q[c][qq], sc);
+              }
+              const double a = warp_sum(sa), bb = warp_sum(sb), cc = warp_sum(sc);
+              if (cc != 0.0 && fabs(cc) > 1e-15 * sqrt(a * bb)) {
+                rotated = true;
+                const double zeta = (bb - a) / (2.0 * cc);
+                const double tt = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+#pragma unroll
+                for (int c = 0; c < MAXC; ++c) {
+                  const double up = q[c][p], uq = q[c][qq];
+                  q[c][p] = cs * up - sn * uq;
+                  q[c][qq] = sn * up + cs * uq;
+                }
+                if (lane < nv) {
+                  const double vp = V[lane][p], vq = V[lane][qq];
+                  V[lane][p] = cs * vp - sn * vq;
+                  V[lane][qq] = sn * vp + cs * vq;
+                }
+                __syncwarp();
+              }
+            }
+          }
+        }
+        if (!rotated) break;
+      }
+      double sig[EMIN_NV_MAX];
+      double smax = 0.0;
+#pragma unroll
+      for (int j = 0; j < EMIN_NV_MAX; ++j) {
+        sig[j] = 0.0;
+        if (j < nv) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) s = fma(q[c][j], q[c][j], s);
+          sig[j] = sqrt(warp_sum(s));
+          smax = fmax(smax, sig[j]);
+        }
+      }
+      int ord[EMIN_NV_MAX];
+      for (int j = 0; j < nv; ++j) ord[j] = j;
+      for (int a = 1; a < nv; ++a)
+        for (int bq = a; bq > 0 && sig[ord[bq]] > sig[ord[bq - 1]]; --bq) {
+          const int tmp = ord[bq]; ord[bq] = ord[bq - 1]; ord[bq - 1] = tmp;
+        }
+      double qn[MAXC][EMIN_NV_MAX];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+        for (int j = 0; j < EMIN_NV_MAX; ++j) qn[c][j] = 0.0;
+      for (int a = 0; a < nv; ++a) {
+        const int ja = ord[a];
+        double sj = 0.0;
+        double ucol[MAXC];
+#pragma unroll
+        for (int j = 0; j < EMIN_NV_MAX; ++j)
+          if (j == ja) {
+            sj = sig[j];
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) ucol[c] = q[c][j];
+          }
+        if (!(smax > 0.0 && sj > tol * smax)) continue;
+        double vr = 0.0;
+        for (int l = 0; l < nv; ++l) vr += V[l][ja] * rv[l];
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+          const double u = ucol[c] / sj;
+#pragma unroll
+          for (int j = 0; j < EMIN_NV_MAX; ++j) if (j == krank) qn[c][j] = u;
+          delta[c] = fma(u, vr / sj, delta[c]);
+        }
+        ++krank;
+      }
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+        for (int j = 0; j < EMIN_NV_MAX; ++j) q[c][j] = qn[c][j];
+      __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int t = lane + 32 * c;
+      if (t < nj) {
+#pragma unroll
+        for (int j = 0; j < EMIN_NV_MAX; ++j) if (j < nv) Qout[(b + t) * nv + j] = q[c][j];
+        w0[b + t] = wh[c] + delta[c];
+      }
+    }
+    if (lane == 0) {
+      if (!qr_ok) atomicAdd(counters + 0, 1ull);
+      if (nj == krank) atomicAdd(counters + 1, 1ull);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_reduce_partials(const double* __restrict__ p, int np, double* out, double add) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) s += p[k];
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) *out = t + add;
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, int64_t n, cudaStream_t s) {
+  return cudaMallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s);
+}
+
+}  // namespace
+
+// ============================================================ host helpers
+int emin_launch_masked(emin_ctx ctx, int mode, const double* X, const double* X2, double* out,
+                       cudaStream_t s);
+emin_status emin_finish_r0(emin_ctx ctx);
+void emin_free_all(emin_ctx ctx);
+
+extern "C" void emin_default_opts(emin_opts* o, int64_t n_global) {
+  std::memset(o, 0, sizeof(*o));
+  o->block_size = 1;
+  o->rank_tol = 1e-10;
+  o->tau = 0.0;
+  o->project_after_jacobi = 0;
+  o->stagnation_rel = 1e-30;
+  o->stream = nullptr;
+  o->nccl_comm = nullptr;
+  o->row_begin = 0;
+  o->row_end = n_global;
+  o->inputs_on_device = 0;
+}
+
+static emin_status fail(emin_ctx ctx, emin_status st, const std::string& msg) {
+  g_setup_error = msg;
+  if (ctx) emin_destroy(ctx);
+  return st;
+}
+
+#define SETUP_TRY(call)                                                                \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? EMIN_ERR_OOM : EMIN_ERR_CUDA, \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+  } while (0)
+
+extern "C" const char* emin_setup_error_internal() { return g_setup_error.c_str(); }
+
+extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_global,
+                                  const int64_t* A_rowptr, const int32_t* A_col, const double* A_val,
+                                  const uint8_t* is_coarse, const int64_t* P_rowptr,
+                                  const int32_t* P_col, const double* P_val, int32_t nv,
+                                  const double* B, const double* Bc, const emin_opts* opts) {
+  emin_ctx ctx = nullptr;
+  if (!out) return fail(ctx, EMIN_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (!opts || !A_rowptr || !A_col || !A_val || !is_coarse || !P_rowptr || !P_col || !B || !Bc)
+    return fail(ctx, EMIN_ERR_ARG, "NULL argument");
+  if (n_global <= 0 || nc_global < 0 || nc_global > n_global || nv < 1 || nv > EMIN_NV_MAX)
+    return fail(ctx, EMIN_ERR_ARG, "bad n_global / nc_global / nv");
+  if (opts->row_begin < 0 || opts->row_end > n_global || opts->row_end <= opts->row_begin)
+    return fail(ctx, EMIN_ERR_ARG, "bad row range");
+  if (opts->nccl_comm)
+    return fail(ctx, EMIN_ERR_ARG, "multi-GPU contexts are created with emin_setup_dist");
+  if (n_global > INT32_MAX || nc_global > INT32_MAX)
+    return fail(ctx, EMIN_ERR_ARG, "n_global exceeds the int32 column range");
+
+  ctx = new emin_ctx_s();
+  ctx->opts = *opts;
+  ctx->stream = (cudaStream_t)opts->stream;
+  ctx->n_global = n_global;
+  ctx->nc_global = nc_global;
+  ctx->m_owned = opts->row_end - opts->row_begin;
+  ctx->nv = nv;
+  cudaStream_t s = ctx->stream;
+  const int64_t m = ctx->m_owned;
+  const int SM = emin_num_sms();
+
+  // ---- stage the inputs on the device (host pointers are copied)
+  int64_t nnzA = 0, nnzP = 0, a0 = 0, p0 = 0;
+  const int64_t *dArp = A_rowptr, *dPrp = P_rowptr;
+  const int32_t *dAcol = A_col, *dPcol = P_col;
+  const double *dAval = A_val, *dPval = P_val, *dB = B, *dBc = Bc;
+  const uint8_t* dIsc = is_coarse;
+  std::vector<void*> temps;
+  auto tmp_free = [&]() { for (void* p : temps) cudaFreeAsync(p, s); temps.clear(); };
+  if (!opts->inputs_on_device) {
+    a0 = A_rowptr[0]; nnzA = A_rowptr[m] - a0;
+    p0 = P_rowptr[0]; nnzP = P_rowptr[m] - p0;
+    int64_t *t1; int32_t *t2; double *t3; uint8_t *t4;
+    SETUP_TRY(dalloc(&t1, m + 1, s)); temps.push_back(t1);
+    SETUP_TRY(cudaMemcpyAsync(t1, A_rowptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, s)); dArp = t1;
+    SETUP_TRY(dalloc(&t2, nnzA, s)); temps.push_back(t2);
+    SETUP_TRY(cudaMemcpyAsync(t2, A_col + a0, sizeof(int32_t) * nnzA, cudaMemcpyHostToDevice, s)); dAcol = t2;
+    SETUP_TRY(dalloc(&t3, nnzA, s)); temps.push_back(t3);
+    SETUP_TRY(cudaMemcpyAsync(t3, A_val + a0, sizeof(double) * nnzA, cudaMemcpyHostToDevice, s)); dAval = t3;
+    SETUP_TRY(dalloc(&t4, n_global, s)); temps.push_back(t4);
+    SETUP_TRY(cudaMemcpyAsync(t4, is_coarse, n_global, cudaMemcpyHostToDevice, s)); dIsc = t4;
+    SETUP_TRY(dalloc(&t1, m + 1, s)); temps.push_back(t1);
+    SETUP_TRY(cudaMemcpyAsync(t1, P_rowptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, s)); dPrp = t1;
+    SETUP_TRY(dalloc(&t2, nnzP, s)); temps.push_back(t2);
+    SETUP_TRY(cudaMemcpyAsync(t2, P_col + p0, sizeof(int32_t) * nnzP, cudaMemcpyHostToDevice, s)); dPcol = t2;
+    if (P_val) {
+      SETUP_TRY(dalloc(&t3, nnzP, s)); temps.push_back(t3);
+      SETUP_TRY(cudaMemcpyAsync(t3, P_val + p0, sizeof(double) * nnzP, cudaMemcpyHostToDevice, s)); dPval = t3;
+    }
+    SETUP_TRY(dalloc(&t3, m * nv, s)); temps.push_back(t3);
+    SETUP_TRY(cudaMemcpyAsync(t3, B, sizeof(double) * m * nv, cudaMemcpyHostToDevice, s)); dB = t3;
+    SETUP_TRY(dalloc(&t3, nc_global * nv, s)); temps.push_back(t3);
+    SETUP_TRY(cudaMemcpyAsync(t3, Bc, sizeof(double) * nc_global * nv, cudaMemcpyHostToDevice, s)); dBc = t3;
+    // the copies start at the first owned entry; kernels index relative to rowptr[0]
+  } else {
+    int64_t hb[2];
+    SETUP_TRY(cudaMemcpyAsync(hb, A_rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SETUP_TRY(cudaMemcpyAsync(hb + 1, A_rowptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    int64_t pb[2];
+    SETUP_TRY(cudaMemcpyAsync(pb, P_rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SETUP_TRY(cudaMemcpyAsync(pb + 1, P_rowptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SETUP_TRY(cudaStreamSynchronize(s));
+    a0 = hb[0]; nnzA = hb[1] - hb[0];
+    p0 = pb[0]; nnzP = pb[1] - pb[0];
+    dAcol = A_col + a0; dAval = A_val + a0; dPcol = P_col + p0;
+    if (P_val) dPval = P_val + p0;
+  }
+  ctx->nnzP = nnzP;
+
+  // ---- coarse numbering: cidx = exclusive scan of is_coarse (global)
+  int64_t *cidx, *scratch, *totals;
+  SETUP_TRY(dalloc(&cidx, n_global + 1, s)); temps.push_back(cidx);
+  SETUP_TRY(dalloc(&scratch, emin_scan_scratch_elems(n_global + m + 8), s)); temps.push_back(scratch);
+  SETUP_TRY(dalloc(&totals, 8, s)); temps.push_back(totals);
+  k_coarse_flags<<<SM * 8, 256, 0, s>>>(dIsc, n_global, cidx);
+  SETUP_TRY(emin_scan_i64(cidx, cidx, n_global, totals + 0, scratch, s));
+  int64_t h_nc = 0, h_cb = 0;
+  SETUP_TRY(cudaMemcpyAsync(&h_nc, totals + 0, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SETUP_TRY(cudaMemcpyAsync(&h_cb, cidx + opts->row_begin, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  int64_t h_ce = 0;
+  if (opts->row_end < n_global)
+    SETUP_TRY(cudaMemcpyAsync(&h_ce, cidx + opts->row_end, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SETUP_TRY(cudaStreamSynchronize(s));
+  if (opts->row_end == n_global) h_ce = h_nc;
+  if (h_nc != nc_global) { tmp_free(); return fail(ctx, EMIN_ERR_ARG, "sum(is_coarse) != nc_global"); }
+  const int64_t fbegin = opts->row_begin - h_cb;
+  const int64_t nF = (opts->row_end - opts->row_begin) - (h_ce - h_cb);
+  ctx->nF = nF;
+  ctx->nFh = nF;
+  ctx->n_crows = h_ce - h_cb;
+
+  // ---- validation + counts
+  int64_t *cnt_ff, *cnt_fc, *cnt_w;
+  double* dcc;
+  int32_t* err;
+  int64_t* err_row;
+  int32_t* max_row;
+  SETUP_TRY(dalloc(&cnt_ff, nF + 1, s)); temps.push_back(cnt_ff);
+  SETUP_TRY(dalloc(&cnt_fc, nF + 1, s)); temps.push_back(cnt_fc);
+  SETUP_TRY(dalloc(&cnt_w, nF + 1, s)); temps.push_back(cnt_w);
+  SETUP_TRY(dalloc(&dcc, m, s)); temps.push_back(dcc);
+  SETUP_TRY(dalloc(&err, 4, s)); temps.push_back(err);
+  SETUP_TRY(dalloc(&err_row, 1, s)); temps.push_back(err_row);
+  max_row = err + 1;
+  SETUP_TRY(dalloc(&ctx->d, nF, s));
+  SETUP_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t) * 4, s));
+  SETUP_TRY(cudaMemsetAsync(err_row, 0x7f, sizeof(int64_t), s));
+  RowsArgs ra;
+  ra.m = m; ra.row_begin = opts->row_begin; ra.row_end = opts->row_end; ra.n_global = n_global;
+  ra.nc_global = nc_global; ra.fbegin = fbegin;
+  ra.Arp = dArp; ra.Acol = dAcol; ra.Aval = dAval; ra.isc = dIsc; ra.cidx = cidx;
+  ra.Prp = dPrp; ra.Pcol = dPcol; ra.Pval = dPval;
+  ra.cnt_ff = cnt_ff; ra.cnt_fc = cnt_fc; ra.cnt_w = cnt_w; ra.d = ctx->d; ra.dcc = dcc;
+  ra.err = err; ra.err_row = err_row; ra.max_row = max_row;
+  k_rows<<<SM * 8, 256, 0, s>>>(ra);
+  k_check_B<<<SM * 8, 256, 0, s>>>(m, opts->row_begin, nv, dIsc, cidx, dB, dBc, nc_global, err, err_row);
+  SETUP_TRY(cudaGetLastError());
+  int32_t h_err[2];
+  int64_t h_err_row;
+  SETUP_TRY(cudaMemcpyAsync(h_err, err, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
+  SETUP_TRY(cudaMemcpyAsync(&h_err_row, err_row, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SETUP_TRY(cudaStreamSynchronize(s));
+  if (h_err[0]) {
+    tmp_free();
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "input validation failed (flags 0x%x) at global row %lld", h_err[0],
+                  (long long)h_err_row);
+    const int32_t f = h_err[0];
+    emin_status st = (f & EF_CSR) ? EMIN_ERR_CSR : (f & EF_NONFINITE) ? EMIN_ERR_NONFINITE
+                   : (f & (EF_PATTERN | EF_ROWLEN)) ? EMIN_ERR_PATTERN : (f & EF_BC) ? EMIN_ERR_BC
+                   : EMIN_ERR_DIAG;
+    return fail(ctx, st, buf);
+  }
+  ctx->max_row = h_err[1];
+
+  // ---- row pointers of the W layout, A_FF and A_FC
+  SETUP_TRY(dalloc(&ctx->wptr, nF + 1, s));
+  SETUP_TRY(dalloc(&ctx->affptr, nF + 1, s));
+  SETUP_TRY(dalloc(&ctx->afcptr, nF + 1, s));
+  SETUP_TRY(emin_scan_i64(cnt_w, ctx->wptr, nF, totals + 1, scratch, s));
+  SETUP_TRY(emin_scan_i64(cnt_ff, ctx->affptr, nF, totals + 2, scratch, s));
+  SETUP_TRY(emin_scan_i64(cnt_fc, ctx->afcptr, nF, totals + 3, scratch, s));
+  SETUP_TRY(cudaMemcpyAsync(ctx->wptr + nF, totals + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  SETUP_TRY(cudaMemcpyAsync(ctx->affptr + nF, totals + 2, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  SETUP_TRY(cudaMemcpyAsync(ctx->afcptr + nF, totals + 3, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  int64_t h_tot[3];
+  SETUP_TRY(cudaMemcpyAsync(h_tot, totals + 1, sizeof(int64_t) * 3, cudaMemcpyDeviceToHost, s));
+  SETUP_TRY(cudaStreamSynchronize(s));
+  ctx->nnzW = ctx->nnzWh = h_tot[0];
+  ctx->nnzAFF = h_tot[1];
+  ctx->nnzAFC = h_tot[2];
+  const int64_t W = ctx->nnzW;
+
+  // ---- fill
+  double* what;
+  SETUP_TRY(dalloc(&ctx->wcol, W, s));
+  SETUP_TRY(dalloc(&what, W, s)); temps.push_back(what);
+  SETUP_TRY(dalloc(&ctx->pofs, nF, s));
+  SETUP_TRY(dalloc(&ctx->cofs, m + 1, s));
+  SETUP_TRY(cudaMemcpyAsync(ctx->cofs, dPrp, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToDevice, s));
+  SETUP_TRY(dalloc(&ctx->isc_own, m, s));
+  SETUP_TRY(cudaMemcpyAsync(ctx->isc_own, dIsc + opts->row_begin, m, cudaMemcpyDeviceToDevice, s));
+  SETUP_TRY(dalloc(&ctx->affcol, ctx->nnzAFF, s));
+  SETUP_TRY(dalloc(&ctx->affval, ctx->nnzAFF, s));
+  SETUP_TRY(dalloc(&ctx->afccol, ctx->nnzAFC, s));
+  SETUP_TRY(dalloc(&ctx->afcval, ctx->nnzAFC, s));
+  int64_t* frow;
+  SETUP_TRY(dalloc(&frow, nF, s)); temps.push_back(frow);
+  FillArgs fa;
+  fa.m = m; fa.row_begin = opts->row_begin; fa.row_end = opts->row_end; fa.fbegin = fbegin; fa.nF = nF;
+  fa.Arp = dArp; fa.Acol = dAcol; fa.Aval = dAval; fa.isc = dIsc; fa.cidx = cidx;
+  fa.Prp = dPrp; fa.Pcol = dPcol; fa.Pval = dPval;
+  fa.wptr = ctx->wptr; fa.affptr = ctx->affptr; fa.afcptr = ctx->afcptr;
+  fa.wcol = ctx->wcol; fa.what = what; fa.pofs = ctx->pofs;
+  fa.affcol = ctx->affcol; fa.affval = ctx->affval; fa.afccol = ctx->afccol; fa.afcval = ctx->afcval;
+  fa.frow = frow;
+  k_fill<<<SM * 16, 256, 0, s>>>(fa);
+  SETUP_TRY(cudaGetLastError());
+
+  // ---- sum of the C-row diagonal (energy constant, Eq. trInc tr(A_cc))
+  SETUP_TRY(dalloc(&ctx->partials, SM * 32, s));
+  ctx->n_partials = SM * 32;
+  double* dsum;
+  SETUP_TRY(dalloc(&dsum, 4, s)); temps.push_back(dsum);
+  k_reduce_partials<<<1, 1024, 0, s>>>(dcc, (int)std::min<int64_t>(m, INT32_MAX), dsum, 0.0);
+
+  // ---- Alg. 2
+  SETUP_TRY(dalloc(&ctx->Q, W * nv, s));
+  SETUP_TRY(dalloc(&ctx->w0, W, s));
+  SETUP_TRY(dalloc(&ctx->dw, W, s));
+  SETUP_TRY(dalloc(&ctx->r, W, s));
+  SETUP_TRY(dalloc(&ctx->y, W, s));
+  SETUP_TRY(dalloc(&ctx->yb, W, s));
+  SETUP_TRY(dalloc(&ctx->st, 1, s));
+  unsigned long long* counters;
+  SETUP_TRY(dalloc(&counters, 2, s)); temps.push_back(counters);
+  SETUP_TRY(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, s));
+  SETUP_TRY(cudaMemsetAsync(ctx->dw, 0, sizeof(double) * W, s));
+  SETUP_TRY(cudaMemsetAsync(ctx->y, 0, sizeof(double) * W, s));
+  SETUP_TRY(cudaMemsetAsync(ctx->yb, 0, sizeof(double) * W, s));
+  const DevView v = ctx->view();
+  const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>((nF + 3) / 4, (int64_t)SM * 16));
+  if (ctx->max_row <= 32)
+    k_alg2<1><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters);
+  else if (ctx->max_row <= 64)
+    k_alg2<2><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters);
+  else
+    k_alg2<4><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters);
+  SETUP_TRY(cudaGetLastError());
+
+  // ---- r0 = -Pi (A P0)|F and E0 = tr(P0^T A P0)
+  double h_sum_cc = 0.0;
+  SETUP_TRY(cudaMemcpyAsync(&h_sum_cc, dsum, sizeof(double), cudaMemcpyDeviceToHost, s));
+  unsigned long long h_cnt[2];
+  SETUP_TRY(cudaMemcpyAsync(h_cnt, counters, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
+  SETUP_TRY(cudaStreamSynchronize(s));
+  ctx->sum_diag_cc = h_sum_cc;
+  ctx->n_svd = (int64_t)h_cnt[0];
+  ctx->n_frozen = (int64_t)h_cnt[1];
+  emin_status st = emin_finish_r0(ctx);
+  tmp_free();
+  if (st != EMIN_OK) return fail(ctx, st, ctx->last_error);
+  SETUP_TRY(cudaStreamSynchronize(s));
+  *out = ctx;
+  return EMIN_OK;
+}

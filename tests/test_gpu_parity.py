@@ -1,0 +1,205 @@
+"""GPU path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): pattern and index structure bit-exact,
+energy within 1e-10 relative, P entries within 1e-8 * max|P|.  The oracle
+always runs the literal Alg. 3 (post-Jacobi projection on); the GPU skips it
+by default (reading A7).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-10
+P_TOL = 1e-8
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2208_02995_b200.build import build
+    build()
+
+
+def _pair(prob, k, device="cuda", project=0, tau=0.0, **kw):
+    from oracle import Oracle
+    from paper_2208_02995_b200 import Emin
+    g = Emin.from_problem(prob, device=device, project_after_jacobi=project, tau=tau, **kw)
+    # the oracle is always the literal Alg. 3 (z = Pi M^-1 r); the GPU
+    # skips that projection unless project=1 (reading A7)
+    o = Oracle(prob, project_z=True, tau=tau)
+    return g, o
+
+
+def _check_layout(g, o, prob):
+    wptr, wcol, pofs = g.layout()
+    owptr, owcol, ofrow = o.layout()
+    assert np.array_equal(wptr, owptr)
+    assert np.array_equal(wcol, owcol)
+    assert np.array_equal(pofs, prob.P_rowptr[ofrow])
+
+
+def _compare(g, o, k, prob):
+    rep0 = g.report()
+    assert abs(rep0["E0"] - o.E0) <= E_TOL * abs(o.E0)
+    kd, dE = g.iterate(k)
+    kdo, dEo = o.iterate(k)
+    assert kd == kdo
+    if kd:
+        assert np.allclose(dE, dEo, rtol=1e-8, atol=1e-12 * abs(o.E0))
+    E, Eo = g.energy(), o.energy()
+    assert abs(E - Eo) <= E_TOL * abs(Eo), (E, Eo)
+    P, Po = g.get_P(), o.get_P()
+    assert np.abs(P - Po).max() <= P_TOL * np.abs(Po).max()
+    rep = g.report()
+    assert rep["k_total"] == o.k_total
+    return P, E
+
+
+SMALL = [("1", None, 20), ("1b", None, 20), ("1d", 33, 40), ("2b", 10, 30), ("2", 12, 30),
+         ("3", 12, 40), ("3", 17, 40), ("4", 3, 30), ("4", 5, 30), ("5", 8, 40)]
+
+
+@pytest.mark.parametrize("name,size,k", SMALL)
+def test_parity_small(name, size, k):
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    g, o = _pair(prob, k)
+    _check_layout(g, o, prob)
+    _compare(g, o, k, prob)
+    rep = g.report()
+    assert rep["n_svd_rows"] == o.n_svd and rep["n_frozen_rows"] == o.n_frozen
+
+
+@pytest.mark.parametrize("name,size", [("1b", None), ("4", 3)])
+def test_parity_with_post_projection(name, size):
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    g, o = _pair(prob, 15, project=1)
+    _compare(g, o, 15, prob)
+
+
+def test_host_inputs_equal_device_inputs_bitwise():
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    prob = make_config("3", size=12)
+    a = Emin.from_problem(prob, device="cuda")
+    b = Emin.from_problem(prob, device="host")
+    a.iterate(20)
+    b.iterate(20)
+    assert np.array_equal(a.get_P(), b.get_P())
+    assert a.energy() == b.energy()
+
+
+def test_composable_and_deterministic():
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    prob = make_config("4", size=4)
+    a = Emin.from_problem(prob)
+    b = Emin.from_problem(prob)
+    a.iterate(7)
+    a.get_P()            # a flush in the middle must not change the trajectory
+    a.iterate(5)
+    b.iterate(12)
+    assert np.array_equal(a.get_P(), b.get_P())
+    c = Emin.from_problem(prob)
+    c.iterate(12)
+    assert np.array_equal(b.get_P(), c.get_P())
+    c.reset()
+    c.iterate(12)
+    assert np.array_equal(b.get_P(), c.get_P())
+
+
+def test_tau_stop():
+    from workloads.problems import make_config
+    prob = make_config("1b", size=16)
+    g, o = _pair(prob, 20, tau=1.0)
+    kd, _ = g.iterate(20)
+    kdo, _ = o.iterate(20)
+    assert kd == kdo == 1
+    assert g.report()["stop_reason"] == 3
+
+
+def test_rank_deficient_rows_take_svd_branch():
+    """nv = 2 with B = [1, 1]: every M_i has rank 1 -> SVD branch, k_i = 1."""
+    from workloads.problems import make_config
+    prob = make_config("3", size=9)
+    prob.B = np.ascontiguousarray(np.repeat(prob.B, 2, axis=1))
+    prob.Bc = np.ascontiguousarray(np.repeat(prob.Bc, 2, axis=1))
+    prob.nv = 2
+    g, o = _pair(prob, 20)
+    assert g.report()["n_svd_rows"] == prob.n_F == o.n_svd
+    _compare(g, o, 20, prob)
+
+
+def test_validation_errors_match_oracle():
+    from oracle import Oracle, OracleError
+    from paper_2208_02995_b200 import Emin, EminError
+    from workloads.problems import make_config
+    def bad_bc(p):
+        p.Bc = p.Bc.copy(); p.Bc[0, 0] = 2.0
+    def bad_pattern(p):
+        c = int(np.flatnonzero(p.is_coarse)[0]); p.P_col = p.P_col.copy(); p.P_col[p.P_rowptr[c]] = 1
+    def bad_diag(p):
+        p.A_val = p.A_val.copy(); rows = np.repeat(np.arange(p.n), np.diff(p.A_rowptr))
+        f = int(np.flatnonzero(p.is_coarse == 0)[0]); p.A_val[(rows == f) & (p.A_col == f)] = -1.0
+    def bad_csr(p):
+        p.A_col = p.A_col.copy(); p.A_col[[0, 1]] = p.A_col[[1, 0]]
+    for mut, code in [(bad_bc, 4), (bad_pattern, 3), (bad_diag, 5), (bad_csr, 2)]:
+        p = make_config("1b", size=8)
+        mut(p)
+        with pytest.raises(EminError) as e:
+            Emin.from_problem(p)
+        assert e.value.code == code
+        with pytest.raises(OracleError) as e2:
+            Oracle(p)
+        assert e2.value.code == code
+
+
+def test_no_free_dof_rows_and_all_coarse_edge():
+    """Rows with |J_i| = 1 (config 1 has 33) are frozen; a problem whose
+    only F row has one column cannot move (dE = 0 -> stop)."""
+    from workloads.problems import make_config
+    prob = make_config("1", size=3)
+    g, o = _pair(prob, 5)
+    _compare(g, o, 5, prob)
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE sizes, in the configuration bench.py times
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,k", [("2b", 30), ("3", 40)])
+def test_parity_full_size_scalar(name, k):
+    from workloads.problems import make_config
+    prob = make_config(name)
+    g, o = _pair(prob, k)
+    _check_layout(g, o, prob)
+    _compare(g, o, k, prob)
+
+
+def test_parity_full_size_elasticity_config4():
+    from workloads.problems import make_config
+    prob = make_config("4")
+    g, o = _pair(prob, 6)
+    _check_layout(g, o, prob)
+    _compare(g, o, 6, prob)
+    # the remaining prescribed steps: properties (monotone, constraint)
+    kd, dE = g.iterate(24)
+    assert kd == 24 and np.all(dE > 0)
+    P = g.get_P()
+    _constraint_sampled(prob, P, 2000)
+
+
+def _constraint_sampled(prob, P, nsample, seed=0):
+    rng = np.random.default_rng(seed)
+    f = prob.fine_rows
+    rows = rng.choice(f, size=min(nsample, f.size), replace=False)
+    worst = 0.0
+    for r in rows:
+        s, e = prob.P_rowptr[r], prob.P_rowptr[r + 1]
+        res = P[s:e] @ prob.Bc[prob.P_col[s:e]] - prob.B[r]
+        worst = max(worst, np.abs(res).max() / max(1.0, np.abs(prob.B[r]).max()))
+    assert worst <= 1e-12, worst
