@@ -89,6 +89,7 @@ typedef struct {
   int64_t n_fine, nnz_W, nnz_AFF;  /* owned F rows, W entries, A_FF entries */
   int32_t kernel_path; /* 0 generic warp-per-row, 1 scalar lane-per-entry, 2 nodal 3x3 */
   int32_t nranks;
+  int64_t launches;    /* kernels this context has enqueued so far (setup included) */
 } emin_report_t;
 
 /* Fill opts with defaults (rank_tol 1e-10, tau 0, project_after_jacobi 0,

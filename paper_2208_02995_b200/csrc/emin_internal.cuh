@@ -69,6 +69,9 @@ struct emin_ctx_s {
   uint8_t* isc_own = nullptr;  // is_coarse of the owned rows
   cudaStream_t cap_stream = nullptr;  // capture stream for the CUDA graphs
   int64_t k_launched = 0;      // upper bound of k_total (host side)
+  int64_t launches = 0;        // kernels enqueued by this context
+  void* fast = nullptr;        // specialised-path plan (kernels_fast.cuh)
+  int32_t* erow = nullptr;     // F-row id of every W entry (streaming stages)
   int breakdown_reported = 0;
   int32_t *wcol = nullptr, *affcol = nullptr, *afccol = nullptr;
   double *affval = nullptr, *afcval = nullptr, *d = nullptr, *Q = nullptr;

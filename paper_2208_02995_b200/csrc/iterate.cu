@@ -124,6 +124,89 @@ k_stage2(DevView v, const double* __restrict__ r, double* __restrict__ y, double
   }
 }
 
+// ------------------------------------------------------------ entry-parallel stages
+// (no post-Jacobi projection): one thread per W entry, row from erow[], UNR
+// independent entries in flight per thread.
+constexpr int STAGE_UNR = 4;
+
+__global__ void __launch_bounds__(256)
+k_stage1_e(DevView v, const int32_t* __restrict__ erow, double* __restrict__ r, const double* __restrict__ yb,
+           double* __restrict__ partials) {
+  __shared__ double sh[32];
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = st->pend;
+  const double ap = st->alpha_pend;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = v.nnzW;
+  double part = 0.0;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += STAGE_UNR * stride) {
+    double rv[STAGE_UNR], dv[STAGE_UNR];
+#pragma unroll
+    for (int u = 0; u < STAGE_UNR; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < n) {
+        rv[u] = r[e];
+        if (pend) rv[u] = rv[u] - ap * yb[e];
+        dv[u] = v.d[erow[e]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < STAGE_UNR; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < n) {
+        if (pend) r[e] = rv[u];
+        const double z = rv[u] / dv[u];
+        part = fma(rv[u], z, part);
+      }
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256)
+k_stage2_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ r, double* __restrict__ y,
+           double* __restrict__ dw) {
+  const DevState* st = v.st;
+  const int stopped = st->stopped;
+  const int pendw = st->pendw;
+  if (stopped && !pendw) return;
+  const double ap = st->alpha_pend;
+  const double beta = st->beta;
+  const bool first = (st->k_total == 0);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = v.nnzW;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += STAGE_UNR * stride) {
+    double yo[STAGE_UNR], rv[STAGE_UNR], dv[STAGE_UNR], dwv[STAGE_UNR];
+#pragma unroll
+    for (int u = 0; u < STAGE_UNR; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < n) {
+        yo[u] = y[e];
+        if (pendw) dwv[u] = dw[e];
+        if (!stopped) { rv[u] = r[e]; dv[u] = v.d[erow[e]]; }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < STAGE_UNR; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < n) {
+        if (pendw) dw[e] = dwv[u] + ap * yo[u];
+        if (!stopped) {
+          const double z = rv[u] / dv[u];
+          y[e] = first ? z : z + beta * yo[u];
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_build_erow(const int64_t* __restrict__ wptr, int64_t nF, int32_t* __restrict__ erow) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t p = wptr[i]; p < wptr[i + 1]; ++p) erow[p] = (int32_t)i;
+}
+
 // ------------------------------------------------------------ scalars
 __device__ double reduce_partials(const double* __restrict__ p, int np, double* sh) {
   double s = 0.0;
@@ -250,6 +333,13 @@ void launch_stage2_g(emin_ctx c, cudaStream_t s) {
     k_stage2<G, false><<<c->grid_rows, 256, 0, s>>>(v, c->r, c->y, c->dw);
 }
 void launch_stage(emin_ctx c, int which, cudaStream_t s) {
+  if (!c->opts.project_after_jacobi) {
+    if (which == 1)
+      k_stage1_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->r, c->yb, c->partials);
+    else
+      k_stage2_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->r, c->y, c->dw);
+    return;
+  }
   switch (c->group) {
 #define CASE_G(GG) case GG: which == 1 ? launch_stage1_g<GG>(c, s) : launch_stage2_g<GG>(c, s); break;
     CASE_G(1) CASE_G(2) CASE_G(4) CASE_G(8) CASE_G(16) CASE_G(32)
@@ -265,8 +355,8 @@ int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, 
                        cudaStream_t s) {
   const DevView v = c->view();
   const int grid = c->grid_spgemm;
-  if (mode == MM_ITER && c->kernel_path == 1) {
-    launch_scalar_spgemm(c, s);
+  if (c->kernel_path == 1) {
+    launch_scalar_masked(c, mode, X, X2, out, s);
     return grid;
   }
   const int mc = c->max_row <= 32 ? 1 : c->max_row <= 64 ? 2 : 4;
@@ -283,24 +373,48 @@ int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, 
   return grid;
 }
 
+// kernel path + launch geometry (end of the index preparation in setup)
+emin_status emin_plan(emin_ctx c) {
+  const int SM = emin_num_sms();
+  c->group = pick_group(c->nF ? (double)c->nnzW / (double)c->nF : 1.0);
+  c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF * c->group + 255) / 256, (int64_t)SM * 8));
+  c->grid_spgemm = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF + 7) / 8, (int64_t)SM * 8));
+  c->kernel_path = select_fast_path(c);
+  if (c->kernel_path == 1) c->grid_spgemm = scalar_spgemm_grid(c);
+  if (!c->opts.project_after_jacobi) {
+    // entry-parallel streaming stages: row id per W entry
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->erow, sizeof(int32_t) * std::max<int64_t>(c->nnzW, 1), c->stream));
+    k_build_erow<<<SM * 8, 256, 0, c->stream>>>(c->wptr, c->nF, c->erow);
+    c->launches += 1;
+    c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * 8));
+  }
+  c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
+  if (c->grid_red > c->n_partials) {
+    cudaFreeAsync(c->partials, c->stream);
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->partials, sizeof(double) * c->grid_red, c->stream));
+    c->n_partials = c->grid_red;
+  }
+  EMIN_CUDA_TRY(c, cudaGetLastError());
+  return EMIN_OK;
+}
+
+// Alg. 2 on a specialised path (false: use the generic warp kernel)
+bool emin_alg2_fast(emin_ctx c, const double* Bc, const double* B, const int64_t* frow, const double* what,
+                    unsigned long long* counters, cudaStream_t s) {
+  if (c->kernel_path != 1) return false;
+  launch_scalar_alg2(c, Bc, B, frow, what, counters, s);
+  return true;
+}
+
 // r0 = -Pi (A P0)|F, E0, fresh CG state (end of setup and emin_reset)
 emin_status emin_finish_r0(emin_ctx c) {
   cudaStream_t s = c->stream;
-  const int SM = emin_num_sms();
-  if (!c->grid_spgemm) {
-    c->group = pick_group(c->nF ? (double)c->nnzW / (double)c->nF : 1.0);
-    c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF * c->group + 255) / 256, (int64_t)SM * 8));
-    c->grid_spgemm = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF + 7) / 8, (int64_t)SM * 8));
-    c->kernel_path = select_fast_path(c);
-    if (c->kernel_path == 1) c->grid_spgemm = scalar_spgemm_grid(c);
-    c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
-    if (c->grid_red > c->n_partials) { c->last_error = "partials buffer too small"; return EMIN_ERR_STATE; }
-  }
   EMIN_CUDA_TRY(c, cudaMemsetAsync(c->dw, 0, sizeof(double) * std::max<int64_t>(c->nnzW, 1), s));
   emin_launch_masked(c, MM_R0, c->w0, nullptr, c->r, s);
   // energy of P0 (dw = 0)
   const int g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, s);
   k_reset_state<<<1, 1024, 0, s>>>(c->st, c->partials, g, c->sum_diag_cc, c->opts.tau, c->opts.stagnation_rel);
+  c->launches += 3;
   EMIN_CUDA_TRY(c, cudaGetLastError());
   c->k_launched = 0;
   c->breakdown_reported = 0;
@@ -309,7 +423,7 @@ emin_status emin_finish_r0(emin_ctx c) {
 
 static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev) {
   auto rec = [&](int t) {
-    if (ev) cudaEventRecordWithFlags(ev[t], s, cudaEventRecordExternal);
+    if (ev) cudaEventRecord(ev[t], s);
   };
   rec(0);
   launch_stage(c, 1, s);
@@ -324,35 +438,32 @@ static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev) {
   rec(5);
 }
 
-static emin_status build_graph(emin_ctx c, int k) {
+// One iteration captured as a CUDA graph (5 kernel nodes, cheap to
+// instantiate per context); emin_iterate(k) launches it k times.
+static emin_status build_graph(emin_ctx c) {
   if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
   if (!c->cap_stream) EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-  const int prof = c->profiling;
-  if (prof) {
-    const size_t need = (size_t)6 * k;
-    while (c->ev.size() < need) {
-      cudaEvent_t e;
-      EMIN_CUDA_TRY(c, cudaEventCreate(&e));
-      c->ev.push_back(e);
-    }
-  }
   cudaStream_t s = c->cap_stream;
   EMIN_CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  cudaMemsetAsync(&c->st->k_call, 0, sizeof(int32_t), s);
-  for (int it = 0; it < k; ++it) enqueue_iteration(c, s, prof ? &c->ev[6 * it] : nullptr);
+  enqueue_iteration(c, s, nullptr);
   cudaGraph_t g;
   EMIN_CUDA_TRY(c, cudaStreamEndCapture(s, &g));
   cudaError_t e = cudaGraphInstantiate(&c->graph, g, 0);
   cudaGraphDestroy(g);
   EMIN_CUDA_TRY(c, e);
-  c->graph_k = k;
-  c->graph_prof = prof;
+  c->graph_k = 1;
   return EMIN_OK;
+}
+
+// process-wide pool of timing events (profiling mode)
+static std::vector<cudaEvent_t>& event_pool() {
+  static std::vector<cudaEvent_t> pool;
+  return pool;
 }
 
 static emin_status ensure_hist(emin_ctx c, int64_t need) {
   if (need <= c->dE_cap) return EMIN_OK;
-  int64_t cap = std::max<int64_t>(need, std::max<int64_t>(64, 2 * c->dE_cap));
+  int64_t cap = std::max<int64_t>(need, std::max<int64_t>(1024, 2 * c->dE_cap));
   double* nh;
   EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&nh, sizeof(double) * cap, c->stream));
   if (c->dE_hist) {
@@ -361,7 +472,7 @@ static emin_status ensure_hist(emin_ctx c, int64_t need) {
   }
   c->dE_hist = nh;
   c->dE_cap = cap;
-  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; c->graph_k = -1; }
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // it captured the old pointer
   return EMIN_OK;
 }
 
@@ -372,16 +483,29 @@ extern "C" emin_status emin_iterate(emin_ctx c, int32_t k, int32_t* k_done, doub
   if (k == 0) return EMIN_OK;
   emin_status st = ensure_hist(c, c->k_launched + k);
   if (st != EMIN_OK) return st;
-  if (!c->graph || c->graph_k != k || c->graph_prof != c->profiling) {
-    st = build_graph(c, k);
-    if (st != EMIN_OK) return st;
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(&c->st->k_call, 0, sizeof(int32_t), c->stream));
+  std::vector<cudaEvent_t>& ev = event_pool();
+  if (c->profiling) {
+    // direct launches with CUDA events between the kernels (on this stream)
+    while (ev.size() < (size_t)6 * k) {
+      cudaEvent_t e;
+      EMIN_CUDA_TRY(c, cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    for (int it = 0; it < k; ++it) enqueue_iteration(c, c->stream, &ev[6 * it]);
+  } else {
+    if (!c->graph) {
+      st = build_graph(c);
+      if (st != EMIN_OK) return st;
+    }
+    for (int it = 0; it < k; ++it) EMIN_CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
   }
-  EMIN_CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
+  c->launches += 5 * (int64_t)k;
   c->k_launched += k;
   if (c->profiling) {
     EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     for (int it = 0; it < k; ++it) {
-      cudaEvent_t* e = &c->ev[6 * it];
+      cudaEvent_t* e = &ev[6 * it];
       float t[5];
       for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&t[j], e[j], e[j + 1]);
       c->prof_ms[0] += t[0];
@@ -423,6 +547,7 @@ extern "C" emin_status emin_energy(emin_ctx c, double* E) {
   double* dev;
   EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&dev, sizeof(double), c->stream));
   k_energy_out<<<1, 1024, 0, c->stream>>>(c->partials, g, c->sum_diag_cc, dev);
+  c->launches += 4;
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(E, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   cudaFreeAsync(dev, c->stream);
   EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -436,8 +561,12 @@ extern "C" emin_status emin_get_P(emin_ctx c, double* P_val) {
   double* out = P_val;
   if (!c->opts.inputs_on_device)
     EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&out, sizeof(double) * std::max<int64_t>(c->nnzP, 1), c->stream));
-  k_get_P<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->w0, c->dw, c->pofs, out);
+  if (c->kernel_path == 1)
+    launch_scalar_get_P(c, out, c->stream);
+  else
+    k_get_P<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->w0, c->dw, c->pofs, out);
   k_get_P_crows<<<SM * 8, 256, 0, c->stream>>>(c->m_owned, c->isc_own, c->cofs, out);
+  c->launches += 4;
   EMIN_CUDA_TRY(c, cudaGetLastError());
   if (!c->opts.inputs_on_device) {
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(P_val, out, sizeof(double) * c->nnzP, cudaMemcpyDeviceToHost, c->stream));
@@ -469,6 +598,7 @@ extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
   rep->nnz_AFF = c->nnzAFF;
   rep->kernel_path = c->kernel_path;
   rep->nranks = c->nranks;
+  rep->launches = c->launches;
   if (h.stopped == 5 && !c->breakdown_reported) {
     c->breakdown_reported = 1;
     return EMIN_ERR_BREAKDOWN;
@@ -506,7 +636,7 @@ void emin_free_all(emin_ctx c) {
   cudaStream_t s = c->stream;
   void* ptrs[] = {c->wptr, c->affptr, c->afcptr, c->pofs, c->cofs, c->isc_own, c->wcol, c->affcol,
                   c->afccol, c->affval, c->afcval, c->d, c->Q, c->w0, c->dw, c->r, c->r0, c->y,
-                  c->yb, c->partials, c->dE_hist, c->st};
+                  c->yb, c->partials, c->dE_hist, c->st, c->erow};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   free_fast_path(c);
@@ -517,7 +647,6 @@ extern "C" void emin_destroy(emin_ctx c) {
   if (!c) return;
   if (c->graph) cudaGraphExecDestroy(c->graph);
   emin_free_all(c);
-  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }

@@ -1,9 +1,593 @@
-// kernels_fast.cuh -- specialised masked-SpGEMM paths (selected at setup).
+// kernels_fast.cuh -- specialised hot-path kernels selected at setup.
+//
+// Scalar path (kernel_path 1): nv = 1 and |J_i| <= 8 (configs 1-3).
+//   Lane-per-W-entry.  The W entries are cut into windows of S = 33 - max|J|
+//   consecutive entries; warp w owns the rows whose first entry lies in
+//   window w, so a warp never holds more than 32 entries and rows never
+//   straddle warps.  Each lane finds its row from a head bitmask
+//   (__reduce_or_sync + popc), so all loads of W-layout vectors are
+//   coalesced and every lane does useful work (S/32 on average).
+//   The masked product uses a per-A_FF-entry record built once at setup
+//   (the pattern is fixed, "the sparsity pattern ... can be
+//   communicated only once"):  {a = A(i,k), ybase = wptr[k], pm}, where
+//   nibble t of pm is the position of J_i[t] in J_k (0xF: absent).  So the
+//   inner loop is one 16-byte broadcast load, a nibble extract and one
+//   gather of y(k, s) -- no search.
 #pragma once
+#include <algorithm>
+#include <cstdlib>
 #include "emin_internal.cuh"
+#include "masked.cuh"
 
-// 0 = generic warp-per-row kernel (masked.cuh)
-static inline int select_fast_path(emin_ctx) { return 0; }
-static inline int scalar_spgemm_grid(emin_ctx c) { return c->grid_spgemm; }
-static inline void launch_scalar_spgemm(emin_ctx, cudaStream_t) {}
-static inline void free_fast_path(emin_ctx) {}
+struct SpEnt {          // 16 bytes, one per A_FF entry
+  double a;
+  int32_t ybase;
+  uint32_t pm;
+};
+
+struct TileHdr;
+struct ScalarPlan {
+  SpEnt* ent = nullptr;
+  int32_t* rowstart = nullptr;   // [nwin + 1]
+  int64_t nwin = 0;
+  int32_t S = 0;
+  TileHdr* hdr = nullptr;        // [ntiles] (staged tile kernel)
+  int64_t ntiles = 0;
+  size_t tile_smem = 0;
+  int use_tiles = 0;
+};
+
+// decode the window: rows [r0, r1), base entry, this lane's row and position
+struct WinLane {
+  int64_t base;   // first W entry of the window
+  int nent;       // entries in the window (<= 32)
+  int rloc;       // lane's row within the window
+  int pos;        // lane's position in its row
+  int rowbeg;     // lane index of its row's first entry
+  int rowlen;
+  bool act;
+};
+
+__device__ __forceinline__ WinLane decode_window(const int64_t* __restrict__ wptr, int64_t r0, int nrows,
+                                                 int lane) {
+  WinLane w;
+  const int64_t myptr = (lane <= nrows) ? wptr[r0 + lane] : 0;
+  w.base = __shfl_sync(0xffffffffu, myptr, 0);
+  const int64_t end = __shfl_sync(0xffffffffu, myptr, nrows);
+  w.nent = (int)(end - w.base);
+  const unsigned bit = (lane < nrows) ? (1u << (unsigned)(myptr - w.base)) : 0u;
+  const unsigned H = __reduce_or_sync(0xffffffffu, bit);
+  const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+  int rl = __popc(H & upto) - 1;
+  if (rl < 0) rl = 0;
+  if (rl >= nrows) rl = nrows - 1;
+  w.rloc = rl;
+  const int64_t rb = __shfl_sync(0xffffffffu, myptr, rl);
+  const int64_t re = __shfl_sync(0xffffffffu, myptr, rl + 1 <= nrows ? rl + 1 : nrows);
+  w.rowbeg = (int)(rb - w.base);
+  w.rowlen = (int)(re - rb);
+  w.pos = lane - w.rowbeg;
+  w.act = lane < w.nent;
+  return w;
+}
+
+// sum of v over the lane's row (segmented inclusive scan, then the row's
+// last lane broadcasts); identical in every lane of the row
+__device__ __forceinline__ double row_sum(double v, const WinLane& L) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, v, o);
+    if (L.pos >= o) v += t;
+  }
+  return __shfl_sync(0xffffffffu, v, L.rowbeg + L.rowlen - 1);
+}
+
+// Masked product on the scalar path, modes as in masked.cuh:
+//   MM_ITER    yb = Pi K y, partial y . yb
+//   MM_R0      r0 = -Pi Pi (A P0)|F (C-identity term included)    (A1)
+//   MM_ENERGY  partial W . (A_FF W + 2 A_FC), W = X + X2          (Eq. trInc)
+template <int MODE>
+__global__ void __launch_bounds__(256)
+k_spgemm_scalar(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict__ rowstart, int64_t nwin,
+                const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+                double* __restrict__ partials) {
+  __shared__ double sh[32];
+  if (MODE == MM_ITER && v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part = 0.0;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int64_t r0 = rowstart[w];
+    const int nrows = (int)(rowstart[w + 1] - r0);
+    if (nrows == 0) continue;                          // warp-uniform
+    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
+    const int64_t i = r0 + L.rloc;
+    const int64_t e = L.base + lane;
+    double acc = 0.0, fc = 0.0;
+    if (L.act) {
+      const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
+      const unsigned sh4 = 4u * (unsigned)L.pos;
+      for (int64_t q = qb; q < qe; ++q) {
+        const SpEnt en = A[q];
+        const unsigned s = (en.pm >> sh4) & 0xFu;
+        if (s != 0xFu) {
+          const int64_t src = (int64_t)en.ybase + s;
+          const double xv = (MODE == MM_ENERGY) ? X[src] + X2[src] : X[src];
+          acc = fma(en.a, xv, acc);
+        }
+      }
+      if (MODE != MM_ITER) {            // A(i, c_j): search the short A_FC row
+        const int32_t j = v.wcol[e];
+        for (int64_t q = v.afcptr[i]; q < v.afcptr[i + 1]; ++q)
+          if (v.afccol[q] == j) { fc = v.afcval[q]; break; }
+      }
+    }
+    if (MODE == MM_ENERGY) {
+      if (L.act) part += (X[e] + X2[e]) * (acc + 2.0 * fc);
+      continue;
+    }
+    // Pi_B, nv = 1: g - q (q . g) over the row
+    const double qv = L.act ? v.Q[e] : 0.0;
+    double g = (MODE == MM_R0) ? acc + fc : acc;
+#pragma unroll
+    for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
+      const double dot = row_sum(qv * g, L);
+      g = g - qv * dot;
+    }
+    if (L.act) {
+      if (MODE == MM_ITER) {
+        out[e] = g;
+        part = fma(X[e], g, part);
+      } else {
+        out[e] = -g;
+      }
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// Alg. 2 for nv = 1 on the window plan (the CGS2 QR of k_alg2 reduces to
+// q = M / |M|, delta = q (r / |M|); |M| = 0 is the rank-0 SVD branch)
+__global__ void __launch_bounds__(256)
+k_alg2_nv1(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const double* __restrict__ Bc,
+           const double* __restrict__ B, const int64_t* __restrict__ frow, const double* __restrict__ what,
+           double* __restrict__ Qout, double* __restrict__ w0, unsigned long long* counters) {
+  __shared__ unsigned long long cnt[2];
+  if (threadIdx.x < 2) cnt[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned n_svd = 0, n_frozen = 0;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int64_t r0 = rowstart[w];
+    const int nrows = (int)(rowstart[w + 1] - r0);
+    if (nrows == 0) continue;
+    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
+    const int64_t e = L.base + lane;
+    const int64_t i = r0 + L.rloc;
+    const double m = L.act ? Bc[v.wcol[e]] : 0.0;
+    const double wh = L.act ? what[e] : 0.0;
+    const double smm = row_sum(m * m, L);
+    const double smw = row_sum(m * wh, L);
+    if (L.act) {
+      const double rv = B[frow[i]] - smw;
+      const double R = sqrt(smm);
+      double q = 0.0, delta = 0.0;
+      int k = 0;
+      if (R > 0.0) {
+        q = m / R;
+        delta = q * (rv / R);
+        k = 1;
+      }
+      Qout[e] = q;
+      w0[e] = wh + delta;
+      if (L.pos == 0) {
+        n_svd += (k == 0);
+        n_frozen += (L.rowlen == k);
+      }
+    }
+  }
+  atomicAdd(&cnt[0], (unsigned long long)n_svd);
+  atomicAdd(&cnt[1], (unsigned long long)n_frozen);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (cnt[0]) atomicAdd(counters + 0, cnt[0]);
+    if (cnt[1]) atomicAdd(counters + 1, cnt[1]);
+  }
+}
+
+// P out on the window plan
+__global__ void __launch_bounds__(256)
+k_get_P_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const double* __restrict__ w0,
+            const double* __restrict__ dw, const int64_t* __restrict__ pofs, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int64_t r0 = rowstart[w];
+    const int nrows = (int)(rowstart[w + 1] - r0);
+    if (nrows == 0) continue;
+    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
+    if (L.act) {
+      const int64_t e = L.base + lane;
+      out[pofs[r0 + L.rloc] + L.pos] = w0[e] + dw[e];
+    }
+  }
+}
+
+// stage I on the window plan: r -= alpha_pend yb ; partial r . (r / d)
+__global__ void __launch_bounds__(256)
+k_stage1_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, double* __restrict__ r,
+             const double* __restrict__ yb, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = st->pend;
+  const double ap = st->alpha_pend;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part = 0.0;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int64_t r0 = rowstart[w];
+    const int nrows = (int)(rowstart[w + 1] - r0);
+    if (nrows == 0) continue;
+    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
+    if (L.act) {
+      const int64_t e = L.base + lane;
+      const double di = v.d[r0 + L.rloc];
+      double rv = r[e];
+      if (pend) { rv = rv - ap * yb[e]; r[e] = rv; }
+      const double z = rv / di;
+      part = fma(rv, z, part);
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// stage II on the window plan: dw += alpha_pend y_old ; y = z + beta y_old
+__global__ void __launch_bounds__(256)
+k_stage2_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const double* __restrict__ r,
+             double* __restrict__ y, double* __restrict__ dw) {
+  const DevState* st = v.st;
+  const int stopped = st->stopped;
+  const int pendw = st->pendw;
+  if (stopped && !pendw) return;
+  const double ap = st->alpha_pend;
+  const double beta = st->beta;
+  const bool first = (st->k_total == 0);
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int64_t r0 = rowstart[w];
+    const int nrows = (int)(rowstart[w + 1] - r0);
+    if (nrows == 0) continue;
+    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
+    if (L.act) {
+      const int64_t e = L.base + lane;
+      const double yo = y[e];
+      if (pendw) dw[e] = dw[e] + ap * yo;
+      if (!stopped) {
+        const double z = r[e] / v.d[r0 + L.rloc];
+        y[e] = first ? z : z + beta * yo;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tiled variant: one CTA per tile of consecutive rows whose first entry lies
+// in [t S_T, (t+1) S_T) (S_T = TILE_E - max|J| + 1, so a tile holds at most
+// TILE_E entries).  Phase A stages the tile's contiguous slices -- the A_FF
+// records [abase, aend), the row pointers -- into shared memory with
+// coalesced 16-byte loads, and loads each thread's own Q and y entries into
+// registers, all independent of one another (one round trip after the tile
+// header).  Phase B does the masked product from shared memory; only the
+// y(k, s) gathers go to L2/HBM.  The row projection sums q.g per row in a
+// fixed order through shared memory (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int TILE_T = 256;                 // threads per CTA
+constexpr int TILE_U = 2;                   // W entries per thread
+constexpr int TILE_E = TILE_T * TILE_U;     // W entries per tile (max)
+
+struct TileHdr {
+  int32_t r0, r1;        // rows [r0, r1)
+  int64_t base, end;     // W entries [base, end)
+  int64_t abase, aend;   // A_FF records [abase, aend)
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(TILE_T)
+k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict__ hdr,
+              const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+              double* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double sh[32];
+  if (MODE == MM_ITER && v.st->stopped) return;
+  const int tid = threadIdx.x;
+  const TileHdr H = hdr[blockIdx.x];
+  const int nrows = H.r1 - H.r0;
+  const int nent = (int)(H.end - H.base);
+  const int nrec = (int)(H.aend - H.abase);
+  SpEnt* s_rec = reinterpret_cast<SpEnt*>(smem_raw);                    // [nrec]
+  int32_t* s_wptr = reinterpret_cast<int32_t*>(s_rec + nrec);          // [nrows+1]
+  int32_t* s_aptr = s_wptr + (TILE_E + 1);                              // [nrows+1]
+  uint16_t* s_erow = reinterpret_cast<uint16_t*>(s_aptr + (TILE_E + 1));// [nent]
+  double* s_qa = reinterpret_cast<double*>(s_erow + TILE_E + 8 - (TILE_E % 8)); // [nent]
+  double* s_dot = s_qa + TILE_E;                                        // [nrows]
+  // ---- phase A: staged loads
+  for (int k = tid; k < nrec; k += TILE_T) s_rec[k] = A[H.abase + k];
+  for (int r = tid; r <= nrows; r += TILE_T) {
+    s_wptr[r] = (int32_t)(v.wptr[H.r0 + r] - H.base);
+    s_aptr[r] = (int32_t)(v.affptr[H.r0 + r] - H.abase);
+  }
+  double qv[TILE_U], xo[TILE_U];
+#pragma unroll
+  for (int u = 0; u < TILE_U; ++u) {
+    const int e = tid + u * TILE_T;
+    qv[u] = 0.0;
+    xo[u] = 0.0;
+    if (e < nent) {
+      if (MODE != MM_ENERGY) qv[u] = v.Q[H.base + e];
+      if (MODE == MM_ITER) xo[u] = X[H.base + e];
+      if (MODE == MM_ENERGY) xo[u] = X[H.base + e] + X2[H.base + e];
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < nrows; r += TILE_T)
+    for (int p = s_wptr[r]; p < s_wptr[r + 1]; ++p) s_erow[p] = (uint16_t)r;
+  __syncthreads();
+  // ---- phase B: masked product from shared memory
+  double g[TILE_U];
+  int rl[TILE_U];
+#pragma unroll
+  for (int u = 0; u < TILE_U; ++u) {
+    const int e = tid + u * TILE_T;
+    g[u] = 0.0;
+    rl[u] = 0;
+    if (e < nent) {
+      const int r = s_erow[e];
+      rl[u] = r;
+      const unsigned sh4 = 4u * (unsigned)(e - s_wptr[r]);
+      double acc = 0.0;
+      const int q1 = s_aptr[r + 1];
+#pragma unroll 4
+      for (int q = s_aptr[r]; q < q1; ++q) {
+        const SpEnt en = s_rec[q];
+        const unsigned s = (en.pm >> sh4) & 0xFu;
+        if (s != 0xFu) {
+          const int64_t src = (int64_t)en.ybase + s;
+          const double xv = (MODE == MM_ENERGY) ? X[src] + X2[src] : X[src];
+          acc = fma(en.a, xv, acc);
+        }
+      }
+      double fc = 0.0;
+      if (MODE != MM_ITER) {
+        const int64_t i = H.r0 + r;
+        const int32_t j = v.wcol[H.base + e];
+        for (int64_t q = v.afcptr[i]; q < v.afcptr[i + 1]; ++q)
+          if (v.afccol[q] == j) { fc = v.afcval[q]; break; }
+      }
+      if (MODE == MM_ENERGY) g[u] = acc + 2.0 * fc;
+      else if (MODE == MM_R0) g[u] = acc + fc;
+      else g[u] = acc;
+    }
+  }
+  double part = 0.0;
+  if (MODE == MM_ENERGY) {
+#pragma unroll
+    for (int u = 0; u < TILE_U; ++u)
+      if (tid + u * TILE_T < nent) part = fma(xo[u], g[u], part);
+  } else {
+    // ---- Pi_B (nv = 1), twice for r0 (see masked.cuh)
+#pragma unroll
+    for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < TILE_U; ++u) {
+        const int e = tid + u * TILE_T;
+        if (e < nent) s_qa[e] = qv[u] * g[u];
+      }
+      __syncthreads();
+      for (int r = tid; r < nrows; r += TILE_T) {
+        double s = 0.0;
+        for (int p = s_wptr[r]; p < s_wptr[r + 1]; ++p) s += s_qa[p];
+        s_dot[r] = s;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < TILE_U; ++u)
+        if (tid + u * TILE_T < nent) g[u] = g[u] - qv[u] * s_dot[rl[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < TILE_U; ++u) {
+      const int e = tid + u * TILE_T;
+      if (e < nent) {
+        if (MODE == MM_ITER) {
+          out[H.base + e] = g[u];
+          part = fma(xo[u], g[u], part);
+        } else {
+          out[H.base + e] = -g[u];
+        }
+      }
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+__global__ void k_tile_headers(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
+                               const int32_t* __restrict__ trow, int64_t ntiles, TileHdr* __restrict__ hdr,
+                               int32_t* __restrict__ maxrec) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    TileHdr h;
+    h.r0 = trow[t];
+    h.r1 = trow[t + 1];
+    h.base = wptr[h.r0];
+    h.end = wptr[h.r1];
+    h.abase = affptr[h.r0];
+    h.aend = affptr[h.r1];
+    hdr[t] = h;
+    atomicMax(maxrec, (int32_t)(h.aend - h.abase));
+  }
+}
+
+static inline size_t tile_smem_bytes(int maxrec) {
+  return (size_t)maxrec * sizeof(SpEnt) + 2 * sizeof(int32_t) * (TILE_E + 1) +
+         sizeof(uint16_t) * (TILE_E + 8) + sizeof(double) * (2 * TILE_E) + 16;
+}
+
+// ---- setup of the scalar plan
+__global__ void k_plan_rowstart(const int64_t* __restrict__ wptr, int64_t nF, int32_t S, int64_t nwin,
+                                int32_t* __restrict__ rowstart) {
+  // rowstart[w] = first row i with wptr[i] >= w S (lower bound), w in [0, nwin]
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nF; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t hi = (i < nF) ? wptr[i] : INT64_MAX / 2;
+    const int64_t lo = (i > 0) ? wptr[i - 1] : -1;
+    // windows w with lo < w S <= hi
+    int64_t w0 = lo < 0 ? 0 : lo / S + 1;
+    int64_t w1 = hi / S;
+    if (w1 > nwin) w1 = nwin;
+    for (int64_t w = w0; w <= w1; ++w) rowstart[w] = (int32_t)i;
+  }
+}
+
+// one group of 8 lanes per F row, lane per A_FF entry (setup only)
+__global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
+  const int lg = threadIdx.x & 7;
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  for (int64_t i = gid; i < v.nF; i += ng) {
+    const int64_t b = v.wptr[i];
+    const int nj = (int)(v.wptr[i + 1] - b);
+    for (int64_t q = v.affptr[i] + lg; q < v.affptr[i + 1]; q += 8) {
+      const int32_t k = v.affcol[q];
+      const int64_t kb = v.wptr[k];
+      const int nk = (int)(v.wptr[k + 1] - kb);
+      uint32_t pm = 0xFFFFFFFFu;
+      for (int t = 0; t < nj; ++t) {
+        const int32_t j = v.wcol[b + t];
+        for (int s = 0; s < nk; ++s)
+          if (v.wcol[kb + s] == j) { pm = (pm & ~(0xFu << (4 * t))) | ((uint32_t)s << (4 * t)); break; }
+      }
+      SpEnt e;
+      e.a = v.affval[q];
+      e.ybase = (int32_t)kb;
+      e.pm = pm;
+      ent[q] = e;
+    }
+  }
+}
+
+// ---- host side ------------------------------------------------------------
+struct FastPaths {
+  ScalarPlan sc;
+};
+static FastPaths* fast_of(emin_ctx c) { return reinterpret_cast<FastPaths*>(c->fast); }
+
+static inline int select_fast_path(emin_ctx c) {
+  if (c->nv != 1 || c->max_row > 8 || c->nnzWh >= INT32_MAX || c->nF >= INT32_MAX || c->nF == 0) return 0;
+  if (getenv("EMIN_FORCE_GENERIC")) return 0;
+  FastPaths* f = new FastPaths();
+  c->fast = f;
+  ScalarPlan& p = f->sc;
+  p.S = std::min(31, 33 - c->max_row);   // <= 31 rows per window (lane nrows loads the end)
+  p.nwin = (c->nnzW + p.S - 1) / p.S;
+  cudaStream_t s = c->stream;
+  if (cudaMallocAsync((void**)&p.rowstart, sizeof(int32_t) * (p.nwin + 1), s) != cudaSuccess) return 0;
+  if (cudaMallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
+  const int SM = emin_num_sms();
+  k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
+  k_plan_entries<<<SM * 8, 256, 0, s>>>(c->view(), p.ent);
+  c->launches += 2;
+  // tile plan for the staged kernel
+  const int ST = TILE_E - c->max_row + 1;
+  p.ntiles = (c->nnzW + ST - 1) / ST;
+  int32_t* trow = nullptr;
+  int32_t* dmax = nullptr;
+  if (cudaMallocAsync((void**)&trow, sizeof(int32_t) * (p.ntiles + 1), s) != cudaSuccess ||
+      cudaMallocAsync((void**)&p.hdr, sizeof(TileHdr) * std::max<int64_t>(p.ntiles, 1), s) != cudaSuccess ||
+      cudaMallocAsync((void**)&dmax, sizeof(int32_t), s) != cudaSuccess)
+    return 1;
+  cudaMemsetAsync(dmax, 0, sizeof(int32_t), s);
+  k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, ST, p.ntiles, trow);
+  k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
+  c->launches += 2;
+  int32_t hmax = 0;
+  cudaMemcpyAsync(&hmax, dmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(trow, s);
+  cudaFreeAsync(dmax, s);
+  cudaStreamSynchronize(s);
+  p.tile_smem = tile_smem_bytes(hmax);
+  if (p.tile_smem <= 160 * 1024 && !getenv("EMIN_NO_TILE")) {
+    p.use_tiles = 1;
+    cudaFuncSetAttribute(k_spgemm_tile<MM_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
+    cudaFuncSetAttribute(k_spgemm_tile<MM_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
+    cudaFuncSetAttribute(k_spgemm_tile<MM_ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
+  }
+  return 1;
+}
+
+static inline int scalar_grid(emin_ctx c) {
+  const int SM = emin_num_sms();
+  const int64_t nwin = fast_of(c)->sc.nwin;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * 8));
+}
+static inline int scalar_spgemm_grid(emin_ctx c) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
+}
+
+static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
+                                        cudaStream_t s) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  const DevView v = c->view();
+  if (p.use_tiles) {
+    const int g = (int)std::max<int64_t>(1, p.ntiles);
+    if (mode == MM_ITER)
+      k_spgemm_tile<MM_ITER><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
+    else if (mode == MM_R0)
+      k_spgemm_tile<MM_R0><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
+    else
+      k_spgemm_tile<MM_ENERGY><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
+    return;
+  }
+  if (mode == MM_ITER)
+    k_spgemm_scalar<MM_ITER><<<c->grid_spgemm, 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
+  else if (mode == MM_R0)
+    k_spgemm_scalar<MM_R0><<<c->grid_spgemm, 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
+  else
+    k_spgemm_scalar<MM_ENERGY><<<c->grid_spgemm, 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
+}
+static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
+                                      const double* what, unsigned long long* counters, cudaStream_t s) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  k_alg2_nv1<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, Bc, B, frow, what, c->Q, c->w0,
+                                            counters);
+}
+static inline void launch_scalar_get_P(emin_ctx c, double* out, cudaStream_t s) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  k_get_P_win<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->w0, c->dw, c->pofs, out);
+}
+static inline void launch_scalar_stage(emin_ctx c, int which, cudaStream_t s) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  if (which == 1)
+    k_stage1_win<<<c->grid_rows, 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->r, c->yb, c->partials);
+  else
+    k_stage2_win<<<c->grid_rows, 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->r, c->y, c->dw);
+}
+
+static inline void free_fast_path(emin_ctx c) {
+  FastPaths* f = fast_of(c);
+  if (!f) return;
+  if (f->sc.rowstart) cudaFreeAsync(f->sc.rowstart, c->stream);
+  if (f->sc.ent) cudaFreeAsync(f->sc.ent, c->stream);
+  if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
+  delete f;
+  c->fast = nullptr;
+}

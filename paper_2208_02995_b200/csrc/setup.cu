@@ -122,33 +122,45 @@ struct FillArgs {
 
 // F rows: copy the pattern into the W layout, split A into A_FF (local F
 // ids) and A_FC (coarse ids).  One warp per owned row (coalesced copies).
+// Groups of FILL_G lanes per row; loops have warp-uniform trip counts because
+// of the warp-wide ballots.
+constexpr int FILL_G = 8;
 __global__ void k_fill(FillArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t rl = gw; rl < a.m; rl += nw) {
-    const int64_t r = a.row_begin + rl;
-    if (a.isc[r]) continue;
-    const int64_t fl = (r - a.cidx[r]) - a.fbegin;
-    if (lane == 0) { a.frow[fl] = rl; a.pofs[fl] = a.Prp[rl] - a.Prp[0]; }
-    const int64_t pb = a.Prp[rl] - a.Prp[0];
-    const int64_t wb = a.wptr[fl];
-    const int len = (int)(a.wptr[fl + 1] - wb);
-    for (int t = lane; t < len; t += 32) {
-      a.wcol[wb + t] = a.Pcol[pb + t];
-      a.what[wb + t] = a.Pval ? a.Pval[pb + t] : 0.0;
+  const int lg = lane & (FILL_G - 1);
+  const int gshift = lane & ~(FILL_G - 1);
+  const unsigned gmask = ((1u << FILL_G) - 1u) << gshift;
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / FILL_G;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / FILL_G;
+  for (int64_t rl = gid; __any_sync(0xffffffffu, rl < a.m); rl += ng) {
+    bool act = rl < a.m;
+    const int64_t r = a.row_begin + (act ? rl : 0);
+    if (act && a.isc[r]) act = false;
+    const int64_t fl = act ? (r - a.cidx[r]) - a.fbegin : 0;
+    int64_t qb = 0, qe = 0, off_ff = 0, off_fc = 0;
+    if (act) {
+      if (lg == 0) { a.frow[fl] = rl; a.pofs[fl] = a.Prp[rl] - a.Prp[0]; }
+      const int64_t pb = a.Prp[rl] - a.Prp[0];
+      const int64_t wb = a.wptr[fl];
+      const int len = (int)(a.wptr[fl + 1] - wb);
+      for (int t = lg; t < len; t += FILL_G) {
+        a.wcol[wb + t] = a.Pcol[pb + t];
+        a.what[wb + t] = a.Pval ? a.Pval[pb + t] : 0.0;
+      }
+      qb = a.Arp[rl] - a.Arp[0];
+      qe = a.Arp[rl + 1] - a.Arp[0];
+      off_ff = a.affptr[fl];
+      off_fc = a.afcptr[fl];
     }
-    const int64_t qb = a.Arp[rl] - a.Arp[0], qe = a.Arp[rl + 1] - a.Arp[0];
-    int64_t off_ff = a.affptr[fl], off_fc = a.afcptr[fl];
-    for (int64_t q0 = qb; q0 < qe; q0 += 32) {
-      const int64_t q = q0 + lane;
-      bool valid = q < qe;
-      int32_t c = valid ? a.Acol[q] : 0;
-      double v = valid ? a.Aval[q] : 0.0;
+    for (int64_t q0 = qb; __any_sync(0xffffffffu, q0 < qe); q0 += FILL_G) {
+      const int64_t q = q0 + lg;
+      const bool valid = q < qe;
+      const int32_t c = valid ? a.Acol[q] : 0;
+      const double v = valid ? a.Aval[q] : 0.0;
       const bool coarse = valid && a.isc[c];
       const bool fine = valid && !coarse;
-      const unsigned mf = __ballot_sync(0xffffffffu, fine);
-      const unsigned mc = __ballot_sync(0xffffffffu, coarse);
+      const unsigned mf = __ballot_sync(0xffffffffu, fine) & gmask;
+      const unsigned mc = __ballot_sync(0xffffffffu, coarse) & gmask;
       const unsigned lt = (1u << lane) - 1u;
       if (fine) {
         const int64_t gF = (int64_t)c - a.cidx[c];
@@ -417,6 +429,16 @@ __global__ void k_reduce_partials(const double* __restrict__ p, int np, double* 
   if (threadIdx.x == 0) *out = t + add;
 }
 
+// first pass of a deterministic two-pass sum: one partial per block
+__global__ void k_block_sums(const double* __restrict__ x, int64_t n, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    s += x[k];
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
 template <typename T>
 cudaError_t dalloc(T** p, int64_t n, cudaStream_t s) {
   return cudaMallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s);
@@ -428,6 +450,9 @@ cudaError_t dalloc(T** p, int64_t n, cudaStream_t s) {
 int emin_launch_masked(emin_ctx ctx, int mode, const double* X, const double* X2, double* out,
                        cudaStream_t s);
 emin_status emin_finish_r0(emin_ctx ctx);
+emin_status emin_plan(emin_ctx ctx);
+bool emin_alg2_fast(emin_ctx c, const double* Bc, const double* B, const int64_t* frow, const double* what,
+                    unsigned long long* counters, cudaStream_t s);
 void emin_free_all(emin_ctx ctx);
 
 extern "C" void emin_default_opts(emin_opts* o, int64_t n_global) {
@@ -479,6 +504,15 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   if (n_global > INT32_MAX || nc_global > INT32_MAX)
     return fail(ctx, EMIN_ERR_ARG, "n_global exceeds the int32 column range");
 
+  {
+    // keep freed blocks in the stream-ordered pool (repeated setups reuse them)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   ctx = new emin_ctx_s();
   ctx->opts = *opts;
   ctx->stream = (cudaStream_t)opts->stream;
@@ -653,7 +687,14 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   ctx->n_partials = SM * 32;
   double* dsum;
   SETUP_TRY(dalloc(&dsum, 4, s)); temps.push_back(dsum);
-  k_reduce_partials<<<1, 1024, 0, s>>>(dcc, (int)std::min<int64_t>(m, INT32_MAX), dsum, 0.0);
+  k_block_sums<<<SM * 4, 256, 0, s>>>(dcc, m, ctx->partials);
+  k_reduce_partials<<<1, 1024, 0, s>>>(ctx->partials, SM * 4, dsum, 0.0);
+
+  // ---- kernel path (scalar window plan / generic) and launch geometry
+  {
+    emin_status pst = emin_plan(ctx);
+    if (pst != EMIN_OK) { tmp_free(); return fail(ctx, pst, ctx->last_error); }
+  }
 
   // ---- Alg. 2
   SETUP_TRY(dalloc(&ctx->Q, W * nv, s));
@@ -671,7 +712,9 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   SETUP_TRY(cudaMemsetAsync(ctx->yb, 0, sizeof(double) * W, s));
   const DevView v = ctx->view();
   const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>((nF + 3) / 4, (int64_t)SM * 16));
-  if (ctx->max_row <= 32)
+  if (emin_alg2_fast(ctx, dBc, dB, frow, what, counters, s))
+    ;
+  else if (ctx->max_row <= 32)
     k_alg2<1><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters);
   else if (ctx->max_row <= 64)
     k_alg2<2><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters);
@@ -688,6 +731,8 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   ctx->sum_diag_cc = h_sum_cc;
   ctx->n_svd = (int64_t)h_cnt[0];
   ctx->n_frozen = (int64_t)h_cnt[1];
+  // kernels enqueued above: coarse flags, 4 scans x 3, rows, check_B, fill, 2 reduce, alg2
+  ctx->launches += 1 + 3 + 2 + (nF > 0 ? 9 : 0) + 1 + 2 + 1;
   emin_status st = emin_finish_r0(ctx);
   tmp_free();
   if (st != EMIN_OK) return fail(ctx, st, ctx->last_error);

@@ -45,7 +45,8 @@ class emin_report_t(C.Structure):
     _fields_ = [("E0", C.c_double), ("dE1", C.c_double), ("k_total", C.c_int64),
                 ("stop_reason", C.c_int32), ("n_svd_rows", C.c_int64),
                 ("n_frozen_rows", C.c_int64), ("n_fine", C.c_int64), ("nnz_W", C.c_int64),
-                ("nnz_AFF", C.c_int64), ("kernel_path", C.c_int32), ("nranks", C.c_int32)]
+                ("nnz_AFF", C.c_int64), ("kernel_path", C.c_int32), ("nranks", C.c_int32),
+                ("launches", C.c_int64)]
 
 
 EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "emin_get_P",
