@@ -216,22 +216,37 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2208_02995_b200 import build as _build
-    _build()
+    if rank == 0:
+        _build()
+    if world > 1:
+        dist.barrier()
     from paper_2208_02995_b200 import emin as E
 
     stream = torch.cuda.current_stream()
     keys = ["A_rowptr", "A_col", "A_val", "is_coarse", "P_rowptr", "P_col", "P_val", "B", "Bc"]
     host = {k: getattr(prob, k) for k in keys}
     dev = {k: (None if v is None else torch.from_numpy(np.ascontiguousarray(v)).cuda()) for k, v in host.items()}
-    nnzP = int(prob.P_rowptr[-1])
+    # row partition (contiguous z-slabs balanced by nnz(W)); NCCL communicator
+    comm = None
+    rb, re_ = 0, prob.n
+    if world > 1:
+        from paper_2208_02995_b200.partition import partition_rows
+        dims = prob.meta["dims"]
+        plane = dims[0] * dims[1] * (3 if prob.block_size == 3 else 1)
+        rb, re_ = partition_rows(prob.P_rowptr, prob.is_coarse, world, plane=plane)[rank]
+        comm = E.nccl_comm_from_torch()
+    nnzP = int(prob.P_rowptr[re_] - prob.P_rowptr[rb])
     out_dev = torch.empty(nnzP, dtype=torch.float64, device="cuda")
     k_it = prob.iters
+    nnzW_global = prob.nnz_W
 
     def setup(arrs):
-        return E.emin_setup(prob.n, prob.nc, arrs["A_rowptr"], arrs["A_col"], arrs["A_val"],
-                            arrs["is_coarse"], arrs["P_rowptr"], arrs["P_col"], arrs["P_val"],
-                            prob.nv, arrs["B"], arrs["Bc"], block_size=prob.block_size,
-                            stagnation_rel=0.0, stream=stream.cuda_stream)
+        nv = prob.nv
+        return E.emin_setup(prob.n, prob.nc, arrs["A_rowptr"][rb:re_ + 1], arrs["A_col"], arrs["A_val"],
+                            arrs["is_coarse"], arrs["P_rowptr"][rb:re_ + 1], arrs["P_col"], arrs["P_val"],
+                            nv, arrs["B"][rb:re_], arrs["Bc"], block_size=prob.block_size,
+                            stagnation_rel=0.0, stream=stream.cuda_stream, nccl_comm=comm,
+                            row_begin=rb, row_end=re_)
 
     stats = {"launches": 0, "spgemm_ms": 0.0, "spgemm_n": 0, "stage_ms": [0.0, 0.0], "scalar_ms": 0.0,
              "k_done": 0, "E": None, "report": None}
@@ -290,7 +305,7 @@ def main():
     nnzW = stats["report"]["nnz_W"]
     nnzAFF = stats["report"]["nnz_AFF"]
     nF = stats["report"]["n_fine"]
-    updates = nnzW * k_it * args.steps
+    updates = nnzW_global * k_it * args.steps
     value = updates / (ms / 1e3)
 
     # ---- iteration-only rate (setup excluded, SURVEY §8d definition)
@@ -353,7 +368,7 @@ def main():
             t = torch.tensor([e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": nnzW * k_it * n_e2e / (e_ms / 1e3), "unit": UNIT,
+        e2e = {"value": nnzW_global * k_it * n_e2e / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_ms / n_e2e, "steps": n_e2e}
 
@@ -371,14 +386,14 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "iters_per_step": k_it, "nnz_W": nnzW,
+        "config": {"workload": WORKLOADS[args.config], "iters_per_step": k_it, "nnz_W": nnzW_global,
                    "nnz_A_FF": nnzAFF, "n_F": nF, "nv": prob.nv,
                    "step": "emin_setup(device inputs) + emin_iterate(k) + emin_energy + emin_get_P + emin_destroy",
                    "l2": "inputs larger than L2 (per-iteration working set %.2f GB > 126 MB)" % (it_bytes / 1e9),
                    "parallelism": f"rows{world}" if world > 1 else "single GPU",
                    "kernel_path": E.KERNEL_PATHS.get(stats["report"]["kernel_path"])},
         "roofline": roofline,
-        "iter_only": {"value": nnzW * k_it / (it_ms_med / 1e3), "unit": UNIT,
+        "iter_only": {"value": nnzW_global * k_it / (it_ms_med / 1e3), "unit": UNIT,
                       "ms_per_iter": it_ms_med / k_it,
                       "GBps_vs_B_iter": it_bytes / (it_ms_med / k_it / 1e3) / 1e9,
                       "frac_of_peak": it_bytes / (it_ms_med / k_it / 1e3) / 1e9 / peak},

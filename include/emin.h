@@ -157,6 +157,19 @@ const char* emin_last_error(emin_ctx ctx);
  * row in the caller's P CSR (relative to P_rowptr[0]).  Synchronous. */
 emin_status emin_get_layout(emin_ctx ctx, int64_t* wptr, int32_t* wcol, int64_t* pofs);
 
+/* Multi-GPU helpers (one process per GPU, NCCL over NVLink/NVSwitch).
+ * emin_nccl_unique_id fills id[128] on one rank; the caller broadcasts it
+ * (e.g. with torch.distributed) and every rank calls emin_nccl_comm_init;
+ * the resulting ncclComm_t goes into emin_opts.nccl_comm.  Row ranges must
+ * be contiguous, ascending with the rank and cover [0, n_global).  Halo
+ * rows (F rows of other ranks that the owned A_FF rows reference) are
+ * found and their pattern exchanged once in emin_setup; per
+ * iteration only y on those rows and two scalars are exchanged.
+ * EMIN_ERR_NCCL if the library was built without NCCL. */
+emin_status emin_nccl_unique_id(uint8_t* id128);
+emin_status emin_nccl_comm_init(void** comm, int32_t nranks, const uint8_t* id128, int32_t rank);
+emin_status emin_nccl_comm_destroy(void* comm);
+
 /* Device time of the most recent emin_iterate's kernels, per kernel class,
  * accumulated with CUDA events on the launching stream when profiling is
  * enabled (emin_set_profiling(ctx, 1)); ms[0] stage I, ms[1] stage II,

@@ -27,7 +27,11 @@ struct DevState {
   int32_t pend;       // r -= alpha_pend yb pending (applied by stage I)
   int32_t pendw;      // dw += alpha_pend y pending (applied by stage II)
   int32_t k_call;     // accepted steps in the current emin_iterate call
+  double red[4];      // multi-GPU: local sums reduced in place by ncclAllReduce
+                      // [0] gamma, [1] y.yb, [2] energy
 };
+
+struct DistPlan;
 
 // Error flag bits raised by the validation kernels.
 enum : int32_t {
@@ -71,7 +75,10 @@ struct emin_ctx_s {
   int64_t k_launched = 0;      // upper bound of k_total (host side)
   int64_t launches = 0;        // kernels enqueued by this context
   void* fast = nullptr;        // specialised-path plan (kernels_fast.cuh)
+  void* nodal = nullptr;       // nodal 3x3 path plan (kernels_nodal.cuh)
   int32_t* erow = nullptr;     // F-row id of every W entry (streaming stages)
+  double* dinv = nullptr;      // 1 / A(i,i) per owned F row
+  DistPlan* dist = nullptr;    // multi-GPU halo plan (dist.cu), null on one GPU
   int breakdown_reported = 0;
   int32_t *wcol = nullptr, *affcol = nullptr, *afccol = nullptr;
   double *affval = nullptr, *afcval = nullptr, *d = nullptr, *Q = nullptr;

@@ -19,6 +19,9 @@
 #include "emin_internal.cuh"
 #include "masked.cuh"
 #include "kernels_fast.cuh"
+#include "dist.cuh"
+#include "kernels_nodal.cuh"
+#include <utility>
 
 namespace {
 
@@ -129,9 +132,18 @@ k_stage2(DevView v, const double* __restrict__ r, double* __restrict__ y, double
 // independent entries in flight per thread.
 constexpr int STAGE_UNR = 4;
 
-__global__ void __launch_bounds__(256)
-k_stage1_e(DevView v, const int32_t* __restrict__ erow, double* __restrict__ r, const double* __restrict__ yb,
-           double* __restrict__ partials) {
+// z = r / d (Jacobi) from a precomputed 1/d: q0 = r (1/d) and one
+// FMA residual correction, which reproduces the IEEE quotient (Markstein)
+// without the register-heavy DDIV sequence.
+__device__ __forceinline__ double jacobi_div(double r, double d, double dinv) {
+  const double q0 = r * dinv;
+  const double res = fma(-q0, d, r);
+  return fma(res, dinv, q0);
+}
+
+__global__ void __launch_bounds__(256, 4)
+k_stage1_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ dinv, double* __restrict__ r,
+           const double* __restrict__ yb, double* __restrict__ partials) {
   __shared__ double sh[32];
   const DevState* st = v.st;
   if (st->stopped) return;
@@ -141,14 +153,16 @@ k_stage1_e(DevView v, const int32_t* __restrict__ erow, double* __restrict__ r, 
   const int64_t n = v.nnzW;
   double part = 0.0;
   for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += STAGE_UNR * stride) {
-    double rv[STAGE_UNR], dv[STAGE_UNR];
+    double rv[STAGE_UNR], dv[STAGE_UNR], iv[STAGE_UNR];
 #pragma unroll
     for (int u = 0; u < STAGE_UNR; ++u) {
       const int64_t e = e0 + u * stride;
       if (e < n) {
         rv[u] = r[e];
         if (pend) rv[u] = rv[u] - ap * yb[e];
-        dv[u] = v.d[erow[e]];
+        const int32_t i = erow[e];
+        dv[u] = v.d[i];
+        iv[u] = dinv[i];
       }
     }
 #pragma unroll
@@ -156,7 +170,7 @@ k_stage1_e(DevView v, const int32_t* __restrict__ erow, double* __restrict__ r, 
       const int64_t e = e0 + u * stride;
       if (e < n) {
         if (pend) r[e] = rv[u];
-        const double z = rv[u] / dv[u];
+        const double z = jacobi_div(rv[u], dv[u], iv[u]);
         part = fma(rv[u], z, part);
       }
     }
@@ -165,9 +179,9 @@ k_stage1_e(DevView v, const int32_t* __restrict__ erow, double* __restrict__ r, 
   if (threadIdx.x == 0) partials[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(256)
-k_stage2_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ r, double* __restrict__ y,
-           double* __restrict__ dw) {
+__global__ void __launch_bounds__(256, 4)
+k_stage2_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ dinv,
+           const double* __restrict__ r, double* __restrict__ y, double* __restrict__ dw) {
   const DevState* st = v.st;
   const int stopped = st->stopped;
   const int pendw = st->pendw;
@@ -178,14 +192,14 @@ k_stage2_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n = v.nnzW;
   for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += STAGE_UNR * stride) {
-    double yo[STAGE_UNR], rv[STAGE_UNR], dv[STAGE_UNR], dwv[STAGE_UNR];
+    double yo[STAGE_UNR], rv[STAGE_UNR], dv[STAGE_UNR], iv[STAGE_UNR], dwv[STAGE_UNR];
 #pragma unroll
     for (int u = 0; u < STAGE_UNR; ++u) {
       const int64_t e = e0 + u * stride;
       if (e < n) {
         yo[u] = y[e];
         if (pendw) dwv[u] = dw[e];
-        if (!stopped) { rv[u] = r[e]; dv[u] = v.d[erow[e]]; }
+        if (!stopped) { rv[u] = r[e]; const int32_t i = erow[e]; dv[u] = v.d[i]; iv[u] = dinv[i]; }
       }
     }
 #pragma unroll
@@ -194,12 +208,17 @@ k_stage2_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict
       if (e < n) {
         if (pendw) dw[e] = dwv[u] + ap * yo[u];
         if (!stopped) {
-          const double z = rv[u] / dv[u];
+          const double z = jacobi_div(rv[u], dv[u], iv[u]);
           y[e] = first ? z : z + beta * yo[u];
         }
       }
     }
   }
+}
+
+__global__ void k_recip(const double* __restrict__ d, int64_t n, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = 1.0 / d[i];
 }
 
 __global__ void k_build_erow(const int64_t* __restrict__ wptr, int64_t nF, int32_t* __restrict__ erow) {
@@ -209,6 +228,7 @@ __global__ void k_build_erow(const int64_t* __restrict__ wptr, int64_t nF, int32
 
 // ------------------------------------------------------------ scalars
 __device__ double reduce_partials(const double* __restrict__ p, int np, double* sh) {
+  if (np < 0) return p[0];   // already reduced over the ranks (DevState::red)
   double s = 0.0;
   for (int k = threadIdx.x; k < np; k += blockDim.x) s += p[k];
   return block_sum(s, sh);
@@ -335,9 +355,9 @@ void launch_stage2_g(emin_ctx c, cudaStream_t s) {
 void launch_stage(emin_ctx c, int which, cudaStream_t s) {
   if (!c->opts.project_after_jacobi) {
     if (which == 1)
-      k_stage1_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->r, c->yb, c->partials);
+      k_stage1_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->yb, c->partials);
     else
-      k_stage2_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->r, c->y, c->dw);
+      k_stage2_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->y, c->dw);
     return;
   }
   switch (c->group) {
@@ -357,7 +377,12 @@ int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, 
   const int grid = c->grid_spgemm;
   if (c->kernel_path == 1) {
     launch_scalar_masked(c, mode, X, X2, out, s);
-    return grid;
+    return mode == MM_ITER ? scalar_iter_grid(c) : grid;
+  }
+  if (c->kernel_path == 2 && mode == MM_ITER) {
+    const NodalPlan* np = static_cast<const NodalPlan*>(c->nodal);
+    launch_nodal_iter(c, np, X, out, s);
+    return nodal_grid(c, np);
   }
   const int mc = c->max_row <= 32 ? 1 : c->max_row <= 64 ? 2 : 4;
 #define LAUNCH_M(MODE, MC, SUMX) \
@@ -380,15 +405,26 @@ emin_status emin_plan(emin_ctx c) {
   c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF * c->group + 255) / 256, (int64_t)SM * 8));
   c->grid_spgemm = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF + 7) / 8, (int64_t)SM * 8));
   c->kernel_path = select_fast_path(c);
+  if (c->kernel_path == 0 && (c->opts.row_begin % 3) == 0) {
+    NodalPlan* np = nullptr;
+    if (select_nodal_path(c, np)) {
+      c->nodal = np;
+      c->kernel_path = 2;
+    }
+  }
   if (c->kernel_path == 1) c->grid_spgemm = scalar_spgemm_grid(c);
   if (!c->opts.project_after_jacobi) {
     // entry-parallel streaming stages: row id per W entry
     EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->erow, sizeof(int32_t) * std::max<int64_t>(c->nnzW, 1), c->stream));
     k_build_erow<<<SM * 8, 256, 0, c->stream>>>(c->wptr, c->nF, c->erow);
-    c->launches += 1;
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->dinv, sizeof(double) * std::max<int64_t>(c->nF, 1), c->stream));
+    k_recip<<<SM * 4, 256, 0, c->stream>>>(c->d, c->nF, c->dinv);
+    c->launches += 2;
     c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * 8));
   }
   c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
+  if (c->kernel_path == 1) c->grid_red = std::max(c->grid_red, scalar_iter_grid(c));
+  if (c->kernel_path == 2) c->grid_red = std::max(c->grid_red, nodal_grid(c, static_cast<NodalPlan*>(c->nodal)));
   if (c->grid_red > c->n_partials) {
     cudaFreeAsync(c->partials, c->stream);
     EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->partials, sizeof(double) * c->grid_red, c->stream));
@@ -407,13 +443,26 @@ bool emin_alg2_fast(emin_ctx c, const double* Bc, const double* B, const int64_t
 }
 
 // r0 = -Pi (A P0)|F, E0, fresh CG state (end of setup and emin_reset)
+// Sum of the per-block partials; on several GPUs: local sum into
+// st->red[slot], ncclAllReduce in place, and the consumer reads it (np = -1).
+// Returns the (pointer, np) pair the consumer kernel takes.
+static std::pair<const double*, int> global_sum(emin_ctx c, int np, int slot, cudaStream_t s) {
+  if (!c->dist) return {c->partials, np};
+  k_energy_out<<<1, 1024, 0, s>>>(c->partials, np, 0.0, &c->st->red[slot]);
+  c->launches += 1;
+  emin_dist_allreduce(c, &c->st->red[slot], 1, s);
+  return {&c->st->red[slot], -1};
+}
+
 emin_status emin_finish_r0(emin_ctx c) {
   cudaStream_t s = c->stream;
-  EMIN_CUDA_TRY(c, cudaMemsetAsync(c->dw, 0, sizeof(double) * std::max<int64_t>(c->nnzW, 1), s));
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(c->dw, 0, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s));
   emin_launch_masked(c, MM_R0, c->w0, nullptr, c->r, s);
   // energy of P0 (dw = 0)
   const int g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, s);
-  k_reset_state<<<1, 1024, 0, s>>>(c->st, c->partials, g, c->sum_diag_cc, c->opts.tau, c->opts.stagnation_rel);
+  const auto red = global_sum(c, g, 2, s);
+  k_reset_state<<<1, 1024, 0, s>>>(c->st, red.first, red.second, c->sum_diag_cc, c->opts.tau,
+                                   c->opts.stagnation_rel);
   c->launches += 3;
   EMIN_CUDA_TRY(c, cudaGetLastError());
   c->k_launched = 0;
@@ -428,13 +477,16 @@ static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev) {
   rec(0);
   launch_stage(c, 1, s);
   rec(1);
-  k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, c->partials, c->grid_rows);
+  const auto r1 = global_sum(c, c->grid_rows, 0, s);
+  k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, r1.first, r1.second);
   rec(2);
   launch_stage(c, 2, s);
+  if (c->dist) emin_dist_halo_values(c, c->y, s);     // y on the halo rows
   rec(3);
   const int g = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
   rec(4);
-  k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, c->partials, g, c->dE_hist);
+  const auto r2 = global_sum(c, g, 1, s);
+  k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, r2.first, r2.second, c->dE_hist);
   rec(5);
 }
 
@@ -543,10 +595,15 @@ static void flush(emin_ctx c) {
 extern "C" emin_status emin_energy(emin_ctx c, double* E) {
   if (!c || !E) return EMIN_ERR_ARG;
   flush(c);
+  if (c->dist) {
+    emin_status st = emin_dist_halo_values(c, c->dw, c->stream);   // W = W0 + dW on the halo rows
+    if (st != EMIN_OK) return st;
+  }
   const int g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, c->stream);
   double* dev;
   EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&dev, sizeof(double), c->stream));
-  k_energy_out<<<1, 1024, 0, c->stream>>>(c->partials, g, c->sum_diag_cc, dev);
+  const auto red = global_sum(c, g, 2, c->stream);
+  k_energy_out<<<1, 1024, 0, c->stream>>>(red.first, red.second, c->sum_diag_cc, dev);
   c->launches += 4;
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(E, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   cudaFreeAsync(dev, c->stream);
@@ -636,10 +693,16 @@ void emin_free_all(emin_ctx c) {
   cudaStream_t s = c->stream;
   void* ptrs[] = {c->wptr, c->affptr, c->afcptr, c->pofs, c->cofs, c->isc_own, c->wcol, c->affcol,
                   c->afccol, c->affval, c->afcval, c->d, c->Q, c->w0, c->dw, c->r, c->r0, c->y,
-                  c->yb, c->partials, c->dE_hist, c->st, c->erow};
+                  c->yb, c->partials, c->dE_hist, c->st, c->erow, c->dinv};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   free_fast_path(c);
+  {
+    NodalPlan* np = static_cast<NodalPlan*>(c->nodal);
+    free_nodal_path(c, np);
+    c->nodal = nullptr;
+  }
+  emin_dist_free(c);
   cudaStreamSynchronize(s);
 }
 

@@ -16,6 +16,7 @@
 #pragma once
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include "emin_internal.cuh"
 #include "masked.cuh"
 
@@ -35,6 +36,10 @@ struct ScalarPlan {
   int64_t ntiles = 0;
   size_t tile_smem = 0;
   int use_tiles = 0;
+  int use_pipe = 0, pipe_grid = 0, rec_cap = 0, rows_cap = 0;   // TMA-pipelined persistent kernel
+  uint32_t pipe_smem = 0;
+  struct WinHdr* whdr = nullptr; // [nwin] window headers
+  int variant = 0;               // per-iteration kernel: 0 hdr, 1 win, 2 tile, 3 pipe
 };
 
 // decode the window: rows [r0, r1), base entry, this lane's row and position
@@ -81,6 +86,94 @@ __device__ __forceinline__ double row_sum(double v, const WinLane& L) {
   }
   return __shfl_sync(0xffffffffu, v, L.rowbeg + L.rowlen - 1);
 }
+
+// Precomputed window header (one 16-byte load per warp; the lane decode is
+// pure ALU): first row, first entry, head bitmask (bit p set if a row starts
+// at window position p), entry count.
+struct WinHdr {
+  int32_t r0;
+  int32_t base;
+  uint32_t head;
+  int32_t nent;
+};
+
+__device__ __forceinline__ WinLane decode_hdr(const WinHdr& h, int lane) {
+  WinLane w;
+  w.base = h.base;
+  w.nent = h.nent;
+  const int l = lane < h.nent ? lane : h.nent - 1;    // inactive lanes mirror the last entry
+  const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+  const unsigned hu = h.head & upto;
+  w.rloc = __popc(hu) - 1;
+  w.rowbeg = 31 - __clz(hu);
+  const unsigned after = h.head & ~upto;
+  const int rowend = after ? (__ffs(after) - 1) : h.nent;
+  w.rowlen = rowend - w.rowbeg;
+  w.pos = lane - w.rowbeg;
+  w.act = lane < h.nent;
+  return w;
+}
+
+__global__ void k_plan_headers(const int64_t* __restrict__ wptr, const int32_t* __restrict__ rowstart,
+                               int64_t nwin, WinHdr* __restrict__ hdr) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r0 = rowstart[w], r1 = rowstart[w + 1];
+    WinHdr h;
+    h.r0 = r0;
+    h.base = (int32_t)(r1 > r0 ? wptr[r0] : 0);
+    h.nent = (int32_t)(r1 > r0 ? wptr[r1] - wptr[r0] : 0);
+    uint32_t head = 0;
+    for (int32_t r = r0; r < r1; ++r) head |= 1u << (unsigned)(wptr[r] - h.base);
+    h.head = head;
+    hdr[w] = h;
+  }
+}
+
+// y^ = Pi K y (nv = 1) on precomputed window headers, next header prefetched
+__global__ void __launch_bounds__(256)
+k_spgemm_hdr(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__ hdr, int64_t nwin,
+             const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  WinHdr h = (w < nwin) ? hdr[w] : WinHdr{0, 0, 0u, 0};
+  while (w < nwin) {
+    const int64_t wn = w + nw;
+    const WinHdr hn = (wn < nwin) ? hdr[wn] : WinHdr{0, 0, 0u, 0};
+    if (h.nent > 0) {                                 // warp-uniform
+      const WinLane L = decode_hdr(h, lane);
+      const int64_t i = (int64_t)h.r0 + L.rloc;
+      const int64_t e = (int64_t)h.base + lane;
+      const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
+      const double qv = L.act ? v.Q[e] : 0.0;
+      const double xo = L.act ? X[e] : 0.0;
+      double acc = 0.0;
+      if (L.act) {
+        const unsigned sh4 = 4u * (unsigned)L.pos;
+#pragma unroll 4
+        for (int64_t q = qb; q < qe; ++q) {
+          const SpEnt en = A[q];
+          const unsigned s = (en.pm >> sh4) & 0xFu;
+          if (s != 0xFu) acc = fma(en.a, X[(int64_t)en.ybase + s], acc);
+        }
+      }
+      const double dot = row_sum(qv * acc, L);
+      const double g = acc - qv * dot;
+      if (L.act) {
+        out[e] = g;
+        part = fma(xo, g, part);
+      }
+    }
+    h = hn;
+    w = wn;
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
 
 // Masked product on the scalar path, modes as in masked.cuh:
 //   MM_ITER    yb = Pi K y, partial y . yb
@@ -421,6 +514,184 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
   if (threadIdx.x == 0) partials[blockIdx.x] = tot;
 }
 
+// ---------------------------------------------------------------------------
+// Persistent, TMA-pipelined variant of the tile kernel (MM_ITER, the hot
+// launch).  Each CTA walks tiles t = blockIdx.x, +gridDim.x, ...; thread 0
+// streams the NEXT tile's contiguous slices (A_FF records, the Q and y
+// slices of its W entries, the wptr / affptr slices) into the other smem
+// stage with cp.async.bulk (1D TMA, completion on an mbarrier) while the CTA
+// computes the current tile.  Only the y(k, s) gathers remain as loads.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct PipeLayout {     // byte offsets of one stage, and of the shared tail
+  uint32_t rec, q, x, wp, ap, stage_bytes;
+  uint32_t erow, qa, dot, bars, total;
+};
+
+__host__ __device__ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
+
+__host__ __device__ inline PipeLayout pipe_layout(int rec_cap, int rows_cap) {
+  PipeLayout L;
+  L.rec = 0;
+  L.q = align16(L.rec + (uint32_t)rec_cap * 16u);
+  L.x = align16(L.q + (TILE_E + 2) * 8u);
+  L.wp = align16(L.x + (TILE_E + 2) * 8u);
+  L.ap = align16(L.wp + ((uint32_t)rows_cap + 3) * 8u);
+  L.stage_bytes = align16(L.ap + ((uint32_t)rows_cap + 3) * 8u);
+  L.erow = 2 * L.stage_bytes;
+  L.qa = align16(L.erow + TILE_E * 2u);
+  L.dot = align16(L.qa + TILE_E * 8u);
+  L.bars = align16(L.dot + ((uint32_t)rows_cap + 1) * 8u);
+  L.total = L.bars + 16u;
+  return L;
+}
+
+// issue the bulk copies of tile h into stage buffer sb (thread 0 only);
+// 8-byte slices are copied from the 16-byte aligned element below their start
+__device__ __forceinline__ void pipe_issue(const TileHdr& h, unsigned char* sb, const PipeLayout& L,
+                                           const SpEnt* __restrict__ A, const double* __restrict__ Q,
+                                           const double* __restrict__ X, const int64_t* __restrict__ wptr,
+                                           const int64_t* __restrict__ affptr, uint64_t* bar) {
+  const int64_t nrec = h.aend - h.abase;
+  const int64_t e0 = h.base & ~1LL, e1 = (h.end + 1) & ~1LL;        // [e0, e1) even-aligned
+  const int64_t r0 = h.r0 & ~1LL, r1 = (h.r1 + 2) & ~1LL;           // rows [r0, r1) cover r0..r1
+  const uint32_t bytes = (uint32_t)(nrec * 16 + 2 * (e1 - e0) * 8 + 2 * (r1 - r0) * 8);
+  mbar_expect_tx(bar, bytes);
+  if (nrec) bulk_g2s(sb + L.rec, A + h.abase, (uint32_t)(nrec * 16), bar);
+  bulk_g2s(sb + L.q, Q + e0, (uint32_t)((e1 - e0) * 8), bar);
+  bulk_g2s(sb + L.x, X + e0, (uint32_t)((e1 - e0) * 8), bar);
+  bulk_g2s(sb + L.wp, wptr + r0, (uint32_t)((r1 - r0) * 8), bar);
+  bulk_g2s(sb + L.ap, affptr + r0, (uint32_t)((r1 - r0) * 8), bar);
+}
+
+__global__ void __launch_bounds__(TILE_T)
+k_spgemm_pipe(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict__ hdr, int64_t ntiles,
+              int rec_cap, int rows_cap, const double* __restrict__ X, double* __restrict__ out,
+              double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double sh[32];
+  if (v.st->stopped) return;
+  const PipeLayout L = pipe_layout(rec_cap, rows_cap);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
+  uint16_t* s_erow = reinterpret_cast<uint16_t*>(smem_raw + L.erow);
+  double* s_qa = reinterpret_cast<double*>(smem_raw + L.qa);
+  double* s_dot = reinterpret_cast<double*>(smem_raw + L.dot);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int64_t t = blockIdx.x;
+  if (tid == 0 && t < ntiles) pipe_issue(hdr[t], smem_raw, L, A, v.Q, X, v.wptr, v.affptr, &bars[0]);
+  double part = 0.0;
+  for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
+    const int st = it & 1;
+    unsigned char* sb = smem_raw + st * L.stage_bytes;
+    const TileHdr H = hdr[t];
+    // prefetch the next tile into the other stage (its last readers passed
+    // the __syncthreads that ended the previous iteration)
+    if (tid == 0 && t + gridDim.x < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      pipe_issue(hdr[t + gridDim.x], smem_raw + (st ^ 1) * L.stage_bytes, L, A, v.Q, X, v.wptr, v.affptr,
+                 &bars[st ^ 1]);
+    }
+    mbar_wait(&bars[st], (uint32_t)((it >> 1) & 1));
+    const SpEnt* s_rec = reinterpret_cast<const SpEnt*>(sb + L.rec);
+    const double* s_q = reinterpret_cast<const double*>(sb + L.q) + (H.base & 1);
+    const double* s_x = reinterpret_cast<const double*>(sb + L.x) + (H.base & 1);
+    const int64_t* s_wp = reinterpret_cast<const int64_t*>(sb + L.wp) + (H.r0 & 1);
+    const int64_t* s_ap = reinterpret_cast<const int64_t*>(sb + L.ap) + (H.r0 & 1);
+    const int nrows = H.r1 - H.r0;
+    const int nent = (int)(H.end - H.base);
+    for (int r = tid; r < nrows; r += TILE_T) {
+      const int pb = (int)(s_wp[r] - H.base), pe = (int)(s_wp[r + 1] - H.base);
+      for (int p = pb; p < pe; ++p) s_erow[p] = (uint16_t)r;
+    }
+    __syncthreads();
+    double g[TILE_U], qv[TILE_U];
+    int rl[TILE_U];
+#pragma unroll
+    for (int u = 0; u < TILE_U; ++u) {
+      const int e = tid + u * TILE_T;
+      g[u] = 0.0;
+      qv[u] = 0.0;
+      rl[u] = 0;
+      if (e < nent) {
+        const int r = s_erow[e];
+        rl[u] = r;
+        qv[u] = s_q[e];
+        const unsigned sh4 = 4u * (unsigned)(e - (int)(s_wp[r] - H.base));
+        const int q0 = (int)(s_ap[r] - H.abase), q1 = (int)(s_ap[r + 1] - H.abase);
+        double acc = 0.0;
+#pragma unroll 4
+        for (int q = q0; q < q1; ++q) {
+          const SpEnt en = s_rec[q];
+          const unsigned s = (en.pm >> sh4) & 0xFu;
+          if (s != 0xFu) acc = fma(en.a, X[(int64_t)en.ybase + s], acc);
+        }
+        g[u] = acc;
+      }
+    }
+    // Pi_B (nv = 1): g - q (q . g) per row, fixed-order row sums
+#pragma unroll
+    for (int u = 0; u < TILE_U; ++u) {
+      const int e = tid + u * TILE_T;
+      if (e < nent) s_qa[e] = qv[u] * g[u];
+    }
+    __syncthreads();
+    for (int r = tid; r < nrows; r += TILE_T) {
+      const int pb = (int)(s_wp[r] - H.base), pe = (int)(s_wp[r + 1] - H.base);
+      double s = 0.0;
+      for (int p = pb; p < pe; ++p) s += s_qa[p];
+      s_dot[r] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < TILE_U; ++u) {
+      const int e = tid + u * TILE_T;
+      if (e < nent) {
+        const double o = g[u] - qv[u] * s_dot[rl[u]];
+        out[H.base + e] = o;
+        part = fma(s_x[e], o, part);
+      }
+    }
+    __syncthreads();   // stage st and the shared tail are free again
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
 __global__ void k_tile_headers(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
                                const int32_t* __restrict__ trow, int64_t ntiles, TileHdr* __restrict__ hdr,
                                int32_t* __restrict__ maxrec) {
@@ -434,6 +705,7 @@ __global__ void k_tile_headers(const int64_t* __restrict__ wptr, const int64_t* 
     h.aend = affptr[h.r1];
     hdr[t] = h;
     atomicMax(maxrec, (int32_t)(h.aend - h.abase));
+    atomicMax(maxrec + 1, h.r1 - h.r0);
   }
 }
 
@@ -465,16 +737,22 @@ __global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
   for (int64_t i = gid; i < v.nF; i += ng) {
     const int64_t b = v.wptr[i];
     const int nj = (int)(v.wptr[i + 1] - b);
+    int32_t ji[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) ji[t] = (t < nj) ? v.wcol[b + t] : -1;
     for (int64_t q = v.affptr[i] + lg; q < v.affptr[i + 1]; q += 8) {
       const int32_t k = v.affcol[q];
       const int64_t kb = v.wptr[k];
       const int nk = (int)(v.wptr[k + 1] - kb);
+      int32_t jk[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) jk[s] = (s < nk) ? v.wcol[kb + s] : -2;
       uint32_t pm = 0xFFFFFFFFu;
-      for (int t = 0; t < nj; ++t) {
-        const int32_t j = v.wcol[b + t];
-        for (int s = 0; s < nk; ++s)
-          if (v.wcol[kb + s] == j) { pm = (pm & ~(0xFu << (4 * t))) | ((uint32_t)s << (4 * t)); break; }
-      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (ji[t] == jk[s]) pm = (pm & ~(0xFu << (4 * t))) | ((uint32_t)s << (4 * t));
       SpEnt e;
       e.a = v.affval[q];
       e.ybase = (int32_t)kb;
@@ -512,23 +790,52 @@ static inline int select_fast_path(emin_ctx c) {
   int32_t* dmax = nullptr;
   if (cudaMallocAsync((void**)&trow, sizeof(int32_t) * (p.ntiles + 1), s) != cudaSuccess ||
       cudaMallocAsync((void**)&p.hdr, sizeof(TileHdr) * std::max<int64_t>(p.ntiles, 1), s) != cudaSuccess ||
-      cudaMallocAsync((void**)&dmax, sizeof(int32_t), s) != cudaSuccess)
+      cudaMallocAsync((void**)&dmax, sizeof(int32_t) * 2, s) != cudaSuccess)
     return 1;
-  cudaMemsetAsync(dmax, 0, sizeof(int32_t), s);
+  cudaMemsetAsync(dmax, 0, sizeof(int32_t) * 2, s);
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, ST, p.ntiles, trow);
   k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
   c->launches += 2;
-  int32_t hmax = 0;
-  cudaMemcpyAsync(&hmax, dmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  int32_t hmax[2] = {0, 0};
+  cudaMemcpyAsync(hmax, dmax, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(trow, s);
   cudaFreeAsync(dmax, s);
   cudaStreamSynchronize(s);
-  p.tile_smem = tile_smem_bytes(hmax);
-  if (p.tile_smem <= 160 * 1024 && !getenv("EMIN_NO_TILE")) {
+  p.tile_smem = tile_smem_bytes(hmax[0]);
+  // window headers (lane decode without the rowstart -> wptr round trips)
+  if (cudaMallocAsync((void**)&p.whdr, sizeof(WinHdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) return 1;
+  k_plan_headers<<<SM * 4, 256, 0, s>>>(c->wptr, p.rowstart, p.nwin, p.whdr);
+  c->launches += 1;
+  // per-iteration kernel variant (EMIN_SPGEMM=hdr|win|tile|pipe; default hdr)
+  const char* var = getenv("EMIN_SPGEMM");
+  p.variant = 0;
+  if (var && !strcmp(var, "win")) p.variant = 1;
+  if (var && !strcmp(var, "tile")) p.variant = 2;
+  if (var && !strcmp(var, "pipe")) p.variant = 3;
+  if (p.tile_smem <= 160 * 1024) {
     p.use_tiles = 1;
     cudaFuncSetAttribute(k_spgemm_tile<MM_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
     cudaFuncSetAttribute(k_spgemm_tile<MM_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
     cudaFuncSetAttribute(k_spgemm_tile<MM_ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
+  } else if (p.variant == 2) {
+    p.variant = 0;
+  }
+  if (p.variant == 3) {
+    // persistent TMA-pipelined kernel
+    p.rec_cap = (hmax[0] + 1) & ~1;
+    p.rows_cap = hmax[1] + 1;
+    p.pipe_smem = pipe_layout(p.rec_cap, p.rows_cap).total;
+    int per_sm = 0;
+    if (p.pipe_smem <= 200 * 1024) {
+      cudaFuncSetAttribute(k_spgemm_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.pipe_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_pipe, TILE_T, p.pipe_smem);
+    }
+    if (per_sm > 0) {
+      p.use_pipe = 1;
+      p.pipe_grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)SM * per_sm));
+    } else {
+      p.variant = 0;
+    }
   }
   return 1;
 }
@@ -538,31 +845,57 @@ static inline int scalar_grid(emin_ctx c) {
   const int64_t nwin = fast_of(c)->sc.nwin;
   return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * 8));
 }
+// grid of the setup-time masked launches (MM_R0, MM_ENERGY)
 static inline int scalar_spgemm_grid(emin_ctx c) {
   const ScalarPlan& p = fast_of(c)->sc;
   return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
+}
+// grid of the per-iteration masked launch (MM_ITER)
+static inline int scalar_iter_grid(emin_ctx c) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  switch (p.variant) {
+    case 2: return (int)std::max<int64_t>(1, p.ntiles);
+    case 3: return p.pipe_grid;
+    default: return scalar_grid(c);
+  }
 }
 
 static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
                                         cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
+  if (mode == MM_ITER) {
+    switch (p.variant) {
+      case 0:
+        k_spgemm_hdr<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, X, out, c->partials);
+        return;
+      case 1:
+        k_spgemm_scalar<MM_ITER><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
+                                                                c->partials);
+        return;
+      case 2:
+        k_spgemm_tile<MM_ITER><<<(int)std::max<int64_t>(1, p.ntiles), TILE_T, p.tile_smem, s>>>(
+            v, p.ent, p.hdr, X, X2, out, c->partials);
+        return;
+      default:
+        k_spgemm_pipe<<<p.pipe_grid, TILE_T, p.pipe_smem, s>>>(v, p.ent, p.hdr, p.ntiles, p.rec_cap, p.rows_cap,
+                                                              X, out, c->partials);
+        return;
+    }
+  }
   if (p.use_tiles) {
     const int g = (int)std::max<int64_t>(1, p.ntiles);
-    if (mode == MM_ITER)
-      k_spgemm_tile<MM_ITER><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
-    else if (mode == MM_R0)
+    if (mode == MM_R0)
       k_spgemm_tile<MM_R0><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
     else
       k_spgemm_tile<MM_ENERGY><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
     return;
   }
-  if (mode == MM_ITER)
-    k_spgemm_scalar<MM_ITER><<<c->grid_spgemm, 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
-  else if (mode == MM_R0)
-    k_spgemm_scalar<MM_R0><<<c->grid_spgemm, 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
+  if (mode == MM_R0)
+    k_spgemm_scalar<MM_R0><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
   else
-    k_spgemm_scalar<MM_ENERGY><<<c->grid_spgemm, 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
+    k_spgemm_scalar<MM_ENERGY><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
+                                                              c->partials);
 }
 static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
                                       const double* what, unsigned long long* counters, cudaStream_t s) {
@@ -588,6 +921,7 @@ static inline void free_fast_path(emin_ctx c) {
   if (f->sc.rowstart) cudaFreeAsync(f->sc.rowstart, c->stream);
   if (f->sc.ent) cudaFreeAsync(f->sc.ent, c->stream);
   if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
+  if (f->sc.whdr) cudaFreeAsync(f->sc.whdr, c->stream);
   delete f;
   c->fast = nullptr;
 }

@@ -1,0 +1,252 @@
+// kernels_nodal.cuh -- nodal (3x3 block) path for vector problems
+// (elasticity, configs 4-5; kernel_path 2), selected when emin_opts.block_size
+// = 3 and the structure checks pass.
+//
+// Rows 3n..3n+2 of an F node n share the pattern J_n (blockwise: columns
+// 3c, 3c+1, 3c+2 for every C node c in J_n) and hence the same M_i =
+// B_c(J_i,:) and the same Q_i; A_FF is made of dense 3x3 blocks (I,K).  The
+// masked product of node I is then
+//     Yb(I,d; c,b) = sum_K sum_d' A_IK[d][d'] Y(K,d'; c,b),  c in J_I n J_K
+// computed by one warp per node: lane t owns the pattern positions t and
+// t+32 (t = 3 s + b: C node s of J_I, component b) for all three output rows
+// d, so each matched (block, position) costs 3 gathers and 9 FMAs and the
+// node-level match (s in J_I -> s_K in J_K) is read once per block and lane
+// from a byte map built at setup.  Q is read once per node (row 3I) instead
+// of three times.
+#pragma once
+#include "emin_internal.cuh"
+
+struct NodalBlk {      // one per A_FF 3x3 block (I,K)
+  int32_t ybase;       // wptr[3K]: first W entry of the neighbour node
+  int32_t nK3;         // 3 |J_K|: row length of the neighbour node
+};
+
+struct NodalPlan {
+  int64_t nFn = 0;            // owned F nodes
+  NodalBlk* blk = nullptr;    // [nblk]
+  int64_t* bptr = nullptr;    // [nFn+1] block offset of node n (= affptr[3n] / 9)
+  uint8_t* pm8 = nullptr;     // [sum_n nblk_n |J_n|] position of J_I[s] in J_K, 0xFF absent
+  int64_t* pmoff = nullptr;   // [nFn+1]
+  int64_t nblk = 0, npm = 0;
+};
+
+// structure checks (one thread per F node); any violation clears *ok
+__global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_len) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = 3 * n;
+    const int64_t wb = v.wptr[r];
+    const int64_t len = v.wptr[r + 1] - wb;
+    bool good = (len % 3 == 0) && len > 0 && len <= 3 * 32;
+    for (int d = 1; d < 3 && good; ++d) good = (v.wptr[r + d + 1] - v.wptr[r + d]) == len;
+    for (int64_t t = 0; t < len && good; ++t) {
+      const int32_t c = v.wcol[wb + t];
+      if ((t % 3 == 0 && c % 3 != 0) || (t % 3 != 0 && c != v.wcol[wb + t - 1] + 1)) good = false;
+      for (int d = 1; d < 3 && good; ++d) good = v.wcol[v.wptr[r + d] + t] == c;
+    }
+    const int64_t ab = v.affptr[r];
+    const int64_t alen = v.affptr[r + 1] - ab;
+    good = good && (alen % 3 == 0);
+    for (int d = 1; d < 3 && good; ++d) good = (v.affptr[r + d + 1] - v.affptr[r + d]) == alen;
+    for (int64_t q = 0; q < alen && good; ++q) {
+      const int32_t k = v.affcol[ab + q];
+      if ((q % 3 == 0 && k % 3 != 0) || (q % 3 != 0 && k != v.affcol[ab + q - 1] + 1)) good = false;
+      for (int d = 1; d < 3 && good; ++d) good = v.affcol[v.affptr[r + d] + q] == k;
+    }
+    if (!good) atomicExch(ok, 0);
+    pm_len[n] = good ? (alen / 3) * (len / 3) : 0;
+  }
+}
+
+// per node: block records and the byte position map (thread per node)
+__global__ void k_nodal_build(DevView v, int64_t nFn, const int64_t* __restrict__ pmoff, NodalBlk* __restrict__ blk,
+                              int64_t* __restrict__ bptr, uint8_t* __restrict__ pm8) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = 3 * n;
+    const int64_t wb = v.wptr[r];
+    const int nJ = (int)((v.wptr[r + 1] - wb) / 3);
+    const int64_t ab = v.affptr[r];
+    const int nb = (int)((v.affptr[r + 1] - ab) / 3);
+    const int64_t b0 = ab / 9;
+    bptr[n] = b0;
+    if (n == nFn - 1) bptr[nFn] = v.affptr[3 * nFn] / 9;
+    int64_t po = pmoff[n];
+    for (int b = 0; b < nb; ++b) {
+      const int32_t K = v.affcol[ab + 3 * b] / 3;
+      const int64_t kb = v.wptr[3 * (int64_t)K];
+      const int nK = (int)((v.wptr[3 * (int64_t)K + 1] - kb) / 3);
+      NodalBlk nbk;
+      nbk.ybase = (int32_t)kb;
+      nbk.nK3 = 3 * nK;
+      blk[b0 + b] = nbk;
+      // merge the two sorted node lists J_I and J_K
+      int sK = 0;
+      for (int s = 0; s < nJ; ++s) {
+        const int32_t c = v.wcol[wb + 3 * s];
+        while (sK < nK && v.wcol[kb + 3 * sK] < c) ++sK;
+        pm8[po + s] = (sK < nK && v.wcol[kb + 3 * sK] == c) ? (uint8_t)sK : (uint8_t)0xFF;
+      }
+      po += nJ;
+    }
+  }
+}
+
+// y^ = Pi K y on the nodal path (+ partial y . y^)
+template <int NV>
+__global__ void __launch_bounds__(256)
+k_spgemm_nodal(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
+               const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
+               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part = 0.0;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t r = 3 * n;
+    const int64_t wb = v.wptr[r];
+    const int n3 = (int)(v.wptr[r + 1] - wb);
+    const int nJ = n3 / 3;
+    const int t0 = lane, t1 = lane + 32;
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
+    const int64_t ab = v.affptr[r];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int64_t rs = 3 * (int64_t)nb;          // row stride of the node's A chunk
+    const int64_t po = pmoff[n];
+    double acc0[3] = {0.0, 0.0, 0.0}, acc1[3] = {0.0, 0.0, 0.0};
+    for (int b = 0; b < nb; ++b) {
+      const NodalBlk k = blk[bb + b];
+      double a[3][3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int e = 0; e < 3; ++e) a[d][e] = __ldg(v.affval + ab + d * rs + 3 * b + e);
+      const int p0 = act0 ? pm8[po + (int64_t)b * nJ + s0] : 0xFF;
+      const int p1 = act1 ? pm8[po + (int64_t)b * nJ + s1] : 0xFF;
+      if (p0 != 0xFF) {
+        double y[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) y[e] = X[(int64_t)k.ybase + e * k.nK3 + 3 * p0 + b0];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) acc0[d] = fma(a[d][e], y[e], acc0[d]);
+      }
+      if (p1 != 0xFF) {
+        double y[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) y[e] = X[(int64_t)k.ybase + e * k.nK3 + 3 * p1 + b1];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) acc1[d] = fma(a[d][e], y[e], acc1[d]);
+      }
+    }
+    // Pi_B per output row (Q of the node, row 3n, shared by its 3 rows)
+    double q0[NV], q1[NV];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      q0[m] = act0 ? v.Q[(wb + t0) * NV + m] : 0.0;
+      q1[m] = act1 ? v.Q[(wb + t1) * NV + m] : 0.0;
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double dots[NV];
+#pragma unroll
+      for (int m = 0; m < NV; ++m) dots[m] = warp_sum(fma(q0[m], acc0[d], q1[m] * acc1[d]));
+      double s0v = 0.0, s1v = 0.0;
+#pragma unroll
+      for (int m = 0; m < NV; ++m) {
+        s0v = fma(q0[m], dots[m], s0v);
+        s1v = fma(q1[m], dots[m], s1v);
+      }
+      const int64_t ro = wb + (int64_t)d * n3;
+      if (act0) {
+        const double g = acc0[d] - s0v;
+        out[ro + t0] = g;
+        part = fma(X[ro + t0], g, part);
+      }
+      if (act1) {
+        const double g = acc1[d] - s1v;
+        out[ro + t1] = g;
+        part = fma(X[ro + t1], g, part);
+      }
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// ---- host side ------------------------------------------------------------
+template <typename T>
+static cudaError_t nd_alloc(T** p, int64_t n, cudaStream_t s) {
+  return cudaMallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s);
+}
+
+// returns true if the nodal path was built
+static inline bool select_nodal_path(emin_ctx c, NodalPlan*& out) {
+  out = nullptr;
+  if (c->opts.block_size != 3 || c->nF % 3 != 0 || c->nF == 0 || c->nv > 8 || c->nnzWh >= INT32_MAX) return false;
+  if (getenv("EMIN_FORCE_GENERIC")) return false;
+  cudaStream_t s = c->stream;
+  const int SM = emin_num_sms();
+  const int64_t nFn = c->nF / 3;
+  int32_t* ok;
+  int64_t *pmlen, *scratch, *tot;
+  if (nd_alloc(&ok, 1, s) || nd_alloc(&pmlen, nFn + 1, s) || nd_alloc(&scratch, emin_scan_scratch_elems(nFn + 1), s) ||
+      nd_alloc(&tot, 1, s))
+    return false;
+  const int32_t one = 1;
+  cudaMemcpyAsync(ok, &one, sizeof(int32_t), cudaMemcpyHostToDevice, s);
+  k_nodal_check<<<SM * 8, 256, 0, s>>>(c->view(), nFn, ok, pmlen);
+  int32_t h_ok = 0;
+  cudaMemcpyAsync(&h_ok, ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  c->launches += 1;
+  if (!h_ok) {
+    cudaFreeAsync(ok, s); cudaFreeAsync(pmlen, s); cudaFreeAsync(scratch, s); cudaFreeAsync(tot, s);
+    return false;
+  }
+  NodalPlan* p = new NodalPlan();
+  p->nFn = nFn;
+  p->nblk = c->nnzAFF / 9;
+  emin_scan_i64(pmlen, pmlen, nFn, tot, scratch, s);     // exclusive -> offsets
+  cudaMemcpyAsync(pmlen + nFn, tot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(&p->npm, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  p->pmoff = pmlen;
+  if (nd_alloc(&p->blk, p->nblk, s) || nd_alloc(&p->bptr, nFn + 1, s) || nd_alloc(&p->pm8, p->npm, s)) {
+    delete p;
+    return false;
+  }
+  k_nodal_build<<<SM * 8, 256, 0, s>>>(c->view(), nFn, p->pmoff, p->blk, p->bptr, p->pm8);
+  c->launches += 4;
+  cudaFreeAsync(ok, s); cudaFreeAsync(scratch, s); cudaFreeAsync(tot, s);
+  out = p;
+  return true;
+}
+
+static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
+  const int SM = emin_num_sms();
+  return (int)std::max<int64_t>(1, std::min<int64_t>((p->nFn + 7) / 8, (int64_t)SM * 16));
+}
+
+static inline void launch_nodal_iter(emin_ctx c, const NodalPlan* p, const double* X, double* out, cudaStream_t s) {
+  const DevView v = c->view();
+  const int g = nodal_grid(c, p);
+  switch (c->nv) {
+#define NV_CASE(N) case N: k_spgemm_nodal<N><<<g, 256, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, out, c->partials); break;
+    NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+#undef NV_CASE
+  }
+}
+
+static inline void free_nodal_path(emin_ctx c, NodalPlan*& p) {
+  if (!p) return;
+  void* ptrs[] = {p->blk, p->bptr, p->pm8, p->pmoff};
+  for (void* q : ptrs) if (q) cudaFreeAsync(q, c->stream);
+  delete p;
+  p = nullptr;
+}

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "emin_internal.cuh"
+#include "dist.cuh"
 #include "masked.cuh"
 
 namespace {
@@ -118,6 +119,7 @@ struct FillArgs {
   int32_t* wcol; double* what; int64_t* pofs;
   int32_t* affcol; double* affval; int32_t* afccol; double* afcval;
   int64_t* frow;   // local F id -> local row
+  const int64_t* hpos;   // multi-GPU: halo slot of a global F id (null on one GPU)
 };
 
 // F rows: copy the pattern into the W layout, split A into A_FF (local F
@@ -164,7 +166,8 @@ __global__ void k_fill(FillArgs a) {
       const unsigned lt = (1u << lane) - 1u;
       if (fine) {
         const int64_t gF = (int64_t)c - a.cidx[c];
-        const int64_t loc = gF - a.fbegin;     // owned (single GPU: always)
+        int64_t loc = gF - a.fbegin;                          // owned row
+        if (loc < 0 || loc >= a.nF) loc = a.nF + a.hpos[gF];  // halo row (multi-GPU)
         const int64_t pos = off_ff + __popc(mf & lt);
         a.affcol[pos] = (int32_t)loc;
         a.affval[pos] = v;
@@ -499,8 +502,6 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     return fail(ctx, EMIN_ERR_ARG, "bad n_global / nc_global / nv");
   if (opts->row_begin < 0 || opts->row_end > n_global || opts->row_end <= opts->row_begin)
     return fail(ctx, EMIN_ERR_ARG, "bad row range");
-  if (opts->nccl_comm)
-    return fail(ctx, EMIN_ERR_ARG, "multi-GPU contexts are created with emin_setup_dist");
   if (n_global > INT32_MAX || nc_global > INT32_MAX)
     return fail(ctx, EMIN_ERR_ARG, "n_global exceeds the int32 column range");
 
@@ -523,6 +524,10 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   cudaStream_t s = ctx->stream;
   const int64_t m = ctx->m_owned;
   const int SM = emin_num_sms();
+  if (opts->nccl_comm) {
+    emin_status st = emin_dist_attach(ctx, opts->nccl_comm);
+    if (st != EMIN_OK) return fail(ctx, st, ctx->last_error);
+  }
 
   // ---- stage the inputs on the device (host pointers are copied)
   int64_t nnzA = 0, nnzP = 0, a0 = 0, p0 = 0;
@@ -620,6 +625,12 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   k_rows<<<SM * 8, 256, 0, s>>>(ra);
   k_check_B<<<SM * 8, 256, 0, s>>>(m, opts->row_begin, nv, dIsc, cidx, dB, dBc, nc_global, err, err_row);
   SETUP_TRY(cudaGetLastError());
+  if (ctx->dist) {
+    // every rank fails together; the longest pattern row is global
+    emin_status st1 = emin_dist_allreduce_max_i32(ctx, err, s);
+    emin_status st2 = emin_dist_allreduce_max_i32(ctx, max_row, s);
+    if (st1 != EMIN_OK || st2 != EMIN_OK) { tmp_free(); return fail(ctx, EMIN_ERR_NCCL, ctx->last_error); }
+  }
   int32_t h_err[2];
   int64_t h_err_row;
   SETUP_TRY(cudaMemcpyAsync(h_err, err, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
@@ -638,9 +649,18 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   }
   ctx->max_row = h_err[1];
 
+  // ---- multi-GPU: halo rows (F rows of other ranks referenced by A_FF)
+  if (ctx->dist) {
+    emin_status st = emin_dist_find_halo(ctx, fbegin, nF, n_global - nc_global, m, dArp, dAcol, dIsc, cidx,
+                                         scratch);
+    if (st != EMIN_OK) { tmp_free(); return fail(ctx, st, ctx->last_error); }
+    ctx->nFh = nF + ctx->dist->nH;
+  }
+
   // ---- row pointers of the W layout, A_FF and A_FC
-  SETUP_TRY(dalloc(&ctx->wptr, nF + 1, s));
-  SETUP_TRY(dalloc(&ctx->affptr, nF + 1, s));
+  // (+2 elements: the TMA slices are read from 16-byte aligned bounds)
+  SETUP_TRY(dalloc(&ctx->wptr, ctx->nFh + 1 + 2, s));
+  SETUP_TRY(dalloc(&ctx->affptr, nF + 1 + 2, s));
   SETUP_TRY(dalloc(&ctx->afcptr, nF + 1, s));
   SETUP_TRY(emin_scan_i64(cnt_w, ctx->wptr, nF, totals + 1, scratch, s));
   SETUP_TRY(emin_scan_i64(cnt_ff, ctx->affptr, nF, totals + 2, scratch, s));
@@ -655,10 +675,17 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   ctx->nnzAFF = h_tot[1];
   ctx->nnzAFC = h_tot[2];
   const int64_t W = ctx->nnzW;
+  if (ctx->dist) {
+    // halo row lengths -> wptr tail; send lists (once)
+    emin_status st = emin_dist_halo_pattern_sizes(ctx, scratch);
+    if (st != EMIN_OK) { tmp_free(); return fail(ctx, st, ctx->last_error); }
+    ctx->nnzWh = W + ctx->dist->nHW;
+  }
+  const int64_t Wh = ctx->nnzWh;
 
   // ---- fill
   double* what;
-  SETUP_TRY(dalloc(&ctx->wcol, W, s));
+  SETUP_TRY(dalloc(&ctx->wcol, Wh, s));
   SETUP_TRY(dalloc(&what, W, s)); temps.push_back(what);
   SETUP_TRY(dalloc(&ctx->pofs, nF, s));
   SETUP_TRY(dalloc(&ctx->cofs, m + 1, s));
@@ -679,8 +706,13 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   fa.wcol = ctx->wcol; fa.what = what; fa.pofs = ctx->pofs;
   fa.affcol = ctx->affcol; fa.affval = ctx->affval; fa.afccol = ctx->afccol; fa.afcval = ctx->afcval;
   fa.frow = frow;
+  fa.hpos = ctx->dist ? ctx->dist->hpos : nullptr;
   k_fill<<<SM * 16, 256, 0, s>>>(fa);
   SETUP_TRY(cudaGetLastError());
+  if (ctx->dist) {
+    emin_status st = emin_dist_halo_wcol(ctx);
+    if (st != EMIN_OK) { tmp_free(); return fail(ctx, st, ctx->last_error); }
+  }
 
   // ---- sum of the C-row diagonal (energy constant, Eq. trInc tr(A_cc))
   SETUP_TRY(dalloc(&ctx->partials, SM * 32, s));
@@ -697,18 +729,19 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   }
 
   // ---- Alg. 2
-  SETUP_TRY(dalloc(&ctx->Q, W * nv, s));
-  SETUP_TRY(dalloc(&ctx->w0, W, s));
-  SETUP_TRY(dalloc(&ctx->dw, W, s));
+  // w0, dw, y carry the halo tail (values of other ranks' rows)
+  SETUP_TRY(dalloc(&ctx->Q, W * nv + 2, s));
+  SETUP_TRY(dalloc(&ctx->w0, Wh + 2, s));
+  SETUP_TRY(dalloc(&ctx->dw, Wh + 2, s));
   SETUP_TRY(dalloc(&ctx->r, W, s));
-  SETUP_TRY(dalloc(&ctx->y, W, s));
+  SETUP_TRY(dalloc(&ctx->y, Wh + 2, s));
   SETUP_TRY(dalloc(&ctx->yb, W, s));
   SETUP_TRY(dalloc(&ctx->st, 1, s));
   unsigned long long* counters;
   SETUP_TRY(dalloc(&counters, 2, s)); temps.push_back(counters);
   SETUP_TRY(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, s));
-  SETUP_TRY(cudaMemsetAsync(ctx->dw, 0, sizeof(double) * W, s));
-  SETUP_TRY(cudaMemsetAsync(ctx->y, 0, sizeof(double) * W, s));
+  SETUP_TRY(cudaMemsetAsync(ctx->dw, 0, sizeof(double) * Wh, s));
+  SETUP_TRY(cudaMemsetAsync(ctx->y, 0, sizeof(double) * Wh, s));
   SETUP_TRY(cudaMemsetAsync(ctx->yb, 0, sizeof(double) * W, s));
   const DevView v = ctx->view();
   const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>((nF + 3) / 4, (int64_t)SM * 16));
@@ -721,6 +754,12 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   else
     k_alg2<4><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters);
   SETUP_TRY(cudaGetLastError());
+  if (ctx->dist) {
+    // W0 on the halo rows (needed by r0 and E0) and the global tr(A_CC)
+    emin_status st1 = emin_dist_halo_values(ctx, ctx->w0, s);
+    emin_status st2 = emin_dist_allreduce(ctx, dsum, 1, s);
+    if (st1 != EMIN_OK || st2 != EMIN_OK) { tmp_free(); return fail(ctx, EMIN_ERR_NCCL, ctx->last_error); }
+  }
 
   // ---- r0 = -Pi (A P0)|F and E0 = tr(P0^T A P0)
   double h_sum_cc = 0.0;

@@ -51,7 +51,8 @@ class emin_report_t(C.Structure):
 
 EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "emin_get_P",
             "emin_reset", "emin_report", "emin_destroy", "emin_status_str", "emin_last_error",
-            "emin_set_profiling", "emin_kernel_times", "emin_get_layout"]
+            "emin_set_profiling", "emin_kernel_times", "emin_get_layout", "emin_nccl_unique_id",
+            "emin_nccl_comm_init", "emin_nccl_comm_destroy"]
 
 
 def load_library():
@@ -92,6 +93,12 @@ def load_library():
     lib.emin_kernel_times.restype = i32
     lib.emin_get_layout.argtypes = [P, P, P, P]
     lib.emin_get_layout.restype = i32
+    lib.emin_nccl_unique_id.argtypes = [P]
+    lib.emin_nccl_unique_id.restype = i32
+    lib.emin_nccl_comm_init.argtypes = [C.POINTER(P), i32, P, i32]
+    lib.emin_nccl_comm_init.restype = i32
+    lib.emin_nccl_comm_destroy.argtypes = [P]
+    lib.emin_nccl_comm_destroy.restype = i32
     _lib = lib
     return lib
 
@@ -220,6 +227,33 @@ def emin_get_layout(ctx):
     pofs = np.empty(max(nF, 1), np.int64)
     _check(load_library().emin_get_layout(ctx, _ptr(wptr), _ptr(wcol), _ptr(pofs)), ctx)
     return wptr, wcol[:W], pofs[:nF]
+
+
+def emin_nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    _check(load_library().emin_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def emin_nccl_comm_init(nranks, uid, rank):
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    comm = C.c_void_p()
+    _check(load_library().emin_nccl_comm_init(C.byref(comm), int(nranks), C.cast(buf, C.c_void_p), int(rank)))
+    return comm
+
+
+def emin_nccl_comm_destroy(comm):
+    _check(load_library().emin_nccl_comm_destroy(comm))
+
+
+def nccl_comm_from_torch(group=None):
+    """Create an NCCL communicator for libemin over the ranks of a
+    torch.distributed group (the unique id travels through torch)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [emin_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return emin_nccl_comm_init(world, obj[0], rank)
 
 
 def emin_set_profiling(ctx, on):

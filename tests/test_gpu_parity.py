@@ -167,6 +167,32 @@ def test_no_free_dof_rows_and_all_coarse_edge():
     _compare(g, o, 5, prob)
 
 
+@pytest.mark.parametrize("name,size", [("3", 12), ("4", 3)])
+def test_nccl_single_rank_path_matches_single_gpu(name, size):
+    """The multi-GPU code path (NCCL communicator, halo plan, allreduced
+    scalars, NCCL calls inside the CUDA graph) on a 1-rank communicator:
+    no halo rows, and the same result as the plain single-GPU context."""
+    from paper_2208_02995_b200 import Emin
+    from paper_2208_02995_b200 import emin as E
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    uid = E.emin_nccl_unique_id()
+    comm = E.emin_nccl_comm_init(1, uid, 0)
+    try:
+        a = Emin.from_problem(prob, nccl_comm=comm)
+        b = Emin.from_problem(prob)
+        assert a.report()["nranks"] == 1
+        kda, dEa = a.iterate(20)
+        kdb, dEb = b.iterate(20)
+        assert kda == kdb and np.allclose(dEa, dEb, rtol=1e-13)
+        assert abs(a.energy() - b.energy()) <= 1e-13 * abs(b.energy())
+        assert np.abs(a.get_P() - b.get_P()).max() <= 1e-13
+        a.close()
+        b.close()
+    finally:
+        E.emin_nccl_comm_destroy(comm)
+
+
 # ---------------------------------------------------------------------------
 # full BASELINE sizes, in the configuration bench.py times
 # ---------------------------------------------------------------------------
