@@ -97,6 +97,10 @@ struct emin_ctx_s {
   int graph_k = -1;
   int graph_prof = 0;
   // profiling
+  cudaGraphExec_t graph_prof_exec = nullptr;   // iteration graph with 6 event-record nodes
+  cudaGraph_t graph_prof_src = nullptr;        // its source graph (owns the node handles)
+  cudaGraphNode_t prof_node[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t prof_pending = 0;                    // iterations recorded, not yet folded
   int profiling = 0;
   std::vector<cudaEvent_t> ev;
   double prof_ms[4] = {0, 0, 0, 0};

@@ -379,9 +379,9 @@ int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, 
     launch_scalar_masked(c, mode, X, X2, out, s);
     return mode == MM_ITER ? scalar_iter_grid(c) : grid;
   }
-  if (c->kernel_path == 2 && mode == MM_ITER) {
+  if (c->kernel_path == 2) {
     const NodalPlan* np = static_cast<const NodalPlan*>(c->nodal);
-    launch_nodal_iter(c, np, X, out, s);
+    launch_nodal(c, np, mode, X, X2, out, s);
     return nodal_grid(c, np);
   }
   const int mc = c->max_row <= 32 ? 1 : c->max_row <= 64 ? 2 : 4;
@@ -470,9 +470,9 @@ emin_status emin_finish_r0(emin_ctx c) {
   return EMIN_OK;
 }
 
-static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev) {
+static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev, int external) {
   auto rec = [&](int t) {
-    if (ev) cudaEventRecord(ev[t], s);
+    if (ev) cudaEventRecordWithFlags(ev[t], s, external ? cudaEventRecordExternal : cudaEventRecordDefault);
   };
   rec(0);
   launch_stage(c, 1, s);
@@ -492,25 +492,79 @@ static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev) {
 
 // One iteration captured as a CUDA graph (5 kernel nodes, cheap to
 // instantiate per context); emin_iterate(k) launches it k times.
-static emin_status build_graph(emin_ctx c) {
-  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
-  if (!c->cap_stream) EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-  cudaStream_t s = c->cap_stream;
-  EMIN_CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  enqueue_iteration(c, s, nullptr);
-  cudaGraph_t g;
-  EMIN_CUDA_TRY(c, cudaStreamEndCapture(s, &g));
-  cudaError_t e = cudaGraphInstantiate(&c->graph, g, 0);
-  cudaGraphDestroy(g);
-  EMIN_CUDA_TRY(c, e);
-  c->graph_k = 1;
-  return EMIN_OK;
-}
-
 // process-wide pool of timing events (profiling mode)
 static std::vector<cudaEvent_t>& event_pool() {
   static std::vector<cudaEvent_t> pool;
   return pool;
+}
+
+// One iteration captured as a CUDA graph (5 kernel nodes, cheap to
+// instantiate per context); emin_iterate(k) launches it k times.  The
+// profiling variant adds 6 event-record nodes around the kernels; before each
+// launch their events are re-pointed (cudaGraphExecEventRecordNodeSetEvent)
+// to fresh events of the pool, so k launches leave 6k timestamps and no
+// synchronisation is needed until emin_kernel_times reads them.
+static emin_status build_graph(emin_ctx c, int prof) {
+  cudaGraphExec_t& ge = prof ? c->graph_prof_exec : c->graph;
+  if (ge) { cudaGraphExecDestroy(ge); ge = nullptr; }
+  if (!c->cap_stream) EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t>& ev = event_pool();
+  while (prof && ev.size() < 6) {
+    cudaEvent_t e;
+    EMIN_CUDA_TRY(c, cudaEventCreate(&e));
+    ev.push_back(e);
+  }
+  cudaStream_t s = c->cap_stream;
+  EMIN_CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  enqueue_iteration(c, s, prof ? ev.data() : nullptr, prof ? 1 : 0);
+  cudaGraph_t g;
+  EMIN_CUDA_TRY(c, cudaStreamEndCapture(s, &g));
+  if (prof) {
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    for (int t = 0; t < 6; ++t) c->prof_node[t] = nullptr;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      cudaGraphNodeGetType(nd, &ty);
+      if (ty != cudaGraphNodeTypeEventRecord) continue;
+      cudaEvent_t e;
+      cudaGraphEventRecordNodeGetEvent(nd, &e);
+      for (int t = 0; t < 6; ++t)
+        if (e == ev[t]) c->prof_node[t] = nd;
+    }
+  }
+  cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  if (prof) {
+    // the event-record node handles stay valid only while their graph lives
+    if (c->graph_prof_src) cudaGraphDestroy(c->graph_prof_src);
+    c->graph_prof_src = g;
+  } else {
+    cudaGraphDestroy(g);
+  }
+  EMIN_CUDA_TRY(c, e);
+  return EMIN_OK;
+}
+
+// fold the recorded iterations into the per-class totals (synchronises)
+static emin_status fold_profile(emin_ctx c) {
+  if (!c->prof_pending) return EMIN_OK;
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  std::vector<cudaEvent_t>& ev = event_pool();
+  for (int64_t it = 0; it < c->prof_pending; ++it) {
+    cudaEvent_t* e = &ev[6 * (it + 1)];
+    float t[5];
+    for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&t[j], e[j], e[j + 1]);
+    c->prof_ms[0] += t[0];
+    c->prof_ms[1] += t[2];
+    c->prof_ms[2] += t[3];
+    c->prof_ms[3] += t[1] + t[4];
+    c->prof_launches[0] += 1; c->prof_launches[1] += 1; c->prof_launches[2] += 1;
+    c->prof_launches[3] += 2;
+  }
+  c->prof_pending = 0;
+  return EMIN_OK;
 }
 
 static emin_status ensure_hist(emin_ctx c, int64_t need) {
@@ -524,7 +578,8 @@ static emin_status ensure_hist(emin_ctx c, int64_t need) {
   }
   c->dE_hist = nh;
   c->dE_cap = cap;
-  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // it captured the old pointer
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }   // they captured the old pointer
+  if (c->graph_prof_exec) { cudaGraphExecDestroy(c->graph_prof_exec); c->graph_prof_exec = nullptr; }
   return EMIN_OK;
 }
 
@@ -536,38 +591,34 @@ extern "C" emin_status emin_iterate(emin_ctx c, int32_t k, int32_t* k_done, doub
   emin_status st = ensure_hist(c, c->k_launched + k);
   if (st != EMIN_OK) return st;
   EMIN_CUDA_TRY(c, cudaMemsetAsync(&c->st->k_call, 0, sizeof(int32_t), c->stream));
-  std::vector<cudaEvent_t>& ev = event_pool();
   if (c->profiling) {
-    // direct launches with CUDA events between the kernels (on this stream)
-    while (ev.size() < (size_t)6 * k) {
+    if (!c->graph_prof_exec) {
+      st = build_graph(c, 1);
+      if (st != EMIN_OK) return st;
+    }
+    std::vector<cudaEvent_t>& ev = event_pool();
+    const size_t need = (size_t)6 * (c->prof_pending + k + 1);
+    while (ev.size() < need) {
       cudaEvent_t e;
       EMIN_CUDA_TRY(c, cudaEventCreate(&e));
       ev.push_back(e);
     }
-    for (int it = 0; it < k; ++it) enqueue_iteration(c, c->stream, &ev[6 * it]);
+    for (int it = 0; it < k; ++it) {
+      cudaEvent_t* e = &ev[6 * (c->prof_pending + 1)];
+      for (int t = 0; t < 6; ++t)
+        if (c->prof_node[t]) EMIN_CUDA_TRY(c, cudaGraphExecEventRecordNodeSetEvent(c->graph_prof_exec, c->prof_node[t], e[t]));
+      EMIN_CUDA_TRY(c, cudaGraphLaunch(c->graph_prof_exec, c->stream));
+      c->prof_pending += 1;
+    }
   } else {
     if (!c->graph) {
-      st = build_graph(c);
+      st = build_graph(c, 0);
       if (st != EMIN_OK) return st;
     }
     for (int it = 0; it < k; ++it) EMIN_CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
   }
   c->launches += 5 * (int64_t)k;
   c->k_launched += k;
-  if (c->profiling) {
-    EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    for (int it = 0; it < k; ++it) {
-      cudaEvent_t* e = &ev[6 * it];
-      float t[5];
-      for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&t[j], e[j], e[j + 1]);
-      c->prof_ms[0] += t[0];
-      c->prof_ms[1] += t[2];
-      c->prof_ms[2] += t[3];
-      c->prof_ms[3] += t[1] + t[4];
-      c->prof_launches[0] += 1; c->prof_launches[1] += 1; c->prof_launches[2] += 1;
-      c->prof_launches[3] += 2;
-    }
-  }
   if (k_done || dE) {
     DevState h;
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(&h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
@@ -675,6 +726,7 @@ extern "C" emin_status emin_get_layout(emin_ctx c, int64_t* wptr, int32_t* wcol,
 
 extern "C" emin_status emin_set_profiling(emin_ctx c, int32_t on) {
   if (!c) return EMIN_ERR_ARG;
+  fold_profile(c);
   c->profiling = on ? 1 : 0;
   for (int j = 0; j < 4; ++j) { c->prof_ms[j] = 0.0; c->prof_launches[j] = 0; }
   return EMIN_OK;
@@ -682,6 +734,10 @@ extern "C" emin_status emin_set_profiling(emin_ctx c, int32_t on) {
 
 extern "C" emin_status emin_kernel_times(emin_ctx c, double* ms, int64_t* launches) {
   if (!c) return EMIN_ERR_ARG;
+  {
+    emin_status st = fold_profile(c);
+    if (st != EMIN_OK) return st;
+  }
   for (int j = 0; j < 4; ++j) {
     if (ms) ms[j] = c->prof_ms[j];
     if (launches) launches[j] = c->prof_launches[j];
@@ -709,6 +765,8 @@ void emin_free_all(emin_ctx c) {
 extern "C" void emin_destroy(emin_ctx c) {
   if (!c) return;
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->graph_prof_exec) cudaGraphExecDestroy(c->graph_prof_exec);
+  if (c->graph_prof_src) cudaGraphDestroy(c->graph_prof_src);
   emin_free_all(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;

@@ -39,7 +39,8 @@ struct ScalarPlan {
   int use_pipe = 0, pipe_grid = 0, rec_cap = 0, rows_cap = 0;   // TMA-pipelined persistent kernel
   uint32_t pipe_smem = 0;
   struct WinHdr* whdr = nullptr; // [nwin] window headers
-  int variant = 0;               // per-iteration kernel: 0 hdr, 1 win, 2 tile, 3 pipe
+  int variant = 0;               // per-iteration kernel: 0 hdr, 1 win, 2 tile, 3 pipe, 4 mask
+  uint16_t* emask = nullptr;     // [nnzW] matching records per W entry (variant 4)
 };
 
 // decode the window: rows [r0, r1), base entry, this lane's row and position
@@ -75,6 +76,9 @@ __device__ __forceinline__ WinLane decode_window(const int64_t* __restrict__ wpt
   w.act = lane < w.nent;
   return w;
 }
+
+// forward declaration (defined below)
+struct WinHdr;
 
 // sum of v over the lane's row (segmented inclusive scan, then the row's
 // last lane broadcasts); identical in every lane of the row
@@ -129,8 +133,159 @@ __global__ void k_plan_headers(const int64_t* __restrict__ wptr, const int32_t* 
   }
 }
 
-// y^ = Pi K y (nv = 1) on precomputed window headers, next header prefetched
+// per W entry: bit q set if record q of the entry's A_FF row matches the
+// entry's column (setup; thread per row, rows with <= 16 A_FF entries)
+__global__ void k_plan_emask(DevView v, const SpEnt* __restrict__ A, uint16_t* __restrict__ emask, int32_t* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v.nF; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = v.wptr[i];
+    const int nj = (int)(v.wptr[i + 1] - b);
+    const int64_t qb = v.affptr[i];
+    const int nq = (int)(v.affptr[i + 1] - qb);
+    if (nq > 16) atomicExch(bad, 1);
+    for (int t = 0; t < nj; ++t) {
+      uint32_t m = 0;
+      for (int q = 0; q < nq && q < 16; ++q)
+        if (((A[qb + q].pm >> (4 * t)) & 0xFu) != 0xFu) m |= 1u << q;
+      emask[b + t] = (uint16_t)m;
+    }
+  }
+}
+
+// y^ = Pi K y (nv = 1): window headers (ALU decode), per-entry match masks
+// (only the ~3.5 matching records of the row are visited, in A order, four
+// loads in flight), row sums of q.g through shared memory (fixed order, no
+// shuffles).
+__global__ void __launch_bounds__(256, 8)
+k_spgemm_mask(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__ hdr, int64_t nwin,
+              const uint16_t* __restrict__ emask, const double* __restrict__ X, double* __restrict__ out,
+              double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  const int4* H4 = reinterpret_cast<const int4*>(hdr);
+  int4 hv = (w < nwin) ? H4[w] : make_int4(0, 0, 0, 0);
+  while (w < nwin) {
+    const int64_t wn = w + nw;
+    const int4 hn = (wn < nwin) ? H4[wn] : make_int4(0, 0, 0, 0);
+    if (hv.w > 0) {                                   // warp-uniform
+      WinHdr h;
+      h.r0 = hv.x; h.base = hv.y; h.head = (uint32_t)hv.z; h.nent = hv.w;
+      const WinLane L = decode_hdr(h, lane);
+      const int64_t i = (int64_t)h.r0 + L.rloc;
+      const int64_t e = (int64_t)h.base + lane;
+      const int64_t qb = v.affptr[i];
+      uint32_t mask = L.act ? emask[e] : 0u;
+      const double qv = L.act ? v.Q[e] : 0.0;
+      const double xo = L.act ? X[e] : 0.0;
+      const unsigned sh4 = 4u * (unsigned)(L.pos & 7);
+      double acc = 0.0;
+      while (mask) {
+        int qa[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          qa[u] = mask ? __ffs(mask) - 1 : -1;
+          mask &= mask - 1u;
+        }
+        SpEnt en[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (qa[u] >= 0) en[u] = A[qb + qa[u]];
+        double yv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (qa[u] >= 0) yv[u] = X[(int64_t)en[u].ybase + ((en[u].pm >> sh4) & 0xFu)];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (qa[u] >= 0) acc = fma(en[u].a, yv[u], acc);
+      }
+      // Pi_B (nv = 1): row sum of q.g in a fixed order through shared memory
+      s_qa[wib][lane] = qv * acc;
+      __syncwarp();
+      double dot = 0.0;
+      for (int p = 0; p < L.rowlen; ++p) dot += s_qa[wib][L.rowbeg + p];
+      __syncwarp();
+      if (L.act) {
+        const double g = acc - qv * dot;
+        out[e] = g;
+        part = fma(xo, g, part);
+      }
+    }
+    hv = hn;
+    w = wn;
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// y^ = Pi K y (nv = 1), window kernel with fewer warp collectives: the
+// window decode derives row starts / lengths from the head bitmask by bit
+// arithmetic (2 shuffles + 1 OR-reduction), the row projection sums q.g
+// through shared memory in a fixed order (no shuffle scan).
 __global__ void __launch_bounds__(256)
+k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict__ rowstart, int64_t nwin,
+              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part = 0.0;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int r0 = rowstart[w];
+    const int nrows = rowstart[w + 1] - r0;
+    if (nrows == 0) continue;                          // warp-uniform
+    const int myptr = (lane <= nrows) ? (int)v.wptr[r0 + lane] : 0;
+    const int base = __shfl_sync(0xffffffffu, myptr, 0);
+    const int nent = __shfl_sync(0xffffffffu, myptr, nrows) - base;
+    const unsigned H = __reduce_or_sync(0xffffffffu, (lane < nrows) ? (1u << (unsigned)(myptr - base)) : 0u);
+    const bool act = lane < nent;
+    const int l = act ? lane : nent - 1;
+    const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+    const unsigned hu = H & upto;
+    const int rloc = __popc(hu) - 1;
+    const int rowbeg = 31 - __clz(hu);
+    const unsigned after = H & ~upto;
+    const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+    const int pos = lane - rowbeg;
+    const int i = r0 + rloc;
+    const int e = base + lane;
+    const int qb = (int)v.affptr[i], qe = (int)v.affptr[i + 1];
+    const double qv = act ? v.Q[e] : 0.0;
+    const double xo = act ? X[e] : 0.0;
+    double acc = 0.0;
+    if (act) {
+      const unsigned sh4 = 4u * (unsigned)pos;
+#pragma unroll 4
+      for (int q = qb; q < qe; ++q) {
+        const SpEnt en = A[q];
+        const unsigned s = (en.pm >> sh4) & 0xFu;
+        if (s != 0xFu) acc = fma(en.a, X[en.ybase + (int)s], acc);
+      }
+    }
+    s_qa[wib][lane] = qv * acc;
+    __syncwarp();
+    double dot = 0.0;
+    for (int p = 0; p < rowlen; ++p) dot += s_qa[wib][rowbeg + p];
+    __syncwarp();
+    if (act) {
+      const double g = acc - qv * dot;
+      out[e] = g;
+      part = fma(xo, g, part);
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// y^ = Pi K y (nv = 1) on precomputed window headers, next header prefetched
+__global__ void __launch_bounds__(256, 8)
 k_spgemm_hdr(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__ hdr, int64_t nwin,
              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
@@ -139,25 +294,29 @@ k_spgemm_hdr(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__ 
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   double part = 0.0;
-  WinHdr h = (w < nwin) ? hdr[w] : WinHdr{0, 0, 0u, 0};
+  // 32-bit indices throughout (the scalar path has nnz(W), nnz(A_FF) < 2^31)
+  const int4* H4 = reinterpret_cast<const int4*>(hdr);
+  int4 h = (w < nwin) ? H4[w] : make_int4(0, 0, 0, 0);
   while (w < nwin) {
     const int64_t wn = w + nw;
-    const WinHdr hn = (wn < nwin) ? hdr[wn] : WinHdr{0, 0, 0u, 0};
-    if (h.nent > 0) {                                 // warp-uniform
-      const WinLane L = decode_hdr(h, lane);
-      const int64_t i = (int64_t)h.r0 + L.rloc;
-      const int64_t e = (int64_t)h.base + lane;
-      const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
+    const int4 hn = (wn < nwin) ? H4[wn] : make_int4(0, 0, 0, 0);
+    if (h.w > 0) {                                    // warp-uniform
+      WinHdr hh;
+      hh.r0 = h.x; hh.base = h.y; hh.head = (uint32_t)h.z; hh.nent = h.w;
+      const WinLane L = decode_hdr(hh, lane);
+      const int i = h.x + L.rloc;
+      const int e = h.y + lane;
+      const int qb = (int)v.affptr[i], qe = (int)v.affptr[i + 1];
       const double qv = L.act ? v.Q[e] : 0.0;
       const double xo = L.act ? X[e] : 0.0;
       double acc = 0.0;
       if (L.act) {
         const unsigned sh4 = 4u * (unsigned)L.pos;
 #pragma unroll 4
-        for (int64_t q = qb; q < qe; ++q) {
+        for (int q = qb; q < qe; ++q) {
           const SpEnt en = A[q];
           const unsigned s = (en.pm >> sh4) & 0xFu;
-          if (s != 0xFu) acc = fma(en.a, X[(int64_t)en.ybase + s], acc);
+          if (s != 0xFu) acc = fma(en.a, X[en.ybase + (int)s], acc);
         }
       }
       const double dot = row_sum(qv * acc, L);
@@ -808,10 +967,29 @@ static inline int select_fast_path(emin_ctx c) {
   c->launches += 1;
   // per-iteration kernel variant (EMIN_SPGEMM=hdr|win|tile|pipe; default hdr)
   const char* var = getenv("EMIN_SPGEMM");
-  p.variant = 0;
+  p.variant = 5;   // default: win2 (fastest measured, profiles/r01/spgemm_variants_c3.log)
+  if (var && !strcmp(var, "hdr")) p.variant = 0;
   if (var && !strcmp(var, "win")) p.variant = 1;
   if (var && !strcmp(var, "tile")) p.variant = 2;
   if (var && !strcmp(var, "pipe")) p.variant = 3;
+  if (var && !strcmp(var, "mask")) p.variant = 4;
+  if (var && !strcmp(var, "win2")) p.variant = 5;
+  if (p.variant == 4) {
+    int32_t* bad = nullptr;
+    if (cudaMallocAsync((void**)&p.emask, sizeof(uint16_t) * std::max<int64_t>(c->nnzW, 1), s) != cudaSuccess ||
+        cudaMallocAsync((void**)&bad, sizeof(int32_t), s) != cudaSuccess) {
+      p.variant = 1;
+    } else {
+      cudaMemsetAsync(bad, 0, sizeof(int32_t), s);
+      k_plan_emask<<<SM * 8, 256, 0, s>>>(c->view(), p.ent, p.emask, bad);
+      c->launches += 1;
+      int32_t hb = 0;
+      cudaMemcpyAsync(&hb, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaFreeAsync(bad, s);
+      cudaStreamSynchronize(s);
+      if (hb) p.variant = 1;
+    }
+  }
   if (p.tile_smem <= 160 * 1024) {
     p.use_tiles = 1;
     cudaFuncSetAttribute(k_spgemm_tile<MM_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
@@ -869,6 +1047,12 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
       case 0:
         k_spgemm_hdr<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, X, out, c->partials);
         return;
+      case 4:
+        k_spgemm_mask<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, p.emask, X, out, c->partials);
+        return;
+      case 5:
+        k_spgemm_win2<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+        return;
       case 1:
         k_spgemm_scalar<MM_ITER><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
                                                                 c->partials);
@@ -922,6 +1106,7 @@ static inline void free_fast_path(emin_ctx c) {
   if (f->sc.ent) cudaFreeAsync(f->sc.ent, c->stream);
   if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
   if (f->sc.whdr) cudaFreeAsync(f->sc.whdr, c->stream);
+  if (f->sc.emask) cudaFreeAsync(f->sc.emask, c->stream);
   delete f;
   c->fast = nullptr;
 }

@@ -15,6 +15,9 @@
 // of three times.
 #pragma once
 #include "emin_internal.cuh"
+#include "masked.cuh"
+#include <cstdlib>
+#include <cstring>
 
 struct NodalBlk {      // one per A_FF 3x3 block (I,K)
   int32_t ybase;       // wptr[3K]: first W entry of the neighbour node
@@ -36,7 +39,7 @@ __global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_l
     const int64_t r = 3 * n;
     const int64_t wb = v.wptr[r];
     const int64_t len = v.wptr[r + 1] - wb;
-    bool good = (len % 3 == 0) && len > 0 && len <= 3 * 32;
+    bool good = (len % 3 == 0) && len > 0 && len <= 64;     // two 32-lane chunks per node
     for (int d = 1; d < 3 && good; ++d) good = (v.wptr[r + d + 1] - v.wptr[r + d]) == len;
     for (int64_t t = 0; t < len && good; ++t) {
       const int32_t c = v.wcol[wb + t];
@@ -45,7 +48,7 @@ __global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_l
     }
     const int64_t ab = v.affptr[r];
     const int64_t alen = v.affptr[r + 1] - ab;
-    good = good && (alen % 3 == 0);
+    good = good && (alen % 3 == 0) && (alen / 3 <= 27);      // <= 27 blocks (staged kernel)
     for (int d = 1; d < 3 && good; ++d) good = (v.affptr[r + d + 1] - v.affptr[r + d]) == alen;
     for (int64_t q = 0; q < alen && good; ++q) {
       const int32_t k = v.affcol[ab + q];
@@ -179,6 +182,140 @@ k_spgemm_nodal(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __res
   if (threadIdx.x == 0) partials[blockIdx.x] = tot;
 }
 
+// Staged variant: the warp first copies its node's A chunk (9 nb doubles),
+// block records and byte map into shared memory with coalesced loads (all
+// independent), then the block loop only gathers y (two blocks per round so
+// that six gathers per lane are in flight).
+constexpr int ND_WARPS = 8;
+constexpr int ND_MAXB = 27;      // blocks per node (27-point node stencil)
+constexpr int ND_MAXJ = 32;      // C nodes per pattern row (3|J| <= 96 entries -> 2 chunks of 32 needs |J| <= 21)
+
+template <int NV, int MODE>
+__global__ void __launch_bounds__(ND_WARPS * 32)
+k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
+                 const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
+                 const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+                 double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_a[ND_WARPS][ND_MAXB * 9];
+  __shared__ NodalBlk s_b[ND_WARPS][ND_MAXB];
+  __shared__ uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
+  if (MODE == MM_ITER && v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  auto xval = [&](int64_t idx) -> double { return MODE == MM_ENERGY ? X[idx] + X2[idx] : X[idx]; };
+  double part = 0.0;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t r = 3 * n;
+    const int64_t wb = v.wptr[r];
+    const int n3 = (int)(v.wptr[r + 1] - wb);
+    const int nJ = n3 / 3;
+    const int64_t ab = v.affptr[r];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int64_t po = pmoff[n];
+    // ---- stage the node's data (re-ordered A chunk: block-major 3x3)
+    const int rs = 3 * nb;
+    for (int k = lane; k < 9 * nb; k += 32) {
+      const int d = k / rs, rem = k - d * rs, b = rem / 3, e = rem - 3 * b;
+      s_a[wib][b * 9 + d * 3 + e] = __ldg(v.affval + ab + k);
+    }
+    for (int k = lane; k < nb; k += 32) s_b[wib][k] = blk[bb + k];
+    for (int k = lane; k < nb * nJ; k += 32) s_pm[wib][k] = pm8[po + k];
+    const int t0 = lane, t1 = lane + 32;
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
+    double q0[NV], q1[NV];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      q0[m] = (MODE != MM_ENERGY && act0) ? v.Q[(wb + t0) * NV + m] : 0.0;
+      q1[m] = (MODE != MM_ENERGY && act1) ? v.Q[(wb + t1) * NV + m] : 0.0;
+    }
+    __syncwarp();
+    double acc0[3] = {0.0, 0.0, 0.0}, acc1[3] = {0.0, 0.0, 0.0};
+#pragma unroll 2
+    for (int b = 0; b < nb; ++b) {
+      const NodalBlk k = s_b[wib][b];
+      const int p0 = act0 ? s_pm[wib][b * nJ + s0] : 0xFF;
+      const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
+      double y0[3] = {0.0, 0.0, 0.0}, y1[3] = {0.0, 0.0, 0.0};
+      if (p0 != 0xFF) {
+#pragma unroll
+        for (int e = 0; e < 3; ++e) y0[e] = xval((int64_t)k.ybase + e * k.nK3 + 3 * p0 + b0);
+      }
+      if (p1 != 0xFF) {
+#pragma unroll
+        for (int e = 0; e < 3; ++e) y1[e] = xval((int64_t)k.ybase + e * k.nK3 + 3 * p1 + b1);
+      }
+      const double* a = &s_a[wib][b * 9];
+      if (p0 != 0xFF) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) acc0[d] = fma(a[d * 3 + e], y0[e], acc0[d]);
+      }
+      if (p1 != 0xFF) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) acc1[d] = fma(a[d * 3 + e], y1[e], acc1[d]);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int64_t ro = wb + (int64_t)d * n3;
+      double g0 = acc0[d], g1 = acc1[d];
+      if (MODE != MM_ITER) {          // C-identity term A(i, c_j) (setup / energy only)
+        const int64_t fb = v.afcptr[r + d], fe = v.afcptr[r + d + 1];
+        double f0 = 0.0, f1 = 0.0;
+        if (act0) {
+          const int32_t j = v.wcol[ro + t0];
+          for (int64_t q = fb; q < fe; ++q) if (v.afccol[q] == j) { f0 = v.afcval[q]; break; }
+        }
+        if (act1) {
+          const int32_t j = v.wcol[ro + t1];
+          for (int64_t q = fb; q < fe; ++q) if (v.afccol[q] == j) { f1 = v.afcval[q]; break; }
+        }
+        if (MODE == MM_ENERGY) {
+          if (act0) part = fma(xval(ro + t0), g0 + 2.0 * f0, part);
+          if (act1) part = fma(xval(ro + t1), g1 + 2.0 * f1, part);
+          continue;
+        }
+        g0 += f0;
+        g1 += f1;
+      }
+      // Pi_B with the node's Q (twice for r0, see masked.cuh)
+#pragma unroll
+      for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
+        double dots[NV];
+#pragma unroll
+        for (int m = 0; m < NV; ++m) dots[m] = warp_sum(fma(q0[m], g0, q1[m] * g1));
+        double s0v = 0.0, s1v = 0.0;
+#pragma unroll
+        for (int m = 0; m < NV; ++m) {
+          s0v = fma(q0[m], dots[m], s0v);
+          s1v = fma(q1[m], dots[m], s1v);
+        }
+        g0 -= s0v;
+        g1 -= s1v;
+      }
+      if (act0) {
+        if (MODE == MM_ITER) { out[ro + t0] = g0; part = fma(X[ro + t0], g0, part); }
+        else out[ro + t0] = -g0;
+      }
+      if (act1) {
+        if (MODE == MM_ITER) { out[ro + t1] = g1; part = fma(X[ro + t1], g1, part); }
+        else out[ro + t1] = -g1;
+      }
+    }
+    __syncwarp();
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
 // ---- host side ------------------------------------------------------------
 template <typename T>
 static cudaError_t nd_alloc(T** p, int64_t n, cudaStream_t s) {
@@ -233,14 +370,33 @@ static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((p->nFn + 7) / 8, (int64_t)SM * 16));
 }
 
-static inline void launch_nodal_iter(emin_ctx c, const NodalPlan* p, const double* X, double* out, cudaStream_t s) {
+static inline void launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const double* X, const double* X2,
+                                double* out, cudaStream_t s) {
   const DevView v = c->view();
   const int g = nodal_grid(c, p);
-  switch (c->nv) {
+  const char* var = getenv("EMIN_NODAL");
+  if (mode == MM_ITER && var && !strcmp(var, "plain")) {
+    switch (c->nv) {
 #define NV_CASE(N) case N: k_spgemm_nodal<N><<<g, 256, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, out, c->partials); break;
-    NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+      NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
 #undef NV_CASE
+    }
+    return;
   }
+#define NV_CASE(N)                                                                                                  \
+  case N:                                                                                                           \
+    if (mode == MM_ITER)                                                                                            \
+      k_spgemm_nodal_s<N, MM_ITER><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, \
+                                                              out, c->partials);                                  \
+    else if (mode == MM_R0)                                                                                         \
+      k_spgemm_nodal_s<N, MM_R0><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2,   \
+                                                            out, c->partials);                                    \
+    else                                                                                                            \
+      k_spgemm_nodal_s<N, MM_ENERGY><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X,   \
+                                                                X2, out, c->partials);                            \
+    break;
+  switch (c->nv) { NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8) }
+#undef NV_CASE
 }
 
 static inline void free_nodal_path(emin_ctx c, NodalPlan*& p) {

@@ -1,6 +1,8 @@
 // setup.cu -- emin_setup: validation, F-row index preparation, Alg. 2
 // (EMIN_SetUp) per F row, r0 and E0 (start of Alg. 3).
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -478,6 +480,18 @@ static emin_status fail(emin_ctx ctx, emin_status st, const std::string& msg) {
   return st;
 }
 
+// EMIN_TRACE=1: synchronise and print the elapsed host time of each setup phase
+struct SetupTrace {
+  bool on = getenv("EMIN_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(cudaStream_t s, const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[emin setup] %8.3f ms  %s\n", ms, what);
+  }
+};
+
 #define SETUP_TRY(call)                                                                \
   do {                                                                                 \
     cudaError_t e_ = (call);                                                           \
@@ -514,6 +528,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
+  SetupTrace trace;
   ctx = new emin_ctx_s();
   ctx->opts = *opts;
   ctx->stream = (cudaStream_t)opts->stream;
@@ -577,6 +592,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   }
   ctx->nnzP = nnzP;
 
+  trace.mark(s, "inputs staged");
   // ---- coarse numbering: cidx = exclusive scan of is_coarse (global)
   int64_t *cidx, *scratch, *totals;
   SETUP_TRY(dalloc(&cidx, n_global + 1, s)); temps.push_back(cidx);
@@ -599,6 +615,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   ctx->nFh = nF;
   ctx->n_crows = h_ce - h_cb;
 
+  trace.mark(s, "coarse numbering");
   // ---- validation + counts
   int64_t *cnt_ff, *cnt_fc, *cnt_w;
   double* dcc;
@@ -648,6 +665,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     return fail(ctx, st, buf);
   }
   ctx->max_row = h_err[1];
+  trace.mark(s, "validation");
 
   // ---- multi-GPU: halo rows (F rows of other ranks referenced by A_FF)
   if (ctx->dist) {
@@ -683,6 +701,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   }
   const int64_t Wh = ctx->nnzWh;
 
+  trace.mark(s, "row pointers");
   // ---- fill
   double* what;
   SETUP_TRY(dalloc(&ctx->wcol, Wh, s));
@@ -714,6 +733,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     if (st != EMIN_OK) { tmp_free(); return fail(ctx, st, ctx->last_error); }
   }
 
+  trace.mark(s, "fill");
   // ---- sum of the C-row diagonal (energy constant, Eq. trInc tr(A_cc))
   SETUP_TRY(dalloc(&ctx->partials, SM * 32, s));
   ctx->n_partials = SM * 32;
@@ -728,6 +748,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     if (pst != EMIN_OK) { tmp_free(); return fail(ctx, pst, ctx->last_error); }
   }
 
+  trace.mark(s, "kernel plan");
   // ---- Alg. 2
   // w0, dw, y carry the halo tail (values of other ranks' rows)
   SETUP_TRY(dalloc(&ctx->Q, W * nv + 2, s));
@@ -761,6 +782,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     if (st1 != EMIN_OK || st2 != EMIN_OK) { tmp_free(); return fail(ctx, EMIN_ERR_NCCL, ctx->last_error); }
   }
 
+  trace.mark(s, "Alg. 2");
   // ---- r0 = -Pi (A P0)|F and E0 = tr(P0^T A P0)
   double h_sum_cc = 0.0;
   SETUP_TRY(cudaMemcpyAsync(&h_sum_cc, dsum, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -776,6 +798,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   tmp_free();
   if (st != EMIN_OK) return fail(ctx, st, ctx->last_error);
   SETUP_TRY(cudaStreamSynchronize(s));
+  trace.mark(s, "r0, E0 (done)");
   *out = ctx;
   return EMIN_OK;
 }

@@ -73,6 +73,30 @@ def test_parity_small(name, size, k):
     assert rep["n_svd_rows"] == o.n_svd and rep["n_frozen_rows"] == o.n_frozen
 
 
+@pytest.mark.parametrize("name,size,path", [("3", 12, 1), ("2b", 10, 1), ("4", 4, 2), ("5", 8, 2)])
+@pytest.mark.parametrize("variant", ["win", "mask", "tile", "hdr", "pipe"])
+def test_kernel_paths_agree(name, size, path, variant, monkeypatch):
+    """The specialised kernels (scalar window/mask/tile/header variants,
+    nodal 3x3) against the generic warp-per-row kernel and the oracle."""
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    if path == 2 and variant != "win":
+        pytest.skip("variants apply to the scalar path")
+    prob = make_config(name, size=size)
+    monkeypatch.setenv("EMIN_SPGEMM", variant)
+    fast = Emin.from_problem(prob)
+    assert fast.report()["kernel_path"] == path
+    monkeypatch.setenv("EMIN_FORCE_GENERIC", "1")
+    gen = Emin.from_problem(prob)
+    assert gen.report()["kernel_path"] == 0
+    kf, dEf = fast.iterate(25)
+    kg, dEg = gen.iterate(25)
+    assert kf == kg and np.allclose(dEf, dEg, rtol=1e-9)
+    Pf, Pg = fast.get_P(), gen.get_P()
+    assert np.abs(Pf - Pg).max() <= 1e-10 * np.abs(Pg).max()
+    assert abs(fast.energy() - gen.energy()) <= 1e-12 * abs(gen.energy())
+
+
 @pytest.mark.parametrize("name,size", [("1b", None), ("4", 3)])
 def test_parity_with_post_projection(name, size):
     from workloads.problems import make_config
