@@ -67,6 +67,7 @@ struct emin_ctx_s {
   int32_t nv = 1;
   int32_t max_row = 0;
   int32_t group = 1;           // lanes per row in the streaming stages
+  int32_t stage_vec = 0;       // 16-byte vectorised streaming stages (EMIN_STAGE=v)
   int32_t kernel_path = 0;
   // device arrays (owned by ctx)
   int64_t *wptr = nullptr, *affptr = nullptr, *afcptr = nullptr, *pofs = nullptr, *cofs = nullptr;

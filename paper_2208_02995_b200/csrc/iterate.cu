@@ -216,6 +216,106 @@ k_stage2_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict
   }
 }
 
+// Vectorised variants: each thread moves pairs of entries with 16-byte loads
+// and stores (double2 / int2); the odd tail entry is handled by thread 0.
+__global__ void __launch_bounds__(256, 4)
+k_stage1_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ dinv, double* __restrict__ r,
+           const double* __restrict__ yb, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = st->pend;
+  const double ap = st->alpha_pend;
+  const int64_t np = v.nnzW >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  const double2* yb2 = reinterpret_cast<const double2*>(yb);
+  const int2* er2 = reinterpret_cast<const int2*>(erow);
+  double part = 0.0;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += 2 * stride) {
+    double2 rv[2];
+    double dv[4], iv[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < np) {
+        rv[u] = r2[p];
+        if (pend) {
+          const double2 b = yb2[p];
+          rv[u].x = rv[u].x - ap * b.x;
+          rv[u].y = rv[u].y - ap * b.y;
+        }
+        const int2 i = er2[p];
+        dv[2 * u] = v.d[i.x]; iv[2 * u] = dinv[i.x];
+        dv[2 * u + 1] = v.d[i.y]; iv[2 * u + 1] = dinv[i.y];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < np) {
+        if (pend) reinterpret_cast<double2*>(r)[p] = rv[u];
+        part = fma(rv[u].x, jacobi_div(rv[u].x, dv[2 * u], iv[2 * u]), part);
+        part = fma(rv[u].y, jacobi_div(rv[u].y, dv[2 * u + 1], iv[2 * u + 1]), part);
+      }
+    }
+  }
+  if ((v.nnzW & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t e = v.nnzW - 1;
+    double x = r[e];
+    if (pend) { x = x - ap * yb[e]; r[e] = x; }
+    part = fma(x, jacobi_div(x, v.d[erow[e]], dinv[erow[e]]), part);
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256, 4)
+k_stage2_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ dinv,
+           const double* __restrict__ r, double* __restrict__ y, double* __restrict__ dw) {
+  const DevState* st = v.st;
+  const int stopped = st->stopped;
+  const int pendw = st->pendw;
+  if (stopped && !pendw) return;
+  const double ap = st->alpha_pend;
+  const double beta = st->beta;
+  const bool first = (st->k_total == 0);
+  const int64_t np = v.nnzW >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double2* y2 = reinterpret_cast<double2*>(y);
+  double2* dw2 = reinterpret_cast<double2*>(dw);
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  const int2* er2 = reinterpret_cast<const int2*>(erow);
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+    const double2 yo = y2[p];
+    if (pendw) {
+      double2 d = dw2[p];
+      d.x = d.x + ap * yo.x;
+      d.y = d.y + ap * yo.y;
+      dw2[p] = d;
+    }
+    if (!stopped) {
+      const double2 rv = r2[p];
+      const int2 i = er2[p];
+      const double z0 = jacobi_div(rv.x, v.d[i.x], dinv[i.x]);
+      const double z1 = jacobi_div(rv.y, v.d[i.y], dinv[i.y]);
+      double2 yn;
+      yn.x = first ? z0 : z0 + beta * yo.x;
+      yn.y = first ? z1 : z1 + beta * yo.y;
+      y2[p] = yn;
+    }
+  }
+  if ((v.nnzW & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t e = v.nnzW - 1;
+    const double yo = y[e];
+    if (pendw) dw[e] = dw[e] + ap * yo;
+    if (!stopped) {
+      const double z = jacobi_div(r[e], v.d[erow[e]], dinv[erow[e]]);
+      y[e] = first ? z : z + beta * yo;
+    }
+  }
+}
+
 __global__ void k_recip(const double* __restrict__ d, int64_t n, double* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = 1.0 / d[i];
@@ -354,6 +454,13 @@ void launch_stage2_g(emin_ctx c, cudaStream_t s) {
 }
 void launch_stage(emin_ctx c, int which, cudaStream_t s) {
   if (!c->opts.project_after_jacobi) {
+    if (c->stage_vec) {
+      if (which == 1)
+        k_stage1_v<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->yb, c->partials);
+      else
+        k_stage2_v<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->y, c->dw);
+      return;
+    }
     if (which == 1)
       k_stage1_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->yb, c->partials);
     else
@@ -421,6 +528,8 @@ emin_status emin_plan(emin_ctx c) {
     k_recip<<<SM * 4, 256, 0, c->stream>>>(c->d, c->nF, c->dinv);
     c->launches += 2;
     c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * 8));
+    const char* sv = getenv("EMIN_STAGE");
+    c->stage_vec = (sv && !strcmp(sv, "e")) ? 0 : 1;   // 16-byte stages unless EMIN_STAGE=e
   }
   c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
   if (c->kernel_path == 1) c->grid_red = std::max(c->grid_red, scalar_iter_grid(c));

@@ -41,6 +41,8 @@ struct ScalarPlan {
   struct WinHdr* whdr = nullptr; // [nwin] window headers
   int variant = 0;               // per-iteration kernel: 0 hdr, 1 win, 2 tile, 3 pipe, 4 mask
   uint16_t* emask = nullptr;     // [nnzW] matching records per W entry (variant 4)
+  int32_t* rowstart3 = nullptr;  // 64-entry windows (variant 6)
+  int64_t nwin3 = 0;
 };
 
 // decode the window: rows [r0, r1), base entry, this lane's row and position
@@ -279,6 +281,86 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
       out[e] = g;
       part = fma(xo, g, part);
     }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// win3: windows of up to 64 entries (two per lane: positions lane and
+// lane + 32), so the per-window decode is amortised over twice the entries
+// and every lane has two independent gather chains in flight.  Rows per
+// window <= 63; head mask 64-bit.
+__global__ void __launch_bounds__(256)
+k_spgemm_win3(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict__ rowstart, int64_t nwin,
+              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][64];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part = 0.0;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int r0 = rowstart[w];
+    const int nrows = rowstart[w + 1] - r0;
+    if (nrows == 0) continue;                          // warp-uniform
+    const int p0 = (lane <= nrows) ? (int)v.wptr[r0 + lane] : 0;
+    const int p1 = (lane + 32 <= nrows) ? (int)v.wptr[r0 + lane + 32] : 0;
+    const int base = __shfl_sync(0xffffffffu, p0, 0);
+    const int endp = (nrows < 32) ? __shfl_sync(0xffffffffu, p0, nrows) : __shfl_sync(0xffffffffu, p1, nrows - 32);
+    const int nent = endp - base;
+    const unsigned h0 = __reduce_or_sync(0xffffffffu, (lane < nrows && p0 - base < 32) ? (1u << (unsigned)(p0 - base)) : 0u) |
+                        __reduce_or_sync(0xffffffffu, (lane + 32 < nrows && p1 - base < 32) ? (1u << (unsigned)(p1 - base)) : 0u);
+    const unsigned h1 = __reduce_or_sync(0xffffffffu, (lane < nrows && p0 - base >= 32) ? (1u << (unsigned)(p0 - base - 32)) : 0u) |
+                        __reduce_or_sync(0xffffffffu, (lane + 32 < nrows && p1 - base >= 32) ? (1u << (unsigned)(p1 - base - 32)) : 0u);
+    const uint64_t H = ((uint64_t)h1 << 32) | h0;
+    double acc[2], qv[2], xo[2];
+    int rb[2], rl[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int t = lane + 32 * u;
+      const bool act = t < nent;
+      const int l = act ? t : nent - 1;
+      const uint64_t upto = (l == 63) ? ~0ull : ((2ull << l) - 1ull);
+      const uint64_t hu = H & upto;
+      const int rloc = __popcll(hu) - 1;
+      rb[u] = 63 - __clzll(hu);
+      const uint64_t after = H & ~upto;
+      rl[u] = (after ? (__ffsll(after) - 1) : nent) - rb[u];
+      const int pos = t - rb[u];
+      const int i = r0 + rloc;
+      const int e = base + t;
+      qv[u] = act ? v.Q[e] : 0.0;
+      xo[u] = act ? X[e] : 0.0;
+      acc[u] = 0.0;
+      if (act) {
+        const int qb = (int)v.affptr[i], qe = (int)v.affptr[i + 1];
+        const unsigned sh4 = 4u * (unsigned)pos;
+        double a = 0.0;
+#pragma unroll 4
+        for (int q = qb; q < qe; ++q) {
+          const SpEnt en = A[q];
+          const unsigned s = (en.pm >> sh4) & 0xFu;
+          if (s != 0xFu) a = fma(en.a, X[en.ybase + (int)s], a);
+        }
+        acc[u] = a;
+      }
+      s_qa[wib][t] = qv[u] * acc[u];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int t = lane + 32 * u;
+      double dot = 0.0;
+      for (int p = 0; p < rl[u]; ++p) dot += s_qa[wib][rb[u] + p];
+      if (t < nent) {
+        const double g = acc[u] - qv[u] * dot;
+        out[base + t] = g;
+        part = fma(xo[u], g, part);
+      }
+    }
+    __syncwarp();
   }
   const double tot = block_sum(part, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = tot;
@@ -974,6 +1056,17 @@ static inline int select_fast_path(emin_ctx c) {
   if (var && !strcmp(var, "pipe")) p.variant = 3;
   if (var && !strcmp(var, "mask")) p.variant = 4;
   if (var && !strcmp(var, "win2")) p.variant = 5;
+  if (var && !strcmp(var, "win3")) p.variant = 6;
+  if (p.variant == 6) {
+    const int S3 = std::min(63, 65 - c->max_row);
+    p.nwin3 = (c->nnzW + S3 - 1) / S3;
+    if (cudaMallocAsync((void**)&p.rowstart3, sizeof(int32_t) * (p.nwin3 + 1), s) != cudaSuccess) {
+      p.variant = 5;
+    } else {
+      k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, S3, p.nwin3, p.rowstart3);
+      c->launches += 1;
+    }
+  }
   if (p.variant == 4) {
     int32_t* bad = nullptr;
     if (cudaMallocAsync((void**)&p.emask, sizeof(uint16_t) * std::max<int64_t>(c->nnzW, 1), s) != cudaSuccess ||
@@ -1053,6 +1146,9 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
       case 5:
         k_spgemm_win2<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
         return;
+      case 6:
+        k_spgemm_win3<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart3, p.nwin3, X, out, c->partials);
+        return;
       case 1:
         k_spgemm_scalar<MM_ITER><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
                                                                 c->partials);
@@ -1107,6 +1203,7 @@ static inline void free_fast_path(emin_ctx c) {
   if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
   if (f->sc.whdr) cudaFreeAsync(f->sc.whdr, c->stream);
   if (f->sc.emask) cudaFreeAsync(f->sc.emask, c->stream);
+  if (f->sc.rowstart3) cudaFreeAsync(f->sc.rowstart3, c->stream);
   delete f;
   c->fast = nullptr;
 }
