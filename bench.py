@@ -332,6 +332,11 @@ def main():
         it_ms.append(ia.elapsed_time(ib))
     E.emin_destroy(h)
     it_ms_med = statistics.median(it_ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([it_ms_med], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        it_ms_med = float(t.item())
 
     # ---- roofline of the dominant kernel (masked SpGEMM), from the timed region
     peak, peak_src = measured_peak()
@@ -381,6 +386,9 @@ def main():
                "ms_per_step": e_ms / n_e2e, "steps": n_e2e}
 
     if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return 0
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

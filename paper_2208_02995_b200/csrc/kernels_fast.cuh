@@ -263,18 +263,24 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
     const double xo = act ? X[e] : 0.0;
     double acc = 0.0;
     if (act) {
+      // record qb is the diagonal A(i,i) (k_plan_entries): its y value is the
+      // lane's own entry, no gather
+      const int4* A4 = reinterpret_cast<const int4*>(A);
+      acc = __hiloint2double(__ldg(&A4[qb]).y, __ldg(&A4[qb]).x) * xo;
       const unsigned sh4 = 4u * (unsigned)pos;
 #pragma unroll 4
-      for (int q = qb; q < qe; ++q) {
-        const SpEnt en = A[q];
-        const unsigned s = (en.pm >> sh4) & 0xFu;
-        if (s != 0xFu) acc = fma(en.a, X[en.ybase + (int)s], acc);
+      for (int q = qb + 1; q < qe; ++q) {
+        const int4 en = __ldg(&A4[q]);              // one 16-byte load: {a, ybase, pm}
+        const unsigned s = ((unsigned)en.w >> sh4) & 0xFu;
+        if (s != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)s], acc);
       }
     }
     s_qa[wib][lane] = qv * acc;
     __syncwarp();
     double dot = 0.0;
-    for (int p = 0; p < rowlen; ++p) dot += s_qa[wib][rowbeg + p];
+#pragma unroll
+    for (int p = 0; p < 8; ++p)                       // |J_i| <= 8 on the scalar path
+      if (p < rowlen) dot += s_qa[wib][rowbeg + p];
     __syncwarp();
     if (act) {
       const double g = acc - qv * dot;
@@ -981,7 +987,14 @@ __global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
     int32_t ji[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) ji[t] = (t < nj) ? v.wcol[b + t] : -1;
-    for (int64_t q = v.affptr[i] + lg; q < v.affptr[i + 1]; q += 8) {
+    // the diagonal record goes first (win2 takes its term from the lane's
+    // own y value); the others keep A's column order
+    const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
+    int64_t qd = qb;
+    for (int64_t q = qb; q < qe; ++q)
+      if (v.affcol[q] == (int32_t)i) { qd = q; break; }
+    for (int64_t q = qb + lg; q < qe; q += 8) {
+      const int64_t dst = (q == qd) ? qb : (q < qd ? q + 1 : q);
       const int32_t k = v.affcol[q];
       const int64_t kb = v.wptr[k];
       const int nk = (int)(v.wptr[k + 1] - kb);
@@ -998,7 +1011,7 @@ __global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
       e.a = v.affval[q];
       e.ybase = (int32_t)kb;
       e.pm = pm;
-      ent[q] = e;
+      ent[dst] = e;
     }
   }
 }

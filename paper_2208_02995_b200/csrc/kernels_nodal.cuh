@@ -191,7 +191,7 @@ constexpr int ND_MAXB = 27;      // blocks per node (27-point node stencil)
 constexpr int ND_MAXJ = 32;      // C nodes per pattern row (3|J| <= 96 entries -> 2 chunks of 32 needs |J| <= 21)
 
 template <int NV, int MODE>
-__global__ void __launch_bounds__(ND_WARPS * 32)
+__global__ void __launch_bounds__(ND_WARPS * 32, 4)
 k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
                  const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
                  const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
@@ -227,12 +227,6 @@ k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __r
     const int t0 = lane, t1 = lane + 32;
     const bool act0 = t0 < n3, act1 = t1 < n3;
     const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
-    double q0[NV], q1[NV];
-#pragma unroll
-    for (int m = 0; m < NV; ++m) {
-      q0[m] = (MODE != MM_ENERGY && act0) ? v.Q[(wb + t0) * NV + m] : 0.0;
-      q1[m] = (MODE != MM_ENERGY && act1) ? v.Q[(wb + t1) * NV + m] : 0.0;
-    }
     __syncwarp();
     double acc0[3] = {0.0, 0.0, 0.0}, acc1[3] = {0.0, 0.0, 0.0};
 #pragma unroll 2
@@ -262,6 +256,14 @@ k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __r
 #pragma unroll
           for (int e = 0; e < 3; ++e) acc1[d] = fma(a[d * 3 + e], y1[e], acc1[d]);
       }
+    }
+    // Q of the node (row 3n) loaded after the block loop: keeps the loop's
+    // register footprint small (occupancy)
+    double q0[NV], q1[NV];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      q0[m] = (MODE != MM_ENERGY && act0) ? v.Q[(wb + t0) * NV + m] : 0.0;
+      q1[m] = (MODE != MM_ENERGY && act1) ? v.Q[(wb + t1) * NV + m] : 0.0;
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {

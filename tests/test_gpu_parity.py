@@ -146,6 +146,22 @@ def test_tau_stop():
     assert g.report()["stop_reason"] == 3
 
 
+@pytest.mark.parametrize("name,size,tau", [("3", 12, 0.1), ("4", 3, 0.1), ("1b", None, 1e-3), ("5", 8, 0.05)])
+def test_tau_production_mode(name, size, tau):
+    """the paper's relRed stop dE_k < tau dE_1 (Eq. relRed,
+    P:705-712; tau = 0.1 default) stops GPU and oracle at the
+    same step with the same P."""
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    g, o = _pair(prob, 200, tau=tau)
+    kd, dE = g.iterate(200)
+    kdo, dEo = o.iterate(200)
+    assert kd == kdo and kd < 200
+    assert g.report()["stop_reason"] == 3 and o.stop_reason == "tau"
+    assert np.abs(g.get_P() - o.get_P()).max() <= P_TOL * np.abs(o.get_P()).max()
+    assert dE[-1] >= tau * dE[0]
+
+
 def test_rank_deficient_rows_take_svd_branch():
     """nv = 2 with B = [1, 1]: every M_i has rank 1 -> SVD branch, k_i = 1."""
     from workloads.problems import make_config
