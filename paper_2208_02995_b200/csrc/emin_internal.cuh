@@ -55,6 +55,7 @@ struct DevView {
   const double* d;       // A(i,i) per owned F row
   const double* Q;       // [nnzW * nv] row-major per entry, zero padded
   DevState* st;
+  int32_t pingpong;      // L2 ping-pong traversal order (see iterate.cu)
 };
 
 struct emin_ctx_s {
@@ -69,6 +70,7 @@ struct emin_ctx_s {
   int32_t group = 1;           // lanes per row in the streaming stages
   int32_t stage_vec = 0;       // 16-byte vectorised streaming stages (EMIN_STAGE=v)
   int32_t kernel_path = 0;
+  int32_t pingpong = 0;        // alternate traversal directions (EMIN_PINGPONG)
   // device arrays (owned by ctx)
   int64_t *wptr = nullptr, *affptr = nullptr, *afcptr = nullptr, *pofs = nullptr, *cofs = nullptr;
   uint8_t* isc_own = nullptr;  // is_coarse of the owned rows
@@ -112,6 +114,7 @@ struct emin_ctx_s {
     v.nF = nF; v.nFh = nFh; v.nnzW = nnzW; v.nv = nv;
     v.wptr = wptr; v.wcol = wcol; v.affptr = affptr; v.affcol = affcol; v.affval = affval;
     v.afcptr = afcptr; v.afccol = afccol; v.afcval = afcval; v.d = d; v.Q = Q; v.st = st;
+    v.pingpong = pingpong;
     return v;
   }
 };

@@ -232,6 +232,9 @@ k_stage1_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict
   const double2* yb2 = reinterpret_cast<const double2*>(yb);
   const int2* er2 = reinterpret_cast<const int2*>(erow);
   double part = 0.0;
+  // L2 ping-pong: odd steps sweep backwards, so the first pairs read are
+  // the last ones the previous kernel wrote (still in the 126 MB L2)
+  const bool rev = v.pingpong && (st->k_total & 1);
   for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += 2 * stride) {
     double2 rv[2];
     double dv[4], iv[4];
@@ -239,13 +242,14 @@ k_stage1_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict
     for (int u = 0; u < 2; ++u) {
       const int64_t p = p0 + u * stride;
       if (p < np) {
-        rv[u] = r2[p];
+        const int64_t pp = rev ? np - 1 - p : p;
+        rv[u] = r2[pp];
         if (pend) {
-          const double2 b = yb2[p];
+          const double2 b = yb2[pp];
           rv[u].x = rv[u].x - ap * b.x;
           rv[u].y = rv[u].y - ap * b.y;
         }
-        const int2 i = er2[p];
+        const int2 i = er2[pp];
         dv[2 * u] = v.d[i.x]; iv[2 * u] = dinv[i.x];
         dv[2 * u + 1] = v.d[i.y]; iv[2 * u + 1] = dinv[i.y];
       }
@@ -254,7 +258,7 @@ k_stage1_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict
     for (int u = 0; u < 2; ++u) {
       const int64_t p = p0 + u * stride;
       if (p < np) {
-        if (pend) reinterpret_cast<double2*>(r)[p] = rv[u];
+        if (pend) reinterpret_cast<double2*>(r)[rev ? np - 1 - p : p] = rv[u];
         part = fma(rv[u].x, jacobi_div(rv[u].x, dv[2 * u], iv[2 * u]), part);
         part = fma(rv[u].y, jacobi_div(rv[u].y, dv[2 * u + 1], iv[2 * u + 1]), part);
       }
@@ -286,7 +290,9 @@ k_stage2_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict
   double2* dw2 = reinterpret_cast<double2*>(dw);
   const double2* r2 = reinterpret_cast<const double2*>(r);
   const int2* er2 = reinterpret_cast<const int2*>(erow);
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+  const bool rev = v.pingpong && !(st->k_total & 1);   // opposite to stage I (L2 ping-pong)
+  for (int64_t p1 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p1 < np; p1 += stride) {
+    const int64_t p = rev ? np - 1 - p1 : p1;
     const double2 yo = y2[p];
     if (pendw) {
       double2 d = dw2[p];
@@ -530,6 +536,8 @@ emin_status emin_plan(emin_ctx c) {
     c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * 8));
     const char* sv = getenv("EMIN_STAGE");
     c->stage_vec = (sv && !strcmp(sv, "e")) ? 0 : 1;   // 16-byte stages unless EMIN_STAGE=e
+    const char* pp = getenv("EMIN_PINGPONG");
+    c->pingpong = (c->stage_vec && !(pp && !strcmp(pp, "0"))) ? 1 : 0;
   }
   c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
   if (c->kernel_path == 1) c->grid_red = std::max(c->grid_red, scalar_iter_grid(c));

@@ -43,7 +43,45 @@ struct ScalarPlan {
   uint16_t* emask = nullptr;     // [nnzW] matching records per W entry (variant 4)
   int32_t* rowstart3 = nullptr;  // 64-entry windows (variant 6)
   int64_t nwin3 = 0;
+  struct Win4Hdr* w4hdr = nullptr; // [nwin] 32-byte window headers (variants 7, 8)
+  int4* w6hdr = nullptr;           // [nwin + 1] 16-byte window headers (variant 9)
+  int4* ell = nullptr;             // [nF * ellW] ELL-padded records (variant 10)
+  int4* w7hdr = nullptr;           // [nwin] {r0, ebase, ehead, nent} (variant 10)
+  int ellW = 0;
+  int w8grid = 0;                  // resident CTAs of win8 (variant 11)
 };
+
+// ---- shared-memory / mbarrier / bulk-copy helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 
 // decode the window: rows [r0, r1), base entry, this lane's row and position
 struct WinLane {
@@ -239,7 +277,9 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double part = 0.0;
-  for (int64_t w = gw; w < nwin; w += nw) {
+  const bool rev = v.pingpong && (v.st->k_total & 1);   // same direction as stage I (L2 ping-pong)
+  for (int64_t w1 = gw; w1 < nwin; w1 += nw) {
+    const int64_t w = rev ? nwin - 1 - w1 : w1;
     const int r0 = rowstart[w];
     const int nrows = rowstart[w + 1] - r0;
     if (nrows == 0) continue;                          // warp-uniform
@@ -371,6 +411,704 @@ k_spgemm_win3(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
   const double tot = block_sum(part, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = tot;
 }
+
+// ---------------------------------------------------------------------------
+// win4 / win5: the window kernel without a dependent-load chain.
+//
+// win2 walks rowstart[w] -> wptr[r0..] -> affptr[i] -> A records -> y: four
+// dependent DRAM round trips before the first gather, ~28 times per warp,
+// which (not bandwidth) bounds it (profiles/r01: 52 % issue-active, DRAM at
+// 44 % of peak).  Here a 32-byte header per window (built once at setup)
+// holds everything the lane decode needs, so after the header every load
+// of the window -- its A records (one coalesced 16-byte load per lane,
+// staged in shared memory), the lanes' Q and y entries, the row pointers --
+// is independent, and only the y gathers depend on the records.  PIPE
+// additionally issues the next window's loads (and the header after it)
+// before the current window's gathers.
+// Arithmetic and summation order are those of win2 (bitwise equal).
+// ---------------------------------------------------------------------------
+struct Win4Hdr {
+  int32_t r0, ebase, abase;
+  uint32_t ehead;            // bit p: a row starts at window entry p
+  int32_t nent, nrows, nrec, pad;
+};
+constexpr int W4_REC = 64;   // records staged per pass (2 per lane)
+
+__global__ void k_plan_win4(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
+                            const int32_t* __restrict__ rowstart, int64_t nwin, Win4Hdr* __restrict__ hdr) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r0 = rowstart[w], r1 = rowstart[w + 1];
+    Win4Hdr h;
+    h.r0 = r0;
+    h.nrows = r1 - r0;
+    h.ebase = (int32_t)(r1 > r0 ? wptr[r0] : 0);
+    h.nent = (int32_t)(r1 > r0 ? wptr[r1] - wptr[r0] : 0);
+    h.abase = (int32_t)(r1 > r0 ? affptr[r0] : 0);
+    h.nrec = (int32_t)(r1 > r0 ? affptr[r1] - affptr[r0] : 0);
+    uint32_t head = 0;
+    for (int32_t r = r0; r < r1; ++r) head |= 1u << (unsigned)(wptr[r] - h.ebase);
+    h.ehead = head;
+    h.pad = 0;
+    hdr[w] = h;
+  }
+}
+
+struct Win4Loads {
+  int4 ra, rb;     // records abase + lane, abase + 32 + lane (first pass)
+  double qv, xo;   // Q and y of the lane's entry
+  int ap;          // affptr[r0 + lane] - abase (lanes 0..nrows)
+};
+
+__device__ __forceinline__ Win4Loads win4_issue(const DevView& v, const int4* __restrict__ A4,
+                                                const double* __restrict__ X, const Win4Hdr& h, int lane) {
+  Win4Loads L;
+  const int4 z4 = make_int4(0, 0, 0, 0);
+  L.ra = lane < h.nrec ? __ldg(A4 + h.abase + lane) : z4;
+  L.rb = lane + 32 < h.nrec ? __ldg(A4 + h.abase + 32 + lane) : z4;
+  const bool act = lane < h.nent;
+  L.qv = act ? __ldg(v.Q + h.ebase + lane) : 0.0;
+  L.xo = act ? X[h.ebase + lane] : 0.0;
+  L.ap = lane <= h.nrows ? (int)(__ldg(v.affptr + h.r0 + lane) - h.abase) : 0;
+  return L;
+}
+
+template <bool PIPE>
+__global__ void __launch_bounds__(256, PIPE ? 3 : 4)
+k_spgemm_win4(DevView v, const int4* __restrict__ A4, const Win4Hdr* __restrict__ hdr, int64_t nwin,
+              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][32];
+  __shared__ int4 s_rec[8][W4_REC];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  // grid-stride over windows: all warps sweep one narrow front of rows, so
+  // the y rows a window gathers were touched by its neighbours moments ago
+  // (L2 hits); a contiguous run of windows per warp spreads the front over
+  // the whole matrix and measured 1.6x slower.
+  const Win4Hdr hz = {0, 0, 0, 0u, 0, 0, 0, 0};
+  Win4Hdr h = w < nwin ? hdr[w] : hz;
+  Win4Hdr hn = (PIPE && w + nw < nwin) ? hdr[w + nw] : hz;
+  Win4Loads cur = win4_issue(v, A4, X, h, lane);
+  while (w < nwin) {
+    Win4Loads nxt;
+    Win4Hdr hnn = hz;
+    if (PIPE) {
+      if (w + nw < nwin) nxt = win4_issue(v, A4, X, hn, lane);
+      if (w + 2 * nw < nwin) hnn = hdr[w + 2 * nw];
+    }
+    const int nent = h.nent, nrows = h.nrows, nrec = h.nrec;
+    if (nrows > 0) {                                   // warp-uniform
+      const unsigned H = h.ehead;
+      const bool act = lane < nent;
+      const int l = act ? lane : nent - 1;
+      const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+      const unsigned hu = H & upto;
+      const int rloc = __popc(hu) - 1;
+      const int rowbeg = 31 - __clz(hu);
+      const unsigned after = H & ~upto;
+      const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+      const unsigned sh4 = 4u * (unsigned)(lane - rowbeg);
+      const int qb = __shfl_sync(0xffffffffu, cur.ap, rloc);
+      const int qe = __shfl_sync(0xffffffffu, cur.ap, rloc + 1);
+      double acc = 0.0;
+      for (int p0 = 0; p0 < nrec; p0 += W4_REC) {      // warp-uniform; one pass unless nrec > 64
+        if (p0 > 0) {
+          __syncwarp();
+          const int4 z4 = make_int4(0, 0, 0, 0);
+          cur.ra = p0 + lane < nrec ? __ldg(A4 + h.abase + p0 + lane) : z4;
+          cur.rb = p0 + 32 + lane < nrec ? __ldg(A4 + h.abase + p0 + 32 + lane) : z4;
+        }
+        s_rec[wib][lane] = cur.ra;
+        s_rec[wib][lane + 32] = cur.rb;
+        __syncwarp();
+        if (act) {
+          int lo = max(qb, p0);
+          const int hi = min(qe, p0 + W4_REC);
+          if (lo == qb && lo < hi) {
+            // record qb is the diagonal A(i,i) (k_plan_entries): own y
+            const int4 en = s_rec[wib][qb - p0];
+            acc = __hiloint2double(en.y, en.x) * cur.xo;
+            ++lo;
+          }
+#pragma unroll 4
+          for (int q = lo; q < hi; ++q) {
+            const int4 en = s_rec[wib][q - p0];         // {a (lo, hi), ybase, pm}
+            const unsigned sidx = ((unsigned)en.w >> sh4) & 0xFu;
+            if (sidx != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)sidx], acc);
+          }
+        }
+      }
+      s_qa[wib][lane] = cur.qv * acc;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)                       // |J_i| <= 8 on the scalar path
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      __syncwarp();
+      if (act) {
+        const double g = acc - cur.qv * dot;
+        out[h.ebase + lane] = g;
+        part = fma(cur.xo, g, part);
+      }
+    }
+    w += nw;
+    if (PIPE) {
+      h = hn;
+      hn = hnn;
+      cur = nxt;
+    } else if (w < nwin) {
+      h = hdr[w];
+      cur = win4_issue(v, A4, X, h, lane);
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// ---------------------------------------------------------------------------
+// win6: win2's lane map and arithmetic, with the next window's data pulled
+// into L2 while the current window computes.
+//
+// win2 is latency bound (profiles/r01: 27 of 35 stall cycles per issued
+// instruction are long-scoreboard waits at 99 % occupancy): per window it
+// walks rowstart -> wptr -> affptr -> records -> y, four dependent DRAM
+// misses and one L2 hit.  Here a 16-byte header per window {r0, abase,
+// ebase, ehead} (nrows, nrec, nent are differences with the next header,
+// so lanes 0 and 1 load both in one 32-byte access) replaces the first two
+// steps, and the warp loads the header of its NEXT window one iteration
+// ahead and issues prefetch.global.L2 for that window's row pointers,
+// A records, Q and y entries before computing the current one.  The
+// remaining chain -- affptr -> records -> y -- then runs on L2 hits.
+// Registers stay at win2's level (no loads held across iterations).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pf_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// lanes [l0, l0 + nl) prefetch the 128-byte lines of [p, p + bytes), one each
+__device__ __forceinline__ void pf_lines(const void* p, size_t bytes, int lane, int l0, int nl) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const int nlines = bytes ? (int)(((a + bytes - 1) >> 7) - (a >> 7)) + 1 : 0;
+  const int j = lane - l0;
+  if (j >= 0 && j < nl && j < nlines) pf_l2(reinterpret_cast<const void*>(((a >> 7) + j) << 7));
+}
+
+__global__ void k_plan_win6(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
+                            const int32_t* __restrict__ rowstart, int64_t nwin, int4* __restrict__ hdr) {
+  // hdr[w] for w in [0, nwin]; hdr[nwin] is the end sentinel
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r0 = rowstart[w];
+    const int32_t r1 = (w < nwin) ? rowstart[w + 1] : r0;
+    uint32_t head = 0;
+    for (int32_t r = r0; r < r1; ++r) head |= 1u << (unsigned)(wptr[r] - wptr[r0]);
+    hdr[w] = make_int4(r0, (int32_t)affptr[r0], (int32_t)wptr[r0], (int32_t)head);
+  }
+}
+
+__global__ void __launch_bounds__(256, 6)
+k_spgemm_win6(DevView v, const int4* __restrict__ A4, const int4* __restrict__ hdr, int64_t nwin,
+              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  // lanes 0 and 1 hold headers w and w + 1 of the current window
+  int4 hc = (w < nwin && lane < 2) ? __ldg(hdr + w + lane) : make_int4(0, 0, 0, 0);
+  while (w < nwin) {
+    const int64_t wn = w + nw;
+    // next window's header pair (consumed next iteration)
+    const int4 hn = (wn < nwin && lane < 2) ? __ldg(hdr + wn + lane) : make_int4(0, 0, 0, 0);
+    const int r0 = __shfl_sync(0xffffffffu, hc.x, 0);
+    const int nrows = __shfl_sync(0xffffffffu, hc.x, 1) - r0;
+    const int abase = __shfl_sync(0xffffffffu, hc.y, 0);
+    const int base = __shfl_sync(0xffffffffu, hc.z, 0);
+    const int nent = __shfl_sync(0xffffffffu, hc.z, 1) - base;
+    const unsigned H = (unsigned)__shfl_sync(0xffffffffu, hc.w, 0);
+    if (nrows > 0) {                                   // warp-uniform
+      const bool act = lane < nent;
+      const int l = act ? lane : nent - 1;
+      const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+      const unsigned hu = H & upto;
+      const int rloc = __popc(hu) - 1;
+      const int rowbeg = 31 - __clz(hu);
+      const unsigned after = H & ~upto;
+      const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+      const int i = r0 + rloc;
+      const int e = base + lane;
+      const int qb = (int)v.affptr[i], qe = (int)v.affptr[i + 1];
+      const double qv = act ? v.Q[e] : 0.0;
+      const double xo = act ? X[e] : 0.0;
+      (void)abase;
+      double acc = 0.0;
+      if (act) {
+        acc = __hiloint2double(__ldg(&A4[qb]).y, __ldg(&A4[qb]).x) * xo;   // diagonal record first
+        const unsigned sh4 = 4u * (unsigned)(lane - rowbeg);
+#pragma unroll 4
+        for (int q = qb + 1; q < qe; ++q) {
+          const int4 en = __ldg(&A4[q]);
+          const unsigned s = ((unsigned)en.w >> sh4) & 0xFu;
+          if (s != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)s], acc);
+        }
+      }
+      s_qa[wib][lane] = qv * acc;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      __syncwarp();
+      if (act) {
+        const double g = acc - qv * dot;
+        out[e] = g;
+        part = fma(xo, g, part);
+      }
+    }
+    // prefetch the next window into L2 (its header pair arrived meanwhile)
+    if (wn < nwin) {
+      const int nr0 = __shfl_sync(0xffffffffu, hn.x, 0);
+      const int nr1 = __shfl_sync(0xffffffffu, hn.x, 1);
+      const int nab = __shfl_sync(0xffffffffu, hn.y, 0);
+      const int nae = __shfl_sync(0xffffffffu, hn.y, 1);
+      const int neb = __shfl_sync(0xffffffffu, hn.z, 0);
+      const int nee = __shfl_sync(0xffffffffu, hn.z, 1);
+      if (nr1 > nr0) {
+        // 128-byte lines of: records [nab, nae), Q and y [neb, nee), affptr [nr0, nr1]
+        pf_lines(A4 + nab, (size_t)(nae - nab) * 16, lane, 0, 16);
+        pf_lines(v.Q + neb, (size_t)(nee - neb) * 8, lane, 16, 4);
+        pf_lines(X + neb, (size_t)(nee - neb) * 8, lane, 20, 4);
+        pf_lines(v.affptr + nr0, (size_t)(nr1 - nr0 + 1) * 8, lane, 24, 4);
+      }
+    }
+    hc = hn;
+    w = wn;
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// ---------------------------------------------------------------------------
+// win7: ELL-padded A records.  Latency model of win2 (fits the measured
+// 117 us on config 3 to 10 %): a warp spends ~8200 cycles per window, seven
+// serialised memory round trips -- rowstart, wptr, affptr, two batches of
+// records, two batches of y gathers.  Here
+//  * row i's records sit at [W i, W i + W) (W = max A_FF row length <= 8,
+//    padding records never match: pm = 0xFFFFFFFF, a = 0), so no affptr;
+//  * a 16-byte window header {r0, ebase, ehead, nent}, loaded one window
+//    ahead, replaces rowstart / wptr;
+//  * all W records of the lane's row are loaded at once (full unroll), then
+//    all its gathers,
+// leaving two round trips per window (records, then y).  Same arithmetic and
+// order as win2 (diagonal first, then A's column order).
+// ---------------------------------------------------------------------------
+__global__ void k_rowlen_max(const int64_t* __restrict__ ptr, int64_t n, int32_t* out) {
+  int32_t m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (int32_t)(ptr[i + 1] - ptr[i]));
+  atomicMax(out, m);
+}
+
+__global__ void k_plan_ell(const int64_t* __restrict__ affptr, int64_t nF, int W, const int4* __restrict__ ent,
+                           int4* __restrict__ ell) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nF * W; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / W;
+    const int q = (int)(k - i * W);
+    const int64_t qb = affptr[i], qe = affptr[i + 1];
+    ell[k] = (qb + q < qe) ? ent[qb + q] : make_int4(0, 0, 0, (int)0xFFFFFFFFu);
+  }
+}
+
+__global__ void k_plan_win7(const int64_t* __restrict__ wptr, const int32_t* __restrict__ rowstart, int64_t nwin,
+                            int4* __restrict__ hdr) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r0 = rowstart[w], r1 = rowstart[w + 1];
+    uint32_t head = 0;
+    for (int32_t r = r0; r < r1; ++r) head |= 1u << (unsigned)(wptr[r] - wptr[r0]);
+    hdr[w] = make_int4(r0, (int32_t)wptr[r0], (int32_t)head, (int32_t)(wptr[r1] - wptr[r0]));
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256, 4)
+k_spgemm_win7(DevView v, const int4* __restrict__ ell, const int4* __restrict__ hdr, int64_t nwin,
+              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  int4 h = w < nwin ? __ldg(hdr + w) : make_int4(0, 0, 0, 0);
+  while (w < nwin) {
+    const int64_t wn = w + nw;
+    const int4 hn = wn < nwin ? __ldg(hdr + wn) : make_int4(0, 0, 0, 0);   // one window ahead
+    const int nent = h.w;
+    if (nent > 0) {                                     // warp-uniform
+      const unsigned H = (unsigned)h.z;
+      const bool act = lane < nent;
+      const int l = act ? lane : nent - 1;
+      const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+      const unsigned hu = H & upto;
+      const int rloc = __popc(hu) - 1;
+      const int rowbeg = 31 - __clz(hu);
+      const unsigned after = H & ~upto;
+      const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+      const int i = h.x + rloc;
+      const int e = h.y + lane;
+      const double qv = act ? v.Q[e] : 0.0;
+      const double xo = act ? X[e] : 0.0;
+      double acc = 0.0;
+      if (act) {
+        // three phases, so that no FMA waiting on a gather holds back the
+        // next load (in-order issue): (1) the {ybase, pm} halves of the W
+        // records, (2) all matching gathers, (3) the a halves (L1 hits: same
+        // lines as phase 1) and the FMAs in A's order
+        const int4* rec = ell + (int64_t)i * W;
+        const unsigned sh4 = 4u * (unsigned)(lane - rowbeg);
+        int yi[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) yi[q] = -1;
+#pragma unroll
+        for (int q = 1; q < W; ++q) {
+          const int2 ip = __ldg(reinterpret_cast<const int2*>(rec + q) + 1);
+          const unsigned s = ((unsigned)ip.y >> sh4) & 0xFu;
+          yi[q] = (s != 0xFu) ? ip.x + (int)s : -1;
+        }
+        // scheduling fences (empty asm): every gather address waits for all
+        // record loads, every FMA for all gathers -- ptxas otherwise places
+        // each load just before its consumer, serialising the round trips
+        asm volatile("" : "+r"(yi[1]), "+r"(yi[2]), "+r"(yi[3]), "+r"(yi[4]), "+r"(yi[5]), "+r"(yi[6]), "+r"(yi[7]));
+        double yv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) yv[q] = 0.0;
+#pragma unroll
+        for (int q = 1; q < W; ++q) yv[q] = (yi[q] >= 0) ? __ldg(X + yi[q]) : 0.0;
+        acc = __ldg(reinterpret_cast<const double*>(rec)) * xo;    // diagonal record first (own y)
+        asm volatile("" : "+d"(acc) : "d"(yv[1]), "d"(yv[2]), "d"(yv[3]), "d"(yv[4]), "d"(yv[5]), "d"(yv[6]), "d"(yv[7]));
+#pragma unroll
+        for (int q = 1; q < W; ++q)
+          if (yi[q] >= 0) acc = fma(__ldg(reinterpret_cast<const double*>(rec + q)), yv[q], acc);
+      }
+      s_qa[wib][lane] = qv * acc;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      __syncwarp();
+      if (act) {
+        const double g = acc - qv * dot;
+        out[e] = g;
+        part = fma(xo, g, part);
+      }
+    }
+    h = hn;
+    w = wn;
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// ---------------------------------------------------------------------------
+// win8: per-warp double-buffered cp.async staging.
+//
+// Measured (profiles/r01b): win2 runs at 99 % occupancy but only ~1 KB of
+// unique DRAM bytes in flight per SM-warp-window, because every lane holds
+// its row's records in registers (a 32-lane broadcast load of 512 register
+// bytes carries ~112 unique bytes); shortening the dependent chain in
+// registers (win4/win7) cost the same factor in occupancy.  Here the window's
+// A records, its lanes' Q and y entries and its row pointers are copied by
+// cp.async straight into shared memory -- no registers wait on them -- for
+// the NEXT window while the current one computes from the other buffer.
+// Per window the only exposed latency left is the y gathers (L2).
+// Header pairs as win6 ({r0, abase, ebase, ehead}; counts are differences
+// with the next header).  Arithmetic and order are win2's.
+// ---------------------------------------------------------------------------
+constexpr int W8_REC = 96;      // records staged per window (more: read from global)
+constexpr int W8_WARPS = 8;
+struct W8Buf {
+  int4 rec[W8_REC];
+  double q[32];
+  double x[32];
+  int64_t ap[33];
+  int64_t pad;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// header pair {r0, abase, ebase, ehead} of window w (lane 0) and w + 1 (lane 1)
+struct W8Win {
+  int r0, nrows, abase, nrec, ebase, nent;
+  unsigned head;
+};
+__device__ __forceinline__ W8Win w8_decode(int4 hp) {
+  W8Win d;
+  d.r0 = __shfl_sync(0xffffffffu, hp.x, 0);
+  d.nrows = __shfl_sync(0xffffffffu, hp.x, 1) - d.r0;
+  d.abase = __shfl_sync(0xffffffffu, hp.y, 0);
+  d.nrec = __shfl_sync(0xffffffffu, hp.y, 1) - d.abase;
+  d.ebase = __shfl_sync(0xffffffffu, hp.z, 0);
+  d.nent = __shfl_sync(0xffffffffu, hp.z, 1) - d.ebase;
+  d.head = (unsigned)__shfl_sync(0xffffffffu, hp.w, 0);
+  return d;
+}
+__device__ __forceinline__ void w8_issue(const W8Win& d, W8Buf* b, const DevView& v, const int4* __restrict__ A4,
+                                         const double* __restrict__ X, int lane) {
+  const int nr = min(d.nrec, W8_REC);
+  for (int j = lane; j < nr; j += 32) cp_async16(&b->rec[j], A4 + d.abase + j);
+  if (lane < d.nent) {
+    cp_async8(&b->q[lane], v.Q + d.ebase + lane);
+    cp_async8(&b->x[lane], X + d.ebase + lane);
+  }
+  if (lane <= d.nrows) cp_async8(&b->ap[lane], v.affptr + d.r0 + lane);
+}
+
+__global__ void __launch_bounds__(W8_WARPS * 32, 4)
+k_spgemm_win8(DevView v, const int4* __restrict__ A4, const int4* __restrict__ hdr, int64_t nwin,
+              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char w8_smem[];
+  __shared__ double sh[32];
+  __shared__ double s_qa[W8_WARPS][32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  W8Buf* bufs = reinterpret_cast<W8Buf*>(w8_smem) + 2 * wib;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  const int4 z4 = make_int4(0, 0, 0, 0);
+  int4 hc = (w < nwin && lane < 2) ? __ldg(hdr + w + lane) : z4;
+  int4 hn = (w + nw < nwin && lane < 2) ? __ldg(hdr + w + nw + lane) : z4;
+  W8Win cur = w8_decode(hc);
+  if (w < nwin) w8_issue(cur, &bufs[0], v, A4, X, lane);
+  cp_async_commit();
+  int bi = 0;
+  while (w < nwin) {
+    const int64_t wn = w + nw;
+    const W8Win nxt = w8_decode(hn);
+    if (wn < nwin) w8_issue(nxt, &bufs[bi ^ 1], v, A4, X, lane);
+    cp_async_commit();
+    const int4 hnn = (wn + nw < nwin && lane < 2) ? __ldg(hdr + wn + nw + lane) : z4;
+    cp_async_wait<1>();                                // this window's group has landed
+    __syncwarp();
+    const W8Buf* b = &bufs[bi];
+    if (cur.nrows > 0) {                               // warp-uniform
+      const int nent = cur.nent;
+      const unsigned H = cur.head;
+      const bool act = lane < nent;
+      const int l = act ? lane : nent - 1;
+      const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+      const unsigned hu = H & upto;
+      const int rloc = __popc(hu) - 1;
+      const int rowbeg = 31 - __clz(hu);
+      const unsigned after = H & ~upto;
+      const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+      const double qv = act ? b->q[lane] : 0.0;
+      const double xo = act ? b->x[lane] : 0.0;
+      double acc = 0.0;
+      if (act) {
+        const int qb = (int)(b->ap[rloc] - cur.abase), qe = (int)(b->ap[rloc + 1] - cur.abase);
+        const unsigned sh4 = 4u * (unsigned)(lane - rowbeg);
+        if (qe <= W8_REC) {
+          const int4 d0 = b->rec[qb];
+          acc = __hiloint2double(d0.y, d0.x) * xo;     // diagonal record first (own y)
+          // all gathers of a chunk are issued before the first FMA that
+          // consumes one (in-order issue: an FMA waiting on its gather would
+          // otherwise hold back the next gather -- one L2 round trip per
+          // record, the measured bottleneck of win2/win8 v1)
+          for (int q0 = qb + 1; q0 < qe; q0 += 8) {
+            double yv[8];
+            unsigned okm = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              // {ybase, pm} half of the record only (8-byte shared load)
+              const int2 ip = reinterpret_cast<const int2*>(&b->rec[min(q0 + j, W8_REC - 1)])[1];
+              const unsigned sidx = ((unsigned)ip.y >> sh4) & 0xFu;
+              const bool ok = (q0 + j < qe) && sidx != 0xFu;
+              okm |= ok ? (1u << j) : 0u;
+              yv[j] = ok ? __ldg(X + ip.x + (int)sidx) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (okm & (1u << j))
+                acc = fma(reinterpret_cast<const double*>(&b->rec[min(q0 + j, W8_REC - 1)])[0], yv[j], acc);
+          }
+        } else {                                        // records beyond the staged part
+          const int4* g = A4 + cur.abase;
+          const int4 d0 = __ldg(g + qb);
+          acc = __hiloint2double(d0.y, d0.x) * xo;
+          for (int q = qb + 1; q < qe; ++q) {
+            const int4 en = __ldg(g + q);
+            const unsigned s = ((unsigned)en.w >> sh4) & 0xFu;
+            if (s != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)s], acc);
+          }
+        }
+      }
+      s_qa[wib][lane] = qv * acc;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      if (act) {
+        const double g = acc - qv * dot;
+        out[cur.ebase + lane] = g;
+        part = fma(xo, g, part);
+      }
+    }
+    __syncwarp();                                      // buffer bi is free for window w + 2 nw
+    cur = nxt;
+    hn = hnn;
+    bi ^= 1;
+    w = wn;
+  }
+  cp_async_wait<0>();
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+static inline size_t w8_smem_bytes() { return sizeof(W8Buf) * 2 * W8_WARPS; }
+
+// ---------------------------------------------------------------------------
+// win9: win8 with the staging done by the bulk-copy (TMA) engine.  win8 cut
+// the long-scoreboard stalls from 27 to 6.6 per issued instruction, but its
+// per-lane cp.async code raised the instruction count 53 % (87 M vs 57 M on
+// config 3).  Here one lane issues four cp.async.bulk copies per window
+// (records; Q, y and affptr spans widened to 16-byte alignment -- every
+// context array has 64 bytes of tail padding) on a per-warp mbarrier, and
+// the gathers of a row are batched as in win8.
+// ---------------------------------------------------------------------------
+struct W9Buf {
+  int4 rec[W8_REC];
+  double q[34];
+  double x[34];
+  int64_t ap[34];
+};
+
+__global__ void __launch_bounds__(W8_WARPS * 32, 4)
+k_spgemm_win9(DevView v, const int4* __restrict__ A4, const int4* __restrict__ hdr, int64_t nwin,
+              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char w9_smem[];
+  __shared__ double sh[32];
+  __shared__ double s_qa[W8_WARPS][32];
+  __shared__ __align__(8) uint64_t s_bar[W8_WARPS][2];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  W9Buf* bufs = reinterpret_cast<W9Buf*>(w9_smem) + 2 * wib;
+  if (lane == 0) {
+    mbar_init(&s_bar[wib][0], 1);
+    mbar_init(&s_bar[wib][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  const int4 z4 = make_int4(0, 0, 0, 0);
+  auto issue = [&](const W8Win& d, W9Buf* b, uint64_t* bar) {
+    // lane 0 only
+    const int nr = min(d.nrec, W8_REC);
+    const int e0 = d.ebase & ~1, e1 = (d.ebase + d.nent + 1) & ~1;
+    const int a0 = d.r0 & ~1, a1 = (d.r0 + d.nrows + 2) & ~1;
+    const uint32_t bytes = (uint32_t)(nr * 16 + 2 * (e1 - e0) * 8 + (a1 - a0) * 8);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, bytes);
+    if (nr) bulk_g2s(b->rec, A4 + d.abase, (uint32_t)(nr * 16), bar);
+    bulk_g2s(b->q, v.Q + e0, (uint32_t)((e1 - e0) * 8), bar);
+    bulk_g2s(b->x, X + e0, (uint32_t)((e1 - e0) * 8), bar);
+    bulk_g2s(b->ap, v.affptr + a0, (uint32_t)((a1 - a0) * 8), bar);
+  };
+  int4 hc = (w < nwin && lane < 2) ? __ldg(hdr + w + lane) : z4;
+  int4 hn = (w + nw < nwin && lane < 2) ? __ldg(hdr + w + nw + lane) : z4;
+  W8Win cur = w8_decode(hc);
+  if (w < nwin && lane == 0) issue(cur, &bufs[0], &s_bar[wib][0]);
+  int it = 0;
+  while (w < nwin) {
+    const int bi = it & 1;
+    const int64_t wn = w + nw;
+    const W8Win nxt = w8_decode(hn);
+    if (wn < nwin && lane == 0) issue(nxt, &bufs[bi ^ 1], &s_bar[wib][bi ^ 1]);
+    const int4 hnn = (wn + nw < nwin && lane < 2) ? __ldg(hdr + wn + nw + lane) : z4;
+    mbar_wait(&s_bar[wib][bi], (uint32_t)((it >> 1) & 1));
+    const W9Buf* b = &bufs[bi];
+    if (cur.nrows > 0) {                               // warp-uniform
+      const int nent = cur.nent;
+      const unsigned H = cur.head;
+      const bool act = lane < nent;
+      const int l = act ? lane : nent - 1;
+      const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+      const unsigned hu = H & upto;
+      const int rloc = __popc(hu) - 1;
+      const int rowbeg = 31 - __clz(hu);
+      const unsigned after = H & ~upto;
+      const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+      const int es = cur.ebase & 1, as = cur.r0 & 1;
+      const double qv = act ? b->q[es + lane] : 0.0;
+      const double xo = act ? b->x[es + lane] : 0.0;
+      double acc = 0.0;
+      if (act) {
+        const int qb = (int)(b->ap[as + rloc] - cur.abase), qe = (int)(b->ap[as + rloc + 1] - cur.abase);
+        const unsigned sh4 = 4u * (unsigned)(lane - rowbeg);
+        const int4* rec = (qe <= W8_REC) ? b->rec : A4 + cur.abase;   // beyond the staged part: global
+        const int4 d0 = rec[qb];
+        acc = __hiloint2double(d0.y, d0.x) * xo;       // diagonal record first (own y)
+        for (int q0 = qb + 1; q0 < qe; q0 += 8) {
+          double yv[8];
+          unsigned okm = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int qq = min(q0 + j, qe - 1);
+            const int2 ip = reinterpret_cast<const int2*>(&rec[qq])[1];
+            const unsigned sidx = ((unsigned)ip.y >> sh4) & 0xFu;
+            const bool ok = (q0 + j < qe) && sidx != 0xFu;
+            okm |= ok ? (1u << j) : 0u;
+            yv[j] = ok ? __ldg(X + ip.x + (int)sidx) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (okm & (1u << j)) acc = fma(reinterpret_cast<const double*>(&rec[q0 + j])[0], yv[j], acc);
+        }
+      }
+      s_qa[wib][lane] = qv * acc;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      if (act) {
+        const double g = acc - qv * dot;
+        out[cur.ebase + lane] = g;
+        part = fma(xo, g, part);
+      }
+    }
+    __syncwarp();                                      // buffer bi is free for window w + 2 nw
+    cur = nxt;
+    hn = hnn;
+    ++it;
+    w = wn;
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+static inline size_t w9_smem_bytes() { return sizeof(W9Buf) * 2 * W8_WARPS; }
 
 // y^ = Pi K y (nv = 1) on precomputed window headers, next header prefetched
 __global__ void __launch_bounds__(256, 8)
@@ -769,36 +1507,6 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
 // stage with cp.async.bulk (1D TMA, completion on an mbarrier) while the CTA
 // computes the current tile.  Only the y(k, s) gathers remain as loads.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 struct PipeLayout {     // byte offsets of one stage, and of the shared tail
   uint32_t rec, q, x, wp, ap, stage_bytes;
   uint32_t erow, qa, dot, bars, total;
@@ -1023,7 +1731,9 @@ struct FastPaths {
 static FastPaths* fast_of(emin_ctx c) { return reinterpret_cast<FastPaths*>(c->fast); }
 
 static inline int select_fast_path(emin_ctx c) {
-  if (c->nv != 1 || c->max_row > 8 || c->nnzWh >= INT32_MAX || c->nF >= INT32_MAX || c->nF == 0) return 0;
+  if (c->nv != 1 || c->max_row > 8 || c->nnzWh >= INT32_MAX || c->nF >= INT32_MAX || c->nnzAFF >= INT32_MAX ||
+      c->nF == 0)
+    return 0;
   if (getenv("EMIN_FORCE_GENERIC")) return 0;
   FastPaths* f = new FastPaths();
   c->fast = f;
@@ -1070,6 +1780,74 @@ static inline int select_fast_path(emin_ctx c) {
   if (var && !strcmp(var, "mask")) p.variant = 4;
   if (var && !strcmp(var, "win2")) p.variant = 5;
   if (var && !strcmp(var, "win3")) p.variant = 6;
+  if (var && !strcmp(var, "win4")) p.variant = 7;
+  if (var && !strcmp(var, "win5")) p.variant = 8;
+  if (var && !strcmp(var, "win6")) p.variant = 9;
+  if (var && !strcmp(var, "win7")) p.variant = 10;
+  if (var && !strcmp(var, "win8")) p.variant = 11;
+  if (var && !strcmp(var, "win9")) p.variant = 12;
+  if (p.variant == 12) {
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_spgemm_win9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w9_smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_win9, W8_WARPS * 32, w9_smem_bytes());
+    if (per_sm < 1 || cudaMallocAsync((void**)&p.w6hdr, sizeof(int4) * (p.nwin + 1), s) != cudaSuccess) {
+      p.variant = 5;
+    } else {
+      p.w8grid = (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + W8_WARPS - 1) / W8_WARPS, (int64_t)SM * per_sm));
+      k_plan_win6<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w6hdr);
+      c->launches += 1;
+    }
+  }
+  if (p.variant == 11) {
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_spgemm_win8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w8_smem_bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_win8, W8_WARPS * 32, w8_smem_bytes());
+    if (per_sm < 1 || cudaMallocAsync((void**)&p.w6hdr, sizeof(int4) * (p.nwin + 1), s) != cudaSuccess) {
+      p.variant = 5;
+    } else {
+      p.w8grid = (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + W8_WARPS - 1) / W8_WARPS, (int64_t)SM * per_sm));
+      k_plan_win6<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w6hdr);
+      c->launches += 1;
+    }
+  }
+  if (p.variant == 10) {
+    int32_t* dmx = nullptr;
+    int32_t hw = 0;
+    if (cudaMallocAsync((void**)&dmx, sizeof(int32_t), s) == cudaSuccess) {
+      cudaMemsetAsync(dmx, 0, sizeof(int32_t), s);
+      k_rowlen_max<<<SM * 4, 256, 0, s>>>(c->affptr, c->nF, dmx);
+      cudaMemcpyAsync(&hw, dmx, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaFreeAsync(dmx, s);
+      cudaStreamSynchronize(s);
+      c->launches += 1;
+    }
+    p.ellW = std::max(4, hw);
+    if (hw < 1 || hw > 8 ||
+        cudaMallocAsync((void**)&p.ell, sizeof(int4) * (size_t)c->nF * p.ellW, s) != cudaSuccess ||
+        cudaMallocAsync((void**)&p.w7hdr, sizeof(int4) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) {
+      p.variant = 5;
+    } else {
+      k_plan_ell<<<SM * 8, 256, 0, s>>>(c->affptr, c->nF, p.ellW, reinterpret_cast<const int4*>(p.ent), p.ell);
+      k_plan_win7<<<SM * 4, 256, 0, s>>>(c->wptr, p.rowstart, p.nwin, p.w7hdr);
+      c->launches += 2;
+    }
+  }
+  if (p.variant == 9) {
+    if (cudaMallocAsync((void**)&p.w6hdr, sizeof(int4) * (p.nwin + 1), s) != cudaSuccess) {
+      p.variant = 5;
+    } else {
+      k_plan_win6<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w6hdr);
+      c->launches += 1;
+    }
+  }
+  if (p.variant == 7 || p.variant == 8) {
+    if (cudaMallocAsync((void**)&p.w4hdr, sizeof(Win4Hdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) {
+      p.variant = 5;
+    } else {
+      k_plan_win4<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w4hdr);
+      c->launches += 1;
+    }
+  }
   if (p.variant == 6) {
     const int S3 = std::min(63, 65 - c->max_row);
     p.nwin3 = (c->nnzW + S3 - 1) / S3;
@@ -1140,6 +1918,7 @@ static inline int scalar_iter_grid(emin_ctx c) {
   switch (p.variant) {
     case 2: return (int)std::max<int64_t>(1, p.ntiles);
     case 3: return p.pipe_grid;
+    case 11: case 12: return p.w8grid;
     default: return scalar_grid(c);
   }
 }
@@ -1158,6 +1937,38 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
         return;
       case 5:
         k_spgemm_win2<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+        return;
+      case 7:
+      case 8: {
+        const int g = scalar_grid(c);
+        if (p.variant == 7)
+          k_spgemm_win4<false><<<g, 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent),
+                                                 p.w4hdr, p.nwin, X, out,
+                                                 c->partials);
+        else
+          k_spgemm_win4<true><<<g, 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent),
+                                                p.w4hdr, p.nwin, X, out,
+                                                c->partials);
+        return;
+      }
+      case 11:
+        k_spgemm_win8<<<p.w8grid, W8_WARPS * 32, w8_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
+                                                                      p.w6hdr, p.nwin, X, out, c->partials);
+        return;
+      case 12:
+        k_spgemm_win9<<<p.w8grid, W8_WARPS * 32, w9_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
+                                                                      p.w6hdr, p.nwin, X, out, c->partials);
+        return;
+      case 10: {
+        const int g = scalar_grid(c);
+#define W7(WW) case WW: k_spgemm_win7<WW><<<g, 256, 0, s>>>(v, p.ell, p.w7hdr, p.nwin, X, out, c->partials); break;
+        switch (p.ellW) { W7(4) W7(5) W7(6) W7(7) W7(8) }
+#undef W7
+        return;
+      }
+      case 9:
+        k_spgemm_win6<<<scalar_grid(c), 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent), p.w6hdr, p.nwin, X,
+                                                     out, c->partials);
         return;
       case 6:
         k_spgemm_win3<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart3, p.nwin3, X, out, c->partials);
@@ -1217,6 +2028,10 @@ static inline void free_fast_path(emin_ctx c) {
   if (f->sc.whdr) cudaFreeAsync(f->sc.whdr, c->stream);
   if (f->sc.emask) cudaFreeAsync(f->sc.emask, c->stream);
   if (f->sc.rowstart3) cudaFreeAsync(f->sc.rowstart3, c->stream);
+  if (f->sc.w4hdr) cudaFreeAsync(f->sc.w4hdr, c->stream);
+  if (f->sc.w6hdr) cudaFreeAsync(f->sc.w6hdr, c->stream);
+  if (f->sc.ell) cudaFreeAsync(f->sc.ell, c->stream);
+  if (f->sc.w7hdr) cudaFreeAsync(f->sc.w7hdr, c->stream);
   delete f;
   c->fast = nullptr;
 }

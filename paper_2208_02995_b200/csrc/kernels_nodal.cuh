@@ -318,6 +318,233 @@ k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __r
   if (threadIdx.x == 0) partials[blockIdx.x] = tot;
 }
 
+// ---------------------------------------------------------------------------
+// v2: same lane map and summation order as k_spgemm_nodal_s, but cut down to
+// what the L1 data pipe must carry (profiles/r01: the staged kernel was
+// bound by L1/shared wavefronts, 74 % of peak, not by DRAM):
+//  * the 3x3 block is read ONCE per block for both lane chunks, as five
+//    16-byte shared loads (block-major, 10-double stride) instead of 2 x 9
+//    8-byte loads;
+//  * Pi_B's nv dots of each of the 3 rows are reduced by a recursive-halving
+//    butterfly (a lane ends owning one dot; 8 doubles exchanged per row for
+//    nv = 6) and broadcast through shared memory, instead of nv full
+//    warp_sum butterflies per row (30 doubles);
+//  * 32-bit entry indices (nnz(W) < 2^31 is checked at plan time).
+// The per-entry arithmetic (block order, 9 FMAs in (d, e) order per block)
+// is unchanged, so y^ is bitwise equal to the staged kernel's except for the
+// order of the nv-dot sums.
+// ---------------------------------------------------------------------------
+constexpr int ND2_AST = 10;      // doubles per staged block (9 + pad, 16-byte aligned)
+
+// recursive-halving reduce-scatter of N values over the 32 lanes.  The N
+// values are padded to P = 2^ceil(log2 N); each halving stage splits a
+// lane's index range with its xor partner (disjoint ranges), and once a
+// range is a single index the remaining stages are plain xor adds (the two
+// partners compute a + b and b + a: bitwise equal).  On return the lane
+// holds in v[0] the full 32-lane sum of value index *own (valid iff
+// *own < N; a valid index may be held, bitwise equal, by several lanes).
+template <int S, int OFF>
+struct Nd2Rs {
+  static __device__ __forceinline__ void run(double* a, int lane, int& lo) {
+    if constexpr (OFF > 0) {
+      if constexpr (S > 1) {
+        constexpr int H = S / 2;
+        const bool lower = !(lane & OFF);
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+          const double send = lower ? a[H + i] : a[i];
+          const double recv = __shfl_xor_sync(0xffffffffu, send, OFF);
+          a[i] = (lower ? a[i] : a[H + i]) + recv;
+        }
+        if (!lower) lo += H;
+        Nd2Rs<H, OFF / 2>::run(a, lane, lo);
+      } else {
+        a[0] += __shfl_xor_sync(0xffffffffu, a[0], OFF);
+        Nd2Rs<1, OFF / 2>::run(a, lane, lo);
+      }
+    }
+  }
+};
+
+template <int N>
+__device__ __forceinline__ void nd2_reduce_scatter(double (&v)[N], int lane, int* own) {
+  constexpr int P = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
+  static_assert(N <= 32, "N <= 32");
+  double a[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) a[i] = i < N ? v[i] : 0.0;
+  int lo = 0;
+  Nd2Rs<P, 16>::run(a, lane, lo);
+  v[0] = a[0];
+  *own = lo;
+}
+
+template <int NV, int MODE>
+__global__ void __launch_bounds__(ND_WARPS * 32, 4)
+k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
+                  const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
+                  const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+                  double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ __align__(16) double s_a[ND_WARPS][ND_MAXB * ND2_AST];
+  __shared__ NodalBlk s_b[ND_WARPS][ND_MAXB];
+  __shared__ uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
+  __shared__ __align__(16) double s_dot[ND_WARPS][3 * NV + 1];
+  if (MODE == MM_ITER && v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  auto xval = [&](int idx) -> double { return MODE == MM_ENERGY ? X[idx] + X2[idx] : X[idx]; };
+  const int t0 = lane, t1 = lane + 32;
+  const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
+  double part = 0.0;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t r = 3 * n;
+    const int wb = (int)v.wptr[r];
+    const int n3 = (int)v.wptr[r + 1] - wb;
+    const int nJ = n3 / 3;
+    const int64_t ab = v.affptr[r];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int64_t po = pmoff[n];
+    // ---- stage the node's data (A chunk re-ordered block-major, 10-double stride)
+    const int rs = 3 * nb;
+    for (int k = lane; k < 9 * nb; k += 32) {
+      const int d = k / rs, rem = k - d * rs, b = rem / 3, e = rem - 3 * b;
+      s_a[wib][b * ND2_AST + d * 3 + e] = __ldg(v.affval + ab + k);
+    }
+    for (int k = lane; k < nb; k += 32) s_b[wib][k] = blk[bb + k];
+    for (int k = lane; k < nb * nJ; k += 32) s_pm[wib][k] = pm8[po + k];
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    const bool any1 = n3 > 32;                          // warp-uniform
+    __syncwarp();
+    double acc0[3] = {0.0, 0.0, 0.0}, acc1[3] = {0.0, 0.0, 0.0};
+    for (int b = 0; b < nb; ++b) {
+      const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][b * ND2_AST]);
+      const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+      const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+      const NodalBlk k = s_b[wib][b];
+      const int p0 = act0 ? s_pm[wib][b * nJ + s0] : 0xFF;
+      if (p0 != 0xFF) {
+        const int i0 = k.ybase + 3 * p0 + b0;
+        const double y0 = xval(i0), y1 = xval(i0 + k.nK3), y2 = xval(i0 + 2 * k.nK3);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          acc0[d] = fma(a[d * 3 + 0], y0, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 1], y1, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 2], y2, acc0[d]);
+        }
+      }
+      if (any1) {
+        const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
+        if (p1 != 0xFF) {
+          const int i1 = k.ybase + 3 * p1 + b1;
+          const double y0 = xval(i1), y1 = xval(i1 + k.nK3), y2 = xval(i1 + 2 * k.nK3);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] = fma(a[d * 3 + 0], y0, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 1], y1, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 2], y2, acc1[d]);
+          }
+        }
+      }
+    }
+    double g0[3], g1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) { g0[d] = acc0[d]; g1[d] = acc1[d]; }
+    if (MODE != MM_ITER) {            // C-identity term A(i, c_j) (setup / energy only)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int64_t fb = v.afcptr[r + d], fe = v.afcptr[r + d + 1];
+        const int ro = wb + d * n3;
+        double f0 = 0.0, f1 = 0.0;
+        if (act0) {
+          const int32_t j = v.wcol[ro + t0];
+          for (int64_t q = fb; q < fe; ++q) if (v.afccol[q] == j) { f0 = v.afcval[q]; break; }
+        }
+        if (act1) {
+          const int32_t j = v.wcol[ro + t1];
+          for (int64_t q = fb; q < fe; ++q) if (v.afccol[q] == j) { f1 = v.afcval[q]; break; }
+        }
+        if (MODE == MM_ENERGY) {
+          if (act0) part = fma(xval(ro + t0), g0[d] + 2.0 * f0, part);
+          if (act1) part = fma(xval(ro + t1), g1[d] + 2.0 * f1, part);
+        } else {
+          g0[d] += f0;
+          g1[d] += f1;
+        }
+      }
+    }
+    if (MODE != MM_ENERGY) {
+      // Q of the node (row 3n, shared by its 3 rows): 16-byte loads
+      double q0[NV], q1[NV];
+#pragma unroll
+      for (int m = 0; m < NV; ++m) { q0[m] = 0.0; q1[m] = 0.0; }
+      if ((NV & 1) == 0) {
+        if (act0) {
+          const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t0) * NV);
+#pragma unroll
+          for (int m = 0; m < NV / 2; ++m) { const double2 t = __ldg(qp + m); q0[2 * m] = t.x; q0[2 * m + 1] = t.y; }
+        }
+        if (act1) {
+          const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t1) * NV);
+#pragma unroll
+          for (int m = 0; m < NV / 2; ++m) { const double2 t = __ldg(qp + m); q1[2 * m] = t.x; q1[2 * m + 1] = t.y; }
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < NV; ++m) {
+          q0[m] = act0 ? __ldg(v.Q + (int64_t)(wb + t0) * NV + m) : 0.0;
+          q1[m] = act1 ? __ldg(v.Q + (int64_t)(wb + t1) * NV + m) : 0.0;
+        }
+      }
+      // Pi_B (twice for r0, see masked.cuh)
+#pragma unroll
+      for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double dv[NV];
+#pragma unroll
+          for (int m = 0; m < NV; ++m) dv[m] = fma(q0[m], g0[d], q1[m] * g1[d]);
+          int own;
+          nd2_reduce_scatter<NV>(dv, lane, &own);
+          if (own < NV) s_dot[wib][d * NV + own] = dv[0];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double s0v = 0.0, s1v = 0.0;
+#pragma unroll
+          for (int m = 0; m < NV; ++m) {
+            const double dm = s_dot[wib][d * NV + m];
+            s0v = fma(q0[m], dm, s0v);
+            s1v = fma(q1[m], dm, s1v);
+          }
+          g0[d] -= s0v;
+          g1[d] -= s1v;
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ro = wb + d * n3;
+        if (act0) {
+          if (MODE == MM_ITER) { out[ro + t0] = g0[d]; part = fma(X[ro + t0], g0[d], part); }
+          else out[ro + t0] = -g0[d];
+        }
+        if (act1) {
+          if (MODE == MM_ITER) { out[ro + t1] = g1[d]; part = fma(X[ro + t1], g1[d], part); }
+          else out[ro + t1] = -g1[d];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
 // ---- host side ------------------------------------------------------------
 template <typename T>
 static cudaError_t nd_alloc(T** p, int64_t n, cudaStream_t s) {
@@ -385,20 +612,25 @@ static inline void launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
     }
     return;
   }
-#define NV_CASE(N)                                                                                                  \
-  case N:                                                                                                           \
-    if (mode == MM_ITER)                                                                                            \
-      k_spgemm_nodal_s<N, MM_ITER><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, \
-                                                              out, c->partials);                                  \
-    else if (mode == MM_R0)                                                                                         \
-      k_spgemm_nodal_s<N, MM_R0><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2,   \
-                                                            out, c->partials);                                    \
-    else                                                                                                            \
-      k_spgemm_nodal_s<N, MM_ENERGY><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X,   \
-                                                                X2, out, c->partials);                            \
+  const bool v2 = !(var && !strcmp(var, "s"));     // EMIN_NODAL=s: the staged v1 kernel
+#define ND_LAUNCH(KER, N)                                                                                  \
+  if (mode == MM_ITER)                                                                                    \
+    KER<N, MM_ITER><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out,   \
+                                                c->partials);                                             \
+  else if (mode == MM_R0)                                                                                 \
+    KER<N, MM_R0><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out,     \
+                                              c->partials);                                               \
+  else                                                                                                    \
+    KER<N, MM_ENERGY><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, \
+                                                  c->partials);
+#define NV_CASE(N)                                   \
+  case N:                                            \
+    if (v2) { ND_LAUNCH(k_spgemm_nodal_v2, N) }      \
+    else { ND_LAUNCH(k_spgemm_nodal_s, N) }          \
     break;
   switch (c->nv) { NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8) }
 #undef NV_CASE
+#undef ND_LAUNCH
 }
 
 static inline void free_nodal_path(emin_ctx c, NodalPlan*& p) {

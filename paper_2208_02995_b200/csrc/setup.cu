@@ -444,9 +444,12 @@ __global__ void k_block_sums(const double* __restrict__ x, int64_t n, double* __
   if (threadIdx.x == 0) partials[blockIdx.x] = t;
 }
 
+// every context array carries 64 bytes of tail padding: the TMA-staged
+// window kernel (win9) copies 16-byte-aligned spans that may end up to one
+// element past an array's last entry (read, never used)
 template <typename T>
 cudaError_t dalloc(T** p, int64_t n, cudaStream_t s) {
-  return cudaMallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s);
+  return cudaMallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1) + 64, s);
 }
 
 }  // namespace

@@ -1,6 +1,6 @@
 """A/B of the per-iteration masked-SpGEMM variants on one config (GPU).
 
-  python profiles/spgemm_variants.py [config] [variants...]
+  python profiles/spgemm_variants.py [config] [variants...]   (win2 | EMIN_NODAL=s ...)
 
 Times every kernel class with CUDA events (emin_kernel_times) over
 emin_iterate(k) after a warm-up call, for each EMIN_SPGEMM variant, and
@@ -30,7 +30,10 @@ def main():
     k = prob.iters
     res = {}
     for var in variants:
-        os.environ["EMIN_SPGEMM"] = var
+        # "win2" sets EMIN_SPGEMM; "EMIN_NODAL=s" sets that variable
+        ek, ev = var.split("=", 1) if "=" in var else ("EMIN_SPGEMM", var)
+        saved = os.environ.get(ek)
+        os.environ[ek] = ev
         h = E.emin_setup(prob.n, prob.nc, dev["A_rowptr"], dev["A_col"], dev["A_val"], dev["is_coarse"],
                          dev["P_rowptr"], dev["P_col"], dev["P_val"], prob.nv, dev["B"], dev["Bc"],
                          block_size=prob.block_size, stagnation_rel=0.0)
@@ -41,6 +44,10 @@ def main():
         kt = E.emin_kernel_times(h)
         en = E.emin_energy(h)
         E.emin_destroy(h)
+        if saved is None:
+            os.environ.pop(ek)
+        else:
+            os.environ[ek] = saved
         res[var] = {n: round(ms / max(c, 1) * 1e3, 2) for n, (ms, c) in kt.items()}
         res[var]["energy"] = en
         print(var, json.dumps(res[var]), flush=True)

@@ -73,17 +73,21 @@ def test_parity_small(name, size, k):
     assert rep["n_svd_rows"] == o.n_svd and rep["n_frozen_rows"] == o.n_frozen
 
 
-@pytest.mark.parametrize("name,size,path", [("3", 12, 1), ("2b", 10, 1), ("4", 4, 2), ("5", 8, 2)])
-@pytest.mark.parametrize("variant", ["win", "mask", "tile", "hdr", "pipe"])
-def test_kernel_paths_agree(name, size, path, variant, monkeypatch):
+SCALAR_VARIANTS = [("EMIN_SPGEMM", v) for v in ("win", "win2", "win4", "win5", "win6", "win7", "win8", "win9", "mask", "tile", "hdr", "pipe")]
+NODAL_VARIANTS = [("EMIN_NODAL", v) for v in ("v2", "s", "plain")]
+
+
+@pytest.mark.parametrize("name,size,path", [("3", 12, 1), ("2b", 10, 1), ("3", 17, 1), ("4", 4, 2), ("5", 8, 2)])
+@pytest.mark.parametrize("env,variant", SCALAR_VARIANTS + NODAL_VARIANTS)
+def test_kernel_paths_agree(name, size, path, env, variant, monkeypatch):
     """The specialised kernels (scalar window/mask/tile/header variants,
-    nodal 3x3) against the generic warp-per-row kernel and the oracle."""
+    nodal 3x3 variants) against the generic warp-per-row kernel."""
     from paper_2208_02995_b200 import Emin
     from workloads.problems import make_config
-    if path == 2 and variant != "win":
-        pytest.skip("variants apply to the scalar path")
+    if (path == 2) != (env == "EMIN_NODAL"):
+        pytest.skip("variant of the other kernel path")
     prob = make_config(name, size=size)
-    monkeypatch.setenv("EMIN_SPGEMM", variant)
+    monkeypatch.setenv(env, variant)
     fast = Emin.from_problem(prob)
     assert fast.report()["kernel_path"] == path
     monkeypatch.setenv("EMIN_FORCE_GENERIC", "1")
