@@ -29,6 +29,7 @@ struct DevState {
   int32_t k_call;     // accepted steps in the current emin_iterate call
   double red[4];      // multi-GPU: local sums reduced in place by ncclAllReduce
                       // [0] gamma, [1] y.yb, [2] energy
+  uint32_t ctr[2];    // fused scalar steps: blocks done in stage I [0] / SpGEMM [1]
 };
 
 struct DistPlan;
@@ -56,6 +57,8 @@ struct DevView {
   const double* Q;       // [nnzW * nv] row-major per entry, zero padded
   DevState* st;
   int32_t pingpong;      // L2 ping-pong traversal order (see iterate.cu)
+  int32_t fuse;          // 1: the last block of stage I / SpGEMM applies the scalar step
+  double* dE_hist;       // per-step energy decrements (scalar step of the SpGEMM)
 };
 
 struct emin_ctx_s {
@@ -71,6 +74,8 @@ struct emin_ctx_s {
   int32_t stage_vec = 0;       // 16-byte vectorised streaming stages (EMIN_STAGE=v)
   int32_t kernel_path = 0;
   int32_t pingpong = 0;        // alternate traversal directions (EMIN_PINGPONG)
+  int32_t fuse = 0;            // scalar steps fused into the producing kernels (EMIN_FUSE)
+  int32_t iter_kernels = 5;    // our kernel launches per CG iteration (set at graph capture)
   // device arrays (owned by ctx)
   int64_t *wptr = nullptr, *affptr = nullptr, *afcptr = nullptr, *pofs = nullptr, *cofs = nullptr;
   uint8_t* isc_own = nullptr;  // is_coarse of the owned rows
@@ -115,6 +120,8 @@ struct emin_ctx_s {
     v.wptr = wptr; v.wcol = wcol; v.affptr = affptr; v.affcol = affcol; v.affval = affval;
     v.afcptr = afcptr; v.afccol = afccol; v.afcval = afcval; v.d = d; v.Q = Q; v.st = st;
     v.pingpong = pingpong;
+    v.fuse = fuse;
+    v.dE_hist = dE_hist;
     return v;
   }
 };
@@ -150,6 +157,74 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* >= 32 */) {
   }
   __syncthreads();
   return t;
+}
+
+// ---- the CG scalar steps (Alg. 3), applied by one thread
+// gamma = r.z; stop if gamma <= 0; beta = gamma / gamma_old
+__device__ __forceinline__ void scalar_gamma_apply(DevState* st, double g) {
+  st->pendw = st->pend;
+  st->pend = 0;
+  if (!(g > 0.0)) { st->stopped = 1; return; }
+  st->beta = (st->k_total == 0) ? 0.0 : g / st->gamma_old;
+  st->gamma = g;
+  st->gamma_old = g;
+}
+// alpha = gamma / y.yb; dE = gamma alpha; stop tests (A4, A18)
+__device__ __forceinline__ void scalar_alpha_apply(DevState* st, double den, double* dE_hist) {
+  st->den = den;
+  if (den < 0.0) { st->stopped = 5; return; }
+  if (den == 0.0) { st->stopped = 2; return; }
+  const double alpha = st->gamma / den;
+  const double dE = st->gamma * alpha;
+  const int64_t k = st->k_total + 1;
+  if (k == 1) st->dE1 = dE;
+  if (st->tau > 0.0 && k > 1 && dE < st->tau * st->dE1) { st->stopped = 3; return; }
+  if (dE <= st->stag * st->E0) { st->stopped = 4; return; }
+  st->alpha_pend = alpha;
+  st->pend = 1;
+  dE_hist[st->k_total] = dE;
+  st->k_total = k;
+  st->k_call += 1;
+}
+
+// Epilogue of a kernel producing per-block partial sums.  which = 0 (stage
+// I: gamma) or 1 (SpGEMM: y.yb) with v.fuse set: the last block to finish
+// (threadfence + counter, as in the CUDA threadFenceReduction sample) sums
+// all partials in a fixed order and applies the scalar step, replacing the
+// separate single-block scalar kernel.  All other blocks have already read
+// the DevState fields the step writes (they read them at kernel start).
+// which < 0 or !v.fuse: plain partial write (consumer kernel reduces).
+__device__ __forceinline__ void block_partial_out(const DevView& v, double* partials, double tot, double* sh,
+                                                  int which) {
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = tot;
+    int last = 0;
+    if (which >= 0 && v.fuse) {
+      __threadfence();
+      last = atomicAdd(&v.st->ctr[which], 1u) == gridDim.x - 1;
+    }
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double sum = 0.0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) sum += __ldcg(partials + k);
+  sum = block_sum(sum, sh);
+  if (threadIdx.x == 0) {
+    if (which == 0) scalar_gamma_apply(v.st, sum);
+    else {
+      v.st->pendw = 0;
+      if (!v.st->stopped) scalar_alpha_apply(v.st, sum, v.dE_hist);
+    }
+    v.st->ctr[which] = 0;
+  }
+}
+// a fused SpGEMM that returns early on a stopped state still retires the
+// pending dw update flag (what the separate alpha kernel did)
+__device__ __forceinline__ void iter_stopped(const DevView& v) {
+  if (v.fuse && blockIdx.x == 0 && threadIdx.x == 0) v.st->pendw = 0;
 }
 
 // lower_bound of key in sorted a[0..n)

@@ -75,7 +75,7 @@ k_stage1(DevView v, double* __restrict__ r, const double* __restrict__ yb, doubl
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 0);
 }
 
 // ------------------------------------------------------------ stage II
@@ -176,7 +176,7 @@ k_stage1_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 0);
 }
 
 __global__ void __launch_bounds__(256, 4)
@@ -271,7 +271,7 @@ k_stage1_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict
     part = fma(x, jacobi_div(x, v.d[erow[e]], dinv[erow[e]]), part);
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 0);
 }
 
 __global__ void __launch_bounds__(256, 4)
@@ -344,14 +344,7 @@ __global__ void k_scalar_gamma(DevState* st, const double* __restrict__ partials
   __shared__ double sh[32];
   if (st->stopped) return;
   const double g = reduce_partials(partials, np, sh);
-  if (threadIdx.x == 0) {
-    st->pendw = st->pend;
-    st->pend = 0;
-    if (!(g > 0.0)) { st->stopped = 1; return; }
-    st->beta = (st->k_total == 0) ? 0.0 : g / st->gamma_old;
-    st->gamma = g;
-    st->gamma_old = g;
-  }
+  if (threadIdx.x == 0) scalar_gamma_apply(st, g);
 }
 
 __global__ void k_scalar_alpha(DevState* st, const double* __restrict__ partials, int np,
@@ -360,22 +353,7 @@ __global__ void k_scalar_alpha(DevState* st, const double* __restrict__ partials
   if (threadIdx.x == 0) st->pendw = 0;
   if (st->stopped) return;
   const double den = reduce_partials(partials, np, sh);
-  if (threadIdx.x == 0) {
-    st->den = den;
-    if (den < 0.0) { st->stopped = 5; return; }
-    if (den == 0.0) { st->stopped = 2; return; }
-    const double alpha = st->gamma / den;
-    const double dE = st->gamma * alpha;
-    const int64_t k = st->k_total + 1;
-    if (k == 1) st->dE1 = dE;
-    if (st->tau > 0.0 && k > 1 && dE < st->tau * st->dE1) { st->stopped = 3; return; }
-    if (dE <= st->stag * st->E0) { st->stopped = 4; return; }
-    st->alpha_pend = alpha;
-    st->pend = 1;
-    dE_hist[st->k_total] = dE;
-    st->k_total = k;
-    st->k_call += 1;
-  }
+  if (threadIdx.x == 0) scalar_alpha_apply(st, den, dE_hist);
 }
 
 // apply a pending update (before reading W or r from outside the loop)
@@ -405,6 +383,7 @@ __global__ void k_reset_state(DevState* st, const double* __restrict__ Epart, in
     st->stopped = 0;
     st->pend = st->pendw = 0;
     st->k_call = 0;
+    st->ctr[0] = st->ctr[1] = 0;
   }
 }
 
@@ -591,20 +570,37 @@ static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev, int e
   auto rec = [&](int t) {
     if (ev) cudaEventRecordWithFlags(ev[t], s, external ? cudaEventRecordExternal : cudaEventRecordDefault);
   };
+  // fused mode (single GPU): the scalar steps run in the last block of stage
+  // I and of the SpGEMM (block_partial_out); with NCCL the partial sums are
+  // reduced over the ranks first, so the single-block scalar kernels stay
+  // opt-in (EMIN_FUSE=1): measured 3.4 us per iteration SLOWER on config 3
+  // (the last block's serial tail -- counter atomic, partial reduction,
+  // dependent DevState loads -- costs what the separate launch did;
+  // profiles/r01b/spgemm_ab_c3.txt)
+  const char* fz = getenv("EMIN_FUSE");
+  c->fuse = (!c->dist && fz && !strcmp(fz, "1")) ? 1 : 0;
   rec(0);
   launch_stage(c, 1, s);
   rec(1);
-  const auto r1 = global_sum(c, c->grid_rows, 0, s);
-  k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, r1.first, r1.second);
+  if (!c->fuse) {
+    const auto r1 = global_sum(c, c->grid_rows, 0, s);
+    k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, r1.first, r1.second);
+  }
   rec(2);
   launch_stage(c, 2, s);
   if (c->dist) emin_dist_halo_values(c, c->y, s);     // y on the halo rows
   rec(3);
   const int g = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
   rec(4);
-  const auto r2 = global_sum(c, g, 1, s);
-  k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, r2.first, r2.second, c->dE_hist);
+  if (!c->fuse) {
+    const auto r2 = global_sum(c, g, 1, s);
+    k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, r2.first, r2.second, c->dE_hist);
+  }
   rec(5);
+  // kernels of ours per iteration: stage I, stage II, SpGEMM (+ the two
+  // scalar kernels, + on several GPUs their rank-local sum kernels and the
+  // halo pack)
+  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 3 : 0);
 }
 
 // One iteration captured as a CUDA graph (5 kernel nodes, cheap to
@@ -734,7 +730,7 @@ extern "C" emin_status emin_iterate(emin_ctx c, int32_t k, int32_t* k_done, doub
     }
     for (int it = 0; it < k; ++it) EMIN_CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
   }
-  c->launches += 5 * (int64_t)k;
+  c->launches += c->iter_kernels * (int64_t)k;
   c->k_launched += k;
   if (k_done || dE) {
     DevState h;

@@ -201,7 +201,7 @@ k_spgemm_mask(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__
               double* __restrict__ partials) {
   __shared__ double sh[32];
   __shared__ double s_qa[8][32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -259,7 +259,7 @@ k_spgemm_mask(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__
     w = wn;
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 // y^ = Pi K y (nv = 1), window kernel with fewer warp collectives: the
@@ -271,7 +271,7 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
   __shared__ double s_qa[8][32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -329,7 +329,7 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 // win3: windows of up to 64 entries (two per lane: positions lane and
@@ -341,7 +341,7 @@ k_spgemm_win3(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
   __shared__ double s_qa[8][64];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -409,7 +409,7 @@ k_spgemm_win3(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
     __syncwarp();
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -479,7 +479,7 @@ k_spgemm_win4(DevView v, const int4* __restrict__ A4, const Win4Hdr* __restrict_
   __shared__ double sh[32];
   __shared__ double s_qa[8][32];
   __shared__ int4 s_rec[8][W4_REC];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -566,7 +566,7 @@ k_spgemm_win4(DevView v, const int4* __restrict__ A4, const Win4Hdr* __restrict_
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -613,7 +613,7 @@ k_spgemm_win6(DevView v, const int4* __restrict__ A4, const int4* __restrict__ h
               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
   __shared__ double s_qa[8][32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -690,7 +690,7 @@ k_spgemm_win6(DevView v, const int4* __restrict__ A4, const int4* __restrict__ h
     w = wn;
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -740,7 +740,7 @@ k_spgemm_win7(DevView v, const int4* __restrict__ ell, const int4* __restrict__ 
               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
   __shared__ double s_qa[8][32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -814,7 +814,7 @@ k_spgemm_win7(DevView v, const int4* __restrict__ ell, const int4* __restrict__ 
     w = wn;
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -887,7 +887,7 @@ k_spgemm_win8(DevView v, const int4* __restrict__ A4, const int4* __restrict__ h
   extern __shared__ __align__(16) unsigned char w8_smem[];
   __shared__ double sh[32];
   __shared__ double s_qa[W8_WARPS][32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   W8Buf* bufs = reinterpret_cast<W8Buf*>(w8_smem) + 2 * wib;
@@ -982,7 +982,7 @@ k_spgemm_win8(DevView v, const int4* __restrict__ A4, const int4* __restrict__ h
   }
   cp_async_wait<0>();
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 static inline size_t w8_smem_bytes() { return sizeof(W8Buf) * 2 * W8_WARPS; }
 
@@ -1009,7 +1009,7 @@ k_spgemm_win9(DevView v, const int4* __restrict__ A4, const int4* __restrict__ h
   __shared__ double sh[32];
   __shared__ double s_qa[W8_WARPS][32];
   __shared__ __align__(8) uint64_t s_bar[W8_WARPS][2];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   W9Buf* bufs = reinterpret_cast<W9Buf*>(w9_smem) + 2 * wib;
@@ -1106,7 +1106,7 @@ k_spgemm_win9(DevView v, const int4* __restrict__ A4, const int4* __restrict__ h
     w = wn;
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 static inline size_t w9_smem_bytes() { return sizeof(W9Buf) * 2 * W8_WARPS; }
 
@@ -1115,7 +1115,7 @@ __global__ void __launch_bounds__(256, 8)
 k_spgemm_hdr(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__ hdr, int64_t nwin,
              const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1156,7 +1156,7 @@ k_spgemm_hdr(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__ 
     w = wn;
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 
@@ -1170,7 +1170,7 @@ k_spgemm_scalar(DevView v, const SpEnt* __restrict__ A, const int32_t* __restric
                 const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
                 double* __restrict__ partials) {
   __shared__ double sh[32];
-  if (MODE == MM_ITER && v.st->stopped) return;
+  if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1223,7 +1223,7 @@ k_spgemm_scalar(DevView v, const SpEnt* __restrict__ A, const int32_t* __restric
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
 }
 
 // Alg. 2 for nv = 1 on the window plan (the CGS2 QR of k_alg2 reduces to
@@ -1324,7 +1324,7 @@ k_stage1_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, doub
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 0);
 }
 
 // stage II on the window plan: dw += alpha_pend y_old ; y = z + beta y_old
@@ -1386,7 +1386,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
               double* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double sh[32];
-  if (MODE == MM_ITER && v.st->stopped) return;
+  if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
   const int tid = threadIdx.x;
   const TileHdr H = hdr[blockIdx.x];
   const int nrows = H.r1 - H.r0;
@@ -1496,7 +1496,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1554,7 +1554,7 @@ k_spgemm_pipe(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
               double* __restrict__ partials) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double sh[32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const PipeLayout L = pipe_layout(rec_cap, rows_cap);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
   uint16_t* s_erow = reinterpret_cast<uint16_t*>(smem_raw + L.erow);
@@ -1644,7 +1644,7 @@ k_spgemm_pipe(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
     __syncthreads();   // stage st and the shared tail are free again
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 __global__ void k_tile_headers(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,

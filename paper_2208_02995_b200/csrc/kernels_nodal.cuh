@@ -100,7 +100,7 @@ k_spgemm_nodal(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __res
                const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
                const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
-  if (v.st->stopped) return;
+  if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -179,7 +179,7 @@ k_spgemm_nodal(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __res
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, 1);
 }
 
 // Staged variant: the warp first copies its node's A chunk (9 nb doubles),
@@ -200,7 +200,7 @@ k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __r
   __shared__ double s_a[ND_WARPS][ND_MAXB * 9];
   __shared__ NodalBlk s_b[ND_WARPS][ND_MAXB];
   __shared__ uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
-  if (MODE == MM_ITER && v.st->stopped) return;
+  if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -315,7 +315,7 @@ k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __r
     __syncwarp();
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
 }
 
 // ---------------------------------------------------------------------------
@@ -390,7 +390,7 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
   __shared__ NodalBlk s_b[ND_WARPS][ND_MAXB];
   __shared__ uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
   __shared__ __align__(16) double s_dot[ND_WARPS][3 * NV + 1];
-  if (MODE == MM_ITER && v.st->stopped) return;
+  if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -542,7 +542,7 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
     __syncwarp();
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
 }
 
 // ---- host side ------------------------------------------------------------

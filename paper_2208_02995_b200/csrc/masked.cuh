@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256)
 k_masked_generic(DevView v, const double* __restrict__ X, const double* __restrict__ X2,
                  double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
-  if (MODE == MM_ITER && v.st->stopped) return;   // uniform over the grid
+  if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }   // uniform over the grid
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -134,5 +134,5 @@ k_masked_generic(DevView v, const double* __restrict__ X, const double* __restri
     }
   }
   const double tot = block_sum(part, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
 }
