@@ -42,7 +42,7 @@ def _load():
         P = C.c_void_p
         i64, i32, dbl = C.c_int64, C.c_int, C.c_double
         lib.oracle_create.argtypes = [C.POINTER(P), i64, i64, P, P, P, P, P, P, P, i32, P, P,
-                                      dbl, dbl, dbl, i32]
+                                      dbl, dbl, dbl, i32, i32, P]
         lib.oracle_create.restype = i32
         lib.oracle_iterate.argtypes = [P, i32, C.POINTER(i32), P]
         lib.oracle_iterate.restype = i32
@@ -62,6 +62,7 @@ def _load():
         lib.oracle_copy_vec.argtypes = [P, i32, P]
         lib.oracle_copy_Q.argtypes = [P, P, P]
         lib.oracle_project.argtypes = [P, P, P]
+        lib.oracle_apply_prec.argtypes = [P, P, P]
         lib.oracle_masked_AX.argtypes = [P, P, i32, P]
         lib.oracle_setup_row.argtypes = [i32, i32, P, P, dbl, P, P, C.POINTER(i32)]
         lib.oracle_setup_row.restype = i32
@@ -83,7 +84,10 @@ class Oracle:
     """Oracle state for one problem (see workloads.problems.Problem)."""
 
     def __init__(self, prob, rank_tol=1e-10, tau=0.0, stagnation_rel=1e-30, project_z=True,
-                 P_val="from_problem"):
+                 P_val="from_problem", precond="jacobi", sgs_key=None):
+        """precond: "jacobi" (M_1) or "sgs" (projected SGS M_2,
+        P:916-938); sgs_key (per global row, optional): SGS visits the rows
+        of each K block in ascending (key, row) order (reading A23)."""
         lib = _load()
         self._keep = []
 
@@ -99,7 +103,9 @@ class Oracle:
                                _p(arr(prob.P_rowptr, np.int64)), _p(arr(prob.P_col, np.int32)),
                                _p(None if Pv is None else arr(Pv, np.float64)),
                                prob.nv, _p(arr(prob.B, np.float64)), _p(arr(prob.Bc, np.float64)),
-                               rank_tol, tau, stagnation_rel, 1 if project_z else 0)
+                               rank_tol, tau, stagnation_rel, 1 if project_z else 0,
+                               {"jacobi": 0, "sgs": 1}[precond],
+                               _p(None if sgs_key is None else arr(sgs_key, np.int64)))
         self._keep = []
         if st != 0:
             raise OracleError(st, "create")
@@ -194,6 +200,13 @@ class Oracle:
         x = np.ascontiguousarray(x, dtype=np.float64)
         out = np.empty_like(x)
         self._lib.oracle_project(self._h, _p(x), _p(out))
+        return out
+
+    def apply_prec(self, x):
+        """z = Pi M^{-1} x with the oracle's preconditioner (Alg. 3 line P:840)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        self._lib.oracle_apply_prec(self._h, _p(x), _p(out))
         return out
 
     def masked_AX(self, X, with_fc=False):

@@ -34,6 +34,14 @@
  *             dE_k <= stag E0 -> stop                       (A18)
  *             dw += alpha y ; r -= alpha yb
  *   energy  tr(P^T A P) by its definition (Eq. trace), P = [W; I].
+ *   precond z = Pi M_2^{-1} r with the projected
+ *           symmetric Gauss-Seidel preconditioner (Eq. SGS_prec
+ *           simplified): M_SGS^{-1} = (L+D)^{-T} D (L+D)^{-1}, K = L + D + L^T
+ *           (K block diagonal, block j = A(I_j, I_j) for coarse
+ *           column j), the unknowns of each block visited in ascending
+ *           (sgs_key, row) order (reading A23); applied matrix-free on the W
+ *           layout as one forward and one backward sweep over the F rows, and
+ *           always followed by Pi (only Jacobi may skip it).
  *
  * Summation order: per-row sums ascending in A's column order; global sums
  * row-ascending with Neumaier compensation.
@@ -71,6 +79,8 @@ typedef struct {
     int nv;
     double rank_tol, tau, stag;
     int project_z;                 /* 1: z = Pi M^-1 r (literal P:840) */
+    int precond;                   /* 0 Jacobi M_1, 1 projected SGS M_2 */
+    int64_t *sgs_key;              /* F index -> SGS ordering key (0 if none given) */
     /* full operator, copied */
     int64_t *Arp; int32_t *Acol; double *Aval;
     uint8_t *isc;
@@ -311,6 +321,100 @@ void oracle_masked_AX(const oracle_t *o, const double *X, int with_fc, double *o
     }
 }
 
+/* does F row k precede F row i in the SGS visiting order?  Ascending
+ * (sgs_key, global row) -- reading A23 (the paper leaves the order of the
+ * unknowns inside a K block open; natural order = all keys equal). */
+static int sgs_before(const oracle_t *o, int64_t k, int64_t i) {
+    if (o->sgs_key[k] != o->sgs_key[i]) return o->sgs_key[k] < o->sgs_key[i];
+    return o->frow[k] < o->frow[i];
+}
+
+/* z = M_SGS^{-1} x = (L+D)^{-T} D (L+D)^{-1} x, K = L + D + L^T.
+ * K is block diagonal over the coarse columns j, block j = A(I_j, I_j)
+ * (Eq. 11blk): the unknown (i, j) couples to (k, j) with weight
+ * A(i,k) for every F row k whose pattern also holds j; D = A(i,i).
+ *   (L+D) u = x   forward:  u(i,j) = (x(i,j) - sum_{k before i} A(i,k) u(k,j)) / A(i,i)
+ *   v = D u
+ *   (L+D)^T z = v backward: z(i,j) = (v(i,j) - sum_{k after i} A(k,i) z(k,j)) / A(i,i)
+ * with A(k,i) = A(i,k) (A symmetric); the sums run over row i of A in
+ * its column order.  Rows are visited in the SGS order (sgs_before); every
+ * entry of row i is solved at once (the blocks j are independent). */
+static void sgs_apply(const oracle_t *o, const double *x, double *z) {
+    int64_t nF = o->nF;
+    int64_t *ord = (int64_t *)malloc(sizeof(int64_t) * (nF ? nF : 1));
+    double *u = (double *)malloc(sizeof(double) * (o->nnzW ? o->nnzW : 1));
+    for (int64_t i = 0; i < nF; ++i) ord[i] = i;
+    /* insertion of the visiting order (stable; plain O(nF log nF) merge sort) */
+    {
+        int64_t *tmp = (int64_t *)malloc(sizeof(int64_t) * (nF ? nF : 1));
+        for (int64_t w = 1; w < nF; w *= 2) {
+            for (int64_t lo = 0; lo < nF; lo += 2 * w) {
+                int64_t mid = lo + w < nF ? lo + w : nF, hi = lo + 2 * w < nF ? lo + 2 * w : nF;
+                int64_t a = lo, b = mid, t = lo;
+                while (a < mid && b < hi) tmp[t++] = sgs_before(o, ord[b], ord[a]) ? ord[b++] : ord[a++];
+                while (a < mid) tmp[t++] = ord[a++];
+                while (b < hi) tmp[t++] = ord[b++];
+            }
+            memcpy(ord, tmp, sizeof(int64_t) * nF);
+        }
+        free(tmp);
+    }
+    /* forward sweep: (L + D) u = x */
+    for (int64_t oi = 0; oi < nF; ++oi) {
+        int64_t i = ord[oi], g = o->frow[i];
+        int64_t b = o->wptr[i], e = o->wptr[i + 1];
+        for (int64_t p = b; p < e; ++p) u[p] = x[p];
+        for (int64_t q = o->Arp[g]; q < o->Arp[g + 1]; ++q) {
+            int64_t c = o->Acol[q];
+            if (o->isc[c] || c == g) continue;
+            int64_t k = o->fid[c];
+            if (!sgs_before(o, k, i)) continue;
+            double a = o->Aval[q];
+            int64_t pi = b, pk = o->wptr[k], ek = o->wptr[k + 1];
+            while (pi < e && pk < ek) {
+                if (o->wcol[pi] == o->wcol[pk]) { u[pi] -= a * u[pk]; ++pi; ++pk; }
+                else if (o->wcol[pi] < o->wcol[pk]) ++pi;
+                else ++pk;
+            }
+        }
+        for (int64_t p = b; p < e; ++p) u[p] = u[p] / o->d[i];
+    }
+    /* v = D u, then backward sweep: (L + D)^T z = v */
+    for (int64_t oi = nF - 1; oi >= 0; --oi) {
+        int64_t i = ord[oi], g = o->frow[i];
+        int64_t b = o->wptr[i], e = o->wptr[i + 1];
+        for (int64_t p = b; p < e; ++p) z[p] = o->d[i] * u[p];
+        for (int64_t q = o->Arp[g]; q < o->Arp[g + 1]; ++q) {
+            int64_t c = o->Acol[q];
+            if (o->isc[c] || c == g) continue;
+            int64_t k = o->fid[c];
+            if (!sgs_before(o, i, k)) continue;
+            double a = o->Aval[q];
+            int64_t pi = b, pk = o->wptr[k], ek = o->wptr[k + 1];
+            while (pi < e && pk < ek) {
+                if (o->wcol[pi] == o->wcol[pk]) { z[pi] -= a * z[pk]; ++pi; ++pk; }
+                else if (o->wcol[pi] < o->wcol[pk]) ++pi;
+                else ++pk;
+            }
+        }
+        for (int64_t p = b; p < e; ++p) z[p] = z[p] / o->d[i];
+    }
+    free(ord);
+    free(u);
+}
+
+/* z = Pi_B M^{-1} x for the selected preconditioner (Alg. 3 line P:840). */
+void oracle_apply_prec(const oracle_t *o, const double *x, double *z) {
+    if (o->precond == 1) {
+        sgs_apply(o, x, z);
+        oracle_project(o, z, z);          /* mandatory for SGS */
+    } else {
+        for (int64_t i = 0; i < o->nF; ++i)
+            for (int64_t p = o->wptr[i]; p < o->wptr[i + 1]; ++p) z[p] = x[p] / o->d[i];
+        if (o->project_z) oracle_project(o, z, z);
+    }
+}
+
 static double dot_w(const oracle_t *o, const double *a, const double *b) {
     nsum_t s = {0.0, 0.0};
     for (int64_t p = 0; p < o->nnzW; ++p) nsum_add(&s, a[p] * b[p]);
@@ -358,7 +462,7 @@ void oracle_destroy(oracle_t *o) {
     free(o->Arp); free(o->Acol); free(o->Aval); free(o->isc); free(o->coarse_of);
     free(o->fid); free(o->frow); free(o->Prp); free(o->Pcol); free(o->wptr);
     free(o->wcol); free(o->Q); free(o->krank); free(o->d); free(o->w0); free(o->dw);
-    free(o->r); free(o->y); free(o->yb); free(o->z);
+    free(o->r); free(o->y); free(o->yb); free(o->z); free(o->sgs_key);
     free(o);
 }
 
@@ -368,12 +472,15 @@ int oracle_create(oracle_t **out, int64_t n, int64_t nc,
                   const uint8_t *is_coarse,
                   const int64_t *P_rowptr, const int32_t *P_col, const double *P_val,
                   int nv, const double *B, const double *Bc,
-                  double rank_tol, double tau, double stag, int project_z) {
+                  double rank_tol, double tau, double stag, int project_z,
+                  int precond, const int64_t *sgs_key) {
     *out = NULL;
     if (n <= 0 || nc < 0 || nv <= 0 || nv > 16) return OR_ERR_ARG;
     oracle_t *o = (oracle_t *)calloc(1, sizeof(oracle_t));
     o->n = n; o->nc = nc; o->nv = nv;
     o->rank_tol = rank_tol; o->tau = tau; o->stag = stag; o->project_z = project_z;
+    if (precond < 0 || precond > 1) { free(o); return OR_ERR_ARG; }
+    o->precond = precond;
     int64_t nnzA = A_rowptr[n];
     o->Arp = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
     o->Acol = (int32_t *)malloc(sizeof(int32_t) * (nnzA ? nnzA : 1));
@@ -405,6 +512,8 @@ int oracle_create(oracle_t **out, int64_t n, int64_t nc,
     o->nF = ff;
     o->frow = (int64_t *)malloc(sizeof(int64_t) * (ff ? ff : 1));
     for (int64_t r = 0; r < n; ++r) if (!is_coarse[r]) o->frow[o->fid[r]] = r;
+    o->sgs_key = (int64_t *)calloc(ff ? ff : 1, sizeof(int64_t));
+    if (sgs_key) for (int64_t i = 0; i < ff; ++i) o->sgs_key[i] = sgs_key[o->frow[i]];
     /* pattern: C row c must be exactly {coarse(c)}; F rows non-empty, sorted */
     int64_t nnzP = P_rowptr[n];
     o->Prp = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
@@ -509,10 +618,9 @@ int oracle_iterate(oracle_t *o, int kmax, int *k_done, double *dE) {
     for (int it = 0; it < kmax; ++it) {
         if (o->stopped) break;
         int64_t k = o->k_total + 1;
-        /* z = Pi M^-1 r, Jacobi M = A(i,i) per row block */
-        for (int64_t i = 0; i < o->nF; ++i)
-            for (int64_t p = o->wptr[i]; p < o->wptr[i + 1]; ++p) o->z[p] = o->r[p] / o->d[i];
-        if (o->project_z) oracle_project(o, o->z, o->z);
+        /* z = Pi M^-1 r: Jacobi M_1 = A(i,i) per row block
+         * or the projected SGS M_2 */
+        oracle_apply_prec(o, o->r, o->z);
         double gamma = dot_w(o, o->r, o->z);
         if (!(gamma > 0.0)) { o->stopped = OR_STOP_GAMMA; break; }
         if (k == 1) { for (int64_t p = 0; p < W; ++p) o->y[p] = o->z[p]; }

@@ -385,3 +385,121 @@ def test_validation_errors():
         Oracle(bad)
     assert e.value.code == 2
     Oracle(p)
+
+
+# --------------------------------------------------------------------------
+# Projected SGS preconditioner M_2
+# --------------------------------------------------------------------------
+
+def _dense_sgs_prec(prob, key):
+    """Pi (L+D)^{-T} D (L+D)^{-1} from the dense K (= H/2 of the dense trace,
+    block diagonal over coarse columns), L = the part of K below
+    the diagonal when each column block's unknowns are ordered by (key, row)
+    (reading A23), Pi = orthogonal projector onto ker(C) (the constraint
+    matrix of P B_c = B).  Library solves only."""
+    H, _, _ = D.quadratic_form(prob)
+    K = H / 2.0
+    r, j = D.w_entries(prob)
+    kk = np.zeros(prob.n, np.int64) if key is None else np.asarray(key)
+    rank = np.lexsort((r, kk[r]))            # position of each unknown in (key, row) order
+    pos = np.empty_like(rank)
+    pos[rank] = np.arange(rank.size)
+    same_col = j[:, None] == j[None, :]
+    before = pos[None, :] < pos[:, None]     # unknown f visited before unknown e
+    Lm = np.where(same_col & before, K, 0.0)
+    Dm = np.diag(np.diag(K))
+    Cm, _ = D.constraint_matrix(prob)
+    Rc = sla.orth(Cm.T)
+    Pi = np.eye(K.shape[0]) - Rc @ Rc.T
+    M = np.linalg.solve((Lm + Dm).T, Dm @ np.linalg.solve(Lm + Dm, np.eye(K.shape[0])))
+    return Pi @ M
+
+
+@pytest.mark.parametrize("name,size,kind", [("1b", 8, "natural"), ("1b", 8, "color"), ("3", 5, "natural"),
+                                            ("3", 5, "color"), ("4", 2, "natural"), ("4", 2, "color")])
+def test_sgs_apply_matches_dense_formula(name, size, kind):
+    """P:917-920 / P:933: z = Pi M_SGS^{-1} x, M_SGS^{-1} = (L+D)^{-T} D (L+D)^{-1}."""
+    from workloads.problems import sgs_key
+    prob = make_config(name, size=size)
+    key = sgs_key(prob, kind)
+    o = Oracle(prob, precond="sgs", sgs_key=key)
+    Md = _dense_sgs_prec(prob, key)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        x = rng.standard_normal(o.nnzW)
+        z = o.apply_prec(x)
+        ref = Md @ x
+        assert np.abs(z - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+def test_sgs_differs_from_jacobi_and_is_spd_on_range():
+    """M_SGS^{-1} is symmetric positive definite (K SPD); restricted to
+    range(Z) (Pi x = x) z^T x > 0, and it is not the Jacobi operator."""
+    prob = make_config("3", size=5)
+    o = Oracle(prob, precond="sgs")
+    oj = Oracle(prob, precond="jacobi", project_z=True)
+    rng = np.random.default_rng(5)
+    for _ in range(4):
+        x = o.project(rng.standard_normal(o.nnzW))
+        z = o.apply_prec(x)
+        assert z @ x > 0
+        assert np.abs(z - oj.apply_prec(x)).max() > 1e-3 * np.abs(z).max()
+    Md = _dense_sgs_prec(prob, None)
+    Cm, _ = D.constraint_matrix(prob)
+    Z = sla.null_space(Cm)
+    S = Z.T @ Md @ Z
+    assert np.allclose(S, S.T, atol=1e-12 * np.abs(S).max())
+    assert np.linalg.eigvalsh((S + S.T) / 2).min() > 0
+
+
+def test_sgs_reduces_to_jacobi_when_A_FF_is_diagonal():
+    """1D Laplacian, C = even points: F points couple only to C points, so
+    K's blocks are diagonal, L = 0 and M_SGS = D (= Jacobi M_1)."""
+    prob = make_config("1d", size=33)
+    oj = Oracle(prob, precond="jacobi", project_z=True, stagnation_rel=0.0)
+    os_ = Oracle(prob, precond="sgs", stagnation_rel=0.0)
+    kj, dEj = oj.iterate(10)
+    ks, dEs = os_.iterate(10)
+    assert kj == ks
+    assert np.allclose(dEj, dEs, rtol=1e-12, atol=0)
+    assert np.abs(oj.get_W() - os_.get_W()).max() <= 1e-13
+
+
+@pytest.mark.parametrize("name,size,kind", [("1b", 10, "natural"), ("3", 6, "color"), ("4", 2, "color")])
+def test_sgs_pcg_converges_to_kkt_monotone_constrained(name, size, kind):
+    """Same constrained minimiser as the dense KKT solve --
+    the preconditioner changes the path, not the solution; energy monotone
+    and telescoping and P B_c = B at every iterate."""
+    from workloads.problems import sgs_key
+    prob = make_config(name, size=size)
+    o = Oracle(prob, precond="sgs", sgs_key=sgs_key(prob, kind), stagnation_rel=1e-28)
+    Cm, b = D.constraint_matrix(prob)
+    E_prev = o.E0
+    tel = o.E0
+    for _ in range(200):
+        k, dE = o.iterate(1)
+        if k == 0:
+            break
+        w = o.get_W()
+        E = D.energy(prob, w)
+        assert E <= E_prev + 1e-12 * abs(E_prev)
+        tel -= dE[0]
+        assert abs(E - tel) <= 1e-10 * abs(o.E0)
+        assert np.abs(Cm @ w - b).max() <= 1e-12
+        E_prev = E
+    w_kkt = D.kkt_solution(prob)
+    assert np.abs(o.get_W() - w_kkt).max() <= 1e-8 * np.abs(w_kkt).max()
+
+
+@pytest.mark.parametrize("name,size", [("3", 8), ("4", 3), ("1b", 16)])
+def test_sgs_reduces_energy_faster_than_jacobi(name, size):
+    """with SGS the energy drops 'more than twice as fast' as
+    with Jacobi per iteration -- after 4 steps the remaining decrease
+    dE_4 / dE_1 is smaller."""
+    prob = make_config(name, size=size)
+    oj = Oracle(prob, precond="jacobi", project_z=True, stagnation_rel=0.0)
+    os_ = Oracle(prob, precond="sgs", stagnation_rel=0.0)
+    _, dEj = oj.iterate(4)
+    _, dEs = os_.iterate(4)
+    assert oj.E0 - dEs.sum() < oj.E0 - dEj.sum() + 1e-12 * abs(oj.E0)
+    assert dEs[3] / dEs[0] < 0.5 * dEj[3] / dEj[0]

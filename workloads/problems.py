@@ -619,3 +619,25 @@ def make_config(name: str, size: Optional[int] = None, seed: int = 0,
         return _elasticity_problem(f"5@{N}", N, 0.25, E, 40, start or "leastnorm",
                                    meta=dict(config="5", seed=seed, E_layers=El.tolist()))
     raise KeyError(name)
+
+
+def sgs_key(prob: Problem, kind: str = "natural") -> Optional[np.ndarray]:
+    """Ordering key (int64 per global row) for the SGS preconditioner's sweeps
+    (reading A23: the unknowns of each K block are visited in ascending
+    (key, row) order).  'natural': None (row order, the paper's enumeration).
+    'color': a proper colouring of the grid graph -- red-black (x + y + z) % 2
+    for the 5/7-point scalar stencils, the 8 parity classes (x%2, y%2, z%2) of
+    the 27-point node graph for elasticity (all 3 dofs of a node share the
+    node's colour) -- so that each sweep has few dependency levels."""
+    if kind == "natural":
+        return None
+    if kind != "color":
+        raise KeyError(kind)
+    nx, ny, nz = prob.meta["dims"]
+    nodes = np.arange(prob.n // prob.block_size)
+    x, y, z = nodes % nx, (nodes // nx) % ny, nodes // (nx * ny)
+    if prob.block_size == 1:
+        col = (x + y + z) % 2
+    else:
+        col = (x % 2) + 2 * (y % 2) + 4 * (z % 2)
+    return np.repeat(col, prob.block_size).astype(np.int64)
