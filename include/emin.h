@@ -76,7 +76,21 @@ typedef struct {
   void*   nccl_comm;            /* ncclComm_t or NULL (one GPU) */
   int64_t row_begin, row_end;   /* owned global rows; [0, n_global) on one GPU */
   int32_t inputs_on_device;     /* 1: the array arguments of emin_setup are device pointers */
+  int32_t precond;              /* EMIN_PREC_JACOBI: M_1 = diag(K), row-wise scaling;
+                                   EMIN_PREC_SGS: projected symmetric Gauss-Seidel
+                                   M_2^-1 = Z^T (L+D)^-T D (L+D)^-1 Z, applied
+                                   matrix-free as a forward and a backward sweep over the F rows
+                                    and always followed by Pi_B.  SGS needs one GPU
+                                   (nccl_comm = NULL), else EMIN_ERR_ARG. */
+  const int64_t* sgs_key;       /* nullable, [m] per owned row: SGS visits the unknowns of each
+                                   K block (coarse column) in ascending (key, global
+                                   row) order (reading A23); NULL = natural row order.  Host or
+                                   device pointer as the other arrays.  A colouring key makes the
+                                   sweeps short (few dependency levels). */
 } emin_opts;
+
+#define EMIN_PREC_JACOBI 0
+#define EMIN_PREC_SGS 1
 
 typedef struct {
   double  E0;          /* tr(P0^T A P0) after Alg. 2 */
@@ -90,10 +104,12 @@ typedef struct {
   int32_t kernel_path; /* 0 generic warp-per-row, 1 scalar lane-per-entry, 2 nodal 3x3 */
   int32_t nranks;
   int64_t launches;    /* kernels this context has enqueued so far (setup included) */
+  int32_t precond;     /* EMIN_PREC_JACOBI or EMIN_PREC_SGS */
+  int64_t sgs_levels;  /* dependency levels of one SGS sweep (0 for Jacobi) */
 } emin_report_t;
 
 /* Fill opts with defaults (rank_tol 1e-10, tau 0, project_after_jacobi 0,
- * stagnation_rel 1e-30, block_size 1, one GPU over [0, n_global)). */
+ * stagnation_rel 1e-30, block_size 1, one GPU over [0, n_global), Jacobi). */
 void emin_default_opts(emin_opts* opts, int64_t n_global);
 
 /* Alg. 2 + the start of Alg. 3:

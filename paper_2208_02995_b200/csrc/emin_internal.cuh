@@ -33,6 +33,7 @@ struct DevState {
 };
 
 struct DistPlan;
+struct SgsPlan;
 
 // Error flag bits raised by the validation kernels.
 enum : int32_t {
@@ -87,6 +88,7 @@ struct emin_ctx_s {
   int32_t* erow = nullptr;     // F-row id of every W entry (streaming stages)
   double* dinv = nullptr;      // 1 / A(i,i) per owned F row
   DistPlan* dist = nullptr;    // multi-GPU halo plan (dist.cu), null on one GPU
+  SgsPlan* sgs = nullptr;      // SGS preconditioner plan (sgs.cu), null for Jacobi
   int breakdown_reported = 0;
   int32_t *wcol = nullptr, *affcol = nullptr, *afccol = nullptr;
   double *affval = nullptr, *afcval = nullptr, *d = nullptr, *Q = nullptr;
@@ -254,3 +256,10 @@ cudaError_t emin_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* t
 int64_t emin_scan_scratch_elems(int64_t n);
 
 int emin_num_sms();
+
+// projected SGS preconditioner (sgs.cu)
+emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* frow, cudaStream_t s);
+int emin_sgs_enqueue(emin_ctx c, cudaStream_t s);
+void emin_sgs_stage2(emin_ctx c, cudaStream_t s);
+void emin_sgs_free(emin_ctx c);
+int64_t emin_sgs_levels(emin_ctx c);

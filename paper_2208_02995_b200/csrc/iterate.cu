@@ -579,15 +579,19 @@ static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev, int e
   // profiles/r01b/spgemm_ab_c3.txt)
   const char* fz = getenv("EMIN_FUSE");
   c->fuse = (!c->dist && fz && !strcmp(fz, "1")) ? 1 : 0;
+  if (c->sgs) c->fuse = 0;
   rec(0);
-  launch_stage(c, 1, s);
+  int g1 = c->grid_rows;
+  if (c->sgs) g1 = emin_sgs_enqueue(c, s);   // z = Pi M_2^-1 r, partial r.z
+  else launch_stage(c, 1, s);
   rec(1);
   if (!c->fuse) {
-    const auto r1 = global_sum(c, c->grid_rows, 0, s);
+    const auto r1 = global_sum(c, g1, 0, s);
     k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, r1.first, r1.second);
   }
   rec(2);
-  launch_stage(c, 2, s);
+  if (c->sgs) emin_sgs_stage2(c, s);
+  else launch_stage(c, 2, s);
   if (c->dist) emin_dist_halo_values(c, c->y, s);     // y on the halo rows
   rec(3);
   const int g = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
@@ -600,7 +604,7 @@ static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev, int e
   // kernels of ours per iteration: stage I, stage II, SpGEMM (+ the two
   // scalar kernels, + on several GPUs their rank-local sum kernels and the
   // halo pack)
-  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 3 : 0);
+  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 3 : 0) + (c->sgs ? (int32_t)(2 * emin_sgs_levels(c)) : 0);
 }
 
 // One iteration captured as a CUDA graph (5 kernel nodes, cheap to
@@ -820,6 +824,8 @@ extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
   rep->kernel_path = c->kernel_path;
   rep->nranks = c->nranks;
   rep->launches = c->launches;
+  rep->precond = c->opts.precond;
+  rep->sgs_levels = emin_sgs_levels(c);
   if (h.stopped == 5 && !c->breakdown_reported) {
     c->breakdown_reported = 1;
     return EMIN_ERR_BREAKDOWN;
@@ -872,6 +878,7 @@ void emin_free_all(emin_ctx c) {
     c->nodal = nullptr;
   }
   emin_dist_free(c);
+  emin_sgs_free(c);
   cudaStreamSynchronize(s);
 }
 

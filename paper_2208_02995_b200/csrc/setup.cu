@@ -475,6 +475,8 @@ extern "C" void emin_default_opts(emin_opts* o, int64_t n_global) {
   o->row_begin = 0;
   o->row_end = n_global;
   o->inputs_on_device = 0;
+  o->precond = EMIN_PREC_JACOBI;
+  o->sgs_key = nullptr;
 }
 
 static emin_status fail(emin_ctx ctx, emin_status st, const std::string& msg) {
@@ -521,6 +523,10 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     return fail(ctx, EMIN_ERR_ARG, "bad row range");
   if (n_global > INT32_MAX || nc_global > INT32_MAX)
     return fail(ctx, EMIN_ERR_ARG, "n_global exceeds the int32 column range");
+  if (opts->precond != EMIN_PREC_JACOBI && opts->precond != EMIN_PREC_SGS)
+    return fail(ctx, EMIN_ERR_ARG, "precond must be EMIN_PREC_JACOBI or EMIN_PREC_SGS");
+  if (opts->precond == EMIN_PREC_SGS && opts->nccl_comm)
+    return fail(ctx, EMIN_ERR_ARG, "the SGS preconditioner runs on one GPU (nccl_comm must be NULL)");
 
   {
     // keep freed blocks in the stream-ordered pool (repeated setups reuse them)
@@ -751,6 +757,10 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     if (pst != EMIN_OK) { tmp_free(); return fail(ctx, pst, ctx->last_error); }
   }
 
+  if (opts->precond == EMIN_PREC_SGS) {
+    emin_status sst = emin_sgs_plan(ctx, opts->sgs_key, frow, s);
+    if (sst != EMIN_OK) { tmp_free(); return fail(ctx, sst, ctx->last_error); }
+  }
   trace.mark(s, "kernel plan");
   // ---- Alg. 2
   // w0, dw, y carry the halo tail (values of other ranks' rows)

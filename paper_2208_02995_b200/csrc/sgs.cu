@@ -1,0 +1,305 @@
+// sgs.cu -- projected symmetric Gauss-Seidel preconditioner M_2 of Alg. 3
+// (SURVEY §8f NEXT-1), selected with emin_opts.precond = 1.
+//
+//   z = Pi M_SGS^{-1} r,  M_SGS^{-1} = (L+D)^{-T} D (L+D)^{-1},  K = L + D + L^T
+//
+// K is block diagonal over the coarse columns j of W, block j = A(I_j, I_j)
+// (Eq. 11blk), so one forward (L+D) solve updates every column at
+// once, row by row:
+//   u(i,j) = (r(i,j) - sum_{k before i} A(i,k) u(k,j)) / A(i,i)
+// and the backward (L+D)^T solve, with v = D u,
+//   z(i,j) = (v(i,j) - sum_{k after i} A(k,i) z(k,j)) / A(i,i),  A(k,i) = A(i,k),
+// both matrix-free on the W layout exactly like the masked product (P:996-
+// 1004: "the symmetric Gauss-Seidel step is then performed matrix-free,
+// similar to the A P product").  "before" = ascending (sgs_key, row)
+// (reading A23; key NULL = natural row order).
+//
+// GPU schedule: at setup the F rows get a dependency level (longest chain of
+// predecessors in the A_FF graph, by in-place relaxation passes) and are
+// bucketed by level; the forward sweep is one kernel per level ascending, the
+// backward one per level descending, warp per row, lane per pattern position.
+// A colouring key (red-black for 7-point operators, 8 parity classes of the
+// 27-point node graph) gives 2-24 levels; the natural order gives O(grid
+// diameter) levels.  The pending r update of the previous step is applied by
+// the forward kernel (each row exactly once), Pi and the partial r.z by one
+// row-parallel kernel.  Single GPU (the sweeps are sequential across ranks).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "emin_internal.cuh"
+
+struct SgsPlan {
+  int64_t* key = nullptr;        // [nF] ordering key of each F row
+  int32_t* lev = nullptr;        // [nF] dependency level
+  int32_t* lvl_rows = nullptr;   // [nF] F rows bucketed by level
+  int32_t* lvl_cnt = nullptr;    // [nlev + 1] scratch
+  std::vector<int64_t> lvl_ptr;  // host [nlev + 1]
+  int64_t nlev = 0;
+  double* u = nullptr;           // [nnzW] u, then z in place
+};
+
+namespace {
+
+constexpr int SGS_MAXC = EMIN_MAX_ROW / 32;   // pattern chunks of 32 lanes
+
+__device__ __forceinline__ bool sgs_before(const int64_t* __restrict__ key, int32_t k, int32_t i) {
+  const int64_t a = key[k], b = key[i];
+  return a != b ? a < b : k < i;     // F index order = global row order
+}
+
+__global__ void k_sgs_key(int64_t nF, const int64_t* __restrict__ frow, const int64_t* __restrict__ key_own,
+                          int64_t* __restrict__ key) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+    key[i] = key_own ? key_own[frow[i]] : 0;
+}
+
+// one relaxation pass of lev(i) = max over predecessors k of lev(k) + 1
+// (in place: a pass propagates along every chain the grid happens to visit
+// in order; repeated until no level changes)
+__global__ void k_sgs_levels(DevView v, const int64_t* __restrict__ key, int32_t* lev, int32_t* changed) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v.nF; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t m = 0;
+    for (int64_t q = v.affptr[i]; q < v.affptr[i + 1]; ++q) {
+      const int32_t k = v.affcol[q];
+      if (k != (int32_t)i && sgs_before(key, k, (int32_t)i)) m = max(m, ((volatile int32_t*)lev)[k] + 1);
+    }
+    if (m > lev[i]) {
+      lev[i] = m;
+      *changed = 1;
+    }
+  }
+}
+
+__global__ void k_sgs_count(int64_t nF, const int32_t* __restrict__ lev, int32_t* cnt, int32_t* maxlev) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(&cnt[lev[i]], 1);
+    atomicMax(maxlev, lev[i]);
+  }
+}
+
+__global__ void k_sgs_scatter(int64_t nF, const int32_t* __restrict__ lev, int32_t* cursor, int32_t* rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+    rows[atomicAdd(&cursor[lev[i]], 1)] = (int32_t)i;
+}
+
+// Forward (L+D) solve on the rows of one level (FWD) or backward (L+D)^T
+// solve (!FWD), warp per row, lane per pattern position t (chunks of 32).
+//   FWD:  x = r [- alpha_pend yb, written back]; u = (x - sum_pred A u) / d
+//   !FWD: z = (d u - sum_succ A z) / d, in place over u
+template <bool FWD>
+__global__ void __launch_bounds__(256)
+k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restrict__ rows, int32_t nrows,
+            double* __restrict__ r, const double* __restrict__ yb, double* u) {
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = FWD ? st->pend : 0;
+  const double ap = st->alpha_pend;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = gw; w < nrows; w += nw) {
+    const int32_t i = rows[w];
+    const int64_t b = v.wptr[i];
+    const int nj = (int)(v.wptr[i + 1] - b);
+    const double di = v.d[i];
+    double acc[SGS_MAXC];
+    int32_t jt[SGS_MAXC];
+#pragma unroll
+    for (int c = 0; c < SGS_MAXC; ++c) {
+      const int t = lane + 32 * c;
+      jt[c] = t < nj ? v.wcol[b + t] : -1;
+      double x = 0.0;
+      if (t < nj) {
+        if (FWD) {
+          x = r[b + t];
+          if (pend) { x = x - ap * yb[b + t]; r[b + t] = x; }
+        } else {
+          x = di * u[b + t];                    // v = D u
+        }
+      }
+      acc[c] = x;
+    }
+    for (int64_t q = v.affptr[i]; q < v.affptr[i + 1]; ++q) {
+      const int32_t k = v.affcol[q];
+      if (k == i) continue;
+      if (FWD != sgs_before(key, k, i)) continue;   // FWD: predecessors, else successors
+      const double a = v.affval[q];
+      const int64_t kb = v.wptr[k];
+      const int nk = (int)(v.wptr[k + 1] - kb);
+#pragma unroll
+      for (int c = 0; c < SGS_MAXC; ++c) {
+        if (jt[c] >= 0) {
+          const int p = lower_bound_i32(v.wcol + kb, nk, jt[c]);
+          if (p < nk && v.wcol[kb + p] == jt[c]) acc[c] -= a * u[kb + p];
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < SGS_MAXC; ++c) {
+      const int t = lane + 32 * c;
+      if (t < nj) u[b + t] = acc[c] / di;
+    }
+  }
+}
+
+// z <- Pi z (per row, Q_i), partial r . z  (Alg. 3 lines P:840-841)
+__global__ void __launch_bounds__(256)
+k_sgs_project(DevView v, const double* __restrict__ r, double* __restrict__ z, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nv = v.nv;
+  double part = 0.0;
+  for (int64_t i = gw; i < v.nF; i += nw) {
+    const int64_t b = v.wptr[i];
+    const int nj = (int)(v.wptr[i + 1] - b);
+    double dots[EMIN_NV_MAX];
+#pragma unroll
+    for (int m = 0; m < EMIN_NV_MAX; ++m) dots[m] = 0.0;
+    for (int t = lane; t < nj; t += 32) {
+      const double zt = z[b + t];
+#pragma unroll
+      for (int m = 0; m < EMIN_NV_MAX; ++m)
+        if (m < nv) dots[m] = fma(v.Q[(b + t) * nv + m], zt, dots[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < EMIN_NV_MAX; ++m)
+      if (m < nv) dots[m] = warp_sum(dots[m]);
+    for (int t = lane; t < nj; t += 32) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < EMIN_NV_MAX; ++m)
+        if (m < nv) s = fma(v.Q[(b + t) * nv + m], dots[m], s);
+      const double zt = z[b + t] - s;
+      z[b + t] = zt;
+      part = fma(r[b + t], zt, part);
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// stage II with a stored z: dw += alpha_pend y_old ; y = z + beta y_old
+__global__ void __launch_bounds__(256)
+k_sgs_stage2(DevView v, const double* __restrict__ z, double* __restrict__ y, double* __restrict__ dw) {
+  const DevState* st = v.st;
+  const int stopped = st->stopped;
+  const int pendw = st->pendw;
+  if (stopped && !pendw) return;
+  const double ap = st->alpha_pend;
+  const double beta = st->beta;
+  const bool first = (st->k_total == 0);
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.nnzW; p += (int64_t)gridDim.x * blockDim.x) {
+    const double yo = y[p];
+    if (pendw) dw[p] = dw[p] + ap * yo;
+    if (!stopped) y[p] = first ? z[p] : z[p] + beta * yo;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* frow, cudaStream_t s) {
+  SgsPlan* p = new SgsPlan();
+  c->sgs = p;
+  const int64_t nF = c->nF;
+  const int SM = emin_num_sms();
+  const int64_t* dkey = key_own;
+  int64_t* tmp = nullptr;
+  if (key_own && !c->opts.inputs_on_device) {
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&tmp, sizeof(int64_t) * std::max<int64_t>(c->m_owned, 1), s));
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(tmp, key_own, sizeof(int64_t) * c->m_owned, cudaMemcpyHostToDevice, s));
+    dkey = tmp;
+  }
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->key, sizeof(int64_t) * std::max<int64_t>(nF, 1), s));
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lev, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lvl_rows, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->u, sizeof(double) * std::max<int64_t>(c->nnzW, 1) + 64, s));
+  int32_t* flag;
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&flag, sizeof(int32_t) * 2, s));
+  k_sgs_key<<<SM * 4, 256, 0, s>>>(nF, frow, dkey, p->key);
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lev, 0, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
+  c->launches += 1;
+  // relaxation passes until no level changes (<= longest chain + 1)
+  for (int64_t pass = 0; pass <= nF; ++pass) {
+    int32_t h = 0;
+    EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+    k_sgs_levels<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->lev, flag);
+    c->launches += 1;
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(&h, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (!h) break;
+  }
+  // bucket the rows by level
+  int32_t hmax = 0;
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(flag + 1, 0, sizeof(int32_t), s));
+  // count into a buffer of nF + 1 (levels <= nF - 1)
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lvl_cnt, sizeof(int32_t) * (nF + 2), s));
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lvl_cnt, 0, sizeof(int32_t) * (nF + 2), s));
+  k_sgs_count<<<SM * 4, 256, 0, s>>>(nF, p->lev, p->lvl_cnt, flag + 1);
+  EMIN_CUDA_TRY(c, cudaMemcpyAsync(&hmax, flag + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+  p->nlev = nF > 0 ? (int64_t)hmax + 1 : 0;
+  std::vector<int32_t> hc((size_t)p->nlev + 1, 0);
+  if (p->nlev)
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(hc.data(), p->lvl_cnt, sizeof(int32_t) * p->nlev, cudaMemcpyDeviceToHost, s));
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+  p->lvl_ptr.assign((size_t)p->nlev + 1, 0);
+  for (int64_t L = 0; L < p->nlev; ++L) p->lvl_ptr[L + 1] = p->lvl_ptr[L] + hc[L];
+  std::vector<int32_t> cur(p->lvl_ptr.begin(), p->lvl_ptr.end() - (p->nlev ? 1 : 0));
+  if (p->nlev) {
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(p->lvl_cnt, cur.data(), sizeof(int32_t) * p->nlev, cudaMemcpyHostToDevice, s));
+    k_sgs_scatter<<<SM * 4, 256, 0, s>>>(nF, p->lev, p->lvl_cnt, p->lvl_rows);
+  }
+  c->launches += 2;
+  cudaFreeAsync(flag, s);
+  if (tmp) cudaFreeAsync(tmp, s);
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+  EMIN_CUDA_TRY(c, cudaGetLastError());
+  return EMIN_OK;
+}
+
+int64_t emin_sgs_levels(emin_ctx c) { return c->sgs ? c->sgs->nlev : 0; }
+
+// z = Pi M_SGS^{-1} r and the partial sums of r.z (in c->partials); returns
+// the grid of the projection kernel (= number of partials)
+int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
+  SgsPlan* p = c->sgs;
+  const DevView v = c->view();
+  const int SM = emin_num_sms();
+  auto grid_for = [&](int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)SM * 8));
+  };
+  for (int64_t L = 0; L < p->nlev; ++L) {
+    const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
+    k_sgs_sweep<true><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb,
+                                                 p->u);
+  }
+  for (int64_t L = p->nlev - 1; L >= 0; --L) {
+    const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
+    k_sgs_sweep<false><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb,
+                                                  p->u);
+  }
+  const int g = grid_for(c->nF);
+  k_sgs_project<<<g, 256, 0, s>>>(v, c->r, p->u, c->partials);
+  return g;
+}
+
+void emin_sgs_stage2(emin_ctx c, cudaStream_t s) {
+  const int SM = emin_num_sms();
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * 8));
+  k_sgs_stage2<<<g, 256, 0, s>>>(c->view(), c->sgs->u, c->y, c->dw);
+}
+
+void emin_sgs_free(emin_ctx c) {
+  SgsPlan* p = c->sgs;
+  if (!p) return;
+  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u};
+  for (void* q : ptrs)
+    if (q) cudaFreeAsync(q, c->stream);
+  delete p;
+  c->sgs = nullptr;
+}

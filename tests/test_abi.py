@@ -77,3 +77,18 @@ def test_missing_library_fails_loudly(tmp_path):
             (ROOT, str(tmp_path / "nope.so")))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     assert "raised" in out.stdout, out.stderr
+
+
+def test_opts_and_report_layout_match_header():
+    """The ctypes mirrors of emin_opts / emin_report_t have the C sizes."""
+    import ctypes as C
+    import subprocess
+    import tempfile
+    from paper_2208_02995_b200 import emin as E
+    src = ('#include <stdio.h>\n#include "%s/include/emin.h"\n'
+           'int main(){printf("%%zu %%zu", sizeof(emin_opts), sizeof(emin_report_t));}\n' % ROOT)
+    with tempfile.TemporaryDirectory() as d:
+        open(os.path.join(d, "s.c"), "w").write(src)
+        subprocess.check_call(["gcc", os.path.join(d, "s.c"), "-o", os.path.join(d, "s")])
+        out = subprocess.check_output([os.path.join(d, "s")]).decode().split()
+    assert [int(x) for x in out] == [C.sizeof(E.emin_opts), C.sizeof(E.emin_report_t)]
