@@ -199,6 +199,10 @@ def main():
     ap.add_argument("--impl", default="emin", choices=["emin", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "sgs"],
+                    help="Alg. 3 preconditioner: Jacobi M_1 (default, the headline) or projected SGS M_2")
+    ap.add_argument("--sgs-key", default="color", choices=["color", "natural"],
+                    help="SGS visiting order (reading A23): a grid colouring or the natural row order")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -248,13 +252,22 @@ def main():
     k_it = prob.iters
     nnzW_global = prob.nnz_W
 
+    key = None
+    if args.precond == "sgs":
+        from workloads.problems import sgs_key
+        key = sgs_key(prob, args.sgs_key)
+    host["sgs_key"] = key
+    dev["sgs_key"] = None if key is None else torch.from_numpy(key).cuda()
+
     def setup(arrs):
         nv = prob.nv
+        kk = arrs["sgs_key"]
         return E.emin_setup(prob.n, prob.nc, arrs["A_rowptr"][rb:re_ + 1], arrs["A_col"], arrs["A_val"],
                             arrs["is_coarse"], arrs["P_rowptr"][rb:re_ + 1], arrs["P_col"], arrs["P_val"],
                             nv, arrs["B"][rb:re_], arrs["Bc"], block_size=prob.block_size,
                             stagnation_rel=0.0, stream=stream.cuda_stream, nccl_comm=comm,
-                            row_begin=rb, row_end=re_)
+                            row_begin=rb, row_end=re_, precond=args.precond,
+                            sgs_key=None if kk is None else kk[rb:re_])
 
     stats = {"launches": 0, "spgemm_ms": 0.0, "spgemm_n": 0, "stage_ms": [0.0, 0.0], "scalar_ms": 0.0,
              "k_done": 0, "E": None, "report": None}
@@ -407,7 +420,9 @@ def main():
                    "step": "emin_setup(device inputs) + emin_iterate(k) + emin_energy + emin_get_P + emin_destroy",
                    "l2": "inputs larger than L2 (per-iteration working set %.2f GB > 126 MB)" % (it_bytes / 1e9),
                    "parallelism": f"rows{world}" if world > 1 else "single GPU",
-                   "kernel_path": E.KERNEL_PATHS.get(stats["report"]["kernel_path"])},
+                   "kernel_path": E.KERNEL_PATHS.get(stats["report"]["kernel_path"]),
+                   "precond": args.precond if args.precond == "jacobi" else
+                   f"sgs ({args.sgs_key} order, {stats['report']['sgs_levels']} levels per sweep)"},
         "roofline": roofline,
         "iter_only": {"value": nnzW_global * k_it / (it_ms_med / 1e3), "unit": UNIT,
                       "ms_per_iter": it_ms_med / k_it,

@@ -263,3 +263,5 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s);
 void emin_sgs_stage2(emin_ctx c, cudaStream_t s);
 void emin_sgs_free(emin_ctx c);
 int64_t emin_sgs_levels(emin_ctx c);
+const int4* emin_scalar_records(emin_ctx c);   // iterate.cu
+const int32_t* emin_scalar_windows(emin_ctx c, int64_t* nwin);

@@ -530,6 +530,19 @@ emin_status emin_plan(emin_ctx c) {
   return EMIN_OK;
 }
 
+// the scalar path's per-A_FF-entry records {a, wptr[k], pm} (diagonal first
+// per row, then A's column order), or null off the scalar path (sgs.cu)
+const int4* emin_scalar_records(emin_ctx c) {
+  return c->kernel_path == 1 ? reinterpret_cast<const int4*>(fast_of(c)->sc.ent) : nullptr;
+}
+// the scalar path's window plan: rows [rowstart[w], rowstart[w+1]) of window
+// w hold <= 32 entries (sgs.cu)
+const int32_t* emin_scalar_windows(emin_ctx c, int64_t* nwin) {
+  if (c->kernel_path != 1) { *nwin = 0; return nullptr; }
+  *nwin = fast_of(c)->sc.nwin;
+  return fast_of(c)->sc.rowstart;
+}
+
 // Alg. 2 on a specialised path (false: use the generic warp kernel)
 bool emin_alg2_fast(emin_ctx c, const double* Bc, const double* B, const int64_t* frow, const double* what,
                     unsigned long long* counters, cudaStream_t s) {

@@ -24,6 +24,7 @@
 // the forward kernel (each row exactly once), Pi and the partial r.z by one
 // row-parallel kernel.  Single GPU (the sweeps are sequential across ranks).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -37,6 +38,12 @@ struct SgsPlan {
   std::vector<int64_t> lvl_ptr;  // host [nlev + 1]
   int64_t nlev = 0;
   double* u = nullptr;           // [nnzW] u, then z in place
+  // scalar-path fast sweeps (kernel_path 1): lane per W entry over windows
+  // of <= 32 entries built from each level's row list
+  const int4* rec = nullptr;     // the scalar path's A_FF records (not owned)
+  uint8_t* dir = nullptr;        // [nnzAFF] per record: 0 diagonal, 1 predecessor, 2 successor
+  int4* win = nullptr;           // [nwin] {j0 (into lvl_rows), head mask, nent, nrows}
+  std::vector<int64_t> win_ptr;  // host [nlev + 1] window range of each level
 };
 
 namespace {
@@ -71,16 +78,33 @@ __global__ void k_sgs_levels(DevView v, const int64_t* __restrict__ key, int32_t
   }
 }
 
+// level histogram / bucketing with warp-aggregated atomics (few levels =>
+// every lane of a warp hits the same counter)
 __global__ void k_sgs_count(int64_t nF, const int32_t* __restrict__ lev, int32_t* cnt, int32_t* maxlev) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x) {
-    atomicAdd(&cnt[lev[i]], 1);
-    atomicMax(maxlev, lev[i]);
+  int32_t mx = 0;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nF; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const int32_t L = i < nF ? lev[i] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, L);
+    if (L >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&cnt[L], __popc(grp));
+    mx = max(mx, L);
   }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxlev, mx);
 }
 
 __global__ void k_sgs_scatter(int64_t nF, const int32_t* __restrict__ lev, int32_t* cursor, int32_t* rows) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
-    rows[atomicAdd(&cursor[lev[i]], 1)] = (int32_t)i;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nF; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const int32_t L = i < nF ? lev[i] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, L);
+    const int leader = __ffs(grp) - 1;
+    int32_t base = 0;
+    if (L >= 0 && lane == leader) base = atomicAdd(&cursor[L], __popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    if (L >= 0) rows[base + __popc(grp & ((1u << lane) - 1u))] = (int32_t)i;
+  }
 }
 
 // Forward (L+D) solve on the rows of one level (FWD) or backward (L+D)^T
@@ -143,6 +167,76 @@ k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restric
   }
 }
 
+// record directions for the windowed sweeps: the scalar path stores row i's
+// records diagonal first, then A's column order (k_plan_entries)
+__global__ void k_sgs_dir(DevView v, const int64_t* __restrict__ key, uint8_t* __restrict__ dir) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v.nF; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
+    int64_t qd = qb;
+    for (int64_t q = qb; q < qe; ++q)
+      if (v.affcol[q] == (int32_t)i) { qd = q; break; }
+    for (int64_t q = qb; q < qe; ++q) {
+      const int64_t dst = (q == qd) ? qb : (q < qd ? q + 1 : q);
+      const int32_t k = v.affcol[q];
+      dir[dst] = (k == (int32_t)i) ? 0 : (sgs_before(key, k, (int32_t)i) ? 1 : 2);
+    }
+  }
+}
+
+// The same sweep as k_sgs_sweep, lane per W entry (the scalar path's window
+// decode of k_spgemm_win2): window {j0, head, nent, nrows} covers rows
+// lvl_rows[j0 .. j0 + nrows) of one level, head bit p set where a row starts.
+// Records are the scalar path's {a, wptr[k], pm} (pm nibble t = position of
+// J_i[t] in J_k), filtered by dir.  Same order of operations as k_sgs_sweep.
+template <bool FWD>
+__global__ void __launch_bounds__(256)
+k_sgs_sweep_win(DevView v, const int4* __restrict__ A4, const uint8_t* __restrict__ dir,
+                const int4* __restrict__ win, int32_t nwin, const int32_t* __restrict__ rows,
+                double* __restrict__ r, const double* __restrict__ yb, double* u) {
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = FWD ? st->pend : 0;
+  const double ap = st->alpha_pend;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint8_t want = FWD ? 1 : 2;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int4 h = __ldg(win + w);
+    const unsigned H = (unsigned)h.y;
+    const int nent = h.z;
+    const bool act = lane < nent;
+    const int l = act ? lane : nent - 1;
+    const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+    const unsigned hu = H & upto;
+    const int rloc = __popc(hu) - 1;
+    const int rowbeg = 31 - __clz(hu);
+    if (!act) continue;
+    const int32_t i = rows[h.x + rloc];
+    const int pos = lane - rowbeg;
+    const int64_t e = v.wptr[i] + pos;
+    const double di = v.d[i];
+    double acc;
+    if (FWD) {
+      double x = r[e];
+      if (pend) { x = x - ap * yb[e]; r[e] = x; }
+      acc = x;
+    } else {
+      acc = di * u[e];                          // v = D u
+    }
+    const int qb = (int)v.affptr[i], qe = (int)v.affptr[i + 1];
+    const unsigned sh4 = 4u * (unsigned)pos;
+#pragma unroll 4
+    for (int q = qb + 1; q < qe; ++q) {         // record qb is the diagonal
+      if (__ldg(dir + q) != want) continue;
+      const int4 en = __ldg(A4 + q);
+      const unsigned sidx = ((unsigned)en.w >> sh4) & 0xFu;
+      if (sidx != 0xFu) acc -= __hiloint2double(en.y, en.x) * u[en.z + (int)sidx];
+    }
+    u[e] = acc / di;
+  }
+}
+
 // z <- Pi z (per row, Q_i), partial r . z  (Alg. 3 lines P:840-841)
 __global__ void __launch_bounds__(256)
 k_sgs_project(DevView v, const double* __restrict__ r, double* __restrict__ z, double* __restrict__ partials) {
@@ -176,6 +270,55 @@ k_sgs_project(DevView v, const double* __restrict__ r, double* __restrict__ z, d
       const double zt = z[b + t] - s;
       z[b + t] = zt;
       part = fma(r[b + t], zt, part);
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+// z <- Pi z, partial r . z on the scalar path (nv = 1): lane per W entry on
+// the scalar window plan, row sums of q z through shared memory in a fixed
+// order (the projection of k_spgemm_win2)
+__global__ void __launch_bounds__(256)
+k_sgs_project_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const double* __restrict__ r,
+                  double* __restrict__ z, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qz[8][32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part = 0.0;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int r0 = rowstart[w];
+    const int nrows = rowstart[w + 1] - r0;
+    if (nrows == 0) continue;                          // warp-uniform
+    const int myptr = (lane <= nrows) ? (int)v.wptr[r0 + lane] : 0;
+    const int base = __shfl_sync(0xffffffffu, myptr, 0);
+    const int nent = __shfl_sync(0xffffffffu, myptr, nrows) - base;
+    const unsigned H = __reduce_or_sync(0xffffffffu, (lane < nrows) ? (1u << (unsigned)(myptr - base)) : 0u);
+    const bool act = lane < nent;
+    const int l = act ? lane : nent - 1;
+    const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+    const unsigned hu = H & upto;
+    const int rowbeg = 31 - __clz(hu);
+    const unsigned after = H & ~upto;
+    const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+    const int e = base + lane;
+    const double qv = act ? v.Q[e] : 0.0;
+    const double zv = act ? z[e] : 0.0;
+    s_qz[wib][lane] = qv * zv;
+    __syncwarp();
+    double dot = 0.0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)                       // |J_i| <= 8 on the scalar path
+      if (p < rowlen) dot += s_qz[wib][rowbeg + p];
+    __syncwarp();
+    if (act) {
+      const double zt = zv - qv * dot;
+      z[e] = zt;
+      part = fma(r[e], zt, part);
     }
   }
   const double tot = block_sum(part, sh);
@@ -255,6 +398,44 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
     k_sgs_scatter<<<SM * 4, 256, 0, s>>>(nF, p->lev, p->lvl_cnt, p->lvl_rows);
   }
   c->launches += 2;
+  // scalar path: per-level windows of <= 32 entries (rows never straddle)
+  p->rec = emin_scalar_records(c);
+  if (p->rec && p->nlev && !getenv("EMIN_SGS_GENERIC")) {
+    std::vector<int32_t> hrows((size_t)nF);
+    std::vector<int64_t> hwptr((size_t)nF + 1);
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(hrows.data(), p->lvl_rows, sizeof(int32_t) * nF, cudaMemcpyDeviceToHost, s));
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(hwptr.data(), c->wptr, sizeof(int64_t) * (nF + 1), cudaMemcpyDeviceToHost, s));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+    std::vector<int4> hw;
+    p->win_ptr.assign((size_t)p->nlev + 1, 0);
+    for (int64_t L = 0; L < p->nlev; ++L) {
+      int64_t j = p->lvl_ptr[L];
+      const int64_t je = p->lvl_ptr[L + 1];
+      while (j < je) {
+        int4 wv = make_int4((int)j, 0, 0, 0);
+        int ne = 0;
+        while (j < je) {
+          const int len = (int)(hwptr[hrows[j] + 1] - hwptr[hrows[j]]);
+          if (ne + len > 32) break;
+          wv.y |= (int)(1u << ne);
+          ne += len;
+          ++wv.w;
+          ++j;
+        }
+        wv.z = ne;
+        hw.push_back(wv);
+      }
+      p->win_ptr[L + 1] = (int64_t)hw.size();
+    }
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->win, sizeof(int4) * std::max<size_t>(hw.size(), 1), s));
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(p->win, hw.data(), sizeof(int4) * hw.size(), cudaMemcpyHostToDevice, s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->dir, std::max<int64_t>(c->nnzAFF, 1), s));
+    k_sgs_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->dir);
+    c->launches += 1;
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));   // hw leaves scope
+  } else {
+    p->rec = nullptr;
+  }
   cudaFreeAsync(flag, s);
   if (tmp) cudaFreeAsync(tmp, s);
   EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -273,15 +454,35 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   auto grid_for = [&](int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)SM * 8));
   };
-  for (int64_t L = 0; L < p->nlev; ++L) {
-    const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
-    k_sgs_sweep<true><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb,
-                                                 p->u);
+  if (p->rec) {
+    for (int64_t L = 0; L < p->nlev; ++L) {
+      const int64_t n = p->win_ptr[L + 1] - p->win_ptr[L];
+      k_sgs_sweep_win<true><<<grid_for(n), 256, 0, s>>>(v, p->rec, p->dir, p->win + p->win_ptr[L], (int32_t)n,
+                                                       p->lvl_rows, c->r, c->yb, p->u);
+    }
+    for (int64_t L = p->nlev - 1; L >= 0; --L) {
+      const int64_t n = p->win_ptr[L + 1] - p->win_ptr[L];
+      k_sgs_sweep_win<false><<<grid_for(n), 256, 0, s>>>(v, p->rec, p->dir, p->win + p->win_ptr[L], (int32_t)n,
+                                                        p->lvl_rows, c->r, c->yb, p->u);
+    }
+  } else {
+    for (int64_t L = 0; L < p->nlev; ++L) {
+      const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
+      k_sgs_sweep<true><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r,
+                                                   c->yb, p->u);
+    }
+    for (int64_t L = p->nlev - 1; L >= 0; --L) {
+      const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
+      k_sgs_sweep<false><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r,
+                                                    c->yb, p->u);
+    }
   }
-  for (int64_t L = p->nlev - 1; L >= 0; --L) {
-    const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
-    k_sgs_sweep<false><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb,
-                                                  p->u);
+  int64_t nwin = 0;
+  const int32_t* rowstart = emin_scalar_windows(c, &nwin);
+  if (rowstart && p->rec) {
+    const int g = grid_for(nwin);
+    k_sgs_project_win<<<g, 256, 0, s>>>(v, rowstart, nwin, c->r, p->u, c->partials);
+    return g;
   }
   const int g = grid_for(c->nF);
   k_sgs_project<<<g, 256, 0, s>>>(v, c->r, p->u, c->partials);
@@ -297,7 +498,7 @@ void emin_sgs_stage2(emin_ctx c, cudaStream_t s) {
 void emin_sgs_free(emin_ctx c) {
   SgsPlan* p = c->sgs;
   if (!p) return;
-  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u};
+  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u, p->dir, p->win};
   for (void* q : ptrs)
     if (q) cudaFreeAsync(q, c->stream);
   delete p;

@@ -324,3 +324,20 @@ def test_sgs_beats_jacobi_per_iteration_on_gpu():
     j.iterate(5)
     s.iterate(5)
     assert s.energy() < j.energy()
+
+
+@pytest.mark.parametrize("name,size,kind", [("3", 12, "color"), ("1b", None, "natural")])
+def test_sgs_generic_sweep_equals_window_sweep(name, size, kind, monkeypatch):
+    """The windowed lane-per-entry SGS sweeps (scalar path) against the
+    generic warp-per-row sweeps: same arithmetic, same order."""
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config, sgs_key
+    prob = make_config(name, size=size)
+    key = sgs_key(prob, kind)
+    a = Emin.from_problem(prob, precond="sgs", sgs_key=key)
+    monkeypatch.setenv("EMIN_SGS_GENERIC", "1")
+    b = Emin.from_problem(prob, precond="sgs", sgs_key=key)
+    ka, dEa = a.iterate(20)
+    kb, dEb = b.iterate(20)
+    assert ka == kb and np.allclose(dEa, dEb, rtol=1e-12)
+    assert np.abs(a.get_P() - b.get_P()).max() <= 1e-12 * np.abs(b.get_P()).max()
