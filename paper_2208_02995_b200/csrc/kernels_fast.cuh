@@ -332,6 +332,81 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
   block_partial_out(v, partials, tot, sh, 1);
 }
 
+// win2's setup / energy modes (same window decode and record loop):
+//   MM_R0      r0 = -Pi Pi (A P0)|F, the C-identity term A(i, c_j) added  (A1/A2)
+//   MM_ENERGY  partial W . (A_FF W + 2 A_FC), W = X + X2                  (Eq. trInc)
+template <int MODE>
+__global__ void __launch_bounds__(256)
+k_spgemm_win2m(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict__ rowstart, int64_t nwin,
+               const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+               double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  auto xval = [&](int idx) -> double { return MODE == MM_ENERGY ? X[idx] + X2[idx] : X[idx]; };
+  double part = 0.0;
+  for (int64_t w = gw; w < nwin; w += nw) {
+    const int r0 = rowstart[w];
+    const int nrows = rowstart[w + 1] - r0;
+    if (nrows == 0) continue;                          // warp-uniform
+    const int myptr = (lane <= nrows) ? (int)v.wptr[r0 + lane] : 0;
+    const int base = __shfl_sync(0xffffffffu, myptr, 0);
+    const int nent = __shfl_sync(0xffffffffu, myptr, nrows) - base;
+    const unsigned H = __reduce_or_sync(0xffffffffu, (lane < nrows) ? (1u << (unsigned)(myptr - base)) : 0u);
+    const bool act = lane < nent;
+    const int l = act ? lane : nent - 1;
+    const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+    const unsigned hu = H & upto;
+    const int rloc = __popc(hu) - 1;
+    const int rowbeg = 31 - __clz(hu);
+    const unsigned after = H & ~upto;
+    const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+    const int pos = lane - rowbeg;
+    const int i = r0 + rloc;
+    const int e = base + lane;
+    const double xo = act ? xval(e) : 0.0;
+    double acc = 0.0, fc = 0.0;
+    if (act) {
+      const int qb = (int)v.affptr[i], qe = (int)v.affptr[i + 1];
+      const int4* A4 = reinterpret_cast<const int4*>(A);
+      acc = __hiloint2double(__ldg(&A4[qb]).y, __ldg(&A4[qb]).x) * xo;   // diagonal record first
+      const unsigned sh4 = 4u * (unsigned)pos;
+#pragma unroll 4
+      for (int q = qb + 1; q < qe; ++q) {
+        const int4 en = __ldg(&A4[q]);
+        const unsigned sidx = ((unsigned)en.w >> sh4) & 0xFu;
+        if (sidx != 0xFu) acc = fma(__hiloint2double(en.y, en.x), xval(en.z + (int)sidx), acc);
+      }
+      const int32_t j = v.wcol[e];                    // A(i, c_j): search the short A_FC row
+      for (int64_t q = v.afcptr[i]; q < v.afcptr[i + 1]; ++q)
+        if (v.afccol[q] == j) { fc = v.afcval[q]; break; }
+    }
+    if (MODE == MM_ENERGY) {
+      if (act) part = fma(xo, acc + 2.0 * fc, part);
+      continue;                                       // warp-uniform (MODE)
+    }
+    const double qv = act ? v.Q[e] : 0.0;
+    double g = acc + fc;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {            // Pi applied twice (reading A2)
+      s_qa[wib][lane] = qv * g;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      __syncwarp();
+      g = g - qv * dot;
+    }
+    if (act) out[e] = -g;
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, -1);
+}
+
 // win3: windows of up to 64 entries (two per lane: positions lane and
 // lane + 32), so the per-window decode is amortised over twice the entries
 // and every lane has two independent gather chains in flight.  Rows per
@@ -1110,6 +1185,130 @@ k_spgemm_win9(DevView v, const int4* __restrict__ A4, const int4* __restrict__ h
 }
 static inline size_t w9_smem_bytes() { return sizeof(W9Buf) * 2 * W8_WARPS; }
 
+// ---------------------------------------------------------------------------
+// win10: win2's lane map with the latency chain cut where it is cheap.
+//  * a 32-byte window header (k_plan_win4) is loaded two windows ahead
+//    (two warp-uniform 16-byte loads, no shuffles);
+//  * lane 0 copies the NEXT window's A records and row pointers into a
+//    per-warp shared buffer with cp.async.bulk on an mbarrier while the
+//    current window computes (no registers wait on them);
+//  * the lane's Q and y entries are plain coalesced loads;
+//  * a row's gathers are issued together before its FMAs (fixed MAXR slots,
+//    MAXR = longest A_FF row - 1), so they cost one L2 round trip, not one
+//    per record.
+// Order of the FMAs and of the row sums as win2 (diagonal first, then A's
+// column order).
+// ---------------------------------------------------------------------------
+struct W10Buf {
+  int4 rec[W8_REC];
+  int64_t ap[36];
+};
+
+template <int MAXR>
+__global__ void __launch_bounds__(W8_WARPS * 32)
+k_spgemm_win10(DevView v, const int4* __restrict__ A4, const Win4Hdr* __restrict__ hdr, int64_t nwin,
+               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char w10_smem[];
+  __shared__ double sh[32];
+  __shared__ double s_qa[W8_WARPS][32];
+  __shared__ __align__(8) uint64_t s_bar[W8_WARPS][2];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  W10Buf* bufs = reinterpret_cast<W10Buf*>(w10_smem) + 2 * wib;
+  if (lane == 0) {
+    mbar_init(&s_bar[wib][0], 1);
+    mbar_init(&s_bar[wib][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double part = 0.0;
+  const int4* H4 = reinterpret_cast<const int4*>(hdr);
+  const int4 z4 = make_int4(0, 0, 0, 0);
+  auto issue = [&](int4 h0, int4 h1, W10Buf* b, uint64_t* bar) {   // lane 0 only
+    // h0 = {r0, ebase, abase, ehead}, h1 = {nent, nrows, nrec, -}
+    const int nr = min(h1.z, W8_REC);
+    const int a0 = h0.x & ~1, a1 = (h0.x + h1.y + 2) & ~1;     // affptr[r0 .. r0 + nrows]
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, (uint32_t)(nr * 16 + (a1 - a0) * 8));
+    if (nr) bulk_g2s(b->rec, A4 + h0.z, (uint32_t)(nr * 16), bar);
+    bulk_g2s(b->ap, v.affptr + a0, (uint32_t)((a1 - a0) * 8), bar);
+  };
+  int4 c0 = z4, c1 = z4, n0 = z4, n1 = z4;
+  if (w < nwin) { c0 = __ldg(H4 + 2 * w); c1 = __ldg(H4 + 2 * w + 1); }
+  if (w + nw < nwin) { n0 = __ldg(H4 + 2 * (w + nw)); n1 = __ldg(H4 + 2 * (w + nw) + 1); }
+  if (w < nwin && lane == 0) issue(c0, c1, &bufs[0], &s_bar[wib][0]);
+  int it = 0;
+  while (w < nwin) {
+    const int bi = it & 1;
+    const int64_t wn = w + nw, wnn = w + 2 * nw;
+    if (wn < nwin && lane == 0) issue(n0, n1, &bufs[bi ^ 1], &s_bar[wib][bi ^ 1]);
+    int4 m0 = z4, m1 = z4;
+    if (wnn < nwin) { m0 = __ldg(H4 + 2 * wnn); m1 = __ldg(H4 + 2 * wnn + 1); }
+    const int nent = c1.x, nrows = c1.y;
+    const bool act = lane < nent;
+    const int e = c0.y + lane;
+    const double qv = act ? __ldg(v.Q + e) : 0.0;
+    const double xo = act ? X[e] : 0.0;
+    mbar_wait(&s_bar[wib][bi], (uint32_t)((it >> 1) & 1));
+    const W10Buf* b = &bufs[bi];
+    if (nrows > 0) {                                   // warp-uniform
+      const unsigned H = (unsigned)c0.w;
+      const int l = act ? lane : nent - 1;
+      const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
+      const unsigned hu = H & upto;
+      const int rloc = __popc(hu) - 1;
+      const int rowbeg = 31 - __clz(hu);
+      const unsigned after = H & ~upto;
+      const int rowlen = (after ? (__ffs(after) - 1) : nent) - rowbeg;
+      double acc = 0.0;
+      if (act) {
+        const int as = c0.x & 1;
+        const int qb = (int)(b->ap[as + rloc] - c0.z), qe = (int)(b->ap[as + rloc + 1] - c0.z);
+        const unsigned sh4 = 4u * (unsigned)(lane - rowbeg);
+        const int4* rec = (qe <= W8_REC) ? b->rec : A4 + c0.z;   // beyond the staged part: global
+        acc = reinterpret_cast<const double*>(rec + qb)[0] * xo;   // diagonal record first (own y)
+        for (int q0 = qb + 1; q0 < qe; q0 += MAXR) {
+          double yv[MAXR];
+          unsigned okm = 0;
+#pragma unroll
+          for (int j = 0; j < MAXR; ++j) {
+            const int qq = min(q0 + j, qe - 1);
+            const int2 ip = reinterpret_cast<const int2*>(rec + qq)[1];
+            const unsigned sidx = ((unsigned)ip.y >> sh4) & 0xFu;
+            const bool ok = (q0 + j < qe) && sidx != 0xFu;
+            okm |= ok ? (1u << j) : 0u;
+            yv[j] = ok ? __ldg(X + ip.x + (int)sidx) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < MAXR; ++j)
+            if (okm & (1u << j)) acc = fma(reinterpret_cast<const double*>(rec + q0 + j)[0], yv[j], acc);
+        }
+      }
+      s_qa[wib][lane] = qv * acc;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      if (act) {
+        const double g = acc - qv * dot;
+        out[e] = g;
+        part = fma(xo, g, part);
+      }
+    }
+    __syncwarp();                                      // buffer bi is free for window w + 2 nw
+    c0 = n0; c1 = n1; n0 = m0; n1 = m1;
+    ++it;
+    w = wn;
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+static inline size_t w10_smem_bytes() { return sizeof(W10Buf) * 2 * W8_WARPS; }
+
 // y^ = Pi K y (nv = 1) on precomputed window headers, next header prefetched
 __global__ void __launch_bounds__(256, 8)
 k_spgemm_hdr(DevView v, const SpEnt* __restrict__ A, const WinHdr* __restrict__ hdr, int64_t nwin,
@@ -1747,31 +1946,38 @@ static inline int select_fast_path(emin_ctx c) {
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
   k_plan_entries<<<SM * 8, 256, 0, s>>>(c->view(), p.ent);
   c->launches += 2;
-  // tile plan for the staged kernel
-  const int ST = TILE_E - c->max_row + 1;
-  p.ntiles = (c->nnzW + ST - 1) / ST;
-  int32_t* trow = nullptr;
-  int32_t* dmax = nullptr;
-  if (cudaMallocAsync((void**)&trow, sizeof(int32_t) * (p.ntiles + 1), s) != cudaSuccess ||
-      cudaMallocAsync((void**)&p.hdr, sizeof(TileHdr) * std::max<int64_t>(p.ntiles, 1), s) != cudaSuccess ||
-      cudaMallocAsync((void**)&dmax, sizeof(int32_t) * 2, s) != cudaSuccess)
-    return 1;
-  cudaMemsetAsync(dmax, 0, sizeof(int32_t) * 2, s);
-  k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, ST, p.ntiles, trow);
-  k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
-  c->launches += 2;
-  int32_t hmax[2] = {0, 0};
-  cudaMemcpyAsync(hmax, dmax, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
-  cudaFreeAsync(trow, s);
-  cudaFreeAsync(dmax, s);
-  cudaStreamSynchronize(s);
-  p.tile_smem = tile_smem_bytes(hmax[0]);
-  // window headers (lane decode without the rowstart -> wptr round trips)
-  if (cudaMallocAsync((void**)&p.whdr, sizeof(WinHdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) return 1;
-  k_plan_headers<<<SM * 4, 256, 0, s>>>(c->wptr, p.rowstart, p.nwin, p.whdr);
-  c->launches += 1;
-  // per-iteration kernel variant (EMIN_SPGEMM=hdr|win|tile|pipe; default hdr)
+  // per-iteration kernel variant (EMIN_SPGEMM, default win2); the tile plan
+  // and the window headers are built only for the variants that use them
   const char* var = getenv("EMIN_SPGEMM");
+  const bool need_tiles = !getenv("EMIN_SETUP_WIN2M") || (var && (!strcmp(var, "tile") || !strcmp(var, "pipe")));
+  const bool need_whdr = var && (!strcmp(var, "hdr") || !strcmp(var, "mask"));
+  int32_t hmax[2] = {0, 0};
+  if (need_tiles) {
+    // tile plan for the staged kernel
+    const int ST = TILE_E - c->max_row + 1;
+    p.ntiles = (c->nnzW + ST - 1) / ST;
+    int32_t* trow = nullptr;
+    int32_t* dmax = nullptr;
+    if (cudaMallocAsync((void**)&trow, sizeof(int32_t) * (p.ntiles + 1), s) != cudaSuccess ||
+        cudaMallocAsync((void**)&p.hdr, sizeof(TileHdr) * std::max<int64_t>(p.ntiles, 1), s) != cudaSuccess ||
+        cudaMallocAsync((void**)&dmax, sizeof(int32_t) * 2, s) != cudaSuccess)
+      return 1;
+    cudaMemsetAsync(dmax, 0, sizeof(int32_t) * 2, s);
+    k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, ST, p.ntiles, trow);
+    k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
+    c->launches += 2;
+    cudaMemcpyAsync(hmax, dmax, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(trow, s);
+    cudaFreeAsync(dmax, s);
+    cudaStreamSynchronize(s);
+    p.tile_smem = tile_smem_bytes(hmax[0]);
+  }
+  if (need_whdr) {
+    // window headers (lane decode without the rowstart -> wptr round trips)
+    if (cudaMallocAsync((void**)&p.whdr, sizeof(WinHdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) return 1;
+    k_plan_headers<<<SM * 4, 256, 0, s>>>(c->wptr, p.rowstart, p.nwin, p.whdr);
+    c->launches += 1;
+  }
   p.variant = 5;   // default: win2 (fastest measured, profiles/r01/spgemm_variants_c3.log)
   if (var && !strcmp(var, "hdr")) p.variant = 0;
   if (var && !strcmp(var, "win")) p.variant = 1;
@@ -1786,6 +1992,33 @@ static inline int select_fast_path(emin_ctx c) {
   if (var && !strcmp(var, "win7")) p.variant = 10;
   if (var && !strcmp(var, "win8")) p.variant = 11;
   if (var && !strcmp(var, "win9")) p.variant = 12;
+  if (var && !strcmp(var, "win10")) p.variant = 13;
+  if (p.variant == 13) {
+    int32_t* dmx = nullptr;
+    int32_t hw = 0;
+    if (cudaMallocAsync((void**)&dmx, sizeof(int32_t), s) == cudaSuccess) {
+      cudaMemsetAsync(dmx, 0, sizeof(int32_t), s);
+      k_rowlen_max<<<SM * 4, 256, 0, s>>>(c->affptr, c->nF, dmx);
+      cudaMemcpyAsync(&hw, dmx, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaFreeAsync(dmx, s);
+      cudaStreamSynchronize(s);
+      c->launches += 1;
+    }
+    p.ellW = std::max(2, hw) - 1;                    // MAXR = longest row - 1 (diagonal apart)
+    int per_sm = 0;
+    if (p.ellW <= 8) {
+      auto kfun = p.ellW <= 4 ? k_spgemm_win10<4> : p.ellW <= 6 ? k_spgemm_win10<6> : k_spgemm_win10<8>;
+      cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w10_smem_bytes());
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfun, W8_WARPS * 32, w10_smem_bytes());
+    }
+    if (per_sm < 1 || cudaMallocAsync((void**)&p.w4hdr, sizeof(Win4Hdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) {
+      p.variant = 5;
+    } else {
+      p.w8grid = (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + W8_WARPS - 1) / W8_WARPS, (int64_t)SM * per_sm));
+      k_plan_win4<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w4hdr);
+      c->launches += 1;
+    }
+  }
   if (p.variant == 12) {
     int per_sm = 0;
     cudaFuncSetAttribute(k_spgemm_win9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w9_smem_bytes());
@@ -1874,13 +2107,13 @@ static inline int select_fast_path(emin_ctx c) {
       if (hb) p.variant = 1;
     }
   }
-  if (p.tile_smem <= 160 * 1024) {
+  if (need_tiles && p.tile_smem <= 160 * 1024) {
     p.use_tiles = 1;
     cudaFuncSetAttribute(k_spgemm_tile<MM_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
     cudaFuncSetAttribute(k_spgemm_tile<MM_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
     cudaFuncSetAttribute(k_spgemm_tile<MM_ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
   } else if (p.variant == 2) {
-    p.variant = 0;
+    p.variant = 5;
   }
   if (p.variant == 3) {
     // persistent TMA-pipelined kernel
@@ -1896,7 +2129,7 @@ static inline int select_fast_path(emin_ctx c) {
       p.use_pipe = 1;
       p.pipe_grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)SM * per_sm));
     } else {
-      p.variant = 0;
+      p.variant = 5;
     }
   }
   return 1;
@@ -1918,7 +2151,7 @@ static inline int scalar_iter_grid(emin_ctx c) {
   switch (p.variant) {
     case 2: return (int)std::max<int64_t>(1, p.ntiles);
     case 3: return p.pipe_grid;
-    case 11: case 12: return p.w8grid;
+    case 11: case 12: case 13: return p.w8grid;
     default: return scalar_grid(c);
   }
 }
@@ -1955,6 +2188,12 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
         k_spgemm_win8<<<p.w8grid, W8_WARPS * 32, w8_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
                                                                       p.w6hdr, p.nwin, X, out, c->partials);
         return;
+      case 13: {
+        const auto kfun = p.ellW <= 4 ? k_spgemm_win10<4> : p.ellW <= 6 ? k_spgemm_win10<6> : k_spgemm_win10<8>;
+        kfun<<<p.w8grid, W8_WARPS * 32, w10_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent), p.w4hdr,
+                                                               p.nwin, X, out, c->partials);
+        return;
+      }
       case 12:
         k_spgemm_win9<<<p.w8grid, W8_WARPS * 32, w9_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
                                                                       p.w6hdr, p.nwin, X, out, c->partials);
@@ -1986,6 +2225,17 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
                                                               X, out, c->partials);
         return;
     }
+  }
+  if (!p.use_tiles) {
+    // setup / energy modes on win2's window kernel (EMIN_SETUP_WIN2M=1; measured
+    // slower than the tile kernel on config 3: r0 + E0 0.47 ms either way,
+    // emin_energy 0.34 vs 0.28 ms)
+    if (mode == MM_R0)
+      k_spgemm_win2m<MM_R0><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
+    else
+      k_spgemm_win2m<MM_ENERGY><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
+                                                              c->partials);
+    return;
   }
   if (p.use_tiles) {
     const int g = (int)std::max<int64_t>(1, p.ntiles);
