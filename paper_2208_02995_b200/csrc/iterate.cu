@@ -535,6 +535,21 @@ emin_status emin_plan(emin_ctx c) {
 const int4* emin_scalar_records(emin_ctx c) {
   return c->kernel_path == 1 ? reinterpret_cast<const int4*>(fast_of(c)->sc.ent) : nullptr;
 }
+// the nodal path's plan (sgs.cu): per F node n its blocks [bptr[n], bptr[n+1])
+// with records {wptr[3K], 3|J_K|} and the byte map pm8 + pmoff[n] (position of
+// J_I[s] in J_K per block, 0xFF absent); false off the nodal path
+bool emin_nodal_plan(emin_ctx c, const int2** blk, const int64_t** bptr, const uint8_t** pm8,
+                     const int64_t** pmoff, int64_t* nFn) {
+  if (c->kernel_path != 2 || !c->nodal) return false;
+  const NodalPlan* np = static_cast<const NodalPlan*>(c->nodal);
+  *blk = reinterpret_cast<const int2*>(np->blk);
+  *bptr = np->bptr;
+  *pm8 = np->pm8;
+  *pmoff = np->pmoff;
+  *nFn = np->nFn;
+  return true;
+}
+
 // the scalar path's window plan: rows [rowstart[w], rowstart[w+1]) of window
 // w hold <= 32 entries (sgs.cu)
 const int32_t* emin_scalar_windows(emin_ctx c, int64_t* nwin) {

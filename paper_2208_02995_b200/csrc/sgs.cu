@@ -44,6 +44,14 @@ struct SgsPlan {
   uint8_t* dir = nullptr;        // [nnzAFF] per record: 0 diagonal, 1 predecessor, 2 successor
   int4* win = nullptr;           // [nwin] {j0 (into lvl_rows), head mask, nent, nrows}
   std::vector<int64_t> win_ptr;  // host [nlev + 1] window range of each level
+  // nodal path (kernel_path 2, 3x3 blocks): levels and sweeps per F node
+  int nodal = 0;
+  const int2* nblk = nullptr;    // {wptr[3K], 3|J_K|} per block (not owned)
+  const int64_t* bptr = nullptr;
+  const uint8_t* pm8 = nullptr;
+  const int64_t* pmoff = nullptr;
+  int64_t nFn = 0;
+  uint8_t* bdir = nullptr;       // [nblk] 0 own node, 1 predecessor node, 2 successor node
 };
 
 namespace {
@@ -237,6 +245,218 @@ k_sgs_sweep_win(DevView v, const int4* __restrict__ A4, const uint8_t* __restric
   }
 }
 
+// ---- nodal path: the 3 dof rows of an F node share J and are visited
+// consecutively (node-constant keys; reading A23 orders rows by (key, row),
+// so node K precedes node I iff (key_K, K) < (key_I, I), and inside a node
+// dof e precedes dof d iff e < d).
+__global__ void k_sgs_node_key_ok(int64_t nFn, const int64_t* __restrict__ key, int32_t* bad) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x)
+    if (key[3 * n + 1] != key[3 * n] || key[3 * n + 2] != key[3 * n]) atomicExch(bad, 1);
+}
+
+__device__ __forceinline__ bool sgs_node_before(const int64_t* __restrict__ key, int64_t K, int64_t I) {
+  const int64_t a = key[3 * K], b = key[3 * I];
+  return a != b ? a < b : K < I;
+}
+
+__global__ void k_sgs_node_dir(DevView v, int64_t nFn, const int64_t* __restrict__ bptr,
+                               const int64_t* __restrict__ key, uint8_t* __restrict__ bdir) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ab = v.affptr[3 * n];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    for (int b = 0; b < nb; ++b) {
+      const int64_t K = v.affcol[ab + 3 * b] / 3;
+      bdir[bb + b] = (K == n) ? 0 : (sgs_node_before(key, K, n) ? 1 : 2);
+    }
+  }
+}
+
+__global__ void k_sgs_node_levels(DevView v, int64_t nFn, const int64_t* __restrict__ bptr,
+                                  const uint8_t* __restrict__ bdir, int32_t* lev, int32_t* changed) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ab = v.affptr[3 * n];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    int32_t m = 0;
+    for (int b = 0; b < nb; ++b)
+      if (bdir[bb + b] == 1) m = max(m, ((volatile int32_t*)lev)[v.affcol[ab + 3 * b] / 3] + 1);
+    if (m > lev[n]) {
+      lev[n] = m;
+      *changed = 1;
+    }
+  }
+}
+
+// Forward (FWD) / backward sweep over the F nodes of one level, warp per
+// node, lane t owns pattern positions t and t + 32 of the node's 3 rows.
+//   FWD:  acc_d = x_d - sum_{pred nodes K, e} A_IK[d][e] u_K[e](pos);
+//         then the node's own 3x3 lower triangle, row by row:
+//         u_d = (acc_d - sum_{e<d} A_II[d][e] u_e) / A_II[d][d]
+//   !FWD: acc_d = A_II[d][d] u_d - sum_{succ nodes K, e} A_IK[d][e] z_K[e](pos);
+//         z_d = (acc_d - sum_{e>d} A_II[d][e] z_e) / A_II[d][d], d = 2, 1, 0
+// (the own-node terms come last, after the other blocks in A's column
+// order; the oracle adds them at their column position -- a rounding-order
+// difference only).
+template <bool FWD>
+__global__ void __launch_bounds__(256)
+k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __restrict__ bptr,
+                  const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
+                  const uint8_t* __restrict__ bdir, const int32_t* __restrict__ nodes, int32_t nnodes,
+                  double* __restrict__ r, const double* __restrict__ yb, double* u) {
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = FWD ? st->pend : 0;
+  const double ap = st->alpha_pend;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int t0 = lane, t1 = lane + 32;
+  const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
+  const uint8_t want = FWD ? 1 : 2;
+  for (int64_t w = gw; w < nnodes; w += nw) {
+    const int64_t n = nodes[w];
+    const int64_t r3 = 3 * n;
+    const int64_t wb = v.wptr[r3];
+    const int n3 = (int)(v.wptr[r3 + 1] - wb);
+    const int nJ = n3 / 3;
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    const int64_t ab = v.affptr[r3];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int64_t rs = 3 * (int64_t)nb;
+    const uint8_t* pm = pm8 + pmoff[n];
+    double acc0[3], acc1[3];
+    double own[9];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int64_t ro = wb + (int64_t)d * n3;
+      double x0 = 0.0, x1 = 0.0;
+      if (FWD) {
+        if (act0) { x0 = r[ro + t0]; if (pend) { x0 = x0 - ap * yb[ro + t0]; r[ro + t0] = x0; } }
+        if (act1) { x1 = r[ro + t1]; if (pend) { x1 = x1 - ap * yb[ro + t1]; r[ro + t1] = x1; } }
+      } else {
+        const double dd = v.d[r3 + d];
+        if (act0) x0 = dd * u[ro + t0];                    // v = D u
+        if (act1) x1 = dd * u[ro + t1];
+      }
+      acc0[d] = x0;
+      acc1[d] = x1;
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) own[q] = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      const uint8_t db = bdir[bb + b];                    // warp-uniform
+      if (db == 0) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) own[d * 3 + e] = __ldg(v.affval + ab + d * rs + 3 * b + e);
+        continue;
+      }
+      if (db != want) continue;
+      double a[9];
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int e = 0; e < 3; ++e) a[d * 3 + e] = __ldg(v.affval + ab + d * rs + 3 * b + e);
+      const int2 k = __ldg(blk + bb + b);
+      const int p0 = act0 ? pm[b * nJ + s0] : 0xFF;
+      const int p1 = act1 ? pm[b * nJ + s1] : 0xFF;
+      if (p0 != 0xFF) {
+        const int64_t i0 = (int64_t)k.x + 3 * p0 + b0;
+        const double y0 = u[i0], y1 = u[i0 + k.y], y2 = u[i0 + 2 * k.y];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          acc0[d] -= a[d * 3 + 0] * y0;
+          acc0[d] -= a[d * 3 + 1] * y1;
+          acc0[d] -= a[d * 3 + 2] * y2;
+        }
+      }
+      if (p1 != 0xFF) {
+        const int64_t i1 = (int64_t)k.x + 3 * p1 + b1;
+        const double y0 = u[i1], y1 = u[i1 + k.y], y2 = u[i1 + 2 * k.y];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          acc1[d] -= a[d * 3 + 0] * y0;
+          acc1[d] -= a[d * 3 + 1] * y1;
+          acc1[d] -= a[d * 3 + 2] * y2;
+        }
+      }
+    }
+    double o0[3], o1[3];
+    if (FWD) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double a0 = acc0[d], a1 = acc1[d];
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+          if (e < d) { a0 -= own[d * 3 + e] * o0[e]; a1 -= own[d * 3 + e] * o1[e]; }
+        o0[d] = a0 / own[d * 3 + d];
+        o1[d] = a1 / own[d * 3 + d];
+      }
+    } else {
+#pragma unroll
+      for (int d = 2; d >= 0; --d) {
+        double a0 = acc0[d], a1 = acc1[d];
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+          if (e > d) { a0 -= own[d * 3 + e] * o0[e]; a1 -= own[d * 3 + e] * o1[e]; }
+        o0[d] = a0 / own[d * 3 + d];
+        o1[d] = a1 / own[d * 3 + d];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int64_t ro = wb + (int64_t)d * n3;
+      if (act0) u[ro + t0] = o0[d];
+      if (act1) u[ro + t1] = o1[d];
+    }
+  }
+}
+
+// z <- Pi z and the partial r . z on the nodal path (Q of row 3n shared by
+// the node's 3 rows), warp per node
+template <int NV>
+__global__ void __launch_bounds__(256)
+k_sgs_project_nodal(DevView v, int64_t nFn, const double* __restrict__ r, double* __restrict__ z,
+                    double* __restrict__ partials) {
+  __shared__ double sh[32];
+  if (v.st->stopped) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int t0 = lane, t1 = lane + 32;
+  double part = 0.0;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t wb = v.wptr[3 * n];
+    const int n3 = (int)(v.wptr[3 * n + 1] - wb);
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    double q0[NV], q1[NV];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      q0[m] = act0 ? v.Q[(wb + t0) * NV + m] : 0.0;
+      q1[m] = act1 ? v.Q[(wb + t1) * NV + m] : 0.0;
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int64_t ro = wb + (int64_t)d * n3;
+      const double z0 = act0 ? z[ro + t0] : 0.0, z1 = act1 ? z[ro + t1] : 0.0;
+      double s0v = 0.0, s1v = 0.0;
+#pragma unroll
+      for (int m = 0; m < NV; ++m) {
+        const double dm = warp_sum(fma(q0[m], z0, q1[m] * z1));
+        s0v = fma(q0[m], dm, s0v);
+        s1v = fma(q1[m], dm, s1v);
+      }
+      if (act0) { const double zz = z0 - s0v; z[ro + t0] = zz; part = fma(r[ro + t0], zz, part); }
+      if (act1) { const double zz = z1 - s1v; z[ro + t1] = zz; part = fma(r[ro + t1], zz, part); }
+    }
+  }
+  const double tot = block_sum(part, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
 // z <- Pi z (per row, Q_i), partial r . z  (Alg. 3 lines P:840-841)
 __global__ void __launch_bounds__(256)
 k_sgs_project(DevView v, const double* __restrict__ r, double* __restrict__ z, double* __restrict__ partials) {
@@ -366,11 +586,32 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   k_sgs_key<<<SM * 4, 256, 0, s>>>(nF, frow, dkey, p->key);
   EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lev, 0, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
   c->launches += 1;
+  // nodal path with node-constant keys: levels, buckets and sweeps per F node
+  int64_t nunits = nF;                               // rows, or nodes on the nodal path
+  if (!getenv("EMIN_SGS_GENERIC") &&
+      emin_nodal_plan(c, &p->nblk, &p->bptr, &p->pm8, &p->pmoff, &p->nFn)) {
+    int32_t hb = 0;
+    EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+    k_sgs_node_key_ok<<<SM * 4, 256, 0, s>>>(p->nFn, p->key, flag);
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(&hb, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+    c->launches += 1;
+    if (!hb) {
+      p->nodal = 1;
+      nunits = p->nFn;
+      EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->bdir, std::max<int64_t>(c->nnzAFF / 9, 1), s));
+      k_sgs_node_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->key, p->bdir);
+      c->launches += 1;
+    }
+  }
   // relaxation passes until no level changes (<= longest chain + 1)
-  for (int64_t pass = 0; pass <= nF; ++pass) {
+  for (int64_t pass = 0; pass <= nunits; ++pass) {
     int32_t h = 0;
     EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
-    k_sgs_levels<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->lev, flag);
+    if (p->nodal)
+      k_sgs_node_levels<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->bdir, p->lev, flag);
+    else
+      k_sgs_levels<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->lev, flag);
     c->launches += 1;
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(&h, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -380,12 +621,12 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   int32_t hmax = 0;
   EMIN_CUDA_TRY(c, cudaMemsetAsync(flag + 1, 0, sizeof(int32_t), s));
   // count into a buffer of nF + 1 (levels <= nF - 1)
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lvl_cnt, sizeof(int32_t) * (nF + 2), s));
-  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lvl_cnt, 0, sizeof(int32_t) * (nF + 2), s));
-  k_sgs_count<<<SM * 4, 256, 0, s>>>(nF, p->lev, p->lvl_cnt, flag + 1);
+  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lvl_cnt, sizeof(int32_t) * (nunits + 2), s));
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lvl_cnt, 0, sizeof(int32_t) * (nunits + 2), s));
+  k_sgs_count<<<SM * 4, 256, 0, s>>>(nunits, p->lev, p->lvl_cnt, flag + 1);
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(&hmax, flag + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
-  p->nlev = nF > 0 ? (int64_t)hmax + 1 : 0;
+  p->nlev = nunits > 0 ? (int64_t)hmax + 1 : 0;
   std::vector<int32_t> hc((size_t)p->nlev + 1, 0);
   if (p->nlev)
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(hc.data(), p->lvl_cnt, sizeof(int32_t) * p->nlev, cudaMemcpyDeviceToHost, s));
@@ -395,11 +636,11 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   std::vector<int32_t> cur(p->lvl_ptr.begin(), p->lvl_ptr.end() - (p->nlev ? 1 : 0));
   if (p->nlev) {
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(p->lvl_cnt, cur.data(), sizeof(int32_t) * p->nlev, cudaMemcpyHostToDevice, s));
-    k_sgs_scatter<<<SM * 4, 256, 0, s>>>(nF, p->lev, p->lvl_cnt, p->lvl_rows);
+    k_sgs_scatter<<<SM * 4, 256, 0, s>>>(nunits, p->lev, p->lvl_cnt, p->lvl_rows);
   }
   c->launches += 2;
   // scalar path: per-level windows of <= 32 entries (rows never straddle)
-  p->rec = emin_scalar_records(c);
+  p->rec = p->nodal ? nullptr : emin_scalar_records(c);
   if (p->rec && p->nlev && !getenv("EMIN_SGS_GENERIC")) {
     std::vector<int32_t> hrows((size_t)nF);
     std::vector<int64_t> hwptr((size_t)nF + 1);
@@ -454,6 +695,25 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   auto grid_for = [&](int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)SM * 8));
   };
+  if (p->nodal) {
+    for (int64_t L = 0; L < p->nlev; ++L) {
+      const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
+      k_sgs_sweep_nodal<true><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
+                                                         p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
+    }
+    for (int64_t L = p->nlev - 1; L >= 0; --L) {
+      const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
+      k_sgs_sweep_nodal<false><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
+                                                          p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
+    }
+    const int g = grid_for(p->nFn);
+    switch (c->nv) {
+#define PN(N) case N: k_sgs_project_nodal<N><<<g, 256, 0, s>>>(v, p->nFn, c->r, p->u, c->partials); break;
+      PN(1) PN(2) PN(3) PN(4) PN(5) PN(6) PN(7) PN(8)
+#undef PN
+    }
+    return g;
+  }
   if (p->rec) {
     for (int64_t L = 0; L < p->nlev; ++L) {
       const int64_t n = p->win_ptr[L + 1] - p->win_ptr[L];
@@ -498,7 +758,7 @@ void emin_sgs_stage2(emin_ctx c, cudaStream_t s) {
 void emin_sgs_free(emin_ctx c) {
   SgsPlan* p = c->sgs;
   if (!p) return;
-  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u, p->dir, p->win};
+  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u, p->dir, p->win, p->bdir};
   for (void* q : ptrs)
     if (q) cudaFreeAsync(q, c->stream);
   delete p;
