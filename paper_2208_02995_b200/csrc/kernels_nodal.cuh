@@ -379,7 +379,7 @@ __device__ __forceinline__ void nd2_reduce_scatter(double (&v)[N], int lane, int
   *own = lo;
 }
 
-template <int NV, int MODE>
+template <int NV, int MODE, bool PRED = false>
 __global__ void __launch_bounds__(ND_WARPS * 32, 4)
 k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
@@ -426,6 +426,32 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
       const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
       const NodalBlk k = s_b[wib][b];
       const int p0 = act0 ? s_pm[wib][b * nJ + s0] : 0xFF;
+      if (PRED) {
+        // branch-free: predicated gathers (0 when unmatched), unconditional
+        // FMAs (fma(a, 0, acc) = acc up to the sign of a zero)
+        const bool m0 = p0 != 0xFF;
+        const int i0 = k.ybase + 3 * (m0 ? p0 : 0) + b0;
+        const double y0 = m0 ? xval(i0) : 0.0, y1 = m0 ? xval(i0 + k.nK3) : 0.0, y2 = m0 ? xval(i0 + 2 * k.nK3) : 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          acc0[d] = fma(a[d * 3 + 0], y0, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 1], y1, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 2], y2, acc0[d]);
+        }
+        if (any1) {
+          const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
+          const bool m1 = p1 != 0xFF;
+          const int i1 = k.ybase + 3 * (m1 ? p1 : 0) + b1;
+          const double z0 = m1 ? xval(i1) : 0.0, z1 = m1 ? xval(i1 + k.nK3) : 0.0, z2 = m1 ? xval(i1 + 2 * k.nK3) : 0.0;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] = fma(a[d * 3 + 0], z0, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 1], z1, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 2], z2, acc1[d]);
+          }
+        }
+        continue;
+      }
       if (p0 != 0xFF) {
         const int i0 = k.ybase + 3 * p0 + b0;
         const double y0 = xval(i0), y1 = xval(i0 + k.nK3), y2 = xval(i0 + 2 * k.nK3);
@@ -613,6 +639,14 @@ static inline void launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
     return;
   }
   const bool v2 = !(var && !strcmp(var, "s"));     // EMIN_NODAL=s: the staged v1 kernel
+  if (mode == MM_ITER && var && !strcmp(var, "v2p")) {    // branch-free block loop (A/B)
+    switch (c->nv) {
+#define NV_CASE(N) case N: k_spgemm_nodal_v2<N, MM_ITER, true><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials); break;
+      NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+#undef NV_CASE
+    }
+    return;
+  }
 #define ND_LAUNCH(KER, N)                                                                                  \
   if (mode == MM_ITER)                                                                                    \
     KER<N, MM_ITER><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out,   \
