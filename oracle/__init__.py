@@ -42,14 +42,15 @@ def _load():
         P = C.c_void_p
         i64, i32, dbl = C.c_int64, C.c_int, C.c_double
         lib.oracle_create.argtypes = [C.POINTER(P), i64, i64, P, P, P, P, P, P, P, i32, P, P,
-                                      dbl, dbl, dbl, i32, i32, P]
+                                      dbl, dbl, dbl, i32, i32, P, i32]
         lib.oracle_create.restype = i32
         lib.oracle_iterate.argtypes = [P, i32, C.POINTER(i32), P]
         lib.oracle_iterate.restype = i32
         for name, rt in [("oracle_nF", i64), ("oracle_nnzW", i64), ("oracle_E0", dbl),
                          ("oracle_dE1", dbl), ("oracle_k_total", i64), ("oracle_stopped", i32),
                          ("oracle_n_svd", i64), ("oracle_n_frozen", i64),
-                         ("oracle_sum_diag_cc", dbl), ("oracle_energy", dbl)]:
+                         ("oracle_sum_diag_cc", dbl), ("oracle_energy", dbl),
+                         ("oracle_n_maxvol_fail", i64)]:
             getattr(lib, name).argtypes = [P]
             getattr(lib, name).restype = rt
         lib.oracle_energy_of.argtypes = [P, P]
@@ -66,6 +67,8 @@ def _load():
         lib.oracle_masked_AX.argtypes = [P, P, i32, P]
         lib.oracle_setup_row.argtypes = [i32, i32, P, P, dbl, P, P, C.POINTER(i32)]
         lib.oracle_setup_row.restype = i32
+        lib.oracle_maxvol.argtypes = [i32, i32, P, P]
+        lib.oracle_maxvol.restype = i32
         _lib = lib
     return _lib
 
@@ -84,10 +87,12 @@ class Oracle:
     """Oracle state for one problem (see workloads.problems.Problem)."""
 
     def __init__(self, prob, rank_tol=1e-10, tau=0.0, stagnation_rel=1e-30, project_z=True,
-                 P_val="from_problem", precond="jacobi", sgs_key=None):
+                 P_val="from_problem", precond="jacobi", sgs_key=None, start="given"):
         """precond: "jacobi" (M_1) or "sgs" (projected SGS M_2,
         P:916-938); sgs_key (per global row, optional): SGS visits the rows
-        of each K block in ascending (key, row) order (reading A23)."""
+        of each K block in ascending (key, row) order (reading A23).
+        start: "given" (P_val, or the least-norm start if None) or "maxvol"
+        (Alg. 1's tentative start on the prescribed pattern, reading A24)."""
         lib = _load()
         self._keep = []
 
@@ -105,7 +110,8 @@ class Oracle:
                                prob.nv, _p(arr(prob.B, np.float64)), _p(arr(prob.Bc, np.float64)),
                                rank_tol, tau, stagnation_rel, 1 if project_z else 0,
                                {"jacobi": 0, "sgs": 1}[precond],
-                               _p(None if sgs_key is None else arr(sgs_key, np.int64)))
+                               _p(None if sgs_key is None else arr(sgs_key, np.int64)),
+                               {"given": 0, "maxvol": 1}[start])
         self._keep = []
         if st != 0:
             raise OracleError(st, "create")
@@ -158,6 +164,10 @@ class Oracle:
     @property
     def n_frozen(self):
         return self._lib.oracle_n_frozen(self._h)
+
+    @property
+    def n_maxvol_fail(self):
+        return self._lib.oracle_n_maxvol_fail(self._h)
 
     def energy(self):
         return self._lib.oracle_energy(self._h)
@@ -214,6 +224,19 @@ class Oracle:
         out = np.empty_like(X)
         self._lib.oracle_masked_AX(self._h, _p(X), 1 if with_fc else 0, _p(out))
         return out
+
+
+def maxvol(M):
+    """Max-vol selection of nv rows of the tall M (m x nv) as the oracle's
+    Alg. 1 start does it (reading A24).  Returns the row indices (or None if
+    no nonsingular selection exists)."""
+    lib = _load()
+    M = np.asarray(M, dtype=np.float64)
+    m, nv = M.shape
+    Mc = np.ascontiguousarray(M.T)            # column-major m x nv
+    S = np.zeros(nv, np.int32)
+    ok = lib.oracle_maxvol(m, nv, _p(Mc), _p(S))
+    return S.copy() if ok else None
 
 
 def setup_row(M, r, tol=1e-10):

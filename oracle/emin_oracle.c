@@ -34,6 +34,11 @@
  *             dE_k <= stag E0 -> stop                       (A18)
  *             dw += alpha y ; r -= alpha yb
  *   energy  tr(P^T A P) by its definition (Eq. trace), P = [W; I].
+ *   start   (optional) the tentative start W^ of Alg. 1
+ *            on the prescribed pattern: per F row the max-vol
+ *           selection of nv columns of V_c(J_i,:)^T (reading A24), the local
+ *           system solved exactly on them, zero elsewhere; rows without a
+ *           nonsingular selection keep W^ = 0.
  *   precond z = Pi M_2^{-1} r with the projected
  *           symmetric Gauss-Seidel preconditioner (Eq. SGS_prec
  *           simplified): M_SGS^{-1} = (L+D)^{-T} D (L+D)^{-1}, K = L + D + L^T
@@ -80,6 +85,7 @@ typedef struct {
     double rank_tol, tau, stag;
     int project_z;                 /* 1: z = Pi M^-1 r (literal P:840) */
     int precond;                   /* 0 Jacobi M_1, 1 projected SGS M_2 */
+    int64_t n_maxvol_fail;         /* F rows where max-vol found no nonsingular selection */
     int64_t *sgs_key;              /* F index -> SGS ordering key (0 if none given) */
     /* full operator, copied */
     int64_t *Arp; int32_t *Acol; double *Aval;
@@ -269,6 +275,115 @@ static int emin_setup_row(int nj, int nv, const double *M, const double *rvec, d
     }
     free(order); free(sig); free(US); free(V);
     return k;
+}
+
+/* ---------------- Alg. 1 tentative start: max-vol selection ------------- */
+/* Reading A24 (the paper cites max vol [Knu85, Gor08] without details):
+ *   M = V_c(J_i,:) (m x nv, column-major), the columns of V_c(J_i,:)^T are
+ *   M's rows.
+ *   initial selection: Gaussian elimination with partial pivoting on a copy
+ *     of M, pivot of column c = the first unselected row t whose |entry| is
+ *     within a factor (1 - 1e-12) of the column maximum; a zero maximum means
+ *     no nonsingular selection (return 0);
+ *   max-vol sweeps (<= 100): C = M B^{-1}, B = M(S,:); (t, c) = the first
+ *     (row-major) entry with |C| within (1 - 1e-12) of max |C|; stop when
+ *     max |C| <= 1 + 1e-8, else S[c] = t (the volume |det B| grows by |C|).
+ *   w = 0 except w(S) = B^{-T} v (the local system B^T w = v solved exactly).
+ * Returns 1 on success. */
+static int maxvol_tol_first(const double *val, int n, double *vmax) {
+    double mx = 0.0;
+    for (int t = 0; t < n; ++t) if (val[t] > mx) mx = val[t];
+    *vmax = mx;
+    for (int t = 0; t < n; ++t) if (val[t] >= (1.0 - 1e-12) * mx && val[t] >= 0.0) return t;
+    return -1;
+}
+
+/* inverse of the nv x nv matrix B (row-major) by Gauss-Jordan with partial
+ * pivoting; returns 0 if singular */
+static int gj_inverse(int nv, const double *Bm, double *inv) {
+    double a[16 * 32];
+    for (int r = 0; r < nv; ++r)
+        for (int c = 0; c < 2 * nv; ++c) a[r * 2 * nv + c] = c < nv ? Bm[r * nv + c] : (c - nv == r ? 1.0 : 0.0);
+    for (int c = 0; c < nv; ++c) {
+        int p = c;
+        for (int r = c + 1; r < nv; ++r) if (fabs(a[r * 2 * nv + c]) > fabs(a[p * 2 * nv + c])) p = r;
+        if (a[p * 2 * nv + c] == 0.0) return 0;
+        if (p != c)
+            for (int k = 0; k < 2 * nv; ++k) { double t = a[c * 2 * nv + k]; a[c * 2 * nv + k] = a[p * 2 * nv + k]; a[p * 2 * nv + k] = t; }
+        double piv = a[c * 2 * nv + c];
+        for (int k = 0; k < 2 * nv; ++k) a[c * 2 * nv + k] /= piv;
+        for (int r = 0; r < nv; ++r) {
+            if (r == c) continue;
+            double f = a[r * 2 * nv + c];
+            if (f != 0.0) for (int k = 0; k < 2 * nv; ++k) a[r * 2 * nv + k] -= f * a[c * 2 * nv + k];
+        }
+    }
+    for (int r = 0; r < nv; ++r)
+        for (int c = 0; c < nv; ++c) inv[r * nv + c] = a[r * 2 * nv + nv + c];
+    return 1;
+}
+
+int oracle_maxvol(int m, int nv, const double *M, int *S) {
+    if (m < nv) return 0;
+    double *W = (double *)malloc(sizeof(double) * m * nv);
+    double *val = (double *)malloc(sizeof(double) * m);
+    int *used = (int *)calloc(m, sizeof(int));
+    memcpy(W, M, sizeof(double) * m * nv);
+    int ok = 1;
+    for (int c = 0; c < nv && ok; ++c) {
+        double mx;
+        for (int t = 0; t < m; ++t) val[t] = used[t] ? -1.0 : fabs(W[t + c * m]);
+        int p = maxvol_tol_first(val, m, &mx);
+        if (p < 0 || mx == 0.0) { ok = 0; break; }
+        S[c] = p;
+        used[p] = 1;
+        for (int t = 0; t < m; ++t) {
+            if (used[t]) continue;
+            double f = W[t + c * m] / W[p + c * m];
+            for (int k = c; k < nv; ++k) W[t + k * m] -= f * W[p + k * m];
+        }
+    }
+    if (ok) {
+        double Bm[256], inv[256];
+        double *C = (double *)malloc(sizeof(double) * m * nv);
+        for (int sweep = 0; sweep < 100 && ok; ++sweep) {
+            for (int a = 0; a < nv; ++a)
+                for (int b = 0; b < nv; ++b) Bm[a * nv + b] = M[S[a] + b * m];
+            if (!gj_inverse(nv, Bm, inv)) { ok = 0; break; }
+            double mx = 0.0;
+            for (int t = 0; t < m; ++t)
+                for (int c = 0; c < nv; ++c) {
+                    double sum = 0.0;
+                    for (int b = 0; b < nv; ++b) sum += M[t + b * m] * inv[b * nv + c];
+                    C[t * nv + c] = fabs(sum);
+                    if (C[t * nv + c] > mx) mx = C[t * nv + c];
+                }
+            if (mx <= 1.0 + 1e-8) break;
+            int bt = -1, bc = -1;
+            for (int t = 0; t < m && bt < 0; ++t)
+                for (int c = 0; c < nv; ++c)
+                    if (C[t * nv + c] >= (1.0 - 1e-12) * mx) { bt = t; bc = c; break; }
+            S[bc] = bt;
+        }
+        free(C);
+    }
+    free(W); free(val); free(used);
+    return ok;
+}
+
+/* w(S) = B^{-T} v, B = M(S,:); zero elsewhere.  Returns 0 if B is singular. */
+static int maxvol_solve(int m, int nv, const double *M, const int *S, const double *v, double *w) {
+    double Bm[256], inv[256];
+    for (int a = 0; a < nv; ++a)
+        for (int b = 0; b < nv; ++b) Bm[a * nv + b] = M[S[a] + b * m];
+    if (!gj_inverse(nv, Bm, inv)) return 0;
+    for (int t = 0; t < m; ++t) w[t] = 0.0;
+    for (int a = 0; a < nv; ++a) {
+        double sum = 0.0;
+        for (int b = 0; b < nv; ++b) sum += inv[b * nv + a] * v[b];
+        w[S[a]] = sum;
+    }
+    return 1;
 }
 
 /* ---------------- the pieces of the path -------------------------------- */
@@ -473,7 +588,7 @@ int oracle_create(oracle_t **out, int64_t n, int64_t nc,
                   const int64_t *P_rowptr, const int32_t *P_col, const double *P_val,
                   int nv, const double *B, const double *Bc,
                   double rank_tol, double tau, double stag, int project_z,
-                  int precond, const int64_t *sgs_key) {
+                  int precond, const int64_t *sgs_key, int start) {
     *out = NULL;
     if (n <= 0 || nc < 0 || nv <= 0 || nv > 16) return OR_ERR_ARG;
     oracle_t *o = (oracle_t *)calloc(1, sizeof(oracle_t));
@@ -584,6 +699,11 @@ int oracle_create(oracle_t **out, int64_t n, int64_t nc,
             for (int m = 0; m < nv; ++m) M[t + m * nj] = Bc[(int64_t)j * nv + m];
             wh[t] = P_val ? P_val[P_rowptr[r] + t] : 0.0;
         }
+        if (start == 1) {                            /* Alg. 1 tentative start (reading A24) */
+            int S[16];
+            int ok = oracle_maxvol(nj, nv, M, S) && maxvol_solve(nj, nv, M, S, B + r * nv, wh);
+            if (!ok) { for (int t = 0; t < nj; ++t) wh[t] = 0.0; o->n_maxvol_fail++; }
+        }
         for (int m = 0; m < nv; ++m) {              /* r_i = v_i - M^T w^ */
             double s = B[r * nv + m];
             for (int t = 0; t < nj; ++t) s -= M[t + m * nj] * wh[t];
@@ -687,6 +807,7 @@ int64_t oracle_k_total(const oracle_t *o) { return o->k_total; }
 int oracle_stopped(const oracle_t *o) { return o->stopped; }
 int64_t oracle_n_svd(const oracle_t *o) { return o->n_svd; }
 int64_t oracle_n_frozen(const oracle_t *o) { return o->n_frozen; }
+int64_t oracle_n_maxvol_fail(const oracle_t *o) { return o->n_maxvol_fail; }
 double oracle_sum_diag_cc(const oracle_t *o) { return o->sum_diag_cc; }
 void oracle_copy_layout(const oracle_t *o, int64_t *wptr, int32_t *wcol, int64_t *frow) {
     memcpy(wptr, o->wptr, sizeof(int64_t) * (o->nF + 1));

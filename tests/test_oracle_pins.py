@@ -503,3 +503,85 @@ def test_sgs_reduces_energy_faster_than_jacobi(name, size):
     _, dEs = os_.iterate(4)
     assert oj.E0 - dEs.sum() < oj.E0 - dEj.sum() + 1e-12 * abs(oj.E0)
     assert dEs[3] / dEs[0] < 0.5 * dEj[3] / dEj[0]
+
+
+# --------------------------------------------------------------------------
+# Alg. 1 tentative start: max-vol selection (P:487-544; NEXT-3, reading A24)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("m,nv,seed", [(12, 6, 0), (41, 6, 1), (54, 6, 2), (7, 3, 3), (9, 1, 4), (6, 6, 5)])
+def test_maxvol_selection_is_dominant(m, nv, seed):
+    """[Gor08]: S is a dominant (locally maximum-volume) submatrix iff every
+    entry of M M(S,:)^{-1} is at most 1 in modulus -- checked with numpy,
+    and no single row swap increases |det M(S,:)|."""
+    from oracle import maxvol
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((m, nv))
+    S = maxvol(M)
+    assert S is not None and len(set(S.tolist())) == nv
+    C = np.linalg.solve(M[S].T, M.T).T
+    assert np.abs(C).max() <= 1 + 1e-8
+    v0 = abs(np.linalg.det(M[S]))
+    for t in range(m):
+        for c in range(nv):
+            S2 = S.copy()
+            S2[c] = t
+            assert abs(np.linalg.det(M[S2])) <= v0 * (1 + 1e-8)
+
+
+def test_maxvol_small_brute_force_ratio():
+    """A dominant submatrix of an m x nv matrix has volume >= max volume /
+    nv^(nv/2) (Goreinov-Tyrtyshnikov); here checked by brute force."""
+    import itertools
+    from oracle import maxvol
+    rng = np.random.default_rng(7)
+    for _ in range(5):
+        M = rng.standard_normal((8, 3))
+        S = maxvol(M)
+        best = max(abs(np.linalg.det(M[list(c)])) for c in itertools.combinations(range(8), 3))
+        assert abs(np.linalg.det(M[S])) >= best / 3 ** 1.5 - 1e-12
+
+
+def test_maxvol_rank_deficient_returns_none():
+    from oracle import maxvol
+    M = np.ones((5, 2))
+    assert maxvol(M) is None
+
+
+@pytest.mark.parametrize("name,size", [("1b", 8), ("3", 6), ("4", 2)])
+def test_maxvol_start_is_sparse_and_exact(name, size):
+    """The Alg. 1 start satisfies each local constraint exactly (P:527-540:
+    ||v - B w|| = 0) with at most nv nonzeros per row, so Alg. 2's correction
+    delta vanishes and W0 is the tentative start itself."""
+    prob = make_config(name, size=size)
+    o = Oracle(prob, start="maxvol")
+    assert o.n_maxvol_fail == 0
+    w0 = o.vec("w0")
+    wptr, wcol, frow = o.layout()
+    Cm, b = D.constraint_matrix(prob)
+    assert np.abs(Cm @ w0 - b).max() <= 1e-13 * max(1.0, np.abs(b).max())
+    for i in range(len(wptr) - 1):
+        row = w0[wptr[i]:wptr[i + 1]]
+        assert np.count_nonzero(np.abs(row) > 1e-13 * np.abs(row).max()) <= prob.nv
+
+
+def test_maxvol_start_scalar_B1_is_injection_from_first_column():
+    """nv = 1, B = 1: all |V_c| equal, the tie goes to the first column of
+    J_i, so the start injects from it: w = 1 there, 0 elsewhere."""
+    prob = make_config("1b", size=8)
+    o = Oracle(prob, start="maxvol")
+    w0 = o.vec("w0")
+    wptr, _, _ = o.layout()
+    for i in range(len(wptr) - 1):
+        row = w0[wptr[i]:wptr[i + 1]]
+        assert abs(row[0] - 1.0) <= 1e-15 and np.all(np.abs(row[1:]) <= 1e-15)
+
+
+@pytest.mark.parametrize("name,size", [("1b", 10), ("4", 2)])
+def test_maxvol_start_converges_to_kkt(name, size):
+    """The minimiser does not depend on the start."""
+    prob = make_config(name, size=size)
+    o = Oracle(prob, start="maxvol", stagnation_rel=1e-28)
+    o.iterate(400)
+    w = D.kkt_solution(prob)
+    assert np.abs(o.get_W() - w).max() <= 1e-8 * np.abs(w).max()
