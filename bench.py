@@ -203,6 +203,8 @@ def main():
                     help="Alg. 3 preconditioner: Jacobi M_1 (default, the headline) or projected SGS M_2")
     ap.add_argument("--sgs-key", default="color", choices=["color", "natural"],
                     help="SGS visiting order (reading A23): a grid colouring or the natural row order")
+    ap.add_argument("--start", default="given", choices=["given", "maxvol"],
+                    help="W^ start: the workload's (least-norm) or Alg. 1's max-vol tentative start")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -266,7 +268,7 @@ def main():
                             arrs["is_coarse"], arrs["P_rowptr"][rb:re_ + 1], arrs["P_col"], arrs["P_val"],
                             nv, arrs["B"][rb:re_], arrs["Bc"], block_size=prob.block_size,
                             stagnation_rel=0.0, stream=stream.cuda_stream, nccl_comm=comm,
-                            row_begin=rb, row_end=re_, precond=args.precond,
+                            row_begin=rb, row_end=re_, precond=args.precond, start=args.start,
                             sgs_key=None if kk is None else kk[rb:re_])
 
     stats = {"launches": 0, "spgemm_ms": 0.0, "spgemm_n": 0, "stage_ms": [0.0, 0.0], "scalar_ms": 0.0,
@@ -422,7 +424,8 @@ def main():
                    "parallelism": f"rows{world}" if world > 1 else "single GPU",
                    "kernel_path": E.KERNEL_PATHS.get(stats["report"]["kernel_path"]),
                    "precond": args.precond if args.precond == "jacobi" else
-                   f"sgs ({args.sgs_key} order, {stats['report']['sgs_levels']} levels per sweep)"},
+                   f"sgs ({args.sgs_key} order, {stats['report']['sgs_levels']} levels per sweep)",
+                   "start": args.start},
         "roofline": roofline,
         "iter_only": {"value": nnzW_global * k_it / (it_ms_med / 1e3), "unit": UNIT,
                       "ms_per_iter": it_ms_med / k_it,

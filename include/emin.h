@@ -87,10 +87,19 @@ typedef struct {
                                    row) order (reading A23); NULL = natural row order.  Host or
                                    device pointer as the other arrays.  A colouring key makes the
                                    sweeps short (few dependency levels). */
+  int32_t start;                /* EMIN_START_GIVEN: W^ = P_val, or the least-norm start if
+                                   P_val is NULL (reading A9);  EMIN_START_MAXVOL: the tentative
+                                   start of Alg. 1 on the given pattern -- per F row
+                                   the max-vol selection of nv columns of V_c(J_i,:)^T, the local
+                                   system solved exactly on them, zero elsewhere (reading A24;
+                                   P_val ignored).  Rows without a nonsingular selection keep
+                                   W^ = 0 (counted in emin_report_t.n_maxvol_fail). */
 } emin_opts;
 
 #define EMIN_PREC_JACOBI 0
 #define EMIN_PREC_SGS 1
+#define EMIN_START_GIVEN 0
+#define EMIN_START_MAXVOL 1
 
 typedef struct {
   double  E0;          /* tr(P0^T A P0) after Alg. 2 */
@@ -106,6 +115,7 @@ typedef struct {
   int64_t launches;    /* kernels this context has enqueued so far (setup included) */
   int32_t precond;     /* EMIN_PREC_JACOBI or EMIN_PREC_SGS */
   int64_t sgs_levels;  /* dependency levels of one SGS sweep (0 for Jacobi) */
+  int64_t n_maxvol_fail;  /* F rows where the max-vol start found no nonsingular selection */
 } emin_report_t;
 
 /* Fill opts with defaults (rank_tol 1e-10, tau 0, project_after_jacobi 0,

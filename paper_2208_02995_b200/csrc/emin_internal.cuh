@@ -99,7 +99,7 @@ struct emin_ctx_s {
   int64_t dE_cap = 0;
   DevState* st = nullptr;
   double sum_diag_cc = 0.0;
-  int64_t n_svd = 0, n_frozen = 0, n_crows = 0;
+  int64_t n_svd = 0, n_frozen = 0, n_crows = 0, n_maxvol_fail = 0;
   // launch geometry
   int grid_rows = 0, grid_spgemm = 0, grid_red = 0;
   // graphs: one per k (cached)
@@ -256,6 +256,10 @@ cudaError_t emin_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* t
 int64_t emin_scan_scratch_elems(int64_t n);
 
 int emin_num_sms();
+
+// Alg. 1 tentative start (maxvol.cu)
+void emin_maxvol_start(emin_ctx c, const double* Bc, const double* B, const int64_t* frow, double* what,
+                       unsigned long long* fails, cudaStream_t s);
 
 // projected SGS preconditioner (sgs.cu)
 emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* frow, cudaStream_t s);

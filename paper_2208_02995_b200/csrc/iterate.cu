@@ -854,6 +854,7 @@ extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
   rep->launches = c->launches;
   rep->precond = c->opts.precond;
   rep->sgs_levels = emin_sgs_levels(c);
+  rep->n_maxvol_fail = c->n_maxvol_fail;
   if (h.stopped == 5 && !c->breakdown_reported) {
     c->breakdown_reported = 1;
     return EMIN_ERR_BREAKDOWN;

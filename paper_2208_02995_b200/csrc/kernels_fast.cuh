@@ -959,7 +959,7 @@ __device__ __forceinline__ void w8_issue(const W8Win& d, W8Buf* b, const DevView
 __global__ void __launch_bounds__(W8_WARPS * 32, 4)
 k_spgemm_win8(DevView v, const int4* __restrict__ A4, const int4* __restrict__ hdr, int64_t nwin,
               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
-  extern __shared__ __align__(16) unsigned char w8_smem[];
+  extern __shared__ __align__(128) unsigned char w8_smem[];
   __shared__ double sh[32];
   __shared__ double s_qa[W8_WARPS][32];
   if (v.st->stopped) { iter_stopped(v); return; }

@@ -477,6 +477,7 @@ extern "C" void emin_default_opts(emin_opts* o, int64_t n_global) {
   o->inputs_on_device = 0;
   o->precond = EMIN_PREC_JACOBI;
   o->sgs_key = nullptr;
+  o->start = EMIN_START_GIVEN;
 }
 
 static emin_status fail(emin_ctx ctx, emin_status st, const std::string& msg) {
@@ -525,6 +526,8 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     return fail(ctx, EMIN_ERR_ARG, "n_global exceeds the int32 column range");
   if (opts->precond != EMIN_PREC_JACOBI && opts->precond != EMIN_PREC_SGS)
     return fail(ctx, EMIN_ERR_ARG, "precond must be EMIN_PREC_JACOBI or EMIN_PREC_SGS");
+  if (opts->start != EMIN_START_GIVEN && opts->start != EMIN_START_MAXVOL)
+    return fail(ctx, EMIN_ERR_ARG, "start must be EMIN_START_GIVEN or EMIN_START_MAXVOL");
   if (opts->precond == EMIN_PREC_SGS && opts->nccl_comm)
     return fail(ctx, EMIN_ERR_ARG, "the SGS preconditioner runs on one GPU (nccl_comm must be NULL)");
 
@@ -772,13 +775,15 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   SETUP_TRY(dalloc(&ctx->yb, W, s));
   SETUP_TRY(dalloc(&ctx->st, 1, s));
   unsigned long long* counters;
-  SETUP_TRY(dalloc(&counters, 2, s)); temps.push_back(counters);
-  SETUP_TRY(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, s));
+  SETUP_TRY(dalloc(&counters, 3, s)); temps.push_back(counters);
+  SETUP_TRY(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 3, s));
   SETUP_TRY(cudaMemsetAsync(ctx->dw, 0, sizeof(double) * Wh, s));
   SETUP_TRY(cudaMemsetAsync(ctx->y, 0, sizeof(double) * Wh, s));
   SETUP_TRY(cudaMemsetAsync(ctx->yb, 0, sizeof(double) * W, s));
   const DevView v = ctx->view();
   const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>((nF + 3) / 4, (int64_t)SM * 16));
+  if (opts->start == EMIN_START_MAXVOL && nF > 0)      // Alg. 1 tentative start (NEXT-3, reading A24)
+    emin_maxvol_start(ctx, dBc, dB, frow, what, counters + 2, s);
   if (emin_alg2_fast(ctx, dBc, dB, frow, what, counters, s))
     ;
   else if (ctx->max_row <= 32)
@@ -799,12 +804,13 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   // ---- r0 = -Pi (A P0)|F and E0 = tr(P0^T A P0)
   double h_sum_cc = 0.0;
   SETUP_TRY(cudaMemcpyAsync(&h_sum_cc, dsum, sizeof(double), cudaMemcpyDeviceToHost, s));
-  unsigned long long h_cnt[2];
+  unsigned long long h_cnt[3];
   SETUP_TRY(cudaMemcpyAsync(h_cnt, counters, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
   SETUP_TRY(cudaStreamSynchronize(s));
   ctx->sum_diag_cc = h_sum_cc;
   ctx->n_svd = (int64_t)h_cnt[0];
   ctx->n_frozen = (int64_t)h_cnt[1];
+  ctx->n_maxvol_fail = (int64_t)h_cnt[2];
   // kernels enqueued above: coarse flags, 4 scans x 3, rows, check_B, fill, 2 reduce, alg2
   ctx->launches += 1 + 3 + 2 + (nF > 0 ? 9 : 0) + 1 + 2 + 1;
   emin_status st = emin_finish_r0(ctx);

@@ -38,11 +38,14 @@ class emin_opts(C.Structure):
                 ("project_after_jacobi", C.c_int32), ("stagnation_rel", C.c_double),
                 ("stream", C.c_void_p), ("nccl_comm", C.c_void_p),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64),
-                ("inputs_on_device", C.c_int32), ("precond", C.c_int32), ("sgs_key", C.c_void_p)]
+                ("inputs_on_device", C.c_int32), ("precond", C.c_int32), ("sgs_key", C.c_void_p),
+                ("start", C.c_int32)]
 
 
 EMIN_PREC_JACOBI, EMIN_PREC_SGS = 0, 1
 PRECONDS = {"jacobi": EMIN_PREC_JACOBI, "sgs": EMIN_PREC_SGS}
+EMIN_START_GIVEN, EMIN_START_MAXVOL = 0, 1
+STARTS = {"given": EMIN_START_GIVEN, "maxvol": EMIN_START_MAXVOL}
 
 
 class emin_report_t(C.Structure):
@@ -50,7 +53,8 @@ class emin_report_t(C.Structure):
                 ("stop_reason", C.c_int32), ("n_svd_rows", C.c_int64),
                 ("n_frozen_rows", C.c_int64), ("n_fine", C.c_int64), ("nnz_W", C.c_int64),
                 ("nnz_AFF", C.c_int64), ("kernel_path", C.c_int32), ("nranks", C.c_int32),
-                ("launches", C.c_int64), ("precond", C.c_int32), ("sgs_levels", C.c_int64)]
+                ("launches", C.c_int64), ("precond", C.c_int32), ("sgs_levels", C.c_int64),
+                ("n_maxvol_fail", C.c_int64)]
 
 
 EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "emin_get_P",
@@ -145,10 +149,11 @@ def _prep(a, np_dtype, torch_dtype=None):
 def emin_setup(n_global, nc_global, A_rowptr, A_col, A_val, is_coarse, P_rowptr, P_col, P_val,
                nv, B, Bc, *, block_size=1, rank_tol=1e-10, tau=0.0, project_after_jacobi=0,
                stagnation_rel=1e-30, stream=None, nccl_comm=None, row_begin=0, row_end=None,
-               precond="jacobi", sgs_key=None):
+               precond="jacobi", sgs_key=None, start="given"):
     """emin_setup (include/emin.h).  Returns the opaque context handle.
     precond: "jacobi" | "sgs" (or EMIN_PREC_*); sgs_key: per owned row,
-    same side (host / cuda) as the other arrays, or None."""
+    same side (host / cuda) as the other arrays, or None.  start: "given"
+    (P_val / least-norm) or "maxvol" (Alg. 1's tentative start)."""
     lib = load_library()
     import torch
     arrs = [A_rowptr, A_col, A_val, is_coarse, P_rowptr, P_col, P_val, B, Bc]
@@ -182,6 +187,7 @@ def emin_setup(n_global, nc_global, A_rowptr, A_col, A_val, is_coarse, P_rowptr,
     o.inputs_on_device = 1 if dev else 0
     o.precond = PRECONDS[precond] if isinstance(precond, str) else int(precond)
     o.sgs_key = _ptr(key)
+    o.start = STARTS[start] if isinstance(start, str) else int(start)
     h = C.c_void_p()
     st = lib.emin_setup(C.byref(h), int(n_global), int(nc_global), *[_ptr(a) for a in keep[:7]],
                         int(nv), _ptr(keep[7]), _ptr(keep[8]), C.byref(o))

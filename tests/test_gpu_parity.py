@@ -382,3 +382,34 @@ def test_sgs_nodal_sweep_equals_generic_sweep(name, size, kind, monkeypatch):
     kb, dEb = b.iterate(20)
     assert ka == kb and np.allclose(dEa, dEb, rtol=1e-9)
     assert np.abs(a.get_P() - b.get_P()).max() <= 1e-10 * np.abs(b.get_P()).max()
+
+
+# --------------------------------------------------------------------------
+# Alg. 1 tentative start by max vol (NEXT-3, reading A24)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,size,k", [("1b", None, 20), ("2b", 10, 30), ("3", 12, 40), ("4", 3, 30),
+                                         ("4", 4, 30), ("5", 8, 40)])
+def test_maxvol_start_parity(name, size, k):
+    from oracle import Oracle
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    g = Emin.from_problem(prob, start="maxvol")
+    o = Oracle(prob, start="maxvol", project_z=True)
+    assert g.report()["n_maxvol_fail"] == o.n_maxvol_fail
+    _check_layout(g, o, prob)
+    _compare(g, o, k, prob)
+
+
+def test_maxvol_start_with_sgs_full_config4():
+    """Alg. 1 start + projected SGS on BASELINE config 4 at full size:
+    monotone energy and the constraint on sampled rows (properties)."""
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config, sgs_key
+    prob = make_config("4")
+    g = Emin.from_problem(prob, start="maxvol", precond="sgs", sgs_key=sgs_key(prob, "color"))
+    assert g.report()["n_maxvol_fail"] == 0
+    kd, dE = g.iterate(10)
+    assert kd == 10 and np.all(dE > 0)
+    _constraint_sampled(prob, g.get_P(), 2000)
