@@ -69,6 +69,10 @@ def _load():
         lib.oracle_setup_row.restype = i32
         lib.oracle_maxvol.argtypes = [i32, i32, P, P]
         lib.oracle_maxvol.restype = i32
+        lib.oracle_pattern.argtypes = [i64, P, P, P, i32, i32, P, i32, i32, P, P, P]
+        lib.oracle_pattern.restype = i64
+        lib.oracle_gram_full_rank.argtypes = [i32, P]
+        lib.oracle_gram_full_rank.restype = i32
         _lib = lib
     return _lib
 
@@ -237,6 +241,29 @@ def maxvol(M):
     S = np.zeros(nv, np.int32)
     ok = lib.oracle_maxvol(m, nv, _p(Mc), _p(S))
     return S.copy() if ok else None
+
+
+def pattern(prob, l0=2, lmax=4):
+    """Alg. 1's pattern growth from the graph of A (reading A25): returns
+    (P_rowptr, P_col, hist) for all rows of prob (C rows identity)."""
+    lib = _load()
+    n = prob.n
+    rp = np.zeros(n + 1, np.int64)
+    hist = np.zeros(lmax + 1, np.int64)
+    args = [np.ascontiguousarray(prob.A_rowptr, np.int64), np.ascontiguousarray(prob.A_col, np.int32),
+            np.ascontiguousarray(prob.is_coarse, np.uint8)]
+    Bc = np.ascontiguousarray(prob.Bc, np.float64)
+    nnz = lib.oracle_pattern(n, _p(args[0]), _p(args[1]), _p(args[2]), prob.block_size, prob.nv, _p(Bc),
+                             l0, lmax, _p(rp), None, None)
+    col = np.zeros(max(nnz, 1), np.int32)
+    lib.oracle_pattern(n, _p(args[0]), _p(args[1]), _p(args[2]), prob.block_size, prob.nv, _p(Bc),
+                       l0, lmax, _p(rp), _p(col), _p(hist))
+    return rp, col[:nnz], hist
+
+
+def gram_full_rank(G):
+    G = np.ascontiguousarray(G, np.float64)
+    return bool(_load().oracle_gram_full_rank(G.shape[0], _p(G)))
 
 
 def setup_row(M, r, tol=1e-10):

@@ -34,6 +34,9 @@
  *             dE_k <= stag E0 -> stop                       (A18)
  *             dw += alpha y ; r -= alpha yb
  *   energy  tr(P^T A P) by its definition (Eq. trace), P = [W; I].
+ *   pattern (NEXT-3) oracle_pattern: the pattern of P from the graph of A by
+ *           Alg. 1's growth loop (reading A25); pinned bit-exactly against
+ *           the independent box-arithmetic input generator.
  *   start   (optional) the tentative start W^ of Alg. 1
  *            on the prescribed pattern: per F row the max-vol
  *           selection of nv columns of V_c(J_i,:)^T (reading A24), the local
@@ -828,4 +831,137 @@ void oracle_copy_Q(const oracle_t *o, double *Q, int *krank) {
 int oracle_setup_row(int nj, int nv, const double *M, const double *rvec, double tol,
                      double *Qrow, double *delta, int *used_svd) {
     return emin_setup_row(nj, nv, M, rvec, tol, Qrow, delta, used_svd);
+}
+
+/* ---------------- Alg. 1 pattern growth (NEXT-3, reading A25) ----------- */
+/* The sparsity pattern of P from the graph of A (Eq. enlPatt, and
+ * the growth loop of Alg. 1): the graph has an edge i ~ k for every
+ * off-diagonal nonzero of A (reading A12, no strength threshold); with
+ * block_size 3 it is the node graph (node I ~ K if the 3x3 block (I,K) has a
+ * nonzero; rows 3I..3I+2 of a node) and the pattern is applied blockwise.
+ * For every F node: N_l = the C nodes within graph distance l, for
+ * l = l0, l0+1, ... until the Gram matrix G = M^T M of M = V_c(J,:) (J = the
+ * dofs of N_l) has lambda_min > 1e-10 lambda_max (full rank; the same
+ * criterion as the input generator), and unconditionally at l = lmax.
+ * Columns ascending (coarse ids).  C rows: {coarse(c)}. */
+
+/* eigenvalues of the symmetric n x n matrix a (row-major, destroyed) by
+ * cyclic Jacobi rotations; returns min and max */
+static void jacobi_eig_minmax(int n, double *a, double *lmin, double *lmax) {
+    for (int sweep = 0; sweep < 50; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) off += a[p * n + q] * a[p * n + q];
+        if (off == 0.0) break;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                double apq = a[p * n + q];
+                if (apq == 0.0) continue;
+                double theta = (a[q * n + q] - a[p * n + p]) / (2.0 * apq);
+                double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < n; ++k) {          /* columns p, q */
+                    double akp = a[k * n + p], akq = a[k * n + q];
+                    a[k * n + p] = c * akp - s * akq;
+                    a[k * n + q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < n; ++k) {          /* rows p, q */
+                    double apk = a[p * n + k], aqk = a[q * n + k];
+                    a[p * n + k] = c * apk - s * aqk;
+                    a[q * n + k] = s * apk + c * aqk;
+                }
+            }
+    }
+    double mn = a[0], mx = a[0];
+    for (int k = 1; k < n; ++k) { if (a[k * n + k] < mn) mn = a[k * n + k]; if (a[k * n + k] > mx) mx = a[k * n + k]; }
+    *lmin = mn; *lmax = mx;
+}
+
+int oracle_gram_full_rank(int nv, const double *G) {
+    double a[256], mn, mx;
+    memcpy(a, G, sizeof(double) * nv * nv);
+    jacobi_eig_minmax(nv, a, &mn, &mx);
+    if (mx < 0.0) mx = 0.0;
+    return mn > 1e-10 * mx;
+}
+
+static int cmp_i64(const void *a, const void *b) {
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* Returns the number of nonzeros of the pattern (all rows); fills P_rowptr
+ * [n+1] and, if P_col != NULL, P_col.  Also the histogram of the distance
+ * used per F node (hist[l], l <= lmax) if hist != NULL. */
+int64_t oracle_pattern(int64_t n, const int64_t *A_rowptr, const int32_t *A_col, const uint8_t *is_coarse,
+                       int block_size, int nv, const double *Bc, int l0, int lmax,
+                       int64_t *P_rowptr, int32_t *P_col, int64_t *hist) {
+    int bs = block_size;
+    int64_t nn = n / bs;                          /* nodes */
+    int64_t *cid = (int64_t *)malloc(sizeof(int64_t) * nn);
+    int64_t nc = 0;
+    for (int64_t u = 0; u < nn; ++u) cid[u] = is_coarse[u * bs] ? nc++ : -1;
+    int64_t *stamp = (int64_t *)malloc(sizeof(int64_t) * nn);
+    for (int64_t u = 0; u < nn; ++u) stamp[u] = -1;
+    int64_t *front = (int64_t *)malloc(sizeof(int64_t) * nn), *next = (int64_t *)malloc(sizeof(int64_t) * nn);
+    int64_t *clist = (int64_t *)malloc(sizeof(int64_t) * nn);
+    int64_t nnz = 0;
+    if (hist) for (int l = 0; l <= lmax; ++l) hist[l] = 0;
+    P_rowptr[0] = 0;
+    for (int64_t I = 0; I < nn; ++I) {
+        int64_t cnt = 0;
+        if (cid[I] >= 0) {
+            cnt = 1;
+        } else {
+            int64_t nf = 1, ncl = 0;
+            front[0] = I;
+            stamp[I] = I;
+            int lused = lmax;
+            for (int l = 1; l <= lmax; ++l) {
+                int64_t nx = 0;
+                for (int64_t f = 0; f < nf; ++f) {
+                    int64_t u = front[f], r = u * bs;
+                    for (int64_t q = A_rowptr[r]; q < A_rowptr[r + 1]; ++q) {
+                        int64_t w = A_col[q] / bs;
+                        if (stamp[w] == I) continue;
+                        stamp[w] = I;
+                        next[nx++] = w;
+                        if (cid[w] >= 0) clist[ncl++] = cid[w];
+                    }
+                }
+                memcpy(front, next, sizeof(int64_t) * nx);
+                nf = nx;
+                if (l < l0) continue;
+                if (l == lmax) break;
+                if (ncl == 0) continue;
+                double G[256];
+                for (int k = 0; k < nv * nv; ++k) G[k] = 0.0;
+                for (int64_t t = 0; t < ncl; ++t)
+                    for (int b = 0; b < bs; ++b) {
+                        const double *row = Bc + (bs * clist[t] + b) * nv;
+                        for (int p = 0; p < nv; ++p)
+                            for (int q = 0; q < nv; ++q) G[p * nv + q] += row[p] * row[q];
+                    }
+                if (oracle_gram_full_rank(nv, G)) { lused = l; break; }
+            }
+            if (hist) hist[lused]++;
+            qsort(clist, ncl, sizeof(int64_t), cmp_i64);
+            cnt = ncl * bs;
+            if (P_col)
+                for (int64_t t = 0; t < ncl; ++t)
+                    for (int b = 0; b < bs; ++b) P_col[nnz + t * bs + b] = (int32_t)(bs * clist[t] + b);
+        }
+        const int64_t base = nnz;
+        if (cid[I] >= 0) {                          /* C rows: each dof row its own column */
+            if (P_col) for (int b = 0; b < bs; ++b) P_col[base + b] = (int32_t)(bs * cid[I] + b);
+        } else if (P_col) {                         /* the bs rows of an F node share the list */
+            for (int b = 1; b < bs; ++b) memcpy(P_col + base + b * cnt, P_col + base, sizeof(int32_t) * cnt);
+        }
+        for (int b = 0; b < bs; ++b) {
+            nnz += cnt;
+            P_rowptr[I * bs + b + 1] = nnz;
+        }
+    }
+    free(cid); free(stamp); free(front); free(next); free(clist);
+    return nnz;
 }

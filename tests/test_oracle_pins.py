@@ -585,3 +585,35 @@ def test_maxvol_start_converges_to_kkt(name, size):
     o.iterate(400)
     w = D.kkt_solution(prob)
     assert np.abs(o.get_W() - w).max() <= 1e-8 * np.abs(w).max()
+
+
+# --------------------------------------------------------------------------
+# Alg. 1 pattern growth from the graph of A (reading A25)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,size", [("1b", None), ("2", 10), ("2b", 12), ("3", 12), ("3", 17),
+                                       ("4", 3), ("4", 6), ("5", 8)])
+def test_pattern_from_graph_matches_generator(name, size):
+    """The oracle's BFS over the graph of A reproduces, bit for bit, the input
+    generator's pattern -- built independently from grid-box arithmetic
+    (Manhattan balls for the 5/7-point stencils, Chebyshev balls of the
+    27-point node graph, per-row growth until full rank)."""
+    from oracle import pattern
+    prob = make_config(name, size=size)
+    rp, col, hist = pattern(prob)
+    assert np.array_equal(rp, prob.P_rowptr) and np.array_equal(col, prob.P_col)
+    nodes = prob.n_F // prob.block_size
+    assert hist.sum() == nodes
+    assert {l: int(c) for l, c in enumerate(hist) if c} == {int(k): int(v) for k, v in prob.meta["growth"].items()}
+
+
+def test_gram_full_rank_matches_numpy():
+    from oracle import gram_full_rank
+    rng = np.random.default_rng(11)
+    for nv in (1, 3, 6):
+        for cond in (1e0, 1e3, 1e8, 1e12, 1e20):
+            U = np.linalg.qr(rng.standard_normal((nv, nv)))[0]
+            ev = np.geomspace(1.0, 1.0 / cond, nv)
+            G = (U * ev) @ U.T
+            ref = np.linalg.eigvalsh(G)
+            assert gram_full_rank(G) == bool(ref[0] > 1e-10 * max(ref[-1], 0.0))
