@@ -183,6 +183,28 @@ const char* emin_last_error(emin_ctx ctx);
  * row in the caller's P CSR (relative to P_rowptr[0]).  Synchronous. */
 emin_status emin_get_layout(emin_ctx ctx, int64_t* wptr, int32_t* wcol, int64_t* pofs);
 
+/* Alg. 1's pattern growth (P:527-540 with Eq. enlPatt; SURVEY §8f
+ * NEXT-3, reading A25) on one GPU: the sparsity pattern of P from the graph
+ * of A.  Graph: an edge i ~ k per off-diagonal nonzero of A (no strength
+ * threshold, reading A12); block_size 3 = the node graph of 3x3 blocks (row
+ * 3I lists node I's neighbours), pattern applied blockwise.  For every F node
+ * the C nodes within graph distance l, l = l0, l0+1, ... until
+ * lambda_min(M^T M) > 1e-10 lambda_max(M^T M), M = Bc(J,:) (J = their
+ * dofs), and unconditionally at l = lmax; columns ascending; C rows
+ * {coarse(c)} (coarse id = rank among C points).
+ *   n, A_rowptr [n+1], A_col : the whole matrix (global); is_coarse [n];
+ *   Bc [nc x nv] row-major; P_rowptr [n+1] out; P_col [nnz] out or NULL
+ *   (count only); P_col_cap its capacity (EMIN_ERR_ARG if < nnz, P_rowptr
+ *   and *nnz_out still filled: call again); all pointers host, or device if
+ *   inputs_on_device; stream = cudaStream_t.  Synchronous.
+ * EMIN_ERR_PATTERN if a neighbourhood exceeds the kernel's shared-memory sets
+ * (2048 visited nodes / 1024 frontier or C nodes per F node). */
+emin_status emin_pattern(int64_t n, const int64_t* A_rowptr, const int32_t* A_col, const uint8_t* is_coarse,
+                         int32_t block_size, int32_t nv, const double* Bc, int64_t nc, int32_t l0,
+                         int32_t lmax, int64_t* P_rowptr, int32_t* P_col, int64_t P_col_cap,
+                         int64_t* nnz_out, int32_t inputs_on_device, void* stream);
+const char* emin_pattern_error(void);
+
 /* Multi-GPU helpers (one process per GPU, NCCL over NVLink/NVSwitch).
  * emin_nccl_unique_id fills id[128] on one rank; the caller broadcasts it
  * (e.g. with torch.distributed) and every rank calls emin_nccl_comm_init;

@@ -60,7 +60,7 @@ class emin_report_t(C.Structure):
 EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "emin_get_P",
             "emin_reset", "emin_report", "emin_destroy", "emin_status_str", "emin_last_error",
             "emin_set_profiling", "emin_kernel_times", "emin_get_layout", "emin_nccl_unique_id",
-            "emin_nccl_comm_init", "emin_nccl_comm_destroy"]
+            "emin_nccl_comm_init", "emin_nccl_comm_destroy", "emin_pattern", "emin_pattern_error"]
 
 
 def load_library():
@@ -107,6 +107,10 @@ def load_library():
     lib.emin_nccl_comm_init.restype = i32
     lib.emin_nccl_comm_destroy.argtypes = [P]
     lib.emin_nccl_comm_destroy.restype = i32
+    lib.emin_pattern.argtypes = [i64, P, P, P, i32, i32, P, i64, i32, i32, P, P, i64, C.POINTER(i64), i32, P]
+    lib.emin_pattern.restype = i32
+    lib.emin_pattern_error.argtypes = []
+    lib.emin_pattern_error.restype = C.c_char_p
     _lib = lib
     return lib
 
@@ -247,6 +251,31 @@ def emin_get_layout(ctx):
     pofs = np.empty(max(nF, 1), np.int64)
     _check(load_library().emin_get_layout(ctx, _ptr(wptr), _ptr(wcol), _ptr(pofs)), ctx)
     return wptr, wcol[:W], pofs[:nF]
+
+
+def emin_pattern(n, A_rowptr, A_col, is_coarse, block_size, nv, Bc, nc, l0=2, lmax=4, stream=None):
+    """emin_pattern (include/emin.h): Alg. 1's pattern growth from the graph
+    of A on the GPU.  Host numpy inputs; returns (P_rowptr, P_col)."""
+    lib = load_library()
+    import torch
+    arrs = [np.ascontiguousarray(A_rowptr, np.int64), np.ascontiguousarray(A_col, np.int32),
+            np.ascontiguousarray(is_coarse, np.uint8), np.ascontiguousarray(Bc, np.float64)]
+    rp = np.zeros(int(n) + 1, np.int64)
+    nnz = C.c_int64(0)
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    st = lib.emin_pattern(int(n), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), int(block_size), int(nv),
+                          _ptr(arrs[3]), int(nc), int(l0), int(lmax), _ptr(rp), None, 0, C.byref(nnz), 0,
+                          C.c_void_p(int(stream)))
+    if st != 0:
+        raise EminError(st, lib.emin_pattern_error().decode())
+    col = np.zeros(max(nnz.value, 1), np.int32)
+    st = lib.emin_pattern(int(n), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), int(block_size), int(nv),
+                          _ptr(arrs[3]), int(nc), int(l0), int(lmax), _ptr(rp), _ptr(col), nnz.value,
+                          C.byref(nnz), 0, C.c_void_p(int(stream)))
+    if st != 0:
+        raise EminError(st, lib.emin_pattern_error().decode())
+    return rp, col[:nnz.value]
 
 
 def emin_nccl_unique_id():

@@ -413,3 +413,25 @@ def test_maxvol_start_with_sgs_full_config4():
     kd, dE = g.iterate(10)
     assert kd == 10 and np.all(dE > 0)
     _constraint_sampled(prob, g.get_P(), 2000)
+
+
+# --------------------------------------------------------------------------
+# Alg. 1 pattern growth on the GPU (NEXT-3, reading A25)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,size", [("1b", None), ("2", 12), ("2b", 10), ("3", 12), ("3", 17), ("4", 3),
+                                       ("4", 6), ("5", 8), ("2", None), ("3", None), ("4", None)])
+def test_pattern_gpu_matches_oracle_and_generator(name, size):
+    """Index structure: bit-exact against the oracle's BFS and against the
+    input generator (independent box arithmetic), full-size configs 2-4
+    included."""
+    from oracle import pattern
+    from paper_2208_02995_b200 import emin as E
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    rp, col = E.emin_pattern(prob.n, prob.A_rowptr, prob.A_col, prob.is_coarse, prob.block_size, prob.nv,
+                             prob.Bc, prob.nc)
+    assert np.array_equal(rp, prob.P_rowptr) and np.array_equal(col, prob.P_col)
+    if prob.n < 400000:
+        orp, ocol, _ = pattern(prob)
+        assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
