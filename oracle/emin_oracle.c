@@ -849,10 +849,15 @@ int oracle_setup_row(int nj, int nv, const double *M, const double *rvec, double
  * cyclic Jacobi rotations; returns min and max */
 static void jacobi_eig_minmax(int n, double *a, double *lmin, double *lmax) {
     for (int sweep = 0; sweep < 50; ++sweep) {
-        double off = 0.0;
-        for (int p = 0; p < n; ++p)
+        /* converged when the off-diagonal mass is below (1e-16 trace)^2: the
+         * eigenvalues are then exact to ~1e-16 lambda_max, far inside the
+         * 1e-10 rank threshold */
+        double off = 0.0, tr = 0.0;
+        for (int p = 0; p < n; ++p) {
+            tr += fabs(a[p * n + p]);
             for (int q = p + 1; q < n; ++q) off += a[p * n + q] * a[p * n + q];
-        if (off == 0.0) break;
+        }
+        if (off <= 1e-32 * tr * tr) break;
         for (int p = 0; p < n; ++p)
             for (int q = p + 1; q < n; ++q) {
                 double apq = a[p * n + q];

@@ -44,35 +44,70 @@ struct PtArgs {
   int32_t* overflow;
 };
 
-__device__ void pt_jacobi_minmax(int n, double* a, double* mn, double* mx) {
+// extreme eigenvalues of the symmetric N x N matrix a (row-major, destroyed)
+// by cyclic Jacobi rotations, fully unrolled (registers); stops when the
+// off-diagonal mass is below (1e-16 trace)^2 (the oracle's criterion)
+template <int N>
+__device__ void pt_jacobi_minmax(double* a, double* mn, double* mx) {
   for (int sweep = 0; sweep < 50; ++sweep) {
-    double off = 0.0;
-    for (int p = 0; p < n; ++p)
-      for (int q = p + 1; q < n; ++q) off += a[p * n + q] * a[p * n + q];
-    if (off == 0.0) break;
-    for (int p = 0; p < n; ++p)
-      for (int q = p + 1; q < n; ++q) {
-        const double apq = a[p * n + q];
+    double off = 0.0, tr = 0.0;
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      tr += fabs(a[p * N + p]);
+#pragma unroll
+      for (int q = p + 1; q < N; ++q) off += a[p * N + q] * a[p * N + q];
+    }
+    if (off <= 1e-32 * tr * tr) break;
+#pragma unroll
+    for (int p = 0; p < N; ++p)
+#pragma unroll
+      for (int q = p + 1; q < N; ++q) {
+        const double apq = a[p * N + q];
         if (apq == 0.0) continue;
-        const double theta = (a[q * n + q] - a[p * n + p]) / (2.0 * apq);
+        const double theta = (a[q * N + q] - a[p * N + p]) / (2.0 * apq);
         const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
         const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < n; ++k) {
-          const double akp = a[k * n + p], akq = a[k * n + q];
-          a[k * n + p] = c * akp - s * akq;
-          a[k * n + q] = s * akp + c * akq;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double akp = a[k * N + p], akq = a[k * N + q];
+          a[k * N + p] = c * akp - s * akq;
+          a[k * N + q] = s * akp + c * akq;
         }
-        for (int k = 0; k < n; ++k) {
-          const double apk = a[p * n + k], aqk = a[q * n + k];
-          a[p * n + k] = c * apk - s * aqk;
-          a[q * n + k] = s * apk + c * aqk;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double apk = a[p * N + k], aqk = a[q * N + k];
+          a[p * N + k] = c * apk - s * aqk;
+          a[q * N + k] = s * apk + c * aqk;
         }
       }
   }
   double lo = a[0], hi = a[0];
-  for (int k = 1; k < n; ++k) { lo = fmin(lo, a[k * n + k]); hi = fmax(hi, a[k * n + k]); }
+#pragma unroll
+  for (int k = 1; k < N; ++k) { lo = fmin(lo, a[k * N + k]); hi = fmax(hi, a[k * N + k]); }
   *mn = lo;
   *mx = hi;
+}
+
+template <int N>
+__device__ bool pt_full_rank(const double* G) {
+  double a[N * N], mn, mx;
+#pragma unroll
+  for (int k = 0; k < N * N; ++k) a[k] = G[k];
+  pt_jacobi_minmax<N>(a, &mn, &mx);
+  return mn > 1e-10 * fmax(mx, 0.0);
+}
+
+__device__ bool pt_full_rank_nv(int nv, const double* G) {
+  switch (nv) {
+    case 1: return pt_full_rank<1>(G);
+    case 2: return pt_full_rank<2>(G);
+    case 3: return pt_full_rank<3>(G);
+    case 4: return pt_full_rank<4>(G);
+    case 5: return pt_full_rank<5>(G);
+    case 6: return pt_full_rank<6>(G);
+    case 7: return pt_full_rank<7>(G);
+    default: return pt_full_rank<8>(G);
+  }
 }
 
 template <bool FILL>
@@ -172,12 +207,7 @@ k_pattern(PtArgs a) {
         if (lane == 0) s_G[wib][pq] = sum;
       }
       __syncwarp();
-      if (lane == 0) {
-        double G[EMIN_NV_MAX * EMIN_NV_MAX], mn, mx;
-        for (int k = 0; k < nv * nv; ++k) G[k] = s_G[wib][k];
-        pt_jacobi_minmax(nv, G, &mn, &mx);
-        s_ok[wib] = mn > 1e-10 * fmax(mx, 0.0);
-      }
+      if (lane == 0) s_ok[wib] = pt_full_rank_nv(nv, s_G[wib]);
       __syncwarp();
       if (s_ok[wib]) break;
     }
