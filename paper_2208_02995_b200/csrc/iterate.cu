@@ -465,15 +465,18 @@ void launch_stage(emin_ctx c, int which, cudaStream_t s) {
 // mode: MM_ITER (X = y), MM_R0 (X = w0), MM_ENERGY (X = w0, X2 = dw)
 int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
                        cudaStream_t s) {
+  // returns the grid (= number of partial sums), or -1 if the kernel path
+  // has no MM_R0E (fused r0 + E0) kernel -- the caller then runs MM_R0 and
+  // MM_ENERGY separately
   const DevView v = c->view();
   const int grid = c->grid_spgemm;
   if (c->kernel_path == 1) {
-    launch_scalar_masked(c, mode, X, X2, out, s);
+    if (!launch_scalar_masked(c, mode, X, X2, out, s)) return -1;
     return mode == MM_ITER ? scalar_iter_grid(c) : grid;
   }
   if (c->kernel_path == 2) {
     const NodalPlan* np = static_cast<const NodalPlan*>(c->nodal);
-    launch_nodal(c, np, mode, X, X2, out, s);
+    if (!launch_nodal(c, np, mode, X, X2, out, s)) return -1;
     return nodal_grid(c, np);
   }
   const int mc = c->max_row <= 32 ? 1 : c->max_row <= 64 ? 2 : 4;
@@ -483,6 +486,8 @@ int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, 
     if (mc == 1) LAUNCH_M(MM_ITER, 1, false); else if (mc == 2) LAUNCH_M(MM_ITER, 2, false); else LAUNCH_M(MM_ITER, 4, false);
   } else if (mode == MM_R0) {
     if (mc == 1) LAUNCH_M(MM_R0, 1, false); else if (mc == 2) LAUNCH_M(MM_R0, 2, false); else LAUNCH_M(MM_R0, 4, false);
+  } else if (mode == MM_R0E) {
+    if (mc == 1) LAUNCH_M(MM_R0E, 1, false); else if (mc == 2) LAUNCH_M(MM_R0E, 2, false); else LAUNCH_M(MM_R0E, 4, false);
   } else {
     if (mc == 1) LAUNCH_M(MM_ENERGY, 1, true); else if (mc == 2) LAUNCH_M(MM_ENERGY, 2, true); else LAUNCH_M(MM_ENERGY, 4, true);
   }
@@ -581,9 +586,13 @@ static std::pair<const double*, int> global_sum(emin_ctx c, int np, int slot, cu
 emin_status emin_finish_r0(emin_ctx c) {
   cudaStream_t s = c->stream;
   EMIN_CUDA_TRY(c, cudaMemsetAsync(c->dw, 0, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s));
-  emin_launch_masked(c, MM_R0, c->w0, nullptr, c->r, s);
-  // energy of P0 (dw = 0)
-  const int g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, s);
+  // r0 and the energy of P0 (dw = 0) share the masked product A P0: one
+  // MM_R0E pass where the kernel path has it, else MM_R0 then MM_ENERGY
+  int g = getenv("EMIN_NO_R0E") ? -1 : emin_launch_masked(c, MM_R0E, c->w0, nullptr, c->r, s);
+  if (g < 0) {
+    emin_launch_masked(c, MM_R0, c->w0, nullptr, c->r, s);
+    g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, s);
+  }
   const auto red = global_sum(c, g, 2, s);
   k_reset_state<<<1, 1024, 0, s>>>(c->st, red.first, red.second, c->sum_diag_cc, c->opts.tau,
                                    c->opts.stagnation_rel);

@@ -1611,7 +1611,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
     xo[u] = 0.0;
     if (e < nent) {
       if (MODE != MM_ENERGY) qv[u] = v.Q[H.base + e];
-      if (MODE == MM_ITER) xo[u] = X[H.base + e];
+      if (MODE == MM_ITER || MODE == MM_R0E) xo[u] = X[H.base + e];
       if (MODE == MM_ENERGY) xo[u] = X[H.base + e] + X2[H.base + e];
     }
   }
@@ -1620,6 +1620,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
     for (int p = s_wptr[r]; p < s_wptr[r + 1]; ++p) s_erow[p] = (uint16_t)r;
   __syncthreads();
   // ---- phase B: masked product from shared memory
+  double part = 0.0;
   double g[TILE_U];
   int rl[TILE_U];
 #pragma unroll
@@ -1651,11 +1652,11 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
           if (v.afccol[q] == j) { fc = v.afcval[q]; break; }
       }
       if (MODE == MM_ENERGY) g[u] = acc + 2.0 * fc;
-      else if (MODE == MM_R0) g[u] = acc + fc;
+      else if (MODE == MM_R0 || MODE == MM_R0E) g[u] = acc + fc;
       else g[u] = acc;
+      if (MODE == MM_R0E) part = fma(xo[u], acc + 2.0 * fc, part);   // E0 term, as MM_ENERGY
     }
   }
-  double part = 0.0;
   if (MODE == MM_ENERGY) {
 #pragma unroll
     for (int u = 0; u < TILE_U; ++u)
@@ -1663,7 +1664,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
   } else {
     // ---- Pi_B (nv = 1), twice for r0 (see masked.cuh)
 #pragma unroll
-    for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
+    for (int pass = 0; pass < ((MODE == MM_R0 || MODE == MM_R0E) ? 2 : 1); ++pass) {
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < TILE_U; ++u) {
@@ -2112,6 +2113,7 @@ static inline int select_fast_path(emin_ctx c) {
     cudaFuncSetAttribute(k_spgemm_tile<MM_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
     cudaFuncSetAttribute(k_spgemm_tile<MM_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
     cudaFuncSetAttribute(k_spgemm_tile<MM_ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
+    cudaFuncSetAttribute(k_spgemm_tile<MM_R0E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
   } else if (p.variant == 2) {
     p.variant = 5;
   }
@@ -2156,7 +2158,7 @@ static inline int scalar_iter_grid(emin_ctx c) {
   }
 }
 
-static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
+static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
                                         cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
@@ -2164,13 +2166,13 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
     switch (p.variant) {
       case 0:
         k_spgemm_hdr<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, X, out, c->partials);
-        return;
+        return true;
       case 4:
         k_spgemm_mask<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, p.emask, X, out, c->partials);
-        return;
+        return true;
       case 5:
         k_spgemm_win2<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
-        return;
+        return true;
       case 7:
       case 8: {
         const int g = scalar_grid(c);
@@ -2182,49 +2184,55 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
           k_spgemm_win4<true><<<g, 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent),
                                                 p.w4hdr, p.nwin, X, out,
                                                 c->partials);
-        return;
+        return true;
       }
       case 11:
         k_spgemm_win8<<<p.w8grid, W8_WARPS * 32, w8_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
                                                                       p.w6hdr, p.nwin, X, out, c->partials);
-        return;
+        return true;
       case 13: {
         const auto kfun = p.ellW <= 4 ? k_spgemm_win10<4> : p.ellW <= 6 ? k_spgemm_win10<6> : k_spgemm_win10<8>;
         kfun<<<p.w8grid, W8_WARPS * 32, w10_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent), p.w4hdr,
                                                                p.nwin, X, out, c->partials);
-        return;
+        return true;
       }
       case 12:
         k_spgemm_win9<<<p.w8grid, W8_WARPS * 32, w9_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
                                                                       p.w6hdr, p.nwin, X, out, c->partials);
-        return;
+        return true;
       case 10: {
         const int g = scalar_grid(c);
 #define W7(WW) case WW: k_spgemm_win7<WW><<<g, 256, 0, s>>>(v, p.ell, p.w7hdr, p.nwin, X, out, c->partials); break;
         switch (p.ellW) { W7(4) W7(5) W7(6) W7(7) W7(8) }
 #undef W7
-        return;
+        return true;
       }
       case 9:
         k_spgemm_win6<<<scalar_grid(c), 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent), p.w6hdr, p.nwin, X,
                                                      out, c->partials);
-        return;
+        return true;
       case 6:
         k_spgemm_win3<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart3, p.nwin3, X, out, c->partials);
-        return;
+        return true;
       case 1:
         k_spgemm_scalar<MM_ITER><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
                                                                 c->partials);
-        return;
+        return true;
       case 2:
         k_spgemm_tile<MM_ITER><<<(int)std::max<int64_t>(1, p.ntiles), TILE_T, p.tile_smem, s>>>(
             v, p.ent, p.hdr, X, X2, out, c->partials);
-        return;
+        return true;
       default:
         k_spgemm_pipe<<<p.pipe_grid, TILE_T, p.pipe_smem, s>>>(v, p.ent, p.hdr, p.ntiles, p.rec_cap, p.rows_cap,
                                                               X, out, c->partials);
-        return;
+        return true;
     }
+  }
+  if (mode == MM_R0E) {                      // fused r0 + E0: the tile kernel only
+    if (!p.use_tiles) return false;
+    k_spgemm_tile<MM_R0E><<<(int)std::max<int64_t>(1, p.ntiles), TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2,
+                                                                                         out, c->partials);
+    return true;
   }
   if (!p.use_tiles) {
     // setup / energy modes on win2's window kernel (EMIN_SETUP_WIN2M=1; measured
@@ -2235,7 +2243,7 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
     else
       k_spgemm_win2m<MM_ENERGY><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
                                                               c->partials);
-    return;
+    return true;
   }
   if (p.use_tiles) {
     const int g = (int)std::max<int64_t>(1, p.ntiles);
@@ -2243,13 +2251,14 @@ static inline void launch_scalar_masked(emin_ctx c, int mode, const double* X, c
       k_spgemm_tile<MM_R0><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
     else
       k_spgemm_tile<MM_ENERGY><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
-    return;
+    return true;
   }
   if (mode == MM_R0)
     k_spgemm_scalar<MM_R0><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
   else
     k_spgemm_scalar<MM_ENERGY><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
                                                               c->partials);
+  return true;
 }
 static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
                                       const double* what, unsigned long long* counters, cudaStream_t s) {

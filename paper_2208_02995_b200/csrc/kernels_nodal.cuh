@@ -493,10 +493,11 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
           const int32_t j = v.wcol[ro + t1];
           for (int64_t q = fb; q < fe; ++q) if (v.afccol[q] == j) { f1 = v.afcval[q]; break; }
         }
-        if (MODE == MM_ENERGY) {
+        if (MODE == MM_ENERGY || MODE == MM_R0E) {
           if (act0) part = fma(xval(ro + t0), g0[d] + 2.0 * f0, part);
           if (act1) part = fma(xval(ro + t1), g1[d] + 2.0 * f1, part);
-        } else {
+        }
+        if (MODE != MM_ENERGY) {
           g0[d] += f0;
           g1[d] += f1;
         }
@@ -527,7 +528,7 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
       }
       // Pi_B (twice for r0, see masked.cuh)
 #pragma unroll
-      for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
+      for (int pass = 0; pass < ((MODE == MM_R0 || MODE == MM_R0E) ? 2 : 1); ++pass) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           double dv[NV];
@@ -625,7 +626,7 @@ static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((p->nFn + 7) / 8, (int64_t)SM * 16));
 }
 
-static inline void launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const double* X, const double* X2,
+static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const double* X, const double* X2,
                                 double* out, cudaStream_t s) {
   const DevView v = c->view();
   const int g = nodal_grid(c, p);
@@ -636,7 +637,7 @@ static inline void launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
       NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
 #undef NV_CASE
     }
-    return;
+    return true;
   }
   const bool v2 = !(var && !strcmp(var, "s"));     // EMIN_NODAL=s: the staged v1 kernel
   if (mode == MM_ITER && var && !strcmp(var, "v2p")) {    // branch-free block loop (A/B)
@@ -645,7 +646,16 @@ static inline void launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
       NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
 #undef NV_CASE
     }
-    return;
+    return true;
+  }
+  if (mode == MM_R0E) {                       // fused r0 + E0: the v2 kernel only
+    if (!v2) return false;
+    switch (c->nv) {
+#define NV_CASE(N) case N: k_spgemm_nodal_v2<N, MM_R0E><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials); break;
+      NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+#undef NV_CASE
+    }
+    return true;
   }
 #define ND_LAUNCH(KER, N)                                                                                  \
   if (mode == MM_ITER)                                                                                    \
@@ -665,6 +675,7 @@ static inline void launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
   switch (c->nv) { NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8) }
 #undef NV_CASE
 #undef ND_LAUNCH
+  return true;
 }
 
 static inline void free_nodal_path(emin_ctx c, NodalPlan*& p) {

@@ -15,7 +15,8 @@
 enum MaskedMode : int {
   MM_ITER = 0,    // out = Pi (A_FF Y)|pattern ; partial += X . out
   MM_R0 = 1,      // out = -Pi (A P)|pattern  incl. the C-identity term (reading A1)
-  MM_ENERGY = 2   // partial += W . (A_FF W + 2 A_FC)|pattern           (Eq. trInc)
+  MM_ENERGY = 2,  // partial += W . (A_FF W + 2 A_FC)|pattern           (Eq. trInc)
+  MM_R0E = 3      // MM_R0 and MM_ENERGY of W = X in one pass (setup: r0 and E0 share A P0)
 };
 
 // X (and X2 when SUMX: X + X2, used for W = W0 + dW) is read on the owned
@@ -73,7 +74,7 @@ k_masked_generic(DevView v, const double* __restrict__ X, const double* __restri
         }
       }
     }
-    if (MODE == MM_ENERGY) {
+    if (MODE == MM_ENERGY || MODE == MM_R0E) {
 #pragma unroll
       for (int c = 0; c < MAXC; ++c) {
         const int t = lane + 32 * c;
@@ -82,18 +83,18 @@ k_masked_generic(DevView v, const double* __restrict__ X, const double* __restri
           part += w * (acc[c] + 2.0 * fc[c]);
         }
       }
-      continue;
+      if (MODE == MM_ENERGY) continue;
     }
     double g[MAXC];
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c) g[c] = (MODE == MM_R0) ? acc[c] + fc[c] : acc[c];
+    for (int c = 0; c < MAXC; ++c) g[c] = (MODE == MM_R0 || MODE == MM_R0E) ? acc[c] + fc[c] : acc[c];
     // Pi_B on row i: g <- g - Q_i (Q_i^T g)   (all dots first, then subtract).
     // r0 is projected twice (Pi^2 = Pi): when the start is already optimal
     // (configs 1, 2) Pi G is pure round-off, and the second pass puts that
     // round-off in ker(B^T) to its own precision, so that skipping the
     // post-Jacobi projection (reading A7) stays exact for it too.
 #pragma unroll
-    for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
+    for (int pass = 0; pass < ((MODE == MM_R0 || MODE == MM_R0E) ? 2 : 1); ++pass) {
       double dots[EMIN_NV_MAX];
 #pragma unroll
       for (int m = 0; m < EMIN_NV_MAX; ++m) {

@@ -435,3 +435,22 @@ def test_pattern_gpu_matches_oracle_and_generator(name, size):
     if prob.n < 400000:
         orp, ocol, _ = pattern(prob)
         assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+
+
+@pytest.mark.parametrize("name,size,env", [("3", 12, None), ("4", 3, None), ("2b", 10, None),
+                                          ("4", 3, ("EMIN_FORCE_GENERIC", "1"))])
+def test_fused_r0_energy_setup_equals_separate(name, size, env, monkeypatch):
+    """r0 and E0 from one MM_R0E pass equal the separate MM_R0 / MM_ENERGY
+    passes bitwise (same arithmetic per entry, same partial order)."""
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    if env:
+        monkeypatch.setenv(*env)
+    a = Emin.from_problem(prob)
+    monkeypatch.setenv("EMIN_NO_R0E", "1")
+    b = Emin.from_problem(prob)
+    assert a.report()["E0"] == b.report()["E0"]
+    ka, dEa = a.iterate(10)
+    kb, dEb = b.iterate(10)
+    assert ka == kb and np.array_equal(dEa, dEb)
