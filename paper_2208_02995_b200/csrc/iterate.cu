@@ -641,7 +641,7 @@ static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev, int e
   // kernels of ours per iteration: stage I, stage II, SpGEMM (+ the two
   // scalar kernels, + on several GPUs their rank-local sum kernels and the
   // halo pack)
-  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 3 : 0) + (c->sgs ? (int32_t)(2 * emin_sgs_levels(c)) : 0);
+  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 3 : 0) + (c->sgs ? (int32_t)(2 * emin_sgs_levels(c) - 1) : 0);
 }
 
 // One iteration captured as a CUDA graph (5 kernel nodes, cheap to

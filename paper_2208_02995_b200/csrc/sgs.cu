@@ -119,7 +119,11 @@ __global__ void k_sgs_scatter(int64_t nF, const int32_t* __restrict__ lev, int32
 // solve (!FWD), warp per row, lane per pattern position t (chunks of 32).
 //   FWD:  x = r [- alpha_pend yb, written back]; u = (x - sum_pred A u) / d
 //   !FWD: z = (d u - sum_succ A z) / d, in place over u
-template <bool FWD>
+// EDGE: the first forward level (rows without predecessors: lev 0 by
+// definition) or the last backward level (rows without successors: a
+// successor's level exceeds its predecessor's), so no coupling term exists
+// and the record loop is skipped (u = x / d, z = v / d)
+template <bool FWD, bool EDGE = false, bool TOP = false>
 __global__ void __launch_bounds__(256)
 k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restrict__ rows, int32_t nrows,
             double* __restrict__ r, const double* __restrict__ yb, double* u) {
@@ -152,7 +156,7 @@ k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restric
       }
       acc[c] = x;
     }
-    for (int64_t q = v.affptr[i]; q < v.affptr[i + 1]; ++q) {
+    for (int64_t q = v.affptr[i]; !EDGE && q < v.affptr[i + 1]; ++q) {
       const int32_t k = v.affcol[q];
       if (k == i) continue;
       if (FWD != sgs_before(key, k, i)) continue;   // FWD: predecessors, else successors
@@ -170,7 +174,11 @@ k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restric
 #pragma unroll
     for (int c = 0; c < SGS_MAXC; ++c) {
       const int t = lane + 32 * c;
-      if (t < nj) u[b + t] = acc[c] / di;
+      if (t < nj) {
+        double ue = acc[c] / di;
+        if (TOP) ue = __ddiv_rn(__dmul_rn(di, ue), di);   // no successors: z = (D u) / d
+        u[b + t] = ue;
+      }
     }
   }
 }
@@ -196,7 +204,11 @@ __global__ void k_sgs_dir(DevView v, const int64_t* __restrict__ key, uint8_t* _
 // lvl_rows[j0 .. j0 + nrows) of one level, head bit p set where a row starts.
 // Records are the scalar path's {a, wptr[k], pm} (pm nibble t = position of
 // J_i[t] in J_k), filtered by dir.  Same order of operations as k_sgs_sweep.
-template <bool FWD>
+// TOP (forward only): the level is the last one, its rows have no
+// successors, so the backward solve of those rows, z = (D u) / d, is done
+// right here (same operations as the backward kernel) and the backward sweep
+// starts one level lower.
+template <bool FWD, bool EDGE = false, bool TOP = false>
 __global__ void __launch_bounds__(256)
 k_sgs_sweep_win(DevView v, const int4* __restrict__ A4, const uint8_t* __restrict__ dir,
                 const int4* __restrict__ win, int32_t nwin, const int32_t* __restrict__ rows,
@@ -235,13 +247,15 @@ k_sgs_sweep_win(DevView v, const int4* __restrict__ A4, const uint8_t* __restric
     const int qb = (int)v.affptr[i], qe = (int)v.affptr[i + 1];
     const unsigned sh4 = 4u * (unsigned)pos;
 #pragma unroll 4
-    for (int q = qb + 1; q < qe; ++q) {         // record qb is the diagonal
+    for (int q = qb + 1; !EDGE && q < qe; ++q) {   // record qb is the diagonal
       if (__ldg(dir + q) != want) continue;
       const int4 en = __ldg(A4 + q);
       const unsigned sidx = ((unsigned)en.w >> sh4) & 0xFu;
       if (sidx != 0xFu) acc -= __hiloint2double(en.y, en.x) * u[en.z + (int)sidx];
     }
-    u[e] = acc / di;
+    double ue = acc / di;
+    if (TOP) ue = __ddiv_rn(__dmul_rn(di, ue), di);   // z = (v - 0) / d, v = D u
+    u[e] = ue;
   }
 }
 
@@ -298,7 +312,7 @@ __global__ void k_sgs_node_levels(DevView v, int64_t nFn, const int64_t* __restr
 // (the own-node terms come last, after the other blocks in A's column
 // order; the oracle adds them at their column position -- a rounding-order
 // difference only).
-template <bool FWD>
+template <bool FWD, bool EDGE = false, bool TOP = false>
 __global__ void __launch_bounds__(256)
 k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
@@ -354,7 +368,7 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
           for (int e = 0; e < 3; ++e) own[d * 3 + e] = __ldg(v.affval + ab + d * rs + 3 * b + e);
         continue;
       }
-      if (db != want) continue;
+      if (EDGE || db != want) continue;          // EDGE: only the own node's 3x3 block couples
       double a[9];
 #pragma unroll
       for (int d = 0; d < 3; ++d)
@@ -394,6 +408,21 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
           if (e < d) { a0 -= own[d * 3 + e] * o0[e]; a1 -= own[d * 3 + e] * o1[e]; }
         o0[d] = a0 / own[d * 3 + d];
         o1[d] = a1 / own[d * 3 + d];
+      }
+      if (TOP) {                                   // no successor nodes: the node's backward solve
+        double u0[3], u1[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) { u0[d] = o0[d]; u1[d] = o1[d]; }
+#pragma unroll
+        for (int d = 2; d >= 0; --d) {
+          const double dd = own[d * 3 + d];
+          double a0 = __dmul_rn(dd, u0[d]), a1 = __dmul_rn(dd, u1[d]);
+#pragma unroll
+          for (int e = 0; e < 3; ++e)
+            if (e > d) { a0 -= own[d * 3 + e] * o0[e]; a1 -= own[d * 3 + e] * o1[e]; }
+          o0[d] = a0 / dd;
+          o1[d] = a1 / dd;
+        }
       }
     } else {
 #pragma unroll
@@ -698,10 +727,15 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   if (p->nodal) {
     for (int64_t L = 0; L < p->nlev; ++L) {
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
-      k_sgs_sweep_nodal<true><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
-                                                         p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
+      const int32_t* rows = p->lvl_rows + p->lvl_ptr[L];
+      const bool first = L == 0, top = L == p->nlev - 1;
+#define NDF(E, T) k_sgs_sweep_nodal<true, E, T><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, \
+                                                                           p->bdir, rows, (int32_t)n, c->r, c->yb, p->u)
+      if (first && top) NDF(true, true); else if (first) NDF(true, false); else if (top) NDF(false, true);
+      else NDF(false, false);
+#undef NDF
     }
-    for (int64_t L = p->nlev - 1; L >= 0; --L) {
+    for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
       k_sgs_sweep_nodal<false><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
                                                           p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
@@ -717,10 +751,14 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   if (p->rec) {
     for (int64_t L = 0; L < p->nlev; ++L) {
       const int64_t n = p->win_ptr[L + 1] - p->win_ptr[L];
-      k_sgs_sweep_win<true><<<grid_for(n), 256, 0, s>>>(v, p->rec, p->dir, p->win + p->win_ptr[L], (int32_t)n,
-                                                       p->lvl_rows, c->r, c->yb, p->u);
+      const bool first = L == 0, top = L == p->nlev - 1;
+#define WF(E, T) k_sgs_sweep_win<true, E, T><<<grid_for(n), 256, 0, s>>>(v, p->rec, p->dir, p->win + p->win_ptr[L], \
+                                                                        (int32_t)n, p->lvl_rows, c->r, c->yb, p->u)
+      if (first && top) WF(true, true); else if (first) WF(true, false); else if (top) WF(false, true);
+      else WF(false, false);
+#undef WF
     }
-    for (int64_t L = p->nlev - 1; L >= 0; --L) {
+    for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->win_ptr[L + 1] - p->win_ptr[L];
       k_sgs_sweep_win<false><<<grid_for(n), 256, 0, s>>>(v, p->rec, p->dir, p->win + p->win_ptr[L], (int32_t)n,
                                                         p->lvl_rows, c->r, c->yb, p->u);
@@ -728,10 +766,14 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   } else {
     for (int64_t L = 0; L < p->nlev; ++L) {
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
-      k_sgs_sweep<true><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r,
-                                                   c->yb, p->u);
+      const int32_t* rows = p->lvl_rows + p->lvl_ptr[L];
+      const bool first = L == 0, top = L == p->nlev - 1;
+#define GF(E, T) k_sgs_sweep<true, E, T><<<grid_for(n), 256, 0, s>>>(v, p->key, rows, (int32_t)n, c->r, c->yb, p->u)
+      if (first && top) GF(true, true); else if (first) GF(true, false); else if (top) GF(false, true);
+      else GF(false, false);
+#undef GF
     }
-    for (int64_t L = p->nlev - 1; L >= 0; --L) {
+    for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
       k_sgs_sweep<false><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r,
                                                     c->yb, p->u);
