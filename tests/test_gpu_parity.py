@@ -59,7 +59,7 @@ def _compare(g, o, k, prob):
 
 
 SMALL = [("1", None, 20), ("1b", None, 20), ("1d", 33, 40), ("2b", 10, 30), ("2", 12, 30),
-         ("3", 12, 40), ("3", 17, 40), ("4", 3, 30), ("4", 5, 30), ("5", 8, 40)]
+         ("3", 12, 40), ("3", 17, 40), ("4", 3, 30), ("4", 5, 30), ("5", 8, 40), ("1v3", 16, 20), ("1v3", 23, 20)]
 
 
 @pytest.mark.parametrize("name,size,k", SMALL)
@@ -280,7 +280,7 @@ def _constraint_sampled(prob, P, nsample, seed=0):
 # projected SGS preconditioner M_2
 # --------------------------------------------------------------------------
 
-SGS_CASES = [("1b", None, 20, "natural"), ("1b", None, 20, "color"), ("2b", 10, 30, "color"),
+SGS_CASES = [("1b", None, 20, "natural"), ("1b", None, 20, "color"), ("2b", 10, 30, "color"), ("1v3", 16, 20, "color"),
              ("3", 12, 40, "natural"), ("3", 12, 40, "color"), ("3", 17, 40, "color"),
              ("4", 3, 30, "natural"), ("4", 4, 30, "color"), ("5", 8, 40, "color")]
 
@@ -389,7 +389,7 @@ def test_sgs_nodal_sweep_equals_generic_sweep(name, size, kind, monkeypatch):
 # --------------------------------------------------------------------------
 
 @pytest.mark.parametrize("name,size,k", [("1b", None, 20), ("2b", 10, 30), ("3", 12, 40), ("4", 3, 30),
-                                         ("4", 4, 30), ("5", 8, 40)])
+                                         ("4", 4, 30), ("5", 8, 40), ("1v3", 16, 20)])
 def test_maxvol_start_parity(name, size, k):
     from oracle import Oracle
     from paper_2208_02995_b200 import Emin
@@ -420,7 +420,7 @@ def test_maxvol_start_with_sgs_full_config4():
 # --------------------------------------------------------------------------
 
 @pytest.mark.parametrize("name,size", [("1b", None), ("2", 12), ("2b", 10), ("3", 12), ("3", 17), ("4", 3),
-                                       ("4", 6), ("5", 8), ("2", None), ("3", None), ("4", None)])
+                                       ("4", 6), ("5", 8), ("2", None), ("3", None), ("4", None), ("1v3", 16)])
 def test_pattern_gpu_matches_oracle_and_generator(name, size):
     """Index structure: bit-exact against the oracle's BFS and against the
     input generator (independent box arithmetic), full-size configs 2-4

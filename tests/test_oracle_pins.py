@@ -592,7 +592,7 @@ def test_maxvol_start_converges_to_kkt(name, size):
 # --------------------------------------------------------------------------
 
 @pytest.mark.parametrize("name,size", [("1b", None), ("2", 10), ("2b", 12), ("3", 12), ("3", 17),
-                                       ("4", 3), ("4", 6), ("5", 8)])
+                                       ("4", 3), ("4", 6), ("5", 8), ("1v3", 16), ("1v3", 11)])
 def test_pattern_from_graph_matches_generator(name, size):
     """The oracle's BFS over the graph of A reproduces, bit for bit, the input
     generator's pattern -- built independently from grid-box arithmetic
@@ -617,3 +617,18 @@ def test_gram_full_rank_matches_numpy():
             G = (U * ev) @ U.T
             ref = np.linalg.eigvalsh(G)
             assert gram_full_rank(G) == bool(ref[0] > 1e-10 * max(ref[-1], 0.0))
+
+
+@pytest.mark.parametrize("precond,start", [("jacobi", "given"), ("sgs", "given"), ("jacobi", "maxvol")])
+def test_linear_modes_nv3_converges_to_kkt(precond, start):
+    """A scalar operator with the 3-mode near kernel {1, x, y} (nv = 3, point
+    rows, pattern grown until rank 3): the converged CG equals the dense KKT
+    solution for both preconditioners and both starts, and the
+    constraint holds to 1e-12."""
+    prob = make_config("1v3", size=8)
+    o = Oracle(prob, precond=precond, start=start, project_z=True, stagnation_rel=1e-28)
+    o.iterate(500)
+    w = D.kkt_solution(prob)
+    assert np.abs(o.get_W() - w).max() <= 1e-8 * np.abs(w).max()
+    Cm, b = D.constraint_matrix(prob)
+    assert np.abs(Cm @ o.get_W() - b).max() <= 1e-12 * max(1.0, np.abs(b).max())

@@ -429,7 +429,7 @@ def _segment_positions(rowptr, rows, lens):
 # Config assembly
 # ---------------------------------------------------------------------------
 
-def _scalar_problem(name, csr, dims, iters, start, seed_pert=1, meta=None):
+def _scalar_problem(name, csr, dims, iters, start, seed_pert=1, meta=None, linear_modes=False):
     rowptr, col, val = csr
     nx, ny, nz = dims
     n = nx * ny * nz
@@ -440,12 +440,17 @@ def _scalar_problem(name, csr, dims, iters, start, seed_pert=1, meta=None):
     cid = np.full(n, -1, dtype=np.int64)
     cid[is_c] = np.arange(int(is_c.sum()))
     nc = int(is_c.sum())
-    nv = 1
-    B = np.ones((n, 1))
-    Bc = np.ones((nc, 1))
+    if linear_modes:
+        # near kernel {1, x, y} (centred grid coordinates): nv = 3 on a scalar
+        # operator -- exercises the general (nv > 1, point) kernel path
+        B = np.stack([np.ones(n), x - (nx - 1) / 2.0, y - (ny - 1) / 2.0], axis=1)
+    else:
+        B = np.ones((n, 1))
+    nv = B.shape[1]
+    Bc = B[is_c].copy()
     fine = np.flatnonzero(~is_c)
     wp, wc, used = _grow_pattern((nx, ny, nz), 0, is_c, cid, fine, "manhattan",
-                                 Bc.reshape(nc, 1, 1), nv, 1)
+                                 Bc.reshape(nc, 1, nv), nv, 1)
     P_rowptr, P_col = _merge_pattern(n, is_c, cid, fine, wp, wc, 1)
     P_val = _start_values(start, n, is_c, fine, P_rowptr, seed_pert)
     m = dict(dims=dims, growth=used, **(meta or {}))
@@ -590,6 +595,13 @@ def make_config(name: str, size: Optional[int] = None, seed: int = 0,
     (scalar) / elements (elasticity) per side."""
     if name == "1d":
         return poisson1d_problem(size or 33, start=start or "leastnorm")
+    if name == "1v3":
+        # test workload (not a BASELINE config): config 1's operator with the
+        # linear near kernel {1, x, y}, perturbed start
+        n = size or 16
+        csr, dims = poisson2d(n)
+        return _scalar_problem(f"1v3@{n}", csr, dims, 20, start or "perturbed", meta=dict(config="1v3"),
+                               linear_modes=True)
     if name in ("1", "1b"):
         n = size or 32
         csr, dims = poisson2d(n)
