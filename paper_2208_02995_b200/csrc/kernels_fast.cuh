@@ -1063,19 +1063,11 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
                                                               c->partials);
     return true;
   }
-  if (p.use_tiles) {
-    const int g = (int)std::max<int64_t>(1, p.ntiles);
-    if (mode == MM_R0)
-      k_spgemm_tile<MM_R0><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
-    else
-      k_spgemm_tile<MM_ENERGY><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
-    return true;
-  }
+  const int g = (int)std::max<int64_t>(1, p.ntiles);
   if (mode == MM_R0)
-    k_spgemm_scalar<MM_R0><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
+    k_spgemm_tile<MM_R0><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
   else
-    k_spgemm_scalar<MM_ENERGY><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
-                                                              c->partials);
+    k_spgemm_tile<MM_ENERGY><<<g, TILE_T, p.tile_smem, s>>>(v, p.ent, p.hdr, X, X2, out, c->partials);
   return true;
 }
 static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
