@@ -454,3 +454,35 @@ def test_fused_r0_energy_setup_equals_separate(name, size, env, monkeypatch):
     ka, dEa = a.iterate(10)
     kb, dEb = b.iterate(10)
     assert ka == kb and np.array_equal(dEa, dEb)
+
+
+def test_option_validation():
+    """precond / start outside their enums, and SGS with an NCCL
+    communicator, are EMIN_ERR_ARG (include/emin.h); emin_pattern rejects a
+    capacity below nnz and keeps P_rowptr."""
+    import ctypes as C
+    from paper_2208_02995_b200 import Emin, EminError
+    from paper_2208_02995_b200 import emin as E
+    from workloads.problems import make_config
+    prob = make_config("1b", size=8)
+    for kw in (dict(precond=2), dict(start=5)):
+        with pytest.raises(EminError) as e:
+            Emin.from_problem(prob, **kw)
+        assert e.value.code == 1
+    comm = E.emin_nccl_comm_init(1, E.emin_nccl_unique_id(), 0)
+    try:
+        with pytest.raises(EminError) as e:
+            Emin.from_problem(prob, precond="sgs", nccl_comm=comm)
+        assert e.value.code == 1
+    finally:
+        E.emin_nccl_comm_destroy(comm)
+    lib = E.load_library()
+    rp = np.zeros(prob.n + 1, np.int64)
+    col = np.zeros(4, np.int32)
+    nnz = C.c_int64(0)
+    arr = [np.ascontiguousarray(prob.A_rowptr, np.int64), np.ascontiguousarray(prob.A_col, np.int32),
+           np.ascontiguousarray(prob.is_coarse, np.uint8), np.ascontiguousarray(prob.Bc, np.float64)]
+    st = lib.emin_pattern(prob.n, arr[0].ctypes.data, arr[1].ctypes.data, arr[2].ctypes.data, 1, 1,
+                          arr[3].ctypes.data, prob.nc, 2, 4, rp.ctypes.data, col.ctypes.data, 4, C.byref(nnz), 0,
+                          None)
+    assert st == 1 and nnz.value == prob.P_rowptr[-1] and np.array_equal(rp, prob.P_rowptr)
