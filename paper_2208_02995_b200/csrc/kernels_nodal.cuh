@@ -379,7 +379,7 @@ __device__ __forceinline__ void nd2_reduce_scatter(double (&v)[N], int lane, int
   *own = lo;
 }
 
-template <int NV, int MODE, bool PRED = false>
+template <int NV, int MODE, bool PRED = false, bool CS = false>
 __global__ void __launch_bounds__(ND_WARPS * 32, 4)
 k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
@@ -412,10 +412,14 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
     const int rs = 3 * nb;
     for (int k = lane; k < 9 * nb; k += 32) {
       const int d = k / rs, rem = k - d * rs, b = rem / 3, e = rem - 3 * b;
-      s_a[wib][b * ND2_AST + d * 3 + e] = __ldg(v.affval + ab + k);
+      s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(v.affval + ab + k) : __ldg(v.affval + ab + k);
     }
-    for (int k = lane; k < nb; k += 32) s_b[wib][k] = blk[bb + k];
-    for (int k = lane; k < nb * nJ; k += 32) s_pm[wib][k] = pm8[po + k];
+    for (int k = lane; k < nb; k += 32) {
+      if (CS) { const int2 t = __ldcs(reinterpret_cast<const int2*>(blk + bb + k)); s_b[wib][k] = NodalBlk{t.x, t.y}; }
+      else s_b[wib][k] = blk[bb + k];
+    }
+    for (int k = lane; k < nb * nJ; k += 32)
+      s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + po + k)) : pm8[po + k];
     const bool act0 = t0 < n3, act1 = t1 < n3;
     const bool any1 = n3 > 32;                          // warp-uniform
     __syncwarp();
@@ -512,12 +516,12 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
         if (act0) {
           const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t0) * NV);
 #pragma unroll
-          for (int m = 0; m < NV / 2; ++m) { const double2 t = __ldg(qp + m); q0[2 * m] = t.x; q0[2 * m + 1] = t.y; }
+          for (int m = 0; m < NV / 2; ++m) { const double2 t = CS ? __ldcs(qp + m) : __ldg(qp + m); q0[2 * m] = t.x; q0[2 * m + 1] = t.y; }
         }
         if (act1) {
           const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t1) * NV);
 #pragma unroll
-          for (int m = 0; m < NV / 2; ++m) { const double2 t = __ldg(qp + m); q1[2 * m] = t.x; q1[2 * m + 1] = t.y; }
+          for (int m = 0; m < NV / 2; ++m) { const double2 t = CS ? __ldcs(qp + m) : __ldg(qp + m); q1[2 * m] = t.x; q1[2 * m + 1] = t.y; }
         }
       } else {
 #pragma unroll
@@ -557,11 +561,11 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
       for (int d = 0; d < 3; ++d) {
         const int ro = wb + d * n3;
         if (act0) {
-          if (MODE == MM_ITER) { out[ro + t0] = g0[d]; part = fma(X[ro + t0], g0[d], part); }
+          if (MODE == MM_ITER) { if (CS) __stcs(out + ro + t0, g0[d]); else out[ro + t0] = g0[d]; part = fma(X[ro + t0], g0[d], part); }
           else out[ro + t0] = -g0[d];
         }
         if (act1) {
-          if (MODE == MM_ITER) { out[ro + t1] = g1[d]; part = fma(X[ro + t1], g1[d], part); }
+          if (MODE == MM_ITER) { if (CS) __stcs(out + ro + t1, g1[d]); else out[ro + t1] = g1[d]; part = fma(X[ro + t1], g1[d], part); }
           else out[ro + t1] = -g1[d];
         }
       }
@@ -640,6 +644,18 @@ static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
     return true;
   }
   const bool v2 = !(var && !strcmp(var, "s"));     // EMIN_NODAL=s: the staged v1 kernel
+  // default per-iteration kernel: v2 with evict-first hints on the streamed
+  // data (A chunk, block records, position bytes, Q, y^), so the L2 keeps the
+  // gathered y rows: config 5 21.89 -> 20.91 ms, config 4 474 -> 478 us
+  // (EMIN_NODAL=v2: without the hints)
+  if (mode == MM_ITER && (!var || !strcmp(var, "v2cs"))) {
+    switch (c->nv) {
+#define NV_CASE(N) case N: k_spgemm_nodal_v2<N, MM_ITER, false, true><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials); break;
+      NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+#undef NV_CASE
+    }
+    return true;
+  }
   if (mode == MM_ITER && var && !strcmp(var, "v2p")) {    // branch-free block loop (A/B)
     switch (c->nv) {
 #define NV_CASE(N) case N: k_spgemm_nodal_v2<N, MM_ITER, true><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials); break;
