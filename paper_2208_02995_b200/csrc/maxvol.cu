@@ -25,31 +25,68 @@
 namespace {
 
 
-// Gauss-Jordan inverse with partial pivoting of the nv x nv row-major B
-// (one thread); false if singular
-__device__ bool mv_gj_inverse(int nv, const double* __restrict__ Bm, double* __restrict__ inv) {
-  double a[EMIN_NV_MAX][2 * EMIN_NV_MAX];
-  for (int r = 0; r < nv; ++r)
-    for (int c = 0; c < 2 * nv; ++c) a[r][c] = c < nv ? Bm[r * nv + c] : (c - nv == r ? 1.0 : 0.0);
-  for (int c = 0; c < nv; ++c) {
+// Gauss-Jordan inverse with partial pivoting of the N x N row-major B (one
+// thread, fully unrolled: registers); false if singular
+template <int N>
+__device__ bool mv_gj_inverse_t(const double* __restrict__ Bm, double* __restrict__ inv) {
+  double a[N][2 * N];
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < 2 * N; ++c) a[r][c] = c < N ? Bm[r * N + c] : (c - N == r ? 1.0 : 0.0);
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
     int p = c;
-    for (int r = c + 1; r < nv; ++r)
+#pragma unroll
+    for (int r = c + 1; r < N; ++r)
       if (fabs(a[r][c]) > fabs(a[p][c])) p = r;
-    if (a[p][c] == 0.0) return false;
-    if (p != c)
-      for (int k = 0; k < 2 * nv; ++k) { const double t = a[c][k]; a[c][k] = a[p][k]; a[p][k] = t; }
+    // row swap c <-> p by selects (p is data dependent)
+    double pivrow[2 * N];
+#pragma unroll
+    for (int k = 0; k < 2 * N; ++k) {
+      double v = a[c][k];
+#pragma unroll
+      for (int r = c + 1; r < N; ++r) if (r == p) v = a[r][k];
+      pivrow[k] = v;
+    }
+#pragma unroll
+    for (int r = c + 1; r < N; ++r)
+      if (r == p)
+#pragma unroll
+        for (int k = 0; k < 2 * N; ++k) a[r][k] = a[c][k];
+#pragma unroll
+    for (int k = 0; k < 2 * N; ++k) a[c][k] = pivrow[k];
+    if (a[c][c] == 0.0) return false;
     const double piv = a[c][c];
-    for (int k = 0; k < 2 * nv; ++k) a[c][k] = __ddiv_rn(a[c][k], piv);
-    for (int r = 0; r < nv; ++r) {
+#pragma unroll
+    for (int k = 0; k < 2 * N; ++k) a[c][k] = __ddiv_rn(a[c][k], piv);
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
       if (r == c) continue;
       const double f = a[r][c];
       if (f != 0.0)
-        for (int k = 0; k < 2 * nv; ++k) a[r][k] = __dsub_rn(a[r][k], __dmul_rn(f, a[c][k]));
+#pragma unroll
+        for (int k = 0; k < 2 * N; ++k) a[r][k] = __dsub_rn(a[r][k], __dmul_rn(f, a[c][k]));
     }
   }
-  for (int r = 0; r < nv; ++r)
-    for (int c = 0; c < nv; ++c) inv[r * nv + c] = a[r][nv + c];
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) inv[r * N + c] = a[r][N + c];
   return true;
+}
+
+__device__ bool mv_gj_inverse(int nv, const double* __restrict__ Bm, double* __restrict__ inv) {
+  switch (nv) {
+    case 1: return mv_gj_inverse_t<1>(Bm, inv);
+    case 2: return mv_gj_inverse_t<2>(Bm, inv);
+    case 3: return mv_gj_inverse_t<3>(Bm, inv);
+    case 4: return mv_gj_inverse_t<4>(Bm, inv);
+    case 5: return mv_gj_inverse_t<5>(Bm, inv);
+    case 6: return mv_gj_inverse_t<6>(Bm, inv);
+    case 7: return mv_gj_inverse_t<7>(Bm, inv);
+    default: return mv_gj_inverse_t<8>(Bm, inv);
+  }
 }
 
 __device__ __forceinline__ double mv_warp_max(double x) {
@@ -65,7 +102,7 @@ __device__ __forceinline__ int mv_warp_min(int x) {
 
 template <int MAXC>
 __global__ void __launch_bounds__(128)
-k_maxvol_start(DevView v, const double* __restrict__ Bc, const double* __restrict__ B,
+k_maxvol_start(DevView v, int rstep, const double* __restrict__ Bc, const double* __restrict__ B,
                const int64_t* __restrict__ frow, double* __restrict__ what, unsigned long long* fails) {
   __shared__ double s_B[4][EMIN_NV_MAX * EMIN_NV_MAX];
   __shared__ double s_inv[4][EMIN_NV_MAX * EMIN_NV_MAX];
@@ -75,7 +112,9 @@ k_maxvol_start(DevView v, const double* __restrict__ Bc, const double* __restric
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int nv = v.nv;
-  for (int64_t i = gw; i < v.nF; i += nw) {
+  // rows i, i + 1, .., i + rstep - 1 share J (nodal path: the 3 dof rows of
+  // an F node), hence M and the selection; each solves with its own v
+  for (int64_t i = gw * rstep; i < v.nF; i += nw * rstep) {
     const int64_t b = v.wptr[i];
     const int m = (int)(v.wptr[i + 1] - b);
     double M[MAXC][EMIN_NV_MAX], W[MAXC][EMIN_NV_MAX];
@@ -203,22 +242,25 @@ k_maxvol_start(DevView v, const double* __restrict__ Bc, const double* __restric
     }
     // ---- w(S) = B^{-T} v, zero elsewhere
     if (ok && !load_inverse()) ok = false;
-    const double* vrow = B + frow[i] * nv;
+    for (int d = 0; d < rstep; ++d) {
+      const double* vrow = B + frow[i + d] * nv;
+      const int64_t bd = v.wptr[i + d];
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c) {
-      const int t = lane + 32 * c;
-      if (t >= m) continue;
-      double w = 0.0;
-      if (ok)
-        for (int a = 0; a < nv; ++a)
-          if (S[a] == t) {
-            double sum = 0.0;
-            for (int bb = 0; bb < nv; ++bb) sum = __dadd_rn(sum, __dmul_rn(s_inv[wib][bb * nv + a], vrow[bb]));
-            w = sum;
-          }
-      what[b + t] = w;
+      for (int c = 0; c < MAXC; ++c) {
+        const int t = lane + 32 * c;
+        if (t >= m) continue;
+        double w = 0.0;
+        if (ok)
+          for (int a = 0; a < nv; ++a)
+            if (S[a] == t) {
+              double sum = 0.0;
+              for (int bb = 0; bb < nv; ++bb) sum = __dadd_rn(sum, __dmul_rn(s_inv[wib][bb * nv + a], vrow[bb]));
+              w = sum;
+            }
+        what[bd + t] = w;
+      }
     }
-    if (!ok && lane == 0) atomicAdd(fails, 1ull);
+    if (!ok && lane == 0) atomicAdd(fails, (unsigned long long)rstep);
     __syncwarp();
   }
 }
@@ -229,10 +271,12 @@ k_maxvol_start(DevView v, const double* __restrict__ Bc, const double* __restric
 void emin_maxvol_start(emin_ctx c, const double* Bc, const double* B, const int64_t* frow, double* what,
                        unsigned long long* fails, cudaStream_t s) {
   const int SM = emin_num_sms();
-  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF + 3) / 4, (int64_t)SM * 16));
+  const int rstep = c->kernel_path == 2 ? 3 : 1;   // nodal path: one selection per F node
+  const int64_t units = c->nF / rstep;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((units + 3) / 4, (int64_t)SM * 16));
   const DevView v = c->view();
-  if (c->max_row <= 32) k_maxvol_start<1><<<g, 128, 0, s>>>(v, Bc, B, frow, what, fails);
-  else if (c->max_row <= 64) k_maxvol_start<2><<<g, 128, 0, s>>>(v, Bc, B, frow, what, fails);
-  else k_maxvol_start<4><<<g, 128, 0, s>>>(v, Bc, B, frow, what, fails);
+  if (c->max_row <= 32) k_maxvol_start<1><<<g, 128, 0, s>>>(v, rstep, Bc, B, frow, what, fails);
+  else if (c->max_row <= 64) k_maxvol_start<2><<<g, 128, 0, s>>>(v, rstep, Bc, B, frow, what, fails);
+  else k_maxvol_start<4><<<g, 128, 0, s>>>(v, rstep, Bc, B, frow, what, fails);
   c->launches += 1;
 }
