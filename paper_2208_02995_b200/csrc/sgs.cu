@@ -318,11 +318,20 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
                   const uint8_t* __restrict__ bdir, const int32_t* __restrict__ nodes, int32_t nnodes,
                   double* __restrict__ r, const double* __restrict__ yb, double* u) {
+  // the node's A chunk (block-major, 10-double stride), block records,
+  // position bytes and block directions are staged per warp in shared
+  // memory with coalesced loads, as in the nodal SpGEMM (k_spgemm_nodal_v2)
+  constexpr int MAXB = 27, MAXJ = 32, AST = 10;   // the nodal plan's limits (k_nodal_check)
+  __shared__ __align__(16) double s_a[8][MAXB * AST];
+  __shared__ int2 s_b[8][MAXB];
+  __shared__ uint8_t s_pm[8][MAXB * MAXJ];
+  __shared__ uint8_t s_dir[8][MAXB];
   const DevState* st = v.st;
   if (st->stopped) return;
   const int pend = FWD ? st->pend : 0;
   const double ap = st->alpha_pend;
   const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int t0 = lane, t1 = lane + 32;
@@ -335,11 +344,19 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
     const int n3 = (int)(v.wptr[r3 + 1] - wb);
     const int nJ = n3 / 3;
     const bool act0 = t0 < n3, act1 = t1 < n3;
+    const bool any1 = n3 > 32;                         // warp-uniform
     const int64_t ab = v.affptr[r3];
     const int64_t bb = bptr[n];
     const int nb = (int)(bptr[n + 1] - bb);
-    const int64_t rs = 3 * (int64_t)nb;
+    const int rs = 3 * nb;
     const uint8_t* pm = pm8 + pmoff[n];
+    __syncwarp();
+    for (int k = lane; k < 9 * nb; k += 32) {
+      const int d = k / rs, rem = k - d * rs, bk = rem / 3, e = rem - 3 * bk;
+      s_a[wib][bk * AST + d * 3 + e] = __ldg(v.affval + ab + k);
+    }
+    for (int k = lane; k < nb; k += 32) { s_b[wib][k] = __ldg(blk + bb + k); s_dir[wib][k] = bdir[bb + k]; }
+    for (int k = lane; k < nb * nJ; k += 32) s_pm[wib][k] = pm[k];
     double acc0[3], acc1[3];
     double own[9];
 #pragma unroll
@@ -357,26 +374,22 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
       acc0[d] = x0;
       acc1[d] = x1;
     }
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < 9; ++q) own[q] = 0.0;
     for (int b = 0; b < nb; ++b) {
-      const uint8_t db = bdir[bb + b];                    // warp-uniform
+      const uint8_t db = s_dir[wib][b];                  // warp-uniform
+      if (db != 0 && (EDGE || db != want)) continue;     // EDGE: only the own node's block couples
+      const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][b * AST]);
+      const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+      const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
       if (db == 0) {
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int e = 0; e < 3; ++e) own[d * 3 + e] = __ldg(v.affval + ab + d * rs + 3 * b + e);
+        for (int q = 0; q < 9; ++q) own[q] = a[q];
         continue;
       }
-      if (EDGE || db != want) continue;          // EDGE: only the own node's 3x3 block couples
-      double a[9];
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-#pragma unroll
-        for (int e = 0; e < 3; ++e) a[d * 3 + e] = __ldg(v.affval + ab + d * rs + 3 * b + e);
-      const int2 k = __ldg(blk + bb + b);
-      const int p0 = act0 ? pm[b * nJ + s0] : 0xFF;
-      const int p1 = act1 ? pm[b * nJ + s1] : 0xFF;
+      const int2 k = s_b[wib][b];
+      const int p0 = act0 ? s_pm[wib][b * nJ + s0] : 0xFF;
       if (p0 != 0xFF) {
         const int64_t i0 = (int64_t)k.x + 3 * p0 + b0;
         const double y0 = u[i0], y1 = u[i0 + k.y], y2 = u[i0 + 2 * k.y];
@@ -387,14 +400,17 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
           acc0[d] -= a[d * 3 + 2] * y2;
         }
       }
-      if (p1 != 0xFF) {
-        const int64_t i1 = (int64_t)k.x + 3 * p1 + b1;
-        const double y0 = u[i1], y1 = u[i1 + k.y], y2 = u[i1 + 2 * k.y];
+      if (any1) {
+        const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
+        if (p1 != 0xFF) {
+          const int64_t i1 = (int64_t)k.x + 3 * p1 + b1;
+          const double y0 = u[i1], y1 = u[i1 + k.y], y2 = u[i1 + 2 * k.y];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          acc1[d] -= a[d * 3 + 0] * y0;
-          acc1[d] -= a[d * 3 + 1] * y1;
-          acc1[d] -= a[d * 3 + 2] * y2;
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] -= a[d * 3 + 0] * y0;
+            acc1[d] -= a[d * 3 + 1] * y1;
+            acc1[d] -= a[d * 3 + 2] * y2;
+          }
         }
       }
     }
