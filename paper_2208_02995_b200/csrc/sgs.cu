@@ -313,7 +313,7 @@ __global__ void k_sgs_node_levels(DevView v, int64_t nFn, const int64_t* __restr
 // order; the oracle adds them at their column position -- a rounding-order
 // difference only).
 template <bool FWD, bool EDGE = false, bool TOP = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
                   const uint8_t* __restrict__ bdir, const int32_t* __restrict__ nodes, int32_t nnodes,
@@ -358,7 +358,6 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
     for (int k = lane; k < nb; k += 32) { s_b[wib][k] = __ldg(blk + bb + k); s_dir[wib][k] = bdir[bb + k]; }
     for (int k = lane; k < nb * nJ; k += 32) s_pm[wib][k] = pm[k];
     double acc0[3], acc1[3];
-    double own[9];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const int64_t ro = wb + (int64_t)d * n3;
@@ -375,41 +374,94 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
       acc1[d] = x1;
     }
     __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 9; ++q) own[q] = 0.0;
-    for (int b = 0; b < nb; ++b) {
-      const uint8_t db = s_dir[wib][b];                  // warp-uniform
-      if (db != 0 && (EDGE || db != want)) continue;     // EDGE: only the own node's block couples
-      const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][b * AST]);
+    // the node's own block, and the coupled blocks (predecessor nodes in
+    // the forward sweep, successors in the backward one) as a bit mask in
+    // ascending block order (nb <= 27 < 32 lanes)
+    const uint8_t dl = lane < nb ? s_dir[wib][lane] : 3;
+    const unsigned ownm = __ballot_sync(0xffffffffu, dl == 0);
+    unsigned cm = EDGE ? 0u : __ballot_sync(0xffffffffu, dl == want);
+    double own[9];
+    {
+      const int bo = __ffs(ownm) - 1;
+      const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][bo * AST]);
       const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
-      const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
-      if (db == 0) {
+      own[0] = a01.x; own[1] = a01.y; own[2] = a23.x; own[3] = a23.y; own[4] = a45.x;
+      own[5] = a45.y; own[6] = a67.x; own[7] = a67.y; own[8] = a8.x;
+    }
+    // two coupled blocks per round: all their gathers are issued before the
+    // FMAs, which run in ascending block order (the order of the plain loop)
+    while (cm) {
+      const int bA = __ffs(cm) - 1;
+      cm &= cm - 1u;
+      const int bB = cm ? __ffs(cm) - 1 : -1;
+      if (cm) cm &= cm - 1u;
+      double yA0[3], yA1[3], yB0[3], yB1[3];
+      bool mA0, mA1, mB0 = false, mB1 = false;
+      {
+        const int2 k = s_b[wib][bA];
+        const int p0 = act0 ? s_pm[wib][bA * nJ + s0] : 0xFF;
+        const int p1 = (any1 && act1) ? s_pm[wib][bA * nJ + s1] : 0xFF;
+        mA0 = p0 != 0xFF;
+        mA1 = p1 != 0xFF;
+        const int64_t i0 = (int64_t)k.x + 3 * (mA0 ? p0 : 0) + b0, i1 = (int64_t)k.x + 3 * (mA1 ? p1 : 0) + b1;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) own[q] = a[q];
-        continue;
-      }
-      const int2 k = s_b[wib][b];
-      const int p0 = act0 ? s_pm[wib][b * nJ + s0] : 0xFF;
-      if (p0 != 0xFF) {
-        const int64_t i0 = (int64_t)k.x + 3 * p0 + b0;
-        const double y0 = u[i0], y1 = u[i0 + k.y], y2 = u[i0 + 2 * k.y];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          acc0[d] -= a[d * 3 + 0] * y0;
-          acc0[d] -= a[d * 3 + 1] * y1;
-          acc0[d] -= a[d * 3 + 2] * y2;
+        for (int e = 0; e < 3; ++e) {
+          yA0[e] = mA0 ? u[i0 + e * k.y] : 0.0;
+          yA1[e] = mA1 ? u[i1 + e * k.y] : 0.0;
         }
       }
-      if (any1) {
-        const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
-        if (p1 != 0xFF) {
-          const int64_t i1 = (int64_t)k.x + 3 * p1 + b1;
-          const double y0 = u[i1], y1 = u[i1 + k.y], y2 = u[i1 + 2 * k.y];
+      if (bB >= 0) {
+        const int2 k = s_b[wib][bB];
+        const int p0 = act0 ? s_pm[wib][bB * nJ + s0] : 0xFF;
+        const int p1 = (any1 && act1) ? s_pm[wib][bB * nJ + s1] : 0xFF;
+        mB0 = p0 != 0xFF;
+        mB1 = p1 != 0xFF;
+        const int64_t i0 = (int64_t)k.x + 3 * (mB0 ? p0 : 0) + b0, i1 = (int64_t)k.x + 3 * (mB1 ? p1 : 0) + b1;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          yB0[e] = mB0 ? u[i0 + e * k.y] : 0.0;
+          yB1[e] = mB1 ? u[i1 + e * k.y] : 0.0;
+        }
+      }
+      {
+        const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][bA * AST]);
+        const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+        const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+        if (mA0) {
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            acc1[d] -= a[d * 3 + 0] * y0;
-            acc1[d] -= a[d * 3 + 1] * y1;
-            acc1[d] -= a[d * 3 + 2] * y2;
+            acc0[d] -= a[d * 3 + 0] * yA0[0];
+            acc0[d] -= a[d * 3 + 1] * yA0[1];
+            acc0[d] -= a[d * 3 + 2] * yA0[2];
+          }
+        }
+        if (mA1) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] -= a[d * 3 + 0] * yA1[0];
+            acc1[d] -= a[d * 3 + 1] * yA1[1];
+            acc1[d] -= a[d * 3 + 2] * yA1[2];
+          }
+        }
+      }
+      if (bB >= 0) {
+        const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][bB * AST]);
+        const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+        const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+        if (mB0) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc0[d] -= a[d * 3 + 0] * yB0[0];
+            acc0[d] -= a[d * 3 + 1] * yB0[1];
+            acc0[d] -= a[d * 3 + 2] * yB0[2];
+          }
+        }
+        if (mB1) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] -= a[d * 3 + 0] * yB1[0];
+            acc1[d] -= a[d * 3 + 1] * yB1[1];
+            acc1[d] -= a[d * 3 + 2] * yB1[2];
           }
         }
       }
