@@ -205,6 +205,29 @@ emin_status emin_pattern(int64_t n, const int64_t* A_rowptr, const int32_t* A_co
                          int64_t* nnz_out, int32_t inputs_on_device, void* stream);
 const char* emin_pattern_error(void);
 
+/* The next level's operator A_c = P^T A P (reading A26):
+ * the matrix whose trace is the energy (Eq. trace), formed by the
+ * coarse grid construction's sparse matrix-matrix product before
+ * the method is re-run on the next level.  T = A P, then A_c = P^T T; every
+ * entry is the sum of its product terms in X order (A's column order, then
+ * P's rows ascending), one rounding per multiply and add -- bitwise
+ * reproducible; structural pattern (cancelled values are kept), columns
+ * ascending.
+ *   n, A_rowptr [n+1], A_col, A_val : A (n x n CSR);  P_rowptr [n+1], P_col
+ *   (coarse ids < nc), P_val : P (n x nc CSR, e.g. from emin_get_P with the
+ *   caller's pattern);  Ac_rowptr [nc+1] out;  Ac_col / Ac_val [Ac_cap] out,
+ *   or Ac_col = NULL to count only (EMIN_ERR_ARG if Ac_cap < nnz, Ac_rowptr
+ *   and *nnz_out still filled: call again);  all pointers host, or device if
+ *   inputs_on_device;  stream = cudaStream_t.  Synchronous; temporaries
+ *   (T, P^T) are allocated on the stream and freed before returning.
+ * EMIN_ERR_CSR on decreasing row pointers or column ids out of range;
+ * EMIN_ERR_ARG if a row of T or A_c has more than 8192 distinct columns. */
+emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_rowptr, const int32_t* A_col,
+                          const double* A_val, const int64_t* P_rowptr, const int32_t* P_col,
+                          const double* P_val, int64_t* Ac_rowptr, int32_t* Ac_col, double* Ac_val,
+                          int64_t Ac_cap, int64_t* nnz_out, int32_t inputs_on_device, void* stream);
+const char* emin_galerkin_error(void);
+
 /* Multi-GPU helpers (one process per GPU, NCCL over NVLink/NVSwitch).
  * emin_nccl_unique_id fills id[128] on one rank; the caller broadcasts it
  * (e.g. with torch.distributed) and every rank calls emin_nccl_comm_init;

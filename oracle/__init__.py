@@ -73,6 +73,8 @@ def _load():
         lib.oracle_pattern.restype = i64
         lib.oracle_gram_full_rank.argtypes = [i32, P]
         lib.oracle_gram_full_rank.restype = i32
+        lib.oracle_galerkin.argtypes = [i64, i64, P, P, P, P, P, P, P, P, P]
+        lib.oracle_galerkin.restype = i64
         _lib = lib
     return _lib
 
@@ -259,6 +261,21 @@ def pattern(prob, l0=2, lmax=4):
     lib.oracle_pattern(n, _p(args[0]), _p(args[1]), _p(args[2]), prob.block_size, prob.nv, _p(Bc),
                        l0, lmax, _p(rp), _p(col), _p(hist))
     return rp, col[:nnz], hist
+
+
+def galerkin(n, nc, A_rowptr, A_col, A_val, P_rowptr, P_col, P_val):
+    """A_c = P^T A P (reading A26, NEXT-4): returns (rowptr, col, val) of the
+    nc x nc coarse operator, columns ascending, structural pattern."""
+    lib = _load()
+    a = [np.ascontiguousarray(A_rowptr, np.int64), np.ascontiguousarray(A_col, np.int32),
+         np.ascontiguousarray(A_val, np.float64), np.ascontiguousarray(P_rowptr, np.int64),
+         np.ascontiguousarray(P_col, np.int32), np.ascontiguousarray(P_val, np.float64)]
+    rp = np.zeros(nc + 1, np.int64)
+    nnz = lib.oracle_galerkin(n, nc, *[_p(x) for x in a], _p(rp), None, None)
+    col = np.zeros(max(nnz, 1), np.int32)
+    val = np.zeros(max(nnz, 1), np.float64)
+    lib.oracle_galerkin(n, nc, *[_p(x) for x in a], _p(rp), _p(col), _p(val))
+    return rp, col[:nnz], val[:nnz]
 
 
 def gram_full_rank(G):

@@ -50,6 +50,12 @@
  *           (sgs_key, row) order (reading A23); applied matrix-free on the W
  *           layout as one forward and one backward sweep over the F rows, and
  *           always followed by Pi (only Jacobi may skip it).
+ *   galerkin (reading A26) A_c = P^T A P, the next
+ *           level's operator (the matrix whose trace is the energy,
+ *           P:248-250; "sparse matrix-matrix product") by its
+ *           two-product definition T = A P, A_c = P^T T; pinned against the
+ *           1D textbook closed form, dense numpy products and
+ *           A_c B_c = P^T A B whenever P B_c = B.
  *
  * Summation order: per-row sums ascending in A's column order; global sums
  * row-ascending with Neumaier compensation.
@@ -968,5 +974,89 @@ int64_t oracle_pattern(int64_t n, const int64_t *A_rowptr, const int32_t *A_col,
         }
     }
     free(cid); free(stamp); free(front); free(next); free(clist);
+    return nnz;
+}
+
+/* ------------------------------------------------------------------------
+ * galerkin (reading A26): the coarse operator of the next
+ * level, A_c = P^T A P -- the matrix whose trace is the energy the method
+ * minimises (Eq. trace), formed by the "sparse matrix-matrix
+ * product" of the coarse grid construction.  Textbook
+ * two-product definition, in this order:
+ *   T = A P            row i of T: T(i,j) = sum_k A(i,k) P(k,j), k in A's
+ *                      column order, one rounding per multiply and add;
+ *   A_c = P^T T        row c of A_c: A_c(c,j) = sum_i P(i,c) T(i,j), i
+ *                      ascending.
+ * Structural pattern: (c, j) is stored if some product term exists (values
+ * that cancel to 0 are kept); columns ascending.  Returns nnz(A_c); fills
+ * Ac_rowptr [nc+1] and, when Ac_col != NULL, Ac_col / Ac_val.
+ * ------------------------------------------------------------------------ */
+int64_t oracle_galerkin(int64_t n, int64_t nc, const int64_t *A_rowptr, const int32_t *A_col,
+                        const double *A_val, const int64_t *P_rowptr, const int32_t *P_col,
+                        const double *P_val, int64_t *Ac_rowptr, int32_t *Ac_col, double *Ac_val) {
+    /* T = A P, dense accumulator + marker per row (Gustavson) */
+    double *acc = (double *)calloc(nc > 0 ? nc : 1, sizeof(double));
+    int64_t *mark = (int64_t *)malloc(sizeof(int64_t) * (nc > 0 ? nc : 1));
+    int64_t *list = (int64_t *)malloc(sizeof(int64_t) * (nc > 0 ? nc : 1));
+    for (int64_t j = 0; j < nc; ++j) mark[j] = -1;
+    int64_t *Trp = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+    int64_t cap = 1024, nnzT = 0;
+    int32_t *Tcol = (int32_t *)malloc(sizeof(int32_t) * cap);
+    double *Tval = (double *)malloc(sizeof(double) * cap);
+    Trp[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t m = 0;
+        for (int64_t q = A_rowptr[i]; q < A_rowptr[i + 1]; ++q) {
+            int64_t k = A_col[q];
+            for (int64_t s = P_rowptr[k]; s < P_rowptr[k + 1]; ++s) {
+                int64_t j = P_col[s];
+                if (mark[j] != i) { mark[j] = i; acc[j] = 0.0; list[m++] = j; }
+                acc[j] = acc[j] + A_val[q] * P_val[s];
+            }
+        }
+        if (nnzT + m > cap) {
+            while (nnzT + m > cap) cap *= 2;
+            Tcol = (int32_t *)realloc(Tcol, sizeof(int32_t) * cap);
+            Tval = (double *)realloc(Tval, sizeof(double) * cap);
+        }
+        for (int64_t t = 0; t < m; ++t) { Tcol[nnzT] = (int32_t)list[t]; Tval[nnzT] = acc[list[t]]; ++nnzT; }
+        Trp[i + 1] = nnzT;
+    }
+    /* P^T by counting (rows i ascending within each column c) */
+    int64_t nnzP = P_rowptr[n];
+    int64_t *Ptp = (int64_t *)calloc(nc + 1, sizeof(int64_t));
+    for (int64_t s = 0; s < nnzP; ++s) Ptp[P_col[s] + 1]++;
+    for (int64_t c = 0; c < nc; ++c) Ptp[c + 1] += Ptp[c];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (nc > 0 ? nc : 1));
+    for (int64_t c = 0; c < nc; ++c) fill[c] = Ptp[c];
+    int64_t *Ptrow = (int64_t *)malloc(sizeof(int64_t) * (nnzP > 0 ? nnzP : 1));
+    double *Ptval = (double *)malloc(sizeof(double) * (nnzP > 0 ? nnzP : 1));
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t s = P_rowptr[i]; s < P_rowptr[i + 1]; ++s) {
+            int64_t c = P_col[s];
+            Ptrow[fill[c]] = i; Ptval[fill[c]] = P_val[s]; fill[c]++;
+        }
+    /* A_c = P^T T */
+    for (int64_t j = 0; j < nc; ++j) mark[j] = -1;
+    int64_t nnz = 0;
+    Ac_rowptr[0] = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+        int64_t m = 0;
+        for (int64_t s = Ptp[c]; s < Ptp[c + 1]; ++s) {
+            int64_t i = Ptrow[s];
+            for (int64_t t = Trp[i]; t < Trp[i + 1]; ++t) {
+                int64_t j = Tcol[t];
+                if (mark[j] != c) { mark[j] = c; acc[j] = 0.0; list[m++] = j; }
+                acc[j] = acc[j] + Ptval[s] * Tval[t];
+            }
+        }
+        qsort(list, m, sizeof(int64_t), cmp_i64);
+        if (Ac_col)
+            for (int64_t t = 0; t < m; ++t) { Ac_col[nnz + t] = (int32_t)list[t]; Ac_val[nnz + t] = acc[list[t]]; }
+        nnz += m;
+        Ac_rowptr[c + 1] = nnz;
+    }
+    free(acc); free(mark); free(list); free(Trp); free(Tcol); free(Tval);
+    free(Ptp); free(fill); free(Ptrow); free(Ptval);
     return nnz;
 }

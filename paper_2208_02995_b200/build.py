@@ -34,15 +34,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(OUT)
         if all(os.path.getmtime(d) <= t for d in deps if os.path.exists(d)):
             return OUT
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC", "-shared", "-o", OUT] + srcs
+    # one object per source, compiled in parallel, then one link (same flags)
+    flags = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+             "-Xcompiler", "-fPIC"]
     inc, lib = _nccl_paths()
     if inc:
-        cmd += ["-DEMIN_WITH_NCCL=1", "-I", inc, "-L", lib, "-l:libnccl.so.2",
-                "-Xlinker", "-rpath", "-Xlinker", lib]
+        flags += ["-DEMIN_WITH_NCCL=1", "-I", inc]
+    objdir = os.path.join(_HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    cmds = [flags + ["-c", s, "-o", o] for s, o in zip(srcs, objs)]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        for c in cmds:
+            print(" ".join(c))
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT] + objs
+    if inc:
+        link += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", lib]
+    if verbose:
+        print(" ".join(link))
+    subprocess.check_call(link)
     return OUT
 
 

@@ -60,7 +60,8 @@ class emin_report_t(C.Structure):
 EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "emin_get_P",
             "emin_reset", "emin_report", "emin_destroy", "emin_status_str", "emin_last_error",
             "emin_set_profiling", "emin_kernel_times", "emin_get_layout", "emin_nccl_unique_id",
-            "emin_nccl_comm_init", "emin_nccl_comm_destroy", "emin_pattern", "emin_pattern_error"]
+            "emin_nccl_comm_init", "emin_nccl_comm_destroy", "emin_pattern", "emin_pattern_error",
+            "emin_galerkin", "emin_galerkin_error"]
 
 
 def load_library():
@@ -111,6 +112,10 @@ def load_library():
     lib.emin_pattern.restype = i32
     lib.emin_pattern_error.argtypes = []
     lib.emin_pattern_error.restype = C.c_char_p
+    lib.emin_galerkin.argtypes = [i64, i64, P, P, P, P, P, P, P, P, P, i64, C.POINTER(i64), i32, P]
+    lib.emin_galerkin.restype = i32
+    lib.emin_galerkin_error.argtypes = []
+    lib.emin_galerkin_error.restype = C.c_char_p
     _lib = lib
     return lib
 
@@ -255,27 +260,73 @@ def emin_get_layout(ctx):
 
 def emin_pattern(n, A_rowptr, A_col, is_coarse, block_size, nv, Bc, nc, l0=2, lmax=4, stream=None):
     """emin_pattern (include/emin.h): Alg. 1's pattern growth from the graph
-    of A on the GPU.  Host numpy inputs; returns (P_rowptr, P_col)."""
+    of A on the GPU.  Inputs all host numpy arrays (returns numpy) or all
+    CUDA tensors (returns CUDA tensors); returns (P_rowptr, P_col)."""
     lib = load_library()
     import torch
-    arrs = [np.ascontiguousarray(A_rowptr, np.int64), np.ascontiguousarray(A_col, np.int32),
-            np.ascontiguousarray(is_coarse, np.uint8), np.ascontiguousarray(Bc, np.float64)]
-    rp = np.zeros(int(n) + 1, np.int64)
+    dev = _is_torch(A_rowptr)
+    if dev:
+        arrs = [A_rowptr.to(torch.int64).contiguous(), A_col.to(torch.int32).contiguous(),
+                is_coarse.to(torch.uint8).contiguous(), Bc.to(torch.float64).contiguous()]
+        rp = torch.zeros(int(n) + 1, dtype=torch.int64, device=A_rowptr.device)
+    else:
+        arrs = [np.ascontiguousarray(A_rowptr, np.int64), np.ascontiguousarray(A_col, np.int32),
+                np.ascontiguousarray(is_coarse, np.uint8), np.ascontiguousarray(Bc, np.float64)]
+        rp = np.zeros(int(n) + 1, np.int64)
     nnz = C.c_int64(0)
     if stream is None:
         stream = torch.cuda.current_stream().cuda_stream
     st = lib.emin_pattern(int(n), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), int(block_size), int(nv),
-                          _ptr(arrs[3]), int(nc), int(l0), int(lmax), _ptr(rp), None, 0, C.byref(nnz), 0,
-                          C.c_void_p(int(stream)))
+                          _ptr(arrs[3]), int(nc), int(l0), int(lmax), _ptr(rp), None, 0, C.byref(nnz),
+                          int(dev), C.c_void_p(int(stream)))
     if st != 0:
         raise EminError(st, lib.emin_pattern_error().decode())
-    col = np.zeros(max(nnz.value, 1), np.int32)
+    m = max(nnz.value, 1)
+    col = torch.zeros(m, dtype=torch.int32, device=A_rowptr.device) if dev else np.zeros(m, np.int32)
     st = lib.emin_pattern(int(n), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), int(block_size), int(nv),
                           _ptr(arrs[3]), int(nc), int(l0), int(lmax), _ptr(rp), _ptr(col), nnz.value,
-                          C.byref(nnz), 0, C.c_void_p(int(stream)))
+                          C.byref(nnz), int(dev), C.c_void_p(int(stream)))
     if st != 0:
         raise EminError(st, lib.emin_pattern_error().decode())
     return rp, col[:nnz.value]
+
+
+def emin_galerkin(n, nc, A_rowptr, A_col, A_val, P_rowptr, P_col, P_val, stream=None):
+    """emin_galerkin (include/emin.h): A_c = P^T A P on the GPU.  Inputs all
+    host numpy arrays (returns numpy) or all CUDA tensors (returns CUDA
+    tensors, nothing leaves the device but the nnz count)."""
+    lib = load_library()
+    import torch
+    dev = _is_torch(A_rowptr)
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    if dev:
+        arrs = [A_rowptr.to(torch.int64).contiguous(), A_col.to(torch.int32).contiguous(),
+                A_val.to(torch.float64).contiguous(), P_rowptr.to(torch.int64).contiguous(),
+                P_col.to(torch.int32).contiguous(), P_val.to(torch.float64).contiguous()]
+        rp = torch.zeros(int(nc) + 1, dtype=torch.int64, device=A_rowptr.device)
+    else:
+        arrs = [np.ascontiguousarray(A_rowptr, np.int64), np.ascontiguousarray(A_col, np.int32),
+                np.ascontiguousarray(A_val, np.float64), np.ascontiguousarray(P_rowptr, np.int64),
+                np.ascontiguousarray(P_col, np.int32), np.ascontiguousarray(P_val, np.float64)]
+        rp = np.zeros(int(nc) + 1, np.int64)
+    nnz = C.c_int64(0)
+    sp = C.c_void_p(int(stream))
+    st = lib.emin_galerkin(int(n), int(nc), *[_ptr(a) for a in arrs], _ptr(rp), None, None, 0, C.byref(nnz),
+                           int(dev), sp)
+    if st != 0:
+        raise EminError(st, lib.emin_galerkin_error().decode())
+    m = max(nnz.value, 1)
+    if dev:
+        col = torch.empty(m, dtype=torch.int32, device=A_rowptr.device)
+        val = torch.empty(m, dtype=torch.float64, device=A_rowptr.device)
+    else:
+        col, val = np.zeros(m, np.int32), np.zeros(m, np.float64)
+    st = lib.emin_galerkin(int(n), int(nc), *[_ptr(a) for a in arrs], _ptr(rp), _ptr(col), _ptr(val), m,
+                           C.byref(nnz), int(dev), sp)
+    if st != 0:
+        raise EminError(st, lib.emin_galerkin_error().decode())
+    return rp, col[:nnz.value], val[:nnz.value]
 
 
 def emin_nccl_unique_id():

@@ -632,3 +632,104 @@ def test_linear_modes_nv3_converges_to_kkt(precond, start):
     assert np.abs(o.get_W() - w).max() <= 1e-8 * np.abs(w).max()
     Cm, b = D.constraint_matrix(prob)
     assert np.abs(Cm @ o.get_W() - b).max() <= 1e-12 * max(1.0, np.abs(b).max())
+
+
+# --------------------------------------------------------------------------
+# Galerkin coarse operator A_c = P^T A P (reading A26;
+# Eq. trace, coarse grid construction P:957-961)
+# --------------------------------------------------------------------------
+
+def _linear_interp_1d(prob):
+    """1D linear interpolation on prob's (wider) pattern: W(i, c) = 1/2 for
+    the two C neighbours of F point i, 0 on the other pattern entries."""
+    P = np.zeros(prob.P_rowptr[-1])
+    for i in range(prob.n):
+        for q in range(prob.P_rowptr[i], prob.P_rowptr[i + 1]):
+            c = prob.P_col[q]
+            if prob.is_coarse[i]:
+                P[q] = 1.0
+            elif abs(2 * c - i) == 1:
+                P[q] = 0.5
+    return P
+
+
+def test_galerkin_1d_linear_interpolation_closed_form():
+    # textbook: P^T tridiag(-1, 2, -1) P with linear interpolation =
+    # (1/2) tridiag(-1, 2, -1) on the coarse grid; at the Dirichlet ends
+    # A_c(0, 0) = A00 + A01 + A11 / 4 = 3/2.  Exact in binary.
+    from oracle import galerkin
+    p = make_config("1d", 17)
+    Pv = _linear_interp_1d(p)
+    rp, col, val = galerkin(p.n, p.nc, p.A_rowptr, p.A_col, p.A_val, p.P_rowptr, p.P_col, Pv)
+    Ac = np.zeros((p.nc, p.nc))
+    for c in range(p.nc):
+        assert np.all(np.diff(col[rp[c]:rp[c + 1]]) > 0)
+        Ac[c, col[rp[c]:rp[c + 1]]] = val[rp[c]:rp[c + 1]]
+    want = np.diag(np.full(p.nc, 1.0)) - 0.5 * (np.eye(p.nc, k=1) + np.eye(p.nc, k=-1))
+    want[0, 0] = want[-1, -1] = 1.5
+    assert np.array_equal(Ac, want)
+    # structural pattern: distance-3 pattern of P, A tridiagonal -> |c - c'| <= 3
+    # wherever a product chain exists (checked against boolean matrix products)
+    Pb = np.zeros((p.n, p.nc), np.int64)
+    for i in range(p.n):
+        Pb[i, p.P_col[p.P_rowptr[i]:p.P_rowptr[i + 1]]] = 1
+    Ab = (np.abs(np.eye(p.n, k=1)) + np.eye(p.n) + np.eye(p.n, k=-1)).astype(np.int64)
+    S = (Pb.T @ Ab @ Pb) > 0
+    got = np.zeros_like(S)
+    for c in range(p.nc):
+        got[c, col[rp[c]:rp[c + 1]]] = True
+    assert np.array_equal(got, S)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_galerkin_matches_dense_product(seed):
+    from oracle import galerkin
+    rng = np.random.default_rng(seed)
+    n, nc = 70, 17
+    M = (rng.random((n, n)) < 0.08) * rng.standard_normal((n, n))
+    A = M + M.T + np.diag(rng.random(n) + 1.0)
+    Pd = (rng.random((n, nc)) < 0.2) * rng.standard_normal((n, nc))
+    Pd[rng.integers(0, n, 5), :] = 0.0                       # a few empty rows of P
+    def csr(D):
+        rp = np.zeros(D.shape[0] + 1, np.int64)
+        cols, vals = [], []
+        for i in range(D.shape[0]):
+            nz = np.flatnonzero(D[i])
+            cols.append(nz); vals.append(D[i, nz]); rp[i + 1] = rp[i] + nz.size
+        return rp, np.concatenate(cols).astype(np.int32), np.concatenate(vals)
+    Arp, Acol, Aval = csr(A)
+    Prp, Pcol, Pval = csr(Pd)
+    rp, col, val = galerkin(n, nc, Arp, Acol, Aval, Prp, Pcol, Pval)
+    Ac = np.zeros((nc, nc))
+    got = np.zeros((nc, nc), bool)
+    for c in range(nc):
+        Ac[c, col[rp[c]:rp[c + 1]]] = val[rp[c]:rp[c + 1]]
+        got[c, col[rp[c]:rp[c + 1]]] = True
+    dense = Pd.T @ A @ Pd
+    assert np.allclose(Ac, dense, rtol=0, atol=1e-13 * np.abs(dense).max())
+    S = ((Pd != 0).astype(np.int64).T @ (A != 0).astype(np.int64) @ (Pd != 0).astype(np.int64)) > 0
+    assert np.array_equal(got, S)
+
+
+@pytest.mark.parametrize("name,size", [("3", 12), ("4", 4), ("1v3", 10)])
+def test_galerkin_trace_is_energy_symmetric_and_keeps_near_kernel(name, size):
+    # tr(P^T A P) is the energy (Eq. trace P:248-250) computed by the
+    # oracle's own energy routine; A_c symmetric; and because every iterate
+    # keeps P B_c = B (P:355-370), A_c B_c = P^T A P B_c = P^T (A B)
+    import scipy.sparse as sp
+    from oracle import galerkin
+    p = make_config(name, size)
+    o = Oracle(p)
+    o.iterate(6)
+    Pv = o.get_P()
+    rp, col, val = galerkin(p.n, p.nc, p.A_rowptr, p.A_col, p.A_val, p.P_rowptr, p.P_col, Pv)
+    Ac = sp.csr_matrix((val, col, rp), shape=(p.nc, p.nc))
+    assert abs(Ac.diagonal().sum() - o.energy()) <= 1e-12 * abs(o.energy())
+    d = (Ac - Ac.T).tocoo()
+    assert np.abs(d.data).max(initial=0.0) <= 1e-13 * np.abs(val).max()
+    assert (Ac != 0).sum() <= Ac.nnz and np.array_equal(np.sort(Ac.indices), np.sort(Ac.T.tocsr().indices))
+    A = sp.csr_matrix((p.A_val, p.A_col, p.A_rowptr), shape=(p.n, p.n))
+    P = sp.csr_matrix((Pv, p.P_col, p.P_rowptr), shape=(p.n, p.nc))
+    lhs = Ac @ p.Bc
+    rhs = P.T @ (A @ p.B)
+    assert np.abs(lhs - rhs).max() <= 1e-10 * max(np.abs(rhs).max(), np.abs(lhs).max(), 1.0)

@@ -548,7 +548,7 @@ def _elasticity_problem(name, N, nu, E_elem, iters, start, seed_pert=1, meta=Non
     B = Bn.reshape(n, 6)
     Bc = B[is_c].copy()
     P_val = _start_values(start, n, is_c, None, P_rowptr, seed_pert)
-    m = dict(dims=(nxn, nyn, nzn), growth=used, n_cnode=ncn, n_fnode=int(fine_nodes.size),
+    m = dict(dims=(nxn, nyn, nzn), zlo=1, growth=used, n_cnode=ncn, n_fnode=int(fine_nodes.size),
              **(meta or {}))
     return Problem(name, n, 3 * ncn, rowptr, col, val, is_c.astype(np.uint8), P_rowptr, P_col,
                    P_val, 6, B, Bc, iters, 3, m)
@@ -631,6 +631,45 @@ def make_config(name: str, size: Optional[int] = None, seed: int = 0,
         return _elasticity_problem(f"5@{N}", N, 0.25, E, 40, start or "leastnorm",
                                    meta=dict(config="5", seed=seed, E_layers=El.tolist()))
     raise KeyError(name)
+
+
+def coarse_split(dims, zlo=0):
+    """Geometric 2x coarsening of a lexicographic node grid (x fastest), the
+    splitting every level of the configs uses (reading A26: PMIS is out of
+    scope): node (x, y, zlo + z) is a C node iff x, y and zlo + z are even.
+    Returns (is_c_node bool [nx*ny*nz], coarse dims, coarse zlo); coarse ids
+    (ranks among the C nodes) are again lexicographic on the coarse grid."""
+    nx, ny, nz = dims
+    nodes = np.arange(nx * ny * nz)
+    x, y, z = nodes % nx, (nodes // nx) % ny, zlo + nodes // (nx * ny)
+    is_c = (x % 2 == 0) & (y % 2 == 0) & (z % 2 == 0)
+    zc = np.arange(zlo, zlo + nz)
+    zc = zc[zc % 2 == 0]
+    cdims = ((nx + 1) // 2, (ny + 1) // 2, int(zc.size))
+    czlo = int(zc[0] // 2) if zc.size else 0
+    return is_c, cdims, czlo
+
+
+def coarse_problem(prob: Problem, Ac_rowptr, Ac_col, Ac_val, iters: Optional[int] = None) -> Problem:
+    """The next level of a hierarchy: operator A_c (=
+    P^T A P, computed by the caller), C/F from ``coarse_split`` of the coarse
+    grid, near kernel B_next = B_c of this level, B_c,next its injection;
+    P's pattern is left to the caller (P_rowptr / P_col None: Alg. 1's growth
+    on the graph of A_c), least-norm start (P_val None)."""
+    dims, zlo = prob.meta["dims"], prob.meta.get("zlo", 0)
+    bs = prob.block_size
+    is_c_node, cdims, czlo = coarse_split(dims, zlo)
+    if not np.array_equal(np.repeat(is_c_node, bs), prob.is_coarse.astype(bool)):
+        raise ValueError("prob's C/F splitting is not the geometric one")
+    # the next level's nodes are this level's C nodes (lexicographic on cdims)
+    is_c2 = np.repeat(coarse_split(cdims, czlo)[0], bs)
+    B2 = np.ascontiguousarray(prob.Bc)
+    Bc2 = B2[is_c2].copy()
+    lev = prob.meta.get("level", 1) + 1
+    meta = dict(dims=cdims, zlo=czlo, level=lev, config=prob.meta.get("config"))
+    return Problem(f"{prob.name}/L{lev}", prob.nc, int(is_c2.sum()), np.asarray(Ac_rowptr, np.int64),
+                   np.asarray(Ac_col, np.int32), np.asarray(Ac_val, np.float64), is_c2.astype(np.uint8),
+                   None, None, None, prob.nv, B2, Bc2, iters or prob.iters, bs, meta)
 
 
 def sgs_key(prob: Problem, kind: str = "natural") -> Optional[np.ndarray]:
