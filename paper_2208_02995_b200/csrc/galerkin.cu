@@ -20,8 +20,9 @@
 // multiply and per add (__dmul_rn / __dadd_rn) -- within a round the lanes
 // that hit the same slot (__match_any_sync) are added by the lowest of them
 // in lane order, i.e. in X order, and rounds run in X order.  A row goes to
-// the smallest of three table sizes (256 / 2048 / 16384 slots) that keeps the
-// load factor <= 1/2; wider rows are an error.
+// the smallest of four table sizes (256 / 512 / 2048 / 16384 slots) that
+// keeps the load factor <= 1/2 (the small tables keep 32-64 warps per SM);
+// wider rows are an error.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <string>
@@ -31,8 +32,9 @@
 
 namespace {
 
-constexpr int GK_LOG[3] = {8, 11, 14};       // table slots 256 / 2048 / 16384
-constexpr int GK_WARPS[3] = {8, 4, 1};       // warps per CTA
+constexpr int GK_TIERS = 4;
+constexpr int GK_LOG[GK_TIERS] = {8, 9, 11, 14};   // table slots 256 / 512 / 2048 / 16384
+constexpr int GK_WARPS[GK_TIERS] = {8, 8, 4, 1};   // warps per CTA
 
 struct GkArgs {
   int64_t nrows;
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(GK_WARPS[T] * 32) k_gk_symbolic(GkArgs a) {
     });
     if (lane == 0) {
       if (count <= CAP / 2) a.cnt[row] = count;
-      else if (T == 2) { a.cnt[row] = 0; atomicOr(a.err, 2); }
+      else if (T == GK_TIERS - 1) { a.cnt[row] = 0; atomicOr(a.err, 2); }
       else a.cnt[row] = -(T + 1);
     }
     for (int s = lane; s < CAP; s += 32) keys[s] = -1;
@@ -146,7 +148,8 @@ __global__ void __launch_bounds__(GK_WARPS[T] * 32) k_gk_symbolic(GkArgs a) {
   }
 }
 
-__device__ __forceinline__ int gk_tier(int64_t c) { return c <= 128 ? 0 : (c <= 1024 ? 1 : 2); }
+// the table a row of c distinct columns goes to (load factor <= 1/2)
+__device__ __forceinline__ int gk_tier(int64_t c) { return c <= 128 ? 0 : c <= 256 ? 1 : c <= 1024 ? 2 : 3; }
 
 template <int T>
 __global__ void __launch_bounds__(GK_WARPS[T] * 32) k_gk_numeric(GkArgs a) {
@@ -244,12 +247,21 @@ cudaError_t gk_launch(bool numeric, const GkArgs& a, int SM, cudaStream_t s) {
   cudaError_t e = numeric ? cudaFuncSetAttribute(k_gk_numeric<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)
                           : cudaFuncSetAttribute(k_gk_symbolic<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  const int per_sm = T == 0 ? 8 : (T == 1 ? 2 : 1);
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2048 / (GK_WARPS[T] * 32), (220u << 10) / sm));
   const int64_t want = (a.nrows + GK_WARPS[T] - 1) / GK_WARPS[T];
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)SM * per_sm));
   if (numeric) k_gk_numeric<T><<<g, GK_WARPS[T] * 32, sm, s>>>(a);
   else k_gk_symbolic<T><<<g, GK_WARPS[T] * 32, sm, s>>>(a);
   return cudaGetLastError();
+}
+
+// every tier in order (symbolic: tier t > 0 re-counts the rows tier t - 1 overflowed)
+cudaError_t gk_launch_all(bool numeric, const GkArgs& a, int SM, cudaStream_t s) {
+  cudaError_t e = gk_launch<0>(numeric, a, SM, s);
+  if (e == cudaSuccess) e = gk_launch<1>(numeric, a, SM, s);
+  if (e == cudaSuccess) e = gk_launch<2>(numeric, a, SM, s);
+  if (e == cudaSuccess) e = gk_launch<3>(numeric, a, SM, s);
+  return e;
 }
 
 }  // namespace
@@ -330,9 +342,7 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
     GkArgs a{};
     a.nrows = nrows; a.Xrp = Xrp; a.Xcol = Xcol; a.Xval = Xval; a.Yrp = Yrp; a.Ycol = Ycol; a.Yval = Yval;
     a.cnt = cnt; a.sort = sort; a.err = err;
-    if (gk_launch<0>(false, a, SM, s) != cudaSuccess || gk_launch<1>(false, a, SM, s) != cudaSuccess ||
-        gk_launch<2>(false, a, SM, s) != cudaSuccess)
-      return EMIN_ERR_CUDA;
+    if (gk_launch_all(false, a, SM, s) != cudaSuccess) return EMIN_ERR_CUDA;
     int32_t h = 0;
     if (cudaMemcpyAsync(&h, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
@@ -350,9 +360,7 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
     }
     if (!*Ocol) return EMIN_OK;
     a.Orp = Orp; a.Ocol = *Ocol; a.Oval = *Oval;
-    if (gk_launch<0>(true, a, SM, s) != cudaSuccess || gk_launch<1>(true, a, SM, s) != cudaSuccess ||
-        gk_launch<2>(true, a, SM, s) != cudaSuccess)
-      return EMIN_ERR_CUDA;
+    if (gk_launch_all(true, a, SM, s) != cudaSuccess) return EMIN_ERR_CUDA;
     return EMIN_OK;
   };
 
@@ -412,9 +420,7 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
     GkArgs a{};
     a.nrows = nc; a.Xrp = Ptp; a.Xcol = Ptrow; a.Xval = vout; a.Yrp = Trp; a.Ycol = Tcol; a.Yval = Tval;
     a.cnt = cntC; a.Orp = Crp; a.Ocol = Ccol; a.Oval = Cval; a.sort = 1; a.err = err;
-    GK_TRY(gk_launch<0>(true, a, SM, s));
-    GK_TRY(gk_launch<1>(true, a, SM, s));
-    GK_TRY(gk_launch<2>(true, a, SM, s));
+    GK_TRY(gk_launch_all(true, a, SM, s));
     if (!inputs_on_device) {
       GK_TRY(cudaMemcpyAsync(Ac_col, Ccol, sizeof(int32_t) * nnzC, cudaMemcpyDeviceToHost, s));
       GK_TRY(cudaMemcpyAsync(Ac_val, Cval, sizeof(double) * nnzC, cudaMemcpyDeviceToHost, s));

@@ -547,6 +547,7 @@ bool emin_nodal_plan(emin_ctx c, const int2** blk, const int64_t** bptr, const u
                      const int64_t** pmoff, int64_t* nFn) {
   if (c->kernel_path != 2 || !c->nodal) return false;
   const NodalPlan* np = static_cast<const NodalPlan*>(c->nodal);
+  if (np->max_nb > ND_MAXB) return false;      // the SGS nodal sweeps stage <= ND_MAXB blocks
   *blk = reinterpret_cast<const int2*>(np->blk);
   *bptr = np->bptr;
   *pm8 = np->pm8;

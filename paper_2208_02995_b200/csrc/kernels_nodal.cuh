@@ -31,10 +31,11 @@ struct NodalPlan {
   uint8_t* pm8 = nullptr;     // [sum_n nblk_n |J_n|] position of J_I[s] in J_K, 0xFF absent
   int64_t* pmoff = nullptr;   // [nFn+1]
   int64_t nblk = 0, npm = 0;
+  int32_t max_nb = 0;         // most blocks of one node (> ND_MAXB: v2 stages in chunks; SGS goes generic)
 };
 
 // structure checks (one thread per F node); any violation clears *ok
-__global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_len) {
+__global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_len, int32_t* max_nb) {
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = 3 * n;
     const int64_t wb = v.wptr[r];
@@ -48,7 +49,8 @@ __global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_l
     }
     const int64_t ab = v.affptr[r];
     const int64_t alen = v.affptr[r + 1] - ab;
-    good = good && (alen % 3 == 0) && (alen / 3 <= 27);      // <= 27 blocks (staged kernel)
+    good = good && (alen % 3 == 0);
+    if (good) atomicMax(max_nb, (int32_t)(alen / 3));
     for (int d = 1; d < 3 && good; ++d) good = (v.affptr[r + d + 1] - v.affptr[r + d]) == alen;
     for (int64_t q = 0; q < alen && good; ++q) {
       const int32_t k = v.affcol[ab + q];
@@ -379,7 +381,7 @@ __device__ __forceinline__ void nd2_reduce_scatter(double (&v)[N], int lane, int
   *own = lo;
 }
 
-template <int NV, int MODE, bool PRED = false, bool CS = false>
+template <int NV, int MODE, bool PRED = false, bool CS = false, bool WIDE = false>
 __global__ void __launch_bounds__(ND_WARPS * 32, 4)
 k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
@@ -408,23 +410,33 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
     const int64_t bb = bptr[n];
     const int nb = (int)(bptr[n + 1] - bb);
     const int64_t po = pmoff[n];
-    // ---- stage the node's data (A chunk re-ordered block-major, 10-double stride)
     const int rs = 3 * nb;
-    for (int k = lane; k < 9 * nb; k += 32) {
-      const int d = k / rs, rem = k - d * rs, b = rem / 3, e = rem - 3 * b;
-      s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(v.affval + ab + k) : __ldg(v.affval + ab + k);
-    }
-    for (int k = lane; k < nb; k += 32) {
-      if (CS) { const int2 t = __ldcs(reinterpret_cast<const int2*>(blk + bb + k)); s_b[wib][k] = NodalBlk{t.x, t.y}; }
-      else s_b[wib][k] = blk[bb + k];
-    }
-    for (int k = lane; k < nb * nJ; k += 32)
-      s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + po + k)) : pm8[po + k];
     const bool act0 = t0 < n3, act1 = t1 < n3;
     const bool any1 = n3 > 32;                          // warp-uniform
-    __syncwarp();
     double acc0[3] = {0.0, 0.0, 0.0}, acc1[3] = {0.0, 0.0, 0.0};
-    for (int b = 0; b < nb; ++b) {
+    // nodes with more than ND_MAXB blocks (Galerkin operators of coarse
+    // levels, NEXT-4) are staged ND_MAXB blocks at a time, same block order
+    // (template WIDE; otherwise the one chunk is the whole node, c0 = 0)
+    for (int cl = 0; cl < nb; cl += WIDE ? ND_MAXB : nb) {
+    const int c0 = WIDE ? cl : 0;
+    const int cb = WIDE ? min(ND_MAXB, nb - c0) : nb, cs = 3 * cb;
+    if (WIDE && c0) __syncwarp();
+    // ---- stage the node's data (A chunk re-ordered block-major, 10-double stride)
+    for (int k = lane; k < 9 * cb; k += 32) {
+      const int d = k / cs, rem = k - d * cs, b = rem / 3, e = rem - 3 * b;
+      const int64_t src = WIDE ? ab + (int64_t)d * rs + 3 * c0 + rem : ab + k;
+      s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(v.affval + src) : __ldg(v.affval + src);
+    }
+    for (int k = lane; k < cb; k += 32) {
+      if (CS) { const int2 t = __ldcs(reinterpret_cast<const int2*>(blk + bb + c0 + k)); s_b[wib][k] = NodalBlk{t.x, t.y}; }
+      else s_b[wib][k] = blk[bb + c0 + k];
+    }
+    for (int k = lane; k < cb * nJ; k += 32) {
+      const int64_t src = po + (int64_t)c0 * nJ + k;
+      s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + src)) : pm8[src];
+    }
+    __syncwarp();
+    for (int b = 0; b < cb; ++b) {
       const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][b * ND2_AST]);
       const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
       const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
@@ -480,6 +492,7 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
         }
       }
     }
+    }  // chunks of ND_MAXB blocks
     double g0[3], g1[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) { g0[d] = acc0[d]; g1[d] = acc1[d]; }
@@ -592,15 +605,16 @@ static inline bool select_nodal_path(emin_ctx c, NodalPlan*& out) {
   const int64_t nFn = c->nF / 3;
   int32_t* ok;
   int64_t *pmlen, *scratch, *tot;
-  if (nd_alloc(&ok, 1, s) || nd_alloc(&pmlen, nFn + 1, s) || nd_alloc(&scratch, emin_scan_scratch_elems(nFn + 1), s) ||
+  if (nd_alloc(&ok, 2, s) || nd_alloc(&pmlen, nFn + 1, s) || nd_alloc(&scratch, emin_scan_scratch_elems(nFn + 1), s) ||
       nd_alloc(&tot, 1, s))
     return false;
-  const int32_t one = 1;
-  cudaMemcpyAsync(ok, &one, sizeof(int32_t), cudaMemcpyHostToDevice, s);
-  k_nodal_check<<<SM * 8, 256, 0, s>>>(c->view(), nFn, ok, pmlen);
-  int32_t h_ok = 0;
-  cudaMemcpyAsync(&h_ok, ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  const int32_t init[2] = {1, 0};
+  cudaMemcpyAsync(ok, init, sizeof(int32_t) * 2, cudaMemcpyHostToDevice, s);
+  k_nodal_check<<<SM * 8, 256, 0, s>>>(c->view(), nFn, ok, pmlen, ok + 1);
+  int32_t h_ok2[2] = {0, 0};
+  cudaMemcpyAsync(h_ok2, ok, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
+  const int32_t h_ok = h_ok2[0];
   c->launches += 1;
   if (!h_ok) {
     cudaFreeAsync(ok, s); cudaFreeAsync(pmlen, s); cudaFreeAsync(scratch, s); cudaFreeAsync(tot, s);
@@ -608,6 +622,7 @@ static inline bool select_nodal_path(emin_ctx c, NodalPlan*& out) {
   }
   NodalPlan* p = new NodalPlan();
   p->nFn = nFn;
+  p->max_nb = h_ok2[1];
   p->nblk = c->nnzAFF / 9;
   emin_scan_i64(pmlen, pmlen, nFn, tot, scratch, s);     // exclusive -> offsets
   cudaMemcpyAsync(pmlen + nFn, tot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s);
@@ -634,6 +649,22 @@ static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
                                 double* out, cudaStream_t s) {
   const DevView v = c->view();
   const int g = nodal_grid(c, p);
+  if (p->max_nb > ND_MAXB) {
+    // Galerkin levels (NEXT-4): nodes with more than ND_MAXB blocks, v2 staged
+    // in chunks (ITER with the evict-first hints, the setup/energy modes plain)
+#define NDW(N, M, CSX) k_spgemm_nodal_v2<N, M, false, CSX, true><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials)
+#define NV_CASE(N)                                            \
+  case N:                                                     \
+    if (mode == MM_ITER) NDW(N, MM_ITER, true);               \
+    else if (mode == MM_R0) NDW(N, MM_R0, false);             \
+    else if (mode == MM_R0E) NDW(N, MM_R0E, false);           \
+    else NDW(N, MM_ENERGY, false);                            \
+    break;
+    switch (c->nv) { NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8) }
+#undef NV_CASE
+#undef NDW
+    return true;
+  }
   const char* var = getenv("EMIN_NODAL");
   if (mode == MM_ITER && var && !strcmp(var, "plain")) {
     switch (c->nv) {
