@@ -381,7 +381,7 @@ __device__ __forceinline__ void nd2_reduce_scatter(double (&v)[N], int lane, int
   *own = lo;
 }
 
-template <int NV, int MODE, bool PRED = false, bool CS = false, bool WIDE = false>
+template <int NV, int MODE, bool PRED = false, bool CS = false, bool WIDE = false, int GRP = 1>
 __global__ void __launch_bounds__(ND_WARPS * 32, 4)
 k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
@@ -436,6 +436,53 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
       s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + src)) : pm8[src];
     }
     __syncwarp();
+    if (GRP > 1) {
+      // GRP blocks per round: the (up to 6 GRP) gathers of all of them are
+      // issued before the FMAs, which run in ascending block order with the
+      // same skips as the loop below (bitwise the same sums)
+      for (int b = 0; b < cb; b += GRP) {
+        double y0[GRP][3], y1[GRP][3];
+        bool m0[GRP], m1[GRP];
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) {
+          const bool has = b + g < cb;
+          const NodalBlk k = s_b[wib][has ? b + g : b];
+          const int p0 = (has && act0) ? s_pm[wib][(b + g) * nJ + s0] : 0xFF;
+          const int p1 = (has && any1 && act1) ? s_pm[wib][(b + g) * nJ + s1] : 0xFF;
+          m0[g] = p0 != 0xFF;
+          m1[g] = p1 != 0xFF;
+          const int i0 = k.ybase + 3 * (m0[g] ? p0 : 0) + b0, i1 = k.ybase + 3 * (m1[g] ? p1 : 0) + b1;
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            y0[g][e] = m0[g] ? xval(i0 + e * k.nK3) : 0.0;
+            y1[g][e] = m1[g] ? xval(i1 + e * k.nK3) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) {
+          if (b + g >= cb) break;
+          const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][(b + g) * ND2_AST]);
+          const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+          const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+          if (m0[g]) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              acc0[d] = fma(a[d * 3 + 0], y0[g][0], acc0[d]);
+              acc0[d] = fma(a[d * 3 + 1], y0[g][1], acc0[d]);
+              acc0[d] = fma(a[d * 3 + 2], y0[g][2], acc0[d]);
+            }
+          }
+          if (m1[g]) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              acc1[d] = fma(a[d * 3 + 0], y1[g][0], acc1[d]);
+              acc1[d] = fma(a[d * 3 + 1], y1[g][1], acc1[d]);
+              acc1[d] = fma(a[d * 3 + 2], y1[g][2], acc1[d]);
+            }
+          }
+        }
+      }
+    } else
     for (int b = 0; b < cb; ++b) {
       const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][b * ND2_AST]);
       const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
@@ -645,28 +692,54 @@ static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((p->nFn + 7) / 8, (int64_t)SM * 16));
 }
 
+// one v2 configuration for every mode: CS = evict-first hints (iteration
+// only), WIDE = chunked staging (> ND_MAXB blocks per node), GRP = blocks per
+// round
+template <int NV, bool CS, bool WIDE, int GRP>
+static inline void nd_v2(int mode, const DevView& v, const NodalPlan* p, int g, const double* X, const double* X2,
+                         double* out, double* partials, cudaStream_t s) {
+#define ND_ARGS <<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, partials)
+  if (mode == MM_ITER) k_spgemm_nodal_v2<NV, MM_ITER, false, CS, WIDE, GRP> ND_ARGS;
+  else if (mode == MM_R0) k_spgemm_nodal_v2<NV, MM_R0, false, false, WIDE, GRP> ND_ARGS;
+  else if (mode == MM_R0E) k_spgemm_nodal_v2<NV, MM_R0E, false, false, WIDE, GRP> ND_ARGS;
+  else k_spgemm_nodal_v2<NV, MM_ENERGY, false, false, WIDE, GRP> ND_ARGS;
+#undef ND_ARGS
+}
+
+template <bool CS, bool WIDE, int GRP>
+static inline void nd_v2_nv(int nv, int mode, const DevView& v, const NodalPlan* p, int g, const double* X,
+                            const double* X2, double* out, double* partials, cudaStream_t s) {
+  switch (nv) {
+#define NV_CASE(N) case N: nd_v2<N, CS, WIDE, GRP>(mode, v, p, g, X, X2, out, partials, s); break;
+    NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+#undef NV_CASE
+  }
+}
+
 static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const double* X, const double* X2,
                                 double* out, cudaStream_t s) {
   const DevView v = c->view();
   const int g = nodal_grid(c, p);
+  // Default: v2 with two blocks per round (all gathers of both issued before
+  // the FMAs; config 5 20.7 -> 15.9 ms, config 4 471 -> 420 us; three or four
+  // per round spill or lose occupancy: 16.6 / 21.0+ ms) and, in the
+  // iteration, evict-first hints on the streamed data (A chunk, block
+  // records, position bytes, Q, y^) so the L2 keeps the gathered y rows.
+  // Galerkin levels (NEXT-4, > ND_MAXB blocks per node): the same, staged in
+  // chunks.  EMIN_NODAL selects the A/B variants (v2cs / v2: one block per
+  // round with / without hints, v2p branch-free, s staged v1, plain).
   if (p->max_nb > ND_MAXB) {
-    // Galerkin levels (NEXT-4): nodes with more than ND_MAXB blocks, v2 staged
-    // in chunks (ITER with the evict-first hints, the setup/energy modes plain)
-#define NDW(N, M, CSX) k_spgemm_nodal_v2<N, M, false, CSX, true><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials)
-#define NV_CASE(N)                                            \
-  case N:                                                     \
-    if (mode == MM_ITER) NDW(N, MM_ITER, true);               \
-    else if (mode == MM_R0) NDW(N, MM_R0, false);             \
-    else if (mode == MM_R0E) NDW(N, MM_R0E, false);           \
-    else NDW(N, MM_ENERGY, false);                            \
-    break;
-    switch (c->nv) { NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8) }
-#undef NV_CASE
-#undef NDW
+    nd_v2_nv<true, true, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
     return true;
   }
   const char* var = getenv("EMIN_NODAL");
-  if (mode == MM_ITER && var && !strcmp(var, "plain")) {
+  if (!var || !strcmp(var, "v2x")) {
+    nd_v2_nv<true, false, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
+    return true;
+  }
+  if (!strcmp(var, "v2cs")) { nd_v2_nv<true, false, 1>(c->nv, mode, v, p, g, X, X2, out, c->partials, s); return true; }
+  if (!strcmp(var, "v2")) { nd_v2_nv<false, false, 1>(c->nv, mode, v, p, g, X, X2, out, c->partials, s); return true; }
+  if (mode == MM_ITER && !strcmp(var, "plain")) {
     switch (c->nv) {
 #define NV_CASE(N) case N: k_spgemm_nodal<N><<<g, 256, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, out, c->partials); break;
       NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
@@ -674,20 +747,7 @@ static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
     }
     return true;
   }
-  const bool v2 = !(var && !strcmp(var, "s"));     // EMIN_NODAL=s: the staged v1 kernel
-  // default per-iteration kernel: v2 with evict-first hints on the streamed
-  // data (A chunk, block records, position bytes, Q, y^), so the L2 keeps the
-  // gathered y rows: config 5 21.89 -> 20.91 ms, config 4 474 -> 478 us
-  // (EMIN_NODAL=v2: without the hints)
-  if (mode == MM_ITER && (!var || !strcmp(var, "v2cs"))) {
-    switch (c->nv) {
-#define NV_CASE(N) case N: k_spgemm_nodal_v2<N, MM_ITER, false, true><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials); break;
-      NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
-#undef NV_CASE
-    }
-    return true;
-  }
-  if (mode == MM_ITER && var && !strcmp(var, "v2p")) {    // branch-free block loop (A/B)
+  if (mode == MM_ITER && !strcmp(var, "v2p")) {    // branch-free block loop (A/B)
     switch (c->nv) {
 #define NV_CASE(N) case N: k_spgemm_nodal_v2<N, MM_ITER, true><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials); break;
       NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
@@ -695,33 +755,28 @@ static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
     }
     return true;
   }
-  if (mode == MM_R0E) {                       // fused r0 + E0: the v2 kernel only
-    if (!v2) return false;
+  if (!strcmp(var, "s")) {                          // the staged v1 kernel
+    if (mode == MM_R0E) return false;               // (no fused r0 + E0 mode)
+#define ND_LAUNCH(N)                                                                                                   \
+  if (mode == MM_ITER)                                                                                                  \
+    k_spgemm_nodal_s<N, MM_ITER><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out,   \
+                                                           c->partials);                                               \
+  else if (mode == MM_R0)                                                                                               \
+    k_spgemm_nodal_s<N, MM_R0><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out,     \
+                                                         c->partials);                                                 \
+  else                                                                                                                  \
+    k_spgemm_nodal_s<N, MM_ENERGY><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, \
+                                                             c->partials);
     switch (c->nv) {
-#define NV_CASE(N) case N: k_spgemm_nodal_v2<N, MM_R0E><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, c->partials); break;
+#define NV_CASE(N) case N: ND_LAUNCH(N) break;
       NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
 #undef NV_CASE
     }
+#undef ND_LAUNCH
     return true;
   }
-#define ND_LAUNCH(KER, N)                                                                                  \
-  if (mode == MM_ITER)                                                                                    \
-    KER<N, MM_ITER><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out,   \
-                                                c->partials);                                             \
-  else if (mode == MM_R0)                                                                                 \
-    KER<N, MM_R0><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out,     \
-                                              c->partials);                                               \
-  else                                                                                                    \
-    KER<N, MM_ENERGY><<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, \
-                                                  c->partials);
-#define NV_CASE(N)                                   \
-  case N:                                            \
-    if (v2) { ND_LAUNCH(k_spgemm_nodal_v2, N) }      \
-    else { ND_LAUNCH(k_spgemm_nodal_s, N) }          \
-    break;
-  switch (c->nv) { NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8) }
-#undef NV_CASE
-#undef ND_LAUNCH
+  // unknown variant name (or plain / v2p outside the iteration): the default
+  nd_v2_nv<true, false, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
   return true;
 }
 
