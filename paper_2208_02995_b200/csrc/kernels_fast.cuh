@@ -180,6 +180,7 @@ __global__ void k_plan_headers(const int64_t* __restrict__ wptr, const int32_t* 
 // window decode derives row starts / lengths from the head bitmask by bit
 // arithmetic (2 shuffles + 1 OR-reduction), the row projection sums q.g
 // through shared memory in a fixed order (no shuffle scan).
+template <int GRP = 1>
 __global__ void __launch_bounds__(256)
 k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict__ rowstart, int64_t nwin,
               const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
@@ -222,8 +223,29 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
       const int4* A4 = reinterpret_cast<const int4*>(A);
       acc = __hiloint2double(__ldg(&A4[qb]).y, __ldg(&A4[qb]).x) * xo;
       const unsigned sh4 = 4u * (unsigned)pos;
+      int q = qb + 1;
+      if (GRP > 1) {
+        // GRP records per round: their gathers are issued before the FMAs
+        // (same ascending order of the sum)
+        for (; q + GRP <= qe; q += GRP) {
+          int4 en[GRP];
+          double y[GRP];
+          bool m[GRP];
+#pragma unroll
+          for (int g = 0; g < GRP; ++g) en[g] = __ldg(&A4[q + g]);
+#pragma unroll
+          for (int g = 0; g < GRP; ++g) {
+            const unsigned s = ((unsigned)en[g].w >> sh4) & 0xFu;
+            m[g] = s != 0xFu;
+            y[g] = m[g] ? X[en[g].z + (int)s] : 0.0;
+          }
+#pragma unroll
+          for (int g = 0; g < GRP; ++g)
+            if (m[g]) acc = fma(__hiloint2double(en[g].y, en[g].x), y[g], acc);
+        }
+      }
 #pragma unroll 4
-      for (int q = qb + 1; q < qe; ++q) {
+      for (; q < qe; ++q) {
         const int4 en = __ldg(&A4[q]);              // one 16-byte load: {a, ybase, pm}
         const unsigned s = ((unsigned)en.w >> sh4) & 0xFu;
         if (s != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)s], acc);
@@ -812,6 +834,10 @@ static inline int select_fast_path(emin_ctx c) {
   if (var && !strcmp(var, "win8")) p.variant = 11;
   if (var && !strcmp(var, "win9")) p.variant = 12;
   if (var && !strcmp(var, "win10")) p.variant = 13;
+  if (var && !strcmp(var, "win2g1")) p.variant = 14;
+  if (var && !strcmp(var, "win2g2")) p.variant = 5;
+  if (var && !strcmp(var, "win2g3")) p.variant = 15;
+  if (var && !strcmp(var, "win2g4")) p.variant = 16;
   if (p.variant == 13) {
     int32_t* dmx = nullptr;
     int32_t hw = 0;
@@ -988,8 +1014,17 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
       case 4:
         k_spgemm_mask<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, p.emask, X, out, c->partials);
         return true;
-      case 5:
-        k_spgemm_win2<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+      case 5:     // default: two records per round (119.1 vs 120.8 us with one, config 3)
+        k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+        return true;
+      case 14:
+        k_spgemm_win2<1><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+        return true;
+      case 15:
+        k_spgemm_win2<3><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+        return true;
+      case 16:
+        k_spgemm_win2<4><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
         return true;
       case 7:
       case 8: {

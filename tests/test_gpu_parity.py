@@ -73,7 +73,7 @@ def test_parity_small(name, size, k):
     assert rep["n_svd_rows"] == o.n_svd and rep["n_frozen_rows"] == o.n_frozen
 
 
-SCALAR_VARIANTS = [("EMIN_SPGEMM", v) for v in ("win", "win2", "win4", "win5", "win6", "win7", "win8", "win9", "win10",
+SCALAR_VARIANTS = [("EMIN_SPGEMM", v) for v in ("win", "win2", "win2g1", "win2g4", "win4", "win5", "win6", "win7", "win8", "win9", "win10",
                                                  "mask", "tile", "hdr", "pipe")] + [("EMIN_SETUP_WIN2M", "1")]
 NODAL_VARIANTS = [("EMIN_NODAL", v) for v in ("v2", "v2p", "v2cs", "v2x", "s", "plain")]
 
