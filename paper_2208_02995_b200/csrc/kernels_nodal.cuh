@@ -464,7 +464,9 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
           const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][min(b + g, cb - 1) * ND2_AST]);
           const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
           const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
-          if (m0[g]) {
+          // PRED: no branches, fma(a, 0, acc) = acc on unmatched positions
+          // (up to the sign of a zero sum)
+          if (PRED || m0[g]) {
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
               acc0[d] = fma(a[d * 3 + 0], y0[g][0], acc0[d]);
@@ -472,7 +474,7 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
               acc0[d] = fma(a[d * 3 + 2], y0[g][2], acc0[d]);
             }
           }
-          if (m1[g]) {
+          if (PRED ? any1 : m1[g]) {
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
               acc1[d] = fma(a[d * 3 + 0], y1[g][0], acc1[d]);
@@ -695,22 +697,22 @@ static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
 // one v2 configuration for every mode: CS = evict-first hints (iteration
 // only), WIDE = chunked staging (> ND_MAXB blocks per node), GRP = blocks per
 // round
-template <int NV, bool CS, bool WIDE, int GRP, int MINB = 4>
+template <int NV, bool CS, bool WIDE, int GRP, int MINB = 4, bool PRED = false>
 static inline void nd_v2(int mode, const DevView& v, const NodalPlan* p, int g, const double* X, const double* X2,
                          double* out, double* partials, cudaStream_t s) {
 #define ND_ARGS <<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, partials)
-  if (mode == MM_ITER) k_spgemm_nodal_v2<NV, MM_ITER, false, CS, WIDE, GRP, MINB> ND_ARGS;
+  if (mode == MM_ITER) k_spgemm_nodal_v2<NV, MM_ITER, PRED, CS, WIDE, GRP, MINB> ND_ARGS;
   else if (mode == MM_R0) k_spgemm_nodal_v2<NV, MM_R0, false, false, WIDE, GRP> ND_ARGS;
   else if (mode == MM_R0E) k_spgemm_nodal_v2<NV, MM_R0E, false, false, WIDE, GRP> ND_ARGS;
   else k_spgemm_nodal_v2<NV, MM_ENERGY, false, false, WIDE, GRP> ND_ARGS;
 #undef ND_ARGS
 }
 
-template <bool CS, bool WIDE, int GRP, int MINB = 4>
+template <bool CS, bool WIDE, int GRP, int MINB = 4, bool PRED = false>
 static inline void nd_v2_nv(int nv, int mode, const DevView& v, const NodalPlan* p, int g, const double* X,
                             const double* X2, double* out, double* partials, cudaStream_t s) {
   switch (nv) {
-#define NV_CASE(N) case N: nd_v2<N, CS, WIDE, GRP, MINB>(mode, v, p, g, X, X2, out, partials, s); break;
+#define NV_CASE(N) case N: nd_v2<N, CS, WIDE, GRP, MINB, PRED>(mode, v, p, g, X, X2, out, partials, s); break;
     NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
 #undef NV_CASE
   }
@@ -737,6 +739,7 @@ static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
     nd_v2_nv<true, false, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
     return true;
   }
+  if (!strcmp(var, "v2xp")) { nd_v2_nv<true, false, 2, 4, true>(c->nv, mode, v, p, g, X, X2, out, c->partials, s); return true; }
   if (!strcmp(var, "v2x3b")) { nd_v2_nv<true, false, 2, 3>(c->nv, mode, v, p, g, X, X2, out, c->partials, s); return true; }
   if (!strcmp(var, "v2cs")) { nd_v2_nv<true, false, 1>(c->nv, mode, v, p, g, X, X2, out, c->partials, s); return true; }
   if (!strcmp(var, "v2")) { nd_v2_nv<false, false, 1>(c->nv, mode, v, p, g, X, X2, out, c->partials, s); return true; }

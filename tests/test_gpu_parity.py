@@ -75,7 +75,7 @@ def test_parity_small(name, size, k):
 
 SCALAR_VARIANTS = [("EMIN_SPGEMM", v) for v in ("win", "win2", "win2g1", "win2g4", "win4", "win5", "win6", "win7", "win8", "win9", "win10",
                                                  "mask", "tile", "hdr", "pipe")] + [("EMIN_SETUP_WIN2M", "1")]
-NODAL_VARIANTS = [("EMIN_NODAL", v) for v in ("v2", "v2p", "v2cs", "v2x", "s", "plain")]
+NODAL_VARIANTS = [("EMIN_NODAL", v) for v in ("v2", "v2p", "v2cs", "v2x", "v2xp", "s", "plain")]
 
 
 @pytest.mark.parametrize("name,size,path", [("3", 12, 1), ("2b", 10, 1), ("3", 17, 1), ("4", 4, 2), ("5", 8, 2)])
