@@ -23,10 +23,18 @@
 
 namespace {
 
-constexpr int PT_WARPS = 1;    // 28 KB of sets per warp (static shared memory <= 48 KB)
+// two tiers of per-warp sets: every node first runs with the small sets (4
+// warps per CTA, ~7.7 KB each -> 32 warps per SM); the nodes whose
+// neighbourhood overflows them are flagged and re-run with the large sets
+// (one warp per CTA, 28 KB).  Static shared memory stays <= 48 KB per CTA.
+constexpr int PT_WARPS = 1;       // large tier
 constexpr int PT_HASH = 2048;     // visited-set slots per warp
 constexpr int PT_FRONT = 1024;    // frontier capacity
 constexpr int PT_CLIST = 1024;    // C nodes reached
+constexpr int PS_WARPS = 4;       // small tier
+constexpr int PS_HASH = 512;
+constexpr int PS_FRONT = 256;
+constexpr int PS_CLIST = 256;
 
 struct PtArgs {
   int64_t nn;                     // nodes (= n / bs)
@@ -42,6 +50,7 @@ struct PtArgs {
   int32_t* col;                   // fill pass output (P_col)
   const int64_t* rowofs;          // [nn * bs + 1] row pointers (fill pass)
   int32_t* overflow;
+  uint8_t* big;                   // [nfn] node overflowed the small sets
 };
 
 // extreme eigenvalues of the symmetric N x N matrix a (row-major, destroyed)
@@ -110,29 +119,35 @@ __device__ bool pt_full_rank_nv(int nv, const double* G) {
   }
 }
 
-template <bool FILL>
-__global__ void __launch_bounds__(PT_WARPS * 32)
+template <bool FILL, bool BIG, int WARPS, int HASH, int FRONT, int CLIST>
+__global__ void __launch_bounds__(WARPS * 32)
 k_pattern(PtArgs a) {
-  __shared__ unsigned long long s_hash[PT_WARPS][PT_HASH];   // (generation << 32) | node
-  __shared__ int32_t s_front[PT_WARPS][2][PT_FRONT];
-  __shared__ int32_t s_cl[PT_WARPS][PT_CLIST];
-  __shared__ int32_t s_n[PT_WARPS][3];                       // frontier size, next size, C count
-  __shared__ double s_G[PT_WARPS][EMIN_NV_MAX * EMIN_NV_MAX];
-  __shared__ int s_ok[PT_WARPS];
+  __shared__ unsigned long long s_hash[WARPS][HASH];   // (generation << 32) | node
+  __shared__ int32_t s_front[WARPS][2][FRONT];
+  __shared__ int32_t s_cl[WARPS][CLIST];
+  __shared__ int32_t s_n[WARPS][3];                       // frontier size, next size, C count
+  __shared__ double s_G[WARPS][EMIN_NV_MAX * EMIN_NV_MAX];
+  __shared__ int s_ok[WARPS];
+  __shared__ int s_ovf[WARPS];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int k = lane; k < PT_HASH; k += 32) s_hash[wib][k] = ~0ull;
+  for (int k = lane; k < HASH; k += 32) s_hash[wib][k] = ~0ull;
   __syncwarp();
   const int nv = a.nv, bs = a.bs;
+  // small tier: an overflow flags the node (re-run by the large tier);
+  // large tier: only flagged nodes, an overflow is an error
+  auto overflow = [&]() { if (BIG) atomicExch(a.overflow, 1); else s_ovf[wib] = 1; };
   for (int64_t f = gw; f < a.nfn; f += nw) {
+    if (BIG ? !a.big[f] : (FILL && a.big[f])) continue;     // warp-uniform
+    if (lane == 0) s_ovf[wib] = 0;
     const unsigned long long gen = (unsigned long long)(f + 1) << 32;   // this node's tag (never ~0)
     const int32_t I = (int32_t)a.fnode[f];
     auto insert = [&](int32_t w) -> bool {      // true if w was not yet visited for this node
-      unsigned h = ((unsigned)w * 2654435761u) & (PT_HASH - 1);
+      unsigned h = ((unsigned)w * 2654435761u) & (HASH - 1);
       const unsigned long long key = gen | (unsigned)w;
-      for (int probe = 0; probe < PT_HASH; ++probe) {
+      for (int probe = 0; probe < HASH; ++probe) {
         const unsigned long long cur = s_hash[wib][h];
         if (cur == key) return false;
         if ((cur >> 32) != (gen >> 32)) {      // stale or empty slot: claim it
@@ -141,9 +156,9 @@ k_pattern(PtArgs a) {
           if (prev == key) return false;
           continue;                            // lost the race to another key: re-read
         }
-        h = (h + 1) & (PT_HASH - 1);
+        h = (h + 1) & (HASH - 1);
       }
-      atomicExch(a.overflow, 1);
+      overflow();
       return false;
     };
     // s_cl[0 .. ncl) ascending (the coarse ids are distinct: rank = position)
@@ -173,25 +188,29 @@ k_pattern(PtArgs a) {
       const int nf = s_n[wib][0];
       for (int x = lane; x < nf; x += 32) {
         const int64_t r = (int64_t)s_front[wib][cur][x] * bs;
+        int32_t prevw = -1;
         for (int64_t q = a.Arp[r]; q < a.Arp[r + 1]; ++q) {
           const int32_t w = a.Acol[q] / bs;
+          if (w == prevw) continue;               // the other dofs of the same node (3x3 blocks)
+          prevw = w;
           if (!insert(w)) continue;
           const int pos = atomicAdd(&s_n[wib][1], 1);
-          if (pos < PT_FRONT) s_front[wib][cur ^ 1][pos] = w; else atomicExch(a.overflow, 1);
+          if (pos < FRONT) s_front[wib][cur ^ 1][pos] = w; else overflow();
           const int64_t c = a.cid[w];
           if (c >= 0) {
             const int cp = atomicAdd(&s_n[wib][2], 1);
-            if (cp < PT_CLIST) s_cl[wib][cp] = (int32_t)c; else atomicExch(a.overflow, 1);
+            if (cp < CLIST) s_cl[wib][cp] = (int32_t)c; else overflow();
           }
         }
       }
       __syncwarp();
-      if (lane == 0) s_n[wib][0] = min(s_n[wib][1], PT_FRONT);
+      if (lane == 0) s_n[wib][0] = min(s_n[wib][1], FRONT);
       cur ^= 1;
       __syncwarp();
       if (l < a.l0) continue;
       if (l == a.lmax) break;
-      const int ncl = min(s_n[wib][2], PT_CLIST);
+      if (!BIG && s_ovf[wib]) break;          // flagged: the large tier redoes this node
+      const int ncl = min(s_n[wib][2], CLIST);
       if (ncl == 0) continue;
       sort_clist(ncl, s_front[wib][cur ^ 1]);   // deterministic Gram summation order
       // Gram matrix of M = V_c(J,:), J = the dofs of the C nodes reached
@@ -211,7 +230,13 @@ k_pattern(PtArgs a) {
       __syncwarp();
       if (s_ok[wib]) break;
     }
-    const int ncl = min(s_n[wib][2], PT_CLIST);
+    __syncwarp();
+    if (!BIG && s_ovf[wib]) {                   // (count pass only: fill skips flagged nodes)
+      if (lane == 0) a.big[f] = 1;
+      __syncwarp();
+      continue;
+    }
+    const int ncl = min(s_n[wib][2], CLIST);
     if (!FILL) {
       if (lane == 0) a.cnt[f] = ncl;
     } else {
@@ -333,8 +358,16 @@ extern "C" emin_status emin_pattern(int64_t n, const int64_t* A_rowptr, const in
   pa.nn = nn; pa.bs = bs; pa.nv = nv; pa.l0 = l0; pa.lmax = lmax;
   pa.Arp = dArp; pa.Acol = dAcol; pa.cid = cid; pa.Bc = dBc; pa.fnode = fnode; pa.nfn = nfn;
   pa.cnt = cnt; pa.colofs = nullptr; pa.col = nullptr; pa.rowofs = nullptr; pa.overflow = ovf;
+  uint8_t* big;
+  PT_TRY(dal((void**)&big, std::max<int64_t>(nfn, 1)));
+  PT_TRY(cudaMemsetAsync(big, 0, std::max<int64_t>(nfn, 1), s));
+  pa.big = big;
+  const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((nfn + PS_WARPS - 1) / PS_WARPS, (int64_t)SM * 8));
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nfn + PT_WARPS - 1) / PT_WARPS, (int64_t)SM * 8));
-  if (nfn) k_pattern<false><<<g, PT_WARPS * 32, 0, s>>>(pa);
+  if (nfn) {
+    k_pattern<false, false, PS_WARPS, PS_HASH, PS_FRONT, PS_CLIST><<<gs, PS_WARPS * 32, 0, s>>>(pa);
+    k_pattern<false, true, PT_WARPS, PT_HASH, PT_FRONT, PT_CLIST><<<g, PT_WARPS * 32, 0, s>>>(pa);
+  }
   k_pt_rowlen<<<SM * 4, 256, 0, s>>>(nn, bs, cid, fpos, cnt, rowlen);
   PT_TRY(emin_scan_i64(rowlen, rowofs, n, tot + 1, scratch, s));
   PT_TRY(cudaMemcpyAsync(rowofs + n, tot + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
@@ -353,7 +386,10 @@ extern "C" emin_status emin_pattern(int64_t n, const int64_t* A_rowptr, const in
     if (!inputs_on_device) PT_TRY(dal((void**)&dcol, sizeof(int32_t) * std::max<int64_t>(h_nnz, 1)));
     pa.col = dcol;
     pa.rowofs = rowofs;
-    if (nfn) k_pattern<true><<<g, PT_WARPS * 32, 0, s>>>(pa);
+    if (nfn) {
+      k_pattern<true, false, PS_WARPS, PS_HASH, PS_FRONT, PS_CLIST><<<gs, PS_WARPS * 32, 0, s>>>(pa);
+      k_pattern<true, true, PT_WARPS, PT_HASH, PT_FRONT, PT_CLIST><<<g, PT_WARPS * 32, 0, s>>>(pa);
+    }
     k_pt_crows<<<SM * 4, 256, 0, s>>>(nn, bs, cid, rowofs, dcol);
     if (!inputs_on_device) PT_TRY(cudaMemcpyAsync(P_col, dcol, sizeof(int32_t) * h_nnz, cudaMemcpyDeviceToHost, s));
   }
