@@ -227,6 +227,11 @@ emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_rowptr, const 
                           const double* P_val, int64_t* Ac_rowptr, int32_t* Ac_col, double* Ac_val,
                           int64_t Ac_cap, int64_t* nnz_out, int32_t inputs_on_device, void* stream);
 const char* emin_galerkin_error(void);
+/* Which product the last emin_galerkin call of this thread used: 1 = the 3x3
+ * block path (A in full 3x3 node blocks, P blockwise on F nodes and the
+ * identity on C nodes -- the elasticity structure; same sums, bitwise), 0 =
+ * the point path. */
+int32_t emin_galerkin_path(void);
 
 /* Multi-GPU helpers (one process per GPU, NCCL over NVLink/NVSwitch).
  * emin_nccl_unique_id fills id[128] on one rank; the caller broadcasts it

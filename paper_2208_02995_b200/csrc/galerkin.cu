@@ -255,6 +255,8 @@ cudaError_t gk_launch(bool numeric, const GkArgs& a, int SM, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+#include "galerkin_bsr.cuh"
+
 // every tier in order (symbolic: tier t > 0 re-counts the rows tier t - 1 overflowed)
 cudaError_t gk_launch_all(bool numeric, const GkArgs& a, int SM, cudaStream_t s) {
   cudaError_t e = gk_launch<0>(numeric, a, SM, s);
@@ -267,12 +269,14 @@ cudaError_t gk_launch_all(bool numeric, const GkArgs& a, int SM, cudaStream_t s)
 }  // namespace
 
 static thread_local std::string g_galerkin_error;
+static thread_local int32_t g_galerkin_path = 0;
 
 extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_rowptr, const int32_t* A_col,
                                      const double* A_val, const int64_t* P_rowptr, const int32_t* P_col,
                                      const double* P_val, int64_t* Ac_rowptr, int32_t* Ac_col, double* Ac_val,
                                      int64_t Ac_cap, int64_t* nnz_out, int32_t inputs_on_device, void* stream) {
   g_galerkin_error.clear();
+  g_galerkin_path = 0;
   if (n <= 0 || nc <= 0 || n >= INT32_MAX || nc >= INT32_MAX || !A_rowptr || !A_col || !A_val || !P_rowptr ||
       !P_col || !P_val || !Ac_rowptr || !nnz_out || (Ac_col && !Ac_val)) {
     g_galerkin_error = "bad argument";
@@ -334,6 +338,111 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
   GK_TRY(cudaMemcpyAsync(&h_err, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   GK_TRY(cudaStreamSynchronize(s));
   if (h_err) return done(EMIN_ERR_CSR, "row pointers decrease or column ids out of range");
+
+  // ---- 3x3-block path (elasticity-structured A and P; same sums, bitwise)
+  if (!getenv("EMIN_GALERKIN_POINT") && n % 3 == 0 && nc % 3 == 0) {
+    const int64_t nn = n / 3, nnc = nc / 3;
+    GK_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
+    k_bsr_check<<<G, 256, 0, s>>>(nn, dArp, dAcol, dPrp, dPcol, err);
+    GK_TRY(cudaMemcpyAsync(&h_err, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    GK_TRY(cudaStreamSynchronize(s));
+    if (!h_err) {
+      auto sync_err = [&]() -> int32_t {
+        int32_t h = 0;
+        cudaMemcpyAsync(&h, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        return h;
+      };
+      // T = A P (BSR)
+      BsrAP opT{dArp, dAcol, dAval, dPrp, dPcol, dPval};
+      int64_t *cntT, *Tnp, nbT = 0;
+      GK_TRY(dal((void**)&cntT, sizeof(int64_t) * (nn + 1)));
+      GK_TRY(dal((void**)&Tnp, sizeof(int64_t) * (nn + 1)));
+      BsrOut oT{};
+      oT.nrows = nn; oT.cnt = cntT; oT.err = err;
+      GK_TRY((bs_launch_all<0>(false, opT, oT, SM, s)));
+      if (sync_err()) return done(EMIN_ERR_ARG, "A P: a node row wider than 1024 node columns");
+      GK_TRY(emin_scan_i64(cntT, Tnp, nn, tot, scratch, s));
+      GK_TRY(cudaMemcpyAsync(Tnp + nn, tot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+      GK_TRY(cudaMemcpyAsync(&nbT, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      GK_TRY(cudaStreamSynchronize(s));
+      int32_t* Tnc;
+      double* Tv;
+      if (dal((void**)&Tnc, sizeof(int32_t) * std::max<int64_t>(nbT, 1)) != cudaSuccess ||
+          dal((void**)&Tv, sizeof(double) * 9 * std::max<int64_t>(nbT, 1)) != cudaSuccess)
+        return done(EMIN_ERR_OOM, "A P: out of memory");
+      oT.Onp = Tnp; oT.Onc = Tnc; oT.Ov = Tv;
+      GK_TRY((bs_launch_all<0>(true, opT, oT, SM, s)));
+      // P^T at node level: (c, I) entries sorted, with the position s of c in J_I
+      int64_t *nlen, *nofs, *ccount, *Ptnp, M = 0;
+      GK_TRY(dal((void**)&nlen, sizeof(int64_t) * (nn + 1)));
+      GK_TRY(dal((void**)&nofs, sizeof(int64_t) * (nn + 1)));
+      GK_TRY(dal((void**)&ccount, sizeof(int64_t) * (nnc + 1)));
+      GK_TRY(dal((void**)&Ptnp, sizeof(int64_t) * (nnc + 1)));
+      k_bsr_nodelen<<<G, 256, 0, s>>>(nn, dPrp, nlen);
+      GK_TRY(emin_scan_i64(nlen, nofs, nn, tot + 1, scratch, s));
+      GK_TRY(cudaMemcpyAsync(&M, tot + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      GK_TRY(cudaStreamSynchronize(s));
+      if (M >= INT32_MAX) return done(EMIN_ERR_ARG, "P: too many node entries");
+      uint64_t *kin, *kout;
+      int32_t *sin, *sout, *PtI;
+      GK_TRY(dal((void**)&kin, sizeof(uint64_t) * std::max<int64_t>(M, 1)));
+      GK_TRY(dal((void**)&kout, sizeof(uint64_t) * std::max<int64_t>(M, 1)));
+      GK_TRY(dal((void**)&sin, sizeof(int32_t) * std::max<int64_t>(M, 1)));
+      GK_TRY(dal((void**)&sout, sizeof(int32_t) * std::max<int64_t>(M, 1)));
+      GK_TRY(dal((void**)&PtI, sizeof(int32_t) * std::max<int64_t>(M, 1)));
+      GK_TRY(cudaMemsetAsync(ccount, 0, sizeof(int64_t) * (nnc + 1), s));
+      k_bsr_tkeys<<<G, 256, 0, s>>>(nn, dPrp, dPcol, nofs, kin, sin, ccount);
+      int eb = 1;
+      while (eb < 64 && (((unsigned __int128)1) << eb) < (unsigned __int128)nnc * (unsigned __int128)nn) ++eb;
+      size_t tb = 0;
+      GK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, sin, sout, (int)M, 0, eb, s));
+      void* ct;
+      GK_TRY(dal(&ct, tb));
+      GK_TRY(cub::DeviceRadixSort::SortPairs(ct, tb, kin, kout, sin, sout, (int)M, 0, eb, s));
+      k_bsr_trows<<<G, 256, 0, s>>>(M, nn, kout, PtI);
+      GK_TRY(emin_scan_i64(ccount, Ptnp, nnc, tot + 1, scratch, s));
+      GK_TRY(cudaMemcpyAsync(Ptnp + nnc, tot + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+      // A_c = P^T T: node counts, point row pointers, values
+      BsrPtT opC{Ptnp, PtI, sout, dPrp, dPval, Tnp, Tnc, Tv};
+      int64_t *cntC, *nbC, NB = 0;
+      GK_TRY(dal((void**)&cntC, sizeof(int64_t) * (nnc + 1)));
+      GK_TRY(dal((void**)&nbC, sizeof(int64_t) * (nnc + 1)));
+      BsrOut oC{};
+      oC.nrows = nnc; oC.cnt = cntC; oC.err = err;
+      GK_TRY((bs_launch_all<1>(false, opC, oC, SM, s)));
+      if (sync_err()) return done(EMIN_ERR_ARG, "P^T (A P): a node row wider than 1024 node columns");
+      GK_TRY(emin_scan_i64(cntC, nbC, nnc, tot, scratch, s));
+      GK_TRY(cudaMemcpyAsync(&NB, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      int64_t* Crp = Ac_rowptr;
+      if (!inputs_on_device) GK_TRY(dal((void**)&Crp, sizeof(int64_t) * (nc + 1)));
+      k_bsr_crp<<<G, 256, 0, s>>>(nnc, nbC, cntC, Crp);
+      GK_TRY(cudaStreamSynchronize(s));
+      const int64_t nnzC = 9 * NB;
+      *nnz_out = nnzC;
+      if (!inputs_on_device)
+        GK_TRY(cudaMemcpyAsync(Ac_rowptr, Crp, sizeof(int64_t) * (nc + 1), cudaMemcpyDeviceToHost, s));
+      if (Ac_col) {
+        if (Ac_cap < nnzC) return done(EMIN_ERR_ARG, "Ac_cap < nnz (call again with a larger buffer)");
+        int32_t* Ccol = Ac_col;
+        double* Cval = Ac_val;
+        if (!inputs_on_device) {
+          GK_TRY(dal((void**)&Ccol, sizeof(int32_t) * std::max<int64_t>(nnzC, 1)));
+          GK_TRY(dal((void**)&Cval, sizeof(double) * std::max<int64_t>(nnzC, 1)));
+        }
+        oC.Crp = Crp; oC.Ccol = Ccol; oC.Cval = Cval;
+        GK_TRY((bs_launch_all<1>(true, opC, oC, SM, s)));
+        if (!inputs_on_device) {
+          GK_TRY(cudaMemcpyAsync(Ac_col, Ccol, sizeof(int32_t) * nnzC, cudaMemcpyDeviceToHost, s));
+          GK_TRY(cudaMemcpyAsync(Ac_val, Cval, sizeof(double) * nnzC, cudaMemcpyDeviceToHost, s));
+        }
+      }
+      GK_TRY(cudaGetLastError());
+      g_galerkin_path = 1;
+      return done(EMIN_OK, nullptr);
+    }
+    GK_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
+  }
 
   // one product X * Y -> O (symbolic, row pointers, numeric)
   auto product = [&](int64_t nrows, const int64_t* Xrp, const int32_t* Xcol, const double* Xval,
@@ -432,3 +541,4 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
 }
 
 extern "C" const char* emin_galerkin_error() { return g_galerkin_error.c_str(); }
+extern "C" int32_t emin_galerkin_path() { return g_galerkin_path; }

@@ -61,7 +61,7 @@ EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "e
             "emin_reset", "emin_report", "emin_destroy", "emin_status_str", "emin_last_error",
             "emin_set_profiling", "emin_kernel_times", "emin_get_layout", "emin_nccl_unique_id",
             "emin_nccl_comm_init", "emin_nccl_comm_destroy", "emin_pattern", "emin_pattern_error",
-            "emin_galerkin", "emin_galerkin_error"]
+            "emin_galerkin", "emin_galerkin_error", "emin_galerkin_path"]
 
 
 def load_library():
@@ -116,6 +116,8 @@ def load_library():
     lib.emin_galerkin.restype = i32
     lib.emin_galerkin_error.argtypes = []
     lib.emin_galerkin_error.restype = C.c_char_p
+    lib.emin_galerkin_path.argtypes = []
+    lib.emin_galerkin_path.restype = i32
     _lib = lib
     return lib
 

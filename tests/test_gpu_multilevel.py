@@ -62,6 +62,25 @@ def test_galerkin_bitwise_matches_oracle(name, size, k, device):
     _assert_bitwise(got, want)
 
 
+@pytest.mark.parametrize("name,size", [("4", 4), ("4", 7), ("5", 5)])
+def test_galerkin_block_path_equals_point_path(name, size, monkeypatch):
+    # elasticity inputs take the 3x3-block product; it must give the point
+    # path's (and the oracle's) bits
+    import torch
+    from paper_2208_02995_b200.emin import emin_galerkin, load_library
+    from workloads.problems import make_config
+    p = make_config(name, size)
+    Pv = _oracle_P(p, 3)
+    args = [torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            for a in (p.A_rowptr, p.A_col, p.A_val, p.P_rowptr, p.P_col, Pv)]
+    blk = [t.cpu().numpy() for t in emin_galerkin(p.n, p.nc, *args)]
+    assert load_library().emin_galerkin_path() == 1
+    monkeypatch.setenv("EMIN_GALERKIN_POINT", "1")
+    pt = [t.cpu().numpy() for t in emin_galerkin(p.n, p.nc, *args)]
+    assert load_library().emin_galerkin_path() == 0
+    _assert_bitwise(blk, pt)
+
+
 def _csr(D):
     rp = np.zeros(D.shape[0] + 1, np.int64)
     cols, vals = [], []
