@@ -422,6 +422,17 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
     const int cb = WIDE ? min(ND_MAXB, nb - c0) : nb, cs = 3 * cb;
     if (WIDE && c0) __syncwarp();
     // ---- stage the node's data (A chunk re-ordered block-major, 10-double stride)
+    if (GRP > 1) {
+      // row by row: no division by the (variable) row length
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double* srow = v.affval + ab + (int64_t)d * rs + 3 * c0;
+        for (int j = lane; j < cs; j += 32) {
+          const int b = j / 3, e = j - 3 * b;
+          s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(srow + j) : __ldg(srow + j);
+        }
+      }
+    } else
     for (int k = lane; k < 9 * cb; k += 32) {
       const int d = k / cs, rem = k - d * cs, b = rem / 3, e = rem - 3 * b;
       const int64_t src = WIDE ? ab + (int64_t)d * rs + 3 * c0 + rem : ab + k;
