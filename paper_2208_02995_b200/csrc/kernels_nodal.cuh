@@ -58,7 +58,8 @@ __global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_l
       for (int d = 1; d < 3 && good; ++d) good = v.affcol[v.affptr[r + d] + q] == k;
     }
     if (!good) atomicExch(ok, 0);
-    pm_len[n] = good ? (alen / 3) * (len / 3) : 0;
+    // (each node's byte map starts 16-byte aligned: staged with 16-byte loads)
+    pm_len[n] = good ? (((alen / 3) * (len / 3) + 15) & ~(int64_t)15) : 0;
   }
 }
 
@@ -390,7 +391,7 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
   __shared__ double sh[32];
   __shared__ __align__(16) double s_a[ND_WARPS][ND_MAXB * ND2_AST];
   __shared__ NodalBlk s_b[ND_WARPS][ND_MAXB];
-  __shared__ uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
+  __shared__ __align__(16) uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
   __shared__ __align__(16) double s_dot[ND_WARPS][3 * NV + 1];
   if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
@@ -442,6 +443,12 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
       if (CS) { const int2 t = __ldcs(reinterpret_cast<const int2*>(blk + bb + c0 + k)); s_b[wib][k] = NodalBlk{t.x, t.y}; }
       else s_b[wib][k] = blk[bb + c0 + k];
     }
+    if (GRP > 1 && !WIDE) {
+      // 16-byte loads (the node's map is 16-byte aligned, padded)
+      const uint4* src4 = reinterpret_cast<const uint4*>(pm8 + po);
+      uint4* dst4 = reinterpret_cast<uint4*>(&s_pm[wib][0]);
+      for (int k = lane; k < ((cb * nJ + 15) >> 4); k += 32) dst4[k] = CS ? __ldcs(src4 + k) : src4[k];
+    } else
     for (int k = lane; k < cb * nJ; k += 32) {
       const int64_t src = po + (int64_t)c0 * nJ + k;
       s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + src)) : pm8[src];

@@ -324,7 +324,7 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
   constexpr int MAXB = 27, MAXJ = 32, AST = 10;   // the nodal plan's limits (k_nodal_check)
   __shared__ __align__(16) double s_a[8][MAXB * AST];
   __shared__ int2 s_b[8][MAXB];
-  __shared__ uint8_t s_pm[8][MAXB * MAXJ];
+  __shared__ __align__(16) uint8_t s_pm[8][MAXB * MAXJ];
   __shared__ uint8_t s_dir[8][MAXB];
   const DevState* st = v.st;
   if (st->stopped) return;
@@ -356,7 +356,11 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
       s_a[wib][bk * AST + d * 3 + e] = __ldg(v.affval + ab + k);
     }
     for (int k = lane; k < nb; k += 32) { s_b[wib][k] = __ldg(blk + bb + k); s_dir[wib][k] = bdir[bb + k]; }
-    for (int k = lane; k < nb * nJ; k += 32) s_pm[wib][k] = pm[k];
+    {   // the node's byte map is 16-byte aligned and padded (k_nodal_check)
+      const uint4* src4 = reinterpret_cast<const uint4*>(pm);
+      uint4* dst4 = reinterpret_cast<uint4*>(&s_pm[wib][0]);
+      for (int k = lane; k < ((nb * nJ + 15) >> 4); k += 32) dst4[k] = src4[k];
+    }
     double acc0[3], acc1[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
