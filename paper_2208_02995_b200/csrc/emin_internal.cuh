@@ -270,4 +270,4 @@ int64_t emin_sgs_levels(emin_ctx c);
 const int4* emin_scalar_records(emin_ctx c);   // iterate.cu
 const int32_t* emin_scalar_windows(emin_ctx c, int64_t* nwin);
 bool emin_nodal_plan(emin_ctx c, const int2** blk, const int64_t** bptr, const uint8_t** pm8,
-                     const int64_t** pmoff, int64_t* nFn);
+                     const int64_t** pmoff, int64_t* nFn, int32_t* max_nb);

@@ -544,10 +544,10 @@ const int4* emin_scalar_records(emin_ctx c) {
 // with records {wptr[3K], 3|J_K|} and the byte map pm8 + pmoff[n] (position of
 // J_I[s] in J_K per block, 0xFF absent); false off the nodal path
 bool emin_nodal_plan(emin_ctx c, const int2** blk, const int64_t** bptr, const uint8_t** pm8,
-                     const int64_t** pmoff, int64_t* nFn) {
+                     const int64_t** pmoff, int64_t* nFn, int32_t* max_nb) {
   if (c->kernel_path != 2 || !c->nodal) return false;
   const NodalPlan* np = static_cast<const NodalPlan*>(c->nodal);
-  if (np->max_nb > ND_MAXB) return false;      // the SGS nodal sweeps stage <= ND_MAXB blocks
+  *max_nb = np->max_nb;
   *blk = reinterpret_cast<const int2*>(np->blk);
   *bptr = np->bptr;
   *pm8 = np->pm8;

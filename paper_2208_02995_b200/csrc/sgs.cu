@@ -51,6 +51,7 @@ struct SgsPlan {
   const uint8_t* pm8 = nullptr;
   const int64_t* pmoff = nullptr;
   int64_t nFn = 0;
+  int32_t max_nb = 0;            // > 27: Galerkin level, sweeps stage the blocks in chunks
   uint8_t* bdir = nullptr;       // [nblk] 0 own node, 1 predecessor node, 2 successor node
 };
 
@@ -312,7 +313,7 @@ __global__ void k_sgs_node_levels(DevView v, int64_t nFn, const int64_t* __restr
 // (the own-node terms come last, after the other blocks in A's column
 // order; the oracle adds them at their column position -- a rounding-order
 // difference only).
-template <bool FWD, bool EDGE = false, bool TOP = false>
+template <bool FWD, bool EDGE = false, bool TOP = false, bool WIDE = false>
 __global__ void __launch_bounds__(256, 4)
 k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
@@ -350,17 +351,6 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
     const int nb = (int)(bptr[n + 1] - bb);
     const int rs = 3 * nb;
     const uint8_t* pm = pm8 + pmoff[n];
-    __syncwarp();
-    for (int k = lane; k < 9 * nb; k += 32) {
-      const int d = k / rs, rem = k - d * rs, bk = rem / 3, e = rem - 3 * bk;
-      s_a[wib][bk * AST + d * 3 + e] = __ldg(v.affval + ab + k);
-    }
-    for (int k = lane; k < nb; k += 32) { s_b[wib][k] = __ldg(blk + bb + k); s_dir[wib][k] = bdir[bb + k]; }
-    {   // the node's byte map is 16-byte aligned and padded (k_nodal_check)
-      const uint4* src4 = reinterpret_cast<const uint4*>(pm);
-      uint4* dst4 = reinterpret_cast<uint4*>(&s_pm[wib][0]);
-      for (int k = lane; k < ((nb * nJ + 15) >> 4); k += 32) dst4[k] = src4[k];
-    }
     double acc0[3], acc1[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -377,15 +367,34 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
       acc0[d] = x0;
       acc1[d] = x1;
     }
+    double own[9];
+    // nodes with more than MAXB blocks (Galerkin levels, NEXT-4; template
+    // WIDE) are staged MAXB blocks at a time, in the same block order
+    for (int cl = 0; cl < nb; cl += WIDE ? MAXB : nb) {
+    const int c0 = WIDE ? cl : 0;
+    const int cb = WIDE ? min(MAXB, nb - c0) : nb, cs = 3 * cb;
+    __syncwarp();
+    for (int k = lane; k < 9 * cb; k += 32) {
+      const int d = k / cs, rem = k - d * cs, bk = rem / 3, e = rem - 3 * bk;
+      const int64_t src = WIDE ? ab + (int64_t)d * rs + 3 * c0 + rem : ab + k;
+      s_a[wib][bk * AST + d * 3 + e] = __ldg(v.affval + src);
+    }
+    for (int k = lane; k < cb; k += 32) { s_b[wib][k] = __ldg(blk + bb + c0 + k); s_dir[wib][k] = bdir[bb + c0 + k]; }
+    if (!WIDE) {   // the node's byte map is 16-byte aligned and padded (k_nodal_check)
+      const uint4* src4 = reinterpret_cast<const uint4*>(pm);
+      uint4* dst4 = reinterpret_cast<uint4*>(&s_pm[wib][0]);
+      for (int k = lane; k < ((nb * nJ + 15) >> 4); k += 32) dst4[k] = src4[k];
+    } else {
+      for (int k = lane; k < cb * nJ; k += 32) s_pm[wib][k] = pm[(int64_t)c0 * nJ + k];
+    }
     __syncwarp();
     // the node's own block, and the coupled blocks (predecessor nodes in
     // the forward sweep, successors in the backward one) as a bit mask in
-    // ascending block order (nb <= 27 < 32 lanes)
-    const uint8_t dl = lane < nb ? s_dir[wib][lane] : 3;
+    // ascending block order (cb <= 27 < 32 lanes)
+    const uint8_t dl = lane < cb ? s_dir[wib][lane] : 3;
     const unsigned ownm = __ballot_sync(0xffffffffu, dl == 0);
     unsigned cm = EDGE ? 0u : __ballot_sync(0xffffffffu, dl == want);
-    double own[9];
-    {
+    if (ownm) {
       const int bo = __ffs(ownm) - 1;
       const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][bo * AST]);
       const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
@@ -470,6 +479,7 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
         }
       }
     }
+    }  // chunks
     double o0[3], o1[3];
     if (FWD) {
 #pragma unroll
@@ -690,7 +700,7 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   // nodal path with node-constant keys: levels, buckets and sweeps per F node
   int64_t nunits = nF;                               // rows, or nodes on the nodal path
   if (!getenv("EMIN_SGS_GENERIC") &&
-      emin_nodal_plan(c, &p->nblk, &p->bptr, &p->pm8, &p->pmoff, &p->nFn)) {
+      emin_nodal_plan(c, &p->nblk, &p->bptr, &p->pm8, &p->pmoff, &p->nFn, &p->max_nb)) {
     int32_t hb = 0;
     EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
     k_sgs_node_key_ok<<<SM * 4, 256, 0, s>>>(p->nFn, p->key, flag);
@@ -801,16 +811,25 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
       const int32_t* rows = p->lvl_rows + p->lvl_ptr[L];
       const bool first = L == 0, top = L == p->nlev - 1;
-#define NDF(E, T) k_sgs_sweep_nodal<true, E, T><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, \
-                                                                           p->bdir, rows, (int32_t)n, c->r, c->yb, p->u)
-      if (first && top) NDF(true, true); else if (first) NDF(true, false); else if (top) NDF(false, true);
-      else NDF(false, false);
+#define NDF(E, T, W) k_sgs_sweep_nodal<true, E, T, W><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, \
+                                                                     p->pmoff, p->bdir, rows, (int32_t)n, c->r, c->yb, p->u)
+      if (p->max_nb > 27) {
+        if (first && top) NDF(true, true, true); else if (first) NDF(true, false, true);
+        else if (top) NDF(false, true, true); else NDF(false, false, true);
+      } else {
+        if (first && top) NDF(true, true, false); else if (first) NDF(true, false, false);
+        else if (top) NDF(false, true, false); else NDF(false, false, false);
+      }
 #undef NDF
     }
     for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
-      k_sgs_sweep_nodal<false><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
-                                                          p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
+      if (p->max_nb > 27)
+        k_sgs_sweep_nodal<false, false, false, true><<<grid_for(n), 256, 0, s>>>(
+            v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
+      else
+        k_sgs_sweep_nodal<false><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
+                                                            p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
     }
     const int g = grid_for(p->nFn);
     switch (c->nv) {

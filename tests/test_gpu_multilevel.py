@@ -188,6 +188,33 @@ def test_multilevel_matches_oracle(name, size, nlev, iters):
             assert g["kernel_path"] == 2
 
 
+def test_sgs_on_a_galerkin_level_matches_oracle():
+    # projected SGS on the elasticity level-2 operator (up to 125 blocks per
+    # node: the nodal sweeps stage them in chunks of 27)
+    from oracle import Oracle, galerkin, pattern
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import coarse_problem, make_config, sgs_key
+    p = make_config("4", 8)
+    o = Oracle(p)
+    o.iterate(5)
+    Ac = galerkin(p.n, p.nc, p.A_rowptr, p.A_col, p.A_val, p.P_rowptr, p.P_col, o.get_P())
+    p2 = coarse_problem(p, *Ac, iters=8)
+    p2.P_rowptr, p2.P_col, _ = pattern(p2, l0=1, lmax=4)
+    for kind in ("color", "natural"):
+        key = sgs_key(p2, kind)
+        g = Emin.from_problem(p2, device="cuda", precond="sgs", sgs_key=key)
+        assert g.report()["kernel_path"] == 2
+        o2 = Oracle(p2, precond="sgs", sgs_key=key)
+        kd, _ = g.iterate(8)
+        kdo, _ = o2.iterate(8)
+        assert kd == kdo
+        E, Eo = g.energy(), o2.energy()
+        assert abs(E - Eo) <= E_TOL * abs(Eo)
+        P, Po = g.get_P(), o2.get_P()
+        assert np.abs(P - Po).max() <= P_TOL * np.abs(Po).max()
+        g.close()
+
+
 def test_galerkin_full_size_config3_bitwise():
     # BASELINE config 3 at full size (2.1M rows, 40 oracle iterations would
     # take minutes: 3 here) -- the production sizes of T and A_c
