@@ -198,7 +198,8 @@ template <int MAXC>
 __global__ void __launch_bounds__(128)
 k_alg2(DevView v, const double* __restrict__ Bc, const double* __restrict__ B,
        const int64_t* __restrict__ frow, const double* __restrict__ what, double tol,
-       double* __restrict__ Qout, double* __restrict__ w0, unsigned long long* counters) {
+       double* __restrict__ Qout, double* __restrict__ w0, unsigned long long* counters,
+       const uint8_t* __restrict__ only = nullptr) {
   __shared__ double Rs[4][EMIN_NV_MAX][EMIN_NV_MAX];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -207,6 +208,7 @@ k_alg2(DevView v, const double* __restrict__ Bc, const double* __restrict__ B,
   const int nv = v.nv;
   double (*R)[EMIN_NV_MAX] = Rs[wib];
   for (int64_t i = gw; i < v.nF; i += nw) {
+    if (only && !only[i / 3]) continue;          // (node-level fallback: flagged nodes only)
     const int64_t b = v.wptr[i];
     const int nj = (int)(v.wptr[i + 1] - b);
     const int64_t rl = frow[i];
@@ -423,6 +425,145 @@ k_alg2(DevView v, const double* __restrict__ Bc, const double* __restrict__ B,
       if (nj == krank) atomicAdd(counters + 1, 1ull);
     }
     __syncwarp();
+  }
+}
+
+// Alg. 2 on the nodal path: the 3 rows of an F node share J, hence M = B_c(J,:)
+// and its QR; one warp per node factors M once (the same CGS2 operations as
+// k_alg2, so Q and R are bitwise the per-row ones) and solves the 3 right-hand
+// sides.  Nodes whose QR is rank deficient are flagged and redone row by row
+// by k_alg2 (SVD branch).
+template <int MAXC>
+__global__ void __launch_bounds__(128)
+k_alg2_nodal(DevView v, const double* __restrict__ Bc, const double* __restrict__ B,
+             const int64_t* __restrict__ frow, const double* __restrict__ what, double tol,
+             double* __restrict__ Qout, double* __restrict__ w0, unsigned long long* counters,
+             uint8_t* __restrict__ flag) {
+  __shared__ double Rs[4][EMIN_NV_MAX][EMIN_NV_MAX];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nv = v.nv;
+  double (*R)[EMIN_NV_MAX] = Rs[wib];
+  unsigned long long frozen = 0, nflag = 0;
+  for (int64_t nd = gw; nd < v.nF / 3; nd += nw) {
+    const int64_t i0 = 3 * nd;
+    const int64_t b0 = v.wptr[i0];
+    const int nj = (int)(v.wptr[i0 + 1] - b0);
+    int32_t jj[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int t = lane + 32 * c;
+      jj[c] = (t < nj) ? v.wcol[b0 + t] : 0;
+    }
+    auto Mval = [&](int c, int m) -> double {
+      return (lane + 32 * c < nj) ? __ldg(Bc + (int64_t)jj[c] * nv + m) : 0.0;
+    };
+    double q[MAXC][EMIN_NV_MAX];
+    bool qr_ok = false;
+    if (nj >= nv) {
+#pragma unroll
+      for (int j = 0; j < EMIN_NV_MAX; ++j) {
+        if (j >= nv) break;
+        double vc[MAXC];
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) vc[c] = Mval(c, j);
+        double rcol[EMIN_NV_MAX];
+#pragma unroll
+        for (int l = 0; l < EMIN_NV_MAX; ++l) rcol[l] = 0.0;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+          for (int l = 0; l < EMIN_NV_MAX; ++l) {
+            if (l < j) {
+              double s = 0.0;
+#pragma unroll
+              for (int c = 0; c < MAXC; ++c) s = fma(q[c][l], vc[c], s);
+              const double h = warp_sum(s);
+              rcol[l] += h;
+#pragma unroll
+              for (int c = 0; c < MAXC; ++c) vc[c] = fma(-h, q[c][l], vc[c]);
+            }
+          }
+        }
+        double s2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) s2 = fma(vc[c], vc[c], s2);
+        const double nrm = sqrt(warp_sum(s2));
+        rcol[j] = nrm;
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) q[c][j] = (nrm > 0.0) ? vc[c] / nrm : 0.0;
+        if (lane == 0) {
+#pragma unroll
+          for (int l = 0; l < EMIN_NV_MAX; ++l) if (l <= j) R[l][j] = rcol[l];
+        }
+      }
+      __syncwarp();
+      double rmax = 0.0, rmin = INFINITY;
+      for (int j = 0; j < nv; ++j) {
+        const double a = fabs(R[j][j]);
+        rmax = fmax(rmax, a);
+        rmin = fmin(rmin, a);
+      }
+      qr_ok = (rmax > 0.0) && (rmin > tol * rmax);
+    }
+    if (!qr_ok) {                                 // SVD branch: row by row (k_alg2)
+      if (lane == 0) { flag[nd] = 1; ++nflag; }
+      __syncwarp();
+      continue;
+    }
+    for (int d = 0; d < 3; ++d) {
+      const int64_t i = i0 + d;
+      const int64_t b = v.wptr[i];
+      const int64_t rl = frow[i];
+      double wh[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int t = lane + 32 * c;
+        wh[c] = (t < nj) ? what[b + t] : 0.0;
+      }
+      double rv[EMIN_NV_MAX];
+#pragma unroll
+      for (int m = 0; m < EMIN_NV_MAX; ++m) {
+        rv[m] = 0.0;
+        if (m < nv) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) s = fma(Mval(c, m), wh[c], s);
+          rv[m] = B[rl * nv + m] - warp_sum(s);
+        }
+      }
+      double u[EMIN_NV_MAX];
+#pragma unroll
+      for (int j = 0; j < EMIN_NV_MAX; ++j) {
+        u[j] = 0.0;
+        if (j < nv) {
+          double s = rv[j];
+#pragma unroll
+          for (int l = 0; l < EMIN_NV_MAX; ++l) if (l < j) s -= R[l][j] * u[l];
+          u[j] = s / R[j][j];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int t = lane + 32 * c;
+        if (t < nj) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < EMIN_NV_MAX; ++j) if (j < nv) s = fma(q[c][j], u[j], s);
+#pragma unroll
+          for (int j = 0; j < EMIN_NV_MAX; ++j) if (j < nv) Qout[(b + t) * nv + j] = q[c][j];
+          w0[b + t] = wh[c] + s;
+        }
+      }
+    }
+    if (lane == 0 && nj == nv) frozen += 3;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (frozen) atomicAdd(counters + 1, frozen);
+    if (nflag) atomicAdd(counters + 3, nflag);
   }
 }
 
@@ -775,8 +916,8 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   SETUP_TRY(dalloc(&ctx->yb, W, s));
   SETUP_TRY(dalloc(&ctx->st, 1, s));
   unsigned long long* counters;
-  SETUP_TRY(dalloc(&counters, 3, s)); temps.push_back(counters);
-  SETUP_TRY(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 3, s));
+  SETUP_TRY(dalloc(&counters, 4, s)); temps.push_back(counters);
+  SETUP_TRY(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 4, s));
   SETUP_TRY(cudaMemsetAsync(ctx->dw, 0, sizeof(double) * Wh, s));
   SETUP_TRY(cudaMemsetAsync(ctx->y, 0, sizeof(double) * Wh, s));
   SETUP_TRY(cudaMemsetAsync(ctx->yb, 0, sizeof(double) * W, s));
@@ -784,7 +925,33 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   const int agrid = (int)std::max<int64_t>(1, std::min<int64_t>((nF + 3) / 4, (int64_t)SM * 16));
   if (opts->start == EMIN_START_MAXVOL && nF > 0)      // Alg. 1 tentative start (NEXT-3, reading A24)
     emin_maxvol_start(ctx, dBc, dB, frow, what, counters + 2, s);
-  if (emin_alg2_fast(ctx, dBc, dB, frow, what, counters, s))
+  bool alg2_done = emin_alg2_fast(ctx, dBc, dB, frow, what, counters, s);
+  if (!alg2_done && ctx->kernel_path == 2 && ctx->max_row <= 128 && !getenv("EMIN_ALG2_ROWS")) {
+    // nodal path: one QR per F node; rank-deficient nodes redone row by row
+    uint8_t* nflag;
+    SETUP_TRY(dalloc(&nflag, nF / 3 + 1, s)); temps.push_back(nflag);
+    SETUP_TRY(cudaMemsetAsync(nflag, 0, nF / 3 + 1, s));
+    const int ng = (int)std::max<int64_t>(1, std::min<int64_t>((nF / 3 + 3) / 4, (int64_t)SM * 16));
+    if (ctx->max_row <= 32)
+      k_alg2_nodal<1><<<ng, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
+    else if (ctx->max_row <= 64)
+      k_alg2_nodal<2><<<ng, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
+    else
+      k_alg2_nodal<4><<<ng, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
+    unsigned long long h_nflag = 0;
+    SETUP_TRY(cudaMemcpyAsync(&h_nflag, counters + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SETUP_TRY(cudaStreamSynchronize(s));
+    if (h_nflag) {
+      if (ctx->max_row <= 32)
+        k_alg2<1><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
+      else if (ctx->max_row <= 64)
+        k_alg2<2><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
+      else
+        k_alg2<4><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
+    }
+    alg2_done = true;
+  }
+  if (alg2_done)
     ;
   else if (ctx->max_row <= 32)
     k_alg2<1><<<agrid, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters);

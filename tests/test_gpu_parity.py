@@ -179,6 +179,20 @@ def test_rank_deficient_rows_take_svd_branch():
     _compare(g, o, 20, prob)
 
 
+def test_rank_deficient_nodes_take_svd_branch_nodal():
+    """Elasticity (nodal path, one QR per F node) with B = the 3
+    translations twice: every node's M has rank 3 < nv = 6 -> all nodes are
+    flagged and redone row by row in the SVD branch."""
+    from workloads.problems import make_config
+    prob = make_config("4", size=4)
+    prob.B = np.ascontiguousarray(prob.B[:, [0, 1, 2, 0, 1, 2]])
+    prob.Bc = np.ascontiguousarray(prob.Bc[:, [0, 1, 2, 0, 1, 2]])
+    g, o = _pair(prob, 10)
+    assert g.report()["kernel_path"] == 2
+    assert g.report()["n_svd_rows"] == prob.n_F == o.n_svd
+    _compare(g, o, 10, prob)
+
+
 def test_validation_errors_match_oracle():
     from oracle import Oracle, OracleError
     from paper_2208_02995_b200 import Emin, EminError
