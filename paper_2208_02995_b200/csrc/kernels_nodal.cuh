@@ -34,49 +34,65 @@ struct NodalPlan {
   int32_t max_nb = 0;         // most blocks of one node (> ND_MAXB: v2 stages in chunks; SGS goes generic)
 };
 
-// structure checks (one thread per F node); any violation clears *ok
+// structure checks, one warp per F node (lanes over pattern positions and A
+// entries, coalesced); any violation clears *ok
 __global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_len, int32_t* max_nb) {
-  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = gw; n < nFn; n += nw) {
     const int64_t r = 3 * n;
     const int64_t wb = v.wptr[r];
     const int64_t len = v.wptr[r + 1] - wb;
     bool good = (len % 3 == 0) && len > 0 && len <= 64;     // two 32-lane chunks per node
     for (int d = 1; d < 3 && good; ++d) good = (v.wptr[r + d + 1] - v.wptr[r + d]) == len;
-    for (int64_t t = 0; t < len && good; ++t) {
-      const int32_t c = v.wcol[wb + t];
-      if ((t % 3 == 0 && c % 3 != 0) || (t % 3 != 0 && c != v.wcol[wb + t - 1] + 1)) good = false;
-      for (int d = 1; d < 3 && good; ++d) good = v.wcol[v.wptr[r + d] + t] == c;
-    }
+    bool lg = true;
+    if (good)
+      for (int64_t t = lane; t < len; t += 32) {
+        const int32_t c = v.wcol[wb + t];
+        if ((t % 3 == 0 && c % 3 != 0) || (t % 3 != 0 && c != v.wcol[wb + t - 1] + 1)) lg = false;
+        for (int d = 1; d < 3; ++d) lg = lg && v.wcol[v.wptr[r + d] + t] == c;
+      }
     const int64_t ab = v.affptr[r];
     const int64_t alen = v.affptr[r + 1] - ab;
     good = good && (alen % 3 == 0);
-    if (good) atomicMax(max_nb, (int32_t)(alen / 3));
     for (int d = 1; d < 3 && good; ++d) good = (v.affptr[r + d + 1] - v.affptr[r + d]) == alen;
-    for (int64_t q = 0; q < alen && good; ++q) {
-      const int32_t k = v.affcol[ab + q];
-      if ((q % 3 == 0 && k % 3 != 0) || (q % 3 != 0 && k != v.affcol[ab + q - 1] + 1)) good = false;
-      for (int d = 1; d < 3 && good; ++d) good = v.affcol[v.affptr[r + d] + q] == k;
+    if (good)
+      for (int64_t q = lane; q < alen; q += 32) {
+        const int32_t k = v.affcol[ab + q];
+        if ((q % 3 == 0 && k % 3 != 0) || (q % 3 != 0 && k != v.affcol[ab + q - 1] + 1)) lg = false;
+        for (int d = 1; d < 3; ++d) lg = lg && v.affcol[v.affptr[r + d] + q] == k;
+      }
+    good = __all_sync(0xffffffffu, good && lg);
+    if (lane == 0) {
+      if (!good) atomicExch(ok, 0);
+      else atomicMax(max_nb, (int32_t)(alen / 3));
+      // (each node's byte map starts 16-byte aligned: staged with 16-byte loads)
+      pm_len[n] = good ? (((alen / 3) * (len / 3) + 15) & ~(int64_t)15) : 0;
     }
-    if (!good) atomicExch(ok, 0);
-    // (each node's byte map starts 16-byte aligned: staged with 16-byte loads)
-    pm_len[n] = good ? (((alen / 3) * (len / 3) + 15) & ~(int64_t)15) : 0;
   }
 }
 
-// per node: block records and the byte position map (thread per node)
+// per node: block records and the byte position map, one warp per node
+// (lane per block: the merge of the sorted node lists J_I and J_K)
 __global__ void k_nodal_build(DevView v, int64_t nFn, const int64_t* __restrict__ pmoff, NodalBlk* __restrict__ blk,
                               int64_t* __restrict__ bptr, uint8_t* __restrict__ pm8) {
-  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = gw; n < nFn; n += nw) {
     const int64_t r = 3 * n;
     const int64_t wb = v.wptr[r];
     const int nJ = (int)((v.wptr[r + 1] - wb) / 3);
     const int64_t ab = v.affptr[r];
     const int nb = (int)((v.affptr[r + 1] - ab) / 3);
     const int64_t b0 = ab / 9;
-    bptr[n] = b0;
-    if (n == nFn - 1) bptr[nFn] = v.affptr[3 * nFn] / 9;
-    int64_t po = pmoff[n];
-    for (int b = 0; b < nb; ++b) {
+    if (lane == 0) {
+      bptr[n] = b0;
+      if (n == nFn - 1) bptr[nFn] = v.affptr[3 * nFn] / 9;
+    }
+    const int64_t po = pmoff[n];
+    for (int b = lane; b < nb; b += 32) {
       const int32_t K = v.affcol[ab + 3 * b] / 3;
       const int64_t kb = v.wptr[3 * (int64_t)K];
       const int nK = (int)((v.wptr[3 * (int64_t)K + 1] - kb) / 3);
@@ -84,14 +100,12 @@ __global__ void k_nodal_build(DevView v, int64_t nFn, const int64_t* __restrict_
       nbk.ybase = (int32_t)kb;
       nbk.nK3 = 3 * nK;
       blk[b0 + b] = nbk;
-      // merge the two sorted node lists J_I and J_K
       int sK = 0;
       for (int s = 0; s < nJ; ++s) {
         const int32_t c = v.wcol[wb + 3 * s];
         while (sK < nK && v.wcol[kb + 3 * sK] < c) ++sK;
-        pm8[po + s] = (sK < nK && v.wcol[kb + 3 * sK] == c) ? (uint8_t)sK : (uint8_t)0xFF;
+        pm8[po + (int64_t)b * nJ + s] = (sK < nK && v.wcol[kb + 3 * sK] == c) ? (uint8_t)sK : (uint8_t)0xFF;
       }
-      po += nJ;
     }
   }
 }
