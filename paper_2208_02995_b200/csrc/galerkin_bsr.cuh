@@ -4,8 +4,8 @@
 // the same C nodes in full 3x3 blocks and P's C-node rows the single entry
 // P(3K+e, 3c+e).  Then T = A P and A_c = P^T T are made of full 3x3 blocks
 // and the products can be formed per (block, block) pair: one hash probe per
-// pair instead of 27, the 9 output elements of a pair on 9 lanes (3 pairs per
-// round), each lane adding its <= 3 terms.
+// pair instead of 27, the 3 output rows of a pair on 3 lanes (10 pairs per
+// round), each lane adding <= 3 terms to each of its 3 elements.
 //
 // Same sums as the point path and the oracle, term by term: an output element
 // (d, b) of a node row collects the terms of its pairs in X order (A's blocks /
@@ -75,13 +75,14 @@ struct BsrPtT {
   }
 };
 
-// pairs of output node row R, PPR per round (32: lane per pair; 3: 9 lanes
-// per pair, elem = lane % 9); f(act, m, K, s, elem) returns false to stop
-template <int PPR, class OP, class F>
+// pairs of output node row R, PPR per round with LPP lanes each (32 x 1:
+// lane per pair; 10 x 3: elem = lane % 3 = the output row d of the pair);
+// f(act, m, K, s, elem) returns false to stop
+template <int PPR, int LPP, class OP, class F>
 __device__ __forceinline__ void bsr_pairs(const OP& op, int64_t R, int lane, F&& f) {
   const int64_t nxr = op.nx(R);
-  const int pl = PPR == 32 ? lane : (lane < 9 * PPR ? lane / 9 : -1);
-  const int elem = PPR == 32 ? 0 : lane - 9 * (lane / 9);
+  const int pl = LPP == 1 ? lane : (lane < LPP * PPR ? lane / LPP : -1);
+  const int elem = LPP == 1 ? 0 : lane - LPP * (lane / LPP);
   for (int64_t xb = 0; xb < nxr; xb += 32) {
     const int64_t xi = xb + lane;
     const int nx = (int)(nxr - xb < 32 ? nxr - xb : 32);
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(BS_WARPS[T] * 32) k_bsr_symbolic(OP op, BsrOut
   for (int64_t R = (int64_t)blockIdx.x * W + w; R < o.nrows; R += (int64_t)gridDim.x * W) {
     if (T > 0 && o.cnt[R] != -T) continue;
     int64_t count = 0;
-    bsr_pairs<32>(op, R, lane, [&](bool act, int64_t m, int32_t K, int64_t s, int) {
+    bsr_pairs<32, 1>(op, R, lane, [&](bool act, int64_t m, int32_t K, int64_t s, int) {
       bool fresh = false;
       if (act) gk_insert(keys, LOG, op.ycol(K, s), &fresh);
       count += __popc(__ballot_sync(0xffffffffu, fresh));
@@ -164,9 +165,9 @@ __global__ void __launch_bounds__(BS_WARPS[T] * 32) k_bsr_numeric(OP op, BsrOut 
   constexpr int LOG = BS_LOG[T], CAP = 1 << LOG, W = BS_WARPS[T];
   extern __shared__ double bs_smemd[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double* vals = bs_smemd + (size_t)w * (9 * CAP + 96);
-  double* contrib = vals + 9 * CAP;                        // [32][3]
-  int32_t* keys = reinterpret_cast<int32_t*>(bs_smemd + (size_t)W * (9 * CAP + 96)) + w * (CAP + 32);
+  double* vals = bs_smemd + (size_t)w * (9 * CAP + 288);
+  double* contrib = vals + 9 * CAP;                        // [32][3 bb][3 terms]
+  int32_t* keys = reinterpret_cast<int32_t*>(bs_smemd + (size_t)W * (9 * CAP + 288)) + w * (CAP + 32);
   int32_t* ncontrib = keys + CAP;                          // [32]
   for (int s = lane; s < CAP; s += 32) keys[s] = -1;
   for (int s = lane; s < 9 * CAP; s += 32) vals[s] = 0.0;
@@ -174,30 +175,37 @@ __global__ void __launch_bounds__(BS_WARPS[T] * 32) k_bsr_numeric(OP op, BsrOut 
   for (int64_t R = (int64_t)blockIdx.x * W + w; R < o.nrows; R += (int64_t)gridDim.x * W) {
     const int64_t mR = o.cnt[R];
     if (bs_tier(mR) != T || mR == 0) continue;
-    bsr_pairs<3>(op, R, lane, [&](bool act, int64_t m, int32_t K, int64_t s, int elem) {
+    // 10 pairs per round, 3 lanes per pair: lane d computes the output row d
+    // of its pair (3 elements, <= 3 terms each)
+    bsr_pairs<10, 3>(op, R, lane, [&](bool act, int64_t m, int32_t K, int64_t s, int d) {
       int slot = 0;
-      if (act && elem == 0) {
+      if (act && d == 0) {
         bool fresh;
         slot = gk_insert(keys, LOG, op.ycol(K, s), &fresh);
       }
-      slot = __shfl_sync(0xffffffffu, slot, lane - elem);
+      slot = __shfl_sync(0xffffffffu, slot, lane - d);
       int nt = 0;
-      double t[3];
-      if (act) nt = op.terms(R, m, K, s, elem / 3, elem - 3 * (elem / 3), t);
-      contrib[3 * lane + 0] = t[0];
-      contrib[3 * lane + 1] = t[1];
-      contrib[3 * lane + 2] = t[2];
+      if (act) {
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) nt = op.terms(R, m, K, s, d, bb, contrib + 9 * lane + 3 * bb);
+      }
       ncontrib[lane] = nt;
       __syncwarp();
-      const int key = act ? slot * 9 + elem : -1 - lane;
+      const int key = act ? slot * 3 + d : -1 - lane;
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       if (act && (__ffs(peers) - 1) == lane) {
-        double acc = vals[key];
+        double acc[3];
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) acc[bb] = vals[9 * slot + 3 * d + bb];
         for (unsigned pm = peers; pm; pm &= pm - 1) {
           const int q = __ffs(pm) - 1;
-          for (int k = 0; k < ncontrib[q]; ++k) acc = __dadd_rn(acc, contrib[3 * q + k]);
+          const int nq = ncontrib[q];
+#pragma unroll
+          for (int bb = 0; bb < 3; ++bb)
+            for (int k = 0; k < nq; ++k) acc[bb] = __dadd_rn(acc[bb], contrib[9 * q + 3 * bb + k]);
         }
-        vals[key] = acc;
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) vals[9 * slot + 3 * d + bb] = acc[bb];
       }
       __syncwarp();
       return true;
@@ -321,7 +329,7 @@ __global__ void k_bsr_crp(int64_t nnc, const int64_t* __restrict__ nb, const int
 }
 
 template <int T>
-size_t bs_smem_numeric() { return (size_t)BS_WARPS[T] * ((9 * (1 << BS_LOG[T]) + 96) * 8 + ((1 << BS_LOG[T]) + 32) * 4); }
+size_t bs_smem_numeric() { return (size_t)BS_WARPS[T] * ((9 * (1 << BS_LOG[T]) + 288) * 8 + ((1 << BS_LOG[T]) + 32) * 4); }
 template <int T>
 size_t bs_smem_symbolic() { return (size_t)BS_WARPS[T] * (1 << BS_LOG[T]) * 4; }
 
