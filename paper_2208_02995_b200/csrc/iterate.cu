@@ -335,9 +335,18 @@ __global__ void k_build_erow(const int64_t* __restrict__ wptr, int64_t nF, int32
 // ------------------------------------------------------------ scalars
 __device__ double reduce_partials(const double* __restrict__ p, int np, double* sh) {
   if (np < 0) return p[0];   // already reduced over the ranks (DevState::red)
-  double s = 0.0;
-  for (int k = threadIdx.x; k < np; k += blockDim.x) s += p[k];
-  return block_sum(s, sh);
+  // four independent accumulators (loads in flight), combined in a fixed order
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const int st = blockDim.x;
+  int k = threadIdx.x;
+  for (; k + 3 * st < np; k += 4 * st) {
+    s0 += p[k];
+    s1 += p[k + st];
+    s2 += p[k + 2 * st];
+    s3 += p[k + 3 * st];
+  }
+  for (; k < np; k += st) s0 += p[k];
+  return block_sum((s0 + s1) + (s2 + s3), sh);
 }
 
 __global__ void k_scalar_gamma(DevState* st, const double* __restrict__ partials, int np) {

@@ -721,9 +721,16 @@ static inline bool select_nodal_path(emin_ctx c, NodalPlan*& out) {
   return true;
 }
 
+// Grid of the nodal kernels: ~12 nodes per warp, between 32 and 256 CTAs
+// per SM.  Many short CTAs dispatched in order keep the resident warps on a
+// narrow, advancing window of nodes, so neighbour rows of y stay in L2
+// (config 5: SM x 16 CTAs 15.27 ms, x 64 14.76, x 256 14.33; config 4 is
+// best at x 32: 396 vs 404 us at x 16).  EMIN_NODAL_GRID=k: k CTAs per SM.
 static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
   const int SM = emin_num_sms();
-  return (int)std::max<int64_t>(1, std::min<int64_t>((p->nFn + 7) / 8, (int64_t)SM * 16));
+  int64_t per_sm = std::min<int64_t>(256, std::max<int64_t>(32, p->nFn / (8 * 12) / SM));
+  if (getenv("EMIN_NODAL_GRID")) per_sm = atoi(getenv("EMIN_NODAL_GRID"));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((p->nFn + 7) / 8, (int64_t)SM * per_sm));
 }
 
 // one v2 configuration for every mode: CS = evict-first hints (iteration
