@@ -984,7 +984,8 @@ static inline int select_fast_path(emin_ctx c) {
 static inline int scalar_grid(emin_ctx c) {
   const int SM = emin_num_sms();
   const int64_t nwin = fast_of(c)->sc.nwin;
-  return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * 8));
+  const int64_t per_sm = getenv("EMIN_SCALAR_GRID") ? atoi(getenv("EMIN_SCALAR_GRID")) : 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * per_sm));
 }
 // grid of the setup-time masked launches (MM_R0, MM_ENERGY)
 static inline int scalar_spgemm_grid(emin_ctx c) {
