@@ -366,6 +366,12 @@ __global__ void k_scalar_alpha(DevState* st, const double* __restrict__ partials
 }
 
 // apply a pending update (before reading W or r from outside the loop)
+__global__ void k_wsum(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                       double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] + b[i];
+}
+
 __global__ void k_flush(DevView v, double* __restrict__ r, const double* __restrict__ yb,
                         double* __restrict__ dw, const double* __restrict__ y) {
   const DevState* st = v.st;
@@ -814,7 +820,16 @@ extern "C" emin_status emin_energy(emin_ctx c, double* E) {
     emin_status st = emin_dist_halo_values(c, c->dw, c->stream);   // W = W0 + dW on the halo rows
     if (st != EMIN_OK) return st;
   }
-  const int g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, c->stream);
+  int g;
+  if (c->kernel_path == 2 && !c->dist) {
+    // nodal path: W = W0 + dW once into the (free after the flush) y^ buffer,
+    // so the energy pass gathers one vector instead of two (same sums)
+    k_wsum<<<emin_num_sms() * 8, 256, 0, c->stream>>>(c->w0, c->dw, c->nnzW, c->yb);
+    c->launches += 1;
+    g = emin_launch_masked(c, MM_ENERGY, c->yb, nullptr, nullptr, c->stream);
+  } else {
+    g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, c->stream);
+  }
   double* dev;
   EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&dev, sizeof(double), c->stream));
   const auto red = global_sum(c, g, 2, c->stream);

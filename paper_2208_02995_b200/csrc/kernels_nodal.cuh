@@ -222,7 +222,8 @@ k_spgemm_nodal_s(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __r
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  auto xval = [&](int64_t idx) -> double { return MODE == MM_ENERGY ? X[idx] + X2[idx] : X[idx]; };
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;    // (X2 null: X already W0 + dW)
+  auto xval = [&](int64_t idx) -> double { return two ? X[idx] + X2[idx] : X[idx]; };
   double part = 0.0;
   for (int64_t n = gw; n < nFn; n += nw) {
     const int64_t r = 3 * n;
@@ -412,7 +413,9 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  auto xval = [&](int idx) -> double { return MODE == MM_ENERGY ? X[idx] + X2[idx] : X[idx]; };
+  // MM_ENERGY: W = X + X2, or X alone when the caller summed it (X2 null)
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;
+  auto xval = [&](int idx) -> double { return two ? X[idx] + X2[idx] : X[idx]; };
   const int t0 = lane, t1 = lane + 32;
   const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
   double part = 0.0;
