@@ -806,12 +806,17 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   auto grid_for = [&](int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)SM * 8));
   };
+  // the sweeps (no partial sums): EMIN_SGS_GRID CTAs per SM (A/B)
+  const int64_t sweep_per_sm = getenv("EMIN_SGS_GRID") ? atoi(getenv("EMIN_SGS_GRID")) : 8;
+  auto sweep_grid = [&](int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)SM * sweep_per_sm));
+  };
   if (p->nodal) {
     for (int64_t L = 0; L < p->nlev; ++L) {
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
       const int32_t* rows = p->lvl_rows + p->lvl_ptr[L];
       const bool first = L == 0, top = L == p->nlev - 1;
-#define NDF(E, T, W) k_sgs_sweep_nodal<true, E, T, W><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, \
+#define NDF(E, T, W) k_sgs_sweep_nodal<true, E, T, W><<<sweep_grid(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, \
                                                                      p->pmoff, p->bdir, rows, (int32_t)n, c->r, c->yb, p->u)
       if (p->max_nb > 27) {
         if (first && top) NDF(true, true, true); else if (first) NDF(true, false, true);
@@ -825,10 +830,10 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
     for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
       if (p->max_nb > 27)
-        k_sgs_sweep_nodal<false, false, false, true><<<grid_for(n), 256, 0, s>>>(
+        k_sgs_sweep_nodal<false, false, false, true><<<sweep_grid(n), 256, 0, s>>>(
             v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
       else
-        k_sgs_sweep_nodal<false><<<grid_for(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
+        k_sgs_sweep_nodal<false><<<sweep_grid(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
                                                             p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
     }
     const int g = grid_for(p->nFn);
