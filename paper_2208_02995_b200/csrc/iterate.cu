@@ -532,7 +532,11 @@ emin_status emin_plan(emin_ctx c) {
     EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->dinv, sizeof(double) * std::max<int64_t>(c->nF, 1), c->stream));
     k_recip<<<SM * 4, 256, 0, c->stream>>>(c->d, c->nF, c->dinv);
     c->launches += 2;
-    c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * 8));
+    // one wave (4 CTAs of 256 per SM, the launch bound): config 3 stage I/II
+    // 39.3 / 51.0 -> 38.3 / 48.6 us, config 4 60.4 / 84.5 -> 59.5 / 82.3 us,
+    // config 5 neutral (EMIN_STAGE_GRID: CTAs per SM, A/B)
+    const int64_t stage_per_sm = getenv("EMIN_STAGE_GRID") ? atoi(getenv("EMIN_STAGE_GRID")) : 4;
+    c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * stage_per_sm));
     const char* sv = getenv("EMIN_STAGE");
     c->stage_vec = (sv && !strcmp(sv, "e")) ? 0 : 1;   // 16-byte stages unless EMIN_STAGE=e
     const char* pp = getenv("EMIN_PINGPONG");
