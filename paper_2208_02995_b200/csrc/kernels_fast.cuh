@@ -785,7 +785,8 @@ static inline int select_fast_path(emin_ctx c) {
   if (cudaMallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
-  k_plan_entries<<<SM * 8, 256, 0, s>>>(c->view(), p.ent);
+  // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3; EMIN_PLAN_GRID: CTAs per SM)
+  k_plan_entries<<<SM * (getenv("EMIN_PLAN_GRID") ? atoi(getenv("EMIN_PLAN_GRID")) : 32), 256, 0, s>>>(c->view(), p.ent);
   c->launches += 2;
   // per-iteration kernel variant (EMIN_SPGEMM, default win2); the tile plan
   // and the window headers are built only for the variants that use them
