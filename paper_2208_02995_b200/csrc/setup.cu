@@ -934,7 +934,8 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     uint8_t* nflag;
     SETUP_TRY(dalloc(&nflag, nF / 3 + 1, s)); temps.push_back(nflag);
     SETUP_TRY(cudaMemsetAsync(nflag, 0, nF / 3 + 1, s));
-    const int ng = (int)std::max<int64_t>(1, std::min<int64_t>((nF / 3 + 3) / 4, (int64_t)SM * 16));
+    const int64_t ngs = getenv("EMIN_ALG2_GRID") ? atoi(getenv("EMIN_ALG2_GRID")) : 16;
+    const int ng = (int)std::max<int64_t>(1, std::min<int64_t>((nF / 3 + 3) / 4, (int64_t)SM * ngs));
     if (ctx->max_row <= 32)
       k_alg2_nodal<1><<<ng, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
     else if (ctx->max_row <= 64)
