@@ -988,6 +988,14 @@ static inline int scalar_grid(emin_ctx c) {
   const int64_t per_sm = getenv("EMIN_SCALAR_GRID") ? atoi(getenv("EMIN_SCALAR_GRID")) : 8;
   return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * per_sm));
 }
+// grid of the one-off window kernels (Alg. 2 for nv = 1, P out): short
+// in-order CTAs (EMIN_WIN_GRID CTAs per SM, A/B)
+static inline int setup_win_grid(emin_ctx c) {
+  const int SM = emin_num_sms();
+  const int64_t nwin = fast_of(c)->sc.nwin;
+  const int64_t per_sm = getenv("EMIN_WIN_GRID") ? atoi(getenv("EMIN_WIN_GRID")) : 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * per_sm));
+}
 // grid of the setup-time masked launches (MM_R0, MM_ENERGY)
 static inline int scalar_spgemm_grid(emin_ctx c) {
   const ScalarPlan& p = fast_of(c)->sc;
@@ -1110,12 +1118,12 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
 static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
                                       const double* what, unsigned long long* counters, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
-  k_alg2_nv1<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, Bc, B, frow, what, c->Q, c->w0,
+  k_alg2_nv1<<<setup_win_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, Bc, B, frow, what, c->Q, c->w0,
                                             counters);
 }
 static inline void launch_scalar_get_P(emin_ctx c, double* out, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
-  k_get_P_win<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->w0, c->dw, c->pofs, out);
+  k_get_P_win<<<setup_win_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->w0, c->dw, c->pofs, out);
 }
 static inline void launch_scalar_stage(emin_ctx c, int which, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
