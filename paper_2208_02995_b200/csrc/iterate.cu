@@ -681,7 +681,17 @@ static std::vector<cudaEvent_t>& event_pool() {
 static emin_status build_graph(emin_ctx c, int prof) {
   cudaGraphExec_t& ge = prof ? c->graph_prof_exec : c->graph;
   if (ge) { cudaGraphExecDestroy(ge); ge = nullptr; }
-  if (!c->cap_stream) EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  if (!c->cap_stream) {
+    // one capture stream per thread and device, kept for the process (the
+    // capture mode is thread-local; creating and destroying a stream per
+    // context cost ~0.1 ms per bench step)
+    static thread_local cudaStream_t cap[64] = {};
+    int dev = 0;
+    EMIN_CUDA_TRY(c, cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return EMIN_ERR_CUDA;
+    if (!cap[dev]) EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&cap[dev], cudaStreamNonBlocking));
+    c->cap_stream = cap[dev];
+  }
   std::vector<cudaEvent_t>& ev = event_pool();
   while (prof && ev.size() < 6) {
     cudaEvent_t e;
@@ -955,8 +965,7 @@ extern "C" void emin_destroy(emin_ctx c) {
   if (c->graph_prof_exec) cudaGraphExecDestroy(c->graph_prof_exec);
   if (c->graph_prof_src) cudaGraphDestroy(c->graph_prof_src);
   emin_free_all(c);
-  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  delete c;
+  delete c;                                   // (the capture stream is kept per thread and device)
 }
 
 extern "C" const char* emin_setup_error_internal();
