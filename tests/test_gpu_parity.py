@@ -130,6 +130,7 @@ def test_composable_and_deterministic():
     b = Emin.from_problem(prob)
     a.iterate(7)
     a.get_P()            # a flush in the middle must not change the trajectory
+    a.energy()           # (nor an energy pass: on the nodal path it reuses y^ as scratch)
     a.iterate(5)
     b.iterate(12)
     assert np.array_equal(a.get_P(), b.get_P())
