@@ -102,6 +102,48 @@ __global__ void k_sgs_count(int64_t nF, const int32_t* __restrict__ lev, int32_t
   if ((threadIdx.x & 31) == 0) atomicMax(maxlev, mx);
 }
 
+// per-level windows on the GPU: rows in level-bucket order j, entry offsets
+// pst[j] (exclusive scan of the row lengths); a row whose offset from its
+// level's start lies in [S w, S w + S) goes to window w of the level, S = 33 -
+// the longest row (<= 8 on the scalar path): a window holds <= 32 entries
+// and every window has a row
+__global__ void k_sgs_wlen(int64_t nF, const int32_t* __restrict__ rows, const int64_t* __restrict__ wptr,
+                           int64_t* __restrict__ len) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nF; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = rows[j];
+    len[j] = wptr[i + 1] - wptr[i];
+  }
+}
+__global__ void k_sgs_wgather(int64_t nlev, const int64_t* __restrict__ lptr, const int64_t* __restrict__ pst,
+                              int64_t* __restrict__ out) {
+  for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L <= nlev; L += (int64_t)gridDim.x * blockDim.x)
+    out[L] = pst[lptr[L]];
+}
+__global__ void k_sgs_wfirst(int64_t nF, const int32_t* __restrict__ rows, const int32_t* __restrict__ lev,
+                             const int64_t* __restrict__ lptr, const int64_t* __restrict__ base,
+                             const int64_t* __restrict__ wbase, const int64_t* __restrict__ pst, int4* __restrict__ win,
+                             int S) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nF; j += (int64_t)gridDim.x * blockDim.x) {
+    const int L = lev[rows[j]];
+    const int64_t wl = (pst[j] - base[L]) / S;
+    const bool first = (j == lptr[L]) || ((pst[j - 1] - base[L]) / S != wl);
+    if (first) win[wbase[L] + wl].x = (int)j;
+  }
+}
+__global__ void k_sgs_wfill(int64_t nF, const int32_t* __restrict__ rows, const int32_t* __restrict__ lev,
+                            const int64_t* __restrict__ base, const int64_t* __restrict__ wbase,
+                            const int64_t* __restrict__ pst, const int64_t* __restrict__ len, int4* __restrict__ win,
+                            int S) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nF; j += (int64_t)gridDim.x * blockDim.x) {
+    const int L = lev[rows[j]];
+    int4* w = &win[wbase[L] + (pst[j] - base[L]) / S];
+    const int64_t o = pst[j] - pst[w->x];
+    atomicOr(&w->y, (int)(1u << (unsigned)o));
+    atomicAdd(&w->z, (int)len[j]);
+    atomicAdd(&w->w, 1);
+  }
+}
+
 __global__ void k_sgs_scatter(int64_t nF, const int32_t* __restrict__ lev, int32_t* cursor, int32_t* rows) {
   const int lane = threadIdx.x & 31;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nF; i0 += (int64_t)gridDim.x * blockDim.x) {
@@ -753,38 +795,38 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   // scalar path: per-level windows of <= 32 entries (rows never straddle)
   p->rec = p->nodal ? nullptr : emin_scalar_records(c);
   if (p->rec && p->nlev && !getenv("EMIN_SGS_GENERIC")) {
-    std::vector<int32_t> hrows((size_t)nF);
-    std::vector<int64_t> hwptr((size_t)nF + 1);
-    EMIN_CUDA_TRY(c, cudaMemcpyAsync(hrows.data(), p->lvl_rows, sizeof(int32_t) * nF, cudaMemcpyDeviceToHost, s));
-    EMIN_CUDA_TRY(c, cudaMemcpyAsync(hwptr.data(), c->wptr, sizeof(int64_t) * (nF + 1), cudaMemcpyDeviceToHost, s));
+    // windows built on the GPU (k_sgs_w*): only nlev + 1 offsets visit the host
+    int64_t *len, *pst, *lptr, *base, *wbase, *tot2, *scr;
+    const int64_t nl = p->nlev;
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&len, sizeof(int64_t) * (nF + 1), s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&pst, sizeof(int64_t) * (nF + 1), s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&lptr, sizeof(int64_t) * (nl + 1), s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&base, sizeof(int64_t) * (nl + 1), s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&wbase, sizeof(int64_t) * (nl + 1), s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&tot2, sizeof(int64_t), s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&scr, sizeof(int64_t) * emin_scan_scratch_elems(nF + 1), s));
+    k_sgs_wlen<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, c->wptr, len);
+    EMIN_CUDA_TRY(c, emin_scan_i64(len, pst, nF, tot2, scr, s));
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(pst + nF, tot2, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(lptr, p->lvl_ptr.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+    k_sgs_wgather<<<1, 256, 0, s>>>(nl, lptr, pst, base);
+    std::vector<int64_t> hb((size_t)nl + 1);
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(hb.data(), base, sizeof(int64_t) * (nl + 1), cudaMemcpyDeviceToHost, s));
     EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
-    std::vector<int4> hw;
-    p->win_ptr.assign((size_t)p->nlev + 1, 0);
-    for (int64_t L = 0; L < p->nlev; ++L) {
-      int64_t j = p->lvl_ptr[L];
-      const int64_t je = p->lvl_ptr[L + 1];
-      while (j < je) {
-        int4 wv = make_int4((int)j, 0, 0, 0);
-        int ne = 0;
-        while (j < je) {
-          const int len = (int)(hwptr[hrows[j] + 1] - hwptr[hrows[j]]);
-          if (ne + len > 32) break;
-          wv.y |= (int)(1u << ne);
-          ne += len;
-          ++wv.w;
-          ++j;
-        }
-        wv.z = ne;
-        hw.push_back(wv);
-      }
-      p->win_ptr[L + 1] = (int64_t)hw.size();
-    }
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->win, sizeof(int4) * std::max<size_t>(hw.size(), 1), s));
-    EMIN_CUDA_TRY(c, cudaMemcpyAsync(p->win, hw.data(), sizeof(int4) * hw.size(), cudaMemcpyHostToDevice, s));
+    p->win_ptr.assign((size_t)nl + 1, 0);
+    const int S = 33 - std::max(1, c->max_row);   // (max_row <= 8 on the scalar path)
+    for (int64_t L = 0; L < nl; ++L) p->win_ptr[L + 1] = p->win_ptr[L] + (hb[L + 1] - hb[L] + S - 1) / S;
+    const int64_t nw = p->win_ptr[nl];
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(wbase, p->win_ptr.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->win, sizeof(int4) * std::max<int64_t>(nw, 1), s));
+    EMIN_CUDA_TRY(c, cudaMemsetAsync(p->win, 0, sizeof(int4) * std::max<int64_t>(nw, 1), s));
+    k_sgs_wfirst<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, p->lev, lptr, base, wbase, pst, p->win, S);
+    k_sgs_wfill<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, p->lev, base, wbase, pst, len, p->win, S);
     EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->dir, std::max<int64_t>(c->nnzAFF, 1), s));
     k_sgs_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->dir);
-    c->launches += 1;
-    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));   // hw leaves scope
+    c->launches += 6;
+    void* fr[] = {len, pst, lptr, base, wbase, tot2, scr};
+    for (void* q : fr) cudaFreeAsync(q, s);
   } else {
     p->rec = nullptr;
   }
