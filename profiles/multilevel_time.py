@@ -34,7 +34,7 @@ def main():
     t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     args = (t(prob.A_rowptr), t(prob.A_col), t(prob.A_val), iscs, t(prob.B))
     kw = dict(block_size=prob.block_size, P_rowptr=t(prob.P_rowptr), P_col=t(prob.P_col),
-              P_val=t(prob.P_val), iters=iters, stagnation_rel=0.0)
+              P_val=t(prob.P_val), iters=iters)
     print(f"# inputs {time.time() - t0:.1f}s", file=sys.stderr)
     emin_multilevel(*args, **kw)                      # warm-up
     torch.cuda.synchronize()
