@@ -221,7 +221,9 @@ const char* emin_pattern_error(void);
  *   inputs_on_device;  stream = cudaStream_t.  Synchronous; temporaries
  *   (T, P^T) are allocated on the stream and freed before returning.
  * EMIN_ERR_CSR on decreasing row pointers or column ids out of range;
- * EMIN_ERR_ARG if a row of T or A_c has more than 8192 distinct columns. */
+ * EMIN_ERR_ARG if a row of T or A_c has more than 8192 distinct columns
+ * (the 3x3-block product handles node rows of up to 1024 node columns and
+ * hands wider ones to the point product). */
 emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_rowptr, const int32_t* A_col,
                           const double* A_val, const int64_t* P_rowptr, const int32_t* P_col,
                           const double* P_val, int64_t* Ac_rowptr, int32_t* Ac_col, double* Ac_val,

@@ -346,7 +346,8 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
     k_bsr_check<<<G, 256, 0, s>>>(nn, dArp, dAcol, dPrp, dPcol, err);
     GK_TRY(cudaMemcpyAsync(&h_err, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     GK_TRY(cudaStreamSynchronize(s));
-    if (!h_err) {
+    // (a node row wider than the largest table: fall back to the point path)
+    if (!h_err) do {
       auto sync_err = [&]() -> int32_t {
         int32_t h = 0;
         cudaMemcpyAsync(&h, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
@@ -361,7 +362,7 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
       BsrOut oT{};
       oT.nrows = nn; oT.cnt = cntT; oT.err = err;
       GK_TRY((bs_launch_all<0>(false, opT, oT, SM, s)));
-      if (sync_err()) return done(EMIN_ERR_ARG, "A P: a node row wider than 1024 node columns");
+      if (sync_err()) break;
       GK_TRY(emin_scan_i64(cntT, Tnp, nn, tot, scratch, s));
       GK_TRY(cudaMemcpyAsync(Tnp + nn, tot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
       GK_TRY(cudaMemcpyAsync(&nbT, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -411,7 +412,7 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
       BsrOut oC{};
       oC.nrows = nnc; oC.cnt = cntC; oC.err = err;
       GK_TRY((bs_launch_all<1>(false, opC, oC, SM, s)));
-      if (sync_err()) return done(EMIN_ERR_ARG, "P^T (A P): a node row wider than 1024 node columns");
+      if (sync_err()) break;
       GK_TRY(emin_scan_i64(cntC, nbC, nnc, tot, scratch, s));
       GK_TRY(cudaMemcpyAsync(&NB, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       int64_t* Crp = Ac_rowptr;
@@ -440,7 +441,7 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
       GK_TRY(cudaGetLastError());
       g_galerkin_path = 1;
       return done(EMIN_OK, nullptr);
-    }
+    } while (0);
     GK_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
   }
 

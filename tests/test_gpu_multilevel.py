@@ -81,6 +81,26 @@ def test_galerkin_block_path_equals_point_path(name, size, monkeypatch):
     _assert_bitwise(blk, pt)
 
 
+def test_galerkin_block_path_falls_back_on_wide_node_rows():
+    # one 3x3-block node whose P row spans 1100 C nodes (> 1024 node columns,
+    # the block path's widest table): the point path takes over, same bits
+    from oracle import galerkin
+    from paper_2208_02995_b200.emin import emin_galerkin, load_library
+    rng = np.random.default_rng(3)
+    n, ncn = 3, 1100
+    nc = 3 * ncn
+    Arp = np.array([0, 3, 6, 9], np.int64)
+    Acol = np.tile(np.arange(3), 3).astype(np.int32)
+    Aval = rng.standard_normal(9) + 3.0 * np.eye(3).reshape(-1)
+    Prp = np.array([0, nc, 2 * nc, 3 * nc], np.int64)
+    Pcol = np.tile(np.arange(nc), 3).astype(np.int32)
+    Pval = rng.standard_normal(3 * nc)
+    want = galerkin(n, nc, Arp, Acol, Aval, Prp, Pcol, Pval)
+    got = emin_galerkin(n, nc, Arp, Acol, Aval, Prp, Pcol, Pval)
+    assert load_library().emin_galerkin_path() == 0
+    _assert_bitwise(got, want)
+
+
 def _csr(D):
     rp = np.zeros(D.shape[0] + 1, np.int64)
     cols, vals = [], []
