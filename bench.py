@@ -336,7 +336,10 @@ def main():
     nnzW = stats["report"]["nnz_W"]
     nnzAFF = stats["report"]["nnz_AFF"]
     nF = stats["report"]["n_fine"]
-    updates = nnzW_global * k_it * args.steps
+    # updates actually performed: if the CG ever stopped before k_it (gamma or
+    # y'Ky at zero), count only the steps it took (never the requested ones)
+    k_eff = stats["k_done"] if 0 < stats["k_done"] < k_it else k_it
+    updates = nnzW_global * k_eff * args.steps
     value = updates / (ms / 1e3)
 
     # ---- iteration-only rate (setup excluded, SURVEY §8d definition)
@@ -465,7 +468,7 @@ def main():
             t = torch.tensor([e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": nnzW_global * k_it * n_e2e / (e_ms / 1e3), "unit": UNIT,
+        e2e = {"value": nnzW_global * k_eff * n_e2e / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_ms / n_e2e, "steps": n_e2e,
                "mode": "serial (host pointers into the C ABI)" if args.e2e_serial else
@@ -498,10 +501,10 @@ def main():
                    f"sgs ({args.sgs_key} order, {stats['report']['sgs_levels']} levels per sweep)",
                    "start": args.start},
         "roofline": roofline,
-        "iter_only": {"value": nnzW_global * k_it / (it_ms_med / 1e3), "unit": UNIT,
-                      "ms_per_iter": it_ms_med / k_it,
-                      "GBps_vs_B_iter": it_bytes / (it_ms_med / k_it / 1e3) / 1e9,
-                      "frac_of_peak": it_bytes / (it_ms_med / k_it / 1e3) / 1e9 / peak},
+        "iter_only": {"value": nnzW_global * k_eff / (it_ms_med / 1e3), "unit": UNIT,
+                      "ms_per_iter": it_ms_med / k_eff,
+                      "GBps_vs_B_iter": it_bytes / (it_ms_med / k_eff / 1e3) / 1e9,
+                      "frac_of_peak": it_bytes / (it_ms_med / k_eff / 1e3) / 1e9 / peak},
         "kernel_ms_per_step": {"spgemm": stats["spgemm_ms"] / nprof,
                                "stage1": stats["stage_ms"][0] / nprof,
                                "stage2": stats["stage_ms"][1] / nprof,
