@@ -282,7 +282,9 @@ k_spgemm_win2m(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict
   const int wib = threadIdx.x >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  auto xval = [&](int idx) -> double { return MODE == MM_ENERGY ? X[idx] + X2[idx] : X[idx]; };
+  // MM_ENERGY: W = X + X2, or X alone when the caller summed it (X2 null)
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;
+  auto xval = [&](int idx) -> double { return two ? X[idx] + X2[idx] : X[idx]; };
   double part = 0.0;
   for (int64_t w = gw; w < nwin; w += nw) {
     const int r0 = rowstart[w];
@@ -356,6 +358,7 @@ k_spgemm_scalar(DevView v, const SpEnt* __restrict__ A, const int32_t* __restric
                 double* __restrict__ partials) {
   __shared__ double sh[32];
   if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;      // (X2 null: X is already W)
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -376,7 +379,7 @@ k_spgemm_scalar(DevView v, const SpEnt* __restrict__ A, const int32_t* __restric
         const unsigned s = (en.pm >> sh4) & 0xFu;
         if (s != 0xFu) {
           const int64_t src = (int64_t)en.ybase + s;
-          const double xv = (MODE == MM_ENERGY) ? X[src] + X2[src] : X[src];
+          const double xv = two ? X[src] + X2[src] : X[src];
           acc = fma(en.a, xv, acc);
         }
       }
@@ -387,7 +390,7 @@ k_spgemm_scalar(DevView v, const SpEnt* __restrict__ A, const int32_t* __restric
       }
     }
     if (MODE == MM_ENERGY) {
-      if (L.act) part += (X[e] + X2[e]) * (acc + 2.0 * fc);
+      if (L.act) part += (two ? X[e] + X2[e] : X[e]) * (acc + 2.0 * fc);
       continue;
     }
     // Pi_B, nv = 1: g - q (q . g) over the row
@@ -572,6 +575,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double sh[32];
   if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;      // (X2 null: X is already W)
   const int tid = threadIdx.x;
   const TileHdr H = hdr[blockIdx.x];
   const int nrows = H.r1 - H.r0;
@@ -598,7 +602,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
     if (e < nent) {
       if (MODE != MM_ENERGY) qv[u] = v.Q[H.base + e];
       if (MODE == MM_ITER || MODE == MM_R0E) xo[u] = X[H.base + e];
-      if (MODE == MM_ENERGY) xo[u] = X[H.base + e] + X2[H.base + e];
+      if (MODE == MM_ENERGY) xo[u] = two ? X[H.base + e] + X2[H.base + e] : X[H.base + e];
     }
   }
   __syncthreads();
@@ -626,7 +630,7 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
         const unsigned s = (en.pm >> sh4) & 0xFu;
         if (s != 0xFu) {
           const int64_t src = (int64_t)en.ybase + s;
-          const double xv = (MODE == MM_ENERGY) ? X[src] + X2[src] : X[src];
+          const double xv = two ? X[src] + X2[src] : X[src];
           acc = fma(en.a, xv, acc);
         }
       }
