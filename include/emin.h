@@ -25,9 +25,10 @@
  *    emin_destroy.  Outputs go to caller-allocated buffers.
  *  - Work is enqueued on opts->stream (cudaStream_t, NULL = legacy default).
  *    emin_iterate is asynchronous unless k_done or dE is non-NULL.
- *  - Multi-GPU: emin_setup, emin_iterate, emin_energy and emin_reset are
- *    collective over opts->nccl_comm (every rank calls them in the same
- *    order); nccl_comm = NULL means one GPU owning all rows.
+ *  - Multi-GPU: emin_setup, emin_iterate, emin_energy, emin_get_P and
+ *    emin_reset are collective over opts->nccl_comm (or the in-process
+ *    opts->loopback group): every rank calls them in the same order;
+ *    nccl_comm = loopback = NULL means one GPU owning all rows.
  *  - After a failing call other than emin_setup the context stays valid;
  *    emin_destroy is always safe (also on NULL).
  */
@@ -94,7 +95,28 @@ typedef struct {
                                    system solved exactly on them, zero elsewhere (reading A24;
                                    P_val ignored).  Rows without a nonsingular selection keep
                                    W^ = 0 (counted in emin_report_t.n_maxvol_fail). */
+  void*   loopback;             /* emin_loopback handle or NULL: the row-partitioned path with
+                                   R ranks as R contexts on ONE device in one process (one
+                                   thread per rank), exchanging through device-to-device
+                                   copies ordered by events and host barriers instead of NCCL
+                                   (see emin_loopback_create).  Mutually exclusive with
+                                   nccl_comm.  Iterations are enqueued eagerly (no CUDA graph). */
+  int32_t loopback_rank;        /* this context's rank in the loopback group */
+  int32_t debug_flags;          /* 0 for production.  Bits (EMIN_DBG_*) select reference or
+                                   alternative code paths for tests and A/B measurements; they
+                                   never change the method, only which kernels compute it. */
 } emin_opts;
+
+/* emin_opts.debug_flags bits */
+#define EMIN_DBG_FORCE_GENERIC 1   /* generic warp-per-row kernels instead of the scalar / nodal
+                                      specialisations (the reference the fast paths are tested
+                                      against) */
+#define EMIN_DBG_NO_R0E 2          /* r0 and E0 by two masked passes instead of the fused one */
+#define EMIN_DBG_SGS_GENERIC 4     /* generic warp-per-row SGS sweeps */
+#define EMIN_DBG_TRACE 8           /* synchronise and print each setup phase's host time */
+#define EMIN_DBG_FUSE_SCALARS 16   /* one GPU: CG scalar steps in the last block of the producing
+                                      kernels instead of separate single-block kernels */
+#define EMIN_DBG_ALG2_ROWS 32      /* nodal path: Alg. 2 row by row instead of once per node */
 
 #define EMIN_PREC_JACOBI 0
 #define EMIN_PREC_SGS 1
@@ -116,6 +138,10 @@ typedef struct {
   int32_t precond;     /* EMIN_PREC_JACOBI or EMIN_PREC_SGS */
   int64_t sgs_levels;  /* dependency levels of one SGS sweep (0 for Jacobi) */
   int64_t n_maxvol_fail;  /* F rows where the max-vol start found no nonsingular selection */
+  int32_t rank;        /* this context's rank (0 on one GPU) */
+  int64_t n_halo_rows; /* F rows of other ranks whose pattern / values this rank receives */
+  int64_t n_halo_entries;  /* their W entries (doubles received per halo exchange) */
+  int64_t n_send_entries;  /* W entries this rank sends per halo exchange */
 } emin_report_t;
 
 /* Fill opts with defaults (rank_tol 1e-10, tau 0, project_after_jacobi 0,
@@ -173,6 +199,14 @@ emin_status emin_report(emin_ctx ctx, emin_report_t* rep);
 void emin_destroy(emin_ctx ctx);
 
 const char* emin_status_str(emin_status s);
+
+/* Device memory: every allocation of the library comes from a library-owned
+ * stream-ordered pool per device (the device's default pool is left as it
+ * is).  Freed blocks stay cached in that pool, so repeated emin_setup calls
+ * reuse them; emin_release_memory() synchronises the device and returns all
+ * cached blocks to the driver (emin_galerkin and emin_pattern release their
+ * temporaries themselves). */
+void emin_release_memory(void);
 /* Last error message recorded on ctx (or of the last failed emin_setup when
  * ctx == NULL).  Never NULL. */
 const char* emin_last_error(emin_ctx ctx);
@@ -218,7 +252,7 @@ const char* emin_pattern_error(void);
  *   caller's pattern);  Ac_rowptr [nc+1] out;  Ac_col / Ac_val [Ac_cap] out,
  *   or Ac_col = NULL to count only (EMIN_ERR_ARG if Ac_cap < nnz, Ac_rowptr
  *   and *nnz_out still filled: call again);  all pointers host, or device if
- *   inputs_on_device;  stream = cudaStream_t.  Synchronous; temporaries
+ *   flags & EMIN_GALERKIN_DEVICE;  stream = cudaStream_t.  Synchronous; temporaries
  *   (T, P^T) are allocated on the stream and freed before returning.
  * EMIN_ERR_CSR on decreasing row pointers or column ids out of range;
  * EMIN_ERR_ARG if a row of T or A_c has more than 8192 distinct columns
@@ -227,8 +261,13 @@ const char* emin_pattern_error(void);
 emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_rowptr, const int32_t* A_col,
                           const double* A_val, const int64_t* P_rowptr, const int32_t* P_col,
                           const double* P_val, int64_t* Ac_rowptr, int32_t* Ac_col, double* Ac_val,
-                          int64_t Ac_cap, int64_t* nnz_out, int32_t inputs_on_device, void* stream);
+                          int64_t Ac_cap, int64_t* nnz_out, int32_t flags, void* stream);
 const char* emin_galerkin_error(void);
+/* emin_galerkin flags: bit 0 (EMIN_GALERKIN_DEVICE) = all pointers are device
+ * pointers; bit 1 (EMIN_GALERKIN_POINT) = always the point product (test of
+ * the 3x3-block path, which must equal it bitwise). */
+#define EMIN_GALERKIN_DEVICE 1
+#define EMIN_GALERKIN_POINT 2
 /* Which product the last emin_galerkin call of this thread used: 1 = the 3x3
  * block path (A in full 3x3 node blocks, P blockwise on F nodes and the
  * identity on C nodes -- the elasticity structure; same sums, bitwise), 0 =
@@ -247,6 +286,24 @@ int32_t emin_galerkin_path(void);
 emin_status emin_nccl_unique_id(uint8_t* id128);
 emin_status emin_nccl_comm_init(void** comm, int32_t nranks, const uint8_t* id128, int32_t rank);
 emin_status emin_nccl_comm_destroy(void* comm);
+
+/* In-process loopback transport (tests and single-GPU emulation of the
+ * row-partitioned path).  R contexts, each set up by its
+ * own host thread with opts.loopback = the handle and opts.loopback_rank = r,
+ * share one device.  Every collective of the NCCL path has a loopback
+ * counterpart with the same data movement: the halo exchange
+ * becomes one cudaMemcpyAsync per (sender, receiver) pair from the sender's
+ * packed buffer into the receiver's halo tail, ordered by CUDA events; the
+ * scalar sums (allreduce) are one small kernel per rank adding the R rank-local
+ * sums in rank order; setup-time gathers go through host memory.  Host threads
+ * rendezvous at a barrier inside each collective, so all R ranks must call the
+ * collective calls (emin_setup, emin_iterate, emin_energy, emin_reset,
+ * emin_get_P) in the same order, each from its own thread.  No kernel waits on
+ * another rank's kernel (stream-ordered copies only).
+ * emin_loopback_create: nranks in [1, 64]; *out = handle.  destroy after every
+ * context of the group is destroyed. */
+emin_status emin_loopback_create(void** out, int32_t nranks);
+void emin_loopback_destroy(void* lb);
 
 /* Device time of the most recent emin_iterate's kernels, per kernel class,
  * accumulated with CUDA events on the launching stream when profiling is

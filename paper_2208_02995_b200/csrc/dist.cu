@@ -1,4 +1,5 @@
-// dist.cu -- row-partitioned multi-GPU plumbing (NCCL over NVLink).
+// dist.cu -- row-partitioned multi-GPU plumbing: the halo plan, and the two
+// transports behind it (NCCL over NVLink; the in-process loopback group).
 //
 // P:980-986 [§4]: "the sparsity pattern adjacency information of P can be
 // communicated only once before entering PCG, then for all the successive
@@ -15,8 +16,19 @@
 // search direction y on those rows are exchanged (ncclSend/ncclRecv grouped,
 // received in place into the halo tail of y); the two CG scalars are
 // combined by ncclAllReduce of one double each.
+//
+// The same plan runs over either transport (dist.cuh::Transport): NCCL, one
+// process per GPU; or the loopback group, R contexts in one process driven
+// by R host threads, whose exchange is one cudaMemcpyAsync per (sender,
+// receiver) pair ordered by CUDA events and whose sums add the R rank-local
+// values in rank order -- so the halo plan, the halo tail of the W layout
+// and the per-iteration exchange run (and are tested) with R > 1 ranks on a
+// single device.
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "emin_internal.cuh"
@@ -85,6 +97,15 @@ __global__ void k_pack(const T* __restrict__ src, const int64_t* __restrict__ id
 
 }  // namespace
 
+__global__ void k_sum_ranks(const double* __restrict__ g, int R, int n, double* __restrict__ out) {
+  const int j = threadIdx.x;
+  if (j < n) {
+    double t = g[j];
+    for (int p = 1; p < R; ++p) t += g[p * n + j];   // rank order
+    out[j] = t;
+  }
+}
+
 #ifdef EMIN_WITH_NCCL
 #define NCCL_TRY(ctx, call)                                                                   \
   do {                                                                                        \
@@ -95,44 +116,280 @@ __global__ void k_pack(const T* __restrict__ src, const int64_t* __restrict__ id
     }                                                                                         \
   } while (0)
 
-static ncclComm_t comm_of(emin_ctx c) { return (ncclComm_t)c->comm; }
-
-template <typename T> static ncclDataType_t nccl_type();
-template <> ncclDataType_t nccl_type<double>() { return ncclFloat64; }
-template <> ncclDataType_t nccl_type<int64_t>() { return ncclInt64; }
-template <> ncclDataType_t nccl_type<int32_t>() { return ncclInt32; }
-
-// grouped point-to-point: send[p] (count, offset in sendbuf) / recv[p]
-template <typename T>
-static emin_status exchange(emin_ctx c, const T* sendbuf, const std::vector<int64_t>& scnt,
-                            const std::vector<int64_t>& soff, T* recvbuf, const std::vector<int64_t>& rcnt,
-                            const std::vector<int64_t>& roff, cudaStream_t s) {
-  NCCL_TRY(c, ncclGroupStart());
-  for (int p = 0; p < c->nranks; ++p) {
-    if (p == c->rank) continue;
-    if (scnt[p]) NCCL_TRY(c, ncclSend(sendbuf + soff[p], (size_t)scnt[p], nccl_type<T>(), p, comm_of(c), s));
-    if (rcnt[p]) NCCL_TRY(c, ncclRecv(recvbuf + roff[p], (size_t)rcnt[p], nccl_type<T>(), p, comm_of(c), s));
+// ---------------------------------------------------------------- NCCL
+struct NcclTransport final : Transport {
+  ncclComm_t comm;
+  explicit NcclTransport(ncclComm_t cm) : comm(cm) {}
+  emin_status allgather_i64(emin_ctx c, const int64_t* mine, int n, int64_t* all) override {
+    cudaStream_t s = c->stream;
+    int64_t* buf;
+    EMIN_CUDA_TRY(c, emin_mallocAsync(&buf, sizeof(int64_t) * n * (1 + c->nranks), s));
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(buf, mine, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    NCCL_TRY(c, ncclAllGather(buf, buf + n, (size_t)n, ncclInt64, comm, s));
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(all, buf + n, sizeof(int64_t) * n * c->nranks, cudaMemcpyDeviceToHost, s));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+    cudaFreeAsync(buf, s);
+    return EMIN_OK;
   }
-  NCCL_TRY(c, ncclGroupEnd());
-  return EMIN_OK;
-}
+  emin_status exchange(emin_ctx c, const void* sendbuf, size_t esz, const std::vector<int64_t>& scnt,
+                       const std::vector<int64_t>& soff, void* recvbuf, const std::vector<int64_t>& rcnt,
+                       const std::vector<int64_t>& roff, cudaStream_t s) override {
+    const char* sb = static_cast<const char*>(sendbuf);
+    char* rb = static_cast<char*>(recvbuf);
+    NCCL_TRY(c, ncclGroupStart());
+    for (int p = 0; p < c->nranks; ++p) {
+      if (p == c->rank) continue;
+      if (scnt[p]) NCCL_TRY(c, ncclSend(sb + soff[p] * esz, (size_t)scnt[p] * esz, ncclInt8, p, comm, s));
+      if (rcnt[p]) NCCL_TRY(c, ncclRecv(rb + roff[p] * esz, (size_t)rcnt[p] * esz, ncclInt8, p, comm, s));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+    return EMIN_OK;
+  }
+  emin_status allreduce_sum(emin_ctx c, const double* in, double* out, int n, cudaStream_t s) override {
+    NCCL_TRY(c, ncclAllReduce(in, out, (size_t)n, ncclFloat64, ncclSum, comm, s));
+    return EMIN_OK;
+  }
+  emin_status allreduce_max_i32(emin_ctx c, int32_t* inout, cudaStream_t s) override {
+    NCCL_TRY(c, ncclAllReduce(inout, inout, 1, ncclInt32, ncclMax, comm, s));
+    return EMIN_OK;
+  }
+  bool capturable() const override { return true; }
+};
 #endif
 
-emin_status emin_dist_attach(emin_ctx c, void* comm) {
+// ---------------------------------------------------------------- loopback
+// Shared by the R contexts of one group.  A generation barrier on the host
+// orders the publication of each rank's buffers and events; the device-side
+// order is carried by the events (stream waits, copies on the waiting
+// rank's stream): nothing on the device waits for another rank's kernel.
+struct LoopbackGroup {
+  int R;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  struct Slot {
+    const void* buf = nullptr;
+    size_t esz = 0;
+    std::vector<int64_t> scnt, soff;
+    std::vector<int64_t> host;
+    cudaEvent_t ready = nullptr, done = nullptr;
+    double* gbuf = nullptr;     // [R * 4] gathered rank-local sums (device of the rank)
+  };
+  std::vector<Slot> slot;
+  bool aborted = false;
+  std::string why;
+  explicit LoopbackGroup(int r) : R(r), slot(r) {}
+  // false if the group was aborted (a rank failed) or a peer did not arrive
+  // within 300 s: no rank is left waiting for a peer that is gone
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return false;
+    const int64_t g = gen;
+    if (++arrived == R) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(300), [&] { return gen != g || aborted; })) {
+      aborted = true;
+      why = "a peer rank did not reach the collective within 300 s";
+      cv.notify_all();
+    }
+    return !aborted;
+  }
+  void abort(const std::string& w) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!aborted) { aborted = true; why = w; }
+    cv.notify_all();
+  }
+};
+
+struct LoopbackTransport final : Transport {
+  LoopbackGroup* G;
+  int r;
+  LoopbackTransport(LoopbackGroup* g, int rank) : G(g), r(rank) {}
+  LoopbackGroup::Slot& me() { return G->slot[r]; }
+  emin_status gone(emin_ctx c) {
+    c->last_error = "loopback group aborted: " + G->why;
+    return EMIN_ERR_CUDA;
+  }
+  void abort(const std::string& why) override { G->abort("rank " + std::to_string(r) + ": " + why); }
+  emin_status allgather_i64(emin_ctx c, const int64_t* mine, int n, int64_t* all) override {
+    me().host.assign(mine, mine + n);
+    if (!G->barrier()) return gone(c);
+    for (int p = 0; p < G->R; ++p)
+      for (int j = 0; j < n; ++j) all[(int64_t)p * n + j] = G->slot[p].host[j];
+    if (!G->barrier()) return gone(c);
+    return EMIN_OK;
+  }
+  emin_status exchange(emin_ctx c, const void* sendbuf, size_t esz, const std::vector<int64_t>& scnt,
+                       const std::vector<int64_t>& soff, void* recvbuf, const std::vector<int64_t>& rcnt,
+                       const std::vector<int64_t>& roff, cudaStream_t s) override {
+    {
+      const cudaError_t e0 = cudaGetLastError();
+      if (e0 != cudaSuccess) {
+        c->last_error = std::string("loopback exchange: error pending before the collective: ") +
+                        cudaGetErrorString(e0);
+        G->abort(c->last_error);
+        return EMIN_ERR_CUDA;
+      }
+    }
+    me().buf = sendbuf;
+    me().esz = esz;
+    me().scnt = scnt;
+    me().soff = soff;
+    cudaError_t e = cudaEventRecord(me().ready, s);
+    if (!G->barrier()) return gone(c);
+    // pull every peer's slice for me (one copy per sender)
+    for (int p = 0; p < G->R && e == cudaSuccess; ++p) {
+      if (p == r || !rcnt[p]) continue;
+      const LoopbackGroup::Slot& q = G->slot[p];
+      if (q.esz != esz || q.scnt[r] != rcnt[p]) {
+        c->last_error = "loopback exchange: rank " + std::to_string(r) + " expects " + std::to_string(rcnt[p]) +
+                        " elements of " + std::to_string(esz) + " bytes from rank " + std::to_string(p) +
+                        ", which sends " + std::to_string(q.scnt[r]) + " of " + std::to_string(q.esz);
+        e = cudaErrorInvalidValue;
+        break;
+      }
+      e = cudaStreamWaitEvent(s, q.ready, 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(static_cast<char*>(recvbuf) + roff[p] * esz,
+                            static_cast<const char*>(q.buf) + q.soff[r] * esz, (size_t)rcnt[p] * esz,
+                            cudaMemcpyDeviceToDevice, s);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(me().done, s);
+    if (e != cudaSuccess) {
+      if (c->last_error.empty()) c->last_error = std::string("loopback exchange: ") + cudaGetErrorString(e);
+      G->abort(c->last_error);
+      return EMIN_ERR_CUDA;
+    }
+    if (!G->barrier()) return gone(c);
+    // the peers that read my buffer are done before my stream may touch it
+    for (int p = 0; p < G->R && e == cudaSuccess; ++p)
+      if (p != r && scnt[p]) e = cudaStreamWaitEvent(s, G->slot[p].done, 0);
+    if (!G->barrier()) return gone(c);
+    if (e != cudaSuccess) {
+      c->last_error = std::string("loopback exchange: ") + cudaGetErrorString(e);
+      G->abort(c->last_error);
+      return EMIN_ERR_CUDA;
+    }
+    return EMIN_OK;
+  }
+  emin_status allreduce_sum(emin_ctx c, const double* in, double* out, int n, cudaStream_t s) override {
+    const char* where = "";
+    auto fail = [&](cudaError_t e) {
+      c->last_error = std::string("loopback allreduce (") + where + "): " + cudaGetErrorString(e);
+      G->abort(c->last_error);
+      return EMIN_ERR_CUDA;
+    };
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { where = "error pending before the collective"; return fail(e); }
+    me().buf = in;
+    where = "record ready";
+    e = cudaEventRecord(me().ready, s);
+    if (e != cudaSuccess) return fail(e);
+    if (!G->barrier()) return gone(c);
+    for (int p = 0; p < G->R; ++p) {
+      if (p != r) {
+        where = "wait ready";
+        e = cudaStreamWaitEvent(s, G->slot[p].ready, 0);
+        if (e != cudaSuccess) return fail(e);
+      }
+      where = "gather copy";
+      e = cudaMemcpyAsync(me().gbuf + p * n, G->slot[p].buf, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return fail(e);
+    }
+    where = "record done";
+    e = cudaEventRecord(me().done, s);
+    if (e != cudaSuccess) return fail(e);
+    if (!G->barrier()) return gone(c);
+    for (int p = 0; p < G->R; ++p)
+      if (p != r) {
+        where = "wait done";
+        e = cudaStreamWaitEvent(s, G->slot[p].done, 0);
+        if (e != cudaSuccess) return fail(e);
+      }
+    if (!G->barrier()) return gone(c);
+    k_sum_ranks<<<1, 32, 0, s>>>(me().gbuf, G->R, n, out);
+    c->launches += 1;
+    where = "rank-sum kernel";
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(e);
+    return EMIN_OK;
+  }
+  emin_status allreduce_max_i32(emin_ctx c, int32_t* inout, cudaStream_t s) override {
+    int32_t v = 0;
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(&v, inout, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+    int64_t mine = v;
+    std::vector<int64_t> all(G->R);
+    {
+      emin_status st = allgather_i64(c, &mine, 1, all.data());
+      if (st != EMIN_OK) return st;
+    }
+    v = (int32_t)*std::max_element(all.begin(), all.end());
+    EMIN_CUDA_TRY(c, cudaMemcpyAsync(inout, &v, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+    return EMIN_OK;
+  }
+  bool capturable() const override { return false; }
+  ~LoopbackTransport() override {
+    if (me().ready) cudaEventDestroy(me().ready);
+    if (me().done) cudaEventDestroy(me().done);
+    if (me().gbuf) cudaFree(me().gbuf);
+    me() = LoopbackGroup::Slot();
+  }
+};
+
+extern "C" emin_status emin_loopback_create(void** out, int32_t nranks) {
+  if (!out || nranks < 1 || nranks > 64) return EMIN_ERR_ARG;
+  *out = new LoopbackGroup(nranks);
+  return EMIN_OK;
+}
+
+extern "C" void emin_loopback_destroy(void* lb) { delete static_cast<LoopbackGroup*>(lb); }
+
+emin_status emin_dist_attach(emin_ctx c, void* nccl_comm, void* loopback, int32_t loopback_rank) {
+  if (loopback) {
+    LoopbackGroup* G = static_cast<LoopbackGroup*>(loopback);
+    if (loopback_rank < 0 || loopback_rank >= G->R) {
+      c->last_error = "loopback_rank out of range";
+      return EMIN_ERR_ARG;
+    }
+    c->nranks = G->R;
+    c->rank = loopback_rank;
+    c->dist = new DistPlan();
+    LoopbackGroup::Slot& sl = G->slot[loopback_rank];
+    EMIN_CUDA_TRY(c, cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+    EMIN_CUDA_TRY(c, cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    EMIN_CUDA_TRY(c, cudaMalloc((void**)&sl.gbuf, sizeof(double) * 4 * G->R));
+    c->dist->tp = new LoopbackTransport(G, loopback_rank);
+    return EMIN_OK;
+  }
 #ifdef EMIN_WITH_NCCL
-  c->comm = comm;
+  ncclComm_t cm = (ncclComm_t)nccl_comm;
   int n = 1, r = 0;
-  NCCL_TRY(c, ncclCommCount(comm_of(c), &n));
-  NCCL_TRY(c, ncclCommUserRank(comm_of(c), &r));
+  NCCL_TRY(c, ncclCommCount(cm, &n));
+  NCCL_TRY(c, ncclCommUserRank(cm, &r));
+  c->comm = nccl_comm;
   c->nranks = n;
   c->rank = r;
   c->dist = new DistPlan();
+  c->dist->tp = new NcclTransport(cm);
   return EMIN_OK;
 #else
-  (void)comm;
+  (void)nccl_comm;
   c->last_error = "libemin was built without NCCL";
   return EMIN_ERR_NCCL;
 #endif
+}
+
+bool emin_dist_capturable(emin_ctx c) { return !c->dist || c->dist->tp->capturable(); }
+
+void emin_dist_abort(emin_ctx c, const std::string& why) {
+  if (c && c->dist && c->dist->tp) c->dist->tp->abort(why);
 }
 
 // Gather every rank's F range; find, request and receive the halo rows'
@@ -141,31 +398,27 @@ emin_status emin_dist_attach(emin_ctx c, void* comm) {
 emin_status emin_dist_find_halo(emin_ctx c, int64_t fbegin, int64_t nF, int64_t nFg, int64_t m,
                                 const int64_t* Arp, const int32_t* Acol, const uint8_t* isc,
                                 const int64_t* cidx, int64_t* scratch) {
-#ifdef EMIN_WITH_NCCL
   DistPlan& d = *c->dist;
   cudaStream_t s = c->stream;
   const int R = c->nranks;
   const int SM = emin_num_sms();
   // ---- all F ranges
-  int64_t* buf;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&buf, sizeof(int64_t) * (2 + 2 * R), s));
-  int64_t mine[2] = {fbegin, nF};
-  EMIN_CUDA_TRY(c, cudaMemcpyAsync(buf, mine, sizeof(mine), cudaMemcpyHostToDevice, s));
-  NCCL_TRY(c, ncclAllGather(buf, buf + 2, 2, ncclInt64, comm_of(c), s));
+  const int64_t mine[2] = {fbegin, nF};
   std::vector<int64_t> all(2 * R);
-  EMIN_CUDA_TRY(c, cudaMemcpyAsync(all.data(), buf + 2, sizeof(int64_t) * 2 * R, cudaMemcpyDeviceToHost, s));
-  EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
-  cudaFreeAsync(buf, s);
+  {
+    emin_status st = d.tp->allgather_i64(c, mine, 2, all.data());
+    if (st != EMIN_OK) return st;
+  }
   d.fbeg.resize(R);
   d.fcnt.resize(R);
   for (int p = 0; p < R; ++p) { d.fbeg[p] = all[2 * p]; d.fcnt[p] = all[2 * p + 1]; }
   // ---- halo rows: F columns of owned rows outside [fbegin, fbegin + nF)
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&d.hflag, sizeof(int64_t) * std::max<int64_t>(nFg, 1), s));
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&d.hpos, sizeof(int64_t) * std::max<int64_t>(nFg + 1, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&d.hflag, sizeof(int64_t) * std::max<int64_t>(nFg, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&d.hpos, sizeof(int64_t) * std::max<int64_t>(nFg + 1, 1), s));
   EMIN_CUDA_TRY(c, cudaMemsetAsync(d.hflag, 0, sizeof(int64_t) * std::max<int64_t>(nFg, 1), s));
   k_mark_halo<<<SM * 8, 256, 0, s>>>(m, c->opts.row_begin, fbegin, fbegin + nF, Arp, Acol, isc, cidx, d.hflag);
   int64_t* tot;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&tot, sizeof(int64_t), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&tot, sizeof(int64_t), s));
   EMIN_CUDA_TRY(c, emin_scan_i64(d.hflag, d.hpos, nFg, tot, scratch, s));
   int64_t nH = 0;
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(&nH, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -173,7 +426,7 @@ emin_status emin_dist_find_halo(emin_ctx c, int64_t fbegin, int64_t nF, int64_t 
   cudaFreeAsync(tot, s);
   d.nH = nH;
   int64_t* hlist;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&hlist, sizeof(int64_t) * std::max<int64_t>(nH, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&hlist, sizeof(int64_t) * std::max<int64_t>(nH, 1), s));
   k_halo_list<<<SM * 8, 256, 0, s>>>(d.hflag, d.hpos, nFg, hlist);
   std::vector<int64_t> h_hlist(nH);
   if (nH) EMIN_CUDA_TRY(c, cudaMemcpyAsync(h_hlist.data(), hlist, sizeof(int64_t) * nH, cudaMemcpyDeviceToHost, s));
@@ -181,21 +434,20 @@ emin_status emin_dist_find_halo(emin_ctx c, int64_t fbegin, int64_t nF, int64_t 
   // ---- rows to receive per owner (hlist is sorted, owners own contiguous ranges)
   d.rrow.assign(R, 0);
   d.rrow_off.assign(R, 0);
+  bool orphan = false;   // (reported after the collective below, so no rank is left waiting)
   for (int64_t h = 0, p = 0; h < nH; ++h) {
     while (p < R && h_hlist[h] >= d.fbeg[p] + d.fcnt[p]) ++p;
-    if (p >= R || h_hlist[h] < d.fbeg[p]) { c->last_error = "halo row owned by no rank"; return EMIN_ERR_ARG; }
+    if (p >= R || h_hlist[h] < d.fbeg[p]) { orphan = true; break; }
     d.rrow[p]++;
   }
   for (int p = 1; p < R; ++p) d.rrow_off[p] = d.rrow_off[p - 1] + d.rrow[p - 1];
   // ---- counts matrix -> rows to send per requester
-  int64_t* cm;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&cm, sizeof(int64_t) * (R + R * R), s));
-  EMIN_CUDA_TRY(c, cudaMemcpyAsync(cm, d.rrow.data(), sizeof(int64_t) * R, cudaMemcpyHostToDevice, s));
-  NCCL_TRY(c, ncclAllGather(cm, cm + R, R, ncclInt64, comm_of(c), s));
   std::vector<int64_t> M(R * R);
-  EMIN_CUDA_TRY(c, cudaMemcpyAsync(M.data(), cm + R, sizeof(int64_t) * R * R, cudaMemcpyDeviceToHost, s));
-  EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
-  cudaFreeAsync(cm, s);
+  {
+    emin_status st = d.tp->allgather_i64(c, d.rrow.data(), R, M.data());
+    if (st != EMIN_OK) return st;
+  }
+  if (orphan) { c->last_error = "halo row owned by no rank"; return EMIN_ERR_ARG; }
   d.srow.assign(R, 0);
   d.srow_off.assign(R, 0);
   for (int p = 0; p < R; ++p) d.srow[p] = M[(int64_t)p * R + c->rank];   // rank p wants this many of mine
@@ -203,39 +455,34 @@ emin_status emin_dist_find_halo(emin_ctx c, int64_t fbegin, int64_t nF, int64_t 
   d.nS = d.srow_off[R - 1] + d.srow[R - 1];
   // ---- the requests themselves (global F ids) -> local ids of rows to send
   int64_t* req;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&req, sizeof(int64_t) * std::max<int64_t>(d.nS, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&req, sizeof(int64_t) * std::max<int64_t>(d.nS, 1), s));
   {
-    emin_status st = exchange<int64_t>(c, hlist, d.rrow, d.rrow_off, req, d.srow, d.srow_off, s);
+    emin_status st = d.tp->exchange(c, hlist, sizeof(int64_t), d.rrow, d.rrow_off, req, d.srow, d.srow_off, s);
     if (st != EMIN_OK) return st;
   }
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&d.send_rows, sizeof(int32_t) * std::max<int64_t>(d.nS, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&d.send_rows, sizeof(int32_t) * std::max<int64_t>(d.nS, 1), s));
   k_to_local<<<SM * 4, 256, 0, s>>>(req, d.nS, fbegin, d.send_rows);
   cudaFreeAsync(req, s);
   cudaFreeAsync(hlist, s);
   c->launches += 4;
   return EMIN_OK;
-#else
-  (void)fbegin; (void)nF; (void)nFg; (void)m; (void)Arp; (void)Acol; (void)isc; (void)cidx; (void)scratch;
-  return EMIN_ERR_NCCL;
-#endif
 }
 
 // After the owned wptr is known: exchange the lengths of the halo rows,
 // extend wptr, build the send-entry list; returns the halo entry count.
 emin_status emin_dist_halo_pattern_sizes(emin_ctx c, int64_t* scratch) {
-#ifdef EMIN_WITH_NCCL
   DistPlan& d = *c->dist;
   cudaStream_t s = c->stream;
   const int R = c->nranks;
   const int SM = emin_num_sms();
   int64_t *slen, *rlen, *excl, *tot;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&slen, sizeof(int64_t) * (d.nS + 1), s));
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&rlen, sizeof(int64_t) * (d.nH + 1), s));
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&excl, sizeof(int64_t) * (std::max(d.nS, d.nH) + 1), s));
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&tot, sizeof(int64_t) * 2, s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&slen, sizeof(int64_t) * (d.nS + 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&rlen, sizeof(int64_t) * (d.nH + 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&excl, sizeof(int64_t) * (std::max(d.nS, d.nH) + 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&tot, sizeof(int64_t) * 2, s));
   k_row_lengths<<<SM * 4, 256, 0, s>>>(d.send_rows, d.nS, c->wptr, slen);
   {
-    emin_status st = exchange<int64_t>(c, slen, d.srow, d.srow_off, rlen, d.rrow, d.rrow_off, s);
+    emin_status st = d.tp->exchange(c, slen, sizeof(int64_t), d.srow, d.srow_off, rlen, d.rrow, d.rrow_off, s);
     if (st != EMIN_OK) return st;
   }
   // halo wptr tail
@@ -264,67 +511,43 @@ emin_status emin_dist_halo_pattern_sizes(emin_ctx c, int64_t* scratch) {
     d.sent_off[p] = h_sexcl[d.srow_off[p]];
     d.sent[p] = h_sexcl[d.srow_off[p] + d.srow[p]] - d.sent_off[p];
   }
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&d.send_eidx, sizeof(int64_t) * std::max<int64_t>(nSE, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&d.send_eidx, sizeof(int64_t) * std::max<int64_t>(nSE, 1), s));
   k_send_entries<<<SM * 4, 256, 0, s>>>(d.send_rows, d.nS, c->wptr, excl, d.send_eidx);
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&d.sendbuf, sizeof(double) * std::max<int64_t>(nSE, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&d.sendbuf, sizeof(double) * std::max<int64_t>(nSE, 1), s));
   cudaFreeAsync(slen, s); cudaFreeAsync(rlen, s); cudaFreeAsync(excl, s); cudaFreeAsync(tot, s);
   c->launches += 3 + 6;
   return EMIN_OK;
-#else
-  (void)scratch;
-  return EMIN_ERR_NCCL;
-#endif
 }
 
 // pattern (coarse ids) of the halo rows, once
 emin_status emin_dist_halo_wcol(emin_ctx c) {
-#ifdef EMIN_WITH_NCCL
   DistPlan& d = *c->dist;
   cudaStream_t s = c->stream;
   int32_t* sb;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&sb, sizeof(int32_t) * std::max<int64_t>(d.nSE, 1), s));
-  k_pack<int32_t><<<emin_num_sms() * 4, 256, 0, s>>>(c->wcol, d.send_eidx, d.nSE, sb);
-  emin_status st = exchange<int32_t>(c, sb, d.sent, d.sent_off, c->wcol + c->nnzW, d.rent, d.rent_off, s);
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&sb, sizeof(int32_t) * std::max<int64_t>(d.nSE, 1), s));
+  if (d.nSE) k_pack<int32_t><<<emin_num_sms() * 4, 256, 0, s>>>(c->wcol, d.send_eidx, d.nSE, sb);
+  emin_status st = d.tp->exchange(c, sb, sizeof(int32_t), d.sent, d.sent_off, c->wcol + c->nnzW, d.rent,
+                                  d.rent_off, s);
   cudaFreeAsync(sb, s);
-  c->launches += 1;
+  c->launches += d.nSE ? 1 : 0;
   return st;
-#else
-  return EMIN_ERR_NCCL;
-#endif
 }
 
 // values of a W-layout vector on the halo rows (per iteration for y)
 emin_status emin_dist_halo_values(emin_ctx c, double* vec, cudaStream_t s) {
-#ifdef EMIN_WITH_NCCL
   DistPlan& d = *c->dist;
   if (d.nSE) k_pack<double><<<emin_num_sms() * 2, 256, 0, s>>>(vec, d.send_eidx, d.nSE, d.sendbuf);
   c->launches += d.nSE ? 1 : 0;
-  return exchange<double>(c, d.sendbuf, d.sent, d.sent_off, vec + c->nnzW, d.rent, d.rent_off, s);
-#else
-  (void)vec; (void)s;
-  return EMIN_ERR_NCCL;
-#endif
+  return d.tp->exchange(c, d.sendbuf, sizeof(double), d.sent, d.sent_off, vec + c->nnzW, d.rent, d.rent_off, s);
 }
 
-// in-place sum of n doubles over the ranks
-emin_status emin_dist_allreduce(emin_ctx c, double* dev, int n, cudaStream_t s) {
-#ifdef EMIN_WITH_NCCL
-  NCCL_TRY(c, ncclAllReduce(dev, dev, (size_t)n, ncclFloat64, ncclSum, comm_of(c), s));
-  return EMIN_OK;
-#else
-  (void)dev; (void)n; (void)s;
-  return EMIN_ERR_NCCL;
-#endif
+// out = sum over the ranks of in (n <= 4 doubles, device, in != out)
+emin_status emin_dist_allreduce(emin_ctx c, const double* in, double* out, int n, cudaStream_t s) {
+  return c->dist->tp->allreduce_sum(c, in, out, n, s);
 }
 
 emin_status emin_dist_allreduce_max_i32(emin_ctx c, int32_t* dev, cudaStream_t s) {
-#ifdef EMIN_WITH_NCCL
-  NCCL_TRY(c, ncclAllReduce(dev, dev, 1, ncclInt32, ncclMax, comm_of(c), s));
-  return EMIN_OK;
-#else
-  (void)dev; (void)s;
-  return EMIN_ERR_NCCL;
-#endif
+  return c->dist->tp->allreduce_max_i32(c, dev, s);
 }
 
 void emin_dist_free(emin_ctx c) {
@@ -333,6 +556,8 @@ void emin_dist_free(emin_ctx c) {
   cudaStream_t s = c->stream;
   void* ptrs[] = {d.hflag, d.hpos, d.send_rows, d.send_eidx, d.sendbuf};
   for (void* p : ptrs) if (p) cudaFreeAsync(p, s);
+  cudaStreamSynchronize(s);
+  delete d.tp;
   delete c->dist;
   c->dist = nullptr;
 }

@@ -27,8 +27,8 @@ struct DevState {
   int32_t pend;       // r -= alpha_pend yb pending (applied by stage I)
   int32_t pendw;      // dw += alpha_pend y pending (applied by stage II)
   int32_t k_call;     // accepted steps in the current emin_iterate call
-  double red[4];      // multi-GPU: local sums reduced in place by ncclAllReduce
-                      // [0] gamma, [1] y.yb, [2] energy
+  double red[4];      // multi-GPU: rank-local sums [0] gamma, [1] y.yb, [2] energy
+  double redg[4];     // ... and their sums over the ranks (allreduce red -> redg)
   uint32_t ctr[2];    // fused scalar steps: blocks done in stage I [0] / SpGEMM [1]
 };
 
@@ -72,10 +72,9 @@ struct emin_ctx_s {
   int32_t nv = 1;
   int32_t max_row = 0;
   int32_t group = 1;           // lanes per row in the streaming stages
-  int32_t stage_vec = 0;       // 16-byte vectorised streaming stages (EMIN_STAGE=v)
   int32_t kernel_path = 0;
-  int32_t pingpong = 0;        // alternate traversal directions (EMIN_PINGPONG)
-  int32_t fuse = 0;            // scalar steps fused into the producing kernels (EMIN_FUSE)
+  int32_t pingpong = 0;        // alternate traversal directions (L2 ping-pong, iterate.cu)
+  int32_t fuse = 0;            // scalar steps fused into the producing kernels (EMIN_DBG_FUSE_SCALARS)
   int32_t iter_kernels = 5;    // our kernel launches per CG iteration (set at graph capture)
   // device arrays (owned by ctx)
   int64_t *wptr = nullptr, *affptr = nullptr, *afcptr = nullptr, *pofs = nullptr, *cofs = nullptr;
@@ -256,6 +255,15 @@ cudaError_t emin_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* t
 int64_t emin_scan_scratch_elems(int64_t n);
 
 int emin_num_sms();
+
+// stream-ordered allocation from the library's own pool (util.cu); freed with
+// cudaFreeAsync
+cudaError_t emin_mallocAsync(void** p, size_t bytes, cudaStream_t s);
+template <typename T>
+inline cudaError_t emin_mallocAsync(T** p, size_t bytes, cudaStream_t s) {
+  return emin_mallocAsync(reinterpret_cast<void**>(p), bytes, s);
+}
+void emin_pool_trim(cudaStream_t s);   // synchronises s, returns the pool's free blocks
 
 // Alg. 1 tentative start (maxvol.cu)
 void emin_maxvol_start(emin_ctx c, const double* Bc, const double* B, const int64_t* frow, double* what,

@@ -274,7 +274,8 @@ static thread_local int32_t g_galerkin_path = 0;
 extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_rowptr, const int32_t* A_col,
                                      const double* A_val, const int64_t* P_rowptr, const int32_t* P_col,
                                      const double* P_val, int64_t* Ac_rowptr, int32_t* Ac_col, double* Ac_val,
-                                     int64_t Ac_cap, int64_t* nnz_out, int32_t inputs_on_device, void* stream) {
+                                     int64_t Ac_cap, int64_t* nnz_out, int32_t flags, void* stream) {
+  const bool inputs_on_device = (flags & EMIN_GALERKIN_DEVICE) != 0;
   g_galerkin_error.clear();
   g_galerkin_path = 0;
   if (n <= 0 || nc <= 0 || n >= INT32_MAX || nc >= INT32_MAX || !A_rowptr || !A_col || !A_val || !P_rowptr ||
@@ -287,13 +288,13 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
   const int G = SM * 4;
   std::vector<void*> tmp;
   auto dal = [&](void** p, size_t bytes) -> cudaError_t {
-    cudaError_t e = cudaMallocAsync(p, bytes + 64, s);
+    cudaError_t e = emin_mallocAsync(p, bytes + 64, s);
     if (e == cudaSuccess) tmp.push_back(*p);
     return e;
   };
   auto done = [&](emin_status st, const char* msg) {
     for (void* p : tmp) cudaFreeAsync(p, s);
-    cudaStreamSynchronize(s);
+    emin_pool_trim(s);   // the temporaries are large and one-off: back to the driver
     if (msg) g_galerkin_error = msg;
     return st;
   };
@@ -340,7 +341,7 @@ extern "C" emin_status emin_galerkin(int64_t n, int64_t nc, const int64_t* A_row
   if (h_err) return done(EMIN_ERR_CSR, "row pointers decrease or column ids out of range");
 
   // ---- 3x3-block path (elasticity-structured A and P; same sums, bitwise)
-  if (!getenv("EMIN_GALERKIN_POINT") && n % 3 == 0 && nc % 3 == 0) {
+  if (!(flags & EMIN_GALERKIN_POINT) && n % 3 == 0 && nc % 3 == 0) {
     const int64_t nn = n / 3, nnc = nc / 3;
     GK_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
     k_bsr_check<<<G, 256, 0, s>>>(nn, dArp, dAcol, dPrp, dPcol, err);

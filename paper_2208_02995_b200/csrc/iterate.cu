@@ -128,9 +128,7 @@ k_stage2(DevView v, const double* __restrict__ r, double* __restrict__ y, double
 }
 
 // ------------------------------------------------------------ entry-parallel stages
-// (no post-Jacobi projection): one thread per W entry, row from erow[], UNR
-// independent entries in flight per thread.
-constexpr int STAGE_UNR = 4;
+// (no post-Jacobi projection): one thread per pair of W entries, row from erow[].
 
 // z = r / d (Jacobi) from a precomputed 1/d: q0 = r (1/d) and one
 // FMA residual correction, which reproduces the IEEE quotient (Markstein)
@@ -141,83 +139,8 @@ __device__ __forceinline__ double jacobi_div(double r, double d, double dinv) {
   return fma(res, dinv, q0);
 }
 
-__global__ void __launch_bounds__(256, 4)
-k_stage1_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ dinv, double* __restrict__ r,
-           const double* __restrict__ yb, double* __restrict__ partials) {
-  __shared__ double sh[32];
-  const DevState* st = v.st;
-  if (st->stopped) return;
-  const int pend = st->pend;
-  const double ap = st->alpha_pend;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t n = v.nnzW;
-  double part = 0.0;
-  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += STAGE_UNR * stride) {
-    double rv[STAGE_UNR], dv[STAGE_UNR], iv[STAGE_UNR];
-#pragma unroll
-    for (int u = 0; u < STAGE_UNR; ++u) {
-      const int64_t e = e0 + u * stride;
-      if (e < n) {
-        rv[u] = r[e];
-        if (pend) rv[u] = rv[u] - ap * yb[e];
-        const int32_t i = erow[e];
-        dv[u] = v.d[i];
-        iv[u] = dinv[i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < STAGE_UNR; ++u) {
-      const int64_t e = e0 + u * stride;
-      if (e < n) {
-        if (pend) r[e] = rv[u];
-        const double z = jacobi_div(rv[u], dv[u], iv[u]);
-        part = fma(rv[u], z, part);
-      }
-    }
-  }
-  const double tot = block_sum(part, sh);
-  block_partial_out(v, partials, tot, sh, 0);
-}
-
-__global__ void __launch_bounds__(256, 4)
-k_stage2_e(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ dinv,
-           const double* __restrict__ r, double* __restrict__ y, double* __restrict__ dw) {
-  const DevState* st = v.st;
-  const int stopped = st->stopped;
-  const int pendw = st->pendw;
-  if (stopped && !pendw) return;
-  const double ap = st->alpha_pend;
-  const double beta = st->beta;
-  const bool first = (st->k_total == 0);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t n = v.nnzW;
-  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += STAGE_UNR * stride) {
-    double yo[STAGE_UNR], rv[STAGE_UNR], dv[STAGE_UNR], iv[STAGE_UNR], dwv[STAGE_UNR];
-#pragma unroll
-    for (int u = 0; u < STAGE_UNR; ++u) {
-      const int64_t e = e0 + u * stride;
-      if (e < n) {
-        yo[u] = y[e];
-        if (pendw) dwv[u] = dw[e];
-        if (!stopped) { rv[u] = r[e]; const int32_t i = erow[e]; dv[u] = v.d[i]; iv[u] = dinv[i]; }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < STAGE_UNR; ++u) {
-      const int64_t e = e0 + u * stride;
-      if (e < n) {
-        if (pendw) dw[e] = dwv[u] + ap * yo[u];
-        if (!stopped) {
-          const double z = jacobi_div(rv[u], dv[u], iv[u]);
-          y[e] = first ? z : z + beta * yo[u];
-        }
-      }
-    }
-  }
-}
-
-// Vectorised variants: each thread moves pairs of entries with 16-byte loads
-// and stores (double2 / int2); the odd tail entry is handled by thread 0.
+// Each thread moves pairs of entries with 16-byte loads and stores (double2 /
+// int2); the odd tail entry is handled by thread 0.
 __global__ void __launch_bounds__(256, 4)
 k_stage1_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict__ dinv, double* __restrict__ r,
            const double* __restrict__ yb, double* __restrict__ partials) {
@@ -454,17 +377,10 @@ void launch_stage2_g(emin_ctx c, cudaStream_t s) {
 }
 void launch_stage(emin_ctx c, int which, cudaStream_t s) {
   if (!c->opts.project_after_jacobi) {
-    if (c->stage_vec) {
-      if (which == 1)
-        k_stage1_v<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->yb, c->partials);
-      else
-        k_stage2_v<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->y, c->dw);
-      return;
-    }
     if (which == 1)
-      k_stage1_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->yb, c->partials);
+      k_stage1_v<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->yb, c->partials);
     else
-      k_stage2_e<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->y, c->dw);
+      k_stage2_v<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->y, c->dw);
     return;
   }
   switch (c->group) {
@@ -527,27 +443,23 @@ emin_status emin_plan(emin_ctx c) {
   if (c->kernel_path == 1) c->grid_spgemm = scalar_spgemm_grid(c);
   if (!c->opts.project_after_jacobi) {
     // entry-parallel streaming stages: row id per W entry
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->erow, sizeof(int32_t) * std::max<int64_t>(c->nnzW, 1), c->stream));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->erow, sizeof(int32_t) * std::max<int64_t>(c->nnzW, 1), c->stream));
     k_build_erow<<<SM * 8, 256, 0, c->stream>>>(c->wptr, c->nF, c->erow);
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->dinv, sizeof(double) * std::max<int64_t>(c->nF, 1), c->stream));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->dinv, sizeof(double) * std::max<int64_t>(c->nF, 1), c->stream));
     k_recip<<<SM * 4, 256, 0, c->stream>>>(c->d, c->nF, c->dinv);
     c->launches += 2;
     // one wave (4 CTAs of 256 per SM, the launch bound): config 3 stage I/II
     // 39.3 / 51.0 -> 38.3 / 48.6 us, config 4 60.4 / 84.5 -> 59.5 / 82.3 us,
-    // config 5 neutral (EMIN_STAGE_GRID: CTAs per SM, A/B)
-    const int64_t stage_per_sm = getenv("EMIN_STAGE_GRID") ? atoi(getenv("EMIN_STAGE_GRID")) : 4;
-    c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * stage_per_sm));
-    const char* sv = getenv("EMIN_STAGE");
-    c->stage_vec = (sv && !strcmp(sv, "e")) ? 0 : 1;   // 16-byte stages unless EMIN_STAGE=e
-    const char* pp = getenv("EMIN_PINGPONG");
-    c->pingpong = (c->stage_vec && !(pp && !strcmp(pp, "0"))) ? 1 : 0;
+    // config 5 neutral
+    c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nnzW + 255) / 256, (int64_t)SM * 4));
+    c->pingpong = 1;
   }
   c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
   if (c->kernel_path == 1) c->grid_red = std::max(c->grid_red, scalar_iter_grid(c));
   if (c->kernel_path == 2) c->grid_red = std::max(c->grid_red, nodal_grid(c, static_cast<NodalPlan*>(c->nodal)));
   if (c->grid_red > c->n_partials) {
     cudaFreeAsync(c->partials, c->stream);
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&c->partials, sizeof(double) * c->grid_red, c->stream));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->partials, sizeof(double) * c->grid_red, c->stream));
     c->n_partials = c->grid_red;
   }
   EMIN_CUDA_TRY(c, cudaGetLastError());
@@ -591,29 +503,34 @@ bool emin_alg2_fast(emin_ctx c, const double* Bc, const double* B, const int64_t
   return true;
 }
 
-// r0 = -Pi (A P0)|F, E0, fresh CG state (end of setup and emin_reset)
-// Sum of the per-block partials; on several GPUs: local sum into
-// st->red[slot], ncclAllReduce in place, and the consumer reads it (np = -1).
-// Returns the (pointer, np) pair the consumer kernel takes.
-static std::pair<const double*, int> global_sum(emin_ctx c, int np, int slot, cudaStream_t s) {
-  if (!c->dist) return {c->partials, np};
+// Sum of the per-block partials; on several GPUs: rank-local sum into
+// st->red[slot], allreduce into st->redg[slot], and the consumer reads that
+// (np = -1).  *res = the (pointer, np) pair the consumer kernel takes.
+static emin_status global_sum(emin_ctx c, int np, int slot, cudaStream_t s, std::pair<const double*, int>* res) {
+  if (!c->dist) { *res = {c->partials, np}; return EMIN_OK; }
   k_energy_out<<<1, 1024, 0, s>>>(c->partials, np, 0.0, &c->st->red[slot]);
   c->launches += 1;
-  emin_dist_allreduce(c, &c->st->red[slot], 1, s);
-  return {&c->st->red[slot], -1};
+  *res = {&c->st->redg[slot], -1};
+  return emin_dist_allreduce(c, &c->st->red[slot], &c->st->redg[slot], 1, s);
 }
+
+// r0 = -Pi (A P0)|F, E0, fresh CG state (end of setup and emin_reset)
 
 emin_status emin_finish_r0(emin_ctx c) {
   cudaStream_t s = c->stream;
   EMIN_CUDA_TRY(c, cudaMemsetAsync(c->dw, 0, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s));
   // r0 and the energy of P0 (dw = 0) share the masked product A P0: one
   // MM_R0E pass where the kernel path has it, else MM_R0 then MM_ENERGY
-  int g = getenv("EMIN_NO_R0E") ? -1 : emin_launch_masked(c, MM_R0E, c->w0, nullptr, c->r, s);
+  int g = (c->opts.debug_flags & EMIN_DBG_NO_R0E) ? -1 : emin_launch_masked(c, MM_R0E, c->w0, nullptr, c->r, s);
   if (g < 0) {
     emin_launch_masked(c, MM_R0, c->w0, nullptr, c->r, s);
     g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, s);
   }
-  const auto red = global_sum(c, g, 2, s);
+  std::pair<const double*, int> red;
+  {
+    emin_status st = global_sum(c, g, 2, s, &red);
+    if (st != EMIN_OK) return st;
+  }
   k_reset_state<<<1, 1024, 0, s>>>(c->st, red.first, red.second, c->sum_diag_cc, c->opts.tau,
                                    c->opts.stagnation_rel);
   c->launches += 3;
@@ -623,54 +540,58 @@ emin_status emin_finish_r0(emin_ctx c) {
   return EMIN_OK;
 }
 
-static void enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev, int external) {
+static emin_status enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev, int external) {
   auto rec = [&](int t) {
     if (ev) cudaEventRecordWithFlags(ev[t], s, external ? cudaEventRecordExternal : cudaEventRecordDefault);
   };
-  // fused mode (single GPU): the scalar steps run in the last block of stage
-  // I and of the SpGEMM (block_partial_out); with NCCL the partial sums are
-  // reduced over the ranks first, so the single-block scalar kernels stay
-  // opt-in (EMIN_FUSE=1): measured 3.4 us per iteration SLOWER on config 3
+  // fused mode (one GPU, EMIN_DBG_FUSE_SCALARS): the scalar steps run in the
+  // last block of stage I and of the SpGEMM (block_partial_out); measured
+  // 3.4 us per iteration SLOWER on config 3 than the single-block kernels
   // (the last block's serial tail -- counter atomic, partial reduction,
   // dependent DevState loads -- costs what the separate launch did;
-  // profiles/r01b/spgemm_ab_c3.txt)
-  const char* fz = getenv("EMIN_FUSE");
-  c->fuse = (!c->dist && fz && !strcmp(fz, "1")) ? 1 : 0;
+  // profiles/r01b/spgemm_ab_c3.txt), so it is not the default
+  c->fuse = (!c->dist && (c->opts.debug_flags & EMIN_DBG_FUSE_SCALARS)) ? 1 : 0;
   if (c->sgs) c->fuse = 0;
+  std::pair<const double*, int> red;
+  emin_status st = EMIN_OK;
   rec(0);
   int g1 = c->grid_rows;
   if (c->sgs) g1 = emin_sgs_enqueue(c, s);   // z = Pi M_2^-1 r, partial r.z
   else launch_stage(c, 1, s);
   rec(1);
   if (!c->fuse) {
-    const auto r1 = global_sum(c, g1, 0, s);
-    k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, r1.first, r1.second);
+    st = global_sum(c, g1, 0, s, &red);
+    if (st != EMIN_OK) return st;
+    k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, red.first, red.second);
   }
   rec(2);
   if (c->sgs) emin_sgs_stage2(c, s);
   else launch_stage(c, 2, s);
-  if (c->dist) emin_dist_halo_values(c, c->y, s);     // y on the halo rows
+  if (c->dist) {
+    st = emin_dist_halo_values(c, c->y, s);     // y on the halo rows
+    if (st != EMIN_OK) return st;
+  }
   rec(3);
   const int g = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
   rec(4);
   if (!c->fuse) {
-    const auto r2 = global_sum(c, g, 1, s);
-    k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, r2.first, r2.second, c->dE_hist);
+    st = global_sum(c, g, 1, s, &red);
+    if (st != EMIN_OK) return st;
+    k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, red.first, red.second, c->dE_hist);
   }
   rec(5);
   // kernels of ours per iteration: stage I, stage II, SpGEMM (+ the two
   // scalar kernels, + on several GPUs their rank-local sum kernels and the
-  // halo pack)
-  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 3 : 0) + (c->sgs ? (int32_t)(2 * emin_sgs_levels(c) - 1) : 0);
+  // halo pack, + with the loopback transport its two rank-sum kernels)
+  const bool lb = c->dist && !emin_dist_capturable(c);
+  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 2 + (c->dist->nSE ? 1 : 0) : 0) + (lb ? 2 : 0) +
+                    (c->sgs ? (int32_t)(2 * emin_sgs_levels(c) - 1) : 0);
+  return cudaGetLastError() == cudaSuccess ? EMIN_OK : EMIN_ERR_CUDA;
 }
 
-// One iteration captured as a CUDA graph (5 kernel nodes, cheap to
-// instantiate per context); emin_iterate(k) launches it k times.
-// process-wide pool of timing events (profiling mode)
-static std::vector<cudaEvent_t>& event_pool() {
-  static std::vector<cudaEvent_t> pool;
-  return pool;
-}
+// timing events of this context's profiling mode (created on its device,
+// destroyed by emin_destroy)
+static std::vector<cudaEvent_t>& event_pool(emin_ctx c) { return c->ev; }
 
 // One iteration captured as a CUDA graph (5 kernel nodes, cheap to
 // instantiate per context); emin_iterate(k) launches it k times.  The
@@ -681,18 +602,19 @@ static std::vector<cudaEvent_t>& event_pool() {
 static emin_status build_graph(emin_ctx c, int prof) {
   cudaGraphExec_t& ge = prof ? c->graph_prof_exec : c->graph;
   if (ge) { cudaGraphExecDestroy(ge); ge = nullptr; }
-  if (!c->cap_stream) {
-    // one capture stream per thread and device, kept for the process (the
-    // capture mode is thread-local; creating and destroying a stream per
-    // context cost ~0.1 ms per bench step)
-    static thread_local cudaStream_t cap[64] = {};
+  // capture on the calling thread's own capture stream (one per thread and
+  // device, kept for the thread's lifetime: the capture mode is
+  // thread-local, and creating and destroying a stream per context cost
+  // ~0.1 ms per bench step)
+  static thread_local cudaStream_t cap[64] = {};
+  {
     int dev = 0;
     EMIN_CUDA_TRY(c, cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return EMIN_ERR_CUDA;
     if (!cap[dev]) EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&cap[dev], cudaStreamNonBlocking));
     c->cap_stream = cap[dev];
   }
-  std::vector<cudaEvent_t>& ev = event_pool();
+  std::vector<cudaEvent_t>& ev = event_pool(c);
   while (prof && ev.size() < 6) {
     cudaEvent_t e;
     EMIN_CUDA_TRY(c, cudaEventCreate(&e));
@@ -700,9 +622,14 @@ static emin_status build_graph(emin_ctx c, int prof) {
   }
   cudaStream_t s = c->cap_stream;
   EMIN_CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  enqueue_iteration(c, s, prof ? ev.data() : nullptr, prof ? 1 : 0);
+  const emin_status est = enqueue_iteration(c, s, prof ? ev.data() : nullptr, prof ? 1 : 0);
   cudaGraph_t g;
   EMIN_CUDA_TRY(c, cudaStreamEndCapture(s, &g));
+  if (est != EMIN_OK) {    // a collective failed while the graph was built
+    cudaGraphDestroy(g);
+    if (c->last_error.empty()) c->last_error = "enqueue of the iteration failed";
+    return est;
+  }
   if (prof) {
     size_t nn = 0;
     cudaGraphGetNodes(g, nullptr, &nn);
@@ -735,7 +662,7 @@ static emin_status build_graph(emin_ctx c, int prof) {
 static emin_status fold_profile(emin_ctx c) {
   if (!c->prof_pending) return EMIN_OK;
   EMIN_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  std::vector<cudaEvent_t>& ev = event_pool();
+  std::vector<cudaEvent_t>& ev = event_pool(c);
   for (int64_t it = 0; it < c->prof_pending; ++it) {
     cudaEvent_t* e = &ev[6 * (it + 1)];
     float t[5];
@@ -755,7 +682,7 @@ static emin_status ensure_hist(emin_ctx c, int64_t need) {
   if (need <= c->dE_cap) return EMIN_OK;
   int64_t cap = std::max<int64_t>(need, std::max<int64_t>(1024, 2 * c->dE_cap));
   double* nh;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&nh, sizeof(double) * cap, c->stream));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&nh, sizeof(double) * cap, c->stream));
   if (c->dE_hist) {
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(nh, c->dE_hist, sizeof(double) * c->dE_cap, cudaMemcpyDeviceToDevice, c->stream));
     cudaFreeAsync(c->dE_hist, c->stream);
@@ -775,12 +702,22 @@ extern "C" emin_status emin_iterate(emin_ctx c, int32_t k, int32_t* k_done, doub
   emin_status st = ensure_hist(c, c->k_launched + k);
   if (st != EMIN_OK) return st;
   EMIN_CUDA_TRY(c, cudaMemsetAsync(&c->st->k_call, 0, sizeof(int32_t), c->stream));
-  if (c->profiling) {
+  if (!emin_dist_capturable(c)) {
+    // loopback transport: its collectives rendezvous on the host, so the
+    // iterations are enqueued eagerly (same kernels, same order)
+    for (int it = 0; it < k; ++it) {
+      st = enqueue_iteration(c, c->stream, nullptr, 0);
+      if (st != EMIN_OK) {
+        emin_dist_abort(c, c->last_error);
+        return st;
+      }
+    }
+  } else if (c->profiling) {
     if (!c->graph_prof_exec) {
       st = build_graph(c, 1);
       if (st != EMIN_OK) return st;
     }
-    std::vector<cudaEvent_t>& ev = event_pool();
+    std::vector<cudaEvent_t>& ev = event_pool(c);
     const size_t need = (size_t)6 * (c->prof_pending + k + 1);
     while (ev.size() < need) {
       cudaEvent_t e;
@@ -846,8 +783,12 @@ extern "C" emin_status emin_energy(emin_ctx c, double* E) {
     g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, c->stream);
   }
   double* dev;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&dev, sizeof(double), c->stream));
-  const auto red = global_sum(c, g, 2, c->stream);
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&dev, sizeof(double), c->stream));
+  std::pair<const double*, int> red;
+  {
+    emin_status st = global_sum(c, g, 2, c->stream, &red);
+    if (st != EMIN_OK) { cudaFreeAsync(dev, c->stream); return st; }
+  }
   k_energy_out<<<1, 1024, 0, c->stream>>>(red.first, red.second, c->sum_diag_cc, dev);
   c->launches += 4;
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(E, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -862,7 +803,7 @@ extern "C" emin_status emin_get_P(emin_ctx c, double* P_val) {
   const int SM = emin_num_sms();
   double* out = P_val;
   if (!c->opts.inputs_on_device)
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&out, sizeof(double) * std::max<int64_t>(c->nnzP, 1), c->stream));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&out, sizeof(double) * std::max<int64_t>(c->nnzP, 1), c->stream));
   if (c->kernel_path == 1)
     launch_scalar_get_P(c, out, c->stream);
   else
@@ -904,6 +845,12 @@ extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
   rep->precond = c->opts.precond;
   rep->sgs_levels = emin_sgs_levels(c);
   rep->n_maxvol_fail = c->n_maxvol_fail;
+  rep->rank = c->rank;
+  if (c->dist) {
+    rep->n_halo_rows = c->dist->nH;
+    rep->n_halo_entries = c->dist->nHW;
+    rep->n_send_entries = c->dist->nSE;
+  }
   if (h.stopped == 5 && !c->breakdown_reported) {
     c->breakdown_reported = 1;
     return EMIN_ERR_BREAKDOWN;
@@ -966,6 +913,7 @@ extern "C" void emin_destroy(emin_ctx c) {
   if (c->graph_prof_exec) cudaGraphExecDestroy(c->graph_prof_exec);
   if (c->graph_prof_src) cudaGraphDestroy(c->graph_prof_src);
   emin_free_all(c);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   delete c;                                   // (the capture stream is kept per thread and device)
 }
 

@@ -13,15 +13,15 @@
 //   nibble t of pm is the position of J_i[t] in J_k (0xF: absent).  So the
 //   inner loop is one 16-byte broadcast load, a nibble extract and one
 //   gather of y(k, s) -- no search.
-// Per-iteration kernel: k_spgemm_win2 (default); setup / energy modes: the
-// tile kernel (k_spgemm_tile, fused MM_R0E at setup).  The A/B variants
-// (EMIN_SPGEMM=win|win3..win10|hdr|mask|pipe) live in kernels_variants*.cuh.
+// Per-iteration kernel: k_spgemm_win2; setup / energy modes: the tile kernel
+// (k_spgemm_tile, fused MM_R0E at setup), or win2's modes (k_spgemm_win2m)
+// when a tile's records do not fit in shared memory.  The round-1 A/B
+// variants (profiles/ab_r01/) are not part of the library.
 #pragma once
 #include <algorithm>
-#include <cstdlib>
-#include <cstring>
 #include "emin_internal.cuh"
 #include "masked.cuh"
+#include "bulk.cuh"
 
 struct SpEnt {          // 16 bytes, one per A_FF entry
   double a;
@@ -35,56 +35,11 @@ struct ScalarPlan {
   int32_t* rowstart = nullptr;   // [nwin + 1]
   int64_t nwin = 0;
   int32_t S = 0;
-  TileHdr* hdr = nullptr;        // [ntiles] (staged tile kernel)
+  TileHdr* hdr = nullptr;        // [ntiles] (staged tile kernel, setup / energy modes)
   int64_t ntiles = 0;
   size_t tile_smem = 0;
   int use_tiles = 0;
-  int use_pipe = 0, pipe_grid = 0, rec_cap = 0, rows_cap = 0;   // TMA-pipelined persistent kernel
-  uint32_t pipe_smem = 0;
-  struct WinHdr* whdr = nullptr; // [nwin] window headers
-  int variant = 0;               // per-iteration kernel: 0 hdr, 1 win, 2 tile, 3 pipe, 4 mask
-  uint16_t* emask = nullptr;     // [nnzW] matching records per W entry (variant 4)
-  int32_t* rowstart3 = nullptr;  // 64-entry windows (variant 6)
-  int64_t nwin3 = 0;
-  struct Win4Hdr* w4hdr = nullptr; // [nwin] 32-byte window headers (variants 7, 8)
-  int4* w6hdr = nullptr;           // [nwin + 1] 16-byte window headers (variant 9)
-  int4* ell = nullptr;             // [nF * ellW] ELL-padded records (variant 10)
-  int4* w7hdr = nullptr;           // [nwin] {r0, ebase, ehead, nent} (variant 10)
-  int ellW = 0;
-  int w8grid = 0;                  // resident CTAs of win8 (variant 11)
 };
-
-// ---- shared-memory / mbarrier / bulk-copy helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 
 // decode the window: rows [r0, r1), base entry, this lane's row and position
 struct WinLane {
@@ -120,9 +75,6 @@ __device__ __forceinline__ WinLane decode_window(const int64_t* __restrict__ wpt
   return w;
 }
 
-// forward declaration (defined below)
-struct WinHdr;
-
 // sum of v over the lane's row (segmented inclusive scan, then the row's
 // last lane broadcasts); identical in every lane of the row
 __device__ __forceinline__ double row_sum(double v, const WinLane& L) {
@@ -132,48 +84,6 @@ __device__ __forceinline__ double row_sum(double v, const WinLane& L) {
     if (L.pos >= o) v += t;
   }
   return __shfl_sync(0xffffffffu, v, L.rowbeg + L.rowlen - 1);
-}
-
-// Precomputed window header (one 16-byte load per warp; the lane decode is
-// pure ALU): first row, first entry, head bitmask (bit p set if a row starts
-// at window position p), entry count.
-struct WinHdr {
-  int32_t r0;
-  int32_t base;
-  uint32_t head;
-  int32_t nent;
-};
-
-__device__ __forceinline__ WinLane decode_hdr(const WinHdr& h, int lane) {
-  WinLane w;
-  w.base = h.base;
-  w.nent = h.nent;
-  const int l = lane < h.nent ? lane : h.nent - 1;    // inactive lanes mirror the last entry
-  const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);
-  const unsigned hu = h.head & upto;
-  w.rloc = __popc(hu) - 1;
-  w.rowbeg = 31 - __clz(hu);
-  const unsigned after = h.head & ~upto;
-  const int rowend = after ? (__ffs(after) - 1) : h.nent;
-  w.rowlen = rowend - w.rowbeg;
-  w.pos = lane - w.rowbeg;
-  w.act = lane < h.nent;
-  return w;
-}
-
-__global__ void k_plan_headers(const int64_t* __restrict__ wptr, const int32_t* __restrict__ rowstart,
-                               int64_t nwin, WinHdr* __restrict__ hdr) {
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r0 = rowstart[w], r1 = rowstart[w + 1];
-    WinHdr h;
-    h.r0 = r0;
-    h.base = (int32_t)(r1 > r0 ? wptr[r0] : 0);
-    h.nent = (int32_t)(r1 > r0 ? wptr[r1] - wptr[r0] : 0);
-    uint32_t head = 0;
-    for (int32_t r = r0; r < r1; ++r) head |= 1u << (unsigned)(wptr[r] - h.base);
-    h.head = head;
-    hdr[w] = h;
-  }
 }
 
 // y^ = Pi K y (nv = 1), window kernel with fewer warp collectives: the
@@ -345,75 +255,6 @@ k_spgemm_win2m(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict
   block_partial_out(v, partials, tot, sh, -1);
 }
 
-#include "kernels_variants.cuh"
-
-// Masked product on the scalar path, modes as in masked.cuh:
-//   MM_ITER    yb = Pi K y, partial y . yb
-//   MM_R0      r0 = -Pi Pi (A P0)|F (C-identity term included)    (A1)
-//   MM_ENERGY  partial W . (A_FF W + 2 A_FC), W = X + X2          (Eq. trInc)
-template <int MODE>
-__global__ void __launch_bounds__(256)
-k_spgemm_scalar(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict__ rowstart, int64_t nwin,
-                const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
-                double* __restrict__ partials) {
-  __shared__ double sh[32];
-  if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
-  const bool two = MODE == MM_ENERGY && X2 != nullptr;      // (X2 null: X is already W)
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double part = 0.0;
-  for (int64_t w = gw; w < nwin; w += nw) {
-    const int64_t r0 = rowstart[w];
-    const int nrows = (int)(rowstart[w + 1] - r0);
-    if (nrows == 0) continue;                          // warp-uniform
-    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
-    const int64_t i = r0 + L.rloc;
-    const int64_t e = L.base + lane;
-    double acc = 0.0, fc = 0.0;
-    if (L.act) {
-      const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
-      const unsigned sh4 = 4u * (unsigned)L.pos;
-      for (int64_t q = qb; q < qe; ++q) {
-        const SpEnt en = A[q];
-        const unsigned s = (en.pm >> sh4) & 0xFu;
-        if (s != 0xFu) {
-          const int64_t src = (int64_t)en.ybase + s;
-          const double xv = two ? X[src] + X2[src] : X[src];
-          acc = fma(en.a, xv, acc);
-        }
-      }
-      if (MODE != MM_ITER) {            // A(i, c_j): search the short A_FC row
-        const int32_t j = v.wcol[e];
-        for (int64_t q = v.afcptr[i]; q < v.afcptr[i + 1]; ++q)
-          if (v.afccol[q] == j) { fc = v.afcval[q]; break; }
-      }
-    }
-    if (MODE == MM_ENERGY) {
-      if (L.act) part += (two ? X[e] + X2[e] : X[e]) * (acc + 2.0 * fc);
-      continue;
-    }
-    // Pi_B, nv = 1: g - q (q . g) over the row
-    const double qv = L.act ? v.Q[e] : 0.0;
-    double g = (MODE == MM_R0) ? acc + fc : acc;
-#pragma unroll
-    for (int pass = 0; pass < (MODE == MM_R0 ? 2 : 1); ++pass) {
-      const double dot = row_sum(qv * g, L);
-      g = g - qv * dot;
-    }
-    if (L.act) {
-      if (MODE == MM_ITER) {
-        out[e] = g;
-        part = fma(X[e], g, part);
-      } else {
-        out[e] = -g;
-      }
-    }
-  }
-  const double tot = block_sum(part, sh);
-  block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
-}
-
 // Alg. 2 for nv = 1 on the window plan (the CGS2 QR of k_alg2 reduces to
 // q = M / |M|, delta = q (r / |M|); |M| = 0 is the rank-0 SVD branch)
 __global__ void __launch_bounds__(256)
@@ -484,70 +325,8 @@ k_get_P_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const
   }
 }
 
-// stage I on the window plan: r -= alpha_pend yb ; partial r . (r / d)
-__global__ void __launch_bounds__(256)
-k_stage1_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, double* __restrict__ r,
-             const double* __restrict__ yb, double* __restrict__ partials) {
-  __shared__ double sh[32];
-  const DevState* st = v.st;
-  if (st->stopped) return;
-  const int pend = st->pend;
-  const double ap = st->alpha_pend;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double part = 0.0;
-  for (int64_t w = gw; w < nwin; w += nw) {
-    const int64_t r0 = rowstart[w];
-    const int nrows = (int)(rowstart[w + 1] - r0);
-    if (nrows == 0) continue;
-    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
-    if (L.act) {
-      const int64_t e = L.base + lane;
-      const double di = v.d[r0 + L.rloc];
-      double rv = r[e];
-      if (pend) { rv = rv - ap * yb[e]; r[e] = rv; }
-      const double z = rv / di;
-      part = fma(rv, z, part);
-    }
-  }
-  const double tot = block_sum(part, sh);
-  block_partial_out(v, partials, tot, sh, 0);
-}
-
-// stage II on the window plan: dw += alpha_pend y_old ; y = z + beta y_old
-__global__ void __launch_bounds__(256)
-k_stage2_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const double* __restrict__ r,
-             double* __restrict__ y, double* __restrict__ dw) {
-  const DevState* st = v.st;
-  const int stopped = st->stopped;
-  const int pendw = st->pendw;
-  if (stopped && !pendw) return;
-  const double ap = st->alpha_pend;
-  const double beta = st->beta;
-  const bool first = (st->k_total == 0);
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = gw; w < nwin; w += nw) {
-    const int64_t r0 = rowstart[w];
-    const int nrows = (int)(rowstart[w + 1] - r0);
-    if (nrows == 0) continue;
-    const WinLane L = decode_window(v.wptr, r0, nrows, lane);
-    if (L.act) {
-      const int64_t e = L.base + lane;
-      const double yo = y[e];
-      if (pendw) dw[e] = dw[e] + ap * yo;
-      if (!stopped) {
-        const double z = r[e] / v.d[r0 + L.rloc];
-        y[e] = first ? z : z + beta * yo;
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
-// Tiled variant: one CTA per tile of consecutive rows whose first entry lies
+// Tiled kernel: one CTA per tile of consecutive rows whose first entry lies
 // in [t S_T, (t+1) S_T) (S_T = TILE_E - max|J| + 1, so a tile holds at most
 // TILE_E entries).  Phase A stages the tile's contiguous slices -- the A_FF
 // records [abase, aend), the row pointers -- into shared memory with
@@ -689,8 +468,6 @@ k_spgemm_tile(DevView v, const SpEnt* __restrict__ A, const TileHdr* __restrict_
   block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
 }
 
-#include "kernels_variants_tile.cuh"
-
 __global__ void k_tile_headers(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
                                const int32_t* __restrict__ trow, int64_t ntiles, TileHdr* __restrict__ hdr,
                                int32_t* __restrict__ maxrec) {
@@ -707,6 +484,8 @@ __global__ void k_tile_headers(const int64_t* __restrict__ wptr, const int64_t* 
     atomicMax(maxrec + 1, h.r1 - h.r0);
   }
 }
+
+constexpr int TILE_SMEM_CAP = 160 * 1024;   // dynamic shared memory of the tile kernel, at most
 
 static inline size_t tile_smem_bytes(int maxrec) {
   return (size_t)maxrec * sizeof(SpEnt) + 2 * sizeof(int32_t) * (TILE_E + 1) +
@@ -778,227 +557,57 @@ static inline int select_fast_path(emin_ctx c) {
   if (c->nv != 1 || c->max_row > 8 || c->nnzWh >= INT32_MAX || c->nF >= INT32_MAX || c->nnzAFF >= INT32_MAX ||
       c->nF == 0)
     return 0;
-  if (getenv("EMIN_FORCE_GENERIC")) return 0;
+  if (c->opts.debug_flags & EMIN_DBG_FORCE_GENERIC) return 0;
   FastPaths* f = new FastPaths();
   c->fast = f;
   ScalarPlan& p = f->sc;
   p.S = std::min(31, 33 - c->max_row);   // <= 31 rows per window (lane nrows loads the end)
   p.nwin = (c->nnzW + p.S - 1) / p.S;
   cudaStream_t s = c->stream;
-  if (cudaMallocAsync((void**)&p.rowstart, sizeof(int32_t) * (p.nwin + 1), s) != cudaSuccess) return 0;
-  if (cudaMallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
+  if (emin_mallocAsync((void**)&p.rowstart, sizeof(int32_t) * (p.nwin + 1), s) != cudaSuccess) return 0;
+  if (emin_mallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
-  // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3; EMIN_PLAN_GRID: CTAs per SM)
-  k_plan_entries<<<SM * (getenv("EMIN_PLAN_GRID") ? atoi(getenv("EMIN_PLAN_GRID")) : 32), 256, 0, s>>>(c->view(), p.ent);
+  // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
+  k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), p.ent);
   c->launches += 2;
-  // per-iteration kernel variant (EMIN_SPGEMM, default win2); the tile plan
-  // and the window headers are built only for the variants that use them
-  const char* var = getenv("EMIN_SPGEMM");
-  const bool need_tiles = !getenv("EMIN_SETUP_WIN2M") || (var && (!strcmp(var, "tile") || !strcmp(var, "pipe")));
-  const bool need_whdr = var && (!strcmp(var, "hdr") || !strcmp(var, "mask"));
+  // tile plan for the staged setup / energy kernel
+  const int ST = TILE_E - c->max_row + 1;
+  p.ntiles = (c->nnzW + ST - 1) / ST;
+  int32_t* trow = nullptr;
+  int32_t* dmax = nullptr;
   int32_t hmax[2] = {0, 0};
-  if (need_tiles) {
-    // tile plan for the staged kernel
-    const int ST = TILE_E - c->max_row + 1;
-    p.ntiles = (c->nnzW + ST - 1) / ST;
-    int32_t* trow = nullptr;
-    int32_t* dmax = nullptr;
-    if (cudaMallocAsync((void**)&trow, sizeof(int32_t) * (p.ntiles + 1), s) != cudaSuccess ||
-        cudaMallocAsync((void**)&p.hdr, sizeof(TileHdr) * std::max<int64_t>(p.ntiles, 1), s) != cudaSuccess ||
-        cudaMallocAsync((void**)&dmax, sizeof(int32_t) * 2, s) != cudaSuccess)
-      return 1;
-    cudaMemsetAsync(dmax, 0, sizeof(int32_t) * 2, s);
-    k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, ST, p.ntiles, trow);
-    k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
-    c->launches += 2;
-    cudaMemcpyAsync(hmax, dmax, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
-    cudaFreeAsync(trow, s);
-    cudaFreeAsync(dmax, s);
-    cudaStreamSynchronize(s);
-    p.tile_smem = tile_smem_bytes(hmax[0]);
-  }
-  if (need_whdr) {
-    // window headers (lane decode without the rowstart -> wptr round trips)
-    if (cudaMallocAsync((void**)&p.whdr, sizeof(WinHdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) return 1;
-    k_plan_headers<<<SM * 4, 256, 0, s>>>(c->wptr, p.rowstart, p.nwin, p.whdr);
-    c->launches += 1;
-  }
-  p.variant = 5;   // default: win2 (fastest measured, profiles/r01/spgemm_variants_c3.log)
-  if (var && !strcmp(var, "hdr")) p.variant = 0;
-  if (var && !strcmp(var, "win")) p.variant = 1;
-  if (var && !strcmp(var, "tile")) p.variant = 2;
-  if (var && !strcmp(var, "pipe")) p.variant = 3;
-  if (var && !strcmp(var, "mask")) p.variant = 4;
-  if (var && !strcmp(var, "win2")) p.variant = 5;
-  if (var && !strcmp(var, "win3")) p.variant = 6;
-  if (var && !strcmp(var, "win4")) p.variant = 7;
-  if (var && !strcmp(var, "win5")) p.variant = 8;
-  if (var && !strcmp(var, "win6")) p.variant = 9;
-  if (var && !strcmp(var, "win7")) p.variant = 10;
-  if (var && !strcmp(var, "win8")) p.variant = 11;
-  if (var && !strcmp(var, "win9")) p.variant = 12;
-  if (var && !strcmp(var, "win10")) p.variant = 13;
-  if (var && !strcmp(var, "win2g1")) p.variant = 14;
-  if (var && !strcmp(var, "win2g2")) p.variant = 5;
-  if (var && !strcmp(var, "win2g3")) p.variant = 15;
-  if (var && !strcmp(var, "win2g4")) p.variant = 16;
-  if (p.variant == 13) {
-    int32_t* dmx = nullptr;
-    int32_t hw = 0;
-    if (cudaMallocAsync((void**)&dmx, sizeof(int32_t), s) == cudaSuccess) {
-      cudaMemsetAsync(dmx, 0, sizeof(int32_t), s);
-      k_rowlen_max<<<SM * 4, 256, 0, s>>>(c->affptr, c->nF, dmx);
-      cudaMemcpyAsync(&hw, dmx, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-      cudaFreeAsync(dmx, s);
-      cudaStreamSynchronize(s);
-      c->launches += 1;
-    }
-    p.ellW = std::max(2, hw) - 1;                    // MAXR = longest row - 1 (diagonal apart)
-    int per_sm = 0;
-    if (p.ellW <= 8) {
-      auto kfun = p.ellW <= 4 ? k_spgemm_win10<4> : p.ellW <= 6 ? k_spgemm_win10<6> : k_spgemm_win10<8>;
-      cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w10_smem_bytes());
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfun, W8_WARPS * 32, w10_smem_bytes());
-    }
-    if (per_sm < 1 || cudaMallocAsync((void**)&p.w4hdr, sizeof(Win4Hdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) {
-      p.variant = 5;
-    } else {
-      p.w8grid = (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + W8_WARPS - 1) / W8_WARPS, (int64_t)SM * per_sm));
-      k_plan_win4<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w4hdr);
-      c->launches += 1;
-    }
-  }
-  if (p.variant == 12) {
-    int per_sm = 0;
-    cudaFuncSetAttribute(k_spgemm_win9, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w9_smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_win9, W8_WARPS * 32, w9_smem_bytes());
-    if (per_sm < 1 || cudaMallocAsync((void**)&p.w6hdr, sizeof(int4) * (p.nwin + 1), s) != cudaSuccess) {
-      p.variant = 5;
-    } else {
-      p.w8grid = (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + W8_WARPS - 1) / W8_WARPS, (int64_t)SM * per_sm));
-      k_plan_win6<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w6hdr);
-      c->launches += 1;
-    }
-  }
-  if (p.variant == 11) {
-    int per_sm = 0;
-    cudaFuncSetAttribute(k_spgemm_win8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w8_smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_win8, W8_WARPS * 32, w8_smem_bytes());
-    if (per_sm < 1 || cudaMallocAsync((void**)&p.w6hdr, sizeof(int4) * (p.nwin + 1), s) != cudaSuccess) {
-      p.variant = 5;
-    } else {
-      p.w8grid = (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + W8_WARPS - 1) / W8_WARPS, (int64_t)SM * per_sm));
-      k_plan_win6<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w6hdr);
-      c->launches += 1;
-    }
-  }
-  if (p.variant == 10) {
-    int32_t* dmx = nullptr;
-    int32_t hw = 0;
-    if (cudaMallocAsync((void**)&dmx, sizeof(int32_t), s) == cudaSuccess) {
-      cudaMemsetAsync(dmx, 0, sizeof(int32_t), s);
-      k_rowlen_max<<<SM * 4, 256, 0, s>>>(c->affptr, c->nF, dmx);
-      cudaMemcpyAsync(&hw, dmx, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-      cudaFreeAsync(dmx, s);
-      cudaStreamSynchronize(s);
-      c->launches += 1;
-    }
-    p.ellW = std::max(4, hw);
-    if (hw < 1 || hw > 8 ||
-        cudaMallocAsync((void**)&p.ell, sizeof(int4) * (size_t)c->nF * p.ellW, s) != cudaSuccess ||
-        cudaMallocAsync((void**)&p.w7hdr, sizeof(int4) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) {
-      p.variant = 5;
-    } else {
-      k_plan_ell<<<SM * 8, 256, 0, s>>>(c->affptr, c->nF, p.ellW, reinterpret_cast<const int4*>(p.ent), p.ell);
-      k_plan_win7<<<SM * 4, 256, 0, s>>>(c->wptr, p.rowstart, p.nwin, p.w7hdr);
-      c->launches += 2;
-    }
-  }
-  if (p.variant == 9) {
-    if (cudaMallocAsync((void**)&p.w6hdr, sizeof(int4) * (p.nwin + 1), s) != cudaSuccess) {
-      p.variant = 5;
-    } else {
-      k_plan_win6<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w6hdr);
-      c->launches += 1;
-    }
-  }
-  if (p.variant == 7 || p.variant == 8) {
-    if (cudaMallocAsync((void**)&p.w4hdr, sizeof(Win4Hdr) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess) {
-      p.variant = 5;
-    } else {
-      k_plan_win4<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.w4hdr);
-      c->launches += 1;
-    }
-  }
-  if (p.variant == 6) {
-    const int S3 = std::min(63, 65 - c->max_row);
-    p.nwin3 = (c->nnzW + S3 - 1) / S3;
-    if (cudaMallocAsync((void**)&p.rowstart3, sizeof(int32_t) * (p.nwin3 + 1), s) != cudaSuccess) {
-      p.variant = 5;
-    } else {
-      k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, S3, p.nwin3, p.rowstart3);
-      c->launches += 1;
-    }
-  }
-  if (p.variant == 4) {
-    int32_t* bad = nullptr;
-    if (cudaMallocAsync((void**)&p.emask, sizeof(uint16_t) * std::max<int64_t>(c->nnzW, 1), s) != cudaSuccess ||
-        cudaMallocAsync((void**)&bad, sizeof(int32_t), s) != cudaSuccess) {
-      p.variant = 1;
-    } else {
-      cudaMemsetAsync(bad, 0, sizeof(int32_t), s);
-      k_plan_emask<<<SM * 8, 256, 0, s>>>(c->view(), p.ent, p.emask, bad);
-      c->launches += 1;
-      int32_t hb = 0;
-      cudaMemcpyAsync(&hb, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-      cudaFreeAsync(bad, s);
-      cudaStreamSynchronize(s);
-      if (hb) p.variant = 1;
-    }
-  }
-  if (need_tiles && p.tile_smem <= 160 * 1024) {
+  if (emin_mallocAsync((void**)&trow, sizeof(int32_t) * (p.ntiles + 1), s) != cudaSuccess ||
+      emin_mallocAsync((void**)&p.hdr, sizeof(TileHdr) * std::max<int64_t>(p.ntiles, 1), s) != cudaSuccess ||
+      emin_mallocAsync((void**)&dmax, sizeof(int32_t) * 2, s) != cudaSuccess)
+    return 1;
+  cudaMemsetAsync(dmax, 0, sizeof(int32_t) * 2, s);
+  k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, ST, p.ntiles, trow);
+  k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
+  c->launches += 2;
+  cudaMemcpyAsync(hmax, dmax, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(trow, s);
+  cudaFreeAsync(dmax, s);
+  cudaStreamSynchronize(s);
+  p.tile_smem = tile_smem_bytes(hmax[0]);
+  if (p.tile_smem <= TILE_SMEM_CAP) {
     p.use_tiles = 1;
-    cudaFuncSetAttribute(k_spgemm_tile<MM_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
-    cudaFuncSetAttribute(k_spgemm_tile<MM_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
-    cudaFuncSetAttribute(k_spgemm_tile<MM_ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
-    cudaFuncSetAttribute(k_spgemm_tile<MM_R0E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_smem);
-  } else if (p.variant == 2) {
-    p.variant = 5;
-  }
-  if (p.variant == 3) {
-    // persistent TMA-pipelined kernel
-    p.rec_cap = (hmax[0] + 1) & ~1;
-    p.rows_cap = hmax[1] + 1;
-    p.pipe_smem = pipe_layout(p.rec_cap, p.rows_cap).total;
-    int per_sm = 0;
-    if (p.pipe_smem <= 200 * 1024) {
-      cudaFuncSetAttribute(k_spgemm_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.pipe_smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_pipe, TILE_T, p.pipe_smem);
-    }
-    if (per_sm > 0) {
-      p.use_pipe = 1;
-      p.pipe_grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)SM * per_sm));
-    } else {
-      p.variant = 5;
-    }
+    // the attribute is per kernel and process-wide: always the cap, never the
+    // size of this context's tiles (contexts set up concurrently by several
+    // threads must not lower it under each other's launches)
+    cudaFuncSetAttribute(k_spgemm_tile<MM_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_CAP);
+    cudaFuncSetAttribute(k_spgemm_tile<MM_ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_CAP);
+    cudaFuncSetAttribute(k_spgemm_tile<MM_R0E>, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_SMEM_CAP);
   }
   return 1;
 }
 
+// grid of the window kernels: short in-order CTAs, 8 per SM (one wave at
+// the 256-thread launch bound)
 static inline int scalar_grid(emin_ctx c) {
   const int SM = emin_num_sms();
   const int64_t nwin = fast_of(c)->sc.nwin;
-  const int64_t per_sm = getenv("EMIN_SCALAR_GRID") ? atoi(getenv("EMIN_SCALAR_GRID")) : 8;
-  return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * per_sm));
-}
-// grid of the one-off window kernels (Alg. 2 for nv = 1, P out): short
-// in-order CTAs (EMIN_WIN_GRID CTAs per SM, A/B)
-static inline int setup_win_grid(emin_ctx c) {
-  const int SM = emin_num_sms();
-  const int64_t nwin = fast_of(c)->sc.nwin;
-  const int64_t per_sm = getenv("EMIN_WIN_GRID") ? atoi(getenv("EMIN_WIN_GRID")) : 8;
-  return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * per_sm));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * 8));
 }
 // grid of the setup-time masked launches (MM_R0, MM_ENERGY)
 static inline int scalar_spgemm_grid(emin_ctx c) {
@@ -1006,94 +615,16 @@ static inline int scalar_spgemm_grid(emin_ctx c) {
   return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
 }
 // grid of the per-iteration masked launch (MM_ITER)
-static inline int scalar_iter_grid(emin_ctx c) {
-  const ScalarPlan& p = fast_of(c)->sc;
-  switch (p.variant) {
-    case 2: return (int)std::max<int64_t>(1, p.ntiles);
-    case 3: return p.pipe_grid;
-    case 11: case 12: case 13: return p.w8grid;
-    default: return scalar_grid(c);
-  }
-}
+static inline int scalar_iter_grid(emin_ctx c) { return scalar_grid(c); }
 
 static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
                                         cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
   if (mode == MM_ITER) {
-    switch (p.variant) {
-      case 0:
-        k_spgemm_hdr<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, X, out, c->partials);
-        return true;
-      case 4:
-        k_spgemm_mask<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.nwin, p.emask, X, out, c->partials);
-        return true;
-      case 5:     // default: two records per round (119.1 vs 120.8 us with one, config 3)
-        k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
-        return true;
-      case 14:
-        k_spgemm_win2<1><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
-        return true;
-      case 15:
-        k_spgemm_win2<3><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
-        return true;
-      case 16:
-        k_spgemm_win2<4><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
-        return true;
-      case 7:
-      case 8: {
-        const int g = scalar_grid(c);
-        if (p.variant == 7)
-          k_spgemm_win4<false><<<g, 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent),
-                                                 p.w4hdr, p.nwin, X, out,
-                                                 c->partials);
-        else
-          k_spgemm_win4<true><<<g, 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent),
-                                                p.w4hdr, p.nwin, X, out,
-                                                c->partials);
-        return true;
-      }
-      case 11:
-        k_spgemm_win8<<<p.w8grid, W8_WARPS * 32, w8_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
-                                                                      p.w6hdr, p.nwin, X, out, c->partials);
-        return true;
-      case 13: {
-        const auto kfun = p.ellW <= 4 ? k_spgemm_win10<4> : p.ellW <= 6 ? k_spgemm_win10<6> : k_spgemm_win10<8>;
-        kfun<<<p.w8grid, W8_WARPS * 32, w10_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent), p.w4hdr,
-                                                               p.nwin, X, out, c->partials);
-        return true;
-      }
-      case 12:
-        k_spgemm_win9<<<p.w8grid, W8_WARPS * 32, w9_smem_bytes(), s>>>(v, reinterpret_cast<const int4*>(p.ent),
-                                                                      p.w6hdr, p.nwin, X, out, c->partials);
-        return true;
-      case 10: {
-        const int g = scalar_grid(c);
-#define W7(WW) case WW: k_spgemm_win7<WW><<<g, 256, 0, s>>>(v, p.ell, p.w7hdr, p.nwin, X, out, c->partials); break;
-        switch (p.ellW) { W7(4) W7(5) W7(6) W7(7) W7(8) }
-#undef W7
-        return true;
-      }
-      case 9:
-        k_spgemm_win6<<<scalar_grid(c), 256, 0, s>>>(v, reinterpret_cast<const int4*>(p.ent), p.w6hdr, p.nwin, X,
-                                                     out, c->partials);
-        return true;
-      case 6:
-        k_spgemm_win3<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart3, p.nwin3, X, out, c->partials);
-        return true;
-      case 1:
-        k_spgemm_scalar<MM_ITER><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out,
-                                                                c->partials);
-        return true;
-      case 2:
-        k_spgemm_tile<MM_ITER><<<(int)std::max<int64_t>(1, p.ntiles), TILE_T, p.tile_smem, s>>>(
-            v, p.ent, p.hdr, X, X2, out, c->partials);
-        return true;
-      default:
-        k_spgemm_pipe<<<p.pipe_grid, TILE_T, p.pipe_smem, s>>>(v, p.ent, p.hdr, p.ntiles, p.rec_cap, p.rows_cap,
-                                                              X, out, c->partials);
-        return true;
-    }
+    // two records per round (119.1 vs 120.8 us with one, config 3)
+    k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+    return true;
   }
   if (mode == MM_R0E) {                      // fused r0 + E0: the tile kernel only
     if (!p.use_tiles) return false;
@@ -1102,9 +633,8 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
     return true;
   }
   if (!p.use_tiles) {
-    // setup / energy modes on win2's window kernel (EMIN_SETUP_WIN2M=1; measured
-    // slower than the tile kernel on config 3: r0 + E0 0.47 ms either way,
-    // emin_energy 0.34 vs 0.28 ms)
+    // a tile's records exceed shared memory: win2's window kernel (measured
+    // slower than the tile kernel on config 3: emin_energy 0.34 vs 0.28 ms)
     if (mode == MM_R0)
       k_spgemm_win2m<MM_R0><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, X2, out, c->partials);
     else
@@ -1122,19 +652,12 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
 static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
                                       const double* what, unsigned long long* counters, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
-  k_alg2_nv1<<<setup_win_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, Bc, B, frow, what, c->Q, c->w0,
+  k_alg2_nv1<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, Bc, B, frow, what, c->Q, c->w0,
                                             counters);
 }
 static inline void launch_scalar_get_P(emin_ctx c, double* out, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
-  k_get_P_win<<<setup_win_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->w0, c->dw, c->pofs, out);
-}
-static inline void launch_scalar_stage(emin_ctx c, int which, cudaStream_t s) {
-  const ScalarPlan& p = fast_of(c)->sc;
-  if (which == 1)
-    k_stage1_win<<<c->grid_rows, 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->r, c->yb, c->partials);
-  else
-    k_stage2_win<<<c->grid_rows, 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->r, c->y, c->dw);
+  k_get_P_win<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->w0, c->dw, c->pofs, out);
 }
 
 static inline void free_fast_path(emin_ctx c) {
@@ -1143,13 +666,6 @@ static inline void free_fast_path(emin_ctx c) {
   if (f->sc.rowstart) cudaFreeAsync(f->sc.rowstart, c->stream);
   if (f->sc.ent) cudaFreeAsync(f->sc.ent, c->stream);
   if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
-  if (f->sc.whdr) cudaFreeAsync(f->sc.whdr, c->stream);
-  if (f->sc.emask) cudaFreeAsync(f->sc.emask, c->stream);
-  if (f->sc.rowstart3) cudaFreeAsync(f->sc.rowstart3, c->stream);
-  if (f->sc.w4hdr) cudaFreeAsync(f->sc.w4hdr, c->stream);
-  if (f->sc.w6hdr) cudaFreeAsync(f->sc.w6hdr, c->stream);
-  if (f->sc.ell) cudaFreeAsync(f->sc.ell, c->stream);
-  if (f->sc.w7hdr) cudaFreeAsync(f->sc.w7hdr, c->stream);
   delete f;
   c->fast = nullptr;
 }

@@ -303,13 +303,13 @@ extern "C" emin_status emin_pattern(int64_t n, const int64_t* A_rowptr, const in
   const int SM = emin_num_sms();
   std::vector<void*> tmp;
   auto dal = [&](void** p, size_t bytes) -> cudaError_t {
-    cudaError_t e = cudaMallocAsync(p, bytes + 64, s);
+    cudaError_t e = emin_mallocAsync(p, bytes + 64, s);
     if (e == cudaSuccess) tmp.push_back(*p);
     return e;
   };
   auto done = [&](emin_status st, const char* msg) {
     for (void* p : tmp) cudaFreeAsync(p, s);
-    cudaStreamSynchronize(s);
+    emin_pool_trim(s);   // the temporaries are large and one-off: back to the driver
     if (msg) g_pattern_error = msg;
     return st;
   };

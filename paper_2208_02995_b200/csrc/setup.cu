@@ -590,7 +590,7 @@ __global__ void k_block_sums(const double* __restrict__ x, int64_t n, double* __
 // element past an array's last entry (read, never used)
 template <typename T>
 cudaError_t dalloc(T** p, int64_t n, cudaStream_t s) {
-  return cudaMallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1) + 64, s);
+  return emin_mallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1) + 64, s);
 }
 
 }  // namespace
@@ -623,13 +623,15 @@ extern "C" void emin_default_opts(emin_opts* o, int64_t n_global) {
 
 static emin_status fail(emin_ctx ctx, emin_status st, const std::string& msg) {
   g_setup_error = msg;
+  emin_dist_abort(ctx, msg);   // a loopback group must not wait for this rank
   if (ctx) emin_destroy(ctx);
   return st;
 }
 
-// EMIN_TRACE=1: synchronise and print the elapsed host time of each setup phase
+// debug_flags & EMIN_DBG_TRACE: synchronise and print the elapsed host time of
+// each setup phase
 struct SetupTrace {
-  bool on = getenv("EMIN_TRACE") != nullptr;
+  bool on = false;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   void mark(cudaStream_t s, const char* what) {
     if (!on) return;
@@ -669,19 +671,13 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     return fail(ctx, EMIN_ERR_ARG, "precond must be EMIN_PREC_JACOBI or EMIN_PREC_SGS");
   if (opts->start != EMIN_START_GIVEN && opts->start != EMIN_START_MAXVOL)
     return fail(ctx, EMIN_ERR_ARG, "start must be EMIN_START_GIVEN or EMIN_START_MAXVOL");
-  if (opts->precond == EMIN_PREC_SGS && opts->nccl_comm)
-    return fail(ctx, EMIN_ERR_ARG, "the SGS preconditioner runs on one GPU (nccl_comm must be NULL)");
+  if (opts->precond == EMIN_PREC_SGS && (opts->nccl_comm || opts->loopback))
+    return fail(ctx, EMIN_ERR_ARG, "the SGS preconditioner runs on one GPU (nccl_comm / loopback must be NULL)");
+  if (opts->nccl_comm && opts->loopback)
+    return fail(ctx, EMIN_ERR_ARG, "nccl_comm and loopback are mutually exclusive");
 
-  {
-    // keep freed blocks in the stream-ordered pool (repeated setups reuse them)
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
   SetupTrace trace;
+  trace.on = (opts->debug_flags & EMIN_DBG_TRACE) != 0;
   ctx = new emin_ctx_s();
   ctx->opts = *opts;
   ctx->stream = (cudaStream_t)opts->stream;
@@ -692,8 +688,8 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   cudaStream_t s = ctx->stream;
   const int64_t m = ctx->m_owned;
   const int SM = emin_num_sms();
-  if (opts->nccl_comm) {
-    emin_status st = emin_dist_attach(ctx, opts->nccl_comm);
+  if (opts->nccl_comm || opts->loopback) {
+    emin_status st = emin_dist_attach(ctx, opts->nccl_comm, opts->loopback, opts->loopback_rank);
     if (st != EMIN_OK) return fail(ctx, st, ctx->last_error);
   }
 
@@ -793,7 +789,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   ra.cnt_ff = cnt_ff; ra.cnt_fc = cnt_fc; ra.cnt_w = cnt_w; ra.d = ctx->d; ra.dcc = dcc;
   ra.err = err; ra.err_row = err_row; ra.max_row = max_row;
   // short in-order CTAs (config 5 validation 10.2 -> 8.5 ms, fill 13.7 -> 11.7 ms; CTAs per SM)
-  const int grows = getenv("EMIN_ROWS_GRID") ? atoi(getenv("EMIN_ROWS_GRID")) : 32;
+  const int grows = 32;
   k_rows<<<SM * grows, 256, 0, s>>>(ra);
   k_check_B<<<SM * 8, 256, 0, s>>>(m, opts->row_begin, nv, dIsc, cidx, dB, dBc, nc_global, err, err_row);
   SETUP_TRY(cudaGetLastError());
@@ -801,7 +797,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     // every rank fails together; the longest pattern row is global
     emin_status st1 = emin_dist_allreduce_max_i32(ctx, err, s);
     emin_status st2 = emin_dist_allreduce_max_i32(ctx, max_row, s);
-    if (st1 != EMIN_OK || st2 != EMIN_OK) { tmp_free(); return fail(ctx, EMIN_ERR_NCCL, ctx->last_error); }
+    if (st1 != EMIN_OK || st2 != EMIN_OK) { tmp_free(); return fail(ctx, st1 != EMIN_OK ? st1 : st2, ctx->last_error); }
   }
   int32_t h_err[2];
   int64_t h_err_row;
@@ -881,7 +877,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   fa.affcol = ctx->affcol; fa.affval = ctx->affval; fa.afccol = ctx->afccol; fa.afcval = ctx->afcval;
   fa.frow = frow;
   fa.hpos = ctx->dist ? ctx->dist->hpos : nullptr;
-  const int gfill = getenv("EMIN_FILL_GRID") ? atoi(getenv("EMIN_FILL_GRID")) : 64;
+  const int gfill = 64;
   k_fill<<<SM * gfill, 256, 0, s>>>(fa);
   SETUP_TRY(cudaGetLastError());
   if (ctx->dist) {
@@ -929,12 +925,12 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   if (opts->start == EMIN_START_MAXVOL && nF > 0)      // Alg. 1 tentative start (NEXT-3, reading A24)
     emin_maxvol_start(ctx, dBc, dB, frow, what, counters + 2, s);
   bool alg2_done = emin_alg2_fast(ctx, dBc, dB, frow, what, counters, s);
-  if (!alg2_done && ctx->kernel_path == 2 && ctx->max_row <= 128 && !getenv("EMIN_ALG2_ROWS")) {
+  if (!alg2_done && ctx->kernel_path == 2 && ctx->max_row <= 128 && !(opts->debug_flags & EMIN_DBG_ALG2_ROWS)) {
     // nodal path: one QR per F node; rank-deficient nodes redone row by row
     uint8_t* nflag;
     SETUP_TRY(dalloc(&nflag, nF / 3 + 1, s)); temps.push_back(nflag);
     SETUP_TRY(cudaMemsetAsync(nflag, 0, nF / 3 + 1, s));
-    const int64_t ngs = getenv("EMIN_ALG2_GRID") ? atoi(getenv("EMIN_ALG2_GRID")) : 16;
+    const int64_t ngs = 16;   // short in-order CTAs (16 per SM)
     const int ng = (int)std::max<int64_t>(1, std::min<int64_t>((nF / 3 + 3) / 4, (int64_t)SM * ngs));
     if (ctx->max_row <= 32)
       k_alg2_nodal<1><<<ng, 128, 0, s>>>(v, dBc, dB, frow, what, opts->rank_tol, ctx->Q, ctx->w0, counters, nflag);
@@ -967,8 +963,10 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   if (ctx->dist) {
     // W0 on the halo rows (needed by r0 and E0) and the global tr(A_CC)
     emin_status st1 = emin_dist_halo_values(ctx, ctx->w0, s);
-    emin_status st2 = emin_dist_allreduce(ctx, dsum, 1, s);
-    if (st1 != EMIN_OK || st2 != EMIN_OK) { tmp_free(); return fail(ctx, EMIN_ERR_NCCL, ctx->last_error); }
+    emin_status st2 = emin_dist_allreduce(ctx, dsum, dsum + 1, 1, s);
+    if (st2 == EMIN_OK)
+      SETUP_TRY(cudaMemcpyAsync(dsum, dsum + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (st1 != EMIN_OK || st2 != EMIN_OK) { tmp_free(); return fail(ctx, st1 != EMIN_OK ? st1 : st2, ctx->last_error); }
   }
 
   trace.mark(s, "Alg. 2");

@@ -726,22 +726,22 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   const int64_t* dkey = key_own;
   int64_t* tmp = nullptr;
   if (key_own && !c->opts.inputs_on_device) {
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&tmp, sizeof(int64_t) * std::max<int64_t>(c->m_owned, 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&tmp, sizeof(int64_t) * std::max<int64_t>(c->m_owned, 1), s));
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(tmp, key_own, sizeof(int64_t) * c->m_owned, cudaMemcpyHostToDevice, s));
     dkey = tmp;
   }
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->key, sizeof(int64_t) * std::max<int64_t>(nF, 1), s));
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lev, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lvl_rows, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->u, sizeof(double) * std::max<int64_t>(c->nnzW, 1) + 64, s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->key, sizeof(int64_t) * std::max<int64_t>(nF, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lev, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lvl_rows, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->u, sizeof(double) * std::max<int64_t>(c->nnzW, 1) + 64, s));
   int32_t* flag;
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&flag, sizeof(int32_t) * 2, s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&flag, sizeof(int32_t) * 2, s));
   k_sgs_key<<<SM * 4, 256, 0, s>>>(nF, frow, dkey, p->key);
   EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lev, 0, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
   c->launches += 1;
   // nodal path with node-constant keys: levels, buckets and sweeps per F node
   int64_t nunits = nF;                               // rows, or nodes on the nodal path
-  if (!getenv("EMIN_SGS_GENERIC") &&
+  if (!(c->opts.debug_flags & EMIN_DBG_SGS_GENERIC) &&
       emin_nodal_plan(c, &p->nblk, &p->bptr, &p->pm8, &p->pmoff, &p->nFn, &p->max_nb)) {
     int32_t hb = 0;
     EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
@@ -752,7 +752,7 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
     if (!hb) {
       p->nodal = 1;
       nunits = p->nFn;
-      EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->bdir, std::max<int64_t>(c->nnzAFF / 9, 1), s));
+      EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->bdir, std::max<int64_t>(c->nnzAFF / 9, 1), s));
       k_sgs_node_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->key, p->bdir);
       c->launches += 1;
     }
@@ -774,7 +774,7 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   int32_t hmax = 0;
   EMIN_CUDA_TRY(c, cudaMemsetAsync(flag + 1, 0, sizeof(int32_t), s));
   // count into a buffer of nF + 1 (levels <= nF - 1)
-  EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->lvl_cnt, sizeof(int32_t) * (nunits + 2), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lvl_cnt, sizeof(int32_t) * (nunits + 2), s));
   EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lvl_cnt, 0, sizeof(int32_t) * (nunits + 2), s));
   k_sgs_count<<<SM * 4, 256, 0, s>>>(nunits, p->lev, p->lvl_cnt, flag + 1);
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(&hmax, flag + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -794,17 +794,17 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
   c->launches += 2;
   // scalar path: per-level windows of <= 32 entries (rows never straddle)
   p->rec = p->nodal ? nullptr : emin_scalar_records(c);
-  if (p->rec && p->nlev && !getenv("EMIN_SGS_GENERIC")) {
+  if (p->rec && p->nlev && !(c->opts.debug_flags & EMIN_DBG_SGS_GENERIC)) {
     // windows built on the GPU (k_sgs_w*): only nlev + 1 offsets visit the host
     int64_t *len, *pst, *lptr, *base, *wbase, *tot2, *scr;
     const int64_t nl = p->nlev;
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&len, sizeof(int64_t) * (nF + 1), s));
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&pst, sizeof(int64_t) * (nF + 1), s));
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&lptr, sizeof(int64_t) * (nl + 1), s));
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&base, sizeof(int64_t) * (nl + 1), s));
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&wbase, sizeof(int64_t) * (nl + 1), s));
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&tot2, sizeof(int64_t), s));
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&scr, sizeof(int64_t) * emin_scan_scratch_elems(nF + 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&len, sizeof(int64_t) * (nF + 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&pst, sizeof(int64_t) * (nF + 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&lptr, sizeof(int64_t) * (nl + 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&base, sizeof(int64_t) * (nl + 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&wbase, sizeof(int64_t) * (nl + 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&tot2, sizeof(int64_t), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&scr, sizeof(int64_t) * emin_scan_scratch_elems(nF + 1), s));
     k_sgs_wlen<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, c->wptr, len);
     EMIN_CUDA_TRY(c, emin_scan_i64(len, pst, nF, tot2, scr, s));
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(pst + nF, tot2, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
@@ -818,11 +818,11 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
     for (int64_t L = 0; L < nl; ++L) p->win_ptr[L + 1] = p->win_ptr[L] + (hb[L + 1] - hb[L] + S - 1) / S;
     const int64_t nw = p->win_ptr[nl];
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(wbase, p->win_ptr.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->win, sizeof(int4) * std::max<int64_t>(nw, 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->win, sizeof(int4) * std::max<int64_t>(nw, 1), s));
     EMIN_CUDA_TRY(c, cudaMemsetAsync(p->win, 0, sizeof(int4) * std::max<int64_t>(nw, 1), s));
     k_sgs_wfirst<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, p->lev, lptr, base, wbase, pst, p->win, S);
     k_sgs_wfill<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, p->lev, base, wbase, pst, len, p->win, S);
-    EMIN_CUDA_TRY(c, cudaMallocAsync((void**)&p->dir, std::max<int64_t>(c->nnzAFF, 1), s));
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->dir, std::max<int64_t>(c->nnzAFF, 1), s));
     k_sgs_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->dir);
     c->launches += 6;
     void* fr[] = {len, pst, lptr, base, wbase, tot2, scr};
@@ -848,8 +848,8 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   auto grid_for = [&](int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)SM * 8));
   };
-  // the sweeps (no partial sums): EMIN_SGS_GRID CTAs per SM (A/B)
-  const int64_t sweep_per_sm = getenv("EMIN_SGS_GRID") ? atoi(getenv("EMIN_SGS_GRID")) : 8;
+  // the sweeps (no partial sums): 8 CTAs per SM
+  const int64_t sweep_per_sm = 8;
   auto sweep_grid = [&](int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)SM * sweep_per_sm));
   };

@@ -1,5 +1,7 @@
 // util.cu -- device-wide exclusive scan (setup-time index preparation) and
 // small host helpers.
+#include <mutex>
+
 #include "emin_internal.cuh"
 
 namespace {
@@ -111,6 +113,53 @@ cudaError_t emin_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* t
   k_scan_tile_sums<<<1, 1024, 0, s>>>(scratch, nb, total_dev);
   k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(in, out, n, scratch);
   return cudaGetLastError();
+}
+
+// Library-owned stream-ordered memory pool, one per device (the
+// release threshold of the device's DEFAULT pool is process-wide state and
+// must not be changed by a library).  Freed blocks stay cached in this pool
+// (repeated emin_setup calls reuse them) and are returned to the driver by
+// emin_release_memory(), and at the end of emin_galerkin / emin_pattern.
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[64] = {};
+
+cudaMemPool_t emin_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pool[dev] = p;
+  }
+  return g_pool[dev];
+}
+
+cudaError_t emin_mallocAsync(void** p, size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = emin_pool();
+  if (!pool) return cudaMallocAsync(p, bytes, s);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+void emin_pool_trim(cudaStream_t s) {
+  cudaMemPool_t pool = emin_pool();
+  if (!pool) return;
+  cudaStreamSynchronize(s);
+  cudaMemPoolTrimTo(pool, 0);
+}
+
+extern "C" void emin_release_memory(void) {
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (cudaMemPool_t p : g_pool)
+    if (p) cudaMemPoolTrimTo(p, 0);
 }
 
 int emin_num_sms() {

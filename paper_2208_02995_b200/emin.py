@@ -39,7 +39,13 @@ class emin_opts(C.Structure):
                 ("stream", C.c_void_p), ("nccl_comm", C.c_void_p),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64),
                 ("inputs_on_device", C.c_int32), ("precond", C.c_int32), ("sgs_key", C.c_void_p),
-                ("start", C.c_int32)]
+                ("start", C.c_int32), ("loopback", C.c_void_p), ("loopback_rank", C.c_int32),
+                ("debug_flags", C.c_int32)]
+
+
+# emin_opts.debug_flags bits (include/emin.h): alternative kernel paths for tests / A/B
+DBG_FORCE_GENERIC, DBG_NO_R0E, DBG_SGS_GENERIC, DBG_TRACE, DBG_FUSE_SCALARS, DBG_ALG2_ROWS = 1, 2, 4, 8, 16, 32
+GALERKIN_DEVICE, GALERKIN_POINT = 1, 2
 
 
 EMIN_PREC_JACOBI, EMIN_PREC_SGS = 0, 1
@@ -54,14 +60,16 @@ class emin_report_t(C.Structure):
                 ("n_frozen_rows", C.c_int64), ("n_fine", C.c_int64), ("nnz_W", C.c_int64),
                 ("nnz_AFF", C.c_int64), ("kernel_path", C.c_int32), ("nranks", C.c_int32),
                 ("launches", C.c_int64), ("precond", C.c_int32), ("sgs_levels", C.c_int64),
-                ("n_maxvol_fail", C.c_int64)]
+                ("n_maxvol_fail", C.c_int64), ("rank", C.c_int32), ("n_halo_rows", C.c_int64),
+                ("n_halo_entries", C.c_int64), ("n_send_entries", C.c_int64)]
 
 
 EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "emin_get_P",
             "emin_reset", "emin_report", "emin_destroy", "emin_status_str", "emin_last_error",
             "emin_set_profiling", "emin_kernel_times", "emin_get_layout", "emin_nccl_unique_id",
             "emin_nccl_comm_init", "emin_nccl_comm_destroy", "emin_pattern", "emin_pattern_error",
-            "emin_galerkin", "emin_galerkin_error", "emin_galerkin_path"]
+            "emin_galerkin", "emin_galerkin_error", "emin_galerkin_path", "emin_loopback_create",
+            "emin_loopback_destroy", "emin_release_memory"]
 
 
 def load_library():
@@ -118,6 +126,12 @@ def load_library():
     lib.emin_galerkin_error.restype = C.c_char_p
     lib.emin_galerkin_path.argtypes = []
     lib.emin_galerkin_path.restype = i32
+    lib.emin_loopback_create.argtypes = [C.POINTER(P), i32]
+    lib.emin_loopback_create.restype = i32
+    lib.emin_loopback_destroy.argtypes = [P]
+    lib.emin_loopback_destroy.restype = None
+    lib.emin_release_memory.argtypes = []
+    lib.emin_release_memory.restype = None
     _lib = lib
     return lib
 
@@ -160,11 +174,15 @@ def _prep(a, np_dtype, torch_dtype=None):
 def emin_setup(n_global, nc_global, A_rowptr, A_col, A_val, is_coarse, P_rowptr, P_col, P_val,
                nv, B, Bc, *, block_size=1, rank_tol=1e-10, tau=0.0, project_after_jacobi=0,
                stagnation_rel=1e-30, stream=None, nccl_comm=None, row_begin=0, row_end=None,
-               precond="jacobi", sgs_key=None, start="given"):
+               precond="jacobi", sgs_key=None, start="given", loopback=None, loopback_rank=0,
+               debug_flags=0):
     """emin_setup (include/emin.h).  Returns the opaque context handle.
     precond: "jacobi" | "sgs" (or EMIN_PREC_*); sgs_key: per owned row,
     same side (host / cuda) as the other arrays, or None.  start: "given"
-    (P_val / least-norm) or "maxvol" (Alg. 1's tentative start)."""
+    (P_val / least-norm) or "maxvol" (Alg. 1's tentative start).
+    loopback / loopback_rank: an emin_loopback_create handle and this
+    context's rank in it (R contexts on one device, one thread each).
+    debug_flags: EMIN_DBG_* bits (alternative kernel paths for tests)."""
     lib = load_library()
     import torch
     arrs = [A_rowptr, A_col, A_val, is_coarse, P_rowptr, P_col, P_val, B, Bc]
@@ -199,6 +217,9 @@ def emin_setup(n_global, nc_global, A_rowptr, A_col, A_val, is_coarse, P_rowptr,
     o.precond = PRECONDS[precond] if isinstance(precond, str) else int(precond)
     o.sgs_key = _ptr(key)
     o.start = STARTS[start] if isinstance(start, str) else int(start)
+    o.loopback = loopback
+    o.loopback_rank = int(loopback_rank)
+    o.debug_flags = int(debug_flags)
     h = C.c_void_p()
     st = lib.emin_setup(C.byref(h), int(n_global), int(nc_global), *[_ptr(a) for a in keep[:7]],
                         int(nv), _ptr(keep[7]), _ptr(keep[8]), C.byref(o))
@@ -293,10 +314,11 @@ def emin_pattern(n, A_rowptr, A_col, is_coarse, block_size, nv, Bc, nc, l0=2, lm
     return rp, col[:nnz.value]
 
 
-def emin_galerkin(n, nc, A_rowptr, A_col, A_val, P_rowptr, P_col, P_val, stream=None):
+def emin_galerkin(n, nc, A_rowptr, A_col, A_val, P_rowptr, P_col, P_val, stream=None, point=False):
     """emin_galerkin (include/emin.h): A_c = P^T A P on the GPU.  Inputs all
     host numpy arrays (returns numpy) or all CUDA tensors (returns CUDA
-    tensors, nothing leaves the device but the nnz count)."""
+    tensors, nothing leaves the device but the nnz count).  point=True forces
+    the point product (EMIN_GALERKIN_POINT)."""
     lib = load_library()
     import torch
     dev = _is_torch(A_rowptr)
@@ -314,8 +336,9 @@ def emin_galerkin(n, nc, A_rowptr, A_col, A_val, P_rowptr, P_col, P_val, stream=
         rp = np.zeros(int(nc) + 1, np.int64)
     nnz = C.c_int64(0)
     sp = C.c_void_p(int(stream))
+    flags = (GALERKIN_DEVICE if dev else 0) | (GALERKIN_POINT if point else 0)
     st = lib.emin_galerkin(int(n), int(nc), *[_ptr(a) for a in arrs], _ptr(rp), None, None, 0, C.byref(nnz),
-                           int(dev), sp)
+                           flags, sp)
     if st != 0:
         raise EminError(st, lib.emin_galerkin_error().decode())
     m = max(nnz.value, 1)
@@ -325,7 +348,7 @@ def emin_galerkin(n, nc, A_rowptr, A_col, A_val, P_rowptr, P_col, P_val, stream=
     else:
         col, val = np.zeros(m, np.int32), np.zeros(m, np.float64)
     st = lib.emin_galerkin(int(n), int(nc), *[_ptr(a) for a in arrs], _ptr(rp), _ptr(col), _ptr(val), m,
-                           C.byref(nnz), int(dev), sp)
+                           C.byref(nnz), flags, sp)
     if st != 0:
         raise EminError(st, lib.emin_galerkin_error().decode())
     return rp, col[:nnz.value], val[:nnz.value]
@@ -356,6 +379,21 @@ def nccl_comm_from_torch(group=None):
     obj = [emin_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return emin_nccl_comm_init(world, obj[0], rank)
+
+
+def emin_loopback_create(nranks):
+    """In-process loopback group of ``nranks`` contexts (include/emin.h)."""
+    h = C.c_void_p()
+    _check(load_library().emin_loopback_create(C.byref(h), int(nranks)))
+    return h
+
+
+def emin_loopback_destroy(h):
+    load_library().emin_loopback_destroy(h)
+
+
+def emin_release_memory():
+    load_library().emin_release_memory()
 
 
 def emin_set_profiling(ctx, on):

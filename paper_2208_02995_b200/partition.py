@@ -64,3 +64,32 @@ def halo_plan(A_rowptr, A_col, is_coarse, ranges, rank):
         franges.append((int(ff[0]), int(ff[-1]) + 1) if ff.size else (0, 0))
     owners = np.array([next(p for p, (x, y) in enumerate(franges) if x <= h < y) for h in halo], dtype=np.int64)
     return halo, owners, (int(fb), int(fe)), franges
+
+
+def rank_slice(prob, rb, re_):
+    """The inputs a rank passes to emin_setup for its rows [rb, re_): its
+    rows of A, P and B only (row pointers rebased to 0, global column ids),
+    plus the global is_coarse and B_c (include/emin.h).  Host numpy arrays."""
+    a0, a1 = int(prob.A_rowptr[rb]), int(prob.A_rowptr[re_])
+    p0, p1 = int(prob.P_rowptr[rb]), int(prob.P_rowptr[re_])
+    return dict(
+        A_rowptr=np.ascontiguousarray(prob.A_rowptr[rb:re_ + 1] - a0),
+        A_col=np.ascontiguousarray(prob.A_col[a0:a1]),
+        A_val=np.ascontiguousarray(prob.A_val[a0:a1]),
+        is_coarse=prob.is_coarse,
+        P_rowptr=np.ascontiguousarray(prob.P_rowptr[rb:re_ + 1] - p0),
+        P_col=np.ascontiguousarray(prob.P_col[p0:p1]),
+        P_val=None if prob.P_val is None else np.ascontiguousarray(prob.P_val[p0:p1]),
+        B=np.ascontiguousarray(prob.B[rb:re_]),
+        Bc=prob.Bc,
+    )
+
+
+def plane_rows(prob):
+    """Rows of one z-plane of the problem's lexicographic grid (the cut unit
+    of partition_rows; whole nodes for the 3-dof elasticity rows)."""
+    dims = prob.meta["dims"]
+    per = 3 if prob.block_size == 3 else 1
+    if len(dims) > 2 and dims[2] > 1:
+        return int(dims[0] * dims[1] * per)
+    return int(dims[0] * per)          # 2D: one grid line

@@ -1,4 +1,4 @@
-"""EMIN_TRACE=1 phases of emin_setup (device inputs) for a config, after a
+"""EMIN_DBG_TRACE phases of emin_setup (device inputs) for a config, after a
 warm-up setup, plus the host-timed iterate/energy/get_P/destroy of one step."""
 import os
 import sys
@@ -13,11 +13,9 @@ from workloads.problems import make_config  # noqa: E402
 
 prob = make_config(sys.argv[1] if len(sys.argv) > 1 else "3")
 for rep in range(3):
-    if rep == 2:
-        os.environ["EMIN_TRACE"] = "1"
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    g = Emin.from_problem(prob, device="cuda", stagnation_rel=0.0)
+    g = Emin.from_problem(prob, device="cuda", stagnation_rel=0.0, debug_flags=8 if rep == 2 else 0)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     g.iterate(prob.iters, want=False)

@@ -1,7 +1,7 @@
 """Host-timed breakdown of one bench step (setup / iterate / energy / get_P /
-destroy) with EMIN_TRACE=1 phase timing of emin_setup.
+destroy) with the EMIN_DBG_TRACE phase timing of emin_setup.
 
-  EMIN_TRACE=1 python profiles/step_breakdown.py [config]
+  python profiles/step_breakdown.py [config]
 """
 import json
 import os
@@ -32,7 +32,7 @@ def main():
         t0 = time.perf_counter()
         h = E.emin_setup(prob.n, prob.nc, dev["A_rowptr"], dev["A_col"], dev["A_val"], dev["is_coarse"],
                          dev["P_rowptr"], dev["P_col"], dev["P_val"], prob.nv, dev["B"], dev["Bc"],
-                         block_size=prob.block_size, stagnation_rel=0.0)
+                         block_size=prob.block_size, stagnation_rel=0.0, debug_flags=8 if rep == 3 else 0)
         torch.cuda.synchronize()
         t["setup"] = time.perf_counter() - t0
         t0 = time.perf_counter()

@@ -63,7 +63,7 @@ def test_galerkin_bitwise_matches_oracle(name, size, k, device):
 
 
 @pytest.mark.parametrize("name,size", [("4", 4), ("4", 7), ("5", 5)])
-def test_galerkin_block_path_equals_point_path(name, size, monkeypatch):
+def test_galerkin_block_path_equals_point_path(name, size):
     # elasticity inputs take the 3x3-block product; it must give the point
     # path's (and the oracle's) bits
     import torch
@@ -75,8 +75,7 @@ def test_galerkin_block_path_equals_point_path(name, size, monkeypatch):
             for a in (p.A_rowptr, p.A_col, p.A_val, p.P_rowptr, p.P_col, Pv)]
     blk = [t.cpu().numpy() for t in emin_galerkin(p.n, p.nc, *args)]
     assert load_library().emin_galerkin_path() == 1
-    monkeypatch.setenv("EMIN_GALERKIN_POINT", "1")
-    pt = [t.cpu().numpy() for t in emin_galerkin(p.n, p.nc, *args)]
+    pt = [t.cpu().numpy() for t in emin_galerkin(p.n, p.nc, *args, point=True)]
     assert load_library().emin_galerkin_path() == 0
     _assert_bitwise(blk, pt)
 

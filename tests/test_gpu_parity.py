@@ -73,26 +73,19 @@ def test_parity_small(name, size, k):
     assert rep["n_svd_rows"] == o.n_svd and rep["n_frozen_rows"] == o.n_frozen
 
 
-SCALAR_VARIANTS = [("EMIN_SPGEMM", v) for v in ("win", "win2", "win2g1", "win2g4", "win4", "win5", "win6", "win7", "win8", "win9", "win10",
-                                                 "mask", "tile", "hdr", "pipe")] + [("EMIN_SETUP_WIN2M", "1")]
-NODAL_VARIANTS = [("EMIN_NODAL", v) for v in ("v2", "v2p", "v2cs", "v2x", "v2xp", "s", "plain")]
-
-
-@pytest.mark.parametrize("name,size,path", [("3", 12, 1), ("2b", 10, 1), ("3", 17, 1), ("4", 4, 2), ("5", 8, 2)])
-@pytest.mark.parametrize("env,variant", SCALAR_VARIANTS + NODAL_VARIANTS)
-def test_kernel_paths_agree(name, size, path, env, variant, monkeypatch):
-    """The specialised kernels (scalar window/mask/tile/header variants,
-    nodal 3x3 variants) against the generic warp-per-row kernel."""
+@pytest.mark.parametrize("name,size,path", [("3", 12, 1), ("2b", 10, 1), ("3", 17, 1), ("1b", None, 1),
+                                            ("4", 4, 2), ("5", 8, 2), ("4", 3, 2)])
+def test_kernel_paths_agree(name, size, path):
+    """The specialised kernels of the library (scalar window kernel + tile
+    kernel, nodal 3x3 kernel) against the generic warp-per-row kernel
+    (EMIN_DBG_FORCE_GENERIC)."""
     from paper_2208_02995_b200 import Emin
+    from paper_2208_02995_b200.emin import DBG_FORCE_GENERIC
     from workloads.problems import make_config
-    if (path == 2) != (env == "EMIN_NODAL"):   # scalar variants (EMIN_SPGEMM, EMIN_SETUP_WIN2M) vs nodal
-        pytest.skip("variant of the other kernel path")
     prob = make_config(name, size=size)
-    monkeypatch.setenv(env, variant)
     fast = Emin.from_problem(prob)
     assert fast.report()["kernel_path"] == path
-    monkeypatch.setenv("EMIN_FORCE_GENERIC", "1")
-    gen = Emin.from_problem(prob)
+    gen = Emin.from_problem(prob, debug_flags=DBG_FORCE_GENERIC)
     assert gen.report()["kernel_path"] == 0
     kf, dEf = fast.iterate(25)
     kg, dEg = gen.iterate(25)
@@ -343,7 +336,7 @@ def test_sgs_beats_jacobi_per_iteration_on_gpu():
 
 
 @pytest.mark.parametrize("name,size,kind", [("3", 12, "color"), ("1b", None, "natural")])
-def test_sgs_generic_sweep_equals_window_sweep(name, size, kind, monkeypatch):
+def test_sgs_generic_sweep_equals_window_sweep(name, size, kind):
     """The windowed lane-per-entry SGS sweeps (scalar path) against the
     generic warp-per-row sweeps: same arithmetic, same order."""
     from paper_2208_02995_b200 import Emin
@@ -351,8 +344,7 @@ def test_sgs_generic_sweep_equals_window_sweep(name, size, kind, monkeypatch):
     prob = make_config(name, size=size)
     key = sgs_key(prob, kind)
     a = Emin.from_problem(prob, precond="sgs", sgs_key=key)
-    monkeypatch.setenv("EMIN_SGS_GENERIC", "1")
-    b = Emin.from_problem(prob, precond="sgs", sgs_key=key)
+    b = Emin.from_problem(prob, precond="sgs", sgs_key=key, debug_flags=4)   # EMIN_DBG_SGS_GENERIC
     ka, dEa = a.iterate(20)
     kb, dEb = b.iterate(20)
     assert ka == kb and np.allclose(dEa, dEb, rtol=1e-12)
@@ -382,7 +374,7 @@ def test_full_size_elasticity_config5_properties():
 
 
 @pytest.mark.parametrize("name,size,kind", [("4", 3, "color"), ("4", 4, "natural"), ("5", 8, "color")])
-def test_sgs_nodal_sweep_equals_generic_sweep(name, size, kind, monkeypatch):
+def test_sgs_nodal_sweep_equals_generic_sweep(name, size, kind):
     """The node-level SGS sweeps (elasticity, 3x3 blocks) against the generic
     row-level sweeps: same solves, own-node terms summed last."""
     from paper_2208_02995_b200 import Emin
@@ -390,8 +382,7 @@ def test_sgs_nodal_sweep_equals_generic_sweep(name, size, kind, monkeypatch):
     prob = make_config(name, size=size)
     key = sgs_key(prob, kind)
     a = Emin.from_problem(prob, precond="sgs", sgs_key=key)
-    monkeypatch.setenv("EMIN_SGS_GENERIC", "1")
-    b = Emin.from_problem(prob, precond="sgs", sgs_key=key)
+    b = Emin.from_problem(prob, precond="sgs", sgs_key=key, debug_flags=4)   # EMIN_DBG_SGS_GENERIC
     assert a.report()["sgs_levels"] < b.report()["sgs_levels"]      # node levels vs row levels
     ka, dEa = a.iterate(20)
     kb, dEb = b.iterate(20)
@@ -452,19 +443,15 @@ def test_pattern_gpu_matches_oracle_and_generator(name, size):
         assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
 
 
-@pytest.mark.parametrize("name,size,env", [("3", 12, None), ("4", 3, None), ("2b", 10, None),
-                                          ("4", 3, ("EMIN_FORCE_GENERIC", "1"))])
-def test_fused_r0_energy_setup_equals_separate(name, size, env, monkeypatch):
+@pytest.mark.parametrize("name,size,dbg", [("3", 12, 0), ("4", 3, 0), ("2b", 10, 0), ("4", 3, 1)])
+def test_fused_r0_energy_setup_equals_separate(name, size, dbg):
     """r0 and E0 from one MM_R0E pass equal the separate MM_R0 / MM_ENERGY
     passes bitwise (same arithmetic per entry, same partial order)."""
     from paper_2208_02995_b200 import Emin
     from workloads.problems import make_config
     prob = make_config(name, size=size)
-    if env:
-        monkeypatch.setenv(*env)
-    a = Emin.from_problem(prob)
-    monkeypatch.setenv("EMIN_NO_R0E", "1")
-    b = Emin.from_problem(prob)
+    a = Emin.from_problem(prob, debug_flags=dbg)
+    b = Emin.from_problem(prob, debug_flags=dbg | 2)     # EMIN_DBG_NO_R0E
     assert a.report()["E0"] == b.report()["E0"]
     ka, dEa = a.iterate(10)
     kb, dEb = b.iterate(10)
