@@ -1,25 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the restricted-PCG energy-minimisation hot path on B200.
 
-One STEP = one pass of the whole hot path (SURVEY §8a rows a0-a10) over the
+One STEP = one pass of the whole hot path (SURVEY §8a rows a0-a11) over the
 synthetic workload, through the C ABI: emin_setup from device-resident inputs
-(validation, index prep, Alg. 2, r0, E0) -> emin_iterate(k) (k restricted-PCG
-steps, CUDA graph) -> emin_energy -> emin_get_P (into a device buffer) ->
-emin_destroy.  ``value`` = P-nonzero updates per second = nnz(W) * k * K /
-(device time of the K timed steps), max over ranks.
+(validation, index prep, halo plan, Alg. 2, r0, E0) -> emin_iterate(k) (k
+restricted-PCG steps, CUDA graph) -> emin_energy -> emin_get_P (into a device
+buffer) -> emin_destroy.  ``value`` = P-nonzero updates per second =
+nnz(W) * k * K / (device time of the K timed steps), max over ranks.
 
 Default workload: BASELINE config 3 (FV lognormal 128^3, 40 iterations), the
 configuration BASELINE.json's metric ("... at 1/2/4/8 GPU") is quoted on.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl reference]
 
+--gpus N without a torchrun environment launches N ranks itself (one process
+per GPU, NCCL); it fails if fewer than N GPUs are visible.  Each rank passes
+emin_setup only its own rows of A, P and B (partition.rank_slice).
 --impl reference runs the CPU oracle (the tier's reference arm) on the host.
+--dry-run (CPU, gloo): the launcher and the partition without a GPU (tests).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,10 +46,16 @@ WORKLOADS = {
     "4": "config4: Q1 elasticity 48^3, E=1, nu=0.3, bottom clamped, 6 RBMs, 30 it",
     "5": "config5: Q1 elasticity 160^3, 8 layers E in 10^U(-2,2), nu=0.25, 6 RBMs, 40 it",
 }
+KEYS = ["A_rowptr", "A_col", "A_val", "is_coarse", "P_rowptr", "P_col", "P_val", "B", "Bc"]
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def workload_name(args):
+    w = WORKLOADS.get(args.config, args.config)
+    return w if args.size is None else f"{w} [reduced size {args.size}]"
 
 
 def measured_peak():
@@ -66,6 +78,16 @@ def iteration_algorithmic_bytes(prob, nnzW, nnzAFF, nF):
     """SURVEY §8d B_iter (fused two-stage schedule): 12 nnz(A_FF) + 4 (n_F+1)
     + nnz(W) (84 + 8 nv)."""
     return 12 * nnzAFF + 4 * (nF + 1) + nnzW * (84 + 8 * prob.nv)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -114,27 +136,78 @@ class ClockSampler:
                                    default=None)}
 
 
-def run_reference(args, prob, rank):
-    """The tier's reference arm: the CPU oracle as it stands, one thread."""
-    if rank != 0:
-        return None
+# ---------------------------------------------------------------------------
+# the CPU oracle legs (reference arm, cpu_baseline): the only places bench.py
+# executes oracle/
+# ---------------------------------------------------------------------------
+
+def oracle_step_rate(prob, threads, budget_s):
+    """One oracle step of ``prob`` (setup + k iterations + energy + P out) on
+    ``threads`` host threads, the iteration count bounded so the step takes
+    about ``budget_s``.  Returns (updates/s, description, seconds, k_used)."""
+    import oracle
     from oracle import Oracle
+    oracle.set_threads(threads)
     k = prob.iters
-    nnzW = prob.nnz_W
-    steps, warm = args.steps, args.warmup
-    # one step = one whole oracle pass (setup + k iterations + energy + P out);
-    # bounded: fewer iterations per step if the full run would exceed ~4 min
     t0 = time.perf_counter()
     o = Oracle(prob)
-    o.iterate(1)
-    t_probe = time.perf_counter() - t0
-    est = t_probe + (k - 1) * 0.25 * t_probe
-    k_step = k
+    t_setup = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    kd1, _ = o.iterate(1)
+    t_it = time.perf_counter() - t1
+    k_s = max(0, min(k - 1, int((budget_s - t_setup) / max(t_it, 1e-4)) - 1))
+    t1 = time.perf_counter()
+    kd2, _ = o.iterate(k_s) if k_s else (0, None)
+    t_its = time.perf_counter() - t1
+    o.energy()
+    o.get_P()
+    tot = time.perf_counter() - t0
+    iters = kd1 + kd2
+    v = prob.nnz_W * iters / tot
+    desc = (f"setup {t_setup:.2f} s + {iters} of {k} iterations ({(t_it + t_its) / max(iters, 1):.3f} s/it) "
+            f"+ energy + P = {tot:.1f} s on {threads} thread(s)")
+    return v, desc, tot, iters
+
+
+def cpu_baseline(prob, args):
+    """The oracle as it stands on this host: all cores, and 1 thread (SURVEY
+    §8d / BASELINE.md §3), each a bounded sample of the same workload (one
+    step, iterations capped to ~15 s per leg).  Config 5 is sampled at the
+    generator's 40^3 size (the full oracle needs ~1 min per iteration)."""
+    import oracle
+    nproc = os.cpu_count() or 1
+    sample_prob, note = prob, ""
+    if args.config == "5" and prob.n > 3_000_000:
+        from workloads.problems import make_config
+        sample_prob = make_config("5", size=40)
+        note = f"same generator at 40^3 elements ({sample_prob.n} dofs): "
+    v_all, d_all, _, _ = oracle_step_rate(sample_prob, nproc, 15.0)
+    v_one, d_one, _, _ = oracle_step_rate(sample_prob, 1, 15.0)
+    oracle.set_threads(nproc)
+    return {"value": v_all, "unit": UNIT, "cores": nproc, "kind": "oracle",
+            "sample": note + "one oracle step of the workload: " + d_all,
+            "cpu_model": cpu_model(), "nproc": nproc,
+            "single_thread": {"value": v_one, "cores": 1, "sample": note + d_one}}
+
+
+def run_reference(args, rank):
+    """The tier's reference arm: the CPU oracle as it stands, all host cores,
+    rank 0 only (the other ranks exit without work)."""
+    if rank != 0:
+        return None
+    from workloads.problems import make_config
+    prob = make_config(args.config, size=args.size)
+    nproc = os.cpu_count() or 1
+    k = prob.iters
+    steps, warm = args.steps, args.warmup
+    # bounded: each step at most ~240 s / (steps + warmup) of CPU time
     budget = 240.0 / max(1, steps + warm)
-    if est > budget:
-        k_step = max(1, int(k * budget / est))
+    v, desc, _, k_step = oracle_step_rate(prob, nproc, budget)
     times = []
     for s in range(warm + steps):
+        import oracle
+        from oracle import Oracle
+        oracle.set_threads(nproc)
         t0 = time.perf_counter()
         o = Oracle(prob)
         kd, _ = o.iterate(k_step)
@@ -144,51 +217,83 @@ def run_reference(args, prob, rank):
         if s >= warm:
             times.append(dt)
     tot = sum(times)
-    v = nnzW * k_step * steps / tot
-    sample = (f"{WORKLOADS[args.config]}: full oracle step (setup + {k_step} of {k} iterations + "
-              f"energy + P) per step, single-threaded C, {steps} timed steps")
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+    v = prob.nnz_W * k_step * steps / tot
+    sample = (f"{workload_name(args)}: full oracle step (setup + {k_step} of {k} iterations + energy + P) "
+              f"per step, C + OpenMP on {nproc} threads ({cpu_model()}), {steps} timed steps")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": warm, "ms_per_step": 1e3 * tot / steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "iters": k_step},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": {"workload": workload_name(args), "iters": k_step},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nproc, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    return line
 
 
-def cpu_baseline(prob, args):
-    """Oracle timed on the host, bounded sample (one full step, ~10-20 s).
-    For the large configs (4, 5) the sample is the same generator at a
-    reduced size (the oracle needs ~1 min per iteration at 160^3)."""
-    from oracle import Oracle
-    if args.config in ("4", "5") and prob.n > 400000:
-        from workloads.problems import make_config
-        small = make_config(args.config, size=24)
-        res = cpu_baseline(small, argparse.Namespace(config="small"))
-        res["sample"] = f"same generator at 24^3 elements ({small.n} dofs): " + res["sample"]
-        return res
-    k = prob.iters
-    t0 = time.perf_counter()
-    o = Oracle(prob)
-    t_setup = time.perf_counter() - t0
-    # bound the sample to ~25 s of CPU work
-    t1 = time.perf_counter()
-    o.iterate(1)
-    t_it = time.perf_counter() - t1
-    k_s = max(1, min(k - 1, int(20.0 / max(t_it, 1e-3))))
-    t1 = time.perf_counter()
-    kd, _ = o.iterate(k_s)
-    t_its = time.perf_counter() - t1
-    o.energy()
-    o.get_P()
-    tot = time.perf_counter() - t0
-    iters = 1 + kd
-    v = prob.nnz_W * iters / tot
-    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"one oracle step of the same workload: setup ({t_setup:.2f} s) + {iters} of "
-                      f"{k} iterations ({(t_it + t_its) / iters:.3f} s/it) + energy + P, "
-                      f"single-threaded C (-O2), {tot:.1f} s"}
+# ---------------------------------------------------------------------------
+# launcher: --gpus N without torchrun spawns the N ranks itself
+# ---------------------------------------------------------------------------
 
+def free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args):
+    n = args.gpus
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < n:
+            print(json.dumps({"error": f"--gpus {n} needs {n} visible GPUs, found {have}", "n_gpus": n}),
+                  flush=True)
+            log(f"[bench] --gpus {n}: only {have} GPU(s) visible; refusing to time fewer ranks than asked")
+            return 2
+    port = free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        out = None if r == 0 else subprocess.DEVNULL
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=out))
+    rcs = [p.wait() for p in procs]
+    return max(rcs)
+
+
+def dry_run(args, world, rank):
+    """CPU-only check of the launcher and the partition: every rank builds
+    its slice, the ranks agree over gloo, rank 0 prints a summary line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2208_02995_b200.partition import partition_rows, plane_rows, rank_slice
+    from workloads.problems import make_config
+    prob = make_config(args.config, size=args.size)
+    if world > 1:
+        dist.init_process_group("gloo")
+    ranges = partition_rows(prob.P_rowptr, prob.is_coarse, world, plane=plane_rows(prob))
+    rb, re_ = ranges[rank]
+    a = rank_slice(prob, rb, re_)
+    mine = torch.tensor([rb, re_, int(a["P_rowptr"][-1]), int(a["A_rowptr"][-1]), os.getpid()], dtype=torch.int64)
+    allv = [torch.zeros_like(mine) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(allv, mine)
+    else:
+        allv = [mine]
+    allv = [t.tolist() for t in allv]
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    covers = allv[0][0] == 0 and allv[-1][1] == prob.n and all(allv[i][1] == allv[i + 1][0] for i in range(world - 1))
+    print(json.dumps({"dry_run": True, "n_gpus": world, "ranges": [v[:2] for v in allv],
+                      "nnz_P_per_rank": [v[2] for v in allv], "nnz_A_per_rank": [v[3] for v in allv],
+                      "pids": [v[4] for v in allv], "covers": bool(covers),
+                      "nnz_P_total_ok": sum(v[2] for v in allv) == int(prob.P_rowptr[-1]),
+                      "workload": workload_name(args)}), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
 
 def main():
     ap = argparse.ArgumentParser()
@@ -196,11 +301,11 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("EMIN_BENCH_CONFIG", "3"))
+    ap.add_argument("--size", type=int, default=None, help="reduced generator size (tests only; not a bench line)")
     ap.add_argument("--impl", default="emin", choices=["emin", "reference"])
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo check of the launcher and partition")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-serial", action="store_true",
-                    help="e2e without the copy/compute pipeline (host pointers into emin_setup, steps back to back)")
     ap.add_argument("--precond", default="jacobi", choices=["jacobi", "sgs"],
                     help="Alg. 3 preconditioner: Jacobi M_1 (default, the headline) or projected SGS M_2")
     ap.add_argument("--sgs-key", default="color", choices=["color", "natural"],
@@ -219,19 +324,27 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
-    from workloads.problems import make_config
-    t0 = time.perf_counter()
-    prob = make_config(args.config)
-    log(f"[bench] generated {prob.name}: n={prob.n} nF={prob.n_F} nnzW={prob.nnz_W} "
-        f"in {time.perf_counter() - t0:.1f}s")
-
     if args.impl == "reference":
-        line = run_reference(args, prob, rank)
+        line = run_reference(args, rank)
         if line is not None:
             print(json.dumps(line), flush=True)
         return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    if args.dry_run:
+        return dry_run(args, world, rank)
+    if world != args.gpus:
+        log(f"[bench] WORLD_SIZE={world} but --gpus {args.gpus}: timing {world} rank(s)")
+
+    from workloads.problems import make_config
+    t0 = time.perf_counter()
+    prob = make_config(args.config, size=args.size)
+    log(f"[bench] rank {rank}: generated {prob.name}: n={prob.n} nF={prob.n_F} nnzW={prob.nnz_W} "
+        f"in {time.perf_counter() - t0:.1f}s")
 
     import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
@@ -242,44 +355,37 @@ def main():
     if world > 1:
         dist.barrier()
     from paper_2208_02995_b200 import emin as E
+    from paper_2208_02995_b200.partition import partition_rows, plane_rows, rank_slice
 
     stream = torch.cuda.current_stream()
-    keys = ["A_rowptr", "A_col", "A_val", "is_coarse", "P_rowptr", "P_col", "P_val", "B", "Bc"]
-    host = {k: getattr(prob, k) for k in keys}
-    dev = {k: (None if v is None else torch.from_numpy(np.ascontiguousarray(v)).cuda()) for k, v in host.items()}
-    # row partition (contiguous z-slabs balanced by nnz(W)); NCCL communicator
+    # row partition (contiguous z-slabs balanced by nnz(W)); each rank gets its
+    # own rows only (rebased row pointers), plus the global is_coarse and B_c
     comm = None
     rb, re_ = 0, prob.n
     if world > 1:
-        from paper_2208_02995_b200.partition import partition_rows
-        dims = prob.meta["dims"]
-        plane = dims[0] * dims[1] * (3 if prob.block_size == 3 else 1)
-        rb, re_ = partition_rows(prob.P_rowptr, prob.is_coarse, world, plane=plane)[rank]
+        rb, re_ = partition_rows(prob.P_rowptr, prob.is_coarse, world, plane=plane_rows(prob))[rank]
         comm = E.nccl_comm_from_torch()
-    nnzP = int(prob.P_rowptr[re_] - prob.P_rowptr[rb])
+    host = rank_slice(prob, rb, re_)
+    key = None
+    if args.precond == "sgs":
+        from workloads.problems import sgs_key
+        key = sgs_key(prob, args.sgs_key)[rb:re_]
+    host["sgs_key"] = key
+    dev = {k: (None if v is None else torch.from_numpy(np.ascontiguousarray(v)).cuda()) for k, v in host.items()}
+    nnzP = int(host["P_rowptr"][-1])
     out_dev = torch.empty(nnzP, dtype=torch.float64, device="cuda")
     k_it = prob.iters
     nnzW_global = prob.nnz_W
 
-    key = None
-    if args.precond == "sgs":
-        from workloads.problems import sgs_key
-        key = sgs_key(prob, args.sgs_key)
-    host["sgs_key"] = key
-    dev["sgs_key"] = None if key is None else torch.from_numpy(key).cuda()
-
     def setup(arrs):
-        nv = prob.nv
-        kk = arrs["sgs_key"]
-        return E.emin_setup(prob.n, prob.nc, arrs["A_rowptr"][rb:re_ + 1], arrs["A_col"], arrs["A_val"],
-                            arrs["is_coarse"], arrs["P_rowptr"][rb:re_ + 1], arrs["P_col"], arrs["P_val"],
-                            nv, arrs["B"][rb:re_], arrs["Bc"], block_size=prob.block_size,
-                            stagnation_rel=0.0, stream=stream.cuda_stream, nccl_comm=comm,
-                            row_begin=rb, row_end=re_, precond=args.precond, start=args.start,
-                            sgs_key=None if kk is None else kk[rb:re_])
+        return E.emin_setup(prob.n, prob.nc, arrs["A_rowptr"], arrs["A_col"], arrs["A_val"], arrs["is_coarse"],
+                            arrs["P_rowptr"], arrs["P_col"], arrs["P_val"], prob.nv, arrs["B"], arrs["Bc"],
+                            block_size=prob.block_size, stagnation_rel=0.0, stream=stream.cuda_stream,
+                            nccl_comm=comm, row_begin=rb, row_end=re_, precond=args.precond, start=args.start,
+                            sgs_key=arrs["sgs_key"])
 
     stats = {"launches": 0, "spgemm_ms": 0.0, "spgemm_n": 0, "stage_ms": [0.0, 0.0], "scalar_ms": 0.0,
-             "k_done": 0, "E": None, "report": None}
+             "k_done": [], "E": None, "report": None}
 
     def step(arrs, out, profile):
         h = setup(arrs)
@@ -290,7 +396,7 @@ def main():
         E.emin_get_P(h, out)
         rep = E.emin_report(h)
         stats["launches"] += rep["launches"]
-        stats["k_done"] = rep["k_total"]
+        stats["k_done"].append(rep["k_total"])
         stats["report"] = rep
         if profile:
             kt = E.emin_kernel_times(h)
@@ -304,15 +410,20 @@ def main():
     # warm-up (untimed)
     for _ in range(args.warmup):
         step(dev, out_dev, True)
-    for k in list(stats):
-        if isinstance(stats[k], (int, float)) and k not in ("E",):
-            stats[k] = 0 if isinstance(stats[k], int) else 0.0
-    stats["stage_ms"] = [0.0, 0.0]
+    stats.update(launches=0, spgemm_ms=0.0, spgemm_n=0, stage_ms=[0.0, 0.0], scalar_ms=0.0, k_done=[])
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     # ---- timed region: K whole-path steps, device-resident inputs
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -326,19 +437,18 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    launches_timed = stats["launches"]
     clocks = clk.summary()
-    nnzW = stats["report"]["nnz_W"]
-    nnzAFF = stats["report"]["nnz_AFF"]
-    nF = stats["report"]["n_fine"]
-    # updates actually performed: if the CG ever stopped before k_it (gamma or
-    # y'Ky at zero), count only the steps it took (never the requested ones)
-    k_eff = stats["k_done"] if 0 < stats["k_done"] < k_it else k_it
+    rep = stats["report"]
+    nnzW, nnzAFF, nF = rep["nnz_W"], rep["nnz_AFF"], rep["n_fine"]
+    # updates actually performed: the CG steps each timed step took (never the
+    # requested ones; 0 if the CG stopped at once).  Value-independent kernels
+    # make every step take the same number (stagnation guard off).
+    kd_steps = stats["k_done"]
+    k_eff = min(min(kd_steps), k_it)
+    if len(set(kd_steps)) != 1:
+        log(f"[bench] warning: k_done differs between steps: {sorted(set(kd_steps))}; counting the minimum")
     updates = nnzW_global * k_eff * args.steps
     value = updates / (ms / 1e3)
 
@@ -351,18 +461,14 @@ def main():
     it_ms = []
     for _ in range(reps):
         E.emin_reset(h)
+        barrier()
         ia.record(stream)
         E.emin_iterate(h, k_it)
         ib.record(stream)
         torch.cuda.synchronize()
         it_ms.append(ia.elapsed_time(ib))
     E.emin_destroy(h)
-    it_ms_med = statistics.median(it_ms)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([it_ms_med], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        it_ms_med = float(t.item())
+    it_ms_med = max_over_ranks(statistics.median(it_ms))
 
     # ---- roofline of the dominant kernel (masked SpGEMM), from the timed region
     peak, peak_src = measured_peak()
@@ -378,20 +484,20 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "masked SpGEMM + Pi_B (ŷ = Pi K y)", "peak_source": peak_src,
+                "kernel": "masked SpGEMM + Pi_B (yb = Pi K y)", "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": sp_bytes,
                 "avg_launch_ms": sp_avg_ms, "launches": stats["spgemm_n"],
                 "share_of_step": (stats["spgemm_ms"] / nprof / (ms / args.steps)) if ms > 0 else None,
-                "profiled_steps": nprof}
+                "profiled_steps": nprof, "rank": rank}
 
-    # ---- e2e: same metric through the public API from HOST buffers (pinned):
-    # every step copies its inputs host -> device and reads P back inside the
-    # timed region.  Default: pipelined over two device buffer sets -- step
-    # s+1's inputs are copied on a copy stream while step s computes (device
-    # inputs to emin_setup), P goes back on a third stream (PCIe is full
-    # duplex).  --e2e-serial: the plain C-ABI call with host pointers (the
-    # library copies), steps back to back.
-    e2e = None
+    # ---- e2e: the same metric through the C ABI with HOST buffers: every
+    # step passes pinned host pointers to emin_setup (the library copies them
+    # to the device inside the call) and emin_get_P writes P into a host
+    # buffer; all of it inside the timed region.  e2e_pipelined: the same
+    # step with the H2D of step s+1 and the D2H of step s overlapped with step
+    # s's compute by the caller (torch copies on side streams into device
+    # buffers, device pointers into the C ABI).
+    e2e = e2e_pipe = None
     if not args.no_e2e:
         pin_t = {k: (None if v is None else torch.from_numpy(np.ascontiguousarray(v)).pin_memory())
                  for k, v in host.items()}
@@ -401,78 +507,90 @@ def main():
         h2d = sum(v.nbytes for v in pin.values() if v is not None)
         d2h = out_host.nbytes + 8
         n_e2e = max(1, args.steps // 2)
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if args.e2e_serial:
-            step(pin, out_host, False)
-            barrier()
-            torch.cuda.synchronize()
-            ea.record(stream)
-            for _ in range(n_e2e):
-                step(pin, out_host, False)
-            eb.record(stream)
-        else:
-            cs, ds = torch.cuda.Stream(), torch.cuda.Stream()
-            bufs = [{k: (None if v is None else torch.empty(v.shape, dtype=v.dtype, device="cuda"))
-                     for k, v in pin_t.items()} for _ in range(2)]
-            outs = [torch.empty(nnzP, dtype=torch.float64, device="cuda") for _ in range(2)]
-            ev = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
-            h2d_done, in_free, out_free, p_ready = ev(), ev(), ev(), ev()
 
-            def enqueue_h2d(s):
-                b = s % 2
-                with torch.cuda.stream(cs):
-                    if s >= 2:
-                        cs.wait_event(in_free[b])
-                    for k, v in pin_t.items():
-                        if v is not None:
-                            bufs[b][k].copy_(v, non_blocking=True)
-                    h2d_done[b].record(cs)
-
-            def pstep(s, n):
-                b = s % 2
-                stream.wait_event(h2d_done[b])
-                if s + 1 < n:
-                    enqueue_h2d(s + 1)
-                h = setup(bufs[b])
-                in_free[b].record(stream)
-                E.emin_iterate(h, k_it)
-                stats["E"] = E.emin_energy(h)
-                if s >= 2:
-                    stream.wait_event(out_free[b])
-                E.emin_get_P(h, outs[b])
-                p_ready[b].record(stream)
-                with torch.cuda.stream(ds):
-                    ds.wait_event(p_ready[b])
-                    out_host_t.copy_(outs[b], non_blocking=True)
-                    out_free[b].record(ds)
-                E.emin_destroy(h)
-
-            def run(n):
-                cs.wait_stream(stream)
-                enqueue_h2d(0)
-                for s_ in range(n):
-                    pstep(s_, n)
-                stream.wait_stream(ds)
-                stream.wait_stream(cs)
-
-            run(2)                                     # untimed warm-up of the pipeline
-            barrier()
-            torch.cuda.synchronize()
-            ea.record(stream)
-            run(n_e2e)
-            eb.record(stream)
-        torch.cuda.synchronize()
-        e_ms = ea.elapsed_time(eb)
-        if world > 1:
+        def whole_job_bytes(b):
+            if world == 1:
+                return int(b)
             import torch.distributed as dist
-            t = torch.tensor([e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+            t = torch.tensor([b], device="cuda", dtype=torch.int64)
+            dist.all_reduce(t)
+            return int(t.item())
+
+        h2d_all, d2h_all = whole_job_bytes(h2d), whole_job_bytes(d2h)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # (a) serial C-ABI calls with host pointers
+        step(pin, out_host, False)
+        barrier()
+        torch.cuda.synchronize()
+        ea.record(stream)
+        for _ in range(n_e2e):
+            step(pin, out_host, False)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(ea.elapsed_time(eb))
         e2e = {"value": nnzW_global * k_eff * n_e2e / (e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e_ms / n_e2e, "steps": n_e2e,
-               "mode": "serial (host pointers into the C ABI)" if args.e2e_serial else
-                       "pipelined (H2D of step s+1 and D2H of step s overlap step s's compute; pinned host buffers)"}
+               "h2d_bytes_per_step": h2d_all, "d2h_bytes_per_step": d2h_all,
+               "h2d_bytes_per_step_per_rank": int(h2d), "ms_per_step": e_ms / n_e2e, "steps": n_e2e,
+               "mode": "serial C-ABI calls with pinned host pointers (emin_setup copies the inputs, "
+                       "emin_get_P writes P to host memory)"}
+        # (b) caller-pipelined
+        cs, ds = torch.cuda.Stream(), torch.cuda.Stream()
+        bufs = [{k: (None if v is None else torch.empty(v.shape, dtype=v.dtype, device="cuda"))
+                 for k, v in pin_t.items()} for _ in range(2)]
+        outs = [torch.empty(nnzP, dtype=torch.float64, device="cuda") for _ in range(2)]
+        mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
+        h2d_done, in_free, out_free, p_ready = mk(), mk(), mk(), mk()
+
+        def enqueue_h2d(s):
+            b = s % 2
+            with torch.cuda.stream(cs):
+                if s >= 2:
+                    cs.wait_event(in_free[b])
+                for k, v in pin_t.items():
+                    if v is not None:
+                        bufs[b][k].copy_(v, non_blocking=True)
+                h2d_done[b].record(cs)
+
+        def pstep(s, n):
+            b = s % 2
+            stream.wait_event(h2d_done[b])
+            if s + 1 < n:
+                enqueue_h2d(s + 1)
+            hh = setup(bufs[b])
+            in_free[b].record(stream)
+            E.emin_iterate(hh, k_it)
+            stats["E"] = E.emin_energy(hh)
+            if s >= 2:
+                stream.wait_event(out_free[b])
+            E.emin_get_P(hh, outs[b])
+            p_ready[b].record(stream)
+            with torch.cuda.stream(ds):
+                ds.wait_event(p_ready[b])
+                out_host_t.copy_(outs[b], non_blocking=True)
+                out_free[b].record(ds)
+            E.emin_destroy(hh)
+
+        def run(n):
+            cs.wait_stream(stream)
+            enqueue_h2d(0)
+            for s_ in range(n):
+                pstep(s_, n)
+            stream.wait_stream(ds)
+            stream.wait_stream(cs)
+
+        run(2)                                     # untimed warm-up of the pipeline
+        barrier()
+        torch.cuda.synchronize()
+        ea.record(stream)
+        run(n_e2e)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        p_ms = max_over_ranks(ea.elapsed_time(eb))
+        e2e_pipe = {"value": nnzW_global * k_eff * n_e2e / (p_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d_all, "d2h_bytes_per_step": d2h_all,
+                    "ms_per_step": p_ms / n_e2e, "steps": n_e2e,
+                    "mode": "caller-pipelined: H2D of step s+1 and D2H of step s overlap step s's compute "
+                            "(pinned host buffers, two device buffer sets)"}
 
     if rank != 0:
         if world > 1:
@@ -489,28 +607,31 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "iters_per_step": k_it, "nnz_W": nnzW_global,
-                   "nnz_A_FF": nnzAFF, "n_F": nF, "nv": prob.nv,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args), "iters_per_step": k_it, "nnz_W": nnzW_global,
+                   "nnz_A_FF_rank0": nnzAFF, "n_F_rank0": nF, "nv": prob.nv,
                    "step": "emin_setup(device inputs) + emin_iterate(k) + emin_energy + emin_get_P + emin_destroy",
                    "l2": "inputs larger than L2 (per-iteration working set %.2f GB > 126 MB)" % (it_bytes / 1e9),
-                   "parallelism": f"rows{world}" if world > 1 else "single GPU",
-                   "kernel_path": E.KERNEL_PATHS.get(stats["report"]["kernel_path"]),
+                   "parallelism": f"rows{world} (z-slab row partition, NCCL halo + allreduce)" if world > 1
+                   else "single GPU",
+                   "kernel_path": E.KERNEL_PATHS.get(rep["kernel_path"]),
                    "precond": args.precond if args.precond == "jacobi" else
-                   f"sgs ({args.sgs_key} order, {stats['report']['sgs_levels']} levels per sweep)",
-                   "start": args.start},
+                   f"sgs ({args.sgs_key} order, {rep['sgs_levels']} levels per sweep)",
+                   "start": args.start,
+                   "halo_rank0": {"rows": rep["n_halo_rows"], "entries": rep["n_halo_entries"],
+                                  "sent_entries": rep["n_send_entries"]} if world > 1 else None},
         "roofline": roofline,
-        "iter_only": {"value": nnzW_global * k_eff / (it_ms_med / 1e3), "unit": UNIT,
-                      "ms_per_iter": it_ms_med / k_eff,
-                      "GBps_vs_B_iter": it_bytes / (it_ms_med / k_eff / 1e3) / 1e9,
-                      "frac_of_peak": it_bytes / (it_ms_med / k_eff / 1e3) / 1e9 / peak},
+        "iter_only": {"value": nnzW_global * k_eff / (it_ms_med / 1e3) if k_eff else 0.0, "unit": UNIT,
+                      "ms_per_iter": it_ms_med / max(k_eff, 1),
+                      "GBps_vs_B_iter_rank0": it_bytes / (it_ms_med / max(k_eff, 1) / 1e3) / 1e9,
+                      "frac_of_peak_rank0": it_bytes / (it_ms_med / max(k_eff, 1) / 1e3) / 1e9 / peak},
         "kernel_ms_per_step": {"spgemm": stats["spgemm_ms"] / nprof,
                                "stage1": stats["stage_ms"][0] / nprof,
                                "stage2": stats["stage_ms"][1] / nprof,
                                "scalar": stats["scalar_ms"] / nprof},
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": stats["launches"], "clocks": clocks,
-        "energy": stats["E"], "k_done": stats["k_done"],
+        "cpu_baseline": cpu, "e2e": e2e, "e2e_pipelined": e2e_pipe,
+        "gpu_launches": launches_timed, "clocks": clocks,
+        "energy": stats["E"], "k_done": k_eff,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -5,7 +5,8 @@ TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
 package.  The product path (``paper_2208_02995_b200``) never imports it, and
 this package never imports the product path: the two share no code.
 
-The arithmetic lives in ``emin_oracle.c`` (plain C, fp64, single thread);
+The arithmetic lives in ``emin_oracle.c`` (plain C, fp64; OpenMP threads only
+on loops whose iterations are independent, every global sum serial);
 this file is ctypes marshalling only.  See the C file's header for the
 paper passages each step follows and DESIGN.md §3 for the readings of the
 garbled passages.
@@ -29,7 +30,7 @@ STOP_REASONS = {0: "running", 1: "gamma<=0", 2: "y'Ky==0", 3: "tau", 4: "stagnat
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (no -ffast-math, IEEE fp64)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC",
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC", "-fopenmp",
                                "-ffp-contract=off", "-o", _LIB_PATH, _SRC, "-lm"])
     return _LIB_PATH
 
@@ -53,6 +54,10 @@ def _load():
                          ("oracle_n_maxvol_fail", i64)]:
             getattr(lib, name).argtypes = [P]
             getattr(lib, name).restype = rt
+        lib.oracle_set_threads.argtypes = [i32]
+        lib.oracle_set_threads.restype = None
+        lib.oracle_max_threads.argtypes = []
+        lib.oracle_max_threads.restype = i32
         lib.oracle_energy_of.argtypes = [P, P]
         lib.oracle_energy_of.restype = dbl
         lib.oracle_destroy.argtypes = [P]
@@ -77,6 +82,15 @@ def _load():
         lib.oracle_galerkin.restype = i64
         _lib = lib
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Threads of the oracle's parallel loops (1 = everything serial)."""
+    _load().oracle_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
 
 
 def _p(a):

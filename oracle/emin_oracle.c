@@ -60,6 +60,15 @@
  * Summation order: per-row sums ascending in A's column order; global sums
  * row-ascending with Neumaier compensation.
  *
+ * Threads (OpenMP, -fopenmp): only loops whose iterations are independent
+ * run in parallel -- the per-row loops of the projection, the masked
+ * product, Alg. 2 and the Jacobi scaling, and the elementwise vector
+ * updates.  Every global sum stays one serial Neumaier pass in the order
+ * above (the energy's per-entry terms are formed in parallel into an array,
+ * then summed serially), and the SGS sweeps stay serial, so the result does
+ * not depend on the thread count (pinned: tests/test_oracle_pins.py compares
+ * 1 thread with all of them bitwise).
+ *
  * Parity pins (tests/test_oracle_*.py): dense KKT solve, null-space solve,
  * 1D closed form, config 1b/2b converge to the symmetric equal-weight P,
  * constraint at every iterate, monotone + telescoping energy, Theorem 1,
@@ -67,6 +76,9 @@
  * energy == dense tr(P^T A P), QR/SVD vs numpy.linalg.
  */
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -400,6 +412,7 @@ static int maxvol_solve(int m, int nv, const double *M, const int *S, const doub
 /* (Pi x)_i = x_i - Q_i (Q_i^T x_i)   (Pi_B = I - Q Q^T) */
 void oracle_project(const oracle_t *o, const double *x, double *out) {
     int nv = o->nv;
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < o->nF; ++i) {
         int64_t b = o->wptr[i], e = o->wptr[i + 1];
         double c[16];
@@ -421,6 +434,7 @@ void oracle_project(const oracle_t *o, const double *x, double *out) {
  * for j in J_i, where X(k,j) = 0 if j not in J_k.  Summed in the order of
  * row i of A; J_i and J_k are merged as sorted lists. */
 void oracle_masked_AX(const oracle_t *o, const double *X, int with_fc, double *out) {
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < o->nF; ++i) {
         int64_t g = o->frow[i];
         int64_t b = o->wptr[i], e = o->wptr[i + 1];
@@ -533,6 +547,7 @@ void oracle_apply_prec(const oracle_t *o, const double *x, double *z) {
         sgs_apply(o, x, z);
         oracle_project(o, z, z);          /* mandatory for SGS */
     } else {
+        #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < o->nF; ++i)
             for (int64_t p = o->wptr[i]; p < o->wptr[i + 1]; ++p) z[p] = x[p] / o->d[i];
         if (o->project_z) oracle_project(o, z, z);
@@ -545,9 +560,13 @@ static double dot_w(const oracle_t *o, const double *a, const double *b) {
     return nsum_val(&s);
 }
 
-/* tr(P^T A P) by definition, P = [W; I] on the full row set (Eq. trace). */
+/* tr(P^T A P) by definition, P = [W; I] on the full row set (Eq. trace):
+ * the terms P(r,j) (A P)(r,j) over the pattern of P in CSR order, summed
+ * row-ascending (Neumaier). */
 double oracle_energy_of(const oracle_t *o, const double *W) {
-    nsum_t tot = {0.0, 0.0};
+    int64_t nnzP = o->Prp[o->n];
+    double *term = (double *)malloc(sizeof(double) * (nnzP ? nnzP : 1));
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t r = 0; r < o->n; ++r) {
         /* P row r: pattern and values */
         int64_t rb, re;
@@ -573,9 +592,12 @@ double oracle_energy_of(const oracle_t *o, const double *W) {
                 }
                 apj += o->Aval[q] * pkj;
             }
-            nsum_add(&tot, prj * apj);
+            term[o->Prp[r] + (p - rb)] = prj * apj;
         }
     }
+    nsum_t tot = {0.0, 0.0};
+    for (int64_t q = 0; q < nnzP; ++q) nsum_add(&tot, term[q]);
+    free(term);
     return nsum_val(&tot);
 }
 
@@ -696,6 +718,8 @@ int oracle_create(oracle_t **out, int64_t n, int64_t nc,
     o->y = (double *)calloc(W, sizeof(double));
     o->yb = (double *)calloc(W, sizeof(double));
     o->z = (double *)calloc(W, sizeof(double));
+    int64_t n_svd = 0, n_frozen = 0, n_mvf = 0;
+    #pragma omp parallel for schedule(dynamic, 256) reduction(+ : n_svd, n_frozen, n_mvf)
     for (int64_t i = 0; i < ff; ++i) {
         int64_t r = o->frow[i], b = o->wptr[i];
         int nj = (int)(o->wptr[i + 1] - b);
@@ -711,7 +735,7 @@ int oracle_create(oracle_t **out, int64_t n, int64_t nc,
         if (start == 1) {                            /* Alg. 1 tentative start (reading A24) */
             int S[16];
             int ok = oracle_maxvol(nj, nv, M, S) && maxvol_solve(nj, nv, M, S, B + r * nv, wh);
-            if (!ok) { for (int t = 0; t < nj; ++t) wh[t] = 0.0; o->n_maxvol_fail++; }
+            if (!ok) { for (int t = 0; t < nj; ++t) wh[t] = 0.0; n_mvf++; }
         }
         for (int m = 0; m < nv; ++m) {              /* r_i = v_i - M^T w^ */
             double s = B[r * nv + m];
@@ -721,11 +745,12 @@ int oracle_create(oracle_t **out, int64_t n, int64_t nc,
         int used_svd = 0;
         int k = emin_setup_row(nj, nv, M, rv, rank_tol, o->Q + b * nv, delta, &used_svd);
         o->krank[i] = k;
-        if (used_svd) o->n_svd++;
-        if (nj == k) o->n_frozen++;
+        if (used_svd) n_svd++;
+        if (nj == k) n_frozen++;
         for (int t = 0; t < nj; ++t) o->w0[b + t] = wh[t] + delta[t];
         free(M); free(wh); free(delta);
     }
+    o->n_svd = n_svd; o->n_frozen = n_frozen; o->n_maxvol_fail = n_mvf;
     /* r0 = -Pi (A P0)|F   (readings A1, A2) */
     double *G = (double *)malloc(sizeof(double) * W);
     oracle_masked_AX(o, o->w0, 1, G);
@@ -752,9 +777,12 @@ int oracle_iterate(oracle_t *o, int kmax, int *k_done, double *dE) {
         oracle_apply_prec(o, o->r, o->z);
         double gamma = dot_w(o, o->r, o->z);                            /* P:841 */
         if (!(gamma > 0.0)) { o->stopped = OR_STOP_GAMMA; break; }
-        if (k == 1) { for (int64_t p = 0; p < W; ++p) o->y[p] = o->z[p]; }  /* P:842-843 */
-        else {
+        if (k == 1) {                                                   /* P:842-843 */
+            #pragma omp parallel for schedule(static)
+            for (int64_t p = 0; p < W; ++p) o->y[p] = o->z[p];
+        } else {
             double beta = gamma / o->gamma_old;                           /* P:845 */
+            #pragma omp parallel for schedule(static)
             for (int64_t p = 0; p < W; ++p) o->y[p] = o->z[p] + beta * o->y[p];
         }
         o->gamma_old = gamma;                                           /* P:848 */
@@ -768,8 +796,11 @@ int oracle_iterate(oracle_t *o, int kmax, int *k_done, double *dE) {
         if (k == 1) o->dE1 = dEk;
         if (o->tau > 0.0 && k > 1 && dEk < o->tau * o->dE1) { o->stopped = OR_STOP_TAU; break; }
         if (dEk <= o->stag * o->E0) { o->stopped = OR_STOP_STAG; break; }
-        for (int64_t p = 0; p < W; ++p) o->dw[p] += alpha * o->y[p];    /* P:853 */
-        for (int64_t p = 0; p < W; ++p) o->r[p] -= alpha * o->yb[p];    /* P:854 */
+        #pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < W; ++p) {
+            o->dw[p] += alpha * o->y[p];                                /* P:853 */
+            o->r[p] -= alpha * o->yb[p];                                /* P:854 */
+        }
         if (dE) dE[*k_done] = dEk;
         o->k_total = k;
         (*k_done)++;
@@ -808,6 +839,21 @@ void oracle_reset(oracle_t *o) {
 }
 
 /* ---------------- accessors for the Python wrapper ----------------------- */
+/* threads of the parallel loops (1 = the serial order everywhere) */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
+#endif
+}
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
 int64_t oracle_nF(const oracle_t *o) { return o->nF; }
 int64_t oracle_nnzW(const oracle_t *o) { return o->nnzW; }
 double oracle_E0(const oracle_t *o) { return o->E0; }

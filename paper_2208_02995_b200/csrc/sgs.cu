@@ -105,8 +105,9 @@ __global__ void k_sgs_count(int64_t nF, const int32_t* __restrict__ lev, int32_t
 // per-level windows on the GPU: rows in level-bucket order j, entry offsets
 // pst[j] (exclusive scan of the row lengths); a row whose offset from its
 // level's start lies in [S w, S w + S) goes to window w of the level, S = 33 -
-// the longest row (<= 8 on the scalar path): a window holds <= 32 entries
-// and every window has a row
+// the longest row (<= 8 on the scalar path): a window holds <= 32 entries.
+// A window can be empty (rows of lengths 8, 8, 8, 6 with S = 25 all start in
+// window 0 and leave window 1 zeroed {0, 0, 0, 0}); the sweeps skip those.
 __global__ void k_sgs_wlen(int64_t nF, const int32_t* __restrict__ rows, const int64_t* __restrict__ wptr,
                            int64_t* __restrict__ len) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nF; j += (int64_t)gridDim.x * blockDim.x) {
@@ -268,6 +269,7 @@ k_sgs_sweep_win(DevView v, const int4* __restrict__ A4, const uint8_t* __restric
     const int4 h = __ldg(win + w);
     const unsigned H = (unsigned)h.y;
     const int nent = h.z;
+    if (nent == 0) continue;     // an empty window (warp-uniform): see k_sgs_wlen
     const bool act = lane < nent;
     const int l = act ? lane : nent - 1;
     const unsigned upto = (l == 31) ? 0xffffffffu : ((2u << l) - 1u);

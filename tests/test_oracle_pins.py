@@ -733,3 +733,29 @@ def test_galerkin_trace_is_energy_symmetric_and_keeps_near_kernel(name, size):
     lhs = Ac @ p.Bc
     rhs = P.T @ (A @ p.B)
     assert np.abs(lhs - rhs).max() <= 1e-10 * max(np.abs(rhs).max(), np.abs(lhs).max(), 1.0)
+
+
+@pytest.mark.parametrize("name,size,k", [("1b", None, 20), ("2b", 8, 30), ("3", 10, 40), ("4", 3, 30),
+                                         ("5", 6, 10)])
+def test_threaded_oracle_equals_serial_order(name, size, k):
+    """The OpenMP loops of the oracle (per-row projection, masked product,
+    Alg. 2, Jacobi scaling, vector updates, per-entry energy terms) leave
+    every global sum serial in its order, so 1 thread and all threads give
+    the same bits: E0, dE_k, E and P."""
+    import oracle
+    from oracle import Oracle
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    out = []
+    orig = oracle.max_threads()
+    try:
+        for nt in (1, max(2, orig)):
+            oracle.set_threads(nt)
+            o = Oracle(prob, project_z=True)
+            kd, dE = o.iterate(k)
+            out.append((o.E0, kd, dE, o.energy(), o.get_P(), o.n_svd, o.n_frozen))
+    finally:
+        oracle.set_threads(orig)
+    a, b = out
+    assert a[0] == b[0] and a[1] == b[1] and np.array_equal(a[2], b[2]) and a[3] == b[3]
+    assert np.array_equal(a[4], b[4]) and a[5:] == b[5:]
