@@ -141,6 +141,20 @@ class ClockSampler:
 # executes oracle/
 # ---------------------------------------------------------------------------
 
+def oracle_iterate_counted(o, k):
+    """o.iterate(k), returning the steps taken even if the unguarded run
+    meets round-off curvature (y'Ky < 0, EMIN_ERR_BREAKDOWN) before k."""
+    from oracle import OracleError
+    if k <= 0:
+        return 0
+    before = o.k_total
+    try:
+        kd, _ = o.iterate(k)
+        return kd
+    except OracleError:
+        return o.k_total - before
+
+
 def oracle_step_rate(prob, threads, budget_s):
     """One oracle step of ``prob`` (setup + k iterations + energy + P out) on
     ``threads`` host threads, the iteration count bounded so the step takes
@@ -150,14 +164,14 @@ def oracle_step_rate(prob, threads, budget_s):
     oracle.set_threads(threads)
     k = prob.iters
     t0 = time.perf_counter()
-    o = Oracle(prob)
+    o = Oracle(prob, stagnation_rel=0.0)      # the GPU arm's setting: all k steps, guard off
     t_setup = time.perf_counter() - t0
     t1 = time.perf_counter()
     kd1, _ = o.iterate(1)
     t_it = time.perf_counter() - t1
     k_s = max(0, min(k - 1, int((budget_s - t_setup) / max(t_it, 1e-4)) - 1))
     t1 = time.perf_counter()
-    kd2, _ = o.iterate(k_s) if k_s else (0, None)
+    kd2 = oracle_iterate_counted(o, k_s)
     t_its = time.perf_counter() - t1
     o.energy()
     o.get_P()
@@ -209,11 +223,12 @@ def run_reference(args, rank):
         from oracle import Oracle
         oracle.set_threads(nproc)
         t0 = time.perf_counter()
-        o = Oracle(prob)
-        kd, _ = o.iterate(k_step)
+        o = Oracle(prob, stagnation_rel=0.0)
+        kd = oracle_iterate_counted(o, k_step)
         o.energy()
         o.get_P()
         dt = time.perf_counter() - t0
+        k_step = min(k_step, kd) if kd else k_step
         if s >= warm:
             times.append(dt)
     tot = sum(times)
