@@ -117,8 +117,8 @@ typedef struct {
 #define EMIN_DBG_FUSE_SCALARS 16   /* one GPU: CG scalar steps in the last block of the producing
                                       kernels instead of separate single-block kernels */
 #define EMIN_DBG_ALG2_ROWS 32      /* nodal path: Alg. 2 row by row instead of once per node */
-#define EMIN_DBG_SPGEMM_WIN2 64    /* scalar path: the round-1 window kernel (win2) for y^ = Pi K y
-                                      instead of the push kernel */
+#define EMIN_DBG_AB1 64            /* A/B switch of the kernel under study;
+                                      no effect in a library without an experiment */
 
 #define EMIN_PREC_JACOBI 0
 #define EMIN_PREC_SGS 1

@@ -74,12 +74,11 @@ def test_parity_small(name, size, k):
 
 
 @pytest.mark.parametrize("name,size,path,dbg", [("3", 12, 1, 0), ("2b", 10, 1, 0), ("3", 17, 1, 0), ("1b", None, 1, 0),
-                                                ("3", 12, 1, 64), ("2b", 10, 1, 64), ("1b", None, 1, 64),
                                                 ("4", 4, 2, 0), ("5", 8, 2, 0), ("4", 3, 2, 0)])
 def test_kernel_paths_agree(name, size, path, dbg):
-    """The specialised kernels of the library (scalar path: the push kernel,
-    or win2 with EMIN_DBG_SPGEMM_WIN2 = 64, + the tile kernel; nodal 3x3
-    kernel) against the generic warp-per-row kernel (EMIN_DBG_FORCE_GENERIC)."""
+    """The specialised kernels of the library (scalar path: the window kernel
+    win2 + the tile kernel; nodal 3x3 kernel) against the generic
+    warp-per-row kernel (EMIN_DBG_FORCE_GENERIC)."""
     from paper_2208_02995_b200 import Emin
     from paper_2208_02995_b200.emin import DBG_FORCE_GENERIC
     from workloads.problems import make_config
