@@ -1,0 +1,846 @@
+// kernels_nodal.cuh -- nodal (3x3 block) path for vector problems
+// (elasticity, configs 4-5; kernel_path 2), selected when emin_opts.block_size
+// = 3 and the structure checks pass.
+//
+// Rows 3n..3n+2 of an F node n share the pattern J_n (blockwise: columns
+// 3c, 3c+1, 3c+2 for every C node c in J_n) and hence the same M_i =
+// B_c(J_i,:) and the same Q_i; A_FF is made of dense 3x3 blocks (I,K).  The
+// masked product of node I is then
+//     Yb(I,d; c,b) = sum_K sum_d' A_IK[d][d'] Y(K,d'; c,b),  c in J_I n J_K
+// computed by one warp per node: lane t owns the pattern positions t and
+// t+32 (t = 3 s + b: C node s of J_I, component b) for all three output rows
+// d, so each matched (block, position) costs 3 gathers and 9 FMAs and the
+// node-level match (s in J_I -> s_K in J_K) is read once per block and lane
+// from a byte map built at setup.  Q is read once per node (row 3I) instead
+// of three times.
+#pragma once
+#include "emin_internal.cuh"
+#include "masked.cuh"
+
+struct NodalBlk {      // one per A_FF 3x3 block (I,K)
+  int32_t ybase;       // wptr[3K]: first W entry of the neighbour node
+  int32_t nK3;         // 3 |J_K|: row length of the neighbour node
+};
+
+struct NodalBlkP {     // pairs kernel: one per A_FF 3x3 block (I,K)
+  int32_t ybase;        // wptr[3K]
+  uint16_t nK3;         // 3 |J_K|
+  uint8_t np;           // matched pairs |J_I n J_K| of the block
+  uint8_t pad;
+};
+
+struct NodalPlan {
+  int64_t nFn = 0;            // owned F nodes
+  // matched-pair lists (iteration kernel k_spgemm_nodal_pr): per node the
+  // pairs (s, p), J_I[s] = J_K[p], block after block, uint16 s | p << 8,
+  // each node's list 16-byte aligned; null when the node stencil is wider
+  // than ND_MAXB blocks (the v2 kernel runs instead)
+  uint16_t* pr = nullptr;     // [sum_n padded pairs_n]
+  int64_t* proff = nullptr;   // [nFn+1]
+  NodalBlkP* blkp = nullptr;  // [nblk]
+  int64_t npr = 0;
+  NodalBlk* blk = nullptr;    // [nblk]
+  int64_t* bptr = nullptr;    // [nFn+1] block offset of node n (= affptr[3n] / 9)
+  uint8_t* pm8 = nullptr;     // [sum_n nblk_n |J_n|] position of J_I[s] in J_K, 0xFF absent
+  int64_t* pmoff = nullptr;   // [nFn+1]
+  int64_t nblk = 0, npm = 0;
+  int32_t max_nb = 0;         // most blocks of one node (> ND_MAXB: v2 stages in chunks; SGS goes generic)
+};
+
+// structure checks, one warp per F node (lanes over pattern positions and A
+// entries, coalesced); any violation clears *ok
+__global__ void k_nodal_check(DevView v, int64_t nFn, int32_t* ok, int64_t* pm_len, int32_t* max_nb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t r = 3 * n;
+    const int64_t wb = v.wptr[r];
+    const int64_t len = v.wptr[r + 1] - wb;
+    bool good = (len % 3 == 0) && len > 0 && len <= 64;     // two 32-lane chunks per node
+    for (int d = 1; d < 3 && good; ++d) good = (v.wptr[r + d + 1] - v.wptr[r + d]) == len;
+    bool lg = true;
+    if (good)
+      for (int64_t t = lane; t < len; t += 32) {
+        const int32_t c = v.wcol[wb + t];
+        if ((t % 3 == 0 && c % 3 != 0) || (t % 3 != 0 && c != v.wcol[wb + t - 1] + 1)) lg = false;
+        for (int d = 1; d < 3; ++d) lg = lg && v.wcol[v.wptr[r + d] + t] == c;
+      }
+    const int64_t ab = v.affptr[r];
+    const int64_t alen = v.affptr[r + 1] - ab;
+    good = good && (alen % 3 == 0);
+    for (int d = 1; d < 3 && good; ++d) good = (v.affptr[r + d + 1] - v.affptr[r + d]) == alen;
+    if (good)
+      for (int64_t q = lane; q < alen; q += 32) {
+        const int32_t k = v.affcol[ab + q];
+        if ((q % 3 == 0 && k % 3 != 0) || (q % 3 != 0 && k != v.affcol[ab + q - 1] + 1)) lg = false;
+        for (int d = 1; d < 3; ++d) lg = lg && v.affcol[v.affptr[r + d] + q] == k;
+      }
+    good = __all_sync(0xffffffffu, good && lg);
+    if (lane == 0) {
+      if (!good) atomicExch(ok, 0);
+      else atomicMax(max_nb, (int32_t)(alen / 3));
+      // (each node's byte map starts 16-byte aligned: staged with 16-byte loads)
+      pm_len[n] = good ? (((alen / 3) * (len / 3) + 15) & ~(int64_t)15) : 0;
+    }
+  }
+}
+
+// per node: block records and the byte position map, one warp per node
+// (lane per block: the merge of the sorted node lists J_I and J_K)
+__global__ void k_nodal_build(DevView v, int64_t nFn, const int64_t* __restrict__ pmoff, NodalBlk* __restrict__ blk,
+                              int64_t* __restrict__ bptr, uint8_t* __restrict__ pm8) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t r = 3 * n;
+    const int64_t wb = v.wptr[r];
+    const int nJ = (int)((v.wptr[r + 1] - wb) / 3);
+    const int64_t ab = v.affptr[r];
+    const int nb = (int)((v.affptr[r + 1] - ab) / 3);
+    const int64_t b0 = ab / 9;
+    if (lane == 0) {
+      bptr[n] = b0;
+      if (n == nFn - 1) bptr[nFn] = v.affptr[3 * nFn] / 9;
+    }
+    const int64_t po = pmoff[n];
+    for (int b = lane; b < nb; b += 32) {
+      const int32_t K = v.affcol[ab + 3 * b] / 3;
+      const int64_t kb = v.wptr[3 * (int64_t)K];
+      const int nK = (int)((v.wptr[3 * (int64_t)K + 1] - kb) / 3);
+      NodalBlk nbk;
+      nbk.ybase = (int32_t)kb;
+      nbk.nK3 = 3 * nK;
+      blk[b0 + b] = nbk;
+      int sK = 0;
+      for (int s = 0; s < nJ; ++s) {
+        const int32_t c = v.wcol[wb + 3 * s];
+        while (sK < nK && v.wcol[kb + 3 * sK] < c) ++sK;
+        pm8[po + (int64_t)b * nJ + s] = (sK < nK && v.wcol[kb + 3 * sK] == c) ? (uint8_t)sK : (uint8_t)0xFF;
+      }
+    }
+  }
+}
+
+constexpr int ND_WARPS = 8;
+constexpr int ND_MAXB = 27;      // blocks per node (27-point node stencil)
+constexpr int ND_MAXJ = 32;      // C nodes per pattern row (3|J| <= 96 entries -> 2 chunks of 32 needs |J| <= 21)
+
+// matched-pair lists from the byte map: per node (warp), lane per block;
+// pass 0 counts (block records + node total, padded to 8 pairs = 16 bytes),
+// pass 1 writes the pairs of each block at the node offset + the exclusive
+// warp prefix of the block counts
+template <int PASS>
+__global__ void k_nodal_pairs(int64_t nFn, const int64_t* __restrict__ bptr, const NodalBlk* __restrict__ blk,
+                              const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
+                              const int64_t* __restrict__ wptr, NodalBlkP* __restrict__ blkp,
+                              int64_t* __restrict__ cnt, const int64_t* __restrict__ proff,
+                              uint16_t* __restrict__ pr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);           // <= ND_MAXB (checked by the caller)
+    const int nJ = (int)((wptr[3 * n + 1] - wptr[3 * n]) / 3);
+    const uint8_t* m = pm8 + pmoff[n];
+    int np = 0;
+    if (lane < nb)
+      for (int sI = 0; sI < nJ; ++sI) np += m[lane * nJ + sI] != 0xFF;
+    if (PASS == 0) {
+      if (lane < nb) {
+        const NodalBlk k = blk[bb + lane];
+        blkp[bb + lane] = NodalBlkP{k.ybase, (uint16_t)k.nK3, (uint8_t)np, 0};
+      }
+      int tot = np;
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      if (lane == 0) cnt[n] = (tot + 7) & ~7;
+    } else {
+      int incl = np;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < nb) {
+        uint16_t* dst = pr + proff[n] + (incl - np);
+        for (int sI = 0; sI < nJ; ++sI) {
+          const uint8_t pK = m[lane * nJ + sI];
+          if (pK != 0xFF) *dst++ = (uint16_t)(sI | (pK << 8));
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// v2: the round-1 staged kernel (k_spgemm_nodal_s, profiles/ab_r01/), cut down to
+// what the L1 data pipe must carry (profiles/r01: the staged kernel was
+// bound by L1/shared wavefronts, 74 % of peak, not by DRAM):
+//  * the 3x3 block is read ONCE per block for both lane chunks, as five
+//    16-byte shared loads (block-major, 10-double stride) instead of 2 x 9
+//    8-byte loads;
+//  * Pi_B's nv dots of each of the 3 rows are reduced by a recursive-halving
+//    butterfly (a lane ends owning one dot; 8 doubles exchanged per row for
+//    nv = 6) and broadcast through shared memory, instead of nv full
+//    warp_sum butterflies per row (30 doubles);
+//  * 32-bit entry indices (nnz(W) < 2^31 is checked at plan time).
+// The per-entry arithmetic (block order, 9 FMAs in (d, e) order per block)
+// is unchanged, so y^ is bitwise equal to the staged kernel's except for the
+// order of the nv-dot sums.
+// ---------------------------------------------------------------------------
+constexpr int ND2_AST = 10;      // doubles per staged block (9 + pad, 16-byte aligned)
+
+// recursive-halving reduce-scatter of N values over the 32 lanes.  The N
+// values are padded to P = 2^ceil(log2 N); each halving stage splits a
+// lane's index range with its xor partner (disjoint ranges), and once a
+// range is a single index the remaining stages are plain xor adds (the two
+// partners compute a + b and b + a: bitwise equal).  On return the lane
+// holds in v[0] the full 32-lane sum of value index *own (valid iff
+// *own < N; a valid index may be held, bitwise equal, by several lanes).
+template <int S, int OFF>
+struct Nd2Rs {
+  static __device__ __forceinline__ void run(double* a, int lane, int& lo) {
+    if constexpr (OFF > 0) {
+      if constexpr (S > 1) {
+        constexpr int H = S / 2;
+        const bool lower = !(lane & OFF);
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+          const double send = lower ? a[H + i] : a[i];
+          const double recv = __shfl_xor_sync(0xffffffffu, send, OFF);
+          a[i] = (lower ? a[i] : a[H + i]) + recv;
+        }
+        if (!lower) lo += H;
+        Nd2Rs<H, OFF / 2>::run(a, lane, lo);
+      } else {
+        a[0] += __shfl_xor_sync(0xffffffffu, a[0], OFF);
+        Nd2Rs<1, OFF / 2>::run(a, lane, lo);
+      }
+    }
+  }
+};
+
+template <int N>
+__device__ __forceinline__ void nd2_reduce_scatter(double (&v)[N], int lane, int* own) {
+  constexpr int P = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
+  static_assert(N <= 32, "N <= 32");
+  double a[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) a[i] = i < N ? v[i] : 0.0;
+  int lo = 0;
+  Nd2Rs<P, 16>::run(a, lane, lo);
+  v[0] = a[0];
+  *own = lo;
+}
+
+template <int NV, int MODE, bool PRED = false, bool CS = false, bool WIDE = false, int GRP = 1, int MINB = 4>
+__global__ void __launch_bounds__(ND_WARPS * 32, MINB)
+k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
+                  const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
+                  const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+                  double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ __align__(16) double s_a[ND_WARPS][ND_MAXB * ND2_AST];
+  __shared__ NodalBlk s_b[ND_WARPS][ND_MAXB];
+  __shared__ __align__(16) uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
+  __shared__ __align__(16) double s_dot[ND_WARPS][3 * NV + 1];
+  if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // MM_ENERGY: W = X + X2, or X alone when the caller summed it (X2 null)
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;
+  auto xval = [&](int idx) -> double { return two ? X[idx] + X2[idx] : X[idx]; };
+  const int t0 = lane, t1 = lane + 32;
+  const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
+  double part = 0.0;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t r = 3 * n;
+    const int wb = (int)v.wptr[r];
+    const int n3 = (int)v.wptr[r + 1] - wb;
+    const int nJ = n3 / 3;
+    const int64_t ab = v.affptr[r];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int64_t po = pmoff[n];
+    const int rs = 3 * nb;
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    const bool any1 = n3 > 32;                          // warp-uniform
+    double acc0[3] = {0.0, 0.0, 0.0}, acc1[3] = {0.0, 0.0, 0.0};
+    // nodes with more than ND_MAXB blocks (Galerkin operators of coarse
+    // levels, NEXT-4) are staged ND_MAXB blocks at a time, same block order
+    // (template WIDE; otherwise the one chunk is the whole node, c0 = 0)
+    for (int cl = 0; cl < nb; cl += WIDE ? ND_MAXB : nb) {
+    const int c0 = WIDE ? cl : 0;
+    const int cb = WIDE ? min(ND_MAXB, nb - c0) : nb, cs = 3 * cb;
+    if (WIDE && c0) __syncwarp();
+    // ---- stage the node's data (A chunk re-ordered block-major, 10-double stride)
+    if (GRP > 1) {
+      // row by row: no division by the (variable) row length
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double* srow = v.affval + ab + (int64_t)d * rs + 3 * c0;
+        for (int j = lane; j < cs; j += 32) {
+          const int b = j / 3, e = j - 3 * b;
+          s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(srow + j) : __ldg(srow + j);
+        }
+      }
+    } else
+    for (int k = lane; k < 9 * cb; k += 32) {
+      const int d = k / cs, rem = k - d * cs, b = rem / 3, e = rem - 3 * b;
+      const int64_t src = WIDE ? ab + (int64_t)d * rs + 3 * c0 + rem : ab + k;
+      s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(v.affval + src) : __ldg(v.affval + src);
+    }
+    for (int k = lane; k < cb; k += 32) {
+      if (CS) { const int2 t = __ldcs(reinterpret_cast<const int2*>(blk + bb + c0 + k)); s_b[wib][k] = NodalBlk{t.x, t.y}; }
+      else s_b[wib][k] = blk[bb + c0 + k];
+    }
+    if (GRP > 1 && !WIDE) {
+      // 16-byte loads (the node's map is 16-byte aligned, padded)
+      const uint4* src4 = reinterpret_cast<const uint4*>(pm8 + po);
+      uint4* dst4 = reinterpret_cast<uint4*>(&s_pm[wib][0]);
+      for (int k = lane; k < ((cb * nJ + 15) >> 4); k += 32) dst4[k] = CS ? __ldcs(src4 + k) : src4[k];
+    } else
+    for (int k = lane; k < cb * nJ; k += 32) {
+      const int64_t src = po + (int64_t)c0 * nJ + k;
+      s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + src)) : pm8[src];
+    }
+    __syncwarp();
+    if (GRP > 1) {
+      // GRP blocks per round: the (up to 6 GRP) gathers of all of them are
+      // issued before the FMAs, which run in ascending block order with the
+      // same skips as the loop below (bitwise the same sums)
+      for (int b = 0; b < cb; b += GRP) {
+        double y0[GRP][3], y1[GRP][3];
+        bool m0[GRP], m1[GRP];
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) {
+          const bool has = b + g < cb;
+          const NodalBlk k = s_b[wib][has ? b + g : b];
+          const int p0 = (has && act0) ? s_pm[wib][(b + g) * nJ + s0] : 0xFF;
+          const int p1 = (has && any1 && act1) ? s_pm[wib][(b + g) * nJ + s1] : 0xFF;
+          m0[g] = p0 != 0xFF;
+          m1[g] = p1 != 0xFF;
+          const int i0 = k.ybase + 3 * (m0[g] ? p0 : 0) + b0, i1 = k.ybase + 3 * (m1[g] ? p1 : 0) + b1;
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            y0[g][e] = m0[g] ? xval(i0 + e * k.nK3) : 0.0;
+            y1[g][e] = m1[g] ? xval(i1 + e * k.nK3) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < GRP; ++g) {
+          // (past the last block: m0 = m1 = false, the A read is clamped)
+          const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][min(b + g, cb - 1) * ND2_AST]);
+          const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+          const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+          // PRED: no branches, fma(a, 0, acc) = acc on unmatched positions
+          // (up to the sign of a zero sum)
+          if (PRED || m0[g]) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              acc0[d] = fma(a[d * 3 + 0], y0[g][0], acc0[d]);
+              acc0[d] = fma(a[d * 3 + 1], y0[g][1], acc0[d]);
+              acc0[d] = fma(a[d * 3 + 2], y0[g][2], acc0[d]);
+            }
+          }
+          if (PRED ? any1 : m1[g]) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              acc1[d] = fma(a[d * 3 + 0], y1[g][0], acc1[d]);
+              acc1[d] = fma(a[d * 3 + 1], y1[g][1], acc1[d]);
+              acc1[d] = fma(a[d * 3 + 2], y1[g][2], acc1[d]);
+            }
+          }
+        }
+      }
+    } else
+    for (int b = 0; b < cb; ++b) {
+      const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][b * ND2_AST]);
+      const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+      const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+      const NodalBlk k = s_b[wib][b];
+      const int p0 = act0 ? s_pm[wib][b * nJ + s0] : 0xFF;
+      if (PRED) {
+        // branch-free: predicated gathers (0 when unmatched), unconditional
+        // FMAs (fma(a, 0, acc) = acc up to the sign of a zero)
+        const bool m0 = p0 != 0xFF;
+        const int i0 = k.ybase + 3 * (m0 ? p0 : 0) + b0;
+        const double y0 = m0 ? xval(i0) : 0.0, y1 = m0 ? xval(i0 + k.nK3) : 0.0, y2 = m0 ? xval(i0 + 2 * k.nK3) : 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          acc0[d] = fma(a[d * 3 + 0], y0, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 1], y1, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 2], y2, acc0[d]);
+        }
+        if (any1) {
+          const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
+          const bool m1 = p1 != 0xFF;
+          const int i1 = k.ybase + 3 * (m1 ? p1 : 0) + b1;
+          const double z0 = m1 ? xval(i1) : 0.0, z1 = m1 ? xval(i1 + k.nK3) : 0.0, z2 = m1 ? xval(i1 + 2 * k.nK3) : 0.0;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] = fma(a[d * 3 + 0], z0, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 1], z1, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 2], z2, acc1[d]);
+          }
+        }
+        continue;
+      }
+      if (p0 != 0xFF) {
+        const int i0 = k.ybase + 3 * p0 + b0;
+        const double y0 = xval(i0), y1 = xval(i0 + k.nK3), y2 = xval(i0 + 2 * k.nK3);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          acc0[d] = fma(a[d * 3 + 0], y0, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 1], y1, acc0[d]);
+          acc0[d] = fma(a[d * 3 + 2], y2, acc0[d]);
+        }
+      }
+      if (any1) {
+        const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
+        if (p1 != 0xFF) {
+          const int i1 = k.ybase + 3 * p1 + b1;
+          const double y0 = xval(i1), y1 = xval(i1 + k.nK3), y2 = xval(i1 + 2 * k.nK3);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] = fma(a[d * 3 + 0], y0, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 1], y1, acc1[d]);
+            acc1[d] = fma(a[d * 3 + 2], y2, acc1[d]);
+          }
+        }
+      }
+    }
+    }  // chunks of ND_MAXB blocks
+    double g0[3], g1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) { g0[d] = acc0[d]; g1[d] = acc1[d]; }
+    if (MODE != MM_ITER) {            // C-identity term A(i, c_j) (setup / energy only)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int64_t fb = v.afcptr[r + d], fe = v.afcptr[r + d + 1];
+        const int ro = wb + d * n3;
+        double f0 = 0.0, f1 = 0.0;
+        if (act0) {
+          const int32_t j = v.wcol[ro + t0];
+          for (int64_t q = fb; q < fe; ++q) if (v.afccol[q] == j) { f0 = v.afcval[q]; break; }
+        }
+        if (act1) {
+          const int32_t j = v.wcol[ro + t1];
+          for (int64_t q = fb; q < fe; ++q) if (v.afccol[q] == j) { f1 = v.afcval[q]; break; }
+        }
+        if (MODE == MM_ENERGY || MODE == MM_R0E) {
+          if (act0) part = fma(xval(ro + t0), g0[d] + 2.0 * f0, part);
+          if (act1) part = fma(xval(ro + t1), g1[d] + 2.0 * f1, part);
+        }
+        if (MODE != MM_ENERGY) {
+          g0[d] += f0;
+          g1[d] += f1;
+        }
+      }
+    }
+    if (MODE != MM_ENERGY) {
+      // Q of the node (row 3n, shared by its 3 rows): 16-byte loads
+      double q0[NV], q1[NV];
+#pragma unroll
+      for (int m = 0; m < NV; ++m) { q0[m] = 0.0; q1[m] = 0.0; }
+      if ((NV & 1) == 0) {
+        if (act0) {
+          const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t0) * NV);
+#pragma unroll
+          for (int m = 0; m < NV / 2; ++m) { const double2 t = CS ? __ldcs(qp + m) : __ldg(qp + m); q0[2 * m] = t.x; q0[2 * m + 1] = t.y; }
+        }
+        if (act1) {
+          const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t1) * NV);
+#pragma unroll
+          for (int m = 0; m < NV / 2; ++m) { const double2 t = CS ? __ldcs(qp + m) : __ldg(qp + m); q1[2 * m] = t.x; q1[2 * m + 1] = t.y; }
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < NV; ++m) {
+          q0[m] = act0 ? __ldg(v.Q + (int64_t)(wb + t0) * NV + m) : 0.0;
+          q1[m] = act1 ? __ldg(v.Q + (int64_t)(wb + t1) * NV + m) : 0.0;
+        }
+      }
+      // Pi_B (twice for r0, see masked.cuh)
+#pragma unroll
+      for (int pass = 0; pass < ((MODE == MM_R0 || MODE == MM_R0E) ? 2 : 1); ++pass) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double dv[NV];
+#pragma unroll
+          for (int m = 0; m < NV; ++m) dv[m] = fma(q0[m], g0[d], q1[m] * g1[d]);
+          int own;
+          nd2_reduce_scatter<NV>(dv, lane, &own);
+          if (own < NV) s_dot[wib][d * NV + own] = dv[0];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double s0v = 0.0, s1v = 0.0;
+#pragma unroll
+          for (int m = 0; m < NV; ++m) {
+            const double dm = s_dot[wib][d * NV + m];
+            s0v = fma(q0[m], dm, s0v);
+            s1v = fma(q1[m], dm, s1v);
+          }
+          g0[d] -= s0v;
+          g1[d] -= s1v;
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ro = wb + d * n3;
+        if (act0) {
+          if (MODE == MM_ITER) { if (CS) __stcs(out + ro + t0, g0[d]); else out[ro + t0] = g0[d]; part = fma(X[ro + t0], g0[d], part); }
+          else out[ro + t0] = -g0[d];
+        }
+        if (act1) {
+          if (MODE == MM_ITER) { if (CS) __stcs(out + ro + t1, g1[d]); else out[ro + t1] = g1[d]; part = fma(X[ro + t1], g1[d], part); }
+          else out[ro + t1] = -g1[d];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, MODE == MM_ITER ? 1 : -1);
+}
+
+// ---------------------------------------------------------------------------
+// y^ = Pi K y on the nodal path, matched-pair kernel (iteration only).
+// ncu on v2 (round 1, config 5): 10.6 G instructions per launch (2.9 k per F
+// node), issue- and L1-bound, because every block is processed for all 64
+// lane slots of the node (2 chunks of 32 positions), matched or not (a node
+// of 41 positions meets ~8 of them per block).  Here the lanes of a round
+// are the matched (pair, component b) slots of ONE block: lane l -> pair l/3,
+// b = l % 3, so ~24 of 32 lanes do useful work and a block costs ~1 round.
+// Each slot gathers y(K row 3K+e, p, b) (e = 0..2) and adds the 3x3 block
+// times them into the node's accumulators acc[d][3s + b] in shared memory:
+// a position occurs at most once per block, so the read-modify-writes of a
+// round never collide, and __syncwarp between blocks keeps the block order.
+// The accumulation order per (row d, position) is v2's (blocks ascending,
+// fma over e = 0..2 from 0.0), so y^ is bitwise v2's.
+constexpr int NPR_MAXP = ((ND_MAXB * 21 + 8 + 7) / 8) * 8;   // pairs per node (|J| <= 21 on the nodal path), 16-byte rows
+
+template <int NV, int PRG>
+__global__ void __launch_bounds__(ND_WARPS * 32, 4)
+k_spgemm_nodal_pr(DevView v, const NodalBlkP* __restrict__ blkp, const int64_t* __restrict__ bptr,
+                  const uint16_t* __restrict__ pr, const int64_t* __restrict__ proff, int64_t nFn,
+                  const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ __align__(16) double s_a[ND_WARPS][ND_MAXB * ND2_AST];
+  __shared__ __align__(16) double s_acc[ND_WARPS][3 * 64];
+  __shared__ int2 s_b[ND_WARPS][ND_MAXB];                 // {ybase, nK3 | np << 8 | pair offset << 16}
+  __shared__ __align__(16) uint16_t s_pr[ND_WARPS][NPR_MAXP];
+  __shared__ __align__(16) double s_dot[ND_WARPS][3 * NV + 1];
+  if (v.st->stopped) { iter_stopped(v); return; }
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int t0 = lane, t1 = lane + 32;
+  double part = 0.0;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t r = 3 * n;
+    const int wb = (int)v.wptr[r];
+    const int n3 = (int)v.wptr[r + 1] - wb;
+    const int64_t ab = v.affptr[r];
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int64_t po = proff[n];
+    const int npp = (int)(proff[n + 1] - po);
+    const int rs = 3 * nb;
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    // ---- stage: A chunk block-major (10-double stride), block records with
+    // the pair offsets (warp scan of the counts), the pair list; zero acc
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double* srow = v.affval + ab + (int64_t)d * rs;
+      for (int j = lane; j < rs; j += 32) {
+        const int b = j / 3, e = j - 3 * b;
+        s_a[wib][b * ND2_AST + d * 3 + e] = __ldcs(srow + j);
+      }
+    }
+    {
+      int2 rec = make_int2(0, 0);
+      int np = 0;
+      if (lane < nb) {
+        rec = __ldcs(reinterpret_cast<const int2*>(blkp + bb + lane));
+        np = (rec.y >> 16) & 0xFF;
+      }
+      int incl = np;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < nb) s_b[wib][lane] = make_int2(rec.x, (rec.y & 0xFF) | (np << 8) | ((incl - np) << 16));
+    }
+    {
+      const uint4* src4 = reinterpret_cast<const uint4*>(pr + po);
+      uint4* dst4 = reinterpret_cast<uint4*>(&s_pr[wib][0]);
+      for (int k = lane; k < (npp >> 3); k += 32) dst4[k] = __ldcs(src4 + k);
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      s_acc[wib][d * 64 + t0] = 0.0;
+      s_acc[wib][d * 64 + t1] = 0.0;
+    }
+    __syncwarp();
+    // ---- blocks in ascending order, lanes over the block's (pair, b) slots;
+    // the gathers of PRG rounds are issued before their read-modify-writes
+    const int lj = lane / 3, lb = lane - 3 * lj;            // slot of this lane in a round
+    int b = 0, j0 = 0;                                      // next round: block b, pairs j0 ..
+    while (b < nb) {
+      double yv[PRG][3];
+      int tt[PRG], bi[PRG];
+#pragma unroll
+      for (int u = 0; u < PRG; ++u) {
+        // advance to the next round (warp-uniform)
+        while (b < nb && j0 >= ((s_b[wib][b].y >> 8) & 0xFF)) { ++b; j0 = 0; }
+        bi[u] = b;
+        tt[u] = -1;
+        yv[u][0] = yv[u][1] = yv[u][2] = 0.0;
+        if (b < nb) {
+          const int2 kr = s_b[wib][b];
+          const int nK3 = kr.y & 0xFF, np = (kr.y >> 8) & 0xFF, pof = (int)((unsigned)kr.y >> 16);
+          const int j = j0 + lj;
+          if (lane < 30 && j < np) {
+            const int pk = s_pr[wib][pof + j];
+            tt[u] = 3 * (pk & 0xFF) + lb;
+            const double* yp = X + kr.x + 3 * (pk >> 8) + lb;
+            yv[u][0] = yp[0];
+            yv[u][1] = yp[nK3];
+            yv[u][2] = yp[2 * nK3];
+          }
+          j0 += 10;                                         // 10 pairs (30 lanes) per round
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PRG; ++u) {
+        if (bi[u] >= nb) break;                             // warp-uniform
+        const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][bi[u] * ND2_AST]);
+        const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+        if (tt[u] >= 0) {
+          double* acc = &s_acc[wib][tt[u]];
+          double c0 = acc[0], c1 = acc[64], c2 = acc[128];
+          c0 = fma(a01.x, yv[u][0], c0); c0 = fma(a01.y, yv[u][1], c0); c0 = fma(a23.x, yv[u][2], c0);
+          c1 = fma(a23.y, yv[u][0], c1); c1 = fma(a45.x, yv[u][1], c1); c1 = fma(a45.y, yv[u][2], c1);
+          c2 = fma(a67.x, yv[u][0], c2); c2 = fma(a67.y, yv[u][1], c2); c2 = fma(a8.x, yv[u][2], c2);
+          acc[0] = c0; acc[64] = c1; acc[128] = c2;
+        }
+        __syncwarp();
+      }
+    }
+    double g0[3], g1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      g0[d] = s_acc[wib][d * 64 + t0];
+      g1[d] = s_acc[wib][d * 64 + t1];
+    }
+    // ---- Pi_B with Q of the node (row 3n, shared by its 3 rows), as v2
+    double q0[NV], q1[NV];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) { q0[m] = 0.0; q1[m] = 0.0; }
+    if ((NV & 1) == 0) {
+      if (act0) {
+        const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t0) * NV);
+#pragma unroll
+        for (int m = 0; m < NV / 2; ++m) { const double2 q = __ldcs(qp + m); q0[2 * m] = q.x; q0[2 * m + 1] = q.y; }
+      }
+      if (act1) {
+        const double2* qp = reinterpret_cast<const double2*>(v.Q + (int64_t)(wb + t1) * NV);
+#pragma unroll
+        for (int m = 0; m < NV / 2; ++m) { const double2 q = __ldcs(qp + m); q1[2 * m] = q.x; q1[2 * m + 1] = q.y; }
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < NV; ++m) {
+        q0[m] = act0 ? __ldg(v.Q + (int64_t)(wb + t0) * NV + m) : 0.0;
+        q1[m] = act1 ? __ldg(v.Q + (int64_t)(wb + t1) * NV + m) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double dv[NV];
+#pragma unroll
+      for (int m = 0; m < NV; ++m) dv[m] = fma(q0[m], g0[d], q1[m] * g1[d]);
+      int own;
+      nd2_reduce_scatter<NV>(dv, lane, &own);
+      if (own < NV) s_dot[wib][d * NV + own] = dv[0];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double s0v = 0.0, s1v = 0.0;
+#pragma unroll
+      for (int m = 0; m < NV; ++m) {
+        const double dm = s_dot[wib][d * NV + m];
+        s0v = fma(q0[m], dm, s0v);
+        s1v = fma(q1[m], dm, s1v);
+      }
+      g0[d] -= s0v;
+      g1[d] -= s1v;
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int ro = wb + d * n3;
+      if (act0) { __stcs(out + ro + t0, g0[d]); part = fma(X[ro + t0], g0[d], part); }
+      if (act1) { __stcs(out + ro + t1, g1[d]); part = fma(X[ro + t1], g1[d], part); }
+    }
+    __syncwarp();
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, 1);
+}
+
+// ---- host side ------------------------------------------------------------
+template <typename T>
+static cudaError_t nd_alloc(T** p, int64_t n, cudaStream_t s) {
+  return emin_mallocAsync((void**)p, sizeof(T) * (size_t)(n > 0 ? n : 1), s);
+}
+
+// returns true if the nodal path was built
+static inline bool select_nodal_path(emin_ctx c, NodalPlan*& out) {
+  out = nullptr;
+  if (c->opts.block_size != 3 || c->nF % 3 != 0 || c->nF == 0 || c->nv > 8 || c->nnzWh >= INT32_MAX) return false;
+  if (c->opts.debug_flags & EMIN_DBG_FORCE_GENERIC) return false;
+  cudaStream_t s = c->stream;
+  const int SM = emin_num_sms();
+  const int64_t nFn = c->nF / 3;
+  int32_t* ok;
+  int64_t *pmlen, *scratch, *tot;
+  if (nd_alloc(&ok, 2, s) || nd_alloc(&pmlen, nFn + 1, s) || nd_alloc(&scratch, emin_scan_scratch_elems(nFn + 1), s) ||
+      nd_alloc(&tot, 1, s))
+    return false;
+  const int32_t init[2] = {1, 0};
+  cudaMemcpyAsync(ok, init, sizeof(int32_t) * 2, cudaMemcpyHostToDevice, s);
+  k_nodal_check<<<SM * 8, 256, 0, s>>>(c->view(), nFn, ok, pmlen, ok + 1);
+  int32_t h_ok2[2] = {0, 0};
+  cudaMemcpyAsync(h_ok2, ok, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  const int32_t h_ok = h_ok2[0];
+  c->launches += 1;
+  if (!h_ok) {
+    cudaFreeAsync(ok, s); cudaFreeAsync(pmlen, s); cudaFreeAsync(scratch, s); cudaFreeAsync(tot, s);
+    return false;
+  }
+  NodalPlan* p = new NodalPlan();
+  p->nFn = nFn;
+  p->max_nb = h_ok2[1];
+  p->nblk = c->nnzAFF / 9;
+  emin_scan_i64(pmlen, pmlen, nFn, tot, scratch, s);     // exclusive -> offsets
+  cudaMemcpyAsync(pmlen + nFn, tot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(&p->npm, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  p->pmoff = pmlen;
+  if (nd_alloc(&p->blk, p->nblk, s) || nd_alloc(&p->bptr, nFn + 1, s) || nd_alloc(&p->pm8, p->npm, s)) {
+    delete p;
+    return false;
+  }
+  k_nodal_build<<<SM * 8, 256, 0, s>>>(c->view(), nFn, p->pmoff, p->blk, p->bptr, p->pm8);
+  c->launches += 4;
+  // matched-pair lists for the iteration kernel (node stencils of <= ND_MAXB blocks)
+  if (p->max_nb <= ND_MAXB) {
+    int64_t* cnt = nullptr;
+    if (!nd_alloc(&p->blkp, p->nblk, s) && !nd_alloc(&p->proff, nFn + 1, s) && !nd_alloc(&cnt, nFn + 1, s)) {
+      k_nodal_pairs<0><<<SM * 8, 256, 0, s>>>(nFn, p->bptr, p->blk, p->pm8, p->pmoff, c->wptr, p->blkp, cnt,
+                                               nullptr, nullptr);
+      emin_scan_i64(cnt, p->proff, nFn, tot, scratch, s);
+      cudaMemcpyAsync(p->proff + nFn, tot, sizeof(int64_t), cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(&p->npr, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      if (!nd_alloc(&p->pr, p->npr + 8, s)) {
+        k_nodal_pairs<1><<<SM * 8, 256, 0, s>>>(nFn, p->bptr, p->blk, p->pm8, p->pmoff, c->wptr, nullptr,
+                                                 nullptr, p->proff, p->pr);
+        c->launches += 5;
+      }
+    }
+    if (cnt) cudaFreeAsync(cnt, s);
+    if (!p->pr) {                       // (allocation failed: the v2 kernel runs instead)
+      if (p->blkp) cudaFreeAsync(p->blkp, s);
+      if (p->proff) cudaFreeAsync(p->proff, s);
+      p->blkp = nullptr;
+      p->proff = nullptr;
+    }
+  }
+  cudaFreeAsync(ok, s); cudaFreeAsync(scratch, s); cudaFreeAsync(tot, s);
+  out = p;
+  return true;
+}
+
+// Grid of the nodal kernels: ~12 nodes per warp, between 32 and 256 CTAs
+// per SM.  Many short CTAs dispatched in order keep the resident warps on a
+// narrow, advancing window of nodes, so neighbour rows of y stay in L2
+// (config 5: SM x 16 CTAs 15.27 ms, x 64 14.76, x 256 14.33; config 4 is
+// best at x 32: 396 vs 404 us at x 16).
+static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
+  const int SM = emin_num_sms();
+  int64_t per_sm = std::min<int64_t>(256, std::max<int64_t>(32, p->nFn / (8 * 12) / SM));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((p->nFn + 7) / 8, (int64_t)SM * per_sm));
+}
+
+// one v2 configuration for every mode: CS = evict-first hints (iteration
+// only), WIDE = chunked staging (> ND_MAXB blocks per node), GRP = blocks per
+// round
+template <int NV, bool CS, bool WIDE, int GRP, int MINB = 4, bool PRED = false>
+static inline void nd_v2(int mode, const DevView& v, const NodalPlan* p, int g, const double* X, const double* X2,
+                         double* out, double* partials, cudaStream_t s) {
+#define ND_ARGS <<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, partials)
+  if (mode == MM_ITER) k_spgemm_nodal_v2<NV, MM_ITER, PRED, CS, WIDE, GRP, MINB> ND_ARGS;
+  else if (mode == MM_R0) k_spgemm_nodal_v2<NV, MM_R0, false, false, WIDE, GRP> ND_ARGS;
+  else if (mode == MM_R0E) k_spgemm_nodal_v2<NV, MM_R0E, false, false, WIDE, GRP> ND_ARGS;
+  else k_spgemm_nodal_v2<NV, MM_ENERGY, false, false, WIDE, GRP> ND_ARGS;
+#undef ND_ARGS
+}
+
+template <bool CS, bool WIDE, int GRP, int MINB = 4, bool PRED = false>
+static inline void nd_v2_nv(int nv, int mode, const DevView& v, const NodalPlan* p, int g, const double* X,
+                            const double* X2, double* out, double* partials, cudaStream_t s) {
+  switch (nv) {
+#define NV_CASE(N) case N: nd_v2<N, CS, WIDE, GRP, MINB, PRED>(mode, v, p, g, X, X2, out, partials, s); break;
+    NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+#undef NV_CASE
+  }
+}
+
+static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const double* X, const double* X2,
+                                double* out, cudaStream_t s) {
+  const DevView v = c->view();
+  const int g = nodal_grid(c, p);
+  // v2 with two blocks per round (all gathers of both issued before the
+  // FMAs; config 5 20.7 -> 15.9 ms, config 4 471 -> 420 us; three or four per
+  // round spill or lose occupancy: 16.6 / 21.0+ ms) and, in the iteration,
+  // evict-first hints on the streamed data (A chunk, block records, position
+  // bytes, Q, y^) so the L2 keeps the gathered y rows.  Galerkin levels
+  // (NEXT-4, > ND_MAXB blocks per node): the same, staged in chunks.
+  if (mode == MM_ITER && p->pr && !(c->opts.debug_flags & EMIN_DBG_AB1)) {
+    // the iteration: matched-pair kernel (bitwise v2's y^)
+    switch (c->nv) {
+#define NV_CASE(N) \
+  case N: k_spgemm_nodal_pr<N, 4><<<g, ND_WARPS * 32, 0, s>>>(v, p->blkp, p->bptr, p->pr, p->proff, p->nFn, X, out, c->partials); break;
+      NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
+#undef NV_CASE
+    }
+    return true;
+  }
+  if (p->max_nb > ND_MAXB)
+    nd_v2_nv<true, true, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
+  else
+    nd_v2_nv<true, false, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
+  return true;
+}
+
+static inline void free_nodal_path(emin_ctx c, NodalPlan*& p) {
+  if (!p) return;
+  void* ptrs[] = {p->blk, p->bptr, p->pm8, p->pmoff};
+  for (void* q : ptrs) if (q) cudaFreeAsync(q, c->stream);
+  void* ptrs2[] = {p->pr, p->proff, p->blkp};
+  for (void* q : ptrs2) if (q) cudaFreeAsync(q, c->stream);
+  delete p;
+  p = nullptr;
+}

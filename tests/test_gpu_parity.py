@@ -523,3 +523,4 @@ def test_option_validation():
                           arr[3].ctypes.data, prob.nc, 2, 4, rp.ctypes.data, col.ctypes.data, 4, C.byref(nnz), 0,
                           None)
     assert st == 1 and nnz.value == prob.P_rowptr[-1] and np.array_equal(rp, prob.P_rowptr)
+
