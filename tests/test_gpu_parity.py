@@ -524,3 +524,78 @@ def test_option_validation():
                           None)
     assert st == 1 and nnz.value == prob.P_rowptr[-1] and np.array_equal(rp, prob.P_rowptr)
 
+
+
+def _indefinite(name, size, scale):
+    """The workload with its off-diagonal couplings scaled up: A(i,i) > 0
+    still holds (so setup accepts it), but A_FF is indefinite and the CG
+    meets negative curvature y^T Pi K y < 0 after a few steps."""
+    from workloads.problems import make_config
+    p = make_config(name, size=size)
+    rows = np.repeat(np.arange(p.n), np.diff(p.A_rowptr))
+    A = p.A_val.copy()
+    A[rows != p.A_col] *= scale
+    p.A_val = A
+    return p
+
+
+@pytest.mark.parametrize("name,size,scale,dbg,path", [("1b", None, 3.0, 0, 1), ("3", 10, 2.0, 0, 1), ("4", 3, 2.0, 0, 2),
+                                                      ("4", 3, 2.0, 1, 0)])
+def test_breakdown_on_negative_curvature(name, size, scale, dbg, path):
+    """S:336 / SURVEY §8b breakdown rule: y^T Pi K y < 0 is EMIN_ERR_BREAKDOWN;
+    GPU and oracle stop at the same step, before applying it (reading A18),
+    with the same P (the steps taken before it agree to the parity bars)."""
+    from oracle import Oracle, OracleError
+    from paper_2208_02995_b200 import Emin, EminError
+    prob = _indefinite(name, size, scale)
+    g = Emin.from_problem(prob, debug_flags=dbg)
+    assert g.report()["kernel_path"] == path
+    with pytest.raises(EminError) as e:
+        g.iterate(30)
+    assert e.value.code == 7
+    rep = g.report()                         # reported once; the report itself is clean
+    assert rep["stop_reason"] == 5
+    o = Oracle(prob, project_z=True)
+    with pytest.raises(OracleError) as eo:
+        o.iterate(30)
+    assert eo.value.code == 7
+    assert rep["k_total"] == o.k_total >= 1
+    Po = o.get_P()
+    assert np.abs(g.get_P() - Po).max() <= P_TOL * np.abs(Po).max()
+    assert abs(g.energy() - o.energy()) <= E_TOL * abs(o.energy())
+    kd, _ = g.iterate(5)                     # stopped: no further steps
+    assert kd == 0 and g.report()["k_total"] == rep["k_total"]
+
+
+@pytest.mark.parametrize("name,size", [("3", 17), ("4", 5), ("2b", 10)])
+def test_repeat_runs_bitwise_identical(name, size):
+    """No races in the warp-synchronous shared-memory code (compute-sanitizer
+    racecheck is closed on this pool): five independent contexts, two of
+    them set up and iterated concurrently from two host threads on their own
+    streams, give bitwise identical trajectories and P."""
+    import threading
+    import torch
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    res = []
+
+    def one():
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            g = Emin.from_problem(prob, stream=s.cuda_stream)
+            kd, dE = g.iterate(25)
+            res.append((kd, dE, g.get_P(), g.energy()))
+            g.close()
+
+    for _ in range(3):
+        one()
+    th = [threading.Thread(target=one) for _ in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert len(res) == 5
+    for r in res[1:]:
+        assert r[0] == res[0][0] and np.array_equal(r[1], res[0][1])
+        assert np.array_equal(r[2], res[0][2]) and r[3] == res[0][3]
