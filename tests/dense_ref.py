@@ -114,3 +114,41 @@ def nullspace_solution(prob, w0):
     Z = s[:, None] * sla.null_space(Cm * s[None, :])   # basis of ker(C), scaled
     u = np.linalg.solve(Z.T @ H @ Z, -Z.T @ (H @ w0 + g))
     return w0 + Z @ u
+
+
+def dense_projected_pcg(prob, w0, k):
+    """Alg. 3 written densely from the quadratic form alone, as
+    a step-by-step reference for the oracle's recurrence.  With
+    E(w) = w^T H w / 2 + g^T w + e0 the paper's K = H / 2 and f = -g / 2
+    (E = w^T K w - 2 f^T w + e0); Pi = I - C^T (C C^T)^+ C is the orthogonal
+    projector onto ker C built from the dense constraint matrix (not from
+    per-row bases); M = diag(K) (Jacobi).  Returns the list of
+    (dE_k, w_k) for k = 1..steps taken (stops, like Alg. 3, when gamma or
+    y^T yb is not positive)."""
+    H, g, _ = quadratic_form(prob)
+    K = H / 2.0
+    f = -g / 2.0
+    Cm, _ = constraint_matrix(prob)
+    Pi = np.eye(K.shape[0]) - Cm.T @ np.linalg.pinv(Cm @ Cm.T) @ Cm
+    dK = np.diag(K)
+    w = w0.copy()
+    r = Pi @ (f - K @ w)                                   # P:838 (readings A1, A2)
+    y = None
+    gamma_old = None
+    out = []
+    for it in range(k):
+        z = Pi @ (r / dK)                                  # P:840
+        gamma = float(r @ z)                               # P:841
+        if not gamma > 0.0:
+            break
+        y = z.copy() if it == 0 else z + (gamma / gamma_old) * y   # P:842-847
+        gamma_old = gamma                                  # P:848
+        yb = Pi @ (K @ y)                                  # P:849
+        den = float(y @ yb)
+        if not den > 0.0:
+            break
+        alpha = gamma / den                                # P:850
+        w = w + alpha * y                                  # P:853
+        r = r - alpha * yb                                 # P:854
+        out.append((gamma * alpha, w.copy()))              # dE_k = gamma alpha, P:851
+    return out
