@@ -144,6 +144,8 @@ typedef struct {
   int64_t n_halo_rows; /* F rows of other ranks whose pattern / values this rank receives */
   int64_t n_halo_entries;  /* their W entries (doubles received per halo exchange) */
   int64_t n_send_entries;  /* W entries this rank sends per halo exchange */
+  int64_t n_interior_units;  /* units (windows / nodes / rows of the kernel path) of y^ = Pi K y
+                                computed while the halo is exchanged (0: no overlap) */
 } emin_report_t;
 
 /* Fill opts with defaults (rank_tol 1e-10, tau 0, project_after_jacobi 0,

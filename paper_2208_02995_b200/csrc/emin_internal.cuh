@@ -58,9 +58,26 @@ struct DevView {
   const double* Q;       // [nnzW * nv] row-major per entry, zero padded
   DevState* st;
   int32_t pingpong;      // L2 ping-pong traversal order (see iterate.cu)
-  int32_t fuse;          // 1: the last block of stage I / SpGEMM applies the scalar step
+  int32_t fuse;          // 1: the last block of stage I / SpGEMM applies the scalar step;
+                         // 2: it writes the rank-local sum to st->red[] (allreduce follows)
   double* dE_hist;       // per-step energy decrements (scalar step of the SpGEMM)
+  // the y^ = Pi K y launch (MM_ITER) may be split into an interior and a
+  // boundary launch (multi-GPU overlap, iterate.cu): units [ubeg, uend)
+  // (windows / nodes / rows of the kernel path; uend < 0 = all) and the
+  // launch's first slot in the partial-sum array
+  int64_t ubeg, uend;
+  int64_t ugap0, ugap1;  // ... minus the units [ugap0, ugap1) (the boundary launch skips the interior)
+  int32_t poff;
 };
+
+// unit range of a (possibly split) y^ launch: idx in [0, unit_count) -> unit
+__device__ __forceinline__ int64_t unit_count(const DevView& v, int64_t n) {
+  return (v.uend < 0 ? n : v.uend) - v.ubeg - (v.ugap1 - v.ugap0);
+}
+__device__ __forceinline__ int64_t unit_of(const DevView& v, int64_t idx) {
+  const int64_t w = v.ubeg + idx;
+  return w >= v.ugap0 ? w + (v.ugap1 - v.ugap0) : w;
+}
 
 struct emin_ctx_s {
   emin_opts opts;
@@ -76,6 +93,15 @@ struct emin_ctx_s {
   int32_t pingpong = 0;        // alternate traversal directions (L2 ping-pong, iterate.cu)
   int32_t fuse = 0;            // scalar steps fused into the producing kernels (EMIN_DBG_FUSE_SCALARS)
   int32_t iter_kernels = 5;    // our kernel launches per CG iteration (set at graph capture)
+  // y^ launch split (multi-GPU): the view of the launch being enqueued
+  int64_t mm_ubeg = 0, mm_uend = -1, mm_ugap0 = 0, mm_ugap1 = 0;
+  int32_t mm_poff = 0;
+  // interior units [split_u0, split_u1) of the y^ launch: no halo row among
+  // their A_FF neighbours (computed by emin_dist_split; split_on = 0: none)
+  int32_t split_on = 0;
+  int64_t split_u0 = 0, split_u1 = 0, split_n = 0;
+  cudaStream_t comm_stream = nullptr;       // halo exchange overlapped with the interior launch
+  cudaEvent_t ev_y = nullptr, ev_halo = nullptr;
   // device arrays (owned by ctx)
   int64_t *wptr = nullptr, *affptr = nullptr, *afcptr = nullptr, *pofs = nullptr, *cofs = nullptr;
   uint8_t* isc_own = nullptr;  // is_coarse of the owned rows
@@ -123,6 +149,11 @@ struct emin_ctx_s {
     v.pingpong = pingpong;
     v.fuse = fuse;
     v.dE_hist = dE_hist;
+    v.ubeg = mm_ubeg;
+    v.uend = mm_uend;
+    v.ugap0 = mm_ugap0;
+    v.ugap1 = mm_ugap1;
+    v.poff = mm_poff;
     return v;
   }
 };
@@ -199,7 +230,7 @@ __device__ __forceinline__ void block_partial_out(const DevView& v, double* part
                                                   int which) {
   __shared__ int s_last;
   if (threadIdx.x == 0) {
-    partials[blockIdx.x] = tot;
+    partials[v.poff + blockIdx.x] = tot;
     int last = 0;
     if (which >= 0 && v.fuse) {
       __threadfence();
@@ -210,11 +241,14 @@ __device__ __forceinline__ void block_partial_out(const DevView& v, double* part
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // (a split launch: the earlier launches' partials [0, poff) precede in
+  // stream order and are complete)
   double sum = 0.0;
-  for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) sum += __ldcg(partials + k);
+  for (int k = threadIdx.x; k < v.poff + (int)gridDim.x; k += blockDim.x) sum += __ldcg(partials + k);
   sum = block_sum(sum, sh);
   if (threadIdx.x == 0) {
-    if (which == 0) scalar_gamma_apply(v.st, sum);
+    if (v.fuse == 2) v.st->red[which] = sum;       // rank-local sum (multi-GPU: allreduce, scalar kernel)
+    else if (which == 0) scalar_gamma_apply(v.st, sum);
     else {
       v.st->pendw = 0;
       if (!v.st->stopped) scalar_alpha_apply(v.st, sum, v.dE_hist);
@@ -225,7 +259,7 @@ __device__ __forceinline__ void block_partial_out(const DevView& v, double* part
 // a fused SpGEMM that returns early on a stopped state still retires the
 // pending dw update flag (what the separate alpha kernel did)
 __device__ __forceinline__ void iter_stopped(const DevView& v) {
-  if (v.fuse && blockIdx.x == 0 && threadIdx.x == 0) v.st->pendw = 0;
+  if (v.fuse == 1 && blockIdx.x == 0 && threadIdx.x == 0) v.st->pendw = 0;
 }
 
 // lower_bound of key in sorted a[0..n)

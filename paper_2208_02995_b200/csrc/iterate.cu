@@ -349,6 +349,44 @@ __global__ void k_get_P_crows(int64_t m, const uint8_t* __restrict__ isc, const 
     if (isc[rl]) out[prp[rl] - prp[0]] = 1.0;
 }
 
+// ------------------------------------------------------------ interior / boundary split (multi-GPU)
+// a row is a boundary row if one of its A_FF neighbours is a halo row (local
+// id >= nF); lohi[0] = 1 + the last boundary row of the lower half, lohi[1] =
+// the first boundary row of the upper half (z-slab partitions: the halo
+// planes sit at both ends of the owned rows)
+__global__ void k_boundary_bounds(const int64_t* __restrict__ affptr, const int32_t* __restrict__ affcol, int64_t nF,
+                                  unsigned long long* lohi) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x) {
+    bool bnd = false;
+    for (int64_t q = affptr[i]; q < affptr[i + 1]; ++q) bnd |= affcol[q] >= nF;
+    if (bnd) {
+      if (i < nF / 2) atomicMax(&lohi[0], (unsigned long long)(i + 1));
+      else atomicMin(&lohi[1], (unsigned long long)i);
+    }
+  }
+}
+__global__ void k_boundary_count(const int64_t* __restrict__ affptr, const int32_t* __restrict__ affcol, int64_t nF,
+                                 const unsigned long long* __restrict__ lohi, unsigned long long* cnt) {
+  const int64_t ib = (int64_t)lohi[0], ie = (int64_t)lohi[1];
+  for (int64_t i = ib + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ie; i += (int64_t)gridDim.x * blockDim.x) {
+    bool bnd = false;
+    for (int64_t q = affptr[i]; q < affptr[i + 1]; ++q) bnd |= affcol[q] >= nF;
+    if (bnd) atomicAdd(cnt, 1ull);
+  }
+}
+// scalar path: the windows whose rows all lie in [ib, ie)
+__global__ void k_window_range(const int32_t* __restrict__ rowstart, int64_t nwin, const unsigned long long* lohi,
+                               unsigned long long* out) {
+  const int64_t ib = (int64_t)lohi[0], ie = (int64_t)lohi[1];
+  int64_t lo = 0, hi = nwin;                 // first w with rowstart[w] >= ib
+  while (lo < hi) { const int64_t m = (lo + hi) / 2; if (rowstart[m] < ib) lo = m + 1; else hi = m; }
+  const int64_t w0 = lo;
+  lo = 0; hi = nwin;                         // windows w with rowstart[w + 1] <= ie
+  while (lo < hi) { const int64_t m = (lo + hi) / 2; if (rowstart[m + 1] <= ie) lo = m + 1; else hi = m; }
+  out[0] = (unsigned long long)w0;
+  out[1] = (unsigned long long)lo;
+}
+
 int pick_group(double avg) {
   int best = 1;
   double best_eff = 0.0;
@@ -426,6 +464,50 @@ int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, 
   return grid;
 }
 
+// Interior units of the y^ launch (multi-GPU): rows / windows / nodes whose
+// A_FF neighbours are all owned, so their part of the masked product can run
+// while the halo of y is exchanged (only the halo rows need the
+// peers' values).  Stays off (split_on = 0) without an interior range.
+static emin_status emin_split_plan(emin_ctx c) {
+  c->split_on = 0;
+  if (!c->dist || c->nF < 64) return EMIN_OK;
+  cudaStream_t s = c->stream;
+  const int SM = emin_num_sms();
+  unsigned long long* d;
+  EMIN_CUDA_TRY(c, emin_mallocAsync(&d, sizeof(unsigned long long) * 5, s));
+  const unsigned long long init[5] = {0ull, (unsigned long long)c->nF, 0ull, 0ull, 0ull};
+  EMIN_CUDA_TRY(c, cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  k_boundary_bounds<<<SM * 4, 256, 0, s>>>(c->affptr, c->affcol, c->nF, d);
+  k_boundary_count<<<SM * 4, 256, 0, s>>>(c->affptr, c->affcol, c->nF, d, d + 2);
+  c->launches += 2;
+  int64_t nunits = c->nF;
+  if (c->kernel_path == 1) {
+    int64_t nwin = 0;
+    const int32_t* rs = emin_scalar_windows(c, &nwin);
+    k_window_range<<<1, 1, 0, s>>>(rs, nwin, d, d + 3);
+    c->launches += 1;
+    nunits = nwin;
+  }
+  unsigned long long h[5];
+  EMIN_CUDA_TRY(c, cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+  EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+  cudaFreeAsync(d, s);
+  const int64_t ib = (int64_t)h[0], ie = (int64_t)h[1];
+  if (h[2] != 0 || ie <= ib) return EMIN_OK;          // boundary rows inside: no split
+  int64_t u0 = ib, u1 = ie;
+  if (c->kernel_path == 1) { u0 = (int64_t)h[3]; u1 = (int64_t)h[4]; }
+  if (c->kernel_path == 2) { u0 = (ib + 2) / 3; u1 = ie / 3; nunits = c->nF / 3; }
+  if (u1 <= u0) return EMIN_OK;
+  c->split_u0 = u0;
+  c->split_u1 = u1;
+  c->split_n = nunits;
+  EMIN_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  EMIN_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_y, cudaEventDisableTiming));
+  EMIN_CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  c->split_on = 1;
+  return EMIN_OK;
+}
+
 // kernel path + launch geometry (end of the index preparation in setup)
 emin_status emin_plan(emin_ctx c) {
   const int SM = emin_num_sms();
@@ -457,6 +539,13 @@ emin_status emin_plan(emin_ctx c) {
   c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
   if (c->kernel_path == 1) c->grid_red = std::max(c->grid_red, scalar_iter_grid(c));
   if (c->kernel_path == 2) c->grid_red = std::max(c->grid_red, nodal_grid(c, static_cast<NodalPlan*>(c->nodal)));
+  if (c->dist) {
+    // the y^ launch may run as an interior and a boundary launch (both
+    // write partial sums): room for two grids
+    c->grid_red *= 2;
+    emin_status sst = emin_split_plan(c);
+    if (sst != EMIN_OK) return sst;
+  }
   if (c->grid_red > c->n_partials) {
     cudaFreeAsync(c->partials, c->stream);
     EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->partials, sizeof(double) * c->grid_red, c->stream));
@@ -506,10 +595,13 @@ bool emin_alg2_fast(emin_ctx c, const double* Bc, const double* B, const int64_t
 // Sum of the per-block partials; on several GPUs: rank-local sum into
 // st->red[slot], allreduce into st->redg[slot], and the consumer reads that
 // (np = -1).  *res = the (pointer, np) pair the consumer kernel takes.
-static emin_status global_sum(emin_ctx c, int np, int slot, cudaStream_t s, std::pair<const double*, int>* res) {
+static emin_status global_sum(emin_ctx c, int np, int slot, cudaStream_t s, std::pair<const double*, int>* res,
+                              bool local_done = false) {
   if (!c->dist) { *res = {c->partials, np}; return EMIN_OK; }
-  k_energy_out<<<1, 1024, 0, s>>>(c->partials, np, 0.0, &c->st->red[slot]);
-  c->launches += 1;
+  if (!local_done) {     // (fused: the producing kernel's last block wrote st->red[slot])
+    k_energy_out<<<1, 1024, 0, s>>>(c->partials, np, 0.0, &c->st->red[slot]);
+    c->launches += 1;
+  }
   *res = {&c->st->redg[slot], -1};
   return emin_dist_allreduce(c, &c->st->red[slot], &c->st->redg[slot], 1, s);
 }
@@ -551,7 +643,12 @@ static emin_status enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev
   // dependent DevState loads -- costs what the separate launch did;
   // profiles/r01b/spgemm_ab_c3.txt), so it is not the default
   c->fuse = (!c->dist && (c->opts.debug_flags & EMIN_DBG_FUSE_SCALARS)) ? 1 : 0;
+  // several GPUs: the rank-local sums are folded into the producing kernels'
+  // last block (st->red[]), so each CG scalar costs one allreduce and the
+  // scalar kernel, no separate reduction kernel
+  if (c->dist) c->fuse = 2;
   if (c->sgs) c->fuse = 0;
+  const bool fused_local = c->fuse == 2;
   std::pair<const double*, int> red;
   emin_status st = EMIN_OK;
   rec(0);
@@ -559,33 +656,56 @@ static emin_status enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev
   if (c->sgs) g1 = emin_sgs_enqueue(c, s);   // z = Pi M_2^-1 r, partial r.z
   else launch_stage(c, 1, s);
   rec(1);
-  if (!c->fuse) {
-    st = global_sum(c, g1, 0, s, &red);
+  if (c->fuse != 1) {
+    st = global_sum(c, g1, 0, s, &red, fused_local);
     if (st != EMIN_OK) return st;
     k_scalar_gamma<<<1, 1024, 0, s>>>(c->st, red.first, red.second);
   }
   rec(2);
   if (c->sgs) emin_sgs_stage2(c, s);
   else launch_stage(c, 2, s);
-  if (c->dist) {
-    st = emin_dist_halo_values(c, c->y, s);     // y on the halo rows
+  int g = 0;
+  if (c->dist && c->split_on) {
+    // the halo of y on the comm stream, overlapped with the
+    // interior part of y^; the boundary part waits for it
+    cudaEventRecord(c->ev_y, s);
+    cudaStreamWaitEvent(c->comm_stream, c->ev_y, 0);
+    st = emin_dist_halo_values(c, c->y, c->comm_stream);
     if (st != EMIN_OK) return st;
+    cudaEventRecord(c->ev_halo, c->comm_stream);
+    rec(3);
+    const int32_t fz = c->fuse;
+    c->fuse = 0;                                       // the interior launch only writes partials
+    c->mm_ubeg = c->split_u0; c->mm_uend = c->split_u1; c->mm_ugap0 = c->mm_ugap1 = 0; c->mm_poff = 0;
+    const int gi = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
+    c->fuse = fz;
+    cudaStreamWaitEvent(s, c->ev_halo, 0);
+    c->mm_ubeg = 0; c->mm_uend = c->split_n; c->mm_ugap0 = c->split_u0; c->mm_ugap1 = c->split_u1; c->mm_poff = gi;
+    const int gb = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
+    c->mm_ubeg = 0; c->mm_uend = -1; c->mm_ugap0 = c->mm_ugap1 = 0; c->mm_poff = 0;
+    g = gi + gb;
+  } else {
+    if (c->dist) {
+      st = emin_dist_halo_values(c, c->y, s);     // y on the halo rows
+      if (st != EMIN_OK) return st;
+    }
+    rec(3);
+    g = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
   }
-  rec(3);
-  const int g = emin_launch_masked(c, MM_ITER, c->y, nullptr, c->yb, s);
   rec(4);
-  if (!c->fuse) {
-    st = global_sum(c, g, 1, s, &red);
+  if (c->fuse != 1) {
+    st = global_sum(c, g, 1, s, &red, fused_local);
     if (st != EMIN_OK) return st;
     k_scalar_alpha<<<1, 1024, 0, s>>>(c->st, red.first, red.second, c->dE_hist);
   }
   rec(5);
-  // kernels of ours per iteration: stage I, stage II, SpGEMM (+ the two
-  // scalar kernels, + on several GPUs their rank-local sum kernels and the
-  // halo pack, + with the loopback transport its two rank-sum kernels)
+  // kernels of ours per iteration: stage I, stage II, y^ (+ the two scalar
+  // kernels; + on several GPUs the halo pack and, with the interior /
+  // boundary split, a second y^ launch; + with the loopback transport its
+  // two rank-sum kernels)
   const bool lb = c->dist && !emin_dist_capturable(c);
-  c->iter_kernels = 3 + (c->fuse ? 0 : 2) + (c->dist ? 2 + (c->dist->nSE ? 1 : 0) : 0) + (lb ? 2 : 0) +
-                    (c->sgs ? (int32_t)(2 * emin_sgs_levels(c) - 1) : 0);
+  c->iter_kernels = 3 + (c->fuse == 1 ? 0 : 2) + (c->dist ? (c->dist->nSE ? 1 : 0) + (c->split_on ? 1 : 0) : 0) +
+                    (lb ? 2 : 0) + (c->sgs ? (int32_t)(2 * emin_sgs_levels(c) - 1) : 0);
   return cudaGetLastError() == cudaSuccess ? EMIN_OK : EMIN_ERR_CUDA;
 }
 
@@ -850,6 +970,7 @@ extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
     rep->n_halo_rows = c->dist->nH;
     rep->n_halo_entries = c->dist->nHW;
     rep->n_send_entries = c->dist->nSE;
+    rep->n_interior_units = c->split_on ? c->split_u1 - c->split_u0 : 0;
   }
   if (h.stopped == 5 && !c->breakdown_reported) {
     c->breakdown_reported = 1;
@@ -914,6 +1035,9 @@ extern "C" void emin_destroy(emin_ctx c) {
   if (c->graph_prof_src) cudaGraphDestroy(c->graph_prof_src);
   emin_free_all(c);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->ev_y) cudaEventDestroy(c->ev_y);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;                                   // (the capture stream is kept per thread and device)
 }
 

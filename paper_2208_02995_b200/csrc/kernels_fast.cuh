@@ -103,8 +103,9 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double part = 0.0;
   const bool rev = v.pingpong && (v.st->k_total & 1);   // same direction as stage I (L2 ping-pong)
-  for (int64_t w1 = gw; w1 < nwin; w1 += nw) {
-    const int64_t w = rev ? nwin - 1 - w1 : w1;
+  const int64_t cnt = unit_count(v, nwin);
+  for (int64_t w1 = gw; w1 < cnt; w1 += nw) {
+    const int64_t w = unit_of(v, rev ? cnt - 1 - w1 : w1);
     const int r0 = rowstart[w];
     const int nrows = rowstart[w + 1] - r0;
     if (nrows == 0) continue;                          // warp-uniform

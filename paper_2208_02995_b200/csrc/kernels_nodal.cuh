@@ -195,7 +195,9 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
   const int t0 = lane, t1 = lane + 32;
   const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
   double part = 0.0;
-  for (int64_t n = gw; n < nFn; n += nw) {
+  const int64_t ncnt = unit_count(v, nFn);
+  for (int64_t n1 = gw; n1 < ncnt; n1 += nw) {
+    const int64_t n = unit_of(v, n1);
     const int64_t r = 3 * n;
     const int wb = (int)v.wptr[r];
     const int n3 = (int)v.wptr[r + 1] - wb;

@@ -32,7 +32,9 @@ k_masked_generic(DevView v, const double* __restrict__ X, const double* __restri
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int nv = v.nv;
   double part = 0.0;
-  for (int64_t i = gw; i < v.nF; i += nw) {
+  const int64_t icnt = unit_count(v, v.nF);
+  for (int64_t i1 = gw; i1 < icnt; i1 += nw) {
+    const int64_t i = unit_of(v, i1);
     const int64_t b = v.wptr[i];
     const int nj = (int)(v.wptr[i + 1] - b);
     int32_t jj[MAXC];

@@ -62,7 +62,8 @@ class emin_report_t(C.Structure):
                 ("nnz_AFF", C.c_int64), ("kernel_path", C.c_int32), ("nranks", C.c_int32),
                 ("launches", C.c_int64), ("precond", C.c_int32), ("sgs_levels", C.c_int64),
                 ("n_maxvol_fail", C.c_int64), ("rank", C.c_int32), ("n_halo_rows", C.c_int64),
-                ("n_halo_entries", C.c_int64), ("n_send_entries", C.c_int64)]
+                ("n_halo_entries", C.c_int64), ("n_send_entries", C.c_int64),
+                ("n_interior_units", C.c_int64)]
 
 
 EXPORTED = ["emin_default_opts", "emin_setup", "emin_iterate", "emin_energy", "emin_get_P",
