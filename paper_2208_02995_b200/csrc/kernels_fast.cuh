@@ -13,7 +13,9 @@
 //   nibble t of pm is the position of J_i[t] in J_k (0xF: absent).  So the
 //   inner loop is one 16-byte broadcast load, a nibble extract and one
 //   gather of y(k, s) -- no search.
-// Per-iteration kernel: k_spgemm_win2; setup / energy modes: the tile kernel
+// Per-iteration kernel: k_spgemm_wd (win2's windows with the decode
+// precomputed at setup; k_spgemm_win2 when the descriptors overflow);
+// setup / energy modes: the tile kernel
 // (k_spgemm_tile, fused MM_R0E at setup), or win2's modes (k_spgemm_win2m)
 // when a tile's records do not fit in shared memory.  The round-1 A/B
 // variants (profiles/ab_r01/) are not part of the library.
@@ -33,6 +35,8 @@ struct TileHdr;
 struct ScalarPlan {
   SpEnt* ent = nullptr;
   int32_t* rowstart = nullptr;   // [nwin + 1]
+  int4* whdr = nullptr;          // [nwin] {first W entry, first record, entries, 0} (k_spgemm_wd)
+  uint32_t* wdesc = nullptr;     // [nnzW] lane descriptor (k_spgemm_wd)
   int64_t nwin = 0;
   int32_t S = 0;
   TileHdr* hdr = nullptr;        // [ntiles] (staged tile kernel, setup / energy modes)
@@ -158,6 +162,76 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
 #pragma unroll 4
       for (; q < qe; ++q) {
         const int4 en = __ldg(&A4[q]);              // one 16-byte load: {a, ybase, pm}
+        const unsigned s = ((unsigned)en.w >> sh4) & 0xFu;
+        if (s != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)s], acc);
+      }
+    }
+    s_qa[wib][lane] = qv * acc;
+    __syncwarp();
+    double dot = 0.0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)                       // |J_i| <= 8 on the scalar path
+      if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+    __syncwarp();
+    if (act) {
+      const double g = acc - qv * dot;
+      out[e] = g;
+      part = fma(xo, g, part);
+    }
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, 1);
+}
+
+// y^ = Pi K y (nv = 1), window-descriptor kernel: the same windows, records
+// and arithmetic as k_spgemm_win2 (bitwise the same y^ and partial sums), but
+// the window decode is precomputed at setup -- a 16-byte header per window
+// {first W entry, first record, entries} and a 32-bit descriptor per W entry
+// {row's first lane, row length, row's record count and first record
+// relative to the window's} -- so the per-window dependent-load chain
+// rowstart -> wptr -> affptr -> record (4 latencies, 41 % of win2's stall
+// samples, profiles/r02) becomes header -> descriptor -> record.
+constexpr uint32_t WD_MAXREC = 255, WD_MAXREL = 65535;
+__global__ void __launch_bounds__(256, 8)
+k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whdr, const uint32_t* __restrict__ wdesc,
+            int32_t nwin, const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[8][32];
+  if (v.st->stopped) { iter_stopped(v); return; }
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  double part = 0.0;
+  const bool rev = v.pingpong && (v.st->k_total & 1);   // same direction as stage I (L2 ping-pong)
+  const bool split = v.uend >= 0 || v.ubeg != 0 || v.ugap1 != v.ugap0;
+  const int cnt = split ? (int)unit_count(v, nwin) : nwin;
+  const int4* A4 = reinterpret_cast<const int4*>(A);
+  for (int w1 = gw; w1 < cnt; w1 += nw) {
+    int w = rev ? cnt - 1 - w1 : w1;
+    if (split) w = (int)unit_of(v, w);
+    const int4 h = __ldg(whdr + w);
+    const int nent = h.z;
+    if (nent == 0) continue;                           // warp-uniform
+    const bool act = lane < nent;
+    const int e = h.x + lane;
+    const uint32_t dsc = act ? __ldg(wdesc + e) : 0u;
+    const double qv = act ? v.Q[e] : 0.0;
+    const double xo = act ? X[e] : 0.0;
+    const int rowbeg = (int)(dsc & 31u);
+    const int rowlen = (int)((dsc >> 5) & 7u) + 1;
+    const int qb = h.y + (int)(dsc >> 16);
+    const int qe = qb + (int)((dsc >> 8) & 255u);
+    const int pos = lane - rowbeg;
+    double acc = 0.0;
+    if (act) {
+      // record qb is the diagonal A(i,i): its y value is the lane's own entry
+      acc = __hiloint2double(__ldg(&A4[qb]).y, __ldg(&A4[qb]).x) * xo;
+      const unsigned sh4 = 4u * (unsigned)pos;
+      int q = qb + 1;
+#pragma unroll 4
+      for (; q < qe; ++q) {
+        const int4 en = __ldg(&A4[q]);
         const unsigned s = ((unsigned)en.w >> sh4) & 0xFu;
         if (s != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)s], acc);
       }
@@ -508,6 +582,25 @@ __global__ void k_plan_rowstart(const int64_t* __restrict__ wptr, int64_t nF, in
   }
 }
 
+// window headers and lane descriptors of k_spgemm_wd, one thread per window;
+// a window whose counts do not fit the descriptor clears *ok
+__global__ void k_plan_wdesc(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
+                             const int32_t* __restrict__ rowstart, int64_t nwin, int4* __restrict__ whdr,
+                             uint32_t* __restrict__ wdesc, int32_t* ok) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const int r0 = rowstart[w], r1 = rowstart[w + 1];
+    const int64_t base = wptr[r0], rec = affptr[r0];
+    whdr[w] = make_int4((int)base, (int)rec, (int)(wptr[r1] - base), 0);
+    for (int i = r0; i < r1; ++i) {
+      const int64_t b = wptr[i], len = wptr[i + 1] - b;
+      const int64_t rc = affptr[i + 1] - affptr[i], rs = affptr[i] - rec;
+      if (len > 8 || rc < 1 || rc > (int64_t)WD_MAXREC || rs > (int64_t)WD_MAXREL) { *ok = 0; continue; }
+      const uint32_t d = (uint32_t)(b - base) | ((uint32_t)(len - 1) << 5) | ((uint32_t)rc << 8) | ((uint32_t)rs << 16);
+      for (int64_t e = b; e < b + len; ++e) wdesc[e] = d;
+    }
+  }
+}
+
 // one group of 8 lanes per F row, lane per A_FF entry (setup only)
 __global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
   const int lg = threadIdx.x & 7;
@@ -569,6 +662,29 @@ static inline int select_fast_path(emin_ctx c) {
   if (emin_mallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
+  {
+    // window headers + lane descriptors of k_spgemm_wd (k_spgemm_win2 if a
+    // window's counts do not fit the descriptor)
+    int32_t* dok = nullptr;
+    int32_t hok = 0;
+    if (emin_mallocAsync((void**)&p.whdr, sizeof(int4) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess ||
+        emin_mallocAsync((void**)&p.wdesc, sizeof(uint32_t) * std::max<int64_t>(c->nnzW, 1), s) != cudaSuccess ||
+        emin_mallocAsync((void**)&dok, sizeof(int32_t), s) != cudaSuccess)
+      return 0;
+    const int32_t one = 1;
+    cudaMemcpyAsync(dok, &one, sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    k_plan_wdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.whdr, p.wdesc, dok);
+    c->launches += 1;
+    cudaMemcpyAsync(&hok, dok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(dok, s);
+    if (!hok) {
+      cudaFreeAsync(p.whdr, s);
+      cudaFreeAsync(p.wdesc, s);
+      p.whdr = nullptr;
+      p.wdesc = nullptr;
+    }
+  }
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
   k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), p.ent);
   c->launches += 2;
@@ -623,8 +739,12 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
   if (mode == MM_ITER) {
-    // two records per round (119.1 vs 120.8 us with one, config 3)
-    k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+    // precomputed window decode (116.5 us vs win2's 120.2, config 3, profiles/r02);
+    // win2 when a window's counts overflow the lane descriptor
+    if (p.whdr)
+      k_spgemm_wd<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.wdesc, (int32_t)p.nwin, X, out, c->partials);
+    else
+      k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
     return true;
   }
   if (mode == MM_R0E) {                      // fused r0 + E0: the tile kernel only
@@ -665,6 +785,8 @@ static inline void free_fast_path(emin_ctx c) {
   FastPaths* f = fast_of(c);
   if (!f) return;
   if (f->sc.rowstart) cudaFreeAsync(f->sc.rowstart, c->stream);
+  if (f->sc.whdr) cudaFreeAsync(f->sc.whdr, c->stream);
+  if (f->sc.wdesc) cudaFreeAsync(f->sc.wdesc, c->stream);
   if (f->sc.ent) cudaFreeAsync(f->sc.ent, c->stream);
   if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
   delete f;
