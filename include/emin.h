@@ -118,7 +118,9 @@ typedef struct {
                                       kernels instead of separate single-block kernels */
 #define EMIN_DBG_ALG2_ROWS 32      /* nodal path: Alg. 2 row by row instead of once per node */
 #define EMIN_DBG_AB1 64            /* A/B switch of the kernel under study;
-                                      no effect in a library without an experiment */
+                                      currently: the nodal SGS sweeps on the unsorted blocks
+                                      (the reference the direction-sorted sweeps are tested
+                                      against) */
 
 #define EMIN_PREC_JACOBI 0
 #define EMIN_PREC_SGS 1

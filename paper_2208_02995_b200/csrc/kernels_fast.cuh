@@ -192,11 +192,13 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
 // rowstart -> wptr -> affptr -> record (4 latencies, 41 % of win2's stall
 // samples, profiles/r02) becomes header -> descriptor -> record.
 constexpr uint32_t WD_MAXREC = 255, WD_MAXREL = 65535;
-__global__ void __launch_bounds__(256, 8)
+constexpr int WD_NT = 1024;    // threads per CTA of the per-iteration launch
+template <int NT = 256>
+__global__ void __launch_bounds__(NT, 2048 / NT)
 k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whdr, const uint32_t* __restrict__ wdesc,
             int32_t nwin, const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
   __shared__ double sh[32];
-  __shared__ double s_qa[8][32];
+  __shared__ double s_qa[NT / 32][32];
   if (v.st->stopped) { iter_stopped(v); return; }
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -732,18 +734,28 @@ static inline int scalar_spgemm_grid(emin_ctx c) {
   return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
 }
 // grid of the per-iteration masked launch (MM_ITER)
-static inline int scalar_iter_grid(emin_ctx c) { return scalar_grid(c); }
+// (k_spgemm_wd: 1024-thread CTAs, 2 per SM -- a CTA's 32 consecutive
+// windows share neighbour y rows in its SM's L1: 114.7 vs 116.8 us with
+// 256-thread CTAs, config 3)
+static inline int scalar_iter_grid(emin_ctx c) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  if (!p.whdr) return scalar_grid(c);
+  const int per = 2048 / WD_NT;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + WD_NT / 32 - 1) / (WD_NT / 32),
+                                                     (int64_t)emin_num_sms() * per));
+}
 
 static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
                                         cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
   if (mode == MM_ITER) {
-    // precomputed window decode (116.5 us vs win2's 120.2, config 3, profiles/r02);
+    // precomputed window decode (114.7 us vs win2's 120.2, config 3, profiles/r02);
     // win2 when a window's counts overflow the lane descriptor
     if (p.whdr)
-      k_spgemm_wd<<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.whdr, p.wdesc, (int32_t)p.nwin, X, out, c->partials);
-    else
+      k_spgemm_wd<WD_NT><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc, (int32_t)p.nwin, X, out,
+                                                               c->partials);
+ else
       k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
     return true;
   }

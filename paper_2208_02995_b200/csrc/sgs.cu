@@ -53,6 +53,11 @@ struct SgsPlan {
   int64_t nFn = 0;
   int32_t max_nb = 0;            // > 27: Galerkin level, sweeps stage the blocks in chunks
   uint8_t* bdir = nullptr;       // [nblk] 0 own node, 1 predecessor node, 2 successor node
+  // direction-sorted copy (k_sgs_node_sort; max_nb <= 27): sweeps stage only what they couple
+  double* sA = nullptr;          // [9 nblk]
+  int2* sblk = nullptr;          // [nblk]
+  uint8_t* spm = nullptr;        // byte map, same offsets as pm8
+  int32_t* npred = nullptr;      // [nFn]
 };
 
 namespace {
@@ -347,6 +352,49 @@ __global__ void k_sgs_node_levels(DevView v, int64_t nFn, const int64_t* __restr
   }
 }
 
+// direction-sorted copy of a node's blocks for k_sgs_sweep_nodal_ds: the
+// own block first, then the predecessor nodes' blocks, then the successors'
+// (each group in A's column order, so the sweeps add them in the same order
+// as the unsorted kernel); A block-major (9 doubles), records and byte-map
+// rows moved with them; npred per node.  Warp per node, lane per block.
+__global__ void k_sgs_node_sort(DevView v, int64_t nFn, const int64_t* __restrict__ bptr,
+                                const uint8_t* __restrict__ bdir, const int2* __restrict__ blk,
+                                const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
+                                double* __restrict__ sA, int2* __restrict__ sblk, uint8_t* __restrict__ spm,
+                                int32_t* __restrict__ npred, int32_t* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = gw; n < nFn; n += nw) {
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int64_t ab = v.affptr[3 * n];
+    const int rs = 3 * nb;
+    const int nJ = (int)((v.wptr[3 * n + 1] - v.wptr[3 * n]) / 3);
+    const uint8_t dl = lane < nb ? bdir[bb + lane] : 3;
+    const unsigned below = (1u << lane) - 1u;
+    const unsigned ownm = __ballot_sync(0xffffffffu, dl == 0);
+    const unsigned prem = __ballot_sync(0xffffffffu, dl == 1);
+    const unsigned sucm = __ballot_sync(0xffffffffu, dl == 2);
+    const int np = __popc(prem);
+    if (lane == 0) {
+      npred[n] = np;
+      if (__popc(ownm) != 1 || nb > 27) atomicExch(bad, 1);
+    }
+    if (lane < nb) {
+      const int j = dl == 0 ? 0 : dl == 1 ? 1 + __popc(prem & below) : 1 + np + __popc(sucm & below);
+      const int b = lane;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int e = 0; e < 3; ++e) sA[9 * (bb + j) + 3 * d + e] = v.affval[ab + (int64_t)d * rs + 3 * b + e];
+      sblk[bb + j] = blk[bb + b];
+      const int64_t po = pmoff[n];
+      for (int t = 0; t < nJ; ++t) spm[po + (int64_t)j * nJ + t] = pm8[po + (int64_t)b * nJ + t];
+    }
+  }
+}
+
 // Forward (FWD) / backward sweep over the F nodes of one level, warp per
 // node, lane t owns pattern positions t and t + 32 of the node's 3 rows.
 //   FWD:  acc_d = x_d - sum_{pred nodes K, e} A_IK[d][e] u_K[e](pos);
@@ -524,6 +572,211 @@ k_sgs_sweep_nodal(DevView v, const int2* __restrict__ blk, const int64_t* __rest
       }
     }
     }  // chunks
+    double o0[3], o1[3];
+    if (FWD) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double a0 = acc0[d], a1 = acc1[d];
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+          if (e < d) { a0 -= own[d * 3 + e] * o0[e]; a1 -= own[d * 3 + e] * o1[e]; }
+        o0[d] = a0 / own[d * 3 + d];
+        o1[d] = a1 / own[d * 3 + d];
+      }
+      if (TOP) {                                   // no successor nodes: the node's backward solve
+        double u0[3], u1[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) { u0[d] = o0[d]; u1[d] = o1[d]; }
+#pragma unroll
+        for (int d = 2; d >= 0; --d) {
+          const double dd = own[d * 3 + d];
+          double a0 = __dmul_rn(dd, u0[d]), a1 = __dmul_rn(dd, u1[d]);
+#pragma unroll
+          for (int e = 0; e < 3; ++e)
+            if (e > d) { a0 -= own[d * 3 + e] * o0[e]; a1 -= own[d * 3 + e] * o1[e]; }
+          o0[d] = a0 / dd;
+          o1[d] = a1 / dd;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int d = 2; d >= 0; --d) {
+        double a0 = acc0[d], a1 = acc1[d];
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+          if (e > d) { a0 -= own[d * 3 + e] * o0[e]; a1 -= own[d * 3 + e] * o1[e]; }
+        o0[d] = a0 / own[d * 3 + d];
+        o1[d] = a1 / own[d * 3 + d];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int64_t ro = wb + (int64_t)d * n3;
+      if (act0) u[ro + t0] = o0[d];
+      if (act1) u[ro + t1] = o1[d];
+    }
+  }
+}
+
+template <bool FWD, bool EDGE = false, bool TOP = false>
+__global__ void __launch_bounds__(256, 4)
+k_sgs_sweep_nodal_ds(DevView v, const int2* __restrict__ blk, const int64_t* __restrict__ bptr,
+                     const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff,
+                     const int32_t* __restrict__ npred, const double* __restrict__ sA,
+                     const int32_t* __restrict__ nodes, int32_t nnodes,
+                     double* __restrict__ r, const double* __restrict__ yb, double* u) {
+  // the node's own block and the blocks this sweep couples (predecessor
+  // nodes forward, successors backward) -- contiguous in the direction-
+  // sorted copy of A, records and byte map built at setup (k_sgs_node_sort)
+  // -- are staged per warp in shared memory: about half of what the
+  // unsorted sweep (k_sgs_sweep_nodal) stages and filters
+  constexpr int MAXB = 27, MAXJ = 32, AST = 10;   // the nodal plan's limits (k_nodal_check)
+  __shared__ __align__(16) double s_a[8][MAXB * AST];
+  __shared__ int2 s_b[8][MAXB];
+  __shared__ __align__(16) uint8_t s_pm[8][MAXB * MAXJ];
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = FWD ? st->pend : 0;
+  const double ap = st->alpha_pend;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int t0 = lane, t1 = lane + 32;
+  const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
+  for (int64_t w = gw; w < nnodes; w += nw) {
+    const int64_t n = nodes[w];
+    const int64_t r3 = 3 * n;
+    const int64_t wb = v.wptr[r3];
+    const int n3 = (int)(v.wptr[r3 + 1] - wb);
+    const int nJ = n3 / 3;
+    const bool act0 = t0 < n3, act1 = t1 < n3;
+    const bool any1 = n3 > 32;                         // warp-uniform
+    const int64_t bb = bptr[n];
+    const int nb = (int)(bptr[n + 1] - bb);
+    const int np = npred[n];
+    // the node's blocks are stored [own, predecessors, successors] (each
+    // group in A's column order): this sweep stages the own block and its
+    // coupled group only, cnt blocks, coupled ones from sorted index lo
+    const int lo = FWD ? 1 : 1 + np;
+    const int cnt = FWD ? 1 + np : nb - np;
+    const uint8_t* pm = pm8 + pmoff[n];
+    double acc0[3], acc1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int64_t ro = wb + (int64_t)d * n3;
+      double x0 = 0.0, x1 = 0.0;
+      if (FWD) {
+        if (act0) { x0 = r[ro + t0]; if (pend) { x0 = x0 - ap * yb[ro + t0]; r[ro + t0] = x0; } }
+        if (act1) { x1 = r[ro + t1]; if (pend) { x1 = x1 - ap * yb[ro + t1]; r[ro + t1] = x1; } }
+      } else {
+        const double dd = v.d[r3 + d];
+        if (act0) x0 = dd * u[ro + t0];                    // v = D u
+        if (act1) x1 = dd * u[ro + t1];
+      }
+      acc0[d] = x0;
+      acc1[d] = x1;
+    }
+    double own[9];
+    {
+    __syncwarp();
+    const double* a0 = sA + 9 * bb;                       // own block
+    const double* a1 = sA + 9 * (bb + lo - 1);            // (k >= 9: coupled blocks)
+    for (int k = lane; k < 9 * cnt; k += 32) {
+      const int j = k / 9, t = k - 9 * j;
+      s_a[wib][j * AST + t] = __ldg((k < 9 ? a0 : a1) + k);
+    }
+    for (int j = lane; j < cnt; j += 32) s_b[wib][j] = __ldg(blk + bb + (j == 0 ? 0 : lo + j - 1));
+    for (int k = lane; k < nJ; k += 32) s_pm[wib][k] = pm[k];
+    for (int k = lane; k < (cnt - 1) * nJ; k += 32) s_pm[wib][nJ + k] = pm[lo * nJ + k];
+    __syncwarp();
+    {
+      const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][0]);
+      const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+      own[0] = a01.x; own[1] = a01.y; own[2] = a23.x; own[3] = a23.y; own[4] = a45.x;
+      own[5] = a45.y; own[6] = a67.x; own[7] = a67.y; own[8] = a8.x;
+    }
+    // coupled blocks 1 .. cnt-1 in ascending order (cnt <= 27)
+    unsigned cm = EDGE ? 0u : (((cnt >= 32) ? 0xffffffffu : ((1u << cnt) - 1u)) & ~1u);
+    // two coupled blocks per round: all their gathers are issued before the
+    // FMAs, which run in ascending block order (the order of the plain loop)
+    while (cm) {
+      const int bA = __ffs(cm) - 1;
+      cm &= cm - 1u;
+      const int bB = cm ? __ffs(cm) - 1 : -1;
+      if (cm) cm &= cm - 1u;
+      double yA0[3], yA1[3], yB0[3], yB1[3];
+      bool mA0, mA1, mB0 = false, mB1 = false;
+      {
+        const int2 k = s_b[wib][bA];
+        const int p0 = act0 ? s_pm[wib][bA * nJ + s0] : 0xFF;
+        const int p1 = (any1 && act1) ? s_pm[wib][bA * nJ + s1] : 0xFF;
+        mA0 = p0 != 0xFF;
+        mA1 = p1 != 0xFF;
+        const int64_t i0 = (int64_t)k.x + 3 * (mA0 ? p0 : 0) + b0, i1 = (int64_t)k.x + 3 * (mA1 ? p1 : 0) + b1;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          yA0[e] = mA0 ? u[i0 + e * k.y] : 0.0;
+          yA1[e] = mA1 ? u[i1 + e * k.y] : 0.0;
+        }
+      }
+      if (bB >= 0) {
+        const int2 k = s_b[wib][bB];
+        const int p0 = act0 ? s_pm[wib][bB * nJ + s0] : 0xFF;
+        const int p1 = (any1 && act1) ? s_pm[wib][bB * nJ + s1] : 0xFF;
+        mB0 = p0 != 0xFF;
+        mB1 = p1 != 0xFF;
+        const int64_t i0 = (int64_t)k.x + 3 * (mB0 ? p0 : 0) + b0, i1 = (int64_t)k.x + 3 * (mB1 ? p1 : 0) + b1;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          yB0[e] = mB0 ? u[i0 + e * k.y] : 0.0;
+          yB1[e] = mB1 ? u[i1 + e * k.y] : 0.0;
+        }
+      }
+      {
+        const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][bA * AST]);
+        const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+        const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+        if (mA0) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc0[d] -= a[d * 3 + 0] * yA0[0];
+            acc0[d] -= a[d * 3 + 1] * yA0[1];
+            acc0[d] -= a[d * 3 + 2] * yA0[2];
+          }
+        }
+        if (mA1) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] -= a[d * 3 + 0] * yA1[0];
+            acc1[d] -= a[d * 3 + 1] * yA1[1];
+            acc1[d] -= a[d * 3 + 2] * yA1[2];
+          }
+        }
+      }
+      if (bB >= 0) {
+        const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][bB * AST]);
+        const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
+        const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
+        if (mB0) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc0[d] -= a[d * 3 + 0] * yB0[0];
+            acc0[d] -= a[d * 3 + 1] * yB0[1];
+            acc0[d] -= a[d * 3 + 2] * yB0[2];
+          }
+        }
+        if (mB1) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            acc1[d] -= a[d * 3 + 0] * yB1[0];
+            acc1[d] -= a[d * 3 + 1] * yB1[1];
+            acc1[d] -= a[d * 3 + 2] * yB1[2];
+          }
+        }
+      }
+    }
+    }
     double o0[3], o1[3];
     if (FWD) {
 #pragma unroll
@@ -757,6 +1010,28 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
       EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->bdir, std::max<int64_t>(c->nnzAFF / 9, 1), s));
       k_sgs_node_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->key, p->bdir);
       c->launches += 1;
+      if (p->max_nb <= 27 && !(c->opts.debug_flags & EMIN_DBG_AB1)) {
+        const int64_t nblk = c->nnzAFF / 9;
+        int64_t npm = 0;
+        EMIN_CUDA_TRY(c, cudaMemcpyAsync(&npm, p->pmoff + p->nFn, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+        EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->sA, sizeof(double) * 9 * std::max<int64_t>(nblk, 1), s));
+        EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->sblk, sizeof(int2) * std::max<int64_t>(nblk, 1), s));
+        EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->spm, std::max<int64_t>(npm, 16), s));
+        EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->npred, sizeof(int32_t) * std::max<int64_t>(p->nFn, 1), s));
+        int32_t hbad = 0;
+        EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+        k_sgs_node_sort<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->bdir, p->nblk, p->pm8, p->pmoff, p->sA,
+                                               p->sblk, p->spm, p->npred, flag);
+        c->launches += 1;
+        EMIN_CUDA_TRY(c, cudaMemcpyAsync(&hbad, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
+        if (hbad) {                                   // (no own block: keep the unsorted sweeps)
+          void* q[] = {p->sA, p->sblk, p->spm, p->npred};
+          for (void* x : q) cudaFreeAsync(x, s);
+          p->sA = nullptr; p->sblk = nullptr; p->spm = nullptr; p->npred = nullptr;
+        }
+      }
     }
   }
   // relaxation passes until no level changes (<= longest chain + 1)
@@ -862,18 +1137,28 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
       const bool first = L == 0, top = L == p->nlev - 1;
 #define NDF(E, T, W) k_sgs_sweep_nodal<true, E, T, W><<<sweep_grid(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, \
                                                                      p->pmoff, p->bdir, rows, (int32_t)n, c->r, c->yb, p->u)
+#define NDS(E, T) k_sgs_sweep_nodal_ds<true, E, T><<<sweep_grid(n), 256, 0, s>>>(v, p->sblk, p->bptr, p->spm, \
+                                                     p->pmoff, p->npred, p->sA, rows, (int32_t)n, c->r, c->yb, p->u)
       if (p->max_nb > 27) {
         if (first && top) NDF(true, true, true); else if (first) NDF(true, false, true);
         else if (top) NDF(false, true, true); else NDF(false, false, true);
+      } else if (p->sA) {
+        if (first && top) NDS(true, true); else if (first) NDS(true, false);
+        else if (top) NDS(false, true); else NDS(false, false);
       } else {
         if (first && top) NDF(true, true, false); else if (first) NDF(true, false, false);
         else if (top) NDF(false, true, false); else NDF(false, false, false);
       }
 #undef NDF
+#undef NDS
     }
     for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
-      if (p->max_nb > 27)
+      if (p->sA)
+        k_sgs_sweep_nodal_ds<false><<<sweep_grid(n), 256, 0, s>>>(v, p->sblk, p->bptr, p->spm, p->pmoff, p->npred,
+                                                                p->sA, p->lvl_rows + p->lvl_ptr[L], (int32_t)n,
+                                                                c->r, c->yb, p->u);
+      else if (p->max_nb > 27)
         k_sgs_sweep_nodal<false, false, false, true><<<sweep_grid(n), 256, 0, s>>>(
             v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
       else
@@ -940,7 +1225,8 @@ void emin_sgs_stage2(emin_ctx c, cudaStream_t s) {
 void emin_sgs_free(emin_ctx c) {
   SgsPlan* p = c->sgs;
   if (!p) return;
-  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u, p->dir, p->win, p->bdir};
+  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u, p->dir, p->win, p->bdir,
+                  p->sA, p->sblk, p->spm, p->npred};
   for (void* q : ptrs)
     if (q) cudaFreeAsync(q, c->stream);
   delete p;

@@ -599,3 +599,24 @@ def test_repeat_runs_bitwise_identical(name, size):
     for r in res[1:]:
         assert r[0] == res[0][0] and np.array_equal(r[1], res[0][1])
         assert np.array_equal(r[2], res[0][2]) and r[3] == res[0][3]
+
+
+@pytest.mark.parametrize("name,size,k", [("4", 4, 12), ("4", 5, 8), ("5", 8, 6)])
+def test_sgs_sorted_nodal_sweeps_equal_unsorted(name, size, k):
+    """The nodal SGS sweeps on the direction-sorted block copy (own,
+    predecessors, successors; k_sgs_sweep_nodal_ds) equal the sweeps over the
+    unsorted blocks with a direction filter (EMIN_DBG_AB1) bitwise: same
+    blocks, same order of the sums."""
+    import torch
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config, sgs_key
+    prob = make_config(name, size=size)
+    key = torch.from_numpy(np.ascontiguousarray(sgs_key(prob, "color"))).cuda()
+    res = []
+    for dbg in (0, 64):
+        g = Emin.from_problem(prob, precond="sgs", sgs_key=key, debug_flags=dbg)
+        assert g.report()["kernel_path"] == 2
+        kd, dE = g.iterate(k)
+        res.append((kd, dE, g.get_P(), g.energy()))
+    a, b = res
+    assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3]
