@@ -81,8 +81,10 @@ typedef struct {
                                    EMIN_PREC_SGS: projected symmetric Gauss-Seidel
                                    M_2^-1 = Z^T (L+D)^-T D (L+D)^-1 Z, applied
                                    matrix-free as a forward and a backward sweep over the F rows
-                                    and always followed by Pi_B.  SGS needs one GPU
-                                   (nccl_comm = NULL), else EMIN_ERR_ARG. */
+                                    and always followed by Pi_B.  On several ranks
+                                   every rank sweeps all global dependency levels and the halo
+                                   rows' values are exchanged after each level (the order is
+                                   global: (sgs_key, global row)). */
   const int64_t* sgs_key;       /* nullable, [m] per owned row: SGS visits the unknowns of each
                                    K block (coarse column) in ascending (key, global
                                    row) order (reading A23); NULL = natural row order.  Host or

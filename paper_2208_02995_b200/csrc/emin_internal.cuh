@@ -305,7 +305,7 @@ void emin_maxvol_start(emin_ctx c, const double* Bc, const double* B, const int6
 
 // projected SGS preconditioner (sgs.cu)
 emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* frow, cudaStream_t s);
-int emin_sgs_enqueue(emin_ctx c, cudaStream_t s);
+emin_status emin_sgs_enqueue(emin_ctx c, cudaStream_t s, int* grid);
 void emin_sgs_stage2(emin_ctx c, cudaStream_t s);
 void emin_sgs_free(emin_ctx c);
 int64_t emin_sgs_levels(emin_ctx c);

@@ -653,8 +653,12 @@ static emin_status enqueue_iteration(emin_ctx c, cudaStream_t s, cudaEvent_t* ev
   emin_status st = EMIN_OK;
   rec(0);
   int g1 = c->grid_rows;
-  if (c->sgs) g1 = emin_sgs_enqueue(c, s);   // z = Pi M_2^-1 r, partial r.z
-  else launch_stage(c, 1, s);
+  if (c->sgs) {                              // z = Pi M_2^-1 r, partial r.z
+    st = emin_sgs_enqueue(c, s, &g1);
+    if (st != EMIN_OK) return st;
+  } else {
+    launch_stage(c, 1, s);
+  }
   rec(1);
   if (c->fuse != 1) {
     st = global_sum(c, g1, 0, s, &red, fused_local);

@@ -671,8 +671,6 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
     return fail(ctx, EMIN_ERR_ARG, "precond must be EMIN_PREC_JACOBI or EMIN_PREC_SGS");
   if (opts->start != EMIN_START_GIVEN && opts->start != EMIN_START_MAXVOL)
     return fail(ctx, EMIN_ERR_ARG, "start must be EMIN_START_GIVEN or EMIN_START_MAXVOL");
-  if (opts->precond == EMIN_PREC_SGS && (opts->nccl_comm || opts->loopback))
-    return fail(ctx, EMIN_ERR_ARG, "the SGS preconditioner runs on one GPU (nccl_comm / loopback must be NULL)");
   if (opts->nccl_comm && opts->loopback)
     return fail(ctx, EMIN_ERR_ARG, "nccl_comm and loopback are mutually exclusive");
 

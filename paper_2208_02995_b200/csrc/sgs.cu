@@ -29,9 +29,11 @@
 #include <vector>
 
 #include "emin_internal.cuh"
+#include "dist.cuh"
 
 struct SgsPlan {
-  int64_t* key = nullptr;        // [nF] ordering key of each F row
+  int64_t* key = nullptr;        // [nFh] ordering key of each F row (owned, then halo rows)
+  int64_t* gid = nullptr;        // [nFh] global F id (the tie-break of the order)
   int32_t* lev = nullptr;        // [nF] dependency level
   int32_t* lvl_rows = nullptr;   // [nF] F rows bucketed by level
   int32_t* lvl_cnt = nullptr;    // [nlev + 1] scratch
@@ -64,32 +66,68 @@ namespace {
 
 constexpr int SGS_MAXC = EMIN_MAX_ROW / 32;   // pattern chunks of 32 lanes
 
-__device__ __forceinline__ bool sgs_before(const int64_t* __restrict__ key, int32_t k, int32_t i) {
+// (key, global F id) order; key and gid cover the owned and the halo rows
+// (local ids >= nF, multi-GPU), the global F id = the global row order
+__device__ __forceinline__ bool sgs_before(const int64_t* __restrict__ key, const int64_t* __restrict__ gid,
+                                           int32_t k, int32_t i) {
   const int64_t a = key[k], b = key[i];
-  return a != b ? a < b : k < i;     // F index order = global row order
+  return a != b ? a < b : gid[k] < gid[i];
 }
 
-__global__ void k_sgs_key(int64_t nF, const int64_t* __restrict__ frow, const int64_t* __restrict__ key_own,
-                          int64_t* __restrict__ key) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+__global__ void k_sgs_key(int64_t nF, int64_t fbegin, const int64_t* __restrict__ frow,
+                          const int64_t* __restrict__ key_own, int64_t* __restrict__ key, int64_t* __restrict__ gid) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x) {
     key[i] = key_own ? key_own[frow[i]] : 0;
+    gid[i] = fbegin + i;
+  }
+}
+
+// per-unit values (rows, or nodes: stride 3) of the halo units from their
+// owners, through the W-layout halo exchange: every W entry of an owned
+// unit's first row carries the value's bits, the halo tail brings them back
+// (every F row has >= 1 entry)
+__global__ void k_sgs_units_to_w(const int64_t* __restrict__ wptr, int64_t nu, int stride,
+                                 const int64_t* __restrict__ val64, const int32_t* __restrict__ val32,
+                                 double* __restrict__ w) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = val64 ? val64[u] : (int64_t)val32[u];
+    const double bits = __longlong_as_double(x);
+    for (int64_t e = wptr[stride * u]; e < wptr[stride * u + 1]; ++e) w[e] = bits;
+  }
+}
+__global__ void k_sgs_w_to_units(const int64_t* __restrict__ wptr, int64_t u0, int64_t u1, int stride,
+                                 const double* __restrict__ w, int64_t* __restrict__ val64,
+                                 int32_t* __restrict__ val32) {
+  for (int64_t u = u0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < u1; u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = __double_as_longlong(w[wptr[stride * u]]);
+    if (val64) val64[u] = x; else val32[u] = (int32_t)x;
+  }
 }
 
 // one relaxation pass of lev(i) = max over predecessors k of lev(k) + 1
 // (in place: a pass propagates along every chain the grid happens to visit
 // in order; repeated until no level changes)
-__global__ void k_sgs_levels(DevView v, const int64_t* __restrict__ key, int32_t* lev, int32_t* changed) {
+__global__ void k_sgs_levels(DevView v, const int64_t* __restrict__ key, const int64_t* __restrict__ gid, int32_t* lev,
+                             int32_t* changed) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v.nF; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t m = 0;
     for (int64_t q = v.affptr[i]; q < v.affptr[i + 1]; ++q) {
       const int32_t k = v.affcol[q];
-      if (k != (int32_t)i && sgs_before(key, k, (int32_t)i)) m = max(m, ((volatile int32_t*)lev)[k] + 1);
+      if (k != (int32_t)i && sgs_before(key, gid, k, (int32_t)i)) m = max(m, ((volatile int32_t*)lev)[k] + 1);
     }
     if (m > lev[i]) {
       lev[i] = m;
       *changed = 1;
     }
   }
+}
+
+__global__ void k_sgs_maxlev(int64_t n, const int32_t* __restrict__ lev, int32_t* maxlev) {
+  int32_t mx = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, lev[i]);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxlev, mx);
 }
 
 // level histogram / bucketing with warp-aggregated atomics (few levels =>
@@ -174,8 +212,9 @@ __global__ void k_sgs_scatter(int64_t nF, const int32_t* __restrict__ lev, int32
 // and the record loop is skipped (u = x / d, z = v / d)
 template <bool FWD, bool EDGE = false, bool TOP = false>
 __global__ void __launch_bounds__(256)
-k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restrict__ rows, int32_t nrows,
-            double* __restrict__ r, const double* __restrict__ yb, double* u) {
+k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int64_t* __restrict__ gid,
+            const int32_t* __restrict__ rows, int32_t nrows, double* __restrict__ r, const double* __restrict__ yb,
+            double* u) {
   const DevState* st = v.st;
   if (st->stopped) return;
   const int pend = FWD ? st->pend : 0;
@@ -208,7 +247,7 @@ k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restric
     for (int64_t q = v.affptr[i]; !EDGE && q < v.affptr[i + 1]; ++q) {
       const int32_t k = v.affcol[q];
       if (k == i) continue;
-      if (FWD != sgs_before(key, k, i)) continue;   // FWD: predecessors, else successors
+      if (FWD != sgs_before(key, gid, k, i)) continue;   // FWD: predecessors, else successors
       const double a = v.affval[q];
       const int64_t kb = v.wptr[k];
       const int nk = (int)(v.wptr[k + 1] - kb);
@@ -234,7 +273,8 @@ k_sgs_sweep(DevView v, const int64_t* __restrict__ key, const int32_t* __restric
 
 // record directions for the windowed sweeps: the scalar path stores row i's
 // records diagonal first, then A's column order (k_plan_entries)
-__global__ void k_sgs_dir(DevView v, const int64_t* __restrict__ key, uint8_t* __restrict__ dir) {
+__global__ void k_sgs_dir(DevView v, const int64_t* __restrict__ key, const int64_t* __restrict__ gid,
+                          uint8_t* __restrict__ dir) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v.nF; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
     int64_t qd = qb;
@@ -243,7 +283,7 @@ __global__ void k_sgs_dir(DevView v, const int64_t* __restrict__ key, uint8_t* _
     for (int64_t q = qb; q < qe; ++q) {
       const int64_t dst = (q == qd) ? qb : (q < qd ? q + 1 : q);
       const int32_t k = v.affcol[q];
-      dir[dst] = (k == (int32_t)i) ? 0 : (sgs_before(key, k, (int32_t)i) ? 1 : 2);
+      dir[dst] = (k == (int32_t)i) ? 0 : (sgs_before(key, gid, k, (int32_t)i) ? 1 : 2);
     }
   }
 }
@@ -318,20 +358,22 @@ __global__ void k_sgs_node_key_ok(int64_t nFn, const int64_t* __restrict__ key, 
     if (key[3 * n + 1] != key[3 * n] || key[3 * n + 2] != key[3 * n]) atomicExch(bad, 1);
 }
 
-__device__ __forceinline__ bool sgs_node_before(const int64_t* __restrict__ key, int64_t K, int64_t I) {
+__device__ __forceinline__ bool sgs_node_before(const int64_t* __restrict__ key, const int64_t* __restrict__ gid,
+                                                int64_t K, int64_t I) {
   const int64_t a = key[3 * K], b = key[3 * I];
-  return a != b ? a < b : K < I;
+  return a != b ? a < b : gid[3 * K] < gid[3 * I];
 }
 
 __global__ void k_sgs_node_dir(DevView v, int64_t nFn, const int64_t* __restrict__ bptr,
-                               const int64_t* __restrict__ key, uint8_t* __restrict__ bdir) {
+                               const int64_t* __restrict__ key, const int64_t* __restrict__ gid,
+                               uint8_t* __restrict__ bdir) {
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < nFn; n += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ab = v.affptr[3 * n];
     const int64_t bb = bptr[n];
     const int nb = (int)(bptr[n + 1] - bb);
     for (int b = 0; b < nb; ++b) {
       const int64_t K = v.affcol[ab + 3 * b] / 3;
-      bdir[bb + b] = (K == n) ? 0 : (sgs_node_before(key, K, n) ? 1 : 2);
+      bdir[bb + b] = (K == n) ? 0 : (sgs_node_before(key, gid, K, n) ? 1 : 2);
     }
   }
 }
@@ -973,27 +1015,55 @@ k_sgs_stage2(DevView v, const double* __restrict__ z, double* __restrict__ y, do
 }  // namespace
 
 // ---------------------------------------------------------------- host side
+// per-unit values of the halo units (multi-GPU): see k_sgs_units_to_w
+static emin_status sgs_halo_units(emin_ctx c, int stride, int64_t* v64, int32_t* v32, double* tmpw, cudaStream_t s) {
+  const int SM = emin_num_sms();
+  const int64_t nu = c->nF / stride, nuh = c->nFh / stride;
+  k_sgs_units_to_w<<<SM * 4, 256, 0, s>>>(c->wptr, nu, stride, v64, v32, tmpw);
+  c->launches += 1;
+  emin_status st = emin_dist_halo_values(c, tmpw, s);
+  if (st != EMIN_OK) return st;
+  if (nuh > nu) {
+    k_sgs_w_to_units<<<SM * 4, 256, 0, s>>>(c->wptr, nu, nuh, stride, tmpw, v64, v32);
+    c->launches += 1;
+  }
+  return EMIN_OK;
+}
+
 emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* frow, cudaStream_t s) {
   SgsPlan* p = new SgsPlan();
   c->sgs = p;
-  const int64_t nF = c->nF;
+  const int64_t nF = c->nF, nFh = c->nFh;
   const int SM = emin_num_sms();
   const int64_t* dkey = key_own;
   int64_t* tmp = nullptr;
+  double* tmpw = nullptr;                            // W-layout scratch of the halo exchanges
   if (key_own && !c->opts.inputs_on_device) {
     EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&tmp, sizeof(int64_t) * std::max<int64_t>(c->m_owned, 1), s));
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(tmp, key_own, sizeof(int64_t) * c->m_owned, cudaMemcpyHostToDevice, s));
     dkey = tmp;
   }
-  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->key, sizeof(int64_t) * std::max<int64_t>(nF, 1), s));
-  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lev, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->key, sizeof(int64_t) * std::max<int64_t>(nFh, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->gid, sizeof(int64_t) * std::max<int64_t>(nFh, 1), s));
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lev, sizeof(int32_t) * std::max<int64_t>(nFh, 1), s));
   EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lvl_rows, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
-  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->u, sizeof(double) * std::max<int64_t>(c->nnzW, 1) + 64, s));
+  // u carries the halo tail: the sweeps read the halo rows' u / z
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->u, sizeof(double) * std::max<int64_t>(c->nnzWh, 1) + 64, s));
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->u, 0, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s));
   int32_t* flag;
   EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&flag, sizeof(int32_t) * 2, s));
-  k_sgs_key<<<SM * 4, 256, 0, s>>>(nF, frow, dkey, p->key);
-  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lev, 0, sizeof(int32_t) * std::max<int64_t>(nF, 1), s));
+  const int64_t fbegin = c->dist ? c->dist->fbeg[c->rank] : 0;
+  k_sgs_key<<<SM * 4, 256, 0, s>>>(nF, fbegin, frow, dkey, p->key, p->gid);
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lev, 0, sizeof(int32_t) * std::max<int64_t>(nFh, 1), s));
   c->launches += 1;
+  if (c->dist) {
+    // the halo rows' keys and global ids from their owners (the sweeps
+    // order the coupled rows across the partition exactly as on one GPU)
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&tmpw, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s));
+    emin_status st = sgs_halo_units(c, 1, p->key, nullptr, tmpw, s);
+    if (st == EMIN_OK) st = sgs_halo_units(c, 1, p->gid, nullptr, tmpw, s);
+    if (st != EMIN_OK) return st;
+  }
   // nodal path with node-constant keys: levels, buckets and sweeps per F node
   int64_t nunits = nF;                               // rows, or nodes on the nodal path
   if (!(c->opts.debug_flags & EMIN_DBG_SGS_GENERIC) &&
@@ -1001,14 +1071,18 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
     int32_t hb = 0;
     EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
     k_sgs_node_key_ok<<<SM * 4, 256, 0, s>>>(p->nFn, p->key, flag);
+    c->launches += 1;
+    if (c->dist) {                                   // every rank takes the same path
+      emin_status st = emin_dist_allreduce_max_i32(c, flag, s);
+      if (st != EMIN_OK) return st;
+    }
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(&hb, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
-    c->launches += 1;
     if (!hb) {
       p->nodal = 1;
       nunits = p->nFn;
       EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->bdir, std::max<int64_t>(c->nnzAFF / 9, 1), s));
-      k_sgs_node_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->key, p->bdir);
+      k_sgs_node_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->key, p->gid, p->bdir);
       c->launches += 1;
       if (p->max_nb <= 27 && !(c->opts.debug_flags & EMIN_DBG_AB1)) {
         const int64_t nblk = c->nnzAFF / 9;
@@ -1034,29 +1108,43 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
       }
     }
   }
-  // relaxation passes until no level changes (<= longest chain + 1)
-  for (int64_t pass = 0; pass <= nunits; ++pass) {
+  // relaxation passes until no level changes (<= longest chain + 1); on
+  // several GPUs the halo units' levels are refreshed from their owners
+  // after every pass and the pass repeats until no rank changed a level
+  for (int64_t pass = 0; pass <= (c->dist ? c->n_global : nunits); ++pass) {
     int32_t h = 0;
     EMIN_CUDA_TRY(c, cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
     if (p->nodal)
       k_sgs_node_levels<<<SM * 8, 256, 0, s>>>(c->view(), p->nFn, p->bptr, p->bdir, p->lev, flag);
     else
-      k_sgs_levels<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->lev, flag);
+      k_sgs_levels<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->gid, p->lev, flag);
     c->launches += 1;
+    if (c->dist) {
+      emin_status st = sgs_halo_units(c, p->nodal ? 3 : 1, nullptr, p->lev, tmpw, s);
+      if (st == EMIN_OK) st = emin_dist_allreduce_max_i32(c, flag, s);
+      if (st != EMIN_OK) return st;
+    }
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(&h, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
     if (!h) break;
   }
+  if (tmpw) cudaFreeAsync(tmpw, s);
   // bucket the rows by level
   int32_t hmax = 0;
   EMIN_CUDA_TRY(c, cudaMemsetAsync(flag + 1, 0, sizeof(int32_t), s));
-  // count into a buffer of nF + 1 (levels <= nF - 1)
-  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lvl_cnt, sizeof(int32_t) * (nunits + 2), s));
-  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lvl_cnt, 0, sizeof(int32_t) * (nunits + 2), s));
-  k_sgs_count<<<SM * 4, 256, 0, s>>>(nunits, p->lev, p->lvl_cnt, flag + 1);
+  // the highest level (over all ranks: every rank sweeps all global levels)
+  k_sgs_maxlev<<<SM * 4, 256, 0, s>>>(nunits, p->lev, flag + 1);
+  c->launches += 1;
+  if (c->dist) {
+    emin_status st = emin_dist_allreduce_max_i32(c, flag + 1, s);
+    if (st != EMIN_OK) return st;
+  }
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(&hmax, flag + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));
-  p->nlev = nunits > 0 ? (int64_t)hmax + 1 : 0;
+  p->nlev = (nunits > 0 || c->dist) ? (int64_t)hmax + 1 : 0;
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->lvl_cnt, sizeof(int32_t) * (p->nlev + 2), s));
+  EMIN_CUDA_TRY(c, cudaMemsetAsync(p->lvl_cnt, 0, sizeof(int32_t) * (p->nlev + 2), s));
+  k_sgs_count<<<SM * 4, 256, 0, s>>>(nunits, p->lev, p->lvl_cnt, flag + 1);
   std::vector<int32_t> hc((size_t)p->nlev + 1, 0);
   if (p->nlev)
     EMIN_CUDA_TRY(c, cudaMemcpyAsync(hc.data(), p->lvl_cnt, sizeof(int32_t) * p->nlev, cudaMemcpyDeviceToHost, s));
@@ -1100,7 +1188,7 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
     k_sgs_wfirst<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, p->lev, lptr, base, wbase, pst, p->win, S);
     k_sgs_wfill<<<SM * 8, 256, 0, s>>>(nF, p->lvl_rows, p->lev, base, wbase, pst, len, p->win, S);
     EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&p->dir, std::max<int64_t>(c->nnzAFF, 1), s));
-    k_sgs_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->dir);
+    k_sgs_dir<<<SM * 8, 256, 0, s>>>(c->view(), p->key, p->gid, p->dir);
     c->launches += 6;
     void* fr[] = {len, pst, lptr, base, wbase, tot2, scr};
     for (void* q : fr) cudaFreeAsync(q, s);
@@ -1116,10 +1204,15 @@ emin_status emin_sgs_plan(emin_ctx c, const int64_t* key_own, const int64_t* fro
 
 int64_t emin_sgs_levels(emin_ctx c) { return c->sgs ? c->sgs->nlev : 0; }
 
-// z = Pi M_SGS^{-1} r and the partial sums of r.z (in c->partials); returns
-// the grid of the projection kernel (= number of partials)
-int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
+// z = Pi M_SGS^{-1} r and the partial sums of r.z (in c->partials); *grid =
+// the grid of the projection kernel (= number of partials).  On several
+// GPUs the halo rows' u (forward) / z (backward) are refreshed from their
+// owners after every level (the sweep is matrix-free like the
+// masked product, so it exchanges only values, never the pattern); every
+// rank runs all global levels, so the exchanges pair up.
+emin_status emin_sgs_enqueue(emin_ctx c, cudaStream_t s, int* grid) {
   SgsPlan* p = c->sgs;
+  auto halo = [&]() -> emin_status { return c->dist ? emin_dist_halo_values(c, p->u, s) : EMIN_OK; };
   const DevView v = c->view();
   const int SM = emin_num_sms();
   auto grid_for = [&](int64_t n) {
@@ -1151,6 +1244,8 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
       }
 #undef NDF
 #undef NDS
+      const emin_status hs = halo();
+      if (hs != EMIN_OK) return hs;
     }
     for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
@@ -1164,6 +1259,10 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
       else
         k_sgs_sweep_nodal<false><<<sweep_grid(n), 256, 0, s>>>(v, p->nblk, p->bptr, p->pm8, p->pmoff, p->bdir,
                                                             p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r, c->yb, p->u);
+      if (L > 0) {
+        const emin_status hs = halo();
+        if (hs != EMIN_OK) return hs;
+      }
     }
     const int g = grid_for(p->nFn);
     switch (c->nv) {
@@ -1171,7 +1270,8 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
       PN(1) PN(2) PN(3) PN(4) PN(5) PN(6) PN(7) PN(8)
 #undef PN
     }
-    return g;
+    *grid = g;
+    return EMIN_OK;
   }
   if (p->rec) {
     for (int64_t L = 0; L < p->nlev; ++L) {
@@ -1182,26 +1282,39 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
       if (first && top) WF(true, true); else if (first) WF(true, false); else if (top) WF(false, true);
       else WF(false, false);
 #undef WF
+      const emin_status hs = halo();
+      if (hs != EMIN_OK) return hs;
     }
     for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->win_ptr[L + 1] - p->win_ptr[L];
       k_sgs_sweep_win<false><<<grid_for(n), 256, 0, s>>>(v, p->rec, p->dir, p->win + p->win_ptr[L], (int32_t)n,
                                                         p->lvl_rows, c->r, c->yb, p->u);
+      if (L > 0) {
+        const emin_status hs = halo();
+        if (hs != EMIN_OK) return hs;
+      }
     }
   } else {
     for (int64_t L = 0; L < p->nlev; ++L) {
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
       const int32_t* rows = p->lvl_rows + p->lvl_ptr[L];
       const bool first = L == 0, top = L == p->nlev - 1;
-#define GF(E, T) k_sgs_sweep<true, E, T><<<grid_for(n), 256, 0, s>>>(v, p->key, rows, (int32_t)n, c->r, c->yb, p->u)
+#define GF(E, T) k_sgs_sweep<true, E, T><<<grid_for(n), 256, 0, s>>>(v, p->key, p->gid, rows, (int32_t)n, c->r, \
+                                                                   c->yb, p->u)
       if (first && top) GF(true, true); else if (first) GF(true, false); else if (top) GF(false, true);
       else GF(false, false);
 #undef GF
+      const emin_status hs = halo();
+      if (hs != EMIN_OK) return hs;
     }
     for (int64_t L = p->nlev - 2; L >= 0; --L) {     // the top level was solved by the forward launch
       const int64_t n = p->lvl_ptr[L + 1] - p->lvl_ptr[L];
-      k_sgs_sweep<false><<<grid_for(n), 256, 0, s>>>(v, p->key, p->lvl_rows + p->lvl_ptr[L], (int32_t)n, c->r,
-                                                    c->yb, p->u);
+      k_sgs_sweep<false><<<grid_for(n), 256, 0, s>>>(v, p->key, p->gid, p->lvl_rows + p->lvl_ptr[L], (int32_t)n,
+                                                    c->r, c->yb, p->u);
+      if (L > 0) {
+        const emin_status hs = halo();
+        if (hs != EMIN_OK) return hs;
+      }
     }
   }
   int64_t nwin = 0;
@@ -1209,11 +1322,13 @@ int emin_sgs_enqueue(emin_ctx c, cudaStream_t s) {
   if (rowstart && p->rec) {
     const int g = grid_for(nwin);
     k_sgs_project_win<<<g, 256, 0, s>>>(v, rowstart, nwin, c->r, p->u, c->partials);
-    return g;
+    *grid = g;
+    return EMIN_OK;
   }
   const int g = grid_for(c->nF);
   k_sgs_project<<<g, 256, 0, s>>>(v, c->r, p->u, c->partials);
-  return g;
+  *grid = g;
+  return EMIN_OK;
 }
 
 void emin_sgs_stage2(emin_ctx c, cudaStream_t s) {
@@ -1225,7 +1340,7 @@ void emin_sgs_stage2(emin_ctx c, cudaStream_t s) {
 void emin_sgs_free(emin_ctx c) {
   SgsPlan* p = c->sgs;
   if (!p) return;
-  void* ptrs[] = {p->key, p->lev, p->lvl_rows, p->lvl_cnt, p->u, p->dir, p->win, p->bdir,
+  void* ptrs[] = {p->key, p->gid, p->lev, p->lvl_rows, p->lvl_cnt, p->u, p->dir, p->win, p->bdir,
                   p->sA, p->sblk, p->spm, p->npred};
   for (void* q : ptrs)
     if (q) cudaFreeAsync(q, c->stream);

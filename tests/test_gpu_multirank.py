@@ -33,9 +33,10 @@ def _gpu():
     build()
 
 
-def run_ranks(prob, R, k, ranges=None, chunks=None, **kw):
+def run_ranks(prob, R, k, ranges=None, chunks=None, sgs_key_global=None, **kw):
     """R loopback ranks, one thread each: setup, report, iterate(k), energy,
-    get_P, layout.  Returns the per-rank results (rank order)."""
+    get_P, layout.  Returns the per-rank results (rank order).  With
+    sgs_key_global every rank passes its owned rows' slice of the key."""
     import torch
     from paper_2208_02995_b200 import emin as E
     from paper_2208_02995_b200.partition import partition_rows, plane_rows, rank_slice
@@ -52,10 +53,16 @@ def run_ranks(prob, R, k, ranges=None, chunks=None, **kw):
             stream = torch.cuda.Stream()
             rb, re_ = ranges[r]
             a = rank_slice(prob, rb, re_)
+            if sgs_key_global is not None:
+                kw_r = dict(kw, sgs_key=np.ascontiguousarray(sgs_key_global[rb:re_]))
+                if hasattr(a["A_val"], "is_cuda"):
+                    kw_r["sgs_key"] = torch.from_numpy(kw_r["sgs_key"]).cuda()
+            else:
+                kw_r = kw
             h = E.emin_setup(prob.n, prob.nc, a["A_rowptr"], a["A_col"], a["A_val"], a["is_coarse"],
                              a["P_rowptr"], a["P_col"], a["P_val"], prob.nv, a["B"], a["Bc"],
                              block_size=prob.block_size, stream=stream.cuda_stream, row_begin=rb,
-                             row_end=re_, loopback=lb, loopback_rank=r, **kw)
+                             row_end=re_, loopback=lb, loopback_rank=r, **kw_r)
             rep0 = E.emin_report(h)
             kd, dE = 0, []
             for kk in (chunks or [k]):
@@ -160,3 +167,46 @@ def test_loopback_uneven_ranges_and_composability():
     P = np.concatenate([r["P"] for r in res])
     assert np.abs(P - P1).max() <= 1e-12 * np.abs(P1).max()
     assert abs(res[0]["E"] - one.energy()) <= 1e-13 * abs(one.energy())
+
+
+SGS_MR_CASES = [("3", 12, 20, 2, "color"), ("3", 12, 12, 3, "natural"), ("2b", 10, 20, 2, "color"),
+                ("2b", 10, 20, 3, "color"), ("4", 4, 15, 2, "color"), ("5", 8, 15, 2, "color"),
+                ("5", 8, 10, 3, "color"), ("1b", None, 12, 2, "natural"), ("4", 3, 10, 2, "natural")]
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("name,size,k,R,kind", SGS_MR_CASES)
+def test_loopback_sgs_matches_oracle(name, size, k, R, kind):
+    """Projected SGS on R ranks: every rank sweeps all global
+    levels and refreshes the halo rows' u / z after each level (P:995-1004:
+    the sweep is matrix-free like the masked product, only values move).
+    The dependency levels equal the single-GPU ones (the order is global:
+    (key, global F id)); P, E, k and dE_k match the single-process oracle to
+    the parity bars and the single-GPU context to round-off."""
+    from oracle import Oracle
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config, sgs_key
+    prob = make_config(name, size=size)
+    key = sgs_key(prob, kind)
+    res, _ = run_ranks(prob, R, k, sgs_key_global=key, precond="sgs")
+    one = Emin.from_problem(prob, precond="sgs", sgs_key=key)
+    rep1 = one.report()
+    for r in res:
+        assert r["rep"]["nranks"] == R and r["rep"]["n_halo_rows"] > 0
+        assert r["rep"]["precond"] == 1
+        assert r["rep"]["sgs_levels"] == rep1["sgs_levels"]
+        assert r["rep"]["kernel_path"] == rep1["kernel_path"]
+        assert r["kd"] == res[0]["kd"] and np.array_equal(r["dE"], res[0]["dE"])
+    k1, dE1 = one.iterate(k)
+    P1 = one.get_P()
+    o = Oracle(prob, precond="sgs", sgs_key=key)
+    kdo, dEo = o.iterate(k)
+    assert res[0]["kd"] == kdo == k1
+    assert np.allclose(res[0]["dE"], dEo, rtol=1e-8, atol=1e-12 * abs(o.E0))
+    assert np.allclose(res[0]["dE"], dE1, rtol=1e-10, atol=1e-14 * abs(o.E0))
+    Eo = o.energy()
+    assert abs(res[0]["E"] - Eo) <= E_TOL * abs(Eo)
+    P = np.concatenate([r["P"] for r in res])
+    Po = o.get_P()
+    assert np.abs(P - Po).max() <= P_TOL * np.abs(Po).max()
+    assert np.abs(P - P1).max() <= 1e-11 * np.abs(P1).max()

@@ -494,9 +494,9 @@ def test_fused_r0_energy_setup_equals_separate(name, size, dbg):
 
 
 def test_option_validation():
-    """precond / start outside their enums, and SGS with an NCCL
-    communicator, are EMIN_ERR_ARG (include/emin.h); emin_pattern rejects a
-    capacity below nnz and keeps P_rowptr."""
+    """precond / start outside their enums are EMIN_ERR_ARG (include/emin.h);
+    SGS with a (1-rank) NCCL communicator sets up and iterates; emin_pattern
+    rejects a capacity below nnz and keeps P_rowptr."""
     import ctypes as C
     from paper_2208_02995_b200 import Emin, EminError
     from paper_2208_02995_b200 import emin as E
@@ -508,9 +508,11 @@ def test_option_validation():
         assert e.value.code == 1
     comm = E.emin_nccl_comm_init(1, E.emin_nccl_unique_id(), 0)
     try:
-        with pytest.raises(EminError) as e:
-            Emin.from_problem(prob, precond="sgs", nccl_comm=comm)
-        assert e.value.code == 1
+        g = Emin.from_problem(prob, precond="sgs", nccl_comm=comm)
+        one = Emin.from_problem(prob, precond="sgs")
+        assert g.iterate(10)[0] == one.iterate(10)[0]
+        assert np.abs(g.get_P() - one.get_P()).max() <= 1e-12 * np.abs(one.get_P()).max()
+        g.close()
     finally:
         E.emin_nccl_comm_destroy(comm)
     lib = E.load_library()
