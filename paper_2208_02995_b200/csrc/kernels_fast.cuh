@@ -664,28 +664,19 @@ static inline int select_fast_path(emin_ctx c) {
   if (emin_mallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
+  int32_t* wd_ok = nullptr;      // (read back with the tile sizes below: one host sync)
   {
     // window headers + lane descriptors of k_spgemm_wd (k_spgemm_win2 if a
     // window's counts do not fit the descriptor)
     int32_t* dok = nullptr;
-    int32_t hok = 0;
     if (emin_mallocAsync((void**)&p.whdr, sizeof(int4) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess ||
         emin_mallocAsync((void**)&p.wdesc, sizeof(uint32_t) * std::max<int64_t>(c->nnzW, 1), s) != cudaSuccess ||
         emin_mallocAsync((void**)&dok, sizeof(int32_t), s) != cudaSuccess)
       return 0;
-    const int32_t one = 1;
-    cudaMemcpyAsync(dok, &one, sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(dok, 0xFF, sizeof(int32_t), s);        // nonzero: the descriptors fit
     k_plan_wdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.whdr, p.wdesc, dok);
     c->launches += 1;
-    cudaMemcpyAsync(&hok, dok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    cudaFreeAsync(dok, s);
-    if (!hok) {
-      cudaFreeAsync(p.whdr, s);
-      cudaFreeAsync(p.wdesc, s);
-      p.whdr = nullptr;
-      p.wdesc = nullptr;
-    }
+    wd_ok = dok;
   }
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
   k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), p.ent);
@@ -705,9 +696,20 @@ static inline int select_fast_path(emin_ctx c) {
   k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
   c->launches += 2;
   cudaMemcpyAsync(hmax, dmax, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
+  int32_t hok = 0;
+  if (wd_ok) cudaMemcpyAsync(&hok, wd_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(trow, s);
   cudaFreeAsync(dmax, s);
   cudaStreamSynchronize(s);
+  if (wd_ok) {
+    cudaFreeAsync(wd_ok, s);
+    if (!hok) {
+      cudaFreeAsync(p.whdr, s);
+      cudaFreeAsync(p.wdesc, s);
+      p.whdr = nullptr;
+      p.wdesc = nullptr;
+    }
+  }
   p.tile_smem = tile_smem_bytes(hmax[0]);
   if (p.tile_smem <= TILE_SMEM_CAP) {
     p.use_tiles = 1;

@@ -39,27 +39,33 @@ __device__ __forceinline__ void raise_err(const RowsArgs& a, int32_t bit, int64_
 
 // Validation + per-row counts (one thread per owned row; setup only).
 __global__ void k_rows(RowsArgs a) {
+  int32_t wmax = 0;                           // longest pattern row seen by this thread
   for (int64_t rl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rl < a.m;
        rl += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = a.row_begin + rl;
     const bool coarse = a.isc[r] != 0;
     const int64_t fl = (r - a.cidx[r]) - a.fbegin;   // local F id (valid if !coarse)
-    // ---- A row
+    // ---- A row (no early exit: the loads of a row are independent, the
+    // error bits and the first bad row are the same)
     const int64_t qb = a.Arp[rl] - a.Arp[0], qe = a.Arp[rl + 1] - a.Arp[0];
     if (qe < qb) { raise_err(a, EF_CSR, r); continue; }
     int64_t nff = 0, nfc = 0;
     double diag = 0.0;
-    bool has_diag = false;
+    bool has_diag = false, bad = false, nonfin = false;
     int32_t prev = -1;
+#pragma unroll 4
     for (int64_t q = qb; q < qe; ++q) {
       const int32_t c = a.Acol[q];
       const double v = a.Aval[q];
-      if (c < 0 || c >= a.n_global || c <= prev) { raise_err(a, EF_CSR, r); break; }
+      const bool ok = c >= 0 && c < a.n_global && c > prev;
+      bad |= !ok;
       prev = c;
-      if (!isfinite(v)) raise_err(a, EF_NONFINITE, r);
+      nonfin |= !isfinite(v);
       if (c == r) { diag = v; has_diag = true; }
-      if (a.isc[c]) ++nfc; else ++nff;
+      if (ok) { if (a.isc[c]) ++nfc; else ++nff; }
     }
+    if (bad) { raise_err(a, EF_CSR, r); continue; }
+    if (nonfin) raise_err(a, EF_NONFINITE, r);
     if (coarse) {
       a.dcc[rl] = diag;
     } else {
@@ -80,16 +86,23 @@ __global__ void k_rows(RowsArgs a) {
       if (len == 0) raise_err(a, EF_PATTERN, r);
       if (len > EMIN_MAX_ROW) raise_err(a, EF_ROWLEN, r);
       int32_t pp = -1;
+      bool pbad = false, pnf = false;
+#pragma unroll 4
       for (int64_t q = pb; q < pe; ++q) {
         const int32_t c = a.Pcol[q];
-        if (c < 0 || c >= a.nc_global || c <= pp) { raise_err(a, EF_PATTERN, r); break; }
+        pbad |= !(c >= 0 && c < a.nc_global && c > pp);
         pp = c;
-        if (a.Pval && !isfinite(a.Pval[q])) raise_err(a, EF_NONFINITE, r);
+        if (a.Pval) pnf |= !isfinite(a.Pval[q]);
       }
+      if (pbad) raise_err(a, EF_PATTERN, r);
+      if (pnf) raise_err(a, EF_NONFINITE, r);
       a.cnt_w[fl] = len;
-      atomicMax(a.max_row, (int32_t)(len < INT_MAX ? len : INT_MAX));
+      wmax = max(wmax, (int32_t)(len < INT_MAX ? len : INT_MAX));
     }
   }
+  // one atomic per warp for the longest row (not one per F row)
+  wmax = __reduce_max_sync(0xffffffffu, wmax);
+  if ((threadIdx.x & 31) == 0 && wmax > 0) atomicMax(a.max_row, wmax);
 }
 
 __global__ void k_check_B(int64_t m, int64_t row_begin, int32_t nv, const uint8_t* __restrict__ isc,
