@@ -35,7 +35,7 @@ struct TileHdr;
 struct ScalarPlan {
   SpEnt* ent = nullptr;
   int32_t* rowstart = nullptr;   // [nwin + 1]
-  int4* whdr = nullptr;          // [nwin] {first W entry, first record, entries, 0} (k_spgemm_wd)
+  int4* whdr = nullptr;          // [nwin] {first W entry, first record, entries, first row} (k_spgemm_wd)
   uint32_t* wdesc = nullptr;     // [nnzW] lane descriptor (k_spgemm_wd)
   int64_t nwin = 0;
   int32_t S = 0;
@@ -190,10 +190,15 @@ k_spgemm_win2(DevView v, const SpEnt* __restrict__ A, const int32_t* __restrict_
 // {row's first lane, row length, row's record count and first record
 // relative to the window's} -- so the per-window dependent-load chain
 // rowstart -> wptr -> affptr -> record (4 latencies, 41 % of win2's stall
-// samples, profiles/r02) becomes header -> descriptor -> record.
+// samples, profiles/r02) becomes header -> descriptor -> record.  In the
+// record loop the {ybase, pm} halves of the next LA records are loaded ahead
+// (a record's gather no longer waits for its own record load) and a(q) is
+// read at use from the line already in L1; LEAN re-reads Q and the own y
+// entry after the loop so that LA = 2 fits 32 registers.
 constexpr uint32_t WD_MAXREC = 255, WD_MAXREL = 65535;
 constexpr int WD_NT = 1024;    // threads per CTA of the per-iteration launch
-template <int NT = 256>
+constexpr int WD_LA = 2;       // records whose {ybase, pm} are in flight ahead of the current one
+template <int NT = 256, int LA = 0, bool LEAN = false>
 __global__ void __launch_bounds__(NT, 2048 / NT)
 k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whdr, const uint32_t* __restrict__ wdesc,
             int32_t nwin, const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
@@ -218,8 +223,10 @@ k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whd
     const bool act = lane < nent;
     const int e = h.x + lane;
     const uint32_t dsc = act ? __ldg(wdesc + e) : 0u;
-    const double qv = act ? v.Q[e] : 0.0;
-    const double xo = act ? X[e] : 0.0;
+    // LEAN: Q and the own y entry are (re)read after the record loop (fewer
+    // live registers in it; the y line is still in L1)
+    double qv = (!LEAN && act) ? v.Q[e] : 0.0;
+    double xo = act ? X[e] : 0.0;
     const int rowbeg = (int)(dsc & 31u);
     const int rowlen = (int)((dsc >> 5) & 7u) + 1;
     const int qb = h.y + (int)(dsc >> 16);
@@ -231,13 +238,33 @@ k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whd
       acc = __hiloint2double(__ldg(&A4[qb]).y, __ldg(&A4[qb]).x) * xo;
       const unsigned sh4 = 4u * (unsigned)pos;
       int q = qb + 1;
+      if constexpr (LA > 0) {
+        // the {ybase, pm} halves of the next LA records are in flight while
+        // record q's gather runs; a(q) is read at use (same line: L1 hit)
+        const int2* I2 = reinterpret_cast<const int2*>(A);
+        const double* Ad = reinterpret_cast<const double*>(A);
+        int2 la[LA > 0 ? LA : 1];
+#pragma unroll
+        for (int j = 0; j < LA; ++j) la[j] = (q + j < qe) ? __ldg(I2 + 2 * (q + j) + 1) : make_int2(0, -1);
+#pragma unroll 2
+        for (; q < qe; ++q) {
+          const int2 cur = la[0];
+#pragma unroll
+          for (int j = 0; j + 1 < LA; ++j) la[j] = la[j + 1];
+          la[LA - 1] = (q + LA < qe) ? __ldg(I2 + 2 * (q + LA) + 1) : make_int2(0, -1);
+          const unsigned s = ((unsigned)cur.y >> sh4) & 0xFu;
+          if (s != 0xFu) acc = fma(__ldg(Ad + 2 * q), X[cur.x + (int)s], acc);
+        }
+      } else {
 #pragma unroll 4
       for (; q < qe; ++q) {
         const int4 en = __ldg(&A4[q]);
         const unsigned s = ((unsigned)en.w >> sh4) & 0xFu;
         if (s != 0xFu) acc = fma(__hiloint2double(en.y, en.x), X[en.z + (int)s], acc);
       }
+      }
     }
+    if (LEAN && act) { qv = v.Q[e]; xo = X[e]; }
     s_qa[wib][lane] = qv * acc;
     __syncwarp();
     double dot = 0.0;
@@ -253,6 +280,83 @@ k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whd
   }
   const double tot = block_sum(part, sh);
   block_partial_out(v, partials, tot, sh, 1);
+}
+
+// k_spgemm_wd's setup / energy modes (the same records and lookahead loop;
+// the lane's row from the window's first row and the head lanes):
+//   MM_R0      r0 = -Pi Pi (A P0)|F, the C-identity term A(i, c_j) added  (A1/A2)
+//   MM_ENERGY  partial W . (A_FF W + 2 A_FC), W = X + X2 (or X)           (Eq. trInc)
+//   MM_R0E     both (setup: they share A P0)
+template <int MODE, int NT = WD_NT>
+__global__ void __launch_bounds__(NT, 2048 / NT)
+k_spgemm_wdm(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whdr, const uint32_t* __restrict__ wdesc,
+             int32_t nwin, const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+             double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[NT / 32][32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;
+  auto xval = [&](int idx) -> double { return two ? X[idx] + X2[idx] : X[idx]; };
+  const int2* I2 = reinterpret_cast<const int2*>(A);
+  const double* Ad = reinterpret_cast<const double*>(A);
+  double part = 0.0;
+  for (int w = gw; w < nwin; w += nw) {
+    const int4 h = __ldg(whdr + w);
+    const int nent = h.z;
+    if (nent == 0) continue;                           // warp-uniform
+    const bool act = lane < nent;
+    const int e = h.x + lane;
+    const uint32_t dsc = act ? __ldg(wdesc + e) : 0u;
+    const int rowbeg = (int)(dsc & 31u);
+    const int rowlen = (int)((dsc >> 5) & 7u) + 1;
+    const int qb = h.y + (int)(dsc >> 16);
+    const int qe = qb + (int)((dsc >> 8) & 255u);
+    const int pos = lane - rowbeg;
+    const unsigned heads = __ballot_sync(0xffffffffu, act && pos == 0);
+    const int i = h.w + __popc(heads & ((2u << rowbeg) - 1u)) - 1;
+    double acc = 0.0, fc = 0.0, xo = 0.0;
+    if (act) {
+      xo = xval(e);
+      acc = Ad[2 * qb] * xo;                           // diagonal record first
+      const unsigned sh4 = 4u * (unsigned)pos;
+      int q = qb + 1;
+      int2 la0 = (q < qe) ? __ldg(I2 + 2 * q + 1) : make_int2(0, -1);
+      int2 la1 = (q + 1 < qe) ? __ldg(I2 + 2 * (q + 1) + 1) : make_int2(0, -1);
+#pragma unroll 2
+      for (; q < qe; ++q) {
+        const int2 cur = la0;
+        la0 = la1;
+        la1 = (q + 2 < qe) ? __ldg(I2 + 2 * (q + 2) + 1) : make_int2(0, -1);
+        const unsigned sidx = ((unsigned)cur.y >> sh4) & 0xFu;
+        if (sidx != 0xFu) acc = fma(__ldg(Ad + 2 * q), xval(cur.x + (int)sidx), acc);
+      }
+      const int32_t j = v.wcol[e];                    // A(i, c_j): search the short A_FC row
+      for (int64_t qq = v.afcptr[i]; qq < v.afcptr[i + 1]; ++qq)
+        if (v.afccol[qq] == j) { fc = v.afcval[qq]; break; }
+    }
+    if (MODE == MM_ENERGY || MODE == MM_R0E)
+      if (act) part = fma(xo, acc + 2.0 * fc, part);
+    if (MODE == MM_ENERGY) continue;                  // warp-uniform (MODE)
+    const double qv = act ? v.Q[e] : 0.0;
+    double g = acc + fc;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {            // Pi applied twice (reading A2)
+      s_qa[wib][lane] = qv * g;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][rowbeg + p];
+      __syncwarp();
+      g = g - qv * dot;
+    }
+    if (act) out[e] = -g;
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, -1);
 }
 
 // win2's setup / energy modes (same window decode and record loop):
@@ -592,7 +696,7 @@ __global__ void k_plan_wdesc(const int64_t* __restrict__ wptr, const int64_t* __
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
     const int r0 = rowstart[w], r1 = rowstart[w + 1];
     const int64_t base = wptr[r0], rec = affptr[r0];
-    whdr[w] = make_int4((int)base, (int)rec, (int)(wptr[r1] - base), 0);
+    whdr[w] = make_int4((int)base, (int)rec, (int)(wptr[r1] - base), r0);
     for (int i = r0; i < r1; ++i) {
       const int64_t b = wptr[i], len = wptr[i + 1] - b;
       const int64_t rc = affptr[i + 1] - affptr[i], rs = affptr[i] - rec;
@@ -730,11 +834,6 @@ static inline int scalar_grid(emin_ctx c) {
   const int64_t nwin = fast_of(c)->sc.nwin;
   return (int)std::max<int64_t>(1, std::min<int64_t>((nwin + 7) / 8, (int64_t)SM * 8));
 }
-// grid of the setup-time masked launches (MM_R0, MM_ENERGY)
-static inline int scalar_spgemm_grid(emin_ctx c) {
-  const ScalarPlan& p = fast_of(c)->sc;
-  return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
-}
 // grid of the per-iteration masked launch (MM_ITER)
 // (k_spgemm_wd: 1024-thread CTAs, 2 per SM -- a CTA's 32 consecutive
 // windows share neighbour y rows in its SM's L1: 114.7 vs 116.8 us with
@@ -747,18 +846,37 @@ static inline int scalar_iter_grid(emin_ctx c) {
                                                      (int64_t)emin_num_sms() * per));
 }
 
+// grid of the setup-time masked launches (MM_R0, MM_R0E, MM_ENERGY): the
+// window-descriptor kernel's, else the tile kernel's (or win2m's)
+static inline int scalar_spgemm_grid(emin_ctx c) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  if (p.whdr && !(c->opts.debug_flags & 256)) return scalar_iter_grid(c);
+  return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
+}
 static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, const double* X2, double* out,
                                         cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
   if (mode == MM_ITER) {
-    // precomputed window decode (114.7 us vs win2's 120.2, config 3, profiles/r02);
+    // precomputed window decode, 1024-thread CTAs, record indices two ahead
+    // (110.4 us vs win2's 120.2, config 3, profiles/r02/spgemm_ab_c3.txt);
     // win2 when a window's counts overflow the lane descriptor
     if (p.whdr)
-      k_spgemm_wd<WD_NT><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc, (int32_t)p.nwin, X, out,
-                                                               c->partials);
- else
+      k_spgemm_wd<WD_NT, WD_LA, true><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc,
+                                                                          (int32_t)p.nwin, X, out, c->partials);
+    else
       k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+    return true;
+  }
+  if (p.whdr && !(c->opts.debug_flags & 256)) {
+    const int g = scalar_iter_grid(c);
+    if (mode == MM_R0E)
+      k_spgemm_wdm<MM_R0E><<<g, WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc, (int32_t)p.nwin, X, X2, out, c->partials);
+    else if (mode == MM_R0)
+      k_spgemm_wdm<MM_R0><<<g, WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc, (int32_t)p.nwin, X, X2, out, c->partials);
+    else
+      k_spgemm_wdm<MM_ENERGY><<<g, WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc, (int32_t)p.nwin, X, X2, out,
+                                                  c->partials);
     return true;
   }
   if (mode == MM_R0E) {                      // fused r0 + E0: the tile kernel only

@@ -622,3 +622,25 @@ def test_sgs_sorted_nodal_sweeps_equal_unsorted(name, size, k):
         res.append((kd, dE, g.get_P(), g.energy()))
     a, b = res
     assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3]
+
+
+@pytest.mark.parametrize("name,size", [("3", 12), ("3", 17), ("2b", 10), ("1b", None)])
+def test_scalar_setup_energy_kernels_agree(name, size):
+    """The scalar path's setup / energy passes (r0, E0 and emin_energy) by the
+    window-descriptor kernel (k_spgemm_wdm, default) and by the staged tile
+    kernel (debug bit 256): the same per-entry sums, different partial-sum
+    grouping -- E0, E and P agree to round-off."""
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    a = Emin.from_problem(prob)
+    b = Emin.from_problem(prob, debug_flags=256)
+    assert a.report()["kernel_path"] == b.report()["kernel_path"] == 1
+    ea, eb = a.report()["E0"], b.report()["E0"]
+    assert abs(ea - eb) <= 1e-13 * abs(eb)
+    ka, dEa = a.iterate(15)
+    kb, dEb = b.iterate(15)
+    assert ka == kb and np.allclose(dEa, dEb, rtol=1e-10, atol=1e-14 * abs(eb))
+    assert abs(a.energy() - b.energy()) <= 1e-13 * abs(b.energy())
+    Pa, Pb = a.get_P(), b.get_P()
+    assert np.abs(Pa - Pb).max() <= 1e-12 * np.abs(Pb).max()
