@@ -487,6 +487,67 @@ k_alg2_nv1(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const 
   }
 }
 
+// k_alg2_nv1 on the window descriptors (k_spgemm_wd's plan): the same
+// windows, lanes and sums (bitwise the same Q and W0), without the run-time
+// window decode
+__global__ void __launch_bounds__(256)
+k_alg2_nv1_wd(DevView v, const int4* __restrict__ whdr, const uint32_t* __restrict__ wdesc, int32_t nwin,
+              const double* __restrict__ Bc, const double* __restrict__ B, const int64_t* __restrict__ frow,
+              const double* __restrict__ what, double* __restrict__ Qout, double* __restrict__ w0,
+              unsigned long long* counters) {
+  __shared__ unsigned long long cnt[2];
+  if (threadIdx.x < 2) cnt[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  unsigned n_svd = 0, n_frozen = 0;
+  for (int w = gw; w < nwin; w += nw) {
+    const int4 h = __ldg(whdr + w);
+    if (h.z == 0) continue;                            // warp-uniform
+    WinLane L;
+    L.base = h.x;
+    L.nent = h.z;
+    L.act = lane < h.z;
+    const uint32_t dsc = L.act ? __ldg(wdesc + h.x + lane) : 0u;
+    L.rowbeg = (int)(dsc & 31u);
+    L.rowlen = (int)((dsc >> 5) & 7u) + 1;
+    L.pos = lane - L.rowbeg;
+    const unsigned heads = __ballot_sync(0xffffffffu, L.act && L.pos == 0);
+    L.rloc = __popc(heads & ((2u << L.rowbeg) - 1u)) - 1;
+    const int64_t e = L.base + lane;
+    const int64_t i = (int64_t)h.w + L.rloc;
+    const double m = L.act ? Bc[v.wcol[e]] : 0.0;
+    const double wh = L.act ? what[e] : 0.0;
+    const double smm = row_sum(m * m, L);
+    const double smw = row_sum(m * wh, L);
+    if (L.act) {
+      const double rv = B[frow[i]] - smw;
+      const double R = sqrt(smm);
+      double q = 0.0, delta = 0.0;
+      int k = 0;
+      if (R > 0.0) {
+        q = m / R;
+        delta = q * (rv / R);
+        k = 1;
+      }
+      Qout[e] = q;
+      w0[e] = wh + delta;
+      if (L.pos == 0) {
+        n_svd += (k == 0);
+        n_frozen += (L.rowlen == k);
+      }
+    }
+  }
+  atomicAdd(&cnt[0], (unsigned long long)n_svd);
+  atomicAdd(&cnt[1], (unsigned long long)n_frozen);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (cnt[0]) atomicAdd(counters + 0, cnt[0]);
+    if (cnt[1]) atomicAdd(counters + 1, cnt[1]);
+  }
+}
+
 // P out on the window plan
 __global__ void __launch_bounds__(256)
 k_get_P_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const double* __restrict__ w0,
@@ -905,8 +966,12 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
 static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
                                       const double* what, unsigned long long* counters, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
-  k_alg2_nv1<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, Bc, B, frow, what, c->Q, c->w0,
-                                            counters);
+  if (p.whdr)
+    k_alg2_nv1_wd<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.whdr, p.wdesc, (int32_t)p.nwin, Bc, B, frow, what,
+                                                 c->Q, c->w0, counters);
+  else
+    k_alg2_nv1<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, Bc, B, frow, what, c->Q, c->w0,
+                                              counters);
 }
 static inline void launch_scalar_get_P(emin_ctx c, double* out, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
