@@ -793,12 +793,16 @@ __global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
       int32_t jk[8];
 #pragma unroll
       for (int s = 0; s < 8; ++s) jk[s] = (s < nk) ? v.wcol[kb + s] : -2;
-      uint32_t pm = 0xFFFFFFFFu;
+      // nibble t = position of J_i[t] in J_k (0xF absent); the lists hold
+      // distinct columns, so at most one s matches a t
+      uint32_t pm = 0u;
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
+      for (int t = 0; t < 8; ++t) {
+        uint32_t nib = 0xFu;
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
-          if (ji[t] == jk[s]) pm = (pm & ~(0xFu << (4 * t))) | ((uint32_t)s << (4 * t));
+        for (int s = 0; s < 8; ++s) nib = (ji[t] == jk[s]) ? (uint32_t)s : nib;
+        pm |= nib << (4 * t);
+      }
       SpEnt e;
       e.a = v.affval[q];
       e.ybase = (int32_t)kb;
@@ -829,7 +833,7 @@ static inline int select_fast_path(emin_ctx c) {
   if (emin_mallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
-  int32_t* wd_ok = nullptr;      // (read back with the tile sizes below: one host sync)
+  int32_t* wd_ok = nullptr;      // descriptors fit (read back below)
   {
     // window headers + lane descriptors of k_spgemm_wd (k_spgemm_win2 if a
     // window's counts do not fit the descriptor)
@@ -846,6 +850,21 @@ static inline int select_fast_path(emin_ctx c) {
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
   k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), p.ent);
   c->launches += 2;
+  if (wd_ok) {
+    int32_t hok = 0;
+    cudaMemcpyAsync(&hok, wd_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(wd_ok, s);
+    if (!hok) {
+      cudaFreeAsync(p.whdr, s);
+      cudaFreeAsync(p.wdesc, s);
+      p.whdr = nullptr;
+      p.wdesc = nullptr;
+    }
+  }
+  // the staged tile kernel (setup / energy modes) is needed only without the
+  // window descriptors (or as the test reference, debug bit 256)
+  if (p.whdr && !(c->opts.debug_flags & 256)) return 1;
   // tile plan for the staged setup / energy kernel
   const int ST = TILE_E - c->max_row + 1;
   p.ntiles = (c->nnzW + ST - 1) / ST;
@@ -861,20 +880,9 @@ static inline int select_fast_path(emin_ctx c) {
   k_tile_headers<<<SM * 4, 256, 0, s>>>(c->wptr, c->affptr, trow, p.ntiles, p.hdr, dmax);
   c->launches += 2;
   cudaMemcpyAsync(hmax, dmax, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s);
-  int32_t hok = 0;
-  if (wd_ok) cudaMemcpyAsync(&hok, wd_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(trow, s);
   cudaFreeAsync(dmax, s);
   cudaStreamSynchronize(s);
-  if (wd_ok) {
-    cudaFreeAsync(wd_ok, s);
-    if (!hok) {
-      cudaFreeAsync(p.whdr, s);
-      cudaFreeAsync(p.wdesc, s);
-      p.whdr = nullptr;
-      p.wdesc = nullptr;
-    }
-  }
   p.tile_smem = tile_smem_bytes(hmax[0]);
   if (p.tile_smem <= TILE_SMEM_CAP) {
     p.use_tiles = 1;
