@@ -111,6 +111,7 @@ struct emin_ctx_s {
   void* fast = nullptr;        // specialised-path plan (kernels_fast.cuh)
   void* nodal = nullptr;       // nodal 3x3 path plan (kernels_nodal.cuh)
   int32_t* erow = nullptr;     // F-row id of every W entry (streaming stages)
+  int32_t* adiag = nullptr;    // position of A(i,i) in A_FF row i (setup: the record plan)
   double* dinv = nullptr;      // 1 / A(i,i) per owned F row
   DistPlan* dist = nullptr;    // multi-GPU halo plan (dist.cu), null on one GPU
   SgsPlan* sgs = nullptr;      // SGS preconditioner plan (sgs.cu), null for Jacobi

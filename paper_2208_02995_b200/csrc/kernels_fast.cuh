@@ -769,7 +769,7 @@ __global__ void k_plan_wdesc(const int64_t* __restrict__ wptr, const int64_t* __
 }
 
 // one group of 8 lanes per F row, lane per A_FF entry (setup only)
-__global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
+__global__ void k_plan_entries(DevView v, const int32_t* __restrict__ adiag, SpEnt* __restrict__ ent) {
   const int lg = threadIdx.x & 7;
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 3;
@@ -782,9 +782,7 @@ __global__ void k_plan_entries(DevView v, SpEnt* __restrict__ ent) {
     // the diagonal record goes first (win2 takes its term from the lane's
     // own y value); the others keep A's column order
     const int64_t qb = v.affptr[i], qe = v.affptr[i + 1];
-    int64_t qd = qb;
-    for (int64_t q = qb; q < qe; ++q)
-      if (v.affcol[q] == (int32_t)i) { qd = q; break; }
+    const int64_t qd = qb + adiag[i];             // (k_fill; validation ensures the diagonal)
     for (int64_t q = qb + lg; q < qe; q += 8) {
       const int64_t dst = (q == qd) ? qb : (q < qd ? q + 1 : q);
       const int32_t k = v.affcol[q];
@@ -848,7 +846,7 @@ static inline int select_fast_path(emin_ctx c) {
     wd_ok = dok;
   }
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
-  k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), p.ent);
+  k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent);
   c->launches += 2;
   if (wd_ok) {
     int32_t hok = 0;

@@ -135,6 +135,7 @@ struct FillArgs {
   int32_t* affcol; double* affval; int32_t* afccol; double* afcval;
   int64_t* frow;   // local F id -> local row
   const int64_t* hpos;   // multi-GPU: halo slot of a global F id (null on one GPU)
+  int32_t* adiag;  // position of A(i,i) in A_FF row i (the record plan puts it first)
 };
 
 // F rows: copy the pattern into the W layout, split A into A_FF (local F
@@ -186,6 +187,7 @@ __global__ void k_fill(FillArgs a) {
         const int64_t pos = off_ff + __popc(mf & lt);
         a.affcol[pos] = (int32_t)loc;
         a.affval[pos] = v;
+        if (loc == fl) a.adiag[fl] = (int32_t)(pos - a.affptr[fl]);
       }
       if (coarse) {
         const int64_t pos = off_fc + __popc(mc & lt);
@@ -888,6 +890,8 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   fa.affcol = ctx->affcol; fa.affval = ctx->affval; fa.afccol = ctx->afccol; fa.afcval = ctx->afcval;
   fa.frow = frow;
   fa.hpos = ctx->dist ? ctx->dist->hpos : nullptr;
+  SETUP_TRY(dalloc(&ctx->adiag, std::max<int64_t>(nF, 1), s));
+  fa.adiag = ctx->adiag;
   const int gfill = 64;
   k_fill<<<SM * gfill, 256, 0, s>>>(fa);
   SETUP_TRY(cudaGetLastError());
