@@ -113,6 +113,8 @@ typedef struct {
 #define EMIN_DBG_FORCE_GENERIC 1   /* generic warp-per-row kernels instead of the scalar / nodal
                                       specialisations (the reference the fast paths are tested
                                       against) */
+#define EMIN_DBG_AB2 128           /* scalar path: the per-iteration masked product with one W
+                                      entry per lane (k_spgemm_wd) instead of two (k_spgemm_wp) */
 #define EMIN_DBG_NO_R0E 2          /* r0 and E0 by two masked passes instead of the fused one */
 #define EMIN_DBG_SGS_GENERIC 4     /* generic warp-per-row SGS sweeps */
 #define EMIN_DBG_TRACE 8           /* synchronise and print each setup phase's host time */

@@ -455,7 +455,7 @@ int emin_launch_masked(emin_ctx c, int mode, const double* X, const double* X2, 
   const int grid = c->grid_spgemm;
   if (c->kernel_path == 1) {
     if (!launch_scalar_masked(c, mode, X, X2, out, s)) return -1;
-    return mode == MM_ITER ? scalar_iter_grid(c) : grid;
+    return mode == MM_ITER ? scalar_iter_launch_grid(c) : grid;
   }
   if (c->kernel_path == 2) {
     const NodalPlan* np = static_cast<const NodalPlan*>(c->nodal);
@@ -497,7 +497,7 @@ static emin_status emin_split_plan(emin_ctx c) {
   int64_t nunits = c->nF;
   if (c->kernel_path == 1) {
     int64_t nwin = 0;
-    const int32_t* rs = emin_scalar_windows(c, &nwin);
+    const int32_t* rs = scalar_iter_windows(c, &nwin);
     k_window_range<<<1, 1, 0, s>>>(rs, nwin, d, d + 3);
     c->launches += 1;
     nunits = nwin;
@@ -551,7 +551,7 @@ emin_status emin_plan(emin_ctx c) {
     c->pingpong = 1;
   }
   c->grid_red = std::max(c->grid_rows, c->grid_spgemm);
-  if (c->kernel_path == 1) c->grid_red = std::max(c->grid_red, scalar_iter_grid(c));
+  if (c->kernel_path == 1) c->grid_red = std::max(c->grid_red, scalar_iter_launch_grid(c));
   if (c->kernel_path == 2) c->grid_red = std::max(c->grid_red, nodal_grid(c, static_cast<NodalPlan*>(c->nodal)));
   if (c->dist) {
     // the y^ launch may run as an interior and a boundary launch (both

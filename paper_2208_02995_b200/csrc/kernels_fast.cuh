@@ -13,9 +13,11 @@
 //   nibble t of pm is the position of J_i[t] in J_k (0xF: absent).  So the
 //   inner loop is one 16-byte broadcast load, a nibble extract and one
 //   gather of y(k, s) -- no search.
-// Per-iteration kernel: k_spgemm_wd (win2's windows with the decode
-// precomputed at setup; k_spgemm_win2 when the descriptors overflow);
-// setup / energy modes: the tile kernel
+// Per-iteration kernel: k_spgemm_wp (two W entries per lane on pair
+// windows, one record load per two gathers; k_spgemm_wd -- one entry per
+// lane, win2's windows with the decode precomputed at setup -- is its A/B
+// reference, k_spgemm_win2 the fallback when the descriptors overflow);
+// setup / energy modes: k_spgemm_wdm on wd's windows, else the tile kernel
 // (k_spgemm_tile, fused MM_R0E at setup), or win2's modes (k_spgemm_win2m)
 // when a tile's records do not fit in shared memory.  The round-1 A/B
 // variants (profiles/ab_r01/) are not part of the library.
@@ -37,6 +39,12 @@ struct ScalarPlan {
   int32_t* rowstart = nullptr;   // [nwin + 1]
   int4* whdr = nullptr;          // [nwin] {first W entry, first record, entries, first row} (k_spgemm_wd)
   uint32_t* wdesc = nullptr;     // [nnzW] lane descriptor (k_spgemm_wd)
+  // pair-lane plan of the per-iteration kernel (k_spgemm_wp)
+  int64_t* lptr = nullptr;       // [nF + 1] first lane slot of each row
+  int32_t* prowstart = nullptr;  // [npwin + 1] first row of each pair window
+  int4* phdr = nullptr;          // [npwin] {first lane slot, first record, lanes, first W entry}
+  int2* pdesc = nullptr;         // [lanes] {first entry, packed row / record fields}
+  int64_t npwin = 0;
   int64_t nwin = 0;
   int32_t S = 0;
   TileHdr* hdr = nullptr;        // [ntiles] (staged tile kernel, setup / energy modes)
@@ -276,6 +284,110 @@ k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whd
       const double g = acc - qv * dot;
       out[e] = g;
       part = fma(xo, g, part);
+    }
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, 1);
+}
+
+// y^ = Pi K y (nv = 1), pair-lane kernel: a lane owns TWO consecutive W
+// entries of its row (positions 2t and 2t+1), so one record load {a, ybase,
+// pm} and its decode serve two gathers and two FMAs, and a window of 32
+// lanes covers up to 64 entries (half as many windows, each with twice the
+// gathers in flight per warp).  Lane slots: row r has ceil(|J_r| / 2) of
+// them (lptr = their prefix sum); windows are cut on lane slots like wd's on
+// entries.  Per window a 16-byte header {first lane slot, first record,
+// lanes, first W entry}; per lane slot an int2 {first entry e0, row's first
+// lane | (|J_r| - 1) << 5 | records << 8 | first record rel. << 16}.  Each
+// entry's sum and the row projection take the same terms in the same order
+// as wd (bitwise the same y^); only the y^T y partials are grouped per lane.
+constexpr int WP_PAD = 4;      // records allocated past nnz(A_FF) (k_spgemm_wp's look-ahead)
+// launch shape of k_spgemm_wp (config 3, us per launch, profiles/r02/spgemm_ab_c3.txt):
+// 512-thread CTAs, 3 per SM (40 registers, 48 warps/SM), record loop unrolled
+// twice: 95.2; 1024 x 2 (32 registers) 97.8-99.1; 768 x 2 96.3-98.5; four
+// entries per lane 122-155
+constexpr int WP_NT = 512, WP_MINB = 3, WP_UNR = 2;
+template <int NT = WD_NT, int MINB = 2048 / NT, int UNR = 1, int E = 2>
+__global__ void __launch_bounds__(NT, MINB)
+k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phdr, const int2* __restrict__ pdesc,
+            int32_t nwin, const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[NT / 32][32 * E];
+  if (v.st->stopped) { iter_stopped(v); return; }
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  double part = 0.0;
+  const bool rev = v.pingpong && (v.st->k_total & 1);   // same direction as stage I (L2 ping-pong)
+  const bool split = v.uend >= 0 || v.ubeg != 0 || v.ugap1 != v.ugap0;
+  const int cnt = split ? (int)unit_count(v, nwin) : nwin;
+  const int2* I2 = reinterpret_cast<const int2*>(A);
+  const double* Ad = reinterpret_cast<const double*>(A);
+  for (int w1 = gw; w1 < cnt; w1 += nw) {
+    int w = rev ? cnt - 1 - w1 : w1;
+    if (split) w = (int)unit_of(v, w);
+    const int4 h = __ldg(phdr + w);
+    const int nl = h.z;
+    if (nl == 0) continue;                             // warp-uniform
+    const bool act = lane < nl;
+    const int2 d = act ? __ldg(pdesc + h.x + lane) : make_int2(0, 0);
+    const int e0 = d.x;
+    const uint32_t dsc = (uint32_t)d.y;
+    const int rowbeg = (int)(dsc & 31u);
+    const int rowlen = (int)((dsc >> 5) & 7u) + 1;
+    const int p0 = E * (lane - rowbeg);                // the lane's first position in its row
+    double acc[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) acc[j] = 0.0;
+    if (act) {
+      const int qb = h.y + (int)(dsc >> 16);
+      const int qe = qb + (int)((dsc >> 8) & 255u);
+      const double ad = __ldg(Ad + 2 * qb);            // record qb: the diagonal A(i,i), own y entries
+#pragma unroll
+      for (int j = 0; j < E; ++j)
+        if (p0 + j < rowlen) acc[j] = ad * X[e0 + j];
+      const unsigned shp = 4u * (unsigned)p0;
+      // the record stream is padded by WP_PAD records, so the look-ahead
+      // load needs no bound check; an absent position gathers nothing and
+      // adds a * 0 (the value of skipping the term, up to the sign of a zero)
+      int2 nxt = __ldg(I2 + 2 * (qb + 1) + 1);
+#pragma unroll UNR
+      for (int q = qb + 1; q < qe; ++q) {
+        const int2 cur = nxt;
+        nxt = __ldg(I2 + 2 * (q + 1) + 1);
+        const unsigned pm = (unsigned)cur.y >> shp;    // positions past the row: 0xF
+        double y[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const unsigned sj = (pm >> (4 * j)) & 0xFu;
+          y[j] = (sj != 0xFu) ? X[cur.x + (int)sj] : 0.0;
+        }
+        const double a = __ldg(Ad + 2 * q);
+#pragma unroll
+        for (int j = 0; j < E; ++j) acc[j] = fma(a, y[j], acc[j]);
+      }
+    }
+    double qv[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      qv[j] = (act && p0 + j < rowlen) ? v.Q[e0 + j] : 0.0;
+      s_qa[wib][E * lane + j] = qv[j] * acc[j];
+    }
+    __syncwarp();
+    double dot = 0.0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)                       // |J_i| <= 8 on the scalar path
+      if (p < rowlen) dot += s_qa[wib][E * rowbeg + p];
+    __syncwarp();
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < E; ++j)
+        if (p0 + j < rowlen) {
+          const double g = acc[j] - qv[j] * dot;
+          out[e0 + j] = g;
+          part = fma(X[e0 + j], g, part);
+        }
     }
   }
   const double tot = block_sum(part, sh);
@@ -810,6 +922,31 @@ __global__ void k_plan_entries(DevView v, const int32_t* __restrict__ adiag, SpE
   }
 }
 
+// k_spgemm_wp's plan: lane slots per row, ceil(|J_r| / 2)
+__global__ void k_plan_lane_count(const int64_t* __restrict__ wptr, int64_t nF, int32_t E, int64_t* __restrict__ lcnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+    lcnt[i] = (wptr[i + 1] - wptr[i] + E - 1) / E;
+}
+// pair-window headers and lane-slot descriptors, one thread per window (the
+// counts fit: rows <= 8 entries and <= WD_MAXREC records were checked for wd,
+// and <= 31 rows of <= 255 records stay below WD_MAXREL)
+__global__ void k_plan_pdesc(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
+                             const int64_t* __restrict__ lptr, const int32_t* __restrict__ rowstart, int64_t nwin,
+                             int32_t E, int4* __restrict__ phdr, int2* __restrict__ pdesc) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const int r0 = rowstart[w], r1 = rowstart[w + 1];
+    const int64_t lb = lptr[r0], rec = affptr[r0];
+    phdr[w] = make_int4((int)lb, (int)rec, (int)(lptr[r1] - lb), (int)wptr[r0]);
+    for (int i = r0; i < r1; ++i) {
+      const int64_t l0 = lptr[i], l1 = lptr[i + 1];
+      const int64_t len = wptr[i + 1] - wptr[i];
+      const int64_t rc = affptr[i + 1] - affptr[i], rs = affptr[i] - rec;
+      const uint32_t d = (uint32_t)(l0 - lb) | ((uint32_t)(len - 1) << 5) | ((uint32_t)rc << 8) | ((uint32_t)rs << 16);
+      for (int64_t l = l0; l < l1; ++l) pdesc[l] = make_int2((int)(wptr[i] + E * (l - l0)), (int)d);
+    }
+  }
+}
+
 // ---- host side ------------------------------------------------------------
 struct FastPaths {
   ScalarPlan sc;
@@ -828,7 +965,8 @@ static inline int select_fast_path(emin_ctx c) {
   p.nwin = (c->nnzW + p.S - 1) / p.S;
   cudaStream_t s = c->stream;
   if (emin_mallocAsync((void**)&p.rowstart, sizeof(int32_t) * (p.nwin + 1), s) != cudaSuccess) return 0;
-  if (emin_mallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)std::max<int64_t>(c->nnzAFF, 1), s) != cudaSuccess) return 0;
+  if (emin_mallocAsync((void**)&p.ent, sizeof(SpEnt) * (size_t)(c->nnzAFF + WP_PAD), s) != cudaSuccess) return 0;
+  cudaMemsetAsync(p.ent + c->nnzAFF, 0, sizeof(SpEnt) * WP_PAD, s);
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
   int32_t* wd_ok = nullptr;      // descriptors fit (read back below)
@@ -848,16 +986,38 @@ static inline int select_fast_path(emin_ctx c) {
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
   k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent);
   c->launches += 2;
-  if (wd_ok) {
-    int32_t hok = 0;
-    cudaMemcpyAsync(&hok, wd_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  // lane slots of the pair-lane kernel (k_spgemm_wp)
+  int64_t* lscr = nullptr;
+  if (emin_mallocAsync((void**)&p.lptr, sizeof(int64_t) * (c->nF + 1), s) != cudaSuccess ||
+      emin_mallocAsync((void**)&lscr, sizeof(int64_t) * emin_scan_scratch_elems(c->nF + 1), s) != cudaSuccess)
+    return 0;
+  k_plan_lane_count<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, 2, p.lptr);   // two entries per lane
+  if (emin_scan_i64(p.lptr, p.lptr, c->nF, p.lptr + c->nF, lscr, s) != cudaSuccess) return 0;
+  c->launches += 4;
+  {
+    int64_t hbuf[2] = {0, 0};        // {descriptors fit, lane slots}
+    cudaMemcpyAsync(&hbuf[0], wd_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&hbuf[1], p.lptr + c->nF, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     cudaFreeAsync(wd_ok, s);
-    if (!hok) {
+    cudaFreeAsync(lscr, s);
+    if (!(int32_t)(hbuf[0] & 0xffffffff)) {
       cudaFreeAsync(p.whdr, s);
       cudaFreeAsync(p.wdesc, s);
       p.whdr = nullptr;
       p.wdesc = nullptr;
+    } else {
+      // pair windows: rows whose first lane slot lies in [w S2, (w+1) S2)
+      const int32_t S2 = std::min(31, 33 - (c->max_row + 1) / 2);
+      const int64_t L = hbuf[1];
+      p.npwin = (L + S2 - 1) / S2;
+      if (emin_mallocAsync((void**)&p.prowstart, sizeof(int32_t) * (p.npwin + 1), s) != cudaSuccess ||
+          emin_mallocAsync((void**)&p.phdr, sizeof(int4) * std::max<int64_t>(p.npwin, 1), s) != cudaSuccess ||
+          emin_mallocAsync((void**)&p.pdesc, sizeof(int2) * std::max<int64_t>(L, 1), s) != cudaSuccess)
+        return 0;
+      k_plan_rowstart<<<SM * 8, 256, 0, s>>>(p.lptr, c->nF, S2, p.npwin, p.prowstart);
+      k_plan_pdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.lptr, p.prowstart, p.npwin, 2, p.phdr, p.pdesc);
+      c->launches += 2;
     }
   }
   // the staged tile kernel (setup / energy modes) is needed only without the
@@ -912,6 +1072,20 @@ static inline int scalar_iter_grid(emin_ctx c) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((p.nwin + WD_NT / 32 - 1) / (WD_NT / 32),
                                                      (int64_t)emin_num_sms() * per));
 }
+// grid of the per-iteration launch (the kernel launch_scalar_masked picks)
+static inline int scalar_iter_launch_grid(emin_ctx c) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  if (!(p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))) return scalar_iter_grid(c);
+  return (int)std::max<int64_t>(1, std::min<int64_t>((p.npwin + WP_NT / 32 - 1) / (WP_NT / 32),
+                                                     (int64_t)emin_num_sms() * WP_MINB));
+}
+// the per-iteration kernel's units (windows): pair windows unless wd runs
+static inline const int32_t* scalar_iter_windows(emin_ctx c, int64_t* nwin) {
+  const ScalarPlan& p = fast_of(c)->sc;
+  if (p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2)) { *nwin = p.npwin; return p.prowstart; }
+  *nwin = p.nwin;
+  return p.rowstart;
+}
 
 // grid of the setup-time masked launches (MM_R0, MM_R0E, MM_ENERGY): the
 // window-descriptor kernel's, else the tile kernel's (or win2m's)
@@ -925,10 +1099,14 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
   if (mode == MM_ITER) {
-    // precomputed window decode, 1024-thread CTAs, record indices two ahead
-    // (110.4 us vs win2's 120.2, config 3, profiles/r02/spgemm_ab_c3.txt);
-    // win2 when a window's counts overflow the lane descriptor
-    if (p.whdr)
+    // two W entries per lane on precomputed pair windows (config 3: 95.2 us
+    // vs wd's 110.6 and win2's 120.2, profiles/r02/spgemm_ab_c3.txt); wd is
+    // the A/B reference (EMIN_DBG_AB2); win2 when a window's counts overflow
+    // the lane descriptor
+    if (p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))
+      k_spgemm_wp<WP_NT, WP_MINB, WP_UNR, 2><<<scalar_iter_launch_grid(c), WP_NT, 0, s>>>(
+          v, p.ent, p.phdr, p.pdesc, (int32_t)p.npwin, X, out, c->partials);
+    else if (p.whdr)
       k_spgemm_wd<WD_NT, WD_LA, true><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc,
                                                                           (int32_t)p.nwin, X, out, c->partials);
     else
@@ -990,6 +1168,10 @@ static inline void free_fast_path(emin_ctx c) {
   if (f->sc.rowstart) cudaFreeAsync(f->sc.rowstart, c->stream);
   if (f->sc.whdr) cudaFreeAsync(f->sc.whdr, c->stream);
   if (f->sc.wdesc) cudaFreeAsync(f->sc.wdesc, c->stream);
+  if (f->sc.lptr) cudaFreeAsync(f->sc.lptr, c->stream);
+  if (f->sc.prowstart) cudaFreeAsync(f->sc.prowstart, c->stream);
+  if (f->sc.phdr) cudaFreeAsync(f->sc.phdr, c->stream);
+  if (f->sc.pdesc) cudaFreeAsync(f->sc.pdesc, c->stream);
   if (f->sc.ent) cudaFreeAsync(f->sc.ent, c->stream);
   if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
   delete f;

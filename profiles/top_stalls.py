@@ -23,4 +23,4 @@ def top(rep, n=25, kernel_idx=0):
 
 
 if __name__ == "__main__":
-    print(top(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25))
+    print(top(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25, int(sys.argv[3]) if len(sys.argv) > 3 else 0))

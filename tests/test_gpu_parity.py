@@ -624,6 +624,27 @@ def test_sgs_sorted_nodal_sweeps_equal_unsorted(name, size, k):
     assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3]
 
 
+@pytest.mark.parametrize("name,size", [("3", 12), ("3", 17), ("2b", 10), ("1b", None), ("3", 24)])
+def test_scalar_pair_kernel_agrees(name, size):
+    """The per-iteration masked product with two W entries per lane
+    (k_spgemm_wp, default) and with one (k_spgemm_wd, EMIN_DBG_AB2): every
+    entry's sum and the row projection take the same terms in the same
+    order, only the y^T y partial sums are grouped differently -- so the
+    trajectories agree to round-off."""
+    from paper_2208_02995_b200 import Emin
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    a = Emin.from_problem(prob)
+    b = Emin.from_problem(prob, debug_flags=128)
+    assert a.report()["kernel_path"] == b.report()["kernel_path"] == 1
+    ka, dEa = a.iterate(20)
+    kb, dEb = b.iterate(20)
+    assert ka == kb and np.allclose(dEa, dEb, rtol=1e-9, atol=1e-13 * abs(dEb[0]))
+    assert abs(a.energy() - b.energy()) <= 1e-12 * abs(b.energy())
+    Pa, Pb = a.get_P(), b.get_P()
+    assert np.abs(Pa - Pb).max() <= 1e-10 * np.abs(Pb).max()
+
+
 @pytest.mark.parametrize("name,size", [("3", 12), ("3", 17), ("2b", 10), ("1b", None)])
 def test_scalar_setup_energy_kernels_agree(name, size):
     """The scalar path's setup / energy passes (r0, E0 and emin_energy) by the
