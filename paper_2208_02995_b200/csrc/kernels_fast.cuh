@@ -322,7 +322,7 @@ k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phd
   const bool rev = v.pingpong && (v.st->k_total & 1);   // same direction as stage I (L2 ping-pong)
   const bool split = v.uend >= 0 || v.ubeg != 0 || v.ugap1 != v.ugap0;
   const int cnt = split ? (int)unit_count(v, nwin) : nwin;
-  const int2* I2 = reinterpret_cast<const int2*>(A);
+  const int4* A4 = reinterpret_cast<const int4*>(A);
   const double* Ad = reinterpret_cast<const double*>(A);
   for (int w1 = gw; w1 < cnt; w1 += nw) {
     int w = rev ? cnt - 1 - w1 : w1;
@@ -348,22 +348,25 @@ k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phd
       for (int j = 0; j < E; ++j)
         if (p0 + j < rowlen) acc[j] = ad * X[e0 + j];
       const unsigned shp = 4u * (unsigned)p0;
-      // the record stream is padded by WP_PAD records, so the look-ahead
-      // load needs no bound check; an absent position gathers nothing and
-      // adds a * 0 (the value of skipping the term, up to the sign of a zero)
-      int2 nxt = __ldg(I2 + 2 * (qb + 1) + 1);
+      // one 16-byte load per record {a, ybase, pm}, one record ahead (split
+      // 8-byte loads of {ybase, pm} and a cost twice the L1 tag requests:
+      // 95.2 vs 91.4 us on config 3); the record stream is padded by WP_PAD
+      // records, so the look-ahead needs no bound check; an absent position
+      // gathers nothing and adds a * 0 (the value of skipping the term, up
+      // to the sign of a zero)
+      int4 nxt = __ldg(A4 + qb + 1);
 #pragma unroll UNR
       for (int q = qb + 1; q < qe; ++q) {
-        const int2 cur = nxt;
-        nxt = __ldg(I2 + 2 * (q + 1) + 1);
-        const unsigned pm = (unsigned)cur.y >> shp;    // positions past the row: 0xF
+        const int4 cur = nxt;
+        nxt = __ldg(A4 + q + 1);
+        const unsigned pm = (unsigned)cur.w >> shp;    // positions past the row: 0xF
         double y[E];
 #pragma unroll
         for (int j = 0; j < E; ++j) {
           const unsigned sj = (pm >> (4 * j)) & 0xFu;
-          y[j] = (sj != 0xFu) ? X[cur.x + (int)sj] : 0.0;
+          y[j] = (sj != 0xFu) ? X[cur.z + (int)sj] : 0.0;
         }
-        const double a = __ldg(Ad + 2 * q);
+        const double a = __hiloint2double(cur.y, cur.x);
 #pragma unroll
         for (int j = 0; j < E; ++j) acc[j] = fma(a, y[j], acc[j]);
       }
@@ -1099,7 +1102,7 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
   const ScalarPlan& p = fast_of(c)->sc;
   const DevView v = c->view();
   if (mode == MM_ITER) {
-    // two W entries per lane on precomputed pair windows (config 3: 95.2 us
+    // two W entries per lane on precomputed pair windows (config 3: 91.4 us
     // vs wd's 110.6 and win2's 120.2, profiles/r02/spgemm_ab_c3.txt); wd is
     // the A/B reference (EMIN_DBG_AB2); win2 when a window's counts overflow
     // the lane descriptor
