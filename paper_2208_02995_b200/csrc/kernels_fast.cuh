@@ -42,7 +42,7 @@ struct ScalarPlan {
   // pair-lane plan of the per-iteration kernel (k_spgemm_wp)
   int64_t* lptr = nullptr;       // [nF + 1] first lane slot of each row
   int32_t* prowstart = nullptr;  // [npwin + 1] first row of each pair window
-  int4* phdr = nullptr;          // [npwin] {first lane slot, first record, lanes, first W entry}
+  int4* phdr = nullptr;          // [npwin] {first lane slot, first record, lanes, first row}
   int2* pdesc = nullptr;         // [lanes] {first entry, packed row / record fields}
   int64_t npwin = 0;
   int64_t nwin = 0;
@@ -297,7 +297,7 @@ k_spgemm_wd(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ whd
 // gathers in flight per warp).  Lane slots: row r has ceil(|J_r| / 2) of
 // them (lptr = their prefix sum); windows are cut on lane slots like wd's on
 // entries.  Per window a 16-byte header {first lane slot, first record,
-// lanes, first W entry}; per lane slot an int2 {first entry e0, row's first
+// lanes, first row}; per lane slot an int2 {first entry e0, row's first
 // lane | (|J_r| - 1) << 5 | records << 8 | first record rel. << 16}.  Each
 // entry's sum and the row projection take the same terms in the same order
 // as wd (bitwise the same y^); only the y^T y partials are grouped per lane.
@@ -395,6 +395,174 @@ k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phd
   }
   const double tot = block_sum(part, sh);
   block_partial_out(v, partials, tot, sh, 1);
+}
+
+// k_spgemm_wp's setup / energy modes on the pair windows (wdm's terms in
+// wdm's order per entry -- the same r0 -- with the partial sums grouped per
+// lane):
+//   MM_R0      r0 = -Pi Pi (A P0)|F, the C-identity term A(i, c_j) added  (A1/A2)
+//   MM_ENERGY  partial W . (A_FF W + 2 A_FC), W = X + X2 (or X)           (Eq. trInc)
+//   MM_R0E     both (setup: they share A P0)
+// The lane's row: the window's first row (header .w) + the row heads before it.
+template <int MODE, int NT = WP_NT, int MINB = WP_MINB>
+__global__ void __launch_bounds__(NT, MINB)
+k_spgemm_wpm(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phdr, const int2* __restrict__ pdesc,
+             int32_t nwin, const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
+             double* __restrict__ partials) {
+  __shared__ double sh[32];
+  __shared__ double s_qa[NT / 32][64];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const bool two = MODE == MM_ENERGY && X2 != nullptr;
+  auto xval = [&](int idx) -> double { return two ? X[idx] + X2[idx] : X[idx]; };
+  const int4* A4 = reinterpret_cast<const int4*>(A);
+  const double* Ad = reinterpret_cast<const double*>(A);
+  double part = 0.0;
+  for (int w = gw; w < nwin; w += nw) {
+    const int4 h = __ldg(phdr + w);
+    const int nl = h.z;
+    if (nl == 0) continue;                             // warp-uniform
+    const bool act = lane < nl;
+    const int2 d = act ? __ldg(pdesc + h.x + lane) : make_int2(0, 0);
+    const int e0 = d.x;
+    const uint32_t dsc = (uint32_t)d.y;
+    const int rowbeg = (int)(dsc & 31u);
+    const int rowlen = (int)((dsc >> 5) & 7u) + 1;
+    const int p0 = 2 * (lane - rowbeg);
+    const bool has1 = p0 + 1 < rowlen;
+    const unsigned heads = __ballot_sync(0xffffffffu, act && p0 == 0);
+    const int i = h.w + __popc(heads & ((2u << rowbeg) - 1u)) - 1;
+    double acc0 = 0.0, acc1 = 0.0, fc0 = 0.0, fc1 = 0.0, xo0 = 0.0, xo1 = 0.0;
+    if (act) {
+      const int qb = h.y + (int)(dsc >> 16);
+      const int qe = qb + (int)((dsc >> 8) & 255u);
+      const double ad = Ad[2 * qb];                    // diagonal record first
+      xo0 = xval(e0);
+      acc0 = ad * xo0;
+      if (has1) { xo1 = xval(e0 + 1); acc1 = ad * xo1; }
+      const unsigned shp = 4u * (unsigned)p0;
+      for (int q = qb + 1; q < qe; ++q) {
+        const int4 cur = __ldg(A4 + q);
+        const unsigned pm = (unsigned)cur.w >> shp;
+        const unsigned s0 = pm & 0xFu, s1 = (pm >> 4) & 0xFu;
+        const double a = __hiloint2double(cur.y, cur.x);
+        if (s0 != 0xFu) acc0 = fma(a, xval(cur.z + (int)s0), acc0);
+        if (s1 != 0xFu) acc1 = fma(a, xval(cur.z + (int)s1), acc1);
+      }
+      // A(i, c_j): search the short A_FC row
+      const int32_t j0 = v.wcol[e0], j1 = has1 ? v.wcol[e0 + 1] : -1;
+      for (int64_t q = v.afcptr[i]; q < v.afcptr[i + 1]; ++q) {
+        const int32_t cq = v.afccol[q];
+        if (cq == j0) fc0 = v.afcval[q];
+        if (cq == j1) fc1 = v.afcval[q];
+      }
+    }
+    if (MODE == MM_ENERGY || MODE == MM_R0E)
+      if (act) {
+        part = fma(xo0, acc0 + 2.0 * fc0, part);
+        if (has1) part = fma(xo1, acc1 + 2.0 * fc1, part);
+      }
+    if (MODE == MM_ENERGY) continue;                  // warp-uniform (MODE)
+    const double qv0 = act ? v.Q[e0] : 0.0;
+    const double qv1 = (act && has1) ? v.Q[e0 + 1] : 0.0;
+    double g0 = acc0 + fc0, g1 = acc1 + fc1;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {            // Pi applied twice (reading A2)
+      s_qa[wib][2 * lane] = qv0 * g0;
+      s_qa[wib][2 * lane + 1] = qv1 * g1;
+      __syncwarp();
+      double dot = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < rowlen) dot += s_qa[wib][2 * rowbeg + p];
+      __syncwarp();
+      g0 = g0 - qv0 * dot;
+      g1 = g1 - qv1 * dot;
+    }
+    if (act) {
+      out[e0] = -g0;
+      if (has1) out[e0 + 1] = -g1;
+    }
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, -1);
+}
+
+// Alg. 2 for nv = 1 on the pair windows (q = M / |M|, delta = q (r / |M|);
+// |M| = 0 is the rank-0 SVD branch): the row sums of m m and m w^ in
+// ascending position order through shared memory
+template <int NT = 256>
+__global__ void __launch_bounds__(NT)
+k_alg2_nv1_wp(DevView v, const int4* __restrict__ phdr, const int2* __restrict__ pdesc, int32_t nwin,
+              const double* __restrict__ Bc, const double* __restrict__ B, const int64_t* __restrict__ frow,
+              const double* __restrict__ what, double* __restrict__ Qout, double* __restrict__ w0,
+              unsigned long long* counters) {
+  __shared__ unsigned long long cnt[2];
+  __shared__ double s_m[NT / 32][64];
+  __shared__ double s_w[NT / 32][64];
+  if (threadIdx.x < 2) cnt[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  unsigned n_svd = 0, n_frozen = 0;
+  for (int w = gw; w < nwin; w += nw) {
+    const int4 h = __ldg(phdr + w);
+    if (h.z == 0) continue;                            // warp-uniform
+    const bool act = lane < h.z;
+    const int2 d = act ? __ldg(pdesc + h.x + lane) : make_int2(0, 0);
+    const int e0 = d.x;
+    const uint32_t dsc = (uint32_t)d.y;
+    const int rowbeg = (int)(dsc & 31u);
+    const int rowlen = (int)((dsc >> 5) & 7u) + 1;
+    const int p0 = 2 * (lane - rowbeg);
+    const bool has1 = p0 + 1 < rowlen;
+    const unsigned heads = __ballot_sync(0xffffffffu, act && p0 == 0);
+    const int i = h.w + __popc(heads & ((2u << rowbeg) - 1u)) - 1;
+    const double m0 = act ? Bc[v.wcol[e0]] : 0.0;
+    const double m1 = (act && has1) ? Bc[v.wcol[e0 + 1]] : 0.0;
+    const double wh0 = act ? what[e0] : 0.0;
+    const double wh1 = (act && has1) ? what[e0 + 1] : 0.0;
+    s_m[wib][2 * lane] = m0 * m0;
+    s_m[wib][2 * lane + 1] = m1 * m1;
+    s_w[wib][2 * lane] = m0 * wh0;
+    s_w[wib][2 * lane + 1] = m1 * wh1;
+    __syncwarp();
+    double smm = 0.0, smw = 0.0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      if (p < rowlen) { smm += s_m[wib][2 * rowbeg + p]; smw += s_w[wib][2 * rowbeg + p]; }
+    __syncwarp();
+    if (act) {
+      const double rv = B[frow[i]] - smw;
+      const double R = sqrt(smm);
+      int k = 0;
+      double q0 = 0.0, q1 = 0.0, dl0 = 0.0, dl1 = 0.0;
+      if (R > 0.0) {
+        const double rr = rv / R;
+        q0 = m0 / R; q1 = m1 / R;
+        dl0 = q0 * rr; dl1 = q1 * rr;
+        k = 1;
+      }
+      Qout[e0] = q0;
+      w0[e0] = wh0 + dl0;
+      if (has1) { Qout[e0 + 1] = q1; w0[e0 + 1] = wh1 + dl1; }
+      if (p0 == 0) {
+        n_svd += (k == 0);
+        n_frozen += (rowlen == k);
+      }
+    }
+  }
+  atomicAdd(&cnt[0], (unsigned long long)n_svd);
+  atomicAdd(&cnt[1], (unsigned long long)n_frozen);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (cnt[0]) atomicAdd(counters + 0, cnt[0]);
+    if (cnt[1]) atomicAdd(counters + 1, cnt[1]);
+  }
 }
 
 // k_spgemm_wd's setup / energy modes (the same records and lookahead loop;
@@ -925,28 +1093,43 @@ __global__ void k_plan_entries(DevView v, const int32_t* __restrict__ adiag, SpE
   }
 }
 
-// k_spgemm_wp's plan: lane slots per row, ceil(|J_r| / 2)
-__global__ void k_plan_lane_count(const int64_t* __restrict__ wptr, int64_t nF, int32_t E, int64_t* __restrict__ lcnt) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+// k_spgemm_wp's plan: lane slots per row, ceil(|J_r| / E), and the longest
+// record run (the descriptor holds <= WD_MAXREC records per row)
+__global__ void k_plan_lane_count(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr, int64_t nF,
+                                  int32_t E, int64_t* __restrict__ lcnt, int32_t* __restrict__ maxrc) {
+  int32_t m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x) {
     lcnt[i] = (wptr[i + 1] - wptr[i] + E - 1) / E;
+    const int64_t rc = affptr[i + 1] - affptr[i];
+    m = max(m, (int32_t)min(rc, (int64_t)INT32_MAX));
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(maxrc, m);
 }
-// pair-window headers and lane-slot descriptors, one thread per window (the
-// counts fit: rows <= 8 entries and <= WD_MAXREC records were checked for wd,
-// and <= 31 rows of <= 255 records stay below WD_MAXREL)
-__global__ void k_plan_pdesc(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
-                             const int64_t* __restrict__ lptr, const int32_t* __restrict__ rowstart, int64_t nwin,
-                             int32_t E, int4* __restrict__ phdr, int2* __restrict__ pdesc) {
+// pair-window headers, one thread per window
+__global__ void k_plan_phdr(const int64_t* __restrict__ affptr, const int64_t* __restrict__ lptr,
+                            const int32_t* __restrict__ rowstart, int64_t nwin, int4* __restrict__ phdr) {
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
     const int r0 = rowstart[w], r1 = rowstart[w + 1];
+    const int64_t lb = lptr[r0];
+    phdr[w] = make_int4((int)lb, (int)affptr[r0], (int)(lptr[r1] - lb), r0);
+  }
+}
+// lane-slot descriptors, one thread per row (row i lies in window
+// lptr[i] / S2: rows whose first lane slot lies in [w S2, (w+1) S2)); the
+// counts fit: <= 8 entries and <= WD_MAXREC records per row, and <= 31 rows
+// per window keep the first record relative to the window below WD_MAXREL
+__global__ void k_plan_pdesc(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
+                             const int64_t* __restrict__ lptr, const int32_t* __restrict__ rowstart, int64_t nF,
+                             int32_t S2, int32_t E, int2* __restrict__ pdesc) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l0 = lptr[i], l1 = lptr[i + 1];
+    const int r0 = rowstart[l0 / S2];
     const int64_t lb = lptr[r0], rec = affptr[r0];
-    phdr[w] = make_int4((int)lb, (int)rec, (int)(lptr[r1] - lb), (int)wptr[r0]);
-    for (int i = r0; i < r1; ++i) {
-      const int64_t l0 = lptr[i], l1 = lptr[i + 1];
-      const int64_t len = wptr[i + 1] - wptr[i];
-      const int64_t rc = affptr[i + 1] - affptr[i], rs = affptr[i] - rec;
-      const uint32_t d = (uint32_t)(l0 - lb) | ((uint32_t)(len - 1) << 5) | ((uint32_t)rc << 8) | ((uint32_t)rs << 16);
-      for (int64_t l = l0; l < l1; ++l) pdesc[l] = make_int2((int)(wptr[i] + E * (l - l0)), (int)d);
-    }
+    const int64_t len = wptr[i + 1] - wptr[i];
+    const int64_t rc = affptr[i + 1] - affptr[i], rs = affptr[i] - rec;
+    const uint32_t d = (uint32_t)(l0 - lb) | ((uint32_t)(len - 1) << 5) | ((uint32_t)rc << 8) | ((uint32_t)rs << 16);
+    for (int64_t l = l0; l < l1; ++l) pdesc[l] = make_int2((int)(wptr[i] + E * (l - l0)), (int)d);
   }
 }
 
@@ -972,60 +1155,55 @@ static inline int select_fast_path(emin_ctx c) {
   cudaMemsetAsync(p.ent + c->nnzAFF, 0, sizeof(SpEnt) * WP_PAD, s);
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
-  int32_t* wd_ok = nullptr;      // descriptors fit (read back below)
-  {
-    // window headers + lane descriptors of k_spgemm_wd (k_spgemm_win2 if a
-    // window's counts do not fit the descriptor)
-    int32_t* dok = nullptr;
-    if (emin_mallocAsync((void**)&p.whdr, sizeof(int4) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess ||
-        emin_mallocAsync((void**)&p.wdesc, sizeof(uint32_t) * std::max<int64_t>(c->nnzW, 1), s) != cudaSuccess ||
-        emin_mallocAsync((void**)&dok, sizeof(int32_t), s) != cudaSuccess)
-      return 0;
-    cudaMemsetAsync(dok, 0xFF, sizeof(int32_t), s);        // nonzero: the descriptors fit
-    k_plan_wdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.whdr, p.wdesc, dok);
-    c->launches += 1;
-    wd_ok = dok;
-  }
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
   k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent);
   c->launches += 2;
-  // lane slots of the pair-lane kernel (k_spgemm_wp)
+  // lane slots of the pair-lane kernel (k_spgemm_wp) and the longest record run
   int64_t* lscr = nullptr;
+  int32_t* dmaxrc = nullptr;
   if (emin_mallocAsync((void**)&p.lptr, sizeof(int64_t) * (c->nF + 1), s) != cudaSuccess ||
-      emin_mallocAsync((void**)&lscr, sizeof(int64_t) * emin_scan_scratch_elems(c->nF + 1), s) != cudaSuccess)
+      emin_mallocAsync((void**)&lscr, sizeof(int64_t) * emin_scan_scratch_elems(c->nF + 1), s) != cudaSuccess ||
+      emin_mallocAsync((void**)&dmaxrc, sizeof(int32_t), s) != cudaSuccess)
     return 0;
-  k_plan_lane_count<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, 2, p.lptr);   // two entries per lane
+  cudaMemsetAsync(dmaxrc, 0, sizeof(int32_t), s);
+  k_plan_lane_count<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, c->nF, 2, p.lptr, dmaxrc);   // two entries per lane
   if (emin_scan_i64(p.lptr, p.lptr, c->nF, p.lptr + c->nF, lscr, s) != cudaSuccess) return 0;
   c->launches += 4;
-  {
-    int64_t hbuf[2] = {0, 0};        // {descriptors fit, lane slots}
-    cudaMemcpyAsync(&hbuf[0], wd_ok, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&hbuf[1], p.lptr + c->nF, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    cudaFreeAsync(wd_ok, s);
-    cudaFreeAsync(lscr, s);
-    if (!(int32_t)(hbuf[0] & 0xffffffff)) {
-      cudaFreeAsync(p.whdr, s);
-      cudaFreeAsync(p.wdesc, s);
-      p.whdr = nullptr;
-      p.wdesc = nullptr;
-    } else {
-      // pair windows: rows whose first lane slot lies in [w S2, (w+1) S2)
-      const int32_t S2 = std::min(31, 33 - (c->max_row + 1) / 2);
-      const int64_t L = hbuf[1];
-      p.npwin = (L + S2 - 1) / S2;
-      if (emin_mallocAsync((void**)&p.prowstart, sizeof(int32_t) * (p.npwin + 1), s) != cudaSuccess ||
-          emin_mallocAsync((void**)&p.phdr, sizeof(int4) * std::max<int64_t>(p.npwin, 1), s) != cudaSuccess ||
-          emin_mallocAsync((void**)&p.pdesc, sizeof(int2) * std::max<int64_t>(L, 1), s) != cudaSuccess)
+  int64_t hL = 0;
+  int32_t hmaxrc = 0;
+  cudaMemcpyAsync(&hmaxrc, dmaxrc, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&hL, p.lptr + c->nF, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaFreeAsync(lscr, s);
+  cudaFreeAsync(dmaxrc, s);
+  if (hmaxrc <= (int32_t)WD_MAXREC) {
+    // pair windows: rows whose first lane slot lies in [w S2, (w+1) S2)
+    const int32_t S2 = std::min(31, 33 - (c->max_row + 1) / 2);
+    p.npwin = (hL + S2 - 1) / S2;
+    if (emin_mallocAsync((void**)&p.prowstart, sizeof(int32_t) * (p.npwin + 1), s) != cudaSuccess ||
+        emin_mallocAsync((void**)&p.phdr, sizeof(int4) * std::max<int64_t>(p.npwin, 1), s) != cudaSuccess ||
+        emin_mallocAsync((void**)&p.pdesc, sizeof(int2) * std::max<int64_t>(hL, 1), s) != cudaSuccess)
+      return 0;
+    k_plan_rowstart<<<SM * 8, 256, 0, s>>>(p.lptr, c->nF, S2, p.npwin, p.prowstart);
+    k_plan_phdr<<<SM * 4, 256, 0, s>>>(c->affptr, p.lptr, p.prowstart, p.npwin, p.phdr);
+    k_plan_pdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.lptr, p.prowstart, c->nF, S2, 2, p.pdesc);
+    c->launches += 3;
+    if (c->opts.debug_flags & EMIN_DBG_AB2) {
+      // window headers + lane descriptors of k_spgemm_wd, the one-entry-per-
+      // lane reference (its counts fit whenever the pair plan's do)
+      int32_t* dok = nullptr;
+      if (emin_mallocAsync((void**)&p.whdr, sizeof(int4) * std::max<int64_t>(p.nwin, 1), s) != cudaSuccess ||
+          emin_mallocAsync((void**)&p.wdesc, sizeof(uint32_t) * std::max<int64_t>(c->nnzW, 1), s) != cudaSuccess ||
+          emin_mallocAsync((void**)&dok, sizeof(int32_t), s) != cudaSuccess)
         return 0;
-      k_plan_rowstart<<<SM * 8, 256, 0, s>>>(p.lptr, c->nF, S2, p.npwin, p.prowstart);
-      k_plan_pdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.lptr, p.prowstart, p.npwin, 2, p.phdr, p.pdesc);
-      c->launches += 2;
+      k_plan_wdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.rowstart, p.nwin, p.whdr, p.wdesc, dok);
+      cudaFreeAsync(dok, s);
+      c->launches += 1;
     }
   }
   // the staged tile kernel (setup / energy modes) is needed only without the
   // window descriptors (or as the test reference, debug bit 256)
-  if (p.whdr && !(c->opts.debug_flags & 256)) return 1;
+  if ((p.phdr || p.whdr) && !(c->opts.debug_flags & 256)) return 1;
   // tile plan for the staged setup / energy kernel
   const int ST = TILE_E - c->max_row + 1;
   p.ntiles = (c->nnzW + ST - 1) / ST;
@@ -1094,6 +1272,7 @@ static inline const int32_t* scalar_iter_windows(emin_ctx c, int64_t* nwin) {
 // window-descriptor kernel's, else the tile kernel's (or win2m's)
 static inline int scalar_spgemm_grid(emin_ctx c) {
   const ScalarPlan& p = fast_of(c)->sc;
+  if (p.phdr && !(c->opts.debug_flags & (256 | EMIN_DBG_AB2))) return scalar_iter_launch_grid(c);
   if (p.whdr && !(c->opts.debug_flags & 256)) return scalar_iter_grid(c);
   return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
 }
@@ -1114,6 +1293,17 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
                                                                           (int32_t)p.nwin, X, out, c->partials);
     else
       k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+    return true;
+  }
+  if (p.phdr && !(c->opts.debug_flags & (256 | EMIN_DBG_AB2))) {
+    const int g = scalar_iter_launch_grid(c);
+    const int np = (int)p.npwin;
+    if (mode == MM_R0E)
+      k_spgemm_wpm<MM_R0E><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials);
+    else if (mode == MM_R0)
+      k_spgemm_wpm<MM_R0><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials);
+    else
+      k_spgemm_wpm<MM_ENERGY><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials);
     return true;
   }
   if (p.whdr && !(c->opts.debug_flags & 256)) {
@@ -1153,7 +1343,10 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
 static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double* B, const int64_t* frow,
                                       const double* what, unsigned long long* counters, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
-  if (p.whdr)
+  if (p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))
+    k_alg2_nv1_wp<<<(int)std::max<int64_t>(1, std::min<int64_t>((p.npwin + 7) / 8, (int64_t)emin_num_sms() * 8)), 256,
+                    0, s>>>(c->view(), p.phdr, p.pdesc, (int32_t)p.npwin, Bc, B, frow, what, c->Q, c->w0, counters);
+  else if (p.whdr)
     k_alg2_nv1_wd<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.whdr, p.wdesc, (int32_t)p.nwin, Bc, B, frow, what,
                                                  c->Q, c->w0, counters);
   else
