@@ -22,6 +22,7 @@ emin_setup only its own rows of A, P and B (partition.rank_slice).
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import platform
@@ -91,8 +92,13 @@ def cpu_model():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region.
+    The sampler process is started before the warm-up (its start-up -- NVML
+    initialisation -- must not fall inside the timed region) and keeps
+    sampling every 50 ms; summary() keeps the samples whose timestamps lie
+    in the timed region (mark_begin / mark_end), falling back to all samples
+    if the region was shorter than the sampling period."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -100,15 +106,31 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.gpu = gpu_index
         self.p = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
         return self
+
+    def wait_first(self, timeout=10.0):
+        """block until the sampler has written its first line"""
+        t = time.time()
+        while self.p is not None and time.time() - t < timeout:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                return
+            time.sleep(0.02)
+
+    def mark_begin(self):
+        self.t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        self.t1 = datetime.datetime.now()
 
     def __exit__(self, *a):
         if self.p is not None:
@@ -120,18 +142,27 @@ class ClockSampler:
 
     def summary(self):
         self.f.flush()
-        self.f.seek(0)
-        rows = [l.strip().split(",") for l in self.f.read().splitlines() if l.strip()]
-        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9]
+        with open(self.f.name) as fh:
+            rows = [l.strip().split(",") for l in fh.read().splitlines() if l.strip()]
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 10]
+
+        def ts(r):
+            try:
+                return datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f")
+            except ValueError:
+                return None
+        inside = [r for r in rows if self.t0 and self.t1 and ts(r) and self.t0 <= ts(r) <= self.t1]
+        rows = inside or rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        rows = [r[1:] for r in rows]
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[j] for r in rows for j in range(4) if r[5 + j].lower() == "active"})
         loaded = [s for s in sm if s > 0.5 * smax] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
-                "reasons": reasons, "samples": len(rows),
+                "reasons": reasons, "samples": len(rows), "samples_in_region": len(inside),
                 "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()),
                                    default=None)}
 
@@ -313,7 +344,7 @@ def dry_run(args, world, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("EMIN_BENCH_CONFIG", "3"))
     ap.add_argument("--size", type=int, default=None, help="reduced generator size (tests only; not a bench line)")
@@ -422,9 +453,14 @@ def main():
             stats["scalar_ms"] += kt["scalar"][0]
         E.emin_destroy(h)
 
+    # the clock sampler starts before the warm-up (its start-up stays out of
+    # the timed region; only samples inside the region are summarised)
+    clk = ClockSampler(local_rank)
+    clk.__enter__()
     # warm-up (untimed)
     for _ in range(args.warmup):
         step(dev, out_dev, True)
+    clk.wait_first()
     stats.update(launches=0, spgemm_ms=0.0, spgemm_n=0, stage_ms=[0.0, 0.0], scalar_ms=0.0, k_done=[])
 
     def barrier():
@@ -445,12 +481,14 @@ def main():
     barrier()
     torch.cuda.synchronize()
     nprof = args.steps if args.profile_steps <= 0 else min(args.profile_steps, args.steps)
-    with ClockSampler(local_rank) as clk:
-        ev0.record(stream)
-        for it in range(args.steps):
-            step(dev, out_dev, it >= args.steps - nprof)
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    clk.mark_begin()
+    ev0.record(stream)
+    for it in range(args.steps):
+        step(dev, out_dev, it >= args.steps - nprof)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark_end()
+    clk.__exit__(None, None, None)
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches_timed = stats["launches"]
