@@ -95,23 +95,26 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region.
     The sampler process is started before the warm-up (its start-up -- NVML
     initialisation -- must not fall inside the timed region) and keeps
-    sampling every 50 ms; summary() keeps the samples whose timestamps lie
+    sampling every 200 ms (the profiling recipe's period); summary() keeps the samples whose timestamps lie
     in the timed region (mark_begin / mark_end), falling back to all samples
     if the region was shorter than the sampling period."""
     Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index=0):
+    def __init__(self, gpu_index=0, period_ms=200):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.gpu = gpu_index
+        self.period = int(period_ms)
         self.p = None
         self.t0 = self.t1 = None
 
     def __enter__(self):
+        if self.period <= 0:          # diagnostics only (--clock-ms 0): no sampler
+            return self
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                       "--format=csv,noheader,nounits", "-lms", str(self.period)],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -345,6 +348,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--clock-ms", type=int, default=200,
+                    help="nvidia-smi sampling period during the timed region (0: no sampler, diagnostics only)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("EMIN_BENCH_CONFIG", "3"))
     ap.add_argument("--size", type=int, default=None, help="reduced generator size (tests only; not a bench line)")
@@ -455,7 +460,7 @@ def main():
 
     # the clock sampler starts before the warm-up (its start-up stays out of
     # the timed region; only samples inside the region are summarised)
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(local_rank, args.clock_ms)
     clk.__enter__()
     # warm-up (untimed)
     for _ in range(args.warmup):
@@ -482,12 +487,17 @@ def main():
     torch.cuda.synchronize()
     nprof = args.steps if args.profile_steps <= 0 else min(args.profile_steps, args.steps)
     clk.mark_begin()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev0.record(stream)
+    evs[0].record(stream)
     for it in range(args.steps):
         step(dev, out_dev, it >= args.steps - nprof)
+        evs[it + 1].record(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     clk.mark_end()
+    per = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+    log(f"[bench] rank {rank}: per-step ms min {per[0]:.3f} median {per[len(per) // 2]:.3f} max {per[-1]:.3f}")
     clk.__exit__(None, None, None)
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))

@@ -113,6 +113,9 @@ typedef struct {
 #define EMIN_DBG_FORCE_GENERIC 1   /* generic warp-per-row kernels instead of the scalar / nodal
                                       specialisations (the reference the fast paths are tested
                                       against) */
+#define EMIN_DBG_UNSCALED 512      /* scalar Jacobi path: the CG vectors in the original variables
+                                      (z = r / d by division, per-entry row gathers of d) instead of
+                                      the symmetrically scaled ones (D^-1/2 A D^-1/2 records) */
 #define EMIN_DBG_AB2 128           /* scalar path: the per-iteration masked product with one W
                                       entry per lane (k_spgemm_wd) instead of two (k_spgemm_wp) */
 #define EMIN_DBG_NO_R0E 2          /* r0 and E0 by two masked passes instead of the fused one */

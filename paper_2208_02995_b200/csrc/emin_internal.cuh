@@ -113,6 +113,11 @@ struct emin_ctx_s {
   int32_t* erow = nullptr;     // F-row id of every W entry (streaming stages)
   int32_t* adiag = nullptr;    // position of A(i,i) in A_FF row i (setup: the record plan)
   double* dinv = nullptr;      // 1 / A(i,i) per owned F row
+  // symmetric Jacobi scaling (scalar path, one GPU, Jacobi without the
+  // post-projection): the CG runs on r~ = S r, y~ = S^-1 y, dW~ = S^-1 dW with
+  // S = D^-1/2 and the records D^-1/2 A_FF D^-1/2, so z~ = r~
+  int32_t sym = 0;
+  double* srow = nullptr;      // S = 1 / sqrt(A(i,i)) per owned F row (sym)
   DistPlan* dist = nullptr;    // multi-GPU halo plan (dist.cu), null on one GPU
   SgsPlan* sgs = nullptr;      // SGS preconditioner plan (sgs.cu), null for Jacobi
   int breakdown_reported = 0;

@@ -245,6 +245,110 @@ k_stage2_v(DevView v, const int32_t* __restrict__ erow, const double* __restrict
   }
 }
 
+// ---- the same two stages under the symmetric Jacobi scaling (ctx sym):
+// z~ = S D^-1 r = S r = r~, so gamma = r~.r~ and y~ = r~ + beta y~ are plain
+// streams with no row ids and no division (24 and 40 bytes per W entry).
+__global__ void __launch_bounds__(256, 4)
+k_stage1_s(DevView v, double* __restrict__ r, const double* __restrict__ yb, double* __restrict__ partials) {
+  __shared__ double sh[32];
+  const DevState* st = v.st;
+  if (st->stopped) return;
+  const int pend = st->pend;
+  const double ap = st->alpha_pend;
+  const int64_t np = v.nnzW >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* yb2 = reinterpret_cast<const double2*>(yb);
+  double part = 0.0;
+  const bool rev = v.pingpong && (st->k_total & 1);   // L2 ping-pong (see k_stage1_v)
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += 2 * stride) {
+    double2 rv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < np) {
+        const int64_t pp = rev ? np - 1 - p : p;
+        rv[u] = r2[pp];
+        if (pend) {
+          const double2 b = yb2[pp];
+          rv[u].x = rv[u].x - ap * b.x;
+          rv[u].y = rv[u].y - ap * b.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t p = p0 + u * stride;
+      if (p < np) {
+        if (pend) r2[rev ? np - 1 - p : p] = rv[u];
+        part = fma(rv[u].x, rv[u].x, part);
+        part = fma(rv[u].y, rv[u].y, part);
+      }
+    }
+  }
+  if ((v.nnzW & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t e = v.nnzW - 1;
+    double x = r[e];
+    if (pend) { x = x - ap * yb[e]; r[e] = x; }
+    part = fma(x, x, part);
+  }
+  const double tot = block_sum(part, sh);
+  block_partial_out(v, partials, tot, sh, 0);
+}
+
+__global__ void __launch_bounds__(256, 4)
+k_stage2_s(DevView v, const double* __restrict__ r, double* __restrict__ y, double* __restrict__ dw) {
+  const DevState* st = v.st;
+  const int stopped = st->stopped;
+  const int pendw = st->pendw;
+  if (stopped && !pendw) return;
+  const double ap = st->alpha_pend;
+  const double beta = st->beta;
+  const bool first = (st->k_total == 0);
+  const int64_t np = v.nnzW >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double2* y2 = reinterpret_cast<double2*>(y);
+  double2* dw2 = reinterpret_cast<double2*>(dw);
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  const bool rev = v.pingpong && !(st->k_total & 1);   // opposite to stage I (L2 ping-pong)
+  for (int64_t p1 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p1 < np; p1 += stride) {
+    const int64_t p = rev ? np - 1 - p1 : p1;
+    const double2 yo = y2[p];
+    if (pendw) {
+      double2 d = dw2[p];
+      d.x = d.x + ap * yo.x;
+      d.y = d.y + ap * yo.y;
+      dw2[p] = d;
+    }
+    if (!stopped) {
+      const double2 rv = r2[p];
+      double2 yn;
+      yn.x = first ? rv.x : rv.x + beta * yo.x;
+      yn.y = first ? rv.y : rv.y + beta * yo.y;
+      y2[p] = yn;
+    }
+  }
+  if ((v.nnzW & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t e = v.nnzW - 1;
+    const double yo = y[e];
+    if (pendw) dw[e] = dw[e] + ap * yo;
+    if (!stopped) y[e] = first ? r[e] : r[e] + beta * yo;
+  }
+}
+
+// x_e *= s(row(e)) (r~ = S r0 at setup / reset)
+__global__ void k_scale_rows(double* __restrict__ x, const int32_t* __restrict__ erow,
+                             const double* __restrict__ srow, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    x[e] = x[e] * srow[erow[e]];
+}
+// out = w0 + S dW~ (W under the symmetric scaling, for the energy pass)
+__global__ void k_wsum_s(const double* __restrict__ w0, const double* __restrict__ dw, const int32_t* __restrict__ erow,
+                         const double* __restrict__ srow, int64_t n, double* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = w0[e] + srow[erow[e]] * dw[e];
+}
+
 __global__ void k_recip(const double* __restrict__ d, int64_t n, double* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = 1.0 / d[i];
@@ -428,6 +532,13 @@ void launch_stage2_g(emin_ctx c, cudaStream_t s) {
     k_stage2<G, false><<<c->grid_rows, 256, 0, s>>>(v, c->r, c->y, c->dw);
 }
 void launch_stage(emin_ctx c, int which, cudaStream_t s) {
+  if (c->sym) {
+    if (which == 1)
+      k_stage1_s<<<c->grid_rows, 256, 0, s>>>(c->view(), c->r, c->yb, c->partials);
+    else
+      k_stage2_s<<<c->grid_rows, 256, 0, s>>>(c->view(), c->r, c->y, c->dw);
+    return;
+  }
   if (!c->opts.project_after_jacobi) {
     if (which == 1)
       k_stage1_v<<<c->grid_rows, 256, 0, s>>>(c->view(), c->erow, c->dinv, c->r, c->yb, c->partials);
@@ -529,6 +640,7 @@ emin_status emin_plan(emin_ctx c) {
   c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF * c->group + 255) / 256, (int64_t)SM * 8));
   c->grid_spgemm = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF + 7) / 8, (int64_t)SM * 8));
   c->kernel_path = select_fast_path(c);
+  if (c->kernel_path != 1) c->sym = 0;        // the scaled records exist on the scalar path only
   if (c->kernel_path == 0 && (c->opts.row_begin % 3) == 0) {
     NodalPlan* np = nullptr;
     if (select_nodal_path(c, np)) {
@@ -541,9 +653,12 @@ emin_status emin_plan(emin_ctx c) {
     // entry-parallel streaming stages: row id per W entry
     EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->erow, sizeof(int32_t) * std::max<int64_t>(c->nnzW, 1), c->stream));
     k_build_erow<<<SM * 8, 256, 0, c->stream>>>(c->wptr, c->nF, c->erow);
-    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->dinv, sizeof(double) * std::max<int64_t>(c->nF, 1), c->stream));
-    k_recip<<<SM * 4, 256, 0, c->stream>>>(c->d, c->nF, c->dinv);
-    c->launches += 2;
+    c->launches += 1;
+    if (!c->sym) {            // the unscaled stages' exact quotient r / d
+      EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->dinv, sizeof(double) * std::max<int64_t>(c->nF, 1), c->stream));
+      k_recip<<<SM * 4, 256, 0, c->stream>>>(c->d, c->nF, c->dinv);
+      c->launches += 1;
+    }
     // one wave (4 CTAs of 256 per SM, the launch bound): config 3 stage I/II
     // 39.3 / 51.0 -> 38.3 / 48.6 us, config 4 60.4 / 84.5 -> 59.5 / 82.3 us,
     // config 5 neutral
@@ -631,6 +746,10 @@ emin_status emin_finish_r0(emin_ctx c) {
   if (g < 0) {
     emin_launch_masked(c, MM_R0, c->w0, nullptr, c->r, s);
     g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, s);
+  }
+  if (c->sym) {                                   // r~ = S r0 (symmetric Jacobi scaling)
+    k_scale_rows<<<emin_num_sms() * 8, 256, 0, s>>>(c->r, c->erow, c->srow, c->nnzW);
+    c->launches += 1;
   }
   std::pair<const double*, int> red;
   {
@@ -910,7 +1029,12 @@ extern "C" emin_status emin_energy(emin_ctx c, double* E) {
     if (st != EMIN_OK) return st;
   }
   int g;
-  if (c->kernel_path == 2 && !c->dist) {
+  if (c->sym) {
+    // W = W0 + S dW~ once into the (free after the flush) y^ buffer
+    k_wsum_s<<<emin_num_sms() * 8, 256, 0, c->stream>>>(c->w0, c->dw, c->erow, c->srow, c->nnzW, c->yb);
+    c->launches += 1;
+    g = emin_launch_masked(c, MM_ENERGY, c->yb, nullptr, nullptr, c->stream);
+  } else if (c->kernel_path == 2 && !c->dist) {
     // nodal path: W = W0 + dW once into the (free after the flush) y^ buffer,
     // so the energy pass gathers one vector instead of two (same sums; on the
     // scalar path the extra pass costs what it saves: 10.13 vs 10.15 ms/step)
@@ -1032,7 +1156,7 @@ void emin_free_all(emin_ctx c) {
   cudaStream_t s = c->stream;
   void* ptrs[] = {c->wptr, c->affptr, c->afcptr, c->pofs, c->cofs, c->isc_own, c->wcol, c->affcol,
                   c->afccol, c->affval, c->afcval, c->d, c->Q, c->w0, c->dw, c->r, c->r0, c->y,
-                  c->yb, c->partials, c->dE_hist, c->st, c->erow, c->dinv, c->adiag};
+                  c->yb, c->partials, c->dE_hist, c->st, c->erow, c->dinv, c->adiag, c->srow};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   free_fast_path(c);

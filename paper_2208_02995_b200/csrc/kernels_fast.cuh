@@ -36,6 +36,7 @@ struct SpEnt {          // 16 bytes, one per A_FF entry
 struct TileHdr;
 struct ScalarPlan {
   SpEnt* ent = nullptr;
+  SpEnt* entS = nullptr;         // the records of D^-1/2 A_FF D^-1/2 (ctx sym; per-iteration product)
   int32_t* rowstart = nullptr;   // [nwin + 1]
   int4* whdr = nullptr;          // [nwin] {first W entry, first record, entries, first row} (k_spgemm_wd)
   uint32_t* wdesc = nullptr;     // [nnzW] lane descriptor (k_spgemm_wd)
@@ -834,7 +835,8 @@ k_alg2_nv1_wd(DevView v, const int4* __restrict__ whdr, const uint32_t* __restri
 // P out on the window plan
 __global__ void __launch_bounds__(256)
 k_get_P_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const double* __restrict__ w0,
-            const double* __restrict__ dw, const int64_t* __restrict__ pofs, double* __restrict__ out) {
+            const double* __restrict__ dw, const int64_t* __restrict__ pofs, double* __restrict__ out,
+            const double* __restrict__ srow) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -845,7 +847,8 @@ k_get_P_win(DevView v, const int32_t* __restrict__ rowstart, int64_t nwin, const
     const WinLane L = decode_window(v.wptr, r0, nrows, lane);
     if (L.act) {
       const int64_t e = L.base + lane;
-      out[pofs[r0 + L.rloc] + L.pos] = w0[e] + dw[e];
+      // dW = S dW~ under the symmetric scaling
+      out[pofs[r0 + L.rloc] + L.pos] = w0[e] + (srow ? srow[r0 + L.rloc] * dw[e] : dw[e]);
     }
   }
 }
@@ -1052,7 +1055,8 @@ __global__ void k_plan_wdesc(const int64_t* __restrict__ wptr, const int64_t* __
 }
 
 // one group of 8 lanes per F row, lane per A_FF entry (setup only)
-__global__ void k_plan_entries(DevView v, const int32_t* __restrict__ adiag, SpEnt* __restrict__ ent) {
+__global__ void k_plan_entries(DevView v, const int32_t* __restrict__ adiag, SpEnt* __restrict__ ent,
+                               const double* __restrict__ srow, SpEnt* __restrict__ entS) {
   const int lg = threadIdx.x & 7;
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 3;
@@ -1089,6 +1093,10 @@ __global__ void k_plan_entries(DevView v, const int32_t* __restrict__ adiag, SpE
       e.ybase = (int32_t)kb;
       e.pm = pm;
       ent[dst] = e;
+      if (entS) {                                 // a~(i,k) = (A(i,k) s_i) s_k
+        e.a = (e.a * srow[i]) * srow[k];
+        entS[dst] = e;
+      }
     }
   }
 }
@@ -1133,6 +1141,12 @@ __global__ void k_plan_pdesc(const int64_t* __restrict__ wptr, const int64_t* __
   }
 }
 
+// s_i = 1 / sqrt(A(i,i)) (symmetric Jacobi scaling)
+__global__ void k_rsqrt(const double* __restrict__ d, int64_t n, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = 1.0 / sqrt(d[i]);
+}
+
 // ---- host side ------------------------------------------------------------
 struct FastPaths {
   ScalarPlan sc;
@@ -1155,8 +1169,20 @@ static inline int select_fast_path(emin_ctx c) {
   cudaMemsetAsync(p.ent + c->nnzAFF, 0, sizeof(SpEnt) * WP_PAD, s);
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
+  // symmetric Jacobi scaling of the CG (see emin_ctx_s::sym): one GPU,
+  // Jacobi without the post-projection
+  c->sym = (!c->dist && c->opts.precond == EMIN_PREC_JACOBI && !c->opts.project_after_jacobi &&
+            !(c->opts.debug_flags & EMIN_DBG_UNSCALED)) ? 1 : 0;
+  if (c->sym) {
+    if (emin_mallocAsync((void**)&c->srow, sizeof(double) * std::max<int64_t>(c->nF, 1), s) != cudaSuccess ||
+        emin_mallocAsync((void**)&p.entS, sizeof(SpEnt) * (size_t)(c->nnzAFF + WP_PAD), s) != cudaSuccess)
+      return 0;
+    cudaMemsetAsync(p.entS + c->nnzAFF, 0, sizeof(SpEnt) * WP_PAD, s);
+    k_rsqrt<<<SM * 4, 256, 0, s>>>(c->d, c->nF, c->srow);
+    c->launches += 1;
+  }
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
-  k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent);
+  k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent, c->srow, p.entS);
   c->launches += 2;
   // lane slots of the pair-lane kernel (k_spgemm_wp) and the longest record run
   int64_t* lscr = nullptr;
@@ -1285,14 +1311,15 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
     // vs wd's 110.6 and win2's 120.2, profiles/r02/spgemm_ab_c3.txt); wd is
     // the A/B reference (EMIN_DBG_AB2); win2 when a window's counts overflow
     // the lane descriptor
+    const SpEnt* rec = c->sym ? p.entS : p.ent;        // D^-1/2 A_FF D^-1/2 under the scaling
     if (p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))
       k_spgemm_wp<WP_NT, WP_MINB, WP_UNR, 2><<<scalar_iter_launch_grid(c), WP_NT, 0, s>>>(
-          v, p.ent, p.phdr, p.pdesc, (int32_t)p.npwin, X, out, c->partials);
+          v, rec, p.phdr, p.pdesc, (int32_t)p.npwin, X, out, c->partials);
     else if (p.whdr)
-      k_spgemm_wd<WD_NT, WD_LA, true><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc,
+      k_spgemm_wd<WD_NT, WD_LA, true><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, rec, p.whdr, p.wdesc,
                                                                           (int32_t)p.nwin, X, out, c->partials);
     else
-      k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
+      k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, rec, p.rowstart, p.nwin, X, out, c->partials);
     return true;
   }
   if (p.phdr && !(c->opts.debug_flags & (256 | EMIN_DBG_AB2))) {
@@ -1355,7 +1382,8 @@ static inline void launch_scalar_alg2(emin_ctx c, const double* Bc, const double
 }
 static inline void launch_scalar_get_P(emin_ctx c, double* out, cudaStream_t s) {
   const ScalarPlan& p = fast_of(c)->sc;
-  k_get_P_win<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->w0, c->dw, c->pofs, out);
+  k_get_P_win<<<scalar_grid(c), 256, 0, s>>>(c->view(), p.rowstart, p.nwin, c->w0, c->dw, c->pofs, out,
+                                             c->sym ? c->srow : nullptr);
 }
 
 static inline void free_fast_path(emin_ctx c) {
@@ -1369,6 +1397,7 @@ static inline void free_fast_path(emin_ctx c) {
   if (f->sc.phdr) cudaFreeAsync(f->sc.phdr, c->stream);
   if (f->sc.pdesc) cudaFreeAsync(f->sc.pdesc, c->stream);
   if (f->sc.ent) cudaFreeAsync(f->sc.ent, c->stream);
+  if (f->sc.entS) cudaFreeAsync(f->sc.entS, c->stream);
   if (f->sc.hdr) cudaFreeAsync(f->sc.hdr, c->stream);
   delete f;
   c->fast = nullptr;

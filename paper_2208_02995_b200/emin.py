@@ -46,6 +46,8 @@ class emin_opts(C.Structure):
 # emin_opts.debug_flags bits (include/emin.h): alternative kernel paths for tests / A/B
 DBG_FORCE_GENERIC, DBG_NO_R0E, DBG_SGS_GENERIC, DBG_TRACE, DBG_FUSE_SCALARS, DBG_ALG2_ROWS = 1, 2, 4, 8, 16, 32
 DBG_AB1 = 64
+DBG_AB2 = 128
+DBG_UNSCALED = 512
 GALERKIN_DEVICE, GALERKIN_POINT = 1, 2
 
 

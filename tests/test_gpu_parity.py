@@ -624,6 +624,36 @@ def test_sgs_sorted_nodal_sweeps_equal_unsorted(name, size, k):
     assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3]
 
 
+@pytest.mark.parametrize("name,size,k", [("3", 12, 25), ("3", 17, 40), ("2b", 10, 30), ("1b", None, 20),
+                                         ("1", None, 20), ("2", 12, 30)])
+def test_symmetric_scaling_agrees(name, size, k):
+    """The scalar Jacobi path runs the CG on the symmetrically scaled vectors
+    (r~ = S r, y~ = S^-1 y, dW~ = S^-1 dW, records of S A_FF S, S = D^-1/2),
+    where z~ = r~ needs no division (default), or in the original variables
+    (EMIN_DBG_UNSCALED): the same iterates up to round-off -- steps taken,
+    dE, E and P agree within the parity tolerances."""
+    from paper_2208_02995_b200 import Emin
+    from paper_2208_02995_b200.emin import DBG_UNSCALED
+    from workloads.problems import make_config
+    prob = make_config(name, size=size)
+    a = Emin.from_problem(prob)
+    b = Emin.from_problem(prob, debug_flags=DBG_UNSCALED)
+    assert a.report()["kernel_path"] == b.report()["kernel_path"] == 1
+    ka, dEa = a.iterate(k)
+    kb, dEb = b.iterate(k)
+    assert ka == kb
+    if len(dEb):
+        assert np.allclose(dEa, dEb, rtol=1e-8, atol=1e-12 * abs(dEb[0]))
+    assert abs(a.energy() - b.energy()) <= 1e-11 * abs(b.energy())
+    Pa, Pb = a.get_P(), b.get_P()
+    assert np.abs(Pa - Pb).max() <= 1e-9 * np.abs(Pb).max()
+    # composability holds in the scaled variables too
+    c = Emin.from_problem(prob)
+    k1, _ = c.iterate(k // 3)
+    k2, _ = c.iterate(k - k // 3)
+    assert k1 + k2 == ka and c.energy() == a.energy() and np.array_equal(c.get_P(), Pa)
+
+
 @pytest.mark.parametrize("name,size", [("3", 12), ("3", 17), ("2b", 10), ("1b", None), ("3", 24)])
 def test_scalar_pair_kernel_agrees(name, size):
     """The per-iteration masked product with two W entries per lane
