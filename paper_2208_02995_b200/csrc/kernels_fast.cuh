@@ -308,7 +308,7 @@ constexpr int WP_PAD = 4;      // records allocated past nnz(A_FF) (k_spgemm_wp'
 // twice: 95.2; 1024 x 2 (32 registers) 97.8-99.1; 768 x 2 96.3-98.5; four
 // entries per lane 122-155
 constexpr int WP_NT = 512, WP_MINB = 3, WP_UNR = 2;
-template <int NT = WD_NT, int MINB = 2048 / NT, int UNR = 1, int E = 2>
+template <int NT = WD_NT, int MINB = 2048 / NT, int UNR = 1, int E = 2, bool SYM = false>
 __global__ void __launch_bounds__(NT, MINB)
 k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phdr, const int2* __restrict__ pdesc,
             int32_t nwin, const double* __restrict__ X, double* __restrict__ out, double* __restrict__ partials) {
@@ -344,10 +344,17 @@ k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phd
     if (act) {
       const int qb = h.y + (int)(dsc >> 16);
       const int qe = qb + (int)((dsc >> 8) & 255u);
-      const double ad = __ldg(Ad + 2 * qb);            // record qb: the diagonal A(i,i), own y entries
+      if (SYM) {
+        // S A_FF S: unit diagonal, the records hold the off-diagonal terms
 #pragma unroll
-      for (int j = 0; j < E; ++j)
-        if (p0 + j < rowlen) acc[j] = ad * X[e0 + j];
+        for (int j = 0; j < E; ++j)
+          if (p0 + j < rowlen) acc[j] = X[e0 + j];
+      } else {
+        const double ad = __ldg(Ad + 2 * qb);          // record qb: the diagonal A(i,i), own y entries
+#pragma unroll
+        for (int j = 0; j < E; ++j)
+          if (p0 + j < rowlen) acc[j] = ad * X[e0 + j];
+      }
       const unsigned shp = 4u * (unsigned)p0;
       // one 16-byte load per record {a, ybase, pm}, one record ahead (split
       // 8-byte loads of {ybase, pm} and a cost twice the L1 tag requests:
@@ -355,9 +362,10 @@ k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phd
       // records, so the look-ahead needs no bound check; an absent position
       // gathers nothing and adds a * 0 (the value of skipping the term, up
       // to the sign of a zero)
-      int4 nxt = __ldg(A4 + qb + 1);
+      const int q0 = SYM ? qb : qb + 1;
+      int4 nxt = __ldg(A4 + q0);
 #pragma unroll UNR
-      for (int q = qb + 1; q < qe; ++q) {
+      for (int q = q0; q < qe; ++q) {
         const int4 cur = nxt;
         nxt = __ldg(A4 + q + 1);
         const unsigned pm = (unsigned)cur.w >> shp;    // positions past the row: 0xF
@@ -409,7 +417,7 @@ template <int MODE, int NT = WP_NT, int MINB = WP_MINB>
 __global__ void __launch_bounds__(NT, MINB)
 k_spgemm_wpm(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phdr, const int2* __restrict__ pdesc,
              int32_t nwin, const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
-             double* __restrict__ partials) {
+             double* __restrict__ partials, int32_t compact) {
   __shared__ double sh[32];
   __shared__ double s_qa[NT / 32][64];
   const int lane = threadIdx.x & 31;
@@ -437,8 +445,10 @@ k_spgemm_wpm(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ ph
     const int i = h.w + __popc(heads & ((2u << rowbeg) - 1u)) - 1;
     double acc0 = 0.0, acc1 = 0.0, fc0 = 0.0, fc1 = 0.0, xo0 = 0.0, xo1 = 0.0;
     if (act) {
-      const int qb = h.y + (int)(dsc >> 16);
-      const int qe = qb + (int)((dsc >> 8) & 255u);
+      // compact descriptors (symmetric scaling) count the diagonal-free
+      // records: row i's full run in A starts i records later, one longer
+      const int qb = h.y + (int)(dsc >> 16) + (compact ? i : 0);
+      const int qe = qb + (int)((dsc >> 8) & 255u) + (compact ? 1 : 0);
       const double ad = Ad[2 * qb];                    // diagonal record first
       xo0 = xval(e0);
       acc0 = ad * xo0;
@@ -1093,9 +1103,9 @@ __global__ void k_plan_entries(DevView v, const int32_t* __restrict__ adiag, SpE
       e.ybase = (int32_t)kb;
       e.pm = pm;
       ent[dst] = e;
-      if (entS) {                                 // a~(i,k) = (A(i,k) s_i) s_k
+      if (entS && q != qd) {          // a~(i,k) = (A(i,k) s_i) s_k, the diagonal left out
         e.a = (e.a * srow[i]) * srow[k];
-        entS[dst] = e;
+        entS[dst - i - 1] = e;        // row i's records start at affptr[i] - i
       }
     }
   }
@@ -1115,12 +1125,15 @@ __global__ void k_plan_lane_count(const int64_t* __restrict__ wptr, const int64_
   if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(maxrc, m);
 }
 // pair-window headers, one thread per window
+// (compact: the record offsets of the diagonal-free records, row i's at
+// affptr[i] - i, k_spgemm_wp<SYM>)
 __global__ void k_plan_phdr(const int64_t* __restrict__ affptr, const int64_t* __restrict__ lptr,
-                            const int32_t* __restrict__ rowstart, int64_t nwin, int4* __restrict__ phdr) {
+                            const int32_t* __restrict__ rowstart, int64_t nwin, int32_t compact,
+                            int4* __restrict__ phdr) {
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
     const int r0 = rowstart[w], r1 = rowstart[w + 1];
     const int64_t lb = lptr[r0];
-    phdr[w] = make_int4((int)lb, (int)affptr[r0], (int)(lptr[r1] - lb), r0);
+    phdr[w] = make_int4((int)lb, (int)(affptr[r0] - (compact ? r0 : 0)), (int)(lptr[r1] - lb), r0);
   }
 }
 // lane-slot descriptors, one thread per row (row i lies in window
@@ -1129,13 +1142,14 @@ __global__ void k_plan_phdr(const int64_t* __restrict__ affptr, const int64_t* _
 // per window keep the first record relative to the window below WD_MAXREL
 __global__ void k_plan_pdesc(const int64_t* __restrict__ wptr, const int64_t* __restrict__ affptr,
                              const int64_t* __restrict__ lptr, const int32_t* __restrict__ rowstart, int64_t nF,
-                             int32_t S2, int32_t E, int2* __restrict__ pdesc) {
+                             int32_t S2, int32_t E, int32_t compact, int2* __restrict__ pdesc) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t l0 = lptr[i], l1 = lptr[i + 1];
     const int r0 = rowstart[l0 / S2];
-    const int64_t lb = lptr[r0], rec = affptr[r0];
+    const int64_t lb = lptr[r0], rec = affptr[r0] - (compact ? r0 : 0);
     const int64_t len = wptr[i + 1] - wptr[i];
-    const int64_t rc = affptr[i + 1] - affptr[i], rs = affptr[i] - rec;
+    const int64_t rc = affptr[i + 1] - affptr[i] - (compact ? 1 : 0);
+    const int64_t rs = affptr[i] - (compact ? i : 0) - rec;
     const uint32_t d = (uint32_t)(l0 - lb) | ((uint32_t)(len - 1) << 5) | ((uint32_t)rc << 8) | ((uint32_t)rs << 16);
     for (int64_t l = l0; l < l1; ++l) pdesc[l] = make_int2((int)(wptr[i] + E * (l - l0)), (int)d);
   }
@@ -1169,21 +1183,6 @@ static inline int select_fast_path(emin_ctx c) {
   cudaMemsetAsync(p.ent + c->nnzAFF, 0, sizeof(SpEnt) * WP_PAD, s);
   const int SM = emin_num_sms();
   k_plan_rowstart<<<SM * 8, 256, 0, s>>>(c->wptr, c->nF, p.S, p.nwin, p.rowstart);
-  // symmetric Jacobi scaling of the CG (see emin_ctx_s::sym): one GPU,
-  // Jacobi without the post-projection
-  c->sym = (!c->dist && c->opts.precond == EMIN_PREC_JACOBI && !c->opts.project_after_jacobi &&
-            !(c->opts.debug_flags & EMIN_DBG_UNSCALED)) ? 1 : 0;
-  if (c->sym) {
-    if (emin_mallocAsync((void**)&c->srow, sizeof(double) * std::max<int64_t>(c->nF, 1), s) != cudaSuccess ||
-        emin_mallocAsync((void**)&p.entS, sizeof(SpEnt) * (size_t)(c->nnzAFF + WP_PAD), s) != cudaSuccess)
-      return 0;
-    cudaMemsetAsync(p.entS + c->nnzAFF, 0, sizeof(SpEnt) * WP_PAD, s);
-    k_rsqrt<<<SM * 4, 256, 0, s>>>(c->d, c->nF, c->srow);
-    c->launches += 1;
-  }
-  // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
-  k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent, c->srow, p.entS);
-  c->launches += 2;
   // lane slots of the pair-lane kernel (k_spgemm_wp) and the longest record run
   int64_t* lscr = nullptr;
   int32_t* dmaxrc = nullptr;
@@ -1194,7 +1193,7 @@ static inline int select_fast_path(emin_ctx c) {
   cudaMemsetAsync(dmaxrc, 0, sizeof(int32_t), s);
   k_plan_lane_count<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, c->nF, 2, p.lptr, dmaxrc);   // two entries per lane
   if (emin_scan_i64(p.lptr, p.lptr, c->nF, p.lptr + c->nF, lscr, s) != cudaSuccess) return 0;
-  c->launches += 4;
+  c->launches += 5;
   int64_t hL = 0;
   int32_t hmaxrc = 0;
   cudaMemcpyAsync(&hmaxrc, dmaxrc, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
@@ -1202,6 +1201,24 @@ static inline int select_fast_path(emin_ctx c) {
   cudaStreamSynchronize(s);
   cudaFreeAsync(lscr, s);
   cudaFreeAsync(dmaxrc, s);
+  const bool pair_ok = hmaxrc <= (int32_t)WD_MAXREC;
+  // symmetric Jacobi scaling of the CG (see emin_ctx_s::sym): one GPU,
+  // Jacobi without the post-projection, on the pair-lane kernel; its records
+  // of S A_FF S leave out the diagonal ((S A S)_ii = 1: s_i = A(i,i)^-1/2)
+  c->sym = (pair_ok && !c->dist && c->opts.precond == EMIN_PREC_JACOBI && !c->opts.project_after_jacobi &&
+            !(c->opts.debug_flags & (EMIN_DBG_UNSCALED | EMIN_DBG_AB2))) ? 1 : 0;
+  if (c->sym) {
+    const int64_t nS = c->nnzAFF - c->nF;
+    if (emin_mallocAsync((void**)&c->srow, sizeof(double) * std::max<int64_t>(c->nF, 1), s) != cudaSuccess ||
+        emin_mallocAsync((void**)&p.entS, sizeof(SpEnt) * (size_t)(nS + WP_PAD), s) != cudaSuccess)
+      return 0;
+    cudaMemsetAsync(p.entS + nS, 0, sizeof(SpEnt) * WP_PAD, s);
+    k_rsqrt<<<SM * 4, 256, 0, s>>>(c->d, c->nF, c->srow);
+    c->launches += 1;
+  }
+  // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
+  k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent, c->srow, p.entS);
+  c->launches += 1;
   if (hmaxrc <= (int32_t)WD_MAXREC) {
     // pair windows: rows whose first lane slot lies in [w S2, (w+1) S2)
     const int32_t S2 = std::min(31, 33 - (c->max_row + 1) / 2);
@@ -1211,8 +1228,8 @@ static inline int select_fast_path(emin_ctx c) {
         emin_mallocAsync((void**)&p.pdesc, sizeof(int2) * std::max<int64_t>(hL, 1), s) != cudaSuccess)
       return 0;
     k_plan_rowstart<<<SM * 8, 256, 0, s>>>(p.lptr, c->nF, S2, p.npwin, p.prowstart);
-    k_plan_phdr<<<SM * 4, 256, 0, s>>>(c->affptr, p.lptr, p.prowstart, p.npwin, p.phdr);
-    k_plan_pdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.lptr, p.prowstart, c->nF, S2, 2, p.pdesc);
+    k_plan_phdr<<<SM * 4, 256, 0, s>>>(c->affptr, p.lptr, p.prowstart, p.npwin, c->sym, p.phdr);
+    k_plan_pdesc<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, p.lptr, p.prowstart, c->nF, S2, 2, c->sym, p.pdesc);
     c->launches += 3;
     if (c->opts.debug_flags & EMIN_DBG_AB2) {
       // window headers + lane descriptors of k_spgemm_wd, the one-entry-per-
@@ -1311,26 +1328,31 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
     // vs wd's 110.6 and win2's 120.2, profiles/r02/spgemm_ab_c3.txt); wd is
     // the A/B reference (EMIN_DBG_AB2); win2 when a window's counts overflow
     // the lane descriptor
-    const SpEnt* rec = c->sym ? p.entS : p.ent;        // D^-1/2 A_FF D^-1/2 under the scaling
-    if (p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))
+    if (c->sym)          // S A_FF S (unit diagonal) on the pair windows
+      k_spgemm_wp<WP_NT, WP_MINB, WP_UNR, 2, true><<<scalar_iter_launch_grid(c), WP_NT, 0, s>>>(
+          v, p.entS, p.phdr, p.pdesc, (int32_t)p.npwin, X, out, c->partials);
+    else if (p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))
       k_spgemm_wp<WP_NT, WP_MINB, WP_UNR, 2><<<scalar_iter_launch_grid(c), WP_NT, 0, s>>>(
-          v, rec, p.phdr, p.pdesc, (int32_t)p.npwin, X, out, c->partials);
+          v, p.ent, p.phdr, p.pdesc, (int32_t)p.npwin, X, out, c->partials);
     else if (p.whdr)
-      k_spgemm_wd<WD_NT, WD_LA, true><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, rec, p.whdr, p.wdesc,
+      k_spgemm_wd<WD_NT, WD_LA, true><<<scalar_iter_grid(c), WD_NT, 0, s>>>(v, p.ent, p.whdr, p.wdesc,
                                                                           (int32_t)p.nwin, X, out, c->partials);
     else
-      k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, rec, p.rowstart, p.nwin, X, out, c->partials);
+      k_spgemm_win2<2><<<scalar_grid(c), 256, 0, s>>>(v, p.ent, p.rowstart, p.nwin, X, out, c->partials);
     return true;
   }
   if (p.phdr && !(c->opts.debug_flags & (256 | EMIN_DBG_AB2))) {
     const int g = scalar_iter_launch_grid(c);
     const int np = (int)p.npwin;
     if (mode == MM_R0E)
-      k_spgemm_wpm<MM_R0E><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials);
+      k_spgemm_wpm<MM_R0E><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials,
+                                              c->sym);
     else if (mode == MM_R0)
-      k_spgemm_wpm<MM_R0><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials);
+      k_spgemm_wpm<MM_R0><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials,
+                                              c->sym);
     else
-      k_spgemm_wpm<MM_ENERGY><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials);
+      k_spgemm_wpm<MM_ENERGY><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials,
+                                              c->sym);
     return true;
   }
   if (p.whdr && !(c->opts.debug_flags & 256)) {

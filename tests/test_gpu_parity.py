@@ -664,7 +664,8 @@ def test_scalar_pair_kernel_agrees(name, size):
     from paper_2208_02995_b200 import Emin
     from workloads.problems import make_config
     prob = make_config(name, size=size)
-    a = Emin.from_problem(prob)
+    # both in the unscaled variables (EMIN_DBG_AB2 implies them)
+    a = Emin.from_problem(prob, debug_flags=512)
     b = Emin.from_problem(prob, debug_flags=128)
     assert a.report()["kernel_path"] == b.report()["kernel_path"] == 1
     ka, dEa = a.iterate(20)
