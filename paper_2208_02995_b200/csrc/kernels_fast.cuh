@@ -308,6 +308,10 @@ constexpr int WP_PAD = 4;      // records allocated past nnz(A_FF) (k_spgemm_wp'
 // twice: 95.2; 1024 x 2 (32 registers) 97.8-99.1; 768 x 2 96.3-98.5; four
 // entries per lane 122-155
 constexpr int WP_NT = 512, WP_MINB = 3, WP_UNR = 2;
+// the unit-diagonal (scaled) instance: 512 x 4 per SM, 31 registers, loop not
+// unrolled: 85.2-85.4 us vs 87.1-87.3 at 512 x 3 / unroll 2 (config 3;
+// 1024 x 2 / unroll 1 the same 85.2-85.3, 256 x 6..8 and 768 x 2 85.6-88.6)
+constexpr int WPS_NT = 512, WPS_MINB = 4, WPS_UNR = 1;
 template <int NT = WD_NT, int MINB = 2048 / NT, int UNR = 1, int E = 2, bool SYM = false>
 __global__ void __launch_bounds__(NT, MINB)
 k_spgemm_wp(DevView v, const SpEnt* __restrict__ A, const int4* __restrict__ phdr, const int2* __restrict__ pdesc,
@@ -1300,6 +1304,9 @@ static inline int scalar_iter_grid(emin_ctx c) {
 static inline int scalar_iter_launch_grid(emin_ctx c) {
   const ScalarPlan& p = fast_of(c)->sc;
   if (!(p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))) return scalar_iter_grid(c);
+  if (c->sym)
+    return (int)std::max<int64_t>(1, std::min<int64_t>((p.npwin + WPS_NT / 32 - 1) / (WPS_NT / 32),
+                                                       (int64_t)emin_num_sms() * WPS_MINB));
   return (int)std::max<int64_t>(1, std::min<int64_t>((p.npwin + WP_NT / 32 - 1) / (WP_NT / 32),
                                                      (int64_t)emin_num_sms() * WP_MINB));
 }
@@ -1315,7 +1322,9 @@ static inline const int32_t* scalar_iter_windows(emin_ctx c, int64_t* nwin) {
 // window-descriptor kernel's, else the tile kernel's (or win2m's)
 static inline int scalar_spgemm_grid(emin_ctx c) {
   const ScalarPlan& p = fast_of(c)->sc;
-  if (p.phdr && !(c->opts.debug_flags & (256 | EMIN_DBG_AB2))) return scalar_iter_launch_grid(c);
+  if (p.phdr && !(c->opts.debug_flags & (256 | EMIN_DBG_AB2)))      // k_spgemm_wpm: 512 x 3 per SM
+    return (int)std::max<int64_t>(1, std::min<int64_t>((p.npwin + WP_NT / 32 - 1) / (WP_NT / 32),
+                                                       (int64_t)emin_num_sms() * WP_MINB));
   if (p.whdr && !(c->opts.debug_flags & 256)) return scalar_iter_grid(c);
   return p.use_tiles ? (int)std::max<int64_t>(1, p.ntiles) : scalar_grid(c);
 }
@@ -1329,7 +1338,7 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
     // the A/B reference (EMIN_DBG_AB2); win2 when a window's counts overflow
     // the lane descriptor
     if (c->sym)          // S A_FF S (unit diagonal) on the pair windows
-      k_spgemm_wp<WP_NT, WP_MINB, WP_UNR, 2, true><<<scalar_iter_launch_grid(c), WP_NT, 0, s>>>(
+      k_spgemm_wp<WPS_NT, WPS_MINB, WPS_UNR, 2, true><<<scalar_iter_launch_grid(c), WPS_NT, 0, s>>>(
           v, p.entS, p.phdr, p.pdesc, (int32_t)p.npwin, X, out, c->partials);
     else if (p.phdr && !(c->opts.debug_flags & EMIN_DBG_AB2))
       k_spgemm_wp<WP_NT, WP_MINB, WP_UNR, 2><<<scalar_iter_launch_grid(c), WP_NT, 0, s>>>(
@@ -1342,7 +1351,7 @@ static inline bool launch_scalar_masked(emin_ctx c, int mode, const double* X, c
     return true;
   }
   if (p.phdr && !(c->opts.debug_flags & (256 | EMIN_DBG_AB2))) {
-    const int g = scalar_iter_launch_grid(c);
+    const int g = scalar_spgemm_grid(c);
     const int np = (int)p.npwin;
     if (mode == MM_R0E)
       k_spgemm_wpm<MM_R0E><<<g, WP_NT, 0, s>>>(v, p.ent, p.phdr, p.pdesc, np, X, X2, out, c->partials,
