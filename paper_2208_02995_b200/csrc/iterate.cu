@@ -1024,15 +1024,20 @@ static void flush(emin_ctx c) {
 extern "C" emin_status emin_energy(emin_ctx c, double* E) {
   if (!c || !E) return EMIN_ERR_ARG;
   flush(c);
-  if (c->dist) {
+  if (c->dist && !c->sym) {
     emin_status st = emin_dist_halo_values(c, c->dw, c->stream);   // W = W0 + dW on the halo rows
     if (st != EMIN_OK) return st;
   }
   int g;
   if (c->sym) {
-    // W = W0 + S dW~ once into the (free after the flush) y^ buffer
+    // W = W0 + S dW~ once into the (free after the flush) y^ buffer; on
+    // several GPUs its halo rows from their owners
     k_wsum_s<<<emin_num_sms() * 8, 256, 0, c->stream>>>(c->w0, c->dw, c->erow, c->srow, c->nnzW, c->yb);
     c->launches += 1;
+    if (c->dist) {
+      emin_status st = emin_dist_halo_values(c, c->yb, c->stream);
+      if (st != EMIN_OK) return st;
+    }
     g = emin_launch_masked(c, MM_ENERGY, c->yb, nullptr, nullptr, c->stream);
   } else if (c->kernel_path == 2 && !c->dist) {
     // nodal path: W = W0 + dW once into the (free after the flush) y^ buffer,

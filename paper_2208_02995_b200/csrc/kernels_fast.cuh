@@ -26,6 +26,7 @@
 #include "emin_internal.cuh"
 #include "masked.cuh"
 #include "bulk.cuh"
+#include "dist.cuh"
 
 struct SpEnt {          // 16 bytes, one per A_FF entry
   double a;
@@ -1165,6 +1166,19 @@ __global__ void k_rsqrt(const double* __restrict__ d, int64_t n, double* __restr
     out[i] = 1.0 / sqrt(d[i]);
 }
 
+// x_e = d(row(e)) over the owned W entries, thread per row
+__global__ void k_spread_rows(const int64_t* __restrict__ wptr, const double* __restrict__ d, int64_t nF,
+                              double* __restrict__ x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = wptr[i]; e < wptr[i + 1]; ++e) x[e] = d[i];
+}
+// s of the halo rows [nF, nFh) from their exchanged first W entry
+__global__ void k_halo_rsqrt(const int64_t* __restrict__ wptr, const double* __restrict__ dW, int64_t nF,
+                             int64_t nFh, double* __restrict__ srow) {
+  for (int64_t i = nF + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nFh; i += (int64_t)gridDim.x * blockDim.x)
+    srow[i] = 1.0 / sqrt(dW[wptr[i]]);
+}
+
 // ---- host side ------------------------------------------------------------
 struct FastPaths {
   ScalarPlan sc;
@@ -1198,6 +1212,8 @@ static inline int select_fast_path(emin_ctx c) {
   k_plan_lane_count<<<SM * 8, 256, 0, s>>>(c->wptr, c->affptr, c->nF, 2, p.lptr, dmaxrc);   // two entries per lane
   if (emin_scan_i64(p.lptr, p.lptr, c->nF, p.lptr + c->nF, lscr, s) != cudaSuccess) return 0;
   c->launches += 5;
+  // several GPUs: every rank takes the same branch below (collectives follow)
+  if (c->dist && emin_dist_allreduce_max_i32(c, dmaxrc, s) != EMIN_OK) return 0;
   int64_t hL = 0;
   int32_t hmaxrc = 0;
   cudaMemcpyAsync(&hmaxrc, dmaxrc, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
@@ -1209,16 +1225,29 @@ static inline int select_fast_path(emin_ctx c) {
   // symmetric Jacobi scaling of the CG (see emin_ctx_s::sym): one GPU,
   // Jacobi without the post-projection, on the pair-lane kernel; its records
   // of S A_FF S leave out the diagonal ((S A S)_ii = 1: s_i = A(i,i)^-1/2)
-  c->sym = (pair_ok && !c->dist && c->opts.precond == EMIN_PREC_JACOBI && !c->opts.project_after_jacobi &&
+  c->sym = (pair_ok && c->opts.precond == EMIN_PREC_JACOBI && !c->opts.project_after_jacobi &&
             !(c->opts.debug_flags & (EMIN_DBG_UNSCALED | EMIN_DBG_AB2))) ? 1 : 0;
   if (c->sym) {
     const int64_t nS = c->nnzAFF - c->nF;
-    if (emin_mallocAsync((void**)&c->srow, sizeof(double) * std::max<int64_t>(c->nF, 1), s) != cudaSuccess ||
+    if (emin_mallocAsync((void**)&c->srow, sizeof(double) * std::max<int64_t>(c->nFh, 1), s) != cudaSuccess ||
         emin_mallocAsync((void**)&p.entS, sizeof(SpEnt) * (size_t)(nS + WP_PAD), s) != cudaSuccess)
       return 0;
     cudaMemsetAsync(p.entS + nS, 0, sizeof(SpEnt) * WP_PAD, s);
     k_rsqrt<<<SM * 4, 256, 0, s>>>(c->d, c->nF, c->srow);
     c->launches += 1;
+    if (c->dist) {
+      // s of the halo rows (their A(i,i) live on the owners): A(i,i) spread
+      // over the owned W entries, the halo exchange of W values, then read
+      // back at each halo row's first entry
+      double* dW = nullptr;
+      if (emin_mallocAsync((void**)&dW, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s) != cudaSuccess) return 0;
+      cudaStreamSynchronize(s);       // the peers copy into it from their streams
+      k_spread_rows<<<SM * 8, 256, 0, s>>>(c->wptr, c->d, c->nF, dW);
+      if (emin_dist_halo_values(c, dW, s) != EMIN_OK) return 0;
+      k_halo_rsqrt<<<SM * 4, 256, 0, s>>>(c->wptr, dW, c->nF, c->nFh, c->srow);
+      cudaFreeAsync(dW, s);
+      c->launches += 2;
+    }
   }
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
   k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent, c->srow, p.entS);
