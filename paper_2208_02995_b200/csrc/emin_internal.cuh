@@ -117,7 +117,8 @@ struct emin_ctx_s {
   // post-projection): the CG runs on r~ = S r, y~ = S^-1 y, dW~ = S^-1 dW with
   // S = D^-1/2 and the records D^-1/2 A_FF D^-1/2, so z~ = r~
   int32_t sym = 0;
-  double* srow = nullptr;      // S = 1 / sqrt(A(i,i)) per owned F row (sym)
+  double* srow = nullptr;      // S = 1 / sqrt(A(i,i)) per owned (+ halo) F row (sym)
+  double* affvalS = nullptr;   // S A_FF S in A_FF's layout (sym on the nodal path)
   DistPlan* dist = nullptr;    // multi-GPU halo plan (dist.cu), null on one GPU
   SgsPlan* sgs = nullptr;      // SGS preconditioner plan (sgs.cu), null for Jacobi
   int breakdown_reported = 0;

@@ -450,7 +450,7 @@ __global__ void k_energy_out(const double* __restrict__ partials, int np, double
 }
 
 __global__ void k_get_P(DevView v, const double* __restrict__ w0, const double* __restrict__ dw,
-                        const int64_t* __restrict__ pofs, double* __restrict__ out) {
+                        const int64_t* __restrict__ pofs, double* __restrict__ out, const double* __restrict__ srow) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -458,7 +458,21 @@ __global__ void k_get_P(DevView v, const double* __restrict__ w0, const double* 
     const int64_t b = v.wptr[i];
     const int nj = (int)(v.wptr[i + 1] - b);
     const int64_t o = pofs[i];
-    for (int t = lane; t < nj; t += 32) out[o + t] = w0[b + t] + dw[b + t];
+    const double si = srow ? srow[i] : 1.0;          // dW = S dW~ under the symmetric scaling
+    for (int t = lane; t < nj; t += 32) out[o + t] = w0[b + t] + (srow ? si * dw[b + t] : dw[b + t]);
+  }
+}
+// S A_FF S in A_FF's layout, warp per owned F row, lanes over its entries
+// (nodal path, sym)
+__global__ void k_scale_aff(const int64_t* __restrict__ affptr, const int32_t* __restrict__ affcol,
+                            const double* __restrict__ affval, const double* __restrict__ srow, int64_t nF,
+                            double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < nF; i += nw) {
+    const double si = srow[i];
+    for (int64_t q = affptr[i] + lane; q < affptr[i + 1]; q += 32) out[q] = (affval[q] * si) * srow[affcol[q]];
   }
 }
 __global__ void k_get_P_crows(int64_t m, const uint8_t* __restrict__ isc, const int64_t* __restrict__ prp,
@@ -640,7 +654,10 @@ emin_status emin_plan(emin_ctx c) {
   c->grid_rows = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF * c->group + 255) / 256, (int64_t)SM * 8));
   c->grid_spgemm = (int)std::max<int64_t>(1, std::min<int64_t>((c->nF + 7) / 8, (int64_t)SM * 8));
   c->kernel_path = select_fast_path(c);
-  if (c->kernel_path != 1) c->sym = 0;        // the scaled records exist on the scalar path only
+  if (c->kernel_path != 1 && c->sym) {        // the scaled records exist on the scalar path only
+    c->sym = 0;
+    if (c->srow) { cudaFreeAsync(c->srow, c->stream); c->srow = nullptr; }
+  }
   if (c->kernel_path == 0 && (c->opts.row_begin % 3) == 0) {
     NodalPlan* np = nullptr;
     if (select_nodal_path(c, np)) {
@@ -649,6 +666,19 @@ emin_status emin_plan(emin_ctx c) {
     }
   }
   if (c->kernel_path == 1) c->grid_spgemm = scalar_spgemm_grid(c);
+  if (c->kernel_path == 2 && c->opts.precond == EMIN_PREC_JACOBI && !c->opts.project_after_jacobi &&
+      !(c->opts.debug_flags & EMIN_DBG_UNSCALED)) {
+    // symmetric Jacobi scaling on the nodal path: the per-iteration product
+    // reads S A_FF S (a scaled copy of A_FF's values); the stages, r0, P and
+    // the energy as on the scalar path
+    c->sym = 1;
+    emin_status sst = emin_build_srow(c);
+    if (sst != EMIN_OK) return sst;
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->affvalS, sizeof(double) * std::max<int64_t>(c->nnzAFF, 1),
+                                      c->stream));
+    k_scale_aff<<<SM * 16, 256, 0, c->stream>>>(c->affptr, c->affcol, c->affval, c->srow, c->nF, c->affvalS);
+    c->launches += 1;
+  }
   if (!c->opts.project_after_jacobi) {
     // entry-parallel streaming stages: row id per W entry
     EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->erow, sizeof(int32_t) * std::max<int64_t>(c->nnzW, 1), c->stream));
@@ -1074,7 +1104,7 @@ extern "C" emin_status emin_get_P(emin_ctx c, double* P_val) {
   if (c->kernel_path == 1)
     launch_scalar_get_P(c, out, c->stream);
   else
-    k_get_P<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->w0, c->dw, c->pofs, out);
+    k_get_P<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->w0, c->dw, c->pofs, out, c->sym ? c->srow : nullptr);
   k_get_P_crows<<<SM * 8, 256, 0, c->stream>>>(c->m_owned, c->isc_own, c->cofs, out);
   c->launches += 4;
   EMIN_CUDA_TRY(c, cudaGetLastError());
@@ -1161,7 +1191,7 @@ void emin_free_all(emin_ctx c) {
   cudaStream_t s = c->stream;
   void* ptrs[] = {c->wptr, c->affptr, c->afcptr, c->pofs, c->cofs, c->isc_own, c->wcol, c->affcol,
                   c->afccol, c->affval, c->afcval, c->d, c->Q, c->w0, c->dw, c->r, c->r0, c->y,
-                  c->yb, c->partials, c->dE_hist, c->st, c->erow, c->dinv, c->adiag, c->srow};
+                  c->yb, c->partials, c->dE_hist, c->st, c->erow, c->dinv, c->adiag, c->srow, c->affvalS};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   free_fast_path(c);

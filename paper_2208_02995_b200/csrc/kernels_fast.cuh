@@ -1180,6 +1180,30 @@ __global__ void k_halo_rsqrt(const int64_t* __restrict__ wptr, const double* __r
 }
 
 // ---- host side ------------------------------------------------------------
+// S = A(i,i)^-1/2 of the owned F rows and, on several GPUs, of the halo rows
+// (their A(i,i) live on the owners: spread over the owned W entries, sent by
+// the W-value halo exchange -- collective -- and read back at each halo
+// row's first entry)
+static emin_status emin_build_srow(emin_ctx c) {
+  cudaStream_t s = c->stream;
+  const int SM = emin_num_sms();
+  EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->srow, sizeof(double) * std::max<int64_t>(c->nFh, 1), s));
+  k_rsqrt<<<SM * 4, 256, 0, s>>>(c->d, c->nF, c->srow);
+  c->launches += 1;
+  if (c->dist) {
+    double* dW = nullptr;
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&dW, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s));
+    EMIN_CUDA_TRY(c, cudaStreamSynchronize(s));       // the peers copy into it from their streams
+    k_spread_rows<<<SM * 8, 256, 0, s>>>(c->wptr, c->d, c->nF, dW);
+    const emin_status st = emin_dist_halo_values(c, dW, s);
+    if (st != EMIN_OK) return st;
+    k_halo_rsqrt<<<SM * 4, 256, 0, s>>>(c->wptr, dW, c->nF, c->nFh, c->srow);
+    cudaFreeAsync(dW, s);
+    c->launches += 2;
+  }
+  return cudaGetLastError() == cudaSuccess ? EMIN_OK : EMIN_ERR_CUDA;
+}
+
 struct FastPaths {
   ScalarPlan sc;
 };
@@ -1229,25 +1253,9 @@ static inline int select_fast_path(emin_ctx c) {
             !(c->opts.debug_flags & (EMIN_DBG_UNSCALED | EMIN_DBG_AB2))) ? 1 : 0;
   if (c->sym) {
     const int64_t nS = c->nnzAFF - c->nF;
-    if (emin_mallocAsync((void**)&c->srow, sizeof(double) * std::max<int64_t>(c->nFh, 1), s) != cudaSuccess ||
-        emin_mallocAsync((void**)&p.entS, sizeof(SpEnt) * (size_t)(nS + WP_PAD), s) != cudaSuccess)
-      return 0;
+    if (emin_mallocAsync((void**)&p.entS, sizeof(SpEnt) * (size_t)(nS + WP_PAD), s) != cudaSuccess) return 0;
     cudaMemsetAsync(p.entS + nS, 0, sizeof(SpEnt) * WP_PAD, s);
-    k_rsqrt<<<SM * 4, 256, 0, s>>>(c->d, c->nF, c->srow);
-    c->launches += 1;
-    if (c->dist) {
-      // s of the halo rows (their A(i,i) live on the owners): A(i,i) spread
-      // over the owned W entries, the halo exchange of W values, then read
-      // back at each halo row's first entry
-      double* dW = nullptr;
-      if (emin_mallocAsync((void**)&dW, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), s) != cudaSuccess) return 0;
-      cudaStreamSynchronize(s);       // the peers copy into it from their streams
-      k_spread_rows<<<SM * 8, 256, 0, s>>>(c->wptr, c->d, c->nF, dW);
-      if (emin_dist_halo_values(c, dW, s) != EMIN_OK) return 0;
-      k_halo_rsqrt<<<SM * 4, 256, 0, s>>>(c->wptr, dW, c->nF, c->nFh, c->srow);
-      cudaFreeAsync(dW, s);
-      c->launches += 2;
-    }
+    if (emin_build_srow(c) != EMIN_OK) return 0;
   }
   // short in-order CTAs (kernel-plan phase 0.45 -> 0.37 ms on config 3)
   k_plan_entries<<<SM * 32, 256, 0, s>>>(c->view(), c->adiag, p.ent, c->srow, p.entS);

@@ -539,7 +539,8 @@ static inline void nd_v2_nv(int nv, int mode, const DevView& v, const NodalPlan*
 
 static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const double* X, const double* X2,
                                 double* out, cudaStream_t s) {
-  const DevView v = c->view();
+  DevView v = c->view();
+  if (mode == MM_ITER && c->sym) v.affval = c->affvalS;   // S A_FF S (symmetric Jacobi scaling)
   const int g = nodal_grid(c, p);
   // v2 with two blocks per round (all gathers of both issued before the
   // FMAs; config 5 20.7 -> 15.9 ms, config 4 471 -> 420 us; three or four per
