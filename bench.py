@@ -462,9 +462,22 @@ def main():
     # the timed region; only samples inside the region are summarised)
     clk = ClockSampler(local_rank, args.clock_ms)
     clk.__enter__()
-    # warm-up (untimed)
-    for _ in range(args.warmup):
-        step(dev, out_dev, True)
+    # warm-up (untimed): the W requested steps, then -- only while the last
+    # steps are not yet steady (a box just freed by a large process was seen
+    # to run every step 3.5x slower for ~0.5 s) -- up to 40 more, about 0.3 s
+    # of extra warm-up at most on config 3
+    wt = []
+    for w_i in range(args.warmup + (40 if world == 1 else 0)):    # ranks step in lockstep (collectives)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        step(dev, out_dev, w_i < args.warmup)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        wt.append(ea.elapsed_time(eb))
+        if w_i + 1 >= args.warmup and len(wt) >= 4 and max(wt[-3:]) <= 1.2 * min(wt[1:]):
+            break
+    if len(wt) > args.warmup:
+        log(f"[bench] rank {rank}: {len(wt) - args.warmup} extra warm-up steps until steady ({wt[-1]:.2f} ms)")
     clk.wait_first()
     stats.update(launches=0, spgemm_ms=0.0, spgemm_n=0, stage_ms=[0.0, 0.0], scalar_ms=0.0, k_done=[])
 
@@ -496,8 +509,13 @@ def main():
     ev1.record(stream)
     torch.cuda.synchronize()
     clk.mark_end()
-    per = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
-    log(f"[bench] rank {rank}: per-step ms min {per[0]:.3f} median {per[len(per) // 2]:.3f} max {per[-1]:.3f}")
+    seq = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    per = sorted(seq)
+    step_stats = {"min": per[0], "median": per[len(per) // 2], "max": per[-1],
+                  "above_1p5x_median": sum(t > 1.5 * per[len(per) // 2] for t in seq)}
+    log(f"[bench] rank {rank}: per-step ms min {per[0]:.3f} median {per[len(per) // 2]:.3f} max {per[-1]:.3f}; "
+        f"steps above 1.5x median: {sum(t > 1.5 * per[len(per) // 2] for t in seq)}")
+    log("[bench] per-step ms: " + " ".join(f"{t:.2f}" for t in seq))
     clk.__exit__(None, None, None)
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
@@ -682,7 +700,8 @@ def main():
                    f"sgs ({args.sgs_key} order, {rep['sgs_levels']} levels per sweep)",
                    "start": args.start,
                    "halo_rank0": {"rows": rep["n_halo_rows"], "entries": rep["n_halo_entries"],
-                                  "sent_entries": rep["n_send_entries"]} if world > 1 else None},
+                                  "sent_entries": rep["n_send_entries"]} if world > 1 else None,
+                   "step_ms_rank0": step_stats},
         "roofline": roofline,
         "iter_only": {"value": nnzW_global * k_eff / (it_ms_med / 1e3) if k_eff else 0.0, "unit": UNIT,
                       "ms_per_iter": it_ms_med / max(k_eff, 1),
