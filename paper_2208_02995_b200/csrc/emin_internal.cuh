@@ -30,6 +30,8 @@ struct DevState {
   double red[4];      // multi-GPU: rank-local sums [0] gamma, [1] y.yb, [2] energy
   double redg[4];     // ... and their sums over the ranks (allreduce red -> redg)
   uint32_t ctr[2];    // fused scalar steps: blocks done in stage I [0] / SpGEMM [1]
+  double sum_cc;      // sum of A(c,c) over the C rows (all ranks; Eq. trInc), set at setup
+  unsigned long long cnt[3];   // setup counters: SVD-branch rows, frozen rows, max-vol failures
 };
 
 struct DistPlan;
@@ -130,8 +132,7 @@ struct emin_ctx_s {
   double *dE_hist = nullptr;
   int64_t dE_cap = 0;
   DevState* st = nullptr;
-  double sum_diag_cc = 0.0;
-  int64_t n_svd = 0, n_frozen = 0, n_crows = 0, n_maxvol_fail = 0;
+  int64_t n_crows = 0;         // (tr(A_CC) and the Alg. 2 counters live in DevState)
   // launch geometry
   int grid_rows = 0, grid_spgemm = 0, grid_red = 0;
   // graphs: one per k (cached)

@@ -426,13 +426,12 @@ __global__ void k_flush(DevView v, double* __restrict__ r, const double* __restr
 }
 __global__ void k_flush_done(DevState* st) { st->pend = 0; }
 
-__global__ void k_reset_state(DevState* st, const double* __restrict__ Epart, int np, double add,
-                              double tau, double stag) {
+__global__ void k_reset_state(DevState* st, const double* __restrict__ Epart, int np, double tau, double stag) {
   __shared__ double sh[32];
   const double e = reduce_partials(Epart, np, sh);
   if (threadIdx.x == 0) {
     st->gamma = st->gamma_old = st->beta = st->alpha_pend = st->den = st->dE1 = 0.0;
-    st->E0 = e + add;
+    st->E0 = e + st->sum_cc;
     st->tau = tau;
     st->stag = stag;
     st->k_total = 0;
@@ -443,10 +442,11 @@ __global__ void k_reset_state(DevState* st, const double* __restrict__ Epart, in
   }
 }
 
-__global__ void k_energy_out(const double* __restrict__ partials, int np, double add, double* out) {
+// (add: a device scalar added to the sum, or null)
+__global__ void k_energy_out(const double* __restrict__ partials, int np, const double* add, double* out) {
   __shared__ double sh[32];
   const double e = reduce_partials(partials, np, sh);
-  if (threadIdx.x == 0) *out = e + add;
+  if (threadIdx.x == 0) *out = add ? e + *add : e;
 }
 
 __global__ void k_get_P(DevView v, const double* __restrict__ w0, const double* __restrict__ dw,
@@ -758,7 +758,7 @@ static emin_status global_sum(emin_ctx c, int np, int slot, cudaStream_t s, std:
                               bool local_done = false) {
   if (!c->dist) { *res = {c->partials, np}; return EMIN_OK; }
   if (!local_done) {     // (fused: the producing kernel's last block wrote st->red[slot])
-    k_energy_out<<<1, 1024, 0, s>>>(c->partials, np, 0.0, &c->st->red[slot]);
+    k_energy_out<<<1, 1024, 0, s>>>(c->partials, np, nullptr, &c->st->red[slot]);
     c->launches += 1;
   }
   *res = {&c->st->redg[slot], -1};
@@ -786,7 +786,7 @@ emin_status emin_finish_r0(emin_ctx c) {
     emin_status st = global_sum(c, g, 2, s, &red);
     if (st != EMIN_OK) return st;
   }
-  k_reset_state<<<1, 1024, 0, s>>>(c->st, red.first, red.second, c->sum_diag_cc, c->opts.tau,
+  k_reset_state<<<1, 1024, 0, s>>>(c->st, red.first, red.second, c->opts.tau,
                                    c->opts.stagnation_rel);
   c->launches += 3;
   EMIN_CUDA_TRY(c, cudaGetLastError());
@@ -1086,7 +1086,7 @@ extern "C" emin_status emin_energy(emin_ctx c, double* E) {
     emin_status st = global_sum(c, g, 2, c->stream, &red);
     if (st != EMIN_OK) { cudaFreeAsync(dev, c->stream); return st; }
   }
-  k_energy_out<<<1, 1024, 0, c->stream>>>(red.first, red.second, c->sum_diag_cc, dev);
+  k_energy_out<<<1, 1024, 0, c->stream>>>(red.first, red.second, &c->st->sum_cc, dev);
   c->launches += 4;
   EMIN_CUDA_TRY(c, cudaMemcpyAsync(E, dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   cudaFreeAsync(dev, c->stream);
@@ -1131,8 +1131,8 @@ extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
   rep->dE1 = h.dE1;
   rep->k_total = h.k_total;
   rep->stop_reason = h.stopped;
-  rep->n_svd_rows = c->n_svd;
-  rep->n_frozen_rows = c->n_frozen;
+  rep->n_svd_rows = (int64_t)h.cnt[0];       // (Alg. 2 counters, kept on the device at setup)
+  rep->n_frozen_rows = (int64_t)h.cnt[1];
   rep->n_fine = c->nF;
   rep->nnz_W = c->nnzW;
   rep->nnz_AFF = c->nnzAFF;
@@ -1141,7 +1141,7 @@ extern "C" emin_status emin_report(emin_ctx c, emin_report_t* rep) {
   rep->launches = c->launches;
   rep->precond = c->opts.precond;
   rep->sgs_levels = emin_sgs_levels(c);
-  rep->n_maxvol_fail = c->n_maxvol_fail;
+  rep->n_maxvol_fail = (int64_t)h.cnt[2];
   rep->rank = c->rank;
   if (c->dist) {
     rep->n_halo_rows = c->dist->nH;

@@ -986,21 +986,19 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
 
   trace.mark(s, "Alg. 2");
   // ---- r0 = -Pi (A P0)|F and E0 = tr(P0^T A P0)
-  double h_sum_cc = 0.0;
-  SETUP_TRY(cudaMemcpyAsync(&h_sum_cc, dsum, sizeof(double), cudaMemcpyDeviceToHost, s));
-  unsigned long long h_cnt[3];
-  SETUP_TRY(cudaMemcpyAsync(h_cnt, counters, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
-  SETUP_TRY(cudaStreamSynchronize(s));
-  ctx->sum_diag_cc = h_sum_cc;
-  ctx->n_svd = (int64_t)h_cnt[0];
-  ctx->n_frozen = (int64_t)h_cnt[1];
-  ctx->n_maxvol_fail = (int64_t)h_cnt[2];
+  // tr(A_CC) and the Alg. 2 counters stay on the device (emin_report reads
+  // them; no host round trip here)
+  SETUP_TRY(cudaMemcpyAsync(&ctx->st->sum_cc, dsum, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  SETUP_TRY(cudaMemcpyAsync(ctx->st->cnt, counters, sizeof(unsigned long long) * 3, cudaMemcpyDeviceToDevice, s));
   // kernels enqueued above: coarse flags, 4 scans x 3, rows, check_B, fill, 2 reduce, alg2
   ctx->launches += 1 + 3 + 2 + (nF > 0 ? 9 : 0) + 1 + 2 + 1;
   emin_status st = emin_finish_r0(ctx);
   tmp_free();
   if (st != EMIN_OK) return fail(ctx, st, ctx->last_error);
-  SETUP_TRY(cudaStreamSynchronize(s));
+  // no final synchronisation: the caller's next call (the iteration graph's
+  // build, typically) overlaps the tail of the setup kernels; a fault in them
+  // surfaces at the next synchronising call
+  SETUP_TRY(cudaGetLastError());
   trace.mark(s, "r0, E0 (done)");
   *out = ctx;
   return EMIN_OK;
