@@ -24,7 +24,7 @@ struct DevState {
   double tau, stag;
   int64_t k_total;    // accepted steps since setup / reset
   int32_t stopped;    // 0 running, 1 gamma<=0, 2 den==0, 3 tau, 4 stagnation, 5 breakdown
-  int32_t pend;       // r -= alpha_pend yb pending (applied by stage I)
+  int32_t pend;       // r -= alpha_pend yb pending (applied by stage I); 1: with dw += alpha_pend y, 2: without
   int32_t pendw;      // dw += alpha_pend y pending (applied by stage II)
   int32_t k_call;     // accepted steps in the current emin_iterate call
   double red[4];      // multi-GPU: rank-local sums [0] gamma, [1] y.yb, [2] energy
@@ -121,6 +121,7 @@ struct emin_ctx_s {
   int32_t sym = 0;
   double* srow = nullptr;      // S = 1 / sqrt(A(i,i)) per owned (+ halo) F row (sym)
   double* affvalS = nullptr;   // S A_FF S in A_FF's layout (sym on the nodal path)
+  double* wtmp = nullptr;      // W = W0 + dW scratch of the energy pass (with the halo tail)
   DistPlan* dist = nullptr;    // multi-GPU halo plan (dist.cu), null on one GPU
   SgsPlan* sgs = nullptr;      // SGS preconditioner plan (sgs.cu), null for Jacobi
   int breakdown_reported = 0;
@@ -202,7 +203,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* >= 32 */) {
 // ---- the CG scalar steps (Alg. 3), applied by one thread
 // gamma = r.z; stop if gamma <= 0; beta = gamma / gamma_old
 __device__ __forceinline__ void scalar_gamma_apply(DevState* st, double g) {
-  st->pendw = st->pend;
+  st->pendw = st->pend == 1;           // pend 2: a flush already applied dw += alpha y
   st->pend = 0;
   if (!(g > 0.0)) { st->stopped = 1; return; }
   st->beta = (st->k_total == 0) ? 0.0 : g / st->gamma_old;

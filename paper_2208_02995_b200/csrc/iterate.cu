@@ -413,18 +413,19 @@ __global__ void k_wsum(const double* __restrict__ a, const double* __restrict__ 
     out[i] = a[i] + b[i];
 }
 
-__global__ void k_flush(DevView v, double* __restrict__ r, const double* __restrict__ yb,
-                        double* __restrict__ dw, const double* __restrict__ y) {
+// W = W0 + dW is read outside the loop (energy, P): apply a pending
+// dw += alpha y; the pending r -= alpha y^ stays with stage I (pend 1 -> 2),
+// so the flush moves 24 instead of 48 bytes per entry and a later
+// emin_iterate takes the same values in the same order
+__global__ void k_flush(DevView v, double* __restrict__ dw, const double* __restrict__ y) {
   const DevState* st = v.st;
-  if (!st->pend) return;
+  if (st->pend != 1) return;
   const double ap = st->alpha_pend;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.nnzW;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    r[p] = r[p] - ap * yb[p];
+       p += (int64_t)gridDim.x * blockDim.x)
     dw[p] = dw[p] + ap * y[p];
-  }
 }
-__global__ void k_flush_done(DevState* st) { st->pend = 0; }
+__global__ void k_flush_done(DevState* st) { if (st->pend == 1) st->pend = 2; }
 
 __global__ void k_reset_state(DevState* st, const double* __restrict__ Epart, int np, double tau, double stag) {
   __shared__ double sh[32];
@@ -1047,7 +1048,7 @@ extern "C" emin_status emin_iterate(emin_ctx c, int32_t k, int32_t* k_done, doub
 
 static void flush(emin_ctx c) {
   const int SM = emin_num_sms();
-  k_flush<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->r, c->yb, c->dw, c->y);
+  k_flush<<<SM * 8, 256, 0, c->stream>>>(c->view(), c->dw, c->y);
   k_flush_done<<<1, 1, 0, c->stream>>>(c->st);
 }
 
@@ -1059,23 +1060,26 @@ extern "C" emin_status emin_energy(emin_ctx c, double* E) {
     if (st != EMIN_OK) return st;
   }
   int g;
+  // W = W0 + dW is summed once into a scratch vector (not y^: the flush
+  // leaves the pending r -= alpha y^ to the next stage I)
+  if ((c->sym || (c->kernel_path == 2 && !c->dist)) && !c->wtmp)
+    EMIN_CUDA_TRY(c, emin_mallocAsync((void**)&c->wtmp, sizeof(double) * std::max<int64_t>(c->nnzWh, 1), c->stream));
   if (c->sym) {
-    // W = W0 + S dW~ once into the (free after the flush) y^ buffer; on
-    // several GPUs its halo rows from their owners
-    k_wsum_s<<<emin_num_sms() * 8, 256, 0, c->stream>>>(c->w0, c->dw, c->erow, c->srow, c->nnzW, c->yb);
+    // W = W0 + S dW~; on several GPUs its halo rows from their owners
+    k_wsum_s<<<emin_num_sms() * 8, 256, 0, c->stream>>>(c->w0, c->dw, c->erow, c->srow, c->nnzW, c->wtmp);
     c->launches += 1;
     if (c->dist) {
-      emin_status st = emin_dist_halo_values(c, c->yb, c->stream);
+      emin_status st = emin_dist_halo_values(c, c->wtmp, c->stream);
       if (st != EMIN_OK) return st;
     }
-    g = emin_launch_masked(c, MM_ENERGY, c->yb, nullptr, nullptr, c->stream);
+    g = emin_launch_masked(c, MM_ENERGY, c->wtmp, nullptr, nullptr, c->stream);
   } else if (c->kernel_path == 2 && !c->dist) {
-    // nodal path: W = W0 + dW once into the (free after the flush) y^ buffer,
-    // so the energy pass gathers one vector instead of two (same sums; on the
-    // scalar path the extra pass costs what it saves: 10.13 vs 10.15 ms/step)
-    k_wsum<<<emin_num_sms() * 8, 256, 0, c->stream>>>(c->w0, c->dw, c->nnzW, c->yb);
+    // nodal path: W = W0 + dW once, so the energy pass gathers one vector
+    // instead of two (same sums; on the scalar path the extra pass costs
+    // what it saves: 10.13 vs 10.15 ms/step)
+    k_wsum<<<emin_num_sms() * 8, 256, 0, c->stream>>>(c->w0, c->dw, c->nnzW, c->wtmp);
     c->launches += 1;
-    g = emin_launch_masked(c, MM_ENERGY, c->yb, nullptr, nullptr, c->stream);
+    g = emin_launch_masked(c, MM_ENERGY, c->wtmp, nullptr, nullptr, c->stream);
   } else {
     g = emin_launch_masked(c, MM_ENERGY, c->w0, c->dw, nullptr, c->stream);
   }
@@ -1191,7 +1195,7 @@ void emin_free_all(emin_ctx c) {
   cudaStream_t s = c->stream;
   void* ptrs[] = {c->wptr, c->affptr, c->afcptr, c->pofs, c->cofs, c->isc_own, c->wcol, c->affcol,
                   c->afccol, c->affval, c->afcval, c->d, c->Q, c->w0, c->dw, c->r, c->r0, c->y,
-                  c->yb, c->partials, c->dE_hist, c->st, c->erow, c->dinv, c->adiag, c->srow, c->affvalS};
+                  c->yb, c->partials, c->dE_hist, c->st, c->erow, c->dinv, c->adiag, c->srow, c->affvalS, c->wtmp};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   free_fast_path(c);

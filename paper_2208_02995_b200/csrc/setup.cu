@@ -927,7 +927,7 @@ extern "C" emin_status emin_setup(emin_ctx* out, int64_t n_global, int64_t nc_gl
   SETUP_TRY(dalloc(&ctx->dw, Wh + 2, s));
   SETUP_TRY(dalloc(&ctx->r, W, s));
   SETUP_TRY(dalloc(&ctx->y, Wh + 2, s));
-  SETUP_TRY(dalloc(&ctx->yb, Wh, s));     // (halo tail: W = W0 + S dW~ of the energy pass, scaled CG)
+  SETUP_TRY(dalloc(&ctx->yb, W, s));
   SETUP_TRY(dalloc(&ctx->st, 1, s));
   unsigned long long* counters;
   SETUP_TRY(dalloc(&counters, 4, s)); temps.push_back(counters);
