@@ -173,15 +173,58 @@ __device__ __forceinline__ void nd2_reduce_scatter(double (&v)[N], int lane, int
   *own = lo;
 }
 
-template <int NV, int MODE, bool PRED = false, bool CS = false, bool WIDE = false, int GRP = 1, int MINB = 4>
+// masked-product sums of one pattern position (C node s, component bc) over
+// the staged blocks bstart, bstart + bstep, ... < cb of a node: GRP blocks per
+// round, the (3 GRP) gathers of the round issued before its FMAs, which run
+// in ascending block order, 9 per matched block in (d, e) order.  Lanes of
+// a warp may take different blocks (the second chunk's groups).
+template <int GRP, typename XV>
+__device__ __forceinline__ void nd2_accum(const double* __restrict__ sa, const uint8_t* __restrict__ spm, int nJ, int cb, int bstart, int bstep,
+                                          int s, int bc, bool act, XV xval, double (&acc)[3]) {
+  for (int b = bstart; b < cb; b += GRP * bstep) {
+    double y[GRP][3], a8[GRP];
+    bool m[GRP];
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) {
+      const int bg = b + g * bstep;
+      const bool has = act && bg < cb;
+      const double2 t = reinterpret_cast<const double2*>(sa + (has ? bg : b) * ND2_AST)[4];
+      a8[g] = t.x;
+      const NodalBlk k{(int32_t)__double2loint(t.y), (int32_t)__double2hiint(t.y)};
+      const int p = has ? spm[bg * nJ + s] : 0xFF;
+      m[g] = p != 0xFF;
+      const int i = k.ybase + 3 * (m[g] ? p : 0) + bc;
+#pragma unroll
+      for (int e = 0; e < 3; ++e) y[g][e] = m[g] ? xval(i + e * k.nK3) : 0.0;
+    }
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) {
+      if (m[g]) {
+        const double2* a2 = reinterpret_cast<const double2*>(sa + (b + g * bstep) * ND2_AST);
+        const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3];
+        const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8[g]};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          acc[d] = fma(a[d * 3 + 0], y[g][0], acc[d]);
+          acc[d] = fma(a[d * 3 + 1], y[g][1], acc[d]);
+          acc[d] = fma(a[d * 3 + 2], y[g][2], acc[d]);
+        }
+      }
+    }
+  }
+}
+
+template <int NV, int MODE, bool CS = false, bool WIDE = false, int GRP = 1, int MINB = 4>
 __global__ void __launch_bounds__(ND_WARPS * 32, MINB)
 k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __restrict__ bptr,
                   const uint8_t* __restrict__ pm8, const int64_t* __restrict__ pmoff, int64_t nFn,
                   const double* __restrict__ X, const double* __restrict__ X2, double* __restrict__ out,
                   double* __restrict__ partials) {
   __shared__ double sh[32];
+  // per warp: the A chunk block-major at a 10-double stride with the block
+  // record {ybase, 3|J_K|} in each block's 10th slot (read with a8 by one
+  // 16-byte load), and the byte map
   __shared__ __align__(16) double s_a[ND_WARPS][ND_MAXB * ND2_AST];
-  __shared__ NodalBlk s_b[ND_WARPS][ND_MAXB];
   __shared__ __align__(16) uint8_t s_pm[ND_WARPS][ND_MAXB * ND_MAXJ];
   __shared__ __align__(16) double s_dot[ND_WARPS][3 * NV + 1];
   if (MODE == MM_ITER && v.st->stopped) { iter_stopped(v); return; }
@@ -193,7 +236,7 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
   const bool two = MODE == MM_ENERGY && X2 != nullptr;
   auto xval = [&](int idx) -> double { return two ? X[idx] + X2[idx] : X[idx]; };
   const int t0 = lane, t1 = lane + 32;
-  const int s0 = t0 / 3, b0 = t0 - 3 * s0, s1 = t1 / 3, b1 = t1 - 3 * s1;
+  const int s0 = t0 / 3, b0 = t0 - 3 * s0;
   double part = 0.0;
   const int64_t ncnt = unit_count(v, nFn);
   for (int64_t n1 = gw; n1 < ncnt; n1 += nw) {
@@ -209,6 +252,9 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
     const int rs = 3 * nb;
     const bool act0 = t0 < n3, act1 = t1 < n3;
     const bool any1 = n3 > 32;                          // warp-uniform
+    // lanes per position of the second chunk: 32 / 2^ceil(log2(n3 - 32))
+    const int l1sh = any1 ? __clz(n3 - 33) - 27 : 0;    // log2 L1 (n3 - 32 in [1, 32])
+    const int L1 = 1 << l1sh;
     double acc0[3] = {0.0, 0.0, 0.0}, acc1[3] = {0.0, 0.0, 0.0};
     // nodes with more than ND_MAXB blocks (Galerkin operators of coarse
     // levels, NEXT-4) are staged ND_MAXB blocks at a time, same block order
@@ -217,144 +263,53 @@ k_spgemm_nodal_v2(DevView v, const NodalBlk* __restrict__ blk, const int64_t* __
     const int c0 = WIDE ? cl : 0;
     const int cb = WIDE ? min(ND_MAXB, nb - c0) : nb, cs = 3 * cb;
     if (WIDE && c0) __syncwarp();
-    // ---- stage the node's data (A chunk re-ordered block-major, 10-double stride)
-    if (GRP > 1) {
-      // row by row: no division by the (variable) row length
+    // ---- stage the chunk (A row by row, re-ordered block-major)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double* srow = v.affval + ab + (int64_t)d * rs + 3 * c0;
-        for (int j = lane; j < cs; j += 32) {
-          const int b = j / 3, e = j - 3 * b;
-          s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(srow + j) : __ldg(srow + j);
-        }
+    for (int d = 0; d < 3; ++d) {
+      const double* srow = v.affval + ab + (int64_t)d * rs + 3 * c0;
+      for (int j = lane; j < cs; j += 32) {
+        const int b = j / 3, e = j - 3 * b;
+        s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(srow + j) : __ldg(srow + j);
       }
-    } else
-    for (int k = lane; k < 9 * cb; k += 32) {
-      const int d = k / cs, rem = k - d * cs, b = rem / 3, e = rem - 3 * b;
-      const int64_t src = WIDE ? ab + (int64_t)d * rs + 3 * c0 + rem : ab + k;
-      s_a[wib][b * ND2_AST + d * 3 + e] = CS ? __ldcs(v.affval + src) : __ldg(v.affval + src);
     }
     for (int k = lane; k < cb; k += 32) {
-      if (CS) { const int2 t = __ldcs(reinterpret_cast<const int2*>(blk + bb + c0 + k)); s_b[wib][k] = NodalBlk{t.x, t.y}; }
-      else s_b[wib][k] = blk[bb + c0 + k];
+      const int2 t = CS ? __ldcs(reinterpret_cast<const int2*>(blk + bb + c0 + k))
+                        : *reinterpret_cast<const int2*>(blk + bb + c0 + k);
+      *reinterpret_cast<int2*>(&s_a[wib][k * ND2_AST + 9]) = t;
     }
-    if (GRP > 1 && !WIDE) {
+    if (!WIDE) {
       // 16-byte loads (the node's map is 16-byte aligned, padded)
       const uint4* src4 = reinterpret_cast<const uint4*>(pm8 + po);
       uint4* dst4 = reinterpret_cast<uint4*>(&s_pm[wib][0]);
       for (int k = lane; k < ((cb * nJ + 15) >> 4); k += 32) dst4[k] = CS ? __ldcs(src4 + k) : src4[k];
     } else
-    for (int k = lane; k < cb * nJ; k += 32) {
-      const int64_t src = po + (int64_t)c0 * nJ + k;
-      s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + src)) : pm8[src];
-    }
+      for (int k = lane; k < cb * nJ; k += 32) {
+        const int64_t src = po + (int64_t)c0 * nJ + k;
+        s_pm[wib][k] = CS ? (uint8_t)__ldcs(reinterpret_cast<const char*>(pm8 + src)) : pm8[src];
+      }
     __syncwarp();
-    if (GRP > 1) {
-      // GRP blocks per round: the (up to 6 GRP) gathers of all of them are
-      // issued before the FMAs, which run in ascending block order with the
-      // same skips as the loop below (bitwise the same sums)
-      for (int b = 0; b < cb; b += GRP) {
-        double y0[GRP][3], y1[GRP][3];
-        bool m0[GRP], m1[GRP];
-#pragma unroll
-        for (int g = 0; g < GRP; ++g) {
-          const bool has = b + g < cb;
-          const NodalBlk k = s_b[wib][has ? b + g : b];
-          const int p0 = (has && act0) ? s_pm[wib][(b + g) * nJ + s0] : 0xFF;
-          const int p1 = (has && any1 && act1) ? s_pm[wib][(b + g) * nJ + s1] : 0xFF;
-          m0[g] = p0 != 0xFF;
-          m1[g] = p1 != 0xFF;
-          const int i0 = k.ybase + 3 * (m0[g] ? p0 : 0) + b0, i1 = k.ybase + 3 * (m1[g] ? p1 : 0) + b1;
-#pragma unroll
-          for (int e = 0; e < 3; ++e) {
-            y0[g][e] = m0[g] ? xval(i0 + e * k.nK3) : 0.0;
-            y1[g][e] = m1[g] ? xval(i1 + e * k.nK3) : 0.0;
-          }
-        }
-#pragma unroll
-        for (int g = 0; g < GRP; ++g) {
-          // (past the last block: m0 = m1 = false, the A read is clamped)
-          const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][min(b + g, cb - 1) * ND2_AST]);
-          const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
-          const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
-          // PRED: no branches, fma(a, 0, acc) = acc on unmatched positions
-          // (up to the sign of a zero sum)
-          if (PRED || m0[g]) {
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              acc0[d] = fma(a[d * 3 + 0], y0[g][0], acc0[d]);
-              acc0[d] = fma(a[d * 3 + 1], y0[g][1], acc0[d]);
-              acc0[d] = fma(a[d * 3 + 2], y0[g][2], acc0[d]);
-            }
-          }
-          if (PRED ? any1 : m1[g]) {
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              acc1[d] = fma(a[d * 3 + 0], y1[g][0], acc1[d]);
-              acc1[d] = fma(a[d * 3 + 1], y1[g][1], acc1[d]);
-              acc1[d] = fma(a[d * 3 + 2], y1[g][2], acc1[d]);
-            }
-          }
-        }
-      }
-    } else
-    for (int b = 0; b < cb; ++b) {
-      const double2* a2 = reinterpret_cast<const double2*>(&s_a[wib][b * ND2_AST]);
-      const double2 a01 = a2[0], a23 = a2[1], a45 = a2[2], a67 = a2[3], a8 = a2[4];
-      const double a[9] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y, a8.x};
-      const NodalBlk k = s_b[wib][b];
-      const int p0 = act0 ? s_pm[wib][b * nJ + s0] : 0xFF;
-      if (PRED) {
-        // branch-free: predicated gathers (0 when unmatched), unconditional
-        // FMAs (fma(a, 0, acc) = acc up to the sign of a zero)
-        const bool m0 = p0 != 0xFF;
-        const int i0 = k.ybase + 3 * (m0 ? p0 : 0) + b0;
-        const double y0 = m0 ? xval(i0) : 0.0, y1 = m0 ? xval(i0 + k.nK3) : 0.0, y2 = m0 ? xval(i0 + 2 * k.nK3) : 0.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          acc0[d] = fma(a[d * 3 + 0], y0, acc0[d]);
-          acc0[d] = fma(a[d * 3 + 1], y1, acc0[d]);
-          acc0[d] = fma(a[d * 3 + 2], y2, acc0[d]);
-        }
-        if (any1) {
-          const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
-          const bool m1 = p1 != 0xFF;
-          const int i1 = k.ybase + 3 * (m1 ? p1 : 0) + b1;
-          const double z0 = m1 ? xval(i1) : 0.0, z1 = m1 ? xval(i1 + k.nK3) : 0.0, z2 = m1 ? xval(i1 + 2 * k.nK3) : 0.0;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            acc1[d] = fma(a[d * 3 + 0], z0, acc1[d]);
-            acc1[d] = fma(a[d * 3 + 1], z1, acc1[d]);
-            acc1[d] = fma(a[d * 3 + 2], z2, acc1[d]);
-          }
-        }
-        continue;
-      }
-      if (p0 != 0xFF) {
-        const int i0 = k.ybase + 3 * p0 + b0;
-        const double y0 = xval(i0), y1 = xval(i0 + k.nK3), y2 = xval(i0 + 2 * k.nK3);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          acc0[d] = fma(a[d * 3 + 0], y0, acc0[d]);
-          acc0[d] = fma(a[d * 3 + 1], y1, acc0[d]);
-          acc0[d] = fma(a[d * 3 + 2], y2, acc0[d]);
-        }
-      }
-      if (any1) {
-        const int p1 = act1 ? s_pm[wib][b * nJ + s1] : 0xFF;
-        if (p1 != 0xFF) {
-          const int i1 = k.ybase + 3 * p1 + b1;
-          const double y0 = xval(i1), y1 = xval(i1 + k.nK3), y2 = xval(i1 + 2 * k.nK3);
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            acc1[d] = fma(a[d * 3 + 0], y0, acc1[d]);
-            acc1[d] = fma(a[d * 3 + 1], y1, acc1[d]);
-            acc1[d] = fma(a[d * 3 + 2], y2, acc1[d]);
-          }
-        }
-      }
+    // positions 0..31: one lane per position, every block of the chunk
+    nd2_accum<GRP>(&s_a[wib][0], &s_pm[wib][0], nJ, cb, 0, 1, s0, b0, act0, xval, acc0);
+    // positions 32..n3-1 (n3 <= 64): L1 lanes per position, lane sub of a
+    // group taking blocks sub, sub + L1, ...; the group's partial sums are
+    // combined after the last chunk (elasticity: n3 = 36, 4 positions x 8
+    // lanes, 4 rounds per node instead of 27 with 28 of 32 lanes idle)
+    if (any1) {
+      const int h = lane >> l1sh, sub = lane & (L1 - 1);
+      const int t = 32 + h, s = t / 3;
+      nd2_accum<GRP>(&s_a[wib][0], &s_pm[wib][0], nJ, cb, sub, L1, s, t - 3 * s, t < n3, xval, acc1);
     }
     }  // chunks of ND_MAXB blocks
+    if (any1) {
+      // sum each group's L1 partials (xor butterfly inside the aligned group),
+      // lane h < n3 - 32 takes group h's sum for position 32 + h
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        for (int o = L1 >> 1; o > 0; o >>= 1) acc1[d] += __shfl_xor_sync(0xffffffffu, acc1[d], o);
+        const double gs = __shfl_sync(0xffffffffu, acc1[d], act1 ? lane << l1sh : 0);
+        acc1[d] = act1 ? gs : 0.0;
+      }
+    }
     double g0[3], g1[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) { g0[d] = acc0[d]; g1[d] = acc1[d]; }
@@ -516,22 +471,22 @@ static inline int nodal_grid(emin_ctx c, const NodalPlan* p) {
 // one v2 configuration for every mode: CS = evict-first hints (iteration
 // only), WIDE = chunked staging (> ND_MAXB blocks per node), GRP = blocks per
 // round
-template <int NV, bool CS, bool WIDE, int GRP, int MINB = 4, bool PRED = false>
+template <int NV, bool CS, bool WIDE, int GRP, int MINB = 4>
 static inline void nd_v2(int mode, const DevView& v, const NodalPlan* p, int g, const double* X, const double* X2,
                          double* out, double* partials, cudaStream_t s) {
 #define ND_ARGS <<<g, ND_WARPS * 32, 0, s>>>(v, p->blk, p->bptr, p->pm8, p->pmoff, p->nFn, X, X2, out, partials)
-  if (mode == MM_ITER) k_spgemm_nodal_v2<NV, MM_ITER, PRED, CS, WIDE, GRP, MINB> ND_ARGS;
-  else if (mode == MM_R0) k_spgemm_nodal_v2<NV, MM_R0, false, false, WIDE, GRP> ND_ARGS;
-  else if (mode == MM_R0E) k_spgemm_nodal_v2<NV, MM_R0E, false, false, WIDE, GRP> ND_ARGS;
-  else k_spgemm_nodal_v2<NV, MM_ENERGY, false, false, WIDE, GRP> ND_ARGS;
+  if (mode == MM_ITER) k_spgemm_nodal_v2<NV, MM_ITER, CS, WIDE, GRP, MINB> ND_ARGS;
+  else if (mode == MM_R0) k_spgemm_nodal_v2<NV, MM_R0, false, WIDE, GRP> ND_ARGS;
+  else if (mode == MM_R0E) k_spgemm_nodal_v2<NV, MM_R0E, false, WIDE, GRP> ND_ARGS;
+  else k_spgemm_nodal_v2<NV, MM_ENERGY, false, WIDE, GRP> ND_ARGS;
 #undef ND_ARGS
 }
 
-template <bool CS, bool WIDE, int GRP, int MINB = 4, bool PRED = false>
+template <bool CS, bool WIDE, int GRP, int MINB = 4>
 static inline void nd_v2_nv(int nv, int mode, const DevView& v, const NodalPlan* p, int g, const double* X,
                             const double* X2, double* out, double* partials, cudaStream_t s) {
   switch (nv) {
-#define NV_CASE(N) case N: nd_v2<N, CS, WIDE, GRP, MINB, PRED>(mode, v, p, g, X, X2, out, partials, s); break;
+#define NV_CASE(N) case N: nd_v2<N, CS, WIDE, GRP, MINB>(mode, v, p, g, X, X2, out, partials, s); break;
     NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6) NV_CASE(7) NV_CASE(8)
 #undef NV_CASE
   }
@@ -551,7 +506,7 @@ static inline bool launch_nodal(emin_ctx c, const NodalPlan* p, int mode, const 
   if (p->max_nb > ND_MAXB)
     nd_v2_nv<true, true, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
   else
-    nd_v2_nv<true, false, 2>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
+    nd_v2_nv<true, false, 3>(c->nv, mode, v, p, g, X, X2, out, c->partials, s);
   return true;
 }
 
