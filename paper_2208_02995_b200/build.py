@@ -37,6 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     # one object per source, compiled in parallel, then one link (same flags)
     flags = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
              "-Xcompiler", "-fPIC"]
+    flags += os.environ.get("EMIN_NVCC_EXTRA", "").split()   # A/B builds only (profiles/*.sh), e.g. -DWP_EVF
     inc, lib = _nccl_paths()
     if inc:
         flags += ["-DEMIN_WITH_NCCL=1", "-I", inc]
